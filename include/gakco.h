@@ -1,0 +1,132 @@
+/*
+ * gakco.h — C-ABI of the B200 gapped k-mer kernel-matrix engine (libgakco.so).
+ *
+ * Computes, for a corpus of N sequences over an alphabet of Σ symbol codes, the
+ * GaKCo quantities of arXiv 1704.07468 (PAPER.md = P):
+ *
+ *   C_m(X,Y)   cumulative mismatch profile: over all C(g,m) ways of removing m of
+ *              the g positions of a g-mer, the number of ordered g-mer pairs
+ *              (a in X, b in Y) whose remaining (g-m)-mers are equal
+ *              (Algorithm 1 MISMATCHPROFILE), m = 0..M;
+ *   N_m(X,Y)   mismatch profile, pairs at Hamming distance exactly m
+ *              (Definition 1), from Eq. 9: N_m = C_m - sum_{j<m} C(g-j,m-j) N_j
+ *              (Algorithm 1 lines 18-21);
+ *   K(X,Y)     = sum_{m=0}^{min(M,g-k)} h_m N_m, h_m = C(g-m,k) (Eq. 6-7);
+ *   Knorm(X,Y) = K(X,Y)/sqrt(K(X,X) K(Y,Y)) in fp64, 0 when a diagonal entry is 0,
+ *              exactly 1.0 on the diagonal where K(X,X) > 0 (BASELINE.json).
+ *
+ * g-mers of a sequence of length l start at positions 0..l-g (a sequence shorter
+ * than g has none and yields a zero row). Self-pairs are counted on the diagonal
+ * (readings A2, A7).
+ *
+ * Conventions for every function:
+ *  - Returns GAKCO_OK or an error code; never aborts. gakco_last_error(plan)
+ *    returns a per-plan message for the most recent error.
+ *  - Matrices are row-major int64 (C, Nm, K) or fp64 (Knorm), little-endian,
+ *    full symmetric N x N, stacked [m][X][Y] for C and Nm. Sequence order is input
+ *    order.
+ *  - The caller owns every input and output buffer. The plan owns its device
+ *    scratch, which it allocates on first use and reuses.
+ *  - All work is enqueued on `cuda_stream` (a cudaStream_t; NULL = legacy default
+ *    stream). Calls that must read device data back (validation, host outputs)
+ *    synchronise that stream.
+ *  - One plan per host thread / stream. Results are bit-identical across runs,
+ *    shard counts, batch sizes and heavy/light thresholds (integer sums).
+ */
+#ifndef GAKCO_H
+#define GAKCO_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct gakco_plan gakco_plan;  /* opaque */
+
+typedef enum {
+    GAKCO_OK = 0,
+    GAKCO_E_ARG = 1,       /* invalid parameter, pointer or shape */
+    GAKCO_E_SYMBOL = 2,    /* a code >= sigma in the corpus */
+    GAKCO_E_RANGE = 3,     /* key+seq id do not fit 64 bits, a segment of more than
+                              2^30 g-mers, or a C_m entry bound overflows int64 */
+    GAKCO_E_NOMEM = 4,     /* device allocation failed */
+    GAKCO_E_CUDA = 5,      /* a CUDA runtime error */
+    GAKCO_E_INTERNAL = 6   /* a failed invariant (negative N_m, K != C_{g-k}) */
+} gakco_status;
+
+/* Tuning / testing options (gakco_set_option). Results never depend on them. */
+typedef enum {
+    GAKCO_OPT_HEAVY_MIN_SEQS = 1, /* groups with at least this many distinct sequences
+                                     go to the dense tensor-core Gram; 0 = automatic,
+                                     a huge value = never (all light); 2 = all heavy */
+    GAKCO_OPT_BATCH_KEYS = 2,     /* max keys (masks x g-mers) per batch; 0 = auto */
+    GAKCO_OPT_TIMING = 3          /* 1 = record per-stage CUDA events (gakco_get_stats) */
+} gakco_option;
+
+/* Counters of the last gakco_accumulate (algorithmic units). */
+typedef struct {
+    int64_t masks;          /* masks processed by this plan's shard */
+    int64_t keys;           /* masked g-mer keys encoded and sorted */
+    int64_t sort_passes;    /* sum over batches of 8-bit LSD passes x keys */
+    int64_t triples;        /* (key, seq, count) runs */
+    int64_t groups_multi;   /* groups with >= 2 distinct sequences */
+    int64_t light_pairs;    /* off-diagonal pair updates done by the light path */
+    int64_t heavy_groups;   /* groups sent to the tensor-core Gram */
+    int64_t heavy_macs;     /* u8 multiply-accumulates issued by the Gram */
+    double ms_encode, ms_sort, ms_segment, ms_light, ms_heavy, ms_epilogue;
+} gakco_stats;
+
+/* Create a plan for alphabet size sigma (1..255), g-mer length g (1..32),
+ * k-mer length k (1..g) and maximum mismatch level M (0..g; the paper's M=g-k,
+ * P:49). M < g-k truncates Eq. 7; M > g-k adds levels with h_m = 0. device is a
+ * CUDA ordinal. On success *out is a new plan (free with gakco_destroy). */
+gakco_status gakco_create(int sigma, int g, int k, int M, int device, gakco_plan** out);
+
+/* Restrict this plan to the masks with global index = rank (mod world), the
+ * masks enumerated level by level (m = 0..M) and lexicographically within a
+ * level (P:127, P:141, P:454 — the C(g,m) masks are independent). Default 0 of 1. */
+gakco_status gakco_set_shard(gakco_plan* plan, int rank, int world);
+
+gakco_status gakco_set_option(gakco_plan* plan, int option, int64_t value);
+
+/* Add this shard's contribution to C: for each of its masks, every pair of
+ * sequences sharing a masked key adds count_X*count_Y.
+ *   codes    uint8[offsets[N]] symbol codes (host or device pointer)
+ *   offsets  int64[N+1], offsets[0] = 0, non-decreasing (host or device)
+ *   C        int64[(M+1)*N*N] DEVICE pointer; the UPPER triangle (Y >= X,
+ *            diagonal included) is incremented, the lower triangle is not touched.
+ *            Zero it before the first call; partial C of several shards add up. */
+gakco_status gakco_accumulate(gakco_plan* plan, const uint8_t* codes, const int64_t* offsets,
+                              int64_t N, int64_t* C, void* cuda_stream);
+
+/* From a complete upper-triangular C (all masks accumulated): mirror C to full
+ * symmetric in place, then write Nm (Eq. 9), K (Eq. 7) and Knorm. Nm, K and
+ * Knorm may be NULL (not produced) and may be host or device pointers; C must
+ * be a device pointer. Fails with GAKCO_E_INTERNAL if an N_m entry is negative
+ * or K != C_{g-k} (when M >= g-k). */
+gakco_status gakco_finalize(gakco_plan* plan, int64_t* C, int64_t N, int64_t* Nm,
+                            int64_t* K, double* Knorm, void* cuda_stream);
+
+/* gakco_accumulate over all masks (shard ignored) followed by gakco_finalize.
+ * C may be NULL (plan scratch is used); any output pointer may be host or
+ * device. This is the single-call public entry point. */
+gakco_status gakco_kernel(gakco_plan* plan, const uint8_t* codes, const int64_t* offsets,
+                          int64_t N, int64_t* C, int64_t* Nm, int64_t* K, double* Knorm,
+                          void* cuda_stream);
+
+/* Counters and (if GAKCO_OPT_TIMING) stage times of the last accumulate /
+ * finalize. Synchronises the plan's last stream. */
+gakco_status gakco_get_stats(gakco_plan* plan, gakco_stats* out);
+
+/* Number of masks c_gk = sum_{m<=M} C(g,m) (Table 1) and of this shard. */
+int64_t gakco_num_masks(const gakco_plan* plan, int shard_only);
+
+const char* gakco_last_error(const gakco_plan* plan);
+const char* gakco_status_string(int status);
+void gakco_destroy(gakco_plan* plan);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GAKCO_H */

@@ -1,0 +1,94 @@
+// encode.cu — g-mer bookkeeping and the mask-encode kernel (removePosition).
+//
+// Algorithm 1 line 13, L^i <- removePosition(L, i) (§2.2 step 3,
+// P:127): for mask i (a set of m removed positions) every g-mer becomes the
+// (g-m)-mer of its kept positions. Here that (g-m)-mer is written as one
+// mixed-radix integer, first kept position most significant,
+//     key = sum_r code[pos + p_r] * sigma^(g-m-1-r),
+// and packed with its sequence id as  composite = key << sb | seq  (sb bits hold
+// the id). Equal keys <=> equal (g-m)-mers, so grouping composites by their key
+// bits groups the paper's matching (g-m)-mers. The g-mer list L of Algorithm 1
+// is never materialised: keys are produced straight from the corpus.
+//
+// The same pass counts the 8-bit digit histograms of every LSD pass the sort
+// will run (the "upfront histogram" of a onesweep radix sort).
+#include "internal.cuh"
+
+namespace gk {
+
+// gm_seq[j] = X for every g-mer j of sequence X (g-mer j of X is gofs[X] + i).
+__global__ void gmer_index_kernel(const int64_t* __restrict__ gofs, int64_t N,
+                                  uint32_t* __restrict__ gm_seq) {
+    for (int64_t x = blockIdx.x; x < N; x += gridDim.x) {
+        int64_t a = gofs[x], b = gofs[x + 1];
+        for (int64_t j = a + threadIdx.x; j < b; j += blockDim.x) gm_seq[j] = (uint32_t)x;
+    }
+}
+
+cudaError_t launch_gmer_index(const int64_t* gofs, int64_t N, uint32_t* gm_seq, cudaStream_t s) {
+    int grid = (int)(N < 65535 ? N : 65535);
+    if (grid > 0) gmer_index_kernel<<<grid, 128, 0, s>>>(gofs, N, gm_seq);
+    return cudaGetLastError();
+}
+
+__global__ void check_codes_kernel(const uint8_t* __restrict__ codes, int64_t len, int sigma,
+                                   int* flags) {
+    int bad = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < len;
+         i += (int64_t)gridDim.x * blockDim.x)
+        bad |= codes[i] >= sigma;
+    if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flags, EF_BAD_SYMBOL);
+}
+
+cudaError_t launch_check_codes(const uint8_t* codes, int64_t len, int sigma, int* flags,
+                               cudaStream_t s) {
+    if (len > 0) {
+        int64_t blocks = (len + 255) / 256;
+        check_codes_kernel<<<(int)(blocks < 4096 ? blocks : 4096), 256, 0, s>>>(codes, len, sigma,
+                                                                                 flags);
+    }
+    return cudaGetLastError();
+}
+
+// grid.y = mask within the batch; grid.x strides over g-mers.
+// kept[b*GMAX + r] = r-th kept position of mask b (ascending).
+__global__ void __launch_bounds__(256) encode_kernel(CorpusView cv, const uint8_t* __restrict__ kept,
+                                                     int nkept, int sigma, int sb, int npass,
+                                                     uint64_t* __restrict__ out,
+                                                     uint32_t* __restrict__ hist) {
+    __shared__ uint32_t sh[MAXPASS][RADIX];
+    __shared__ uint8_t sk[GMAX];
+    const int b = blockIdx.y;
+    for (int i = threadIdx.x; i < MAXPASS * RADIX; i += blockDim.x) (&sh[0][0])[i] = 0;
+    if (threadIdx.x < GMAX) sk[threadIdx.x] = kept[b * GMAX + threadIdx.x];
+    __syncthreads();
+    const uint64_t n = cv.n;
+    uint64_t* o = out + (uint64_t)b * n;
+    for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < n;
+         j += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t x = cv.gm_seq[j];
+        const uint8_t* p = cv.codes + cv.off[x] + ((int64_t)j - cv.gofs[x]);
+        uint64_t key = 0;
+        for (int r = 0; r < nkept; ++r) key = key * (uint64_t)sigma + p[sk[r]];
+        const uint64_t comp = (key << sb) | x;
+        o[j] = comp;
+        for (int q = 0; q < npass; ++q) atomicAdd(&sh[q][(comp >> (sb + RADIX_BITS * q)) & 0xff], 1u);
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < npass * RADIX; i += blockDim.x) {
+        uint32_t v = (&sh[0][0])[i];
+        if (v) atomicAdd(&hist[(b * npass) * RADIX + i], v);
+    }
+}
+
+cudaError_t launch_encode(const CorpusView& cv, const uint8_t* kept, int nkept, int sigma, int sb,
+                          int nmask, int npass, uint64_t* out, uint32_t* hist, cudaStream_t s) {
+    if (cv.n == 0 || nmask == 0) return cudaGetLastError();
+    uint64_t blocks = (cv.n + 256 * 8 - 1) / (256 * 8);
+    if (blocks > 1024) blocks = 1024;
+    dim3 grid((unsigned)blocks, (unsigned)nmask);
+    encode_kernel<<<grid, 256, 0, s>>>(cv, kept, nkept, sigma, sb, npass, out, hist);
+    return cudaGetLastError();
+}
+
+}  // namespace gk

@@ -1,0 +1,192 @@
+// epilogue.cu — inclusion-exclusion, weighting and normalisation.
+//
+//   N_m = C_m - sum_{j<m} C(g-j, m-j) N_j        Eq. 9, PAPER.md:136 (Algorithm 1
+//                                                lines 18-21)
+//   K   = sum_{m<=min(M,g-k)} h_m N_m,
+//         h_m = C(g-m,k) if g-m >= k else 0       Eq. 6-7, P:94-100 (Alg. 1 l.5-7)
+//   Knorm(X,Y) = K(X,Y) / sqrt(K(X,X) K(Y,Y))    BASELINE.json (reading A5)
+//
+// Input: C with a valid upper triangle. Output: C mirrored to full symmetric, and
+// full symmetric Nm, K, Knorm. One CTA per 32x32 tile pair (bi <= bj): the upper
+// tile is read once, its results written to (bi,bj) directly and to (bj,bi)
+// through a shared-memory transpose so both writes are coalesced.
+// Invariant checks: N_m >= 0, K == C_{g-k} when M >= g-k.
+#include <math.h>
+
+#include "internal.cuh"
+
+namespace gk {
+
+struct EpiArgs {
+    int64_t* C;
+    int64_t N;
+    int g, k, M;
+    int64_t* Nm;
+    int64_t* K;
+    double* Knorm;
+    int64_t* kdiag;
+    int* flags;
+};
+
+__device__ __forceinline__ void binom_table(int64_t (*t)[GMAX + 1], int g) {
+    // Pascal's triangle rows 0..g, filled by thread 0 (tiny).
+    if (threadIdx.x == 0 && threadIdx.y == 0) {
+        for (int n = 0; n <= g; ++n)
+            for (int r = 0; r <= GMAX; ++r)
+                t[n][r] = (r == 0) ? 1 : (r > n ? 0 : (r == n ? 1 : t[n - 1][r - 1] + t[n - 1][r]));
+    }
+    __syncthreads();
+}
+
+// Per-entry math. prof[m] = C_m(X,Y) in, N_m(X,Y) out. Returns K(X,Y).
+// Loops run to the compile-time bound MM (guarded by M) so prof stays in registers.
+template <int MM, typename P>
+__device__ __forceinline__ int64_t entry(P prof, const int64_t (*bt)[GMAX + 1], int g,
+                                         int k, int M, int* bad) {
+    int64_t cgk = 0;
+#pragma unroll
+    for (int m = 0; m <= MM; ++m)
+        if (m <= M && m == g - k) cgk = prof[m];
+#pragma unroll
+    for (int m = 0; m <= MM; ++m) {
+        if (m > M) break;
+        int64_t v = prof[m];
+#pragma unroll
+        for (int j = 0; j < m; ++j) v -= bt[g - j][m - j] * prof[j];  // prof[j] is N_j now
+        if (v < 0) *bad |= EF_NEGATIVE_N;
+        prof[m] = v;
+    }
+    int64_t K = 0;
+    const int top = M < g - k ? M : g - k;
+#pragma unroll
+    for (int m = 0; m <= MM; ++m)
+        if (m <= top) K += bt[g - m][k] * prof[m];
+    if (M >= g - k && K != cgk) *bad |= EF_K_MISMATCH;
+    return K;
+}
+
+__global__ void kdiag_kernel(EpiArgs a) {
+    __shared__ int64_t bt[GMAX + 1][GMAX + 1];
+    binom_table(bt, a.g);
+    const int64_t nn = a.N * a.N;
+    int bad = 0;
+    for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < a.N;
+         x += (int64_t)gridDim.x * blockDim.x) {
+        int64_t prof[GMAX + 1];
+        for (int m = 0; m <= a.M; ++m) prof[m] = a.C[m * nn + x * a.N + x];
+        a.kdiag[x] = entry<GMAX>(prof, bt, a.g, a.k, a.M, &bad);
+    }
+    if (bad) atomicOr(a.flags, bad);
+}
+
+__device__ __forceinline__ double knorm(int64_t kxy, int64_t kxx, int64_t kyy, bool diag) {
+    if (kxx <= 0 || kyy <= 0) return 0.0;
+    if (diag) return 1.0;
+    return __ddiv_rn((double)kxy, __dsqrt_rn(__dmul_rn((double)kxx, (double)kyy)));
+}
+
+// blockDim (32, 8); grid (tiles, tiles); block (bx=bj, by=bi) works iff bi <= bj.
+// MM bounds M so the per-thread profiles stay in registers.
+template <int MM>
+__global__ void __launch_bounds__(256) epilogue_kernel(EpiArgs a) {
+    __shared__ int64_t bt[GMAX + 1][GMAX + 1];
+    __shared__ int64_t st[32][33];
+    const int bi = blockIdx.y, bj = blockIdx.x;
+    if (bi > bj) return;
+    binom_table(bt, a.g);
+    const int tx = threadIdx.x, ty = threadIdx.y;
+    const int64_t N = a.N, nn = N * N;
+    const int M = a.M;
+    const bool diag_tile = bi == bj;
+    int64_t prof[4][MM + 1];
+    int64_t kv[4];
+    bool ok[4];
+    int bad = 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        const int r = ty + 8 * q;
+        const int64_t X = (int64_t)bi * 32 + r, Y = (int64_t)bj * 32 + tx;
+        ok[q] = X < N && Y < N;
+        kv[q] = 0;
+        if (!ok[q]) continue;
+        const int64_t src = (diag_tile && r > tx) ? (Y * N + X) : (X * N + Y);  // upper entry
+#pragma unroll
+        for (int m = 0; m <= MM; ++m)
+            if (m <= M) prof[q][m] = a.C[m * nn + src];
+        if (diag_tile && r > tx) {  // mirror C into the lower half of a diagonal tile
+#pragma unroll
+            for (int m = 0; m <= MM; ++m)
+                if (m <= M) a.C[m * nn + X * N + Y] = prof[q][m];
+        }
+        kv[q] = entry<MM>(prof[q], bt, a.g, a.k, M, &bad);  // prof now holds N_m
+        if (a.Nm) {
+#pragma unroll
+            for (int m = 0; m <= MM; ++m)
+                if (m <= M) a.Nm[m * nn + X * N + Y] = prof[q][m];
+        }
+        if (a.K) a.K[X * N + Y] = kv[q];
+        if (a.Knorm) a.Knorm[X * N + Y] = knorm(kv[q], a.kdiag[X], a.kdiag[Y], X == Y);
+    }
+    if (bad) atomicOr(a.flags, bad);
+    if (diag_tile) return;
+    // transposed writes of tile (bj, bi): C mirror, Nm, K, Knorm
+    const int nout = 2 * (M + 1) + 2;
+    for (int o = 0; o < nout; ++o) {
+        bool has;
+        if (o <= M) has = true;                        // C_m mirror (needs original C_m)
+        else if (o <= 2 * M + 1) has = a.Nm != nullptr;
+        else if (o == 2 * M + 2) has = a.K != nullptr;
+        else has = a.Knorm != nullptr;
+        if (!has) continue;
+        __syncthreads();
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int r = ty + 8 * q;
+            if (!ok[q]) continue;
+            const int64_t X = (int64_t)bi * 32 + r, Y = (int64_t)bj * 32 + tx;
+            int64_t v;
+            if (o <= M) v = a.C[o * nn + X * N + Y];
+            else if (o <= 2 * M + 1) {
+                v = 0;
+#pragma unroll
+                for (int m = 0; m <= MM; ++m)
+                    if (m == o - M - 1) v = prof[q][m];
+            }
+            else if (o == 2 * M + 2) v = kv[q];
+            else {
+                double d = knorm(kv[q], a.kdiag[X], a.kdiag[Y], false);
+                v = __double_as_longlong(d);
+            }
+            st[r][tx] = v;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int r = ty + 8 * q;                  // row within the transposed tile
+            const int64_t X = (int64_t)bj * 32 + r, Y = (int64_t)bi * 32 + tx;
+            if (X >= N || Y >= N) continue;
+            const int64_t v = st[tx][r];
+            if (o <= M) a.C[o * nn + X * N + Y] = v;
+            else if (o <= 2 * M + 1) a.Nm[(o - M - 1) * nn + X * N + Y] = v;
+            else if (o == 2 * M + 2) a.K[X * N + Y] = v;
+            else a.Knorm[X * N + Y] = __longlong_as_double(v);
+        }
+    }
+}
+
+cudaError_t launch_epilogue(int64_t* C, int64_t N, int g, int k, int M, int64_t* Nm, int64_t* K,
+                            double* Knorm, int64_t* kdiag, int* flags, cudaStream_t s) {
+    EpiArgs a{C, N, g, k, M, Nm, K, Knorm, kdiag, flags};
+    int64_t blocks = (N + 255) / 256;
+    kdiag_kernel<<<(int)(blocks < 1024 ? blocks : 1024), 256, 0, s>>>(a);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    const unsigned tiles = (unsigned)((N + 31) / 32);
+    if (M <= 7)
+        epilogue_kernel<7><<<dim3(tiles, tiles), dim3(32, 8), 0, s>>>(a);
+    else
+        epilogue_kernel<GMAX><<<dim3(tiles, tiles), dim3(32, 8), 0, s>>>(a);
+    return cudaGetLastError();
+}
+
+}  // namespace gk

@@ -1,0 +1,134 @@
+// internal.cuh — shared declarations of the libgakco.so translation units.
+// Product code: nothing here is shared with oracle/ (see DESIGN.md "Boundary").
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <string>
+#include <vector>
+
+#include "gakco.h"
+
+namespace gk {
+
+constexpr int GMAX = 32;          // longest supported g-mer
+constexpr int RADIX_BITS = 8;     // LSD digit width
+constexpr int RADIX = 256;
+constexpr int MAXPASS = 8;        // 64-bit composite / 8-bit digits
+
+// Onesweep tile: 512 threads x 8 keys.
+constexpr int SORT_THREADS = 512;
+constexpr int SORT_ITEMS = 8;
+constexpr int SORT_TILE = SORT_THREADS * SORT_ITEMS;
+
+// Segment (run-length) tile.
+constexpr int SEG_THREADS = 256;
+constexpr int SEG_ITEMS = 8;
+constexpr int SEG_TILE = SEG_THREADS * SEG_ITEMS;
+
+// Decoupled look-back status word: [63:32] epoch, [31:30] flag, [29:0] value.
+enum : uint32_t { LB_NONE = 0u, LB_AGG = 1u, LB_INC = 2u };
+__host__ __device__ inline uint64_t lb_pack(uint32_t epoch, uint32_t flag, uint32_t value) {
+    return ((uint64_t)epoch << 32) | ((uint64_t)flag << 30) | (uint64_t)(value & 0x3fffffffu);
+}
+
+__device__ __forceinline__ uint32_t lanemask_lt() {
+    uint32_t r;
+    asm("mov.u32 %0, %%lanemask_lt;" : "=r"(r));
+    return r;
+}
+
+// Exclusive scan of one value per thread over the first 256 threads of the block.
+// Must be reached by every thread of the block (threads >= 256 pass 0; their
+// result is meaningless). s_w: 8 words of shared scratch.
+__device__ __forceinline__ uint32_t scan256_excl(uint32_t v, uint32_t* s_w, uint32_t* total = nullptr) {
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    uint32_t inc = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        uint32_t t = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += t;
+    }
+    if (w < 8 && lane == 31) s_w[w] = inc;
+    __syncthreads();
+    uint32_t wp = 0, tot = 0;
+    for (int i = 0; i < 8; ++i) {
+        if (i < w) wp += s_w[i];
+        tot += s_w[i];
+    }
+    if (total) *total = tot;
+    __syncthreads();
+    return wp + inc - v;
+}
+
+// Single-counter decoupled look-back, called by ONE thread of tile `t`:
+// publishes the tile aggregate, returns the exclusive prefix of all earlier tiles
+// and publishes the inclusive one. Tiles must be numbered by an ordered ticket.
+__device__ __forceinline__ uint32_t lookback_one(uint64_t* status, uint32_t t, uint32_t agg,
+                                                 uint32_t epoch) {
+    if (t == 0) {
+        *(volatile uint64_t*)(status) = lb_pack(epoch, LB_INC, agg);
+        return 0;
+    }
+    *(volatile uint64_t*)(status + t) = lb_pack(epoch, LB_AGG, agg);
+    uint32_t excl = 0;
+    int64_t p = (int64_t)t - 1;
+    while (true) {
+        uint64_t v = *(volatile const uint64_t*)(status + p);
+        uint32_t ep = (uint32_t)(v >> 32), fl = (uint32_t)(v >> 30) & 3u;
+        if (ep != epoch || fl == LB_NONE) continue;
+        excl += (uint32_t)(v & 0x3fffffffu);
+        if (fl == LB_INC) break;
+        --p;
+    }
+    *(volatile uint64_t*)(status + t) = lb_pack(epoch, LB_INC, excl + agg);
+    return excl;
+}
+
+// Device counters of gakco_stats (int64 slots).
+enum { ST_KEYS = 0, ST_PASSKEYS, ST_TRIPLES, ST_GROUPS, ST_LIGHT_PAIRS, ST_HEAVY_GROUPS,
+       ST_HEAVY_MACS, ST_COUNT };
+
+// Error flags raised by kernels (bit mask in a device int).
+enum { EF_NEGATIVE_N = 1, EF_K_MISMATCH = 2, EF_BAD_SYMBOL = 4 };
+
+// Per-batch device views used by several kernels.
+struct CorpusView {
+    const uint8_t* codes;    // concatenated symbol codes
+    const int64_t* off;      // [N+1] sequence offsets into codes
+    const int64_t* gofs;     // [N+1] g-mer offsets (prefix sums of n_X)
+    const uint32_t* gm_seq;  // [n] sequence id of each g-mer
+    int64_t N;
+    uint64_t n;              // total g-mers
+};
+
+struct SegmentOut {
+    uint32_t* tseq;          // [T] seq id | (group-head << 31)
+    uint32_t* tcnt;          // [T] run length (count of the (key, seq) pair)
+    uint32_t* gstart;        // [G] first triple of each multi-sequence group
+    uint32_t* gend;          // [G] one past the last triple
+    uint32_t* counts;        // [0] = T, [1] = G
+};
+
+// ---- launchers (each returns cudaGetLastError()) ----
+cudaError_t launch_gmer_index(const int64_t* gofs, int64_t N, uint32_t* gm_seq, cudaStream_t s);
+cudaError_t launch_check_codes(const uint8_t* codes, int64_t len, int sigma, int* flags,
+                               cudaStream_t s);
+cudaError_t launch_encode(const CorpusView& cv, const uint8_t* kept, int nkept, int sigma, int sb,
+                          int nmask, int npass, uint64_t* out, uint32_t* hist, cudaStream_t s);
+cudaError_t launch_onesweep(const uint64_t* in, uint64_t* out, uint64_t n, int nseg, int shift,
+                            const uint32_t* hist, int pass, int npass, uint64_t* status,
+                            uint32_t* ctr, uint32_t epoch, cudaStream_t s);
+cudaError_t launch_triples(const uint64_t* keys, uint64_t n, int nseg, int sb, int64_t N,
+                           int64_t* Cm, uint64_t* status, uint32_t* ctr, uint32_t epoch,
+                           SegmentOut so, unsigned long long* stats, cudaStream_t s);
+cudaError_t launch_groups(uint64_t max_triples, uint64_t* status, uint32_t* ctr, uint32_t epoch,
+                          SegmentOut so, unsigned long long* stats, cudaStream_t s);
+cudaError_t launch_light(SegmentOut so, uint64_t max_groups, int64_t heavy_min, int64_t N,
+                         int64_t* Cm, unsigned long long* stats, int sm_count, cudaStream_t s);
+cudaError_t launch_diag_closed_form(const int64_t* gofs, int64_t N, int64_t nmask, int64_t* Cm,
+                                    cudaStream_t s);
+cudaError_t launch_epilogue(int64_t* C, int64_t N, int g, int k, int M, int64_t* Nm, int64_t* K,
+                            double* Knorm, int64_t* kdiag, int* flags, cudaStream_t s);
+
+}  // namespace gk

@@ -1,0 +1,582 @@
+// plan.cu — the C-ABI (include/gakco.h) and the host orchestration of one call.
+//
+// Order of work for gakco_accumulate (Algorithm 1 MISMATCHPROFILE, PAPER.md:179-199,
+// re-planned for a GPU):
+//   validate -> corpus to device -> g-mer index
+//   for m = 0..M, for each batch of this shard's masks of level m:
+//       encode (+ upfront digit histograms) -> onesweep LSD passes over key digits
+//       -> triples (+ diagonal repeat term) -> multi-sequence groups
+//       -> light pair updates -> closed-form diagonal term
+// Everything is enqueued on the caller's stream; the only host synchronisations
+// are input validation (when inputs live on the device) and reading error flags
+// / stats. Masks are global-round-robin sharded (rank r takes indices = r mod P,
+// P:141): partial C of several shards sum to the full C.
+#include <algorithm>
+#include <array>
+#include <climits>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "internal.cuh"
+
+using namespace gk;
+
+namespace {
+
+struct DevBuf {
+    void* p = nullptr;
+    size_t cap = 0;
+};
+
+enum Stage { S_ENCODE = 0, S_SORT, S_SEGMENT, S_LIGHT, S_HEAVY, S_EPILOGUE, S_NSTAGE };
+
+struct DeviceGuard {
+    int prev = -1;
+    explicit DeviceGuard(int dev) {
+        if (cudaGetDevice(&prev) != cudaSuccess) prev = -1;
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        int cur;
+        if (prev >= 0 && cudaGetDevice(&cur) == cudaSuccess && cur != prev) cudaSetDevice(prev);
+    }
+};
+
+bool is_device_ptr(const void* p) {
+    if (!p) return false;
+    cudaPointerAttributes a;
+    cudaError_t e = cudaPointerGetAttributes(&a, p);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    return a.type == cudaMemoryTypeDevice || a.type == cudaMemoryTypeManaged;
+}
+
+// smallest b with 2^b >= v (v >= 1), for v given as an unsigned 128-bit value
+int bits_for(unsigned __int128 v) {
+    int b = 0;
+    while (b < 128 && ((unsigned __int128)1 << b) < v) ++b;
+    return b;
+}
+
+int64_t binom64(int n, int r) {
+    if (r < 0 || r > n) return 0;
+    int64_t c = 1;
+    for (int i = 1; i <= r; ++i) c = c * (n - r + i) / i;
+    return c;
+}
+
+}  // namespace
+
+struct gakco_plan {
+    int sigma = 0, g = 0, k = 0, M = 0, device = 0;
+    int rank = 0, world = 1;
+    int64_t heavy_min = 0, batch_keys = 0;
+    bool timing = false;
+    int sm_count = 148;
+    std::string err;
+
+    // masks in global order: level by level, lexicographic removed-position sets
+    std::vector<int> mask_level;
+    std::vector<std::array<uint8_t, GMAX>> mask_kept;
+    std::vector<int> key_bits;  // per level
+
+    DevBuf codes, off, gofs, gmseq, keysA, keysB, hist, status, ctr, tseq, tcnt, gstart, gend,
+        counts, kept, stats, flags, kdiag, Cscr, Nmscr, Kscr, Knscr;
+    uint32_t epoch = 1;
+    uint32_t ctr_next = 0;
+    static constexpr uint32_t CTR_SLOTS = 4096;
+
+    std::vector<std::pair<int, std::pair<cudaEvent_t, cudaEvent_t>>> evs;
+    std::vector<cudaEvent_t> ev_pool;
+    size_t ev_used = 0;
+    gakco_stats host_stats{};
+    cudaStream_t last_stream = nullptr;
+    int64_t last_masks = 0;
+
+    std::vector<int64_t> h_off, h_gofs;
+
+    gakco_status fail(gakco_status s, const std::string& msg) {
+        err = msg;
+        return s;
+    }
+    gakco_status cuda_fail(cudaError_t e, const char* where) {
+        err = std::string("CUDA error in ") + where + ": " + cudaGetErrorString(e);
+        return e == cudaErrorMemoryAllocation ? GAKCO_E_NOMEM : GAKCO_E_CUDA;
+    }
+    cudaError_t ensure(DevBuf& b, size_t bytes, cudaStream_t s, bool zero = false) {
+        if (bytes == 0) bytes = 16;
+        if (bytes <= b.cap) return cudaSuccess;
+        if (b.p) {
+            cudaError_t e = cudaStreamSynchronize(s);
+            if (e != cudaSuccess) return e;
+            cudaFree(b.p);
+        }
+        b.p = nullptr;
+        b.cap = 0;
+        size_t alloc = bytes + bytes / 8;
+        cudaError_t e = cudaMalloc(&b.p, alloc);
+        if (e != cudaSuccess) return e;
+        b.cap = alloc;
+        if (zero) return cudaMemsetAsync(b.p, 0, alloc, s);
+        return cudaSuccess;
+    }
+    cudaEvent_t ev() {
+        if (ev_used == ev_pool.size()) {
+            cudaEvent_t e;
+            cudaEventCreate(&e);
+            ev_pool.push_back(e);
+        }
+        return ev_pool[ev_used++];
+    }
+    void stage_begin(cudaStream_t s, cudaEvent_t* a) {
+        if (!timing) return;
+        *a = ev();
+        cudaEventRecord(*a, s);
+    }
+    void stage_end(cudaStream_t s, int stage, cudaEvent_t a) {
+        if (!timing) return;
+        cudaEvent_t b = ev();
+        cudaEventRecord(b, s);
+        evs.push_back({stage, {a, b}});
+    }
+    // next tile-ticket counter slot (reset in bulk when exhausted)
+    cudaError_t next_ctr(cudaStream_t s, uint32_t** out) {
+        if (ctr_next >= CTR_SLOTS) {
+            cudaError_t e = cudaMemsetAsync(ctr.p, 0, CTR_SLOTS * sizeof(uint32_t), s);
+            if (e != cudaSuccess) return e;
+            ctr_next = 0;
+        }
+        *out = (uint32_t*)ctr.p + ctr_next++;
+        return cudaSuccess;
+    }
+};
+
+static const char* kStatusStrings[] = {"ok", "invalid argument", "symbol code >= sigma",
+                                       "value out of range", "out of device memory",
+                                       "CUDA error", "internal invariant failed"};
+
+extern "C" const char* gakco_status_string(int s) {
+    return (s >= 0 && s <= 6) ? kStatusStrings[s] : "unknown status";
+}
+
+extern "C" const char* gakco_last_error(const gakco_plan* p) {
+    return p ? p->err.c_str() : "null plan";
+}
+
+extern "C" gakco_status gakco_create(int sigma, int g, int k, int M, int device, gakco_plan** out) {
+    if (!out) return GAKCO_E_ARG;
+    *out = nullptr;
+    if (sigma < 1 || sigma > 255 || g < 1 || g > GMAX || k < 1 || k > g || M < 0 || M > g)
+        return GAKCO_E_ARG;
+    int ndev = 0;
+    if (cudaGetDeviceCount(&ndev) != cudaSuccess || device < 0 || device >= ndev) {
+        cudaGetLastError();
+        return device < 0 ? GAKCO_E_ARG : GAKCO_E_CUDA;
+    }
+    int64_t total = 0;
+    for (int m = 0; m <= M; ++m) total += binom64(g, m);
+    if (total > (1 << 24)) return GAKCO_E_RANGE;
+    gakco_plan* p = new gakco_plan();
+    p->sigma = sigma;
+    p->g = g;
+    p->k = k;
+    p->M = M;
+    p->device = device;
+    {
+        DeviceGuard dg(device);
+        cudaDeviceGetAttribute(&p->sm_count, cudaDevAttrMultiProcessorCount, device);
+    }
+    // masks: m removed positions, lexicographic over the removed set (reading A9)
+    for (int m = 0; m <= M; ++m) {
+        std::vector<int> rem(m);
+        for (int i = 0; i < m; ++i) rem[i] = i;
+        while (true) {
+            std::array<uint8_t, GMAX> kept{};
+            int r = 0, q = 0;
+            for (int pos = 0; pos < g; ++pos) {
+                if (q < m && rem[q] == pos) {
+                    ++q;
+                    continue;
+                }
+                kept[r++] = (uint8_t)pos;
+            }
+            p->mask_level.push_back(m);
+            p->mask_kept.push_back(kept);
+            int i = m - 1;
+            while (i >= 0 && rem[i] == g - m + i) --i;
+            if (i < 0) break;
+            ++rem[i];
+            for (int j = i + 1; j < m; ++j) rem[j] = rem[j - 1] + 1;
+        }
+        // key bits: sigma^(g-m) distinct keys
+        unsigned __int128 v = 1;
+        bool over = false;
+        for (int i = 0; i < g - m; ++i) {
+            v *= (unsigned)sigma;
+            if (v > ((unsigned __int128)1 << 64)) over = true;
+        }
+        p->key_bits.push_back(over ? 65 : bits_for(v));
+    }
+    *out = p;
+    return GAKCO_OK;
+}
+
+extern "C" void gakco_destroy(gakco_plan* p) {
+    if (!p) return;
+    DeviceGuard dg(p->device);
+    DevBuf* bufs[] = {&p->codes, &p->off,   &p->gofs,  &p->gmseq,  &p->keysA, &p->keysB,
+                      &p->hist,  &p->status, &p->ctr,  &p->tseq,   &p->tcnt,  &p->gstart,
+                      &p->gend,  &p->counts, &p->kept, &p->stats,  &p->flags, &p->kdiag,
+                      &p->Cscr,  &p->Nmscr, &p->Kscr,  &p->Knscr};
+    for (DevBuf* b : bufs)
+        if (b->p) cudaFree(b->p);
+    for (cudaEvent_t e : p->ev_pool) cudaEventDestroy(e);
+    delete p;
+}
+
+extern "C" gakco_status gakco_set_shard(gakco_plan* p, int rank, int world) {
+    if (!p || world < 1 || rank < 0 || rank >= world) return GAKCO_E_ARG;
+    p->rank = rank;
+    p->world = world;
+    return GAKCO_OK;
+}
+
+extern "C" gakco_status gakco_set_option(gakco_plan* p, int option, int64_t value) {
+    if (!p) return GAKCO_E_ARG;
+    switch (option) {
+        case GAKCO_OPT_HEAVY_MIN_SEQS:
+            if (value < 0) return p->fail(GAKCO_E_ARG, "heavy threshold must be >= 0");
+            p->heavy_min = value;
+            return GAKCO_OK;
+        case GAKCO_OPT_BATCH_KEYS:
+            if (value < 0) return p->fail(GAKCO_E_ARG, "batch keys must be >= 0");
+            p->batch_keys = value;
+            return GAKCO_OK;
+        case GAKCO_OPT_TIMING:
+            p->timing = value != 0;
+            return GAKCO_OK;
+        default:
+            return p->fail(GAKCO_E_ARG, "unknown option");
+    }
+}
+
+extern "C" int64_t gakco_num_masks(const gakco_plan* p, int shard_only) {
+    if (!p) return -1;
+    int64_t n = (int64_t)p->mask_level.size();
+    if (!shard_only) return n;
+    return n / p->world + ((n % p->world) > p->rank ? 1 : 0);
+}
+
+// ----------------------------------------------------------------------------
+static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const int64_t* offsets,
+                                    int64_t N, int64_t* C, cudaStream_t s, int rank, int world) {
+#define CK(x)                                          \
+    do {                                               \
+        cudaError_t e_ = (x);                          \
+        if (e_ != cudaSuccess) return p->cuda_fail(e_, #x); \
+    } while (0)
+    if (!codes && N > 0) return p->fail(GAKCO_E_ARG, "codes is NULL");
+    if (!offsets || !C) return p->fail(GAKCO_E_ARG, "offsets or C is NULL");
+    if (N < 1 || N >= ((int64_t)1 << 31)) return p->fail(GAKCO_E_ARG, "N must be in [1, 2^31)");
+    if (!is_device_ptr(C)) return p->fail(GAKCO_E_ARG, "C must be a device pointer");
+    p->last_stream = s;
+    p->evs.clear();
+    p->ev_used = 0;
+    const int g = p->g, M = p->M;
+
+    // offsets -> host, validate
+    p->h_off.resize(N + 1);
+    if (is_device_ptr(offsets)) {
+        CK(cudaMemcpyAsync(p->h_off.data(), offsets, (N + 1) * sizeof(int64_t),
+                           cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+    } else {
+        std::memcpy(p->h_off.data(), offsets, (N + 1) * sizeof(int64_t));
+    }
+    if (p->h_off[0] != 0) return p->fail(GAKCO_E_ARG, "offsets[0] != 0");
+    for (int64_t i = 0; i < N; ++i)
+        if (p->h_off[i + 1] < p->h_off[i]) return p->fail(GAKCO_E_ARG, "offsets decrease");
+    const int64_t L = p->h_off[N];
+
+    // g-mer counts n_X = max(0, l_X - g + 1) (reading A7/A8) and prefix sums
+    p->h_gofs.assign(N + 1, 0);
+    int64_t nmax = 0;
+    for (int64_t i = 0; i < N; ++i) {
+        int64_t nx = std::max<int64_t>(0, p->h_off[i + 1] - p->h_off[i] - g + 1);
+        nmax = std::max(nmax, nx);
+        p->h_gofs[i + 1] = p->h_gofs[i] + nx;
+    }
+    const uint64_t n = (uint64_t)p->h_gofs[N];
+    if (n >= (1ull << 30)) return p->fail(GAKCO_E_RANGE, "more than 2^30 g-mers");
+    // int64 bound of every entry: C_m(X,Y) <= C(g,m) n_X n_Y, K <= C(g,k) n_X n_Y
+    {
+        unsigned __int128 nn = (unsigned __int128)nmax * nmax;
+        for (int m = 0; m <= M; ++m)
+            if (nn * (unsigned __int128)binom64(g, m) > (unsigned __int128)INT64_MAX)
+                return p->fail(GAKCO_E_RANGE, "C_m may overflow int64");
+        if (nn * (unsigned __int128)binom64(g, p->k) > (unsigned __int128)INT64_MAX)
+            return p->fail(GAKCO_E_RANGE, "K may overflow int64");
+    }
+    const int sb = (N <= 1) ? 0 : 64 - __builtin_clzll((unsigned long long)(N - 1));
+    for (int m = 0; m <= M; ++m)
+        if (p->key_bits[m] + sb > 64)
+            return p->fail(GAKCO_E_RANGE, "masked key + sequence id exceed 64 bits");
+
+    // corpus to device (+ symbol check)
+    CK(p->ensure(p->codes, (size_t)L + 16, s));
+    CK(p->ensure(p->flags, 64, s));
+    CK(cudaMemsetAsync(p->flags.p, 0, sizeof(int), s));
+    if (L > 0) {
+        if (is_device_ptr(codes)) {
+            CK(cudaMemcpyAsync(p->codes.p, codes, L, cudaMemcpyDeviceToDevice, s));
+            CK(launch_check_codes((const uint8_t*)p->codes.p, L, p->sigma, (int*)p->flags.p, s));
+            int fl = 0;
+            CK(cudaMemcpyAsync(&fl, p->flags.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+            CK(cudaStreamSynchronize(s));
+            if (fl & EF_BAD_SYMBOL) return p->fail(GAKCO_E_SYMBOL, "a code is >= sigma");
+        } else {
+            for (int64_t i = 0; i < L; ++i)
+                if (codes[i] >= p->sigma) return p->fail(GAKCO_E_SYMBOL, "a code is >= sigma");
+            CK(cudaMemcpyAsync(p->codes.p, codes, L, cudaMemcpyHostToDevice, s));
+        }
+    }
+    CK(p->ensure(p->off, (N + 1) * sizeof(int64_t), s));
+    CK(p->ensure(p->gofs, (N + 1) * sizeof(int64_t), s));
+    CK(cudaMemcpyAsync(p->off.p, p->h_off.data(), (N + 1) * sizeof(int64_t),
+                       cudaMemcpyHostToDevice, s));
+    CK(cudaMemcpyAsync(p->gofs.p, p->h_gofs.data(), (N + 1) * sizeof(int64_t),
+                       cudaMemcpyHostToDevice, s));
+    CK(p->ensure(p->gmseq, n * sizeof(uint32_t), s));
+    CK(launch_gmer_index((const int64_t*)p->gofs.p, N, (uint32_t*)p->gmseq.p, s));
+
+    // this shard's masks, in processing order
+    std::vector<int> mine;
+    for (size_t i = 0; i < p->mask_level.size(); ++i)
+        if ((int)(i % world) == rank) mine.push_back((int)i);
+    std::vector<uint8_t> kept_h(mine.size() * GMAX + GMAX, 0);
+    for (size_t i = 0; i < mine.size(); ++i)
+        std::memcpy(&kept_h[i * GMAX], p->mask_kept[mine[i]].data(), GMAX);
+    CK(p->ensure(p->kept, kept_h.size(), s));
+    CK(cudaMemcpyAsync(p->kept.p, kept_h.data(), kept_h.size(), cudaMemcpyHostToDevice, s));
+    CK(cudaStreamSynchronize(s));  // kept_h / h_* are pageable host staging
+
+    // batch size
+    uint64_t bk = p->batch_keys > 0 ? (uint64_t)p->batch_keys : (1ull << 26);
+    if (bk > (1ull << 30) - 1) bk = (1ull << 30) - 1;
+    const uint64_t bmax_masks = std::max<uint64_t>(1, n ? bk / n : mine.size());
+    const uint64_t cap_keys = std::max<uint64_t>(1, std::min<uint64_t>(bmax_masks, mine.size()) * n);
+    CK(p->ensure(p->keysA, cap_keys * 8, s));
+    CK(p->ensure(p->keysB, cap_keys * 8, s));
+    CK(p->ensure(p->tseq, cap_keys * 4, s));
+    CK(p->ensure(p->tcnt, cap_keys * 4, s));
+    CK(p->ensure(p->gstart, (cap_keys / 2 + 1) * 4, s));
+    CK(p->ensure(p->gend, (cap_keys / 2 + 1) * 4, s));
+    CK(p->ensure(p->counts, 16, s));
+    CK(p->ensure(p->hist, std::min<uint64_t>(bmax_masks, mine.size() + 1) * MAXPASS * RADIX * 4, s));
+    {
+        uint64_t tps = (n + SORT_TILE - 1) / SORT_TILE;
+        uint64_t st_sort = std::min<uint64_t>(bmax_masks, mine.size() + 1) * RADIX * tps;
+        uint64_t st_seg = cap_keys / SEG_TILE + 2;
+        CK(p->ensure(p->status, std::max(st_sort, st_seg) * 8, s, /*zero=*/true));
+    }
+    if (p->ctr.cap == 0) {
+        CK(p->ensure(p->ctr, p->CTR_SLOTS * sizeof(uint32_t), s));
+        p->ctr_next = p->CTR_SLOTS;  // forces a reset on first use
+    }
+    CK(p->ensure(p->stats, ST_COUNT * 8, s));
+    CK(cudaMemsetAsync(p->stats.p, 0, ST_COUNT * 8, s));
+    unsigned long long* stats = (unsigned long long*)p->stats.p;
+
+    const int64_t heavy_min = p->heavy_min > 0 ? p->heavy_min : INT64_MAX;  // no Gram yet
+    CorpusView cv{(const uint8_t*)p->codes.p, (const int64_t*)p->off.p, (const int64_t*)p->gofs.p,
+                  (const uint32_t*)p->gmseq.p, N, n};
+    SegmentOut so{(uint32_t*)p->tseq.p, (uint32_t*)p->tcnt.p, (uint32_t*)p->gstart.p,
+                  (uint32_t*)p->gend.p, (uint32_t*)p->counts.p};
+    int64_t passkeys = 0;
+    const size_t nn = (size_t)N * N;
+
+    size_t pos = 0;
+    while (pos < mine.size()) {
+        const int m = p->mask_level[mine[pos]];
+        size_t end = pos;
+        while (end < mine.size() && p->mask_level[mine[end]] == m && end - pos < bmax_masks) ++end;
+        const int nmask = (int)(end - pos);
+        const int kb = p->key_bits[m];
+        const int npass = (kb + RADIX_BITS - 1) / RADIX_BITS;
+        int64_t* Cm = C + (size_t)m * nn;
+        cudaEvent_t a = nullptr;
+
+        if (n > 0) {
+            p->stage_begin(s, &a);
+            CK(cudaMemsetAsync(p->hist.p, 0, (size_t)nmask * MAXPASS * RADIX * 4, s));
+            CK(launch_encode(cv, (const uint8_t*)p->kept.p + pos * GMAX, g - m, p->sigma, sb,
+                             nmask, npass, (uint64_t*)p->keysA.p, (uint32_t*)p->hist.p, s));
+            p->stage_end(s, S_ENCODE, a);
+
+            p->stage_begin(s, &a);
+            uint64_t* in = (uint64_t*)p->keysA.p;
+            uint64_t* outk = (uint64_t*)p->keysB.p;
+            for (int q = 0; q < npass; ++q) {
+                uint32_t* c;
+                CK(p->next_ctr(s, &c));
+                CK(launch_onesweep(in, outk, n, nmask, sb + RADIX_BITS * q, (const uint32_t*)p->hist.p,
+                                   q, npass, (uint64_t*)p->status.p, c, p->epoch++, s));
+                std::swap(in, outk);
+            }
+            passkeys += (int64_t)npass * nmask * (int64_t)n;
+            p->stage_end(s, S_SORT, a);
+
+            p->stage_begin(s, &a);
+            uint32_t* c1;
+            CK(p->next_ctr(s, &c1));
+            CK(launch_triples(in, n, nmask, sb, N, Cm, (uint64_t*)p->status.p, c1, p->epoch++, so,
+                              stats, s));
+            uint32_t* c2;
+            CK(p->next_ctr(s, &c2));
+            CK(launch_groups(n * nmask, (uint64_t*)p->status.p, c2, p->epoch++, so, stats, s));
+            p->stage_end(s, S_SEGMENT, a);
+
+            p->stage_begin(s, &a);
+            CK(launch_light(so, n * nmask / 2 + 1, heavy_min, N, Cm, stats, p->sm_count, s));
+            p->stage_end(s, S_LIGHT, a);
+        }
+        CK(launch_diag_closed_form((const int64_t*)p->gofs.p, N, nmask, Cm, s));
+        pos = end;
+    }
+    p->last_masks = (int64_t)mine.size();
+    p->host_stats = gakco_stats{};
+    p->host_stats.masks = (int64_t)mine.size();
+    p->host_stats.keys = (int64_t)mine.size() * (int64_t)n;
+    p->host_stats.sort_passes = passkeys;
+    return GAKCO_OK;
+#undef CK
+}
+
+extern "C" gakco_status gakco_accumulate(gakco_plan* p, const uint8_t* codes,
+                                         const int64_t* offsets, int64_t N, int64_t* C,
+                                         void* stream) {
+    if (!p) return GAKCO_E_ARG;
+    DeviceGuard dg(p->device);
+    return accumulate_impl(p, codes, offsets, N, C, (cudaStream_t)stream, p->rank, p->world);
+}
+
+static gakco_status finalize_impl(gakco_plan* p, int64_t* C, int64_t N, int64_t* Nm, int64_t* K,
+                                  double* Knorm, cudaStream_t s, bool keep_events) {
+#define CK(x)                                          \
+    do {                                               \
+        cudaError_t e_ = (x);                          \
+        if (e_ != cudaSuccess) return p->cuda_fail(e_, #x); \
+    } while (0)
+    if (!C || N < 1) return p->fail(GAKCO_E_ARG, "C is NULL or N < 1");
+    if (!is_device_ptr(C)) return p->fail(GAKCO_E_ARG, "C must be a device pointer");
+    if (!keep_events) {
+        p->evs.clear();
+        p->ev_used = 0;
+    }
+    p->last_stream = s;
+    const size_t nn = (size_t)N * N;
+    const int M = p->M;
+    int64_t* dNm = Nm;
+    int64_t* dK = K;
+    double* dKn = Knorm;
+    const bool hNm = Nm && !is_device_ptr(Nm), hK = K && !is_device_ptr(K),
+               hKn = Knorm && !is_device_ptr(Knorm);
+    if (hNm) {
+        CK(p->ensure(p->Nmscr, (M + 1) * nn * 8, s));
+        dNm = (int64_t*)p->Nmscr.p;
+    }
+    if (hK) {
+        CK(p->ensure(p->Kscr, nn * 8, s));
+        dK = (int64_t*)p->Kscr.p;
+    }
+    if (hKn) {
+        CK(p->ensure(p->Knscr, nn * 8, s));
+        dKn = (double*)p->Knscr.p;
+    }
+    CK(p->ensure(p->kdiag, N * 8, s));
+    CK(p->ensure(p->flags, 64, s));
+    CK(cudaMemsetAsync(p->flags.p, 0, sizeof(int), s));
+    cudaEvent_t a = nullptr;
+    p->stage_begin(s, &a);
+    CK(launch_epilogue(C, N, p->g, p->k, M, dNm, dK, dKn, (int64_t*)p->kdiag.p, (int*)p->flags.p,
+                       s));
+    p->stage_end(s, S_EPILOGUE, a);
+    if (hNm) CK(cudaMemcpyAsync(Nm, dNm, (M + 1) * nn * 8, cudaMemcpyDeviceToHost, s));
+    if (hK) CK(cudaMemcpyAsync(K, dK, nn * 8, cudaMemcpyDeviceToHost, s));
+    if (hKn) CK(cudaMemcpyAsync(Knorm, dKn, nn * 8, cudaMemcpyDeviceToHost, s));
+    int fl = 0;
+    CK(cudaMemcpyAsync(&fl, p->flags.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaStreamSynchronize(s));
+    if (fl & EF_NEGATIVE_N) return p->fail(GAKCO_E_INTERNAL, "negative N_m after Eq. 9");
+    if (fl & EF_K_MISMATCH) return p->fail(GAKCO_E_INTERNAL, "K != C_{g-k}");
+    return GAKCO_OK;
+#undef CK
+}
+
+extern "C" gakco_status gakco_finalize(gakco_plan* p, int64_t* C, int64_t N, int64_t* Nm,
+                                       int64_t* K, double* Knorm, void* stream) {
+    if (!p) return GAKCO_E_ARG;
+    DeviceGuard dg(p->device);
+    return finalize_impl(p, C, N, Nm, K, Knorm, (cudaStream_t)stream, false);
+}
+
+extern "C" gakco_status gakco_kernel(gakco_plan* p, const uint8_t* codes, const int64_t* offsets,
+                                     int64_t N, int64_t* C, int64_t* Nm, int64_t* K, double* Knorm,
+                                     void* stream) {
+    if (!p) return GAKCO_E_ARG;
+    if (N < 1 || N >= ((int64_t)1 << 31)) return p->fail(GAKCO_E_ARG, "N must be in [1, 2^31)");
+    DeviceGuard dg(p->device);
+    cudaStream_t s = (cudaStream_t)stream;
+    const size_t bytes = (size_t)(p->M + 1) * N * N * 8;
+    int64_t* dC = C;
+    const bool hC = C && !is_device_ptr(C);
+    if (!C || hC) {
+        cudaError_t e = p->ensure(p->Cscr, bytes, s);
+        if (e != cudaSuccess) return p->cuda_fail(e, "C scratch");
+        dC = (int64_t*)p->Cscr.p;
+    }
+    cudaError_t e = cudaMemsetAsync(dC, 0, bytes, s);
+    if (e != cudaSuccess) return p->cuda_fail(e, "memset C");
+    gakco_status st = accumulate_impl(p, codes, offsets, N, dC, s, 0, 1);
+    if (st != GAKCO_OK) return st;
+    st = finalize_impl(p, dC, N, Nm, K, Knorm, s, true);
+    if (st != GAKCO_OK) return st;
+    if (hC) {
+        e = cudaMemcpyAsync(C, dC, bytes, cudaMemcpyDeviceToHost, s);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(s);
+        if (e != cudaSuccess) return p->cuda_fail(e, "copy C to host");
+    }
+    return GAKCO_OK;
+}
+
+extern "C" gakco_status gakco_get_stats(gakco_plan* p, gakco_stats* out) {
+    if (!p || !out) return GAKCO_E_ARG;
+    DeviceGuard dg(p->device);
+    gakco_stats r = p->host_stats;
+    if (p->stats.p) {
+        unsigned long long d[ST_COUNT];
+        cudaError_t e = cudaMemcpyAsync(d, p->stats.p, sizeof d, cudaMemcpyDeviceToHost,
+                                        p->last_stream);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(p->last_stream);
+        if (e != cudaSuccess) return p->cuda_fail(e, "stats");
+        r.triples = (int64_t)d[ST_TRIPLES];
+        r.groups_multi = (int64_t)d[ST_GROUPS];
+        r.light_pairs = (int64_t)d[ST_LIGHT_PAIRS];
+        r.heavy_groups = (int64_t)d[ST_HEAVY_GROUPS];
+        r.heavy_macs = (int64_t)d[ST_HEAVY_MACS];
+    }
+    double* ms[S_NSTAGE] = {&r.ms_encode, &r.ms_sort, &r.ms_segment,
+                            &r.ms_light,  &r.ms_heavy, &r.ms_epilogue};
+    for (auto& se : p->evs) {
+        float t = 0;
+        cudaEventSynchronize(se.second.second);
+        if (cudaEventElapsedTime(&t, se.second.first, se.second.second) == cudaSuccess)
+            *ms[se.first] += t;
+    }
+    *out = r;
+    return GAKCO_OK;
+}

@@ -1,0 +1,230 @@
+"""Thin ctypes binding of libgakco.so (include/gakco.h): argument marshalling only.
+
+Every step of the path runs in the CUDA library; this module only converts
+pointers, sizes and status codes. There is no CPU fallback: if libgakco.so is
+missing or CUDA is unavailable the calls raise.
+
+Function names follow the C-ABI: gakco_create, gakco_set_shard, gakco_set_option,
+gakco_accumulate, gakco_finalize, gakco_kernel, gakco_get_stats, gakco_num_masks,
+gakco_last_error, gakco_destroy. `Plan` wraps a plan handle; `kernel_matrix` is
+the one-call convenience used by the tests, smoke() and bench.py.
+"""
+from __future__ import annotations
+
+import ctypes
+import os
+
+import numpy as np
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "libgakco.so")
+
+GAKCO_OK = 0
+GAKCO_E_ARG = 1
+GAKCO_E_SYMBOL = 2
+GAKCO_E_RANGE = 3
+GAKCO_E_NOMEM = 4
+GAKCO_E_CUDA = 5
+GAKCO_E_INTERNAL = 6
+
+GAKCO_OPT_HEAVY_MIN_SEQS = 1
+GAKCO_OPT_BATCH_KEYS = 2
+GAKCO_OPT_TIMING = 3
+
+EXPORTS = ("gakco_create", "gakco_set_shard", "gakco_set_option", "gakco_accumulate",
+           "gakco_finalize", "gakco_kernel", "gakco_get_stats", "gakco_num_masks",
+           "gakco_last_error", "gakco_status_string", "gakco_destroy")
+
+
+class gakco_stats(ctypes.Structure):
+    _fields_ = [(n, ctypes.c_int64) for n in (
+        "masks", "keys", "sort_passes", "triples", "groups_multi", "light_pairs",
+        "heavy_groups", "heavy_macs")] + [(n, ctypes.c_double) for n in (
+            "ms_encode", "ms_sort", "ms_segment", "ms_light", "ms_heavy", "ms_epilogue")]
+
+    def as_dict(self):
+        return {n: getattr(self, n) for n, _ in self._fields_}
+
+
+class GakcoError(RuntimeError):
+    def __init__(self, status, msg):
+        super().__init__(f"gakco status {status}: {msg}")
+        self.status = status
+
+
+_lib = None
+
+
+def lib():
+    """Load libgakco.so (raises if it was not built: no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise ImportError(f"{LIB_PATH} not built; run `python -m paper_1704_07468_b200.build`")
+        L = ctypes.CDLL(LIB_PATH)
+        P, i64, ci = ctypes.c_void_p, ctypes.c_int64, ctypes.c_int
+        L.gakco_create.argtypes = [ci, ci, ci, ci, ci, ctypes.POINTER(P)]
+        L.gakco_set_shard.argtypes = [P, ci, ci]
+        L.gakco_set_option.argtypes = [P, ci, i64]
+        L.gakco_accumulate.argtypes = [P, P, P, i64, P, P]
+        L.gakco_finalize.argtypes = [P, P, i64, P, P, P, P]
+        L.gakco_kernel.argtypes = [P, P, P, i64, P, P, P, P, P]
+        L.gakco_get_stats.argtypes = [P, ctypes.POINTER(gakco_stats)]
+        L.gakco_num_masks.argtypes = [P, ci]
+        L.gakco_num_masks.restype = i64
+        L.gakco_last_error.argtypes = [P]
+        L.gakco_last_error.restype = ctypes.c_char_p
+        L.gakco_status_string.argtypes = [ci]
+        L.gakco_status_string.restype = ctypes.c_char_p
+        L.gakco_destroy.argtypes = [P]
+        L.gakco_destroy.restype = None
+        for f in ("gakco_create", "gakco_set_shard", "gakco_set_option", "gakco_accumulate",
+                  "gakco_finalize", "gakco_kernel", "gakco_get_stats"):
+            getattr(L, f).restype = ci
+        _lib = L
+    return _lib
+
+
+def _ptr(x):
+    """Address of a torch tensor (host or device), numpy array, int or None."""
+    if x is None:
+        return None
+    if isinstance(x, int):
+        return x
+    if isinstance(x, np.ndarray):
+        return x.ctypes.data
+    return x.data_ptr()  # torch.Tensor
+
+
+def _stream(stream):
+    if stream is None:
+        return None
+    if isinstance(stream, int):
+        return stream
+    return stream.cuda_stream  # torch.cuda.Stream
+
+
+def gakco_create(sigma, g, k, M, device=0):
+    h = ctypes.c_void_p()
+    st = lib().gakco_create(sigma, g, k, M, device, ctypes.byref(h))
+    if st != GAKCO_OK:
+        raise GakcoError(st, lib().gakco_status_string(st).decode())
+    return h.value
+
+
+def gakco_last_error(plan):
+    return lib().gakco_last_error(plan).decode()
+
+
+def _check(plan, st):
+    if st != GAKCO_OK:
+        raise GakcoError(st, gakco_last_error(plan))
+
+
+def gakco_set_shard(plan, rank, world):
+    _check(plan, lib().gakco_set_shard(plan, rank, world))
+
+
+def gakco_set_option(plan, option, value):
+    _check(plan, lib().gakco_set_option(plan, option, int(value)))
+
+
+def gakco_accumulate(plan, codes, offsets, N, C, stream=None):
+    _check(plan, lib().gakco_accumulate(plan, _ptr(codes), _ptr(offsets), N, _ptr(C),
+                                        _stream(stream)))
+
+
+def gakco_finalize(plan, C, N, Nm=None, K=None, Knorm=None, stream=None):
+    _check(plan, lib().gakco_finalize(plan, _ptr(C), N, _ptr(Nm), _ptr(K), _ptr(Knorm),
+                                      _stream(stream)))
+
+
+def gakco_kernel(plan, codes, offsets, N, C=None, Nm=None, K=None, Knorm=None, stream=None):
+    _check(plan, lib().gakco_kernel(plan, _ptr(codes), _ptr(offsets), N, _ptr(C), _ptr(Nm),
+                                    _ptr(K), _ptr(Knorm), _stream(stream)))
+
+
+def gakco_get_stats(plan):
+    s = gakco_stats()
+    _check(plan, lib().gakco_get_stats(plan, ctypes.byref(s)))
+    return s.as_dict()
+
+
+def gakco_num_masks(plan, shard_only=False):
+    return int(lib().gakco_num_masks(plan, 1 if shard_only else 0))
+
+
+def gakco_destroy(plan):
+    lib().gakco_destroy(plan)
+
+
+class Plan:
+    """Owning wrapper of a gakco_plan."""
+
+    def __init__(self, sigma, g, k, M=None, device=0):
+        self.sigma, self.g, self.k = sigma, g, k
+        self.M = g - k if M is None else M
+        self.device = device
+        self.h = gakco_create(sigma, g, k, self.M, device)
+
+    def set_shard(self, rank, world):
+        gakco_set_shard(self.h, rank, world)
+
+    def set_option(self, option, value):
+        gakco_set_option(self.h, option, value)
+
+    def accumulate(self, codes, offsets, N, C, stream=None):
+        gakco_accumulate(self.h, codes, offsets, N, C, stream)
+
+    def finalize(self, C, N, Nm=None, K=None, Knorm=None, stream=None):
+        gakco_finalize(self.h, C, N, Nm, K, Knorm, stream)
+
+    def kernel(self, codes, offsets, N, C=None, Nm=None, K=None, Knorm=None, stream=None):
+        gakco_kernel(self.h, codes, offsets, N, C, Nm, K, Knorm, stream)
+
+    def stats(self):
+        return gakco_get_stats(self.h)
+
+    def num_masks(self, shard_only=False):
+        return gakco_num_masks(self.h, shard_only)
+
+    def close(self):
+        if self.h:
+            gakco_destroy(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+def kernel_matrix(codes, offsets, sigma, g, k, M=None, device=0, plan=None, outputs=True,
+                  stream=None):
+    """All outputs on `device` as torch tensors: dict C, Nm, K, Knorm.
+
+    `codes` / `offsets` may be numpy arrays (host) or torch tensors (host/device).
+    """
+    import torch
+    M = g - k if M is None else M
+    N = int(offsets.shape[0]) - 1
+    dev = torch.device("cuda", device)
+    own = plan is None
+    plan = plan or Plan(sigma, g, k, M, device)
+    try:
+        C = torch.zeros((M + 1, N, N), dtype=torch.int64, device=dev)
+        Nm = torch.empty((M + 1, N, N), dtype=torch.int64, device=dev) if outputs else None
+        K = torch.empty((N, N), dtype=torch.int64, device=dev)
+        Kn = torch.empty((N, N), dtype=torch.float64, device=dev) if outputs else None
+        codes_c = np.ascontiguousarray(codes, dtype=np.uint8) if isinstance(codes, np.ndarray) else codes
+        off_c = np.ascontiguousarray(offsets, dtype=np.int64) if isinstance(offsets, np.ndarray) else offsets
+        if isinstance(codes_c, np.ndarray) and codes_c.size == 0:
+            codes_c = np.zeros(1, dtype=np.uint8)
+        with torch.cuda.device(dev):
+            s = stream or torch.cuda.current_stream(dev)
+            plan.kernel(codes_c, off_c, N, C, Nm, K, Kn, stream=s)
+        return {"C": C, "Nm": Nm, "K": K, "Knorm": Kn}
+    finally:
+        if own:
+            plan.close()

@@ -1,0 +1,242 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the CPU oracle.
+
+Bar: C_m, N_m, K bit-exact (int64); Knorm within 1e-12
+relative (BASELINE.json north_star), with the diagonal exactly 1.0.
+"""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from synth import corpus as sc
+from tests import refs
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+KNORM_RTOL = 1e-12
+
+
+@pytest.fixture(scope="module")
+def gk():
+    from paper_1704_07468_b200 import build, gakco
+    build.build()
+    assert torch.cuda.is_available(), "GPU tests need a CUDA device"
+    return gakco
+
+
+def run(gk, cp, g, k, M, **opts):
+    plan = gk.Plan(cp.sigma, g, k, M)
+    for opt, val in opts.items():
+        plan.set_option(getattr(gk, "GAKCO_OPT_" + opt.upper()), val)
+    r = gk.kernel_matrix(cp.codes, cp.offsets, cp.sigma, g, k, M, plan=plan)
+    out = {key: v.cpu().numpy() for key, v in r.items()}
+    out["stats"] = plan.stats()
+    plan.close()
+    return out
+
+
+def assert_parity(gpu, ref):
+    assert np.array_equal(gpu["C"], ref["C"])
+    assert np.array_equal(gpu["Nm"], ref["Nm"])
+    assert np.array_equal(gpu["K"], ref["K"])
+    assert_knorm(gpu["Knorm"], ref["Knorm"])
+
+
+def assert_knorm(a, b):
+    assert a.shape == b.shape
+    np.testing.assert_allclose(a, b, rtol=KNORM_RTOL, atol=0)
+    d = np.diag(b)
+    assert np.array_equal(np.diag(a), d)
+
+
+def test_fig2_through_abi(gk, oracle_lib):
+    """N_0(S,T)=2, C_1(S,T)=9, N_1(S,T)=3; K=[[15,9],[9,13]]."""
+    cp = sc.from_strings("ACGT", ["ACACA", "AAACA"])
+    r = run(gk, cp, 3, 2, 1)
+    assert r["Nm"][0, 0, 1] == 2 and r["C"][1, 0, 1] == 9 and r["Nm"][1, 0, 1] == 3
+    assert r["K"].tolist() == [[15, 9], [9, 13]]
+    assert r["Knorm"][0, 1] == pytest.approx(9 / np.sqrt(195), rel=1e-15)
+    assert_parity(r, oracle_lib.compute(cp, 3, 2, 1))
+
+
+def test_tiny_config(gk, oracle_lib):
+    cfg = sc.CONFIGS["tiny"]
+    cp = sc.make("tiny")
+    assert_parity(run(gk, cp, cfg.g, cfg.k, cfg.M), oracle_lib.compute(cp, cfg.g, cfg.k, cfg.M))
+
+
+def test_random_sweep(gk, oracle_lib):
+    """Seeded random corpora: Σ in {2,4,20,36}, ragged lengths (incl. < g and 0)."""
+    rng = np.random.default_rng(101)
+    for it in range(40):
+        sigma = int(rng.choice([2, 4, 20, 36]))
+        g = int(rng.integers(1, 11))
+        k = int(rng.integers(1, g + 1))
+        M = int(rng.integers(0, g + 1))
+        cp = sc.random_small(rng, sigma, n_max=40, l_max=120)
+        assert_parity(run(gk, cp, g, k, M), oracle_lib.compute(cp, g, k, M))
+
+
+def test_several_tiles_ragged(gk, oracle_lib):
+    """Enough g-mers to span many sort tiles (4096 keys) with a ragged tail."""
+    rng = np.random.default_rng(102)
+    seqs = [rng.integers(0, 4, size=int(rng.integers(0, 700))) for _ in range(60)]
+    cp = sc.from_sequences(4, seqs)
+    for (g, k, M) in [(6, 3, 3), (9, 5, 4), (12, 8, 4)]:
+        assert_parity(run(gk, cp, g, k, M), oracle_lib.compute(cp, g, k, M))
+
+
+def test_batch_size_invariance(gk, oracle_lib):
+    """Different mask batch sizes give identical results (integer sums)."""
+    cp = sc.make("tiny")
+    ref = oracle_lib.compute(cp, 7, 5, 2)
+    for bk in (1, 4700, 3 * 4700 + 5, 1 << 20):
+        assert_parity(run(gk, cp, 7, 5, 2, batch_keys=bk), ref)
+
+
+def test_edge_cases(gk, oracle_lib):
+    cases = [
+        (sc.from_sequences(4, [[0, 1, 2, 3, 0, 1]]), 3, 2, 1),      # N = 1
+        (sc.from_sequences(4, [[], [1, 2], [0] * 20]), 3, 1, 2),     # empty and short rows
+        (sc.from_sequences(4, [[], []]), 3, 1, 2),                   # no g-mers at all
+        (sc.from_sequences(1, [[0] * 30, [0] * 7]), 5, 2, 5),        # Σ = 1, M = g
+        (sc.from_sequences(255, [list(range(255)), list(range(254, -1, -1))]), 4, 2, 2),
+        (sc.from_sequences(4, [[0, 1] * 40, [1, 0] * 33]), 8, 8, 0),  # k = g, M = 0
+        (sc.from_sequences(36, [[5] * 200, [5] * 150, [7] * 90]), 10, 5, 10),
+    ]
+    for cp, g, k, M in cases:
+        assert_parity(run(gk, cp, g, k, M), oracle_lib.compute(cp, g, k, M))
+
+
+def test_shard_emulation(gk, oracle_lib):
+    """P shards accumulated into one C equal the 1-GPU result (mask sharding)."""
+    cp = sc.make("tiny")
+    g, k, M = 7, 5, 2
+    ref = oracle_lib.compute(cp, g, k, M)
+    N = cp.n_seq
+    for world in (2, 3, 8, 40):
+        C = torch.zeros((M + 1, N, N), dtype=torch.int64, device="cuda")
+        total = 0
+        for rank in range(world):
+            plan = gk.Plan(cp.sigma, g, k, M)
+            plan.set_shard(rank, world)
+            total += plan.num_masks(shard_only=True)
+            plan.accumulate(cp.codes, cp.offsets, N, C)
+            plan.close()
+        assert total == 29
+        plan = gk.Plan(cp.sigma, g, k, M)
+        Nm = torch.empty_like(C)
+        K = torch.empty((N, N), dtype=torch.int64, device="cuda")
+        Kn = torch.empty((N, N), dtype=torch.float64, device="cuda")
+        plan.finalize(C, N, Nm, K, Kn)
+        plan.close()
+        assert_parity({"C": C.cpu().numpy(), "Nm": Nm.cpu().numpy(), "K": K.cpu().numpy(),
+                       "Knorm": Kn.cpu().numpy()}, ref)
+
+
+def test_host_buffers_e2e(gk, oracle_lib):
+    """Host (pinned) inputs and host outputs through gakco_kernel (the e2e path)."""
+    cp = sc.make("tiny")
+    g, k, M = 7, 5, 2
+    N = cp.n_seq
+    ref = oracle_lib.compute(cp, g, k, M)
+    codes = torch.from_numpy(cp.codes).pin_memory()
+    offs = torch.from_numpy(cp.offsets).pin_memory()
+    K = torch.empty((N, N), dtype=torch.int64).pin_memory()
+    Kn = torch.empty((N, N), dtype=torch.float64).pin_memory()
+    plan = gk.Plan(cp.sigma, g, k, M)
+    plan.kernel(codes, offs, N, None, None, K, Kn)
+    plan.close()
+    assert np.array_equal(K.numpy(), ref["K"])
+    assert_knorm(Kn.numpy(), ref["Knorm"])
+
+
+def test_errors(gk):
+    with pytest.raises(gk.GakcoError) as e:
+        gk.Plan(4, 3, 4, 0)
+    assert e.value.status == gk.GAKCO_E_ARG
+    cp = sc.from_sequences(4, [[0, 1, 2, 3]])
+    bad = cp.codes.copy()
+    bad[1] = 9
+    with pytest.raises(gk.GakcoError) as e:
+        gk.kernel_matrix(bad, cp.offsets, 4, 3, 2, 1)
+    assert e.value.status == gk.GAKCO_E_SYMBOL
+    with pytest.raises(gk.GakcoError) as e:
+        gk.kernel_matrix(cp.codes, np.array([0, 5, 4]), 4, 3, 2, 1)
+    assert e.value.status == gk.GAKCO_E_ARG
+    # 36^12 keys and 11 bits of sequence id do not fit 64 bits at m = 0
+    long = sc.from_sequences(36, [[1] * 20] * 2000)
+    with pytest.raises(gk.GakcoError) as e:
+        gk.kernel_matrix(long.codes, long.offsets, 36, 13, 12, 1)
+    assert e.value.status == gk.GAKCO_E_RANGE
+
+
+def _golden(name):
+    with open(os.path.join(GOLDEN, f"oracle_{name}.json")) as f:
+        return json.load(f)
+
+
+@pytest.mark.parametrize("name", ["tiny", "dna", "protein"])
+def test_full_config_digests(gk, name):
+    """Full-size configs (bench's launch configuration) against the oracle's
+    committed digests (written by oracle/make_digests.py)."""
+    gold = _golden(name)
+    cfg = sc.CONFIGS[name]
+    cp = sc.make(name)
+    assert cp.sha256() == gold["corpus_sha256"], "generator drifted"
+    r = gk.kernel_matrix(cp.codes, cp.offsets, cfg.sigma, cfg.g, cfg.k, cfg.M)
+    d = gold["digests"]
+    for m in range(cfg.M + 1):
+        assert refs.digest_np(r["C"][m].cpu().numpy()) == int(d[f"C{m}"]), f"C{m}"
+        assert refs.digest_np(r["Nm"][m].cpu().numpy()) == int(d[f"N{m}"]), f"N{m}"
+    K = r["K"].cpu().numpy()
+    assert refs.digest_np(K) == int(d["K"])
+    # Knorm: reference recomputed from the verified K with the oracle's formula
+    import oracle
+    assert_knorm(r["Knorm"].cpu().numpy(), oracle.normalize(K))
+
+
+@pytest.mark.parametrize("name", ["text", "scale"])
+def test_large_config_sampled_pairs(gk, oracle_lib, name):
+    """Text / Scale at full size: sampled entries recomputed one by one by the
+    oracle (all diagonal entries of a sample of rows, random off-diagonal pairs,
+    and the highest-K pairs), plus the Knorm recomputation from K."""
+    cfg = sc.CONFIGS[name]
+    cp = sc.make(name)
+    N = cp.n_seq
+    r = gk.kernel_matrix(cp.codes, cp.offsets, cfg.sigma, cfg.g, cfg.k, cfg.M)
+    C = r["C"]
+    K = r["K"]
+    rng = np.random.default_rng(7)
+    X = rng.integers(0, N, 160)
+    Y = rng.integers(0, N, 160)
+    d = rng.integers(0, N, 40)
+    Kd = K.diagonal().cpu().numpy()
+    # the largest off-diagonal entries of a few rows (the most-updated cells)
+    rows = rng.integers(0, N, 8)
+    Kr = K[torch.as_tensor(rows, device=K.device)].clone()
+    Kr[torch.arange(8), torch.as_tensor(rows, device=K.device)] = -1
+    top = Kr.argmax(dim=1).cpu().numpy()
+    X = np.concatenate([X, d, rows])
+    Y = np.concatenate([Y, d, top])
+    nm = oracle_lib.pairs(cp, cfg.g, cfg.M, X, Y)
+    po = oracle_lib.pair_outputs(nm, cfg.g, cfg.k)
+    Xt = torch.as_tensor(X, device=C.device)
+    Yt = torch.as_tensor(Y, device=C.device)
+    assert np.array_equal(r["Nm"][:, Xt, Yt].cpu().numpy().T, nm)
+    assert np.array_equal(C[:, Xt, Yt].cpu().numpy().T, po["C"])
+    assert np.array_equal(K[Xt, Yt].cpu().numpy(), po["K"])
+    # properties at any size: symmetry, K == C_{g-k}
+    assert torch.equal(K, K.T)
+    assert torch.equal(K, C[cfg.g - cfg.k])
+    # Knorm from the (spot-verified) K, rows sampled
+    import oracle
+    sub = np.unique(np.concatenate([X, Y]))[:64]
+    Ks = K[torch.as_tensor(sub, device=K.device)][:, torch.as_tensor(sub, device=K.device)]
+    ref = oracle.normalize(Ks.cpu().numpy())
+    got = r["Knorm"][torch.as_tensor(sub, device=K.device)][:, torch.as_tensor(sub, device=K.device)]
+    assert_knorm(got.cpu().numpy(), ref)
+    assert np.array_equal(Kd[d], po["K"][160:200])
