@@ -1,0 +1,389 @@
+#!/usr/bin/env python
+"""bench.py — the gapped k-mer kernel-matrix step on 1..8 B200s.
+
+One STEP = the whole hot path of SURVEY.md §8(a) for one synthetic corpus:
+zero C -> gakco_accumulate over this rank's masks (encode, onesweep sort,
+segment, light/heavy pair updates, diagonal) -> NCCL int64 reduce of C to rank
+0 (N > 1) -> gakco_finalize on rank 0 (Eq. 9, Eq. 7, normalisation), with the
+corpus already resident in HBM. Masks are round-robin sharded across ranks;
+total work is fixed as N grows ("strong" scaling).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config dna] [--impl reference]
+
+Default workload: BASELINE.json configs[1] ("dna"). Prints ONE JSON line on
+rank 0. value = masked g-mer keys processed per second by the whole job
+(c_gk * n / step time); ms_per_step is the gkm kernel-matrix time.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+from synth import corpus as sc  # noqa: E402
+
+METRIC = "gkm kernel-matrix time (s) at 1/2/4/8 B200; masked g-mer keys sorted/s; HBM %"
+UNIT = "keys/s"
+
+
+def args_():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--config", default="dna", choices=list(sc.CONFIGS))
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0,
+                    help="target seconds of oracle work per CPU sample")
+    ap.add_argument("--heavy-min", type=int, default=0)
+    return ap.parse_args()
+
+
+def dist_env():
+    return (int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)),
+            int(os.environ.get("LOCAL_RANK", 0)))
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return {"hbm_gbs": d["hbm_gbs"], "bf16_tflops": d["bf16_tflops"],
+                "bf16_tflops_sustained": d.get("bf16_tflops_sustained"), "source": "measured"}
+    return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0,
+            "source": "fallback"}
+
+
+def workload(cfg_name):
+    cfg = sc.CONFIGS[cfg_name]
+    cp = sc.make(cfg_name)
+    from math import comb
+    masks = sum(comb(cfg.g, m) for m in range(cfg.M + 1))
+    n = int(sum(max(0, int(l) - cfg.g + 1) for l in cp.lengths()))
+    return cfg, cp, masks, n
+
+
+# --------------------------------------------------------------------- clocks
+class Clocks:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        try:
+            self.p = subprocess.Popen(
+                ["nvidia-smi", "-i", str(gpu_index), f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "200"],
+                stdout=self.f, stderr=subprocess.DEVNULL)
+        except FileNotFoundError:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return None
+        self.p.terminate()
+        try:
+            self.p.wait(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.p.kill()
+        self.f.flush()
+        rows = [r.split(",") for r in open(self.f.name).read().strip().splitlines() if r.strip()]
+        os.unlink(self.f.name)
+        sm, smax, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            r = [x.strip() for x in r]
+            try:
+                sm.append(float(r[1]))
+                smax.append(float(r[2]))
+            except (ValueError, IndexError):
+                continue
+            for nm, v in zip(names, r[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return None
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(smax),
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------- CPU baseline
+def oracle_sample(cp, cfg, seconds, threads):
+    """Time the oracle (as it stands) on rows [0, r) of the matrix; r is sized
+    from a 1-row calibration so the sample takes about `seconds`. Returns
+    (sample seconds, fraction of the full upper-triangle work, rows)."""
+    import numpy as np
+    import oracle
+    n = np.maximum(cp.lengths() - cfg.g + 1, 0).astype(np.float64)
+    suffix = np.cumsum(n[::-1])[::-1]             # sum_{y>=x} n_y
+    row_work = n * suffix                          # window steps of row x (y >= x)
+    total = row_work.sum()
+    t0 = time.perf_counter()
+    oracle.digests(cp, cfg.g, cfg.k, cfg.M, threads=threads, row_begin=0, row_end=1, rows=False)
+    t1 = time.perf_counter() - t0
+    # calibration includes the K(X,X) pass (N pairs); subtract it from the per-row rate
+    rate = max(row_work[0], 1.0) / max(t1, 1e-4)
+    target = rate * seconds
+    r = int(np.searchsorted(np.cumsum(row_work), target)) + 1
+    r = max(1, min(cp.n_seq, r))
+    t0 = time.perf_counter()
+    oracle.digests(cp, cfg.g, cfg.k, cfg.M, threads=threads, row_begin=0, row_end=r, rows=False)
+    dt = time.perf_counter() - t0
+    frac = row_work[:r].sum() / total
+    return dt, frac, r
+
+
+def run_reference(a):
+    """--impl reference: the CPU oracle as it stands, on the host cores."""
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    import oracle
+    oracle.build()
+    cfg, cp, masks, n = workload(a.config)
+    threads = os.cpu_count() or 1
+    per = max(2.0, min(a.cpu_seconds, 150.0 / max(1, a.steps + a.warmup)))
+    for _ in range(a.warmup):
+        oracle_sample(cp, cfg, per / 2, threads)
+    times, fracs, rows = [], [], []
+    for _ in range(a.steps):
+        dt, frac, r = oracle_sample(cp, cfg, per, threads)
+        times.append(dt / frac)   # extrapolated full-matrix seconds
+        fracs.append(frac)
+        rows.append(r)
+    t = statistics.median(times)
+    value = masks * n / t
+    sample = (f"oracle rows [0,{rows[-1]}) x all Y>=X of the {a.config} corpus "
+              f"({100 * fracs[-1]:.2f}% of the upper-triangle pair work), full-matrix time "
+              f"extrapolated by pair work; digests of C_m, N_m, K, Knorm")
+    out = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT,
+           "n_gpus": a.gpus, "steps": a.steps, "warmup": a.warmup, "ms_per_step": t * 1e3,
+           "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "int64",
+           "data": "synthetic",
+           "config": config_dict(a.config, cfg, cp, masks, n, 1),
+           "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle",
+                            "sample": sample},
+           "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
+                   "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+def config_dict(name, cfg, cp, masks, n, world):
+    return {"workload": name, "baseline_config": cfg.description, "N": cp.n_seq,
+            "sigma": cfg.sigma, "g": cfg.g, "k": cfg.k, "M": cfg.M, "masks": masks,
+            "gmers": n, "keys_per_step": masks * n,
+            "parallelism": f"mask-sharded x{world} + NCCL int64 reduce" if world > 1
+            else "1 GPU, all masks",
+            "l2": "flushed between timed steps (256 MiB write)"}
+
+
+# ----------------------------------------------------------------- GPU arm
+def stage_model(stats, cfg, N):
+    """Algorithmic bytes / ops per stage: unit x count."""
+    keys, passes = stats["keys"], stats["sort_passes"]
+    trip, grp = stats["triples"], stats["groups_multi"]
+    M = cfg.M
+    epi = N * N * ((M + 1) * 4 + (M + 1) * 4 + (M + 1) * 8 + 16) + N * (M + 1) * 8
+    return {
+        "encode": ("hbm", 12.0 * keys),            # write 8 B key + read 4 B seq id
+        "sort": ("hbm", 16.0 * passes),            # read + write 8 B per key per pass
+        "segment": ("hbm", 8.0 * keys + 16.0 * trip + 8.0 * grp),
+        "light": ("hbm", 16.0 * stats["light_pairs"]),  # int64 read-modify-write per update
+        "heavy": ("tensor", 2.0 * stats["heavy_macs"]),
+        "epilogue": ("hbm", float(epi)),
+    }
+
+
+def run_ours(a):
+    import torch
+    import torch.distributed as dist
+    from paper_1704_07468_b200 import gakco
+
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    cfg, cp, masks, n = workload(a.config)
+    N = cp.n_seq
+    M = cfg.M
+    codes_d = torch.from_numpy(cp.codes).to(dev)
+    offs_h = torch.from_numpy(cp.offsets).pin_memory()
+    plan = gakco.Plan(cfg.sigma, cfg.g, cfg.k, M, local)
+    plan.set_shard(rank, world)
+    plan.set_option(gakco.GAKCO_OPT_TIMING, 1)
+    if a.heavy_min:
+        plan.set_option(gakco.GAKCO_OPT_HEAVY_MIN_SEQS, a.heavy_min)
+    C = torch.zeros((M + 1, N, N), dtype=torch.int64, device=dev)
+    Nm = torch.empty_like(C) if rank == 0 else None
+    K = torch.empty((N, N), dtype=torch.int64, device=dev) if rank == 0 else None
+    Kn = torch.empty((N, N), dtype=torch.float64, device=dev) if rank == 0 else None
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step():
+        C.zero_()
+        plan.accumulate(codes_d, offs_h, N, C, stream)
+        if world > 1:
+            dist.reduce(C, dst=0, op=dist.ReduceOp.SUM)
+        if rank == 0:
+            plan.finalize(C, N, Nm, K, Kn, stream)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    for _ in range(a.warmup):
+        step()
+    barrier()
+    clk = Clocks(local) if rank == 0 else None
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(a.steps)]
+    stage_ms = {}
+    launches = 0
+    last = None
+    barrier()
+    for i in range(a.steps):
+        flush.fill_(i)                      # L2 flush, outside the step's events
+        ev[i][0].record(stream)
+        step()
+        ev[i][1].record(stream)
+        st = plan.stats()              # synchronises; after the end event
+        for kk, v in st.items():
+            if kk.startswith("ms_"):
+                stage_ms[kk] = stage_ms.get(kk, 0.0) + v
+        launches += st["launches"]
+        last = st
+    barrier()
+    clocks = clk.stop() if clk else None
+    step_ms = [e0.elapsed_time(e1) for e0, e1 in ev]
+    mine = torch.tensor([sum(step_ms)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(mine, op=dist.ReduceOp.MAX)
+    total_ms = float(mine.item())
+    ms_per_step = total_ms / a.steps
+    value = masks * n / (ms_per_step / 1e3)
+
+    # ---- e2e through the public C-ABI with host (pinned) buffers
+    e2e = None
+    if not a.no_e2e:
+        codes_h = torch.from_numpy(cp.codes).pin_memory()
+        Kh = torch.empty((N, N), dtype=torch.int64).pin_memory() if rank == 0 else None
+        Knh = torch.empty((N, N), dtype=torch.float64).pin_memory() if rank == 0 else None
+
+        def e2e_step():
+            if world == 1:
+                plan.kernel(codes_h, offs_h, N, C, None, Kh, Knh, stream)
+            else:
+                C.zero_()
+                plan.accumulate(codes_h, offs_h, N, C, stream)
+                dist.reduce(C, dst=0, op=dist.ReduceOp.SUM)
+                if rank == 0:
+                    plan.finalize(C, N, None, Kh, Knh, stream)
+        for _ in range(2):
+            e2e_step()
+        barrier()
+        ee = []
+        for i in range(a.steps):
+            flush.fill_(i)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            e2e_step()
+            e1.record(stream)
+            torch.cuda.synchronize(dev)
+            ee.append(e0.elapsed_time(e1))
+        t = torch.tensor([sum(ee)], dtype=torch.float64, device=dev)
+        if world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e_ms = float(t.item()) / a.steps
+        h2d = (cp.codes.nbytes + cp.offsets.nbytes) * world
+        d2h = N * N * 16
+        e2e = {"value": masks * n / (e_ms / 1e3), "unit": UNIT, "ms_per_step": e_ms,
+               "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+               "api": "gakco_kernel(host pinned codes/offsets -> host K, Knorm)" if world == 1
+               else "gakco_accumulate(host inputs) + NCCL reduce + gakco_finalize(host K, Knorm)"}
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return
+
+    # ---- roofline of the dominant stage (CUDA events on the launching stream)
+    pk = peaks()
+    model = stage_model(last, cfg, N)
+    per_step = {k[3:]: v / a.steps for k, v in stage_ms.items()}
+    dom = max(per_step, key=lambda s: per_step[s])
+    bound, algo = model[dom]
+    t_dom = per_step[dom] / 1e3
+    stages = {}
+    for s_, ms in per_step.items():
+        b_, alg = model[s_]
+        if ms > 0:
+            stages[s_] = {"ms": round(ms, 4), "bound": b_,
+                          ("GB/s" if b_ == "hbm" else "TOPS"):
+                              round(alg / (ms / 1e3) / (1e9 if b_ == "hbm" else 1e12), 2)}
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(prof):
+        with open(prof) as f:
+            tr = json.load(f)
+        if a.config in tr and dom in tr[a.config]:
+            traffic = tr[a.config][dom]
+    if bound == "hbm":
+        achieved = algo / t_dom / 1e9 if t_dom > 0 else 0.0
+        peak = pk["hbm_gbs"]
+        roof = {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak,
+                "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
+                "algorithmic_bytes_per_step": algo, "peak_source": pk["source"] + " hbm_gbs"}
+    else:
+        achieved = algo / t_dom / 1e12 if t_dom > 0 else 0.0
+        peak = pk["bf16_tflops"] * 2.0  # int8 = 2x bf16 (nominal 4.5 vs 2.25 PFLOP/s)
+        roof = {"bound": "tensor", "kernel": dom, "achieved": achieved, "peak": peak,
+                "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
+                "peak_source": pk["source"] + " bf16_tflops x2 (int8 nominal ratio)"}
+
+    out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
+           "warmup": a.warmup, "ms_per_step": ms_per_step,
+           "kernel_matrix_seconds": ms_per_step / 1e3, "higher_is_better": True,
+           "scaling": "strong", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+           "config": config_dict(a.config, cfg, cp, masks, n, world),
+           "roofline": roof, "stages": stages, "gpu_launches": int(launches),
+           "clocks": clocks, "e2e": e2e,
+           "counters": {k: v for k, v in last.items() if not k.startswith("ms_")}}
+    if world == 1 and not a.no_cpu_baseline:
+        import oracle
+        oracle.build()
+        threads = os.cpu_count() or 1
+        dt, frac, r = oracle_sample(cp, cfg, a.cpu_seconds, threads)
+        out["cpu_baseline"] = {
+            "value": masks * n / (dt / frac), "unit": UNIT, "cores": threads, "kind": "oracle",
+            "sample": f"oracle rows [0,{r}) x all Y>=X ({100 * frac:.2f}% of the upper-triangle "
+                      f"pair work, {dt:.1f} s), extrapolated to the full matrix by pair work"}
+    print(json.dumps(out), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    a = args_()
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        run_ours(a)
+
+
+if __name__ == "__main__":
+    main()

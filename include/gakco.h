@@ -74,6 +74,7 @@ typedef struct {
     int64_t light_pairs;    /* off-diagonal pair updates done by the light path */
     int64_t heavy_groups;   /* groups sent to the tensor-core Gram */
     int64_t heavy_macs;     /* u8 multiply-accumulates issued by the Gram */
+    int64_t launches;       /* kernels launched by the last accumulate + finalize */
     double ms_encode, ms_sort, ms_segment, ms_light, ms_heavy, ms_epilogue;
 } gakco_stats;
 

@@ -1,0 +1,333 @@
+// gram_tc.cu — heavy groups as a dense count Gram on the 5th-gen tensor cores.
+//
+// countAndUpdate adds c_X(key)*c_Y(key) to C_m(X,Y) for every
+// pair of sequences sharing a key. For the R keys ("heavy groups", many
+// sequences each) of a chunk this is exactly
+//     C_m += D D^T,    D[X][r] = count of sequence X in group r  (u8),
+// a dense contraction over r. It runs as tcgen05.mma.kind::i8 (u8 x u8 -> s32,
+// exact) with D tiles brought in by TMA (128B swizzle, K-major) and the s32
+// accumulators in TMEM; the epilogue adds them to the int64 C_m (entries with
+// Y > X only: the diagonal is accounted for by the closed form + repeat term).
+//
+// Exactness: a chunk never spans more masks than (2^31-1)/n_max^2 (per mask an
+// entry grows by at most n_X*n_Y), and counts > 255 are routed to the light
+// path, so the s32 sums are exact and their int64 adds are exact.
+//
+// Kernel layout (one CTA per SM, persistent over output tiles 128 x 256):
+//   warp 4      TMA producer (one elected lane), 4-stage smem ring
+//   warp 5      MMA issuer (one elected lane), 2 TMEM accumulators of 256 cols
+//   warps 0-3   epilogue: tcgen05.ld 32x32b -> +C (int64), lane = output row
+#include <cuda.h>
+
+#include "internal.cuh"
+
+namespace gk {
+
+constexpr int GT_M = 128;              // output rows per tile (TMEM lanes)
+constexpr int GT_N = 256;              // output cols per tile (TMEM columns)
+constexpr int GT_KB = 128;             // bytes (= u8 elements) of K per stage
+constexpr int GT_STAGES = 4;
+constexpr int GT_A_BYTES = GT_M * GT_KB;          // 16 KB
+constexpr int GT_B_BYTES = GT_N * GT_KB;          // 32 KB
+constexpr int GT_STAGE_BYTES = GT_A_BYTES + GT_B_BYTES;
+constexpr int GT_THREADS = 192;
+constexpr size_t GT_SMEM = (size_t)GT_STAGES * GT_STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+
+// ---------------------------------------------------------------- PTX helpers
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(b)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "WAIT_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra WAIT_%=;\n"
+        "}\n" ::"r"(smem_u32(b)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                            int x, int y) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4}], [%2];" ::"r"(smem_u32(dst)),
+        "l"((uint64_t)map), "r"(smem_u32(bar)), "r"(x), "r"(y)
+        : "memory");
+}
+__device__ __forceinline__ void tc_fence_after() {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_fence_before() {
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+}
+__device__ __forceinline__ void tc_commit(uint64_t* b) {
+    asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                     smem_u32(b))
+                 : "memory");
+}
+__device__ __forceinline__ void tc_mma_u8(uint32_t tmem_d, uint64_t adesc, uint64_t bdesc,
+                                          uint32_t idesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "setp.ne.b32 p, %4, 0;\n"
+        "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n"
+        "}\n" ::"r"(tmem_d),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+// 32 lanes x 32 consecutive 32-bit columns; thread t of the warp gets row (lane base + t).
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+        "%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+          "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]),
+          "=r"(v[13]), "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]),
+          "=r"(v[19]), "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]),
+          "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]),
+          "=r"(v[31])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// Shared-memory matrix descriptor, K-major, 128B swizzle: 8-row x 128 B atoms,
+// SBO = 1024 B between 8-row groups, LBO unused (1), version 1 (sm_100).
+__device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr >> 4) & 0x3fff);
+    d |= (uint64_t)1 << 16;                 // LBO (ignored for swizzled K-major)
+    d |= (uint64_t)(1024 >> 4) << 32;       // SBO
+    d |= (uint64_t)1 << 46;                 // descriptor version (sm_100)
+    d |= (uint64_t)2 << 61;                 // SWIZZLE_128B
+    return d;
+}
+
+// Instruction descriptor: u8 x u8 -> s32, K-major A and B, M = 128, N = 256.
+constexpr uint32_t GT_IDESC = (2u << 4)               // D format s32
+                              | (0u << 7) | (0u << 10)  // A, B unsigned 8-bit
+                              | ((uint32_t)(GT_N >> 3) << 17) | ((uint32_t)(GT_M >> 4) << 24);
+
+struct GramArgs {
+    int64_t* Cm;        // [N][N] int64, upper entries Y > X updated
+    int64_t N;
+    int kblocks;        // K / 128
+    const int2* tiles;  // (row block of 128, col block of 256)
+    int ntiles;
+};
+
+__global__ void __launch_bounds__(GT_THREADS, 1)
+    gram_kernel(const __grid_constant__ CUtensorMap dmap, GramArgs a) {
+    extern __shared__ __align__(1024) unsigned char smem_raw[];
+    unsigned char* smem = (unsigned char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+    uint64_t* bars = (uint64_t*)(smem + (size_t)GT_STAGES * GT_STAGE_BYTES);
+    uint64_t* full = bars;                      // [STAGES]
+    uint64_t* empty = bars + GT_STAGES;         // [STAGES]
+    uint64_t* tfull = bars + 2 * GT_STAGES;     // [2]
+    uint64_t* tempty = bars + 2 * GT_STAGES + 2;  // [2]
+    uint32_t* tmem_slot = (uint32_t*)(bars + 2 * GT_STAGES + 4);
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < GT_STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&tfull[i], 1);
+            mbar_init(&tempty[i], 128);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    if (warp == 0) {
+        asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+                         smem_u32(tmem_slot))
+                     : "memory");
+        asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    const uint32_t tmem = *tmem_slot;
+
+    if (warp == 4) {
+        // ------------------------------------------------ TMA producer
+        if (lane == 0) {
+            asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&dmap) : "memory");
+            uint32_t stage = 0, phase = 0;
+            for (int t = blockIdx.x; t < a.ntiles; t += gridDim.x) {
+                const int2 tl = a.tiles[t];
+                for (int kb = 0; kb < a.kblocks; ++kb) {
+                    mbar_wait(&empty[stage], phase ^ 1);
+                    unsigned char* sa = smem + (size_t)stage * GT_STAGE_BYTES;
+                    unsigned char* sbm = sa + GT_A_BYTES;
+                    mbar_expect_tx(&full[stage], GT_STAGE_BYTES);
+                    tma_load_2d(sa, &dmap, &full[stage], kb * GT_KB, tl.x * GT_M);
+                    tma_load_2d(sbm, &dmap, &full[stage], kb * GT_KB, tl.y * GT_N);
+                    tma_load_2d(sbm + GT_A_BYTES, &dmap, &full[stage], kb * GT_KB,
+                                tl.y * GT_N + GT_M);
+                    if (++stage == GT_STAGES) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+            }
+        }
+    } else if (warp == 5) {
+        // ------------------------------------------------ MMA issuer
+        if (lane == 0) {
+            uint32_t stage = 0, phase = 0;
+            int it = 0;
+            for (int t = blockIdx.x; t < a.ntiles; t += gridDim.x, ++it) {
+                const int acc = it & 1;
+                const uint32_t acc_phase = (it >> 1) & 1;
+                mbar_wait(&tempty[acc], acc_phase ^ 1);
+                tc_fence_after();
+                const uint32_t dcol = tmem + acc * GT_N;
+                for (int kb = 0; kb < a.kblocks; ++kb) {
+                    mbar_wait(&full[stage], phase);
+                    tc_fence_after();
+                    const uint32_t sa = smem_u32(smem + (size_t)stage * GT_STAGE_BYTES);
+                    const uint32_t sbm = sa + GT_A_BYTES;
+#pragma unroll
+                    for (int kk = 0; kk < GT_KB / 32; ++kk)
+                        tc_mma_u8(dcol, sw128_desc(sa + kk * 32), sw128_desc(sbm + kk * 32),
+                                  GT_IDESC, (kb | kk) != 0);
+                    tc_commit(&empty[stage]);
+                    if (++stage == GT_STAGES) {
+                        stage = 0;
+                        phase ^= 1;
+                    }
+                }
+                tc_commit(&tfull[acc]);
+            }
+        }
+    } else {
+        // ------------------------------------------------ epilogue (warps 0-3)
+        int it = 0;
+        for (int t = blockIdx.x; t < a.ntiles; t += gridDim.x, ++it) {
+            const int acc = it & 1;
+            const uint32_t acc_phase = (it >> 1) & 1;
+            const int2 tl = a.tiles[t];
+            mbar_wait(&tfull[acc], acc_phase);
+            tc_fence_after();
+            const int64_t x = (int64_t)tl.x * GT_M + warp * 32 + lane;
+            const int64_t y0 = (int64_t)tl.y * GT_N;
+#pragma unroll 1
+            for (int c = 0; c < GT_N; c += 32) {
+                uint32_t v[32];
+                tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16) + acc * GT_N + c, v);
+                if (x < a.N) {
+                    int64_t* row = a.Cm + x * a.N;
+#pragma unroll
+                    for (int j = 0; j < 32; ++j) {
+                        const int64_t y = y0 + c + j;
+                        if (y > x && y < a.N && v[j]) row[y] += (int64_t)(int32_t)v[j];
+                    }
+                }
+            }
+            tc_fence_before();
+            mbar_arrive(&tempty[acc]);
+        }
+    }
+    __syncthreads();
+    if (warp == 0) {
+        tc_fence_after();
+        asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem)
+                     : "memory");
+    }
+}
+
+// ---------------------------------------------------------------- D builder
+// D[x][r] = count of sequence x in heavy group r (buffer zeroed beforehand).
+__global__ void build_dense_kernel(SegmentOut so, const uint32_t* __restrict__ heavy,
+                                   uint32_t r0, uint32_t R, uint32_t ldd,
+                                   uint8_t* __restrict__ D) {
+    const int lane = threadIdx.x & 31;
+    const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
+    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
+    for (uint64_t r = warp; r < R; r += nwarps) {
+        const uint32_t gi = heavy[r0 + r];
+        const uint32_t a = so.gstart[gi], b = so.gend[gi];
+        for (uint32_t t = a + lane; t < b; t += 32) {
+            const uint32_t x = so.tseq[t] & 0x7fffffffu;
+            D[(uint64_t)x * ldd + r] = (uint8_t)so.tcnt[t];
+        }
+    }
+}
+
+// ---------------------------------------------------------------- host side
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeTiledFn get_encode() {
+    static EncodeTiledFn fn = nullptr;
+    if (!fn) {
+        void* p = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) ==
+                cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = (EncodeTiledFn)p;
+    }
+    return fn;
+}
+
+size_t gram_smem_bytes() { return GT_SMEM; }
+
+// Upper tiles (row block of 128 x col block of 256) that hold any Y > X entry.
+std::vector<int2> gram_tiles(int64_t n_pad) {
+    std::vector<int2> t;
+    const int rb = (int)(n_pad / GT_M), cb = (int)(n_pad / GT_N);
+    for (int i = 0; i < rb; ++i)
+        for (int j = 0; j < cb; ++j)
+            if ((int64_t)j * GT_N + GT_N - 1 > (int64_t)i * GT_M) t.push_back(make_int2(i, j));
+    return t;
+}
+
+cudaError_t launch_build_dense(SegmentOut so, const uint32_t* heavy, uint32_t r0, uint32_t R,
+                               uint32_t ldd, uint8_t* D, int sm_count, cudaStream_t s) {
+    if (R == 0) return cudaGetLastError();
+    uint64_t blocks = (R + 7) / 8;
+    if (blocks > (uint64_t)sm_count * 16) blocks = (uint64_t)sm_count * 16;
+    build_dense_kernel<<<(unsigned)blocks, 256, 0, s>>>(so, heavy, r0, R, ldd, D);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_gram(const uint8_t* D, int64_t n_pad, uint32_t ldd, uint32_t kcols,
+                        int64_t* Cm, int64_t N, const int2* tiles, int ntiles, int sm_count,
+                        cudaStream_t s) {
+    EncodeTiledFn enc = get_encode();
+    if (!enc) return cudaErrorNotSupported;
+    CUtensorMap map;
+    cuuint64_t dims[2] = {ldd, (cuuint64_t)n_pad};
+    cuuint64_t strides[1] = {ldd};
+    cuuint32_t box[2] = {GT_KB, GT_M};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = enc(&map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, (void*)D, dims, strides, box, estr,
+                     CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                     CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
+    cudaFuncSetAttribute(gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GT_SMEM);
+    GramArgs a{Cm, N, (int)(kcols / GT_KB), tiles, ntiles};
+    int grid = ntiles < sm_count ? ntiles : sm_count;
+    gram_kernel<<<grid, GT_THREADS, GT_SMEM, s>>>(map, a);
+    return cudaGetLastError();
+}
+
+}  // namespace gk

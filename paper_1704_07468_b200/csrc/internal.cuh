@@ -124,8 +124,19 @@ cudaError_t launch_triples(const uint64_t* keys, uint64_t n, int nseg, int sb, i
                            SegmentOut so, unsigned long long* stats, cudaStream_t s);
 cudaError_t launch_groups(uint64_t max_triples, uint64_t* status, uint32_t* ctr, uint32_t epoch,
                           SegmentOut so, unsigned long long* stats, cudaStream_t s);
+// Light pair updates; groups with >= heavy_min sequences (and counts <= 255) are
+// appended to heavy[] (count in *heavy_count) for the tensor-core Gram instead.
 cudaError_t launch_light(SegmentOut so, uint64_t max_groups, int64_t heavy_min, int64_t N,
-                         int64_t* Cm, unsigned long long* stats, int sm_count, cudaStream_t s);
+                         int64_t* Cm, uint32_t* heavy, uint32_t* heavy_count,
+                         unsigned long long* stats, int sm_count, cudaStream_t s);
+// Heavy path (gram_tc.cu)
+size_t gram_smem_bytes();
+std::vector<int2> gram_tiles(int64_t n_pad);
+cudaError_t launch_build_dense(SegmentOut so, const uint32_t* heavy, uint32_t r0, uint32_t R,
+                               uint32_t ldd, uint8_t* D, int sm_count, cudaStream_t s);
+cudaError_t launch_gram(const uint8_t* D, int64_t n_pad, uint32_t ldd, uint32_t kcols,
+                        int64_t* Cm, int64_t N, const int2* tiles, int ntiles, int sm_count,
+                        cudaStream_t s);
 cudaError_t launch_diag_closed_form(const int64_t* gofs, int64_t N, int64_t nmask, int64_t* Cm,
                                     cudaStream_t s);
 cudaError_t launch_epilogue(int64_t* C, int64_t N, int g, int k, int M, int64_t* Nm, int64_t* K,

@@ -12,16 +12,28 @@
 namespace gk {
 
 __global__ void __launch_bounds__(256) light_kernel(SegmentOut so, int64_t heavy_min, int64_t N,
-                                                    int64_t* Cm, unsigned long long* stats) {
+                                                    int64_t* Cm, uint32_t* heavy,
+                                                    uint32_t* heavy_count,
+                                                    unsigned long long* stats) {
     const uint32_t G = so.counts[1];
     const int lane = threadIdx.x & 31;
     const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
     const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-    unsigned long long pairs = 0;
+    unsigned long long pairs = 0, nheavy = 0;
     for (uint64_t gi = warp; gi < G; gi += nwarps) {
         const uint32_t a0 = so.gstart[gi], b0 = so.gend[gi];
         const uint32_t s = b0 - a0;
-        if ((int64_t)s >= heavy_min) continue;  // dense tensor-core path
+        if ((int64_t)s >= heavy_min) {
+            // dense tensor-core path if every count fits the u8 operand
+            uint32_t cmax = 0;
+            for (uint32_t t = a0 + lane; t < b0; t += 32) cmax = max(cmax, so.tcnt[t]);
+            cmax = __reduce_max_sync(0xffffffffu, cmax);
+            if (cmax <= 255u) {
+                if (lane == 0) heavy[atomicAdd(heavy_count, 1u)] = (uint32_t)gi;
+                ++nheavy;
+                continue;
+            }
+        }
         pairs += (unsigned long long)s * (s - 1) / 2;
         for (uint32_t a = a0; a + 1 < b0; ++a) {
             const int64_t xa = so.tseq[a] & 0x7fffffffu;
@@ -34,15 +46,19 @@ __global__ void __launch_bounds__(256) light_kernel(SegmentOut so, int64_t heavy
         }
     }
     if (lane == 0 && pairs) atomicAdd(&stats[ST_LIGHT_PAIRS], pairs);
+    if (lane == 0 && nheavy) atomicAdd(&stats[ST_HEAVY_GROUPS], nheavy);
 }
 
 cudaError_t launch_light(SegmentOut so, uint64_t max_groups, int64_t heavy_min, int64_t N,
-                         int64_t* Cm, unsigned long long* stats, int sm_count, cudaStream_t s) {
-    if (max_groups == 0) return cudaGetLastError();
+                         int64_t* Cm, uint32_t* heavy, uint32_t* heavy_count,
+                         unsigned long long* stats, int sm_count, cudaStream_t s) {
+    cudaError_t e = cudaMemsetAsync(heavy_count, 0, sizeof(uint32_t), s);
+    if (e != cudaSuccess || max_groups == 0) return e;
     uint64_t blocks = (max_groups + 7) / 8;
     uint64_t cap = (uint64_t)sm_count * 8;
     if (blocks > cap) blocks = cap;
-    light_kernel<<<(unsigned)blocks, 256, 0, s>>>(so, heavy_min, N, Cm, stats);
+    light_kernel<<<(unsigned)blocks, 256, 0, s>>>(so, heavy_min, N, Cm, heavy, heavy_count,
+                                                  stats);
     return cudaGetLastError();
 }
 

@@ -85,7 +85,9 @@ struct gakco_plan {
     std::vector<int> key_bits;  // per level
 
     DevBuf codes, off, gofs, gmseq, keysA, keysB, hist, status, ctr, tseq, tcnt, gstart, gend,
-        counts, kept, stats, flags, kdiag, Cscr, Nmscr, Kscr, Knscr;
+        counts, kept, stats, flags, kdiag, Cscr, Nmscr, Kscr, Knscr, heavy, hcount, dense, tiles;
+    int64_t tiles_npad = -1;
+    int ntiles = 0;
     uint32_t epoch = 1;
     uint32_t ctr_next = 0;
     static constexpr uint32_t CTR_SLOTS = 4096;
@@ -96,6 +98,8 @@ struct gakco_plan {
     gakco_stats host_stats{};
     cudaStream_t last_stream = nullptr;
     int64_t last_masks = 0;
+    int64_t launches = 0;
+    bool after_accumulate = false;
 
     std::vector<int64_t> h_off, h_gofs;
 
@@ -231,7 +235,8 @@ extern "C" void gakco_destroy(gakco_plan* p) {
     DevBuf* bufs[] = {&p->codes, &p->off,   &p->gofs,  &p->gmseq,  &p->keysA, &p->keysB,
                       &p->hist,  &p->status, &p->ctr,  &p->tseq,   &p->tcnt,  &p->gstart,
                       &p->gend,  &p->counts, &p->kept, &p->stats,  &p->flags, &p->kdiag,
-                      &p->Cscr,  &p->Nmscr, &p->Kscr,  &p->Knscr};
+                      &p->Cscr,  &p->Nmscr, &p->Kscr,  &p->Knscr, &p->heavy, &p->hcount,
+                      &p->dense, &p->tiles};
     for (DevBuf* b : bufs)
         if (b->p) cudaFree(b->p);
     for (cudaEvent_t e : p->ev_pool) cudaEventDestroy(e);
@@ -279,6 +284,12 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
         cudaError_t e_ = (x);                          \
         if (e_ != cudaSuccess) return p->cuda_fail(e_, #x); \
     } while (0)
+#define LK(x)        \
+    do {             \
+        ++p->launches; \
+        CK(x);       \
+    } while (0)
+    p->launches = 0;
     if (!codes && N > 0) return p->fail(GAKCO_E_ARG, "codes is NULL");
     if (!offsets || !C) return p->fail(GAKCO_E_ARG, "offsets or C is NULL");
     if (N < 1 || N >= ((int64_t)1 << 31)) return p->fail(GAKCO_E_ARG, "N must be in [1, 2^31)");
@@ -333,7 +344,7 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
     if (L > 0) {
         if (is_device_ptr(codes)) {
             CK(cudaMemcpyAsync(p->codes.p, codes, L, cudaMemcpyDeviceToDevice, s));
-            CK(launch_check_codes((const uint8_t*)p->codes.p, L, p->sigma, (int*)p->flags.p, s));
+            LK(launch_check_codes((const uint8_t*)p->codes.p, L, p->sigma, (int*)p->flags.p, s));
             int fl = 0;
             CK(cudaMemcpyAsync(&fl, p->flags.p, sizeof(int), cudaMemcpyDeviceToHost, s));
             CK(cudaStreamSynchronize(s));
@@ -351,7 +362,7 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
     CK(cudaMemcpyAsync(p->gofs.p, p->h_gofs.data(), (N + 1) * sizeof(int64_t),
                        cudaMemcpyHostToDevice, s));
     CK(p->ensure(p->gmseq, n * sizeof(uint32_t), s));
-    CK(launch_gmer_index((const int64_t*)p->gofs.p, N, (uint32_t*)p->gmseq.p, s));
+    LK(launch_gmer_index((const int64_t*)p->gofs.p, N, (uint32_t*)p->gmseq.p, s));
 
     // this shard's masks, in processing order
     std::vector<int> mine;
@@ -364,10 +375,25 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
     CK(cudaMemcpyAsync(p->kept.p, kept_h.data(), kept_h.size(), cudaMemcpyHostToDevice, s));
     CK(cudaStreamSynchronize(s));  // kept_h / h_* are pageable host staging
 
-    // batch size
+    // heavy / light threshold: a group of s sequences costs ~s^2/2 scattered
+    // updates on the light path and ~N_pad^2/2 u8 MACs on the Gram; with the
+    // measured rates (~1.1e11 updates/s, ~1.5e15 MAC/s) they break even near
+    // s = 0.0085 N_pad.
+    const int64_t n_pad = (N + 255) / 256 * 256;
+    int64_t heavy_min = p->heavy_min;
+    if (heavy_min == 0) heavy_min = std::max<int64_t>(16, (int64_t)(0.0085 * (double)n_pad + 0.999));
+    const bool heavy_on = heavy_min < (int64_t)1 << 40 && N >= 2;
+
+    // batch size (keys cap; with the Gram on, s32 exactness: masks * n_max^2 < 2^31)
     uint64_t bk = p->batch_keys > 0 ? (uint64_t)p->batch_keys : (1ull << 26);
     if (bk > (1ull << 30) - 1) bk = (1ull << 30) - 1;
-    const uint64_t bmax_masks = std::max<uint64_t>(1, n ? bk / n : mine.size());
+    uint64_t bmax_masks = std::max<uint64_t>(1, n ? bk / n : mine.size());
+    if (heavy_on && nmax > 0) {
+        uint64_t lim = (uint64_t)(INT32_MAX / ((uint64_t)nmax * (uint64_t)nmax));
+        bmax_masks = std::max<uint64_t>(1, std::min(bmax_masks, lim));
+    }
+    // a single mask whose n_max^2 exceeds 2^31 would need the light path only
+    const bool gram_ok = heavy_on && (uint64_t)nmax * (uint64_t)nmax <= (uint64_t)INT32_MAX;
     const uint64_t cap_keys = std::max<uint64_t>(1, std::min<uint64_t>(bmax_masks, mine.size()) * n);
     CK(p->ensure(p->keysA, cap_keys * 8, s));
     CK(p->ensure(p->keysB, cap_keys * 8, s));
@@ -391,12 +417,29 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
     CK(cudaMemsetAsync(p->stats.p, 0, ST_COUNT * 8, s));
     unsigned long long* stats = (unsigned long long*)p->stats.p;
 
-    const int64_t heavy_min = p->heavy_min > 0 ? p->heavy_min : INT64_MAX;  // no Gram yet
+    const int64_t light_limit = gram_ok ? heavy_min : INT64_MAX;
+    uint64_t rcap = 0;
+    if (gram_ok) {
+        CK(p->ensure(p->heavy, (cap_keys / 2 + 1) * 4, s));
+        CK(p->ensure(p->hcount, 16, s));
+        // dense chunk: n_pad rows x rcap u8 columns, at most ~256 MB
+        rcap = std::max<uint64_t>(128, ((256ull << 20) / (uint64_t)n_pad) / 128 * 128);
+        CK(p->ensure(p->dense, (size_t)n_pad * rcap, s));
+        if (p->tiles_npad != n_pad) {
+            std::vector<int2> t = gram_tiles(n_pad);
+            CK(p->ensure(p->tiles, t.size() * sizeof(int2), s));
+            CK(cudaMemcpyAsync(p->tiles.p, t.data(), t.size() * sizeof(int2),
+                               cudaMemcpyHostToDevice, s));
+            CK(cudaStreamSynchronize(s));
+            p->ntiles = (int)t.size();
+            p->tiles_npad = n_pad;
+        }
+    }
     CorpusView cv{(const uint8_t*)p->codes.p, (const int64_t*)p->off.p, (const int64_t*)p->gofs.p,
                   (const uint32_t*)p->gmseq.p, N, n};
     SegmentOut so{(uint32_t*)p->tseq.p, (uint32_t*)p->tcnt.p, (uint32_t*)p->gstart.p,
                   (uint32_t*)p->gend.p, (uint32_t*)p->counts.p};
-    int64_t passkeys = 0;
+    int64_t passkeys = 0, heavy_macs = 0;
     const size_t nn = (size_t)N * N;
 
     size_t pos = 0;
@@ -413,7 +456,7 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
         if (n > 0) {
             p->stage_begin(s, &a);
             CK(cudaMemsetAsync(p->hist.p, 0, (size_t)nmask * MAXPASS * RADIX * 4, s));
-            CK(launch_encode(cv, (const uint8_t*)p->kept.p + pos * GMAX, g - m, p->sigma, sb,
+            LK(launch_encode(cv, (const uint8_t*)p->kept.p + pos * GMAX, g - m, p->sigma, sb,
                              nmask, npass, (uint64_t*)p->keysA.p, (uint32_t*)p->hist.p, s));
             p->stage_end(s, S_ENCODE, a);
 
@@ -423,7 +466,7 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
             for (int q = 0; q < npass; ++q) {
                 uint32_t* c;
                 CK(p->next_ctr(s, &c));
-                CK(launch_onesweep(in, outk, n, nmask, sb + RADIX_BITS * q, (const uint32_t*)p->hist.p,
+                LK(launch_onesweep(in, outk, n, nmask, sb + RADIX_BITS * q, (const uint32_t*)p->hist.p,
                                    q, npass, (uint64_t*)p->status.p, c, p->epoch++, s));
                 std::swap(in, outk);
             }
@@ -433,18 +476,37 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
             p->stage_begin(s, &a);
             uint32_t* c1;
             CK(p->next_ctr(s, &c1));
-            CK(launch_triples(in, n, nmask, sb, N, Cm, (uint64_t*)p->status.p, c1, p->epoch++, so,
+            LK(launch_triples(in, n, nmask, sb, N, Cm, (uint64_t*)p->status.p, c1, p->epoch++, so,
                               stats, s));
             uint32_t* c2;
             CK(p->next_ctr(s, &c2));
-            CK(launch_groups(n * nmask, (uint64_t*)p->status.p, c2, p->epoch++, so, stats, s));
+            LK(launch_groups(n * nmask, (uint64_t*)p->status.p, c2, p->epoch++, so, stats, s));
             p->stage_end(s, S_SEGMENT, a);
 
             p->stage_begin(s, &a);
-            CK(launch_light(so, n * nmask / 2 + 1, heavy_min, N, Cm, stats, p->sm_count, s));
+            LK(launch_light(so, n * nmask / 2 + 1, light_limit, N, Cm, (uint32_t*)p->heavy.p,
+                            (uint32_t*)p->hcount.p, stats, p->sm_count, s));
             p->stage_end(s, S_LIGHT, a);
+
+            if (gram_ok) {
+                uint32_t R = 0;
+                CK(cudaMemcpyAsync(&R, p->hcount.p, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
+                CK(cudaStreamSynchronize(s));
+                p->stage_begin(s, &a);
+                for (uint64_t r0 = 0; r0 < R; r0 += rcap) {
+                    const uint32_t rc = (uint32_t)std::min<uint64_t>(rcap, R - r0);
+                    const uint32_t ldd = (rc + 127) / 128 * 128;
+                    CK(cudaMemsetAsync(p->dense.p, 0, (size_t)n_pad * ldd, s));
+                    LK(launch_build_dense(so, (const uint32_t*)p->heavy.p, (uint32_t)r0, rc, ldd,
+                                          (uint8_t*)p->dense.p, p->sm_count, s));
+                    LK(launch_gram((const uint8_t*)p->dense.p, n_pad, ldd, ldd, Cm, N,
+                                   (const int2*)p->tiles.p, p->ntiles, p->sm_count, s));
+                    heavy_macs += (int64_t)p->ntiles * 128 * 256 * (int64_t)ldd;
+                }
+                p->stage_end(s, S_HEAVY, a);
+            }
         }
-        CK(launch_diag_closed_form((const int64_t*)p->gofs.p, N, nmask, Cm, s));
+        LK(launch_diag_closed_form((const int64_t*)p->gofs.p, N, nmask, Cm, s));
         pos = end;
     }
     p->last_masks = (int64_t)mine.size();
@@ -452,8 +514,11 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
     p->host_stats.masks = (int64_t)mine.size();
     p->host_stats.keys = (int64_t)mine.size() * (int64_t)n;
     p->host_stats.sort_passes = passkeys;
+    p->host_stats.heavy_macs = heavy_macs;
+    p->after_accumulate = true;
     return GAKCO_OK;
 #undef CK
+#undef LK
 }
 
 extern "C" gakco_status gakco_accumulate(gakco_plan* p, const uint8_t* codes,
@@ -471,12 +536,21 @@ static gakco_status finalize_impl(gakco_plan* p, int64_t* C, int64_t N, int64_t*
         cudaError_t e_ = (x);                          \
         if (e_ != cudaSuccess) return p->cuda_fail(e_, #x); \
     } while (0)
+#define LK(x)        \
+    do {             \
+        ++p->launches; \
+        CK(x);       \
+    } while (0)
     if (!C || N < 1) return p->fail(GAKCO_E_ARG, "C is NULL or N < 1");
     if (!is_device_ptr(C)) return p->fail(GAKCO_E_ARG, "C must be a device pointer");
-    if (!keep_events) {
+    // A finalize that directly follows an accumulate on this plan appends to its
+    // stage events and launch count (so one stats read covers the whole step).
+    if (!keep_events && !p->after_accumulate) {
         p->evs.clear();
         p->ev_used = 0;
+        p->launches = 0;
     }
+    p->after_accumulate = false;
     p->last_stream = s;
     const size_t nn = (size_t)N * N;
     const int M = p->M;
@@ -502,7 +576,7 @@ static gakco_status finalize_impl(gakco_plan* p, int64_t* C, int64_t N, int64_t*
     CK(cudaMemsetAsync(p->flags.p, 0, sizeof(int), s));
     cudaEvent_t a = nullptr;
     p->stage_begin(s, &a);
-    CK(launch_epilogue(C, N, p->g, p->k, M, dNm, dK, dKn, (int64_t*)p->kdiag.p, (int*)p->flags.p,
+    LK(launch_epilogue(C, N, p->g, p->k, M, dNm, dK, dKn, (int64_t*)p->kdiag.p, (int*)p->flags.p,
                        s));
     p->stage_end(s, S_EPILOGUE, a);
     if (hNm) CK(cudaMemcpyAsync(Nm, dNm, (M + 1) * nn * 8, cudaMemcpyDeviceToHost, s));
@@ -515,6 +589,7 @@ static gakco_status finalize_impl(gakco_plan* p, int64_t* C, int64_t N, int64_t*
     if (fl & EF_K_MISMATCH) return p->fail(GAKCO_E_INTERNAL, "K != C_{g-k}");
     return GAKCO_OK;
 #undef CK
+#undef LK
 }
 
 extern "C" gakco_status gakco_finalize(gakco_plan* p, int64_t* C, int64_t N, int64_t* Nm,
@@ -557,6 +632,7 @@ extern "C" gakco_status gakco_get_stats(gakco_plan* p, gakco_stats* out) {
     if (!p || !out) return GAKCO_E_ARG;
     DeviceGuard dg(p->device);
     gakco_stats r = p->host_stats;
+    r.launches = p->launches;
     if (p->stats.p) {
         unsigned long long d[ST_COUNT];
         cudaError_t e = cudaMemcpyAsync(d, p->stats.p, sizeof d, cudaMemcpyDeviceToHost,
@@ -567,7 +643,6 @@ extern "C" gakco_status gakco_get_stats(gakco_plan* p, gakco_stats* out) {
         r.groups_multi = (int64_t)d[ST_GROUPS];
         r.light_pairs = (int64_t)d[ST_LIGHT_PAIRS];
         r.heavy_groups = (int64_t)d[ST_HEAVY_GROUPS];
-        r.heavy_macs = (int64_t)d[ST_HEAVY_MACS];
     }
     double* ms[S_NSTAGE] = {&r.ms_encode, &r.ms_sort, &r.ms_segment,
                             &r.ms_light,  &r.ms_heavy, &r.ms_epilogue};

@@ -39,7 +39,7 @@ EXPORTS = ("gakco_create", "gakco_set_shard", "gakco_set_option", "gakco_accumul
 class gakco_stats(ctypes.Structure):
     _fields_ = [(n, ctypes.c_int64) for n in (
         "masks", "keys", "sort_passes", "triples", "groups_multi", "light_pairs",
-        "heavy_groups", "heavy_macs")] + [(n, ctypes.c_double) for n in (
+        "heavy_groups", "heavy_macs", "launches")] + [(n, ctypes.c_double) for n in (
             "ms_encode", "ms_sort", "ms_segment", "ms_light", "ms_heavy", "ms_epilogue")]
 
     def as_dict(self):

@@ -89,6 +89,27 @@ def test_several_tiles_ragged(gk, oracle_lib):
         assert_parity(run(gk, cp, g, k, M), oracle_lib.compute(cp, g, k, M))
 
 
+def test_heavy_light_equivalence(gk, oracle_lib):
+    """Forced all-heavy (tensor-core Gram for every multi-sequence group) ==
+    forced all-light == default == oracle (SURVEY §8c GPU-internal pins)."""
+    rng = np.random.default_rng(103)
+    cases = [(sc.make("tiny"), 7, 5, 2)]
+    for _ in range(12):
+        sigma = int(rng.choice([2, 4, 20]))
+        g = int(rng.integers(2, 10))
+        k = int(rng.integers(1, g + 1))
+        cases.append((sc.random_small(rng, sigma, n_max=300, l_max=90), g, k, g - k))
+    # more than 256 rows and columns of tiles, counts up to 255+ (light fallback)
+    cases.append((sc.from_sequences(2, [[0] * 300] + [list(rng.integers(0, 2, 60))
+                                                     for _ in range(520)]), 6, 3, 3))
+    for cp, g, k, M in cases:
+        ref = oracle_lib.compute(cp, g, k, M)
+        heavy = run(gk, cp, g, k, M, heavy_min_seqs=2)
+        assert_parity(heavy, ref)
+        assert_parity(run(gk, cp, g, k, M, heavy_min_seqs=1 << 50), ref)
+        assert_parity(run(gk, cp, g, k, M), ref)
+
+
 def test_batch_size_invariance(gk, oracle_lib):
     """Different mask batch sizes give identical results (integer sums)."""
     cp = sc.make("tiny")
