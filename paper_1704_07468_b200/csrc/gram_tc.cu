@@ -18,6 +18,7 @@
 //   warp 5      MMA issuer (one elected lane), 2 TMEM accumulators of 256 cols
 //   warps 0-3   epilogue: tcgen05.ld 32x32b -> +C (int64), lane = output row
 #include <cuda.h>
+#include <string.h>
 
 #include "internal.cuh"
 
@@ -31,7 +32,10 @@ constexpr int GT_A_BYTES = GT_M * GT_KB;          // 16 KB
 constexpr int GT_B_BYTES = GT_N * GT_KB;          // 32 KB
 constexpr int GT_STAGE_BYTES = GT_A_BYTES + GT_B_BYTES;
 constexpr int GT_THREADS = 192;
-constexpr size_t GT_SMEM = (size_t)GT_STAGES * GT_STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+constexpr int GT_EC = 16;                          // epilogue columns per TMA reduce
+constexpr int GT_EBUF = GT_M * GT_EC * 8;          // 16 KB staging (u64)
+constexpr size_t GT_SMEM =
+    (size_t)GT_STAGES * GT_STAGE_BYTES + 2 * GT_EBUF + 1024 /*align*/ + 256 /*barriers*/;
 
 // ---------------------------------------------------------------- PTX helpers
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -104,6 +108,32 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
     asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
 
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
+    asm volatile(
+        "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,"
+        "%14,%15}, [%16];"
+        : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+          "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]),
+          "=r"(v[13]), "=r"(v[14]), "=r"(v[15])
+        : "r"(taddr));
+    asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+// Element-wise u64 add of a shared-memory box into global memory (TMA reduce).
+__device__ __forceinline__ void tma_reduce_add_2d(const CUtensorMap* map, const void* src, int x,
+                                                  int y) {
+    asm volatile(
+        "cp.reduce.async.bulk.tensor.2d.global.shared::cta.add.tile.bulk_group"
+        " [%0, {%2, %3}], [%1];" ::"l"((uint64_t)map),
+        "r"(smem_u32(src)), "r"(x), "r"(y)
+        : "memory");
+}
+template <int N>
+__device__ __forceinline__ void bulk_wait_read() {
+    asm volatile("cp.async.bulk.wait_group.read %0;" ::"n"(N) : "memory");
+}
+// named barrier 1 over the 128 epilogue threads
+__device__ __forceinline__ void epi_bar() { asm volatile("bar.sync 1, 128;" ::: "memory"); }
+
 // Shared-memory matrix descriptor, K-major, 128B swizzle: 8-row x 128 B atoms,
 // SBO = 1024 B between 8-row groups, LBO unused (1), version 1 (sm_100).
 __device__ __forceinline__ uint64_t sw128_desc(uint32_t saddr) {
@@ -127,13 +157,16 @@ struct GramArgs {
     int kblocks;        // K / 128
     const int2* tiles;  // (row block of 128, col block of 256)
     int ntiles;
+    int tma_epilogue;   // 1: TMA reduce-add into C (rows 16-byte aligned)
 };
 
 __global__ void __launch_bounds__(GT_THREADS, 1)
-    gram_kernel(const __grid_constant__ CUtensorMap dmap, GramArgs a) {
+    gram_kernel(const __grid_constant__ CUtensorMap dmap, const __grid_constant__ CUtensorMap cmap,
+                GramArgs a) {
     extern __shared__ __align__(1024) unsigned char smem_raw[];
     unsigned char* smem = (unsigned char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
-    uint64_t* bars = (uint64_t*)(smem + (size_t)GT_STAGES * GT_STAGE_BYTES);
+    unsigned char* ebuf = smem + (size_t)GT_STAGES * GT_STAGE_BYTES;  // 2 x GT_EBUF
+    uint64_t* bars = (uint64_t*)(ebuf + 2 * GT_EBUF);
     uint64_t* full = bars;                      // [STAGES]
     uint64_t* empty = bars + GT_STAGES;         // [STAGES]
     uint64_t* tfull = bars + 2 * GT_STAGES;     // [2]
@@ -217,31 +250,59 @@ __global__ void __launch_bounds__(GT_THREADS, 1)
         }
     } else {
         // ------------------------------------------------ epilogue (warps 0-3)
-        int it = 0;
+        // TMEM -> registers -> (s32 -> 64-bit, Y > X mask) -> smem [128][16] -> TMA
+        // bulk reduce-add into C_m (coalesced, asynchronous, exact u64 adds).
+        int it = 0, buf = 0;
+        const int row = warp * 32 + lane;
         for (int t = blockIdx.x; t < a.ntiles; t += gridDim.x, ++it) {
             const int acc = it & 1;
             const uint32_t acc_phase = (it >> 1) & 1;
             const int2 tl = a.tiles[t];
             mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
-            const int64_t x = (int64_t)tl.x * GT_M + warp * 32 + lane;
+            const int64_t x = (int64_t)tl.x * GT_M + row;
             const int64_t y0 = (int64_t)tl.y * GT_N;
 #pragma unroll 1
-            for (int c = 0; c < GT_N; c += 32) {
-                uint32_t v[32];
-                tmem_ld32(tmem + ((uint32_t)(warp * 32) << 16) + acc * GT_N + c, v);
-                if (x < a.N) {
-                    int64_t* row = a.Cm + x * a.N;
+            for (int c = 0; c < GT_N; c += GT_EC) {
+                uint32_t v[GT_EC];
+                tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + acc * GT_N + c, v);
+                // the buffer we are about to fill was handed to TMA two chunks ago
+                if (threadIdx.x == 0) bulk_wait_read<1>();
+                epi_bar();
+                unsigned char* sb = ebuf + buf * GT_EBUF;
 #pragma unroll
-                    for (int j = 0; j < 32; ++j) {
-                        const int64_t y = y0 + c + j;
-                        if (y > x && y < a.N && v[j]) row[y] += (int64_t)(int32_t)v[j];
+                for (int j2 = 0; j2 < GT_EC / 2; ++j2) {
+                    const int ch = (j2 + lane) & (GT_EC / 2 - 1);
+                    const int64_t y = y0 + c + 2 * ch;
+                    uint64_t lo = (y > x) ? (uint64_t)v[2 * ch] : 0ull;
+                    uint64_t hi = (y + 1 > x) ? (uint64_t)v[2 * ch + 1] : 0ull;
+                    *(ulonglong2*)(sb + row * (GT_EC * 8) + ch * 16) = make_ulonglong2(lo, hi);
+                }
+                if (a.tma_epilogue) {
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                    epi_bar();
+                    if (threadIdx.x == 0) {
+                        tma_reduce_add_2d(&cmap, sb, (int)(y0 + c), (int)(tl.x * GT_M));
+                        asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+                    }
+                } else {
+                    // rows of C not 16-byte aligned (odd N): coalesced LSU adds
+                    epi_bar();
+                    const uint64_t* s64 = (const uint64_t*)sb;
+#pragma unroll 4
+                    for (int e = threadIdx.x; e < GT_M * GT_EC; e += 128) {
+                        const int64_t xx = (int64_t)tl.x * GT_M + e / GT_EC;
+                        const int64_t yy = y0 + c + e % GT_EC;
+                        const uint64_t val = s64[e];
+                        if (val && xx < a.N && yy < a.N) a.Cm[xx * a.N + yy] += (int64_t)val;
                     }
                 }
+                buf ^= 1;
             }
             tc_fence_before();
             mbar_arrive(&tempty[acc]);
         }
+        if (threadIdx.x == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
     }
     __syncthreads();
     if (warp == 0) {
@@ -323,10 +384,23 @@ cudaError_t launch_gram(const uint8_t* D, int64_t n_pad, uint32_t ldd, uint32_t 
                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
+    // C_m as u64 for the TMA reduce-add (two's-complement add == int64 add)
+    CUtensorMap cmap;
+    memset(&cmap, 0, sizeof cmap);
+    const bool tma_epi = (N % 2 == 0) && (((uintptr_t)Cm & 15) == 0);
+    cuuint64_t cdims[2] = {(cuuint64_t)N, (cuuint64_t)N};
+    cuuint64_t cstr[1] = {(cuuint64_t)N * 8};
+    cuuint32_t cbox[2] = {GT_EC, GT_M};
+    if (tma_epi) {
+        r = enc(&cmap, CU_TENSOR_MAP_DATA_TYPE_UINT64, 2, (void*)Cm, cdims, cstr, cbox, estr,
+                CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
+    }
     cudaFuncSetAttribute(gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GT_SMEM);
-    GramArgs a{Cm, N, (int)(kcols / GT_KB), tiles, ntiles};
+    GramArgs a{Cm, N, (int)(kcols / GT_KB), tiles, ntiles, tma_epi ? 1 : 0};
     int grid = ntiles < sm_count ? ntiles : sm_count;
-    gram_kernel<<<grid, GT_THREADS, GT_SMEM, s>>>(map, a);
+    gram_kernel<<<grid, GT_THREADS, GT_SMEM, s>>>(map, cmap, a);
     return cudaGetLastError();
 }
 

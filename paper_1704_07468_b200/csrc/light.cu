@@ -52,7 +52,8 @@ __global__ void __launch_bounds__(256) light_kernel(SegmentOut so, int64_t heavy
 cudaError_t launch_light(SegmentOut so, uint64_t max_groups, int64_t heavy_min, int64_t N,
                          int64_t* Cm, uint32_t* heavy, uint32_t* heavy_count,
                          unsigned long long* stats, int sm_count, cudaStream_t s) {
-    cudaError_t e = cudaMemsetAsync(heavy_count, 0, sizeof(uint32_t), s);
+    cudaError_t e = heavy_count ? cudaMemsetAsync(heavy_count, 0, sizeof(uint32_t), s)
+                                : cudaSuccess;
     if (e != cudaSuccess || max_groups == 0) return e;
     uint64_t blocks = (max_groups + 7) / 8;
     uint64_t cap = (uint64_t)sm_count * 8;

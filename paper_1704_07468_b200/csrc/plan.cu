@@ -422,8 +422,8 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
     if (gram_ok) {
         CK(p->ensure(p->heavy, (cap_keys / 2 + 1) * 4, s));
         CK(p->ensure(p->hcount, 16, s));
-        // dense chunk: n_pad rows x rcap u8 columns, at most ~256 MB
-        rcap = std::max<uint64_t>(128, ((256ull << 20) / (uint64_t)n_pad) / 128 * 128);
+        // dense chunk: n_pad rows x rcap u8 columns, at most ~1 GB
+        rcap = std::max<uint64_t>(128, ((1024ull << 20) / (uint64_t)n_pad) / 128 * 128);
         CK(p->ensure(p->dense, (size_t)n_pad * rcap, s));
         if (p->tiles_npad != n_pad) {
             std::vector<int2> t = gram_tiles(n_pad);

@@ -25,8 +25,8 @@ constexpr size_t ONESWEEP_SMEM = SORT_TILE * 8 + RADIX * 8 + (SORT_THREADS / 32)
 
 __global__ void __launch_bounds__(SORT_THREADS) onesweep_kernel(
     const uint64_t* __restrict__ in, uint64_t* __restrict__ out, uint64_t n, uint32_t tps,
-    int shift, const uint32_t* __restrict__ hist, int pass, int npass, uint64_t* status,
-    uint32_t* ctr, uint32_t epoch) {
+    uint32_t nseg, int shift, const uint32_t* __restrict__ hist, int pass, int npass,
+    uint64_t* status, uint32_t* ctr, uint32_t epoch) {
     constexpr int WARPS = SORT_THREADS / 32;
     extern __shared__ __align__(16) unsigned char smem[];
     uint64_t* s_keys = (uint64_t*)smem;                                   // [SORT_TILE]
@@ -40,8 +40,10 @@ __global__ void __launch_bounds__(SORT_THREADS) onesweep_kernel(
     if (tid == 0) s_tile = atomicAdd(ctr, 1u);
     for (int i = tid; i < WARPS * RADIX; i += SORT_THREADS) (&s_whist[0][0])[i] = 0;
     __syncthreads();
+    // tickets interleave the segments (ticket t -> tile t / nseg of segment
+    // t % nseg) so the tiles in flight spread over many look-back chains
     const uint32_t t = s_tile;
-    const uint32_t seg = t / tps, ts = t - seg * tps;
+    const uint32_t ts = t / nseg, seg = t - ts * nseg;
     const uint64_t seg_base = (uint64_t)seg * n;
     const uint64_t tile_base = seg_base + (uint64_t)ts * SORT_TILE;
     const uint64_t rem = n - (uint64_t)ts * SORT_TILE;
@@ -93,15 +95,36 @@ __global__ void __launch_bounds__(SORT_THREADS) onesweep_kernel(
         s_doff[tid] = doff;
         uint32_t excl = 0;
         if (ts > 0) {
+            // windowed look-back: the statuses of one (segment, digit) are contiguous
+            // over tiles, so LB_WIN predecessors are read with independent loads per
+            // round trip; consume them nearest-first until an inclusive prefix.
+            constexpr int LB_WIN = 8;
             const uint64_t* col = status + ((uint64_t)seg * RADIX + tid) * tps;
             int64_t p = (int64_t)ts - 1;
-            while (true) {
-                uint64_t v = *(volatile const uint64_t*)(col + p);
-                uint32_t ep = (uint32_t)(v >> 32), fl = (uint32_t)(v >> 30) & 3u;
-                if (ep != epoch || fl == LB_NONE) continue;
-                excl += (uint32_t)(v & 0x3fffffffu);
-                if (fl == LB_INC) break;
-                --p;
+            bool done = false;
+            while (!done) {
+                uint64_t v[LB_WIN];
+#pragma unroll
+                for (int j = 0; j < LB_WIN; ++j)
+                    v[j] = (p - j >= 0) ? *(volatile const uint64_t*)(col + p - j) : 0ull;
+                int used = 0;
+                bool stop = false;
+#pragma unroll
+                for (int j = 0; j < LB_WIN; ++j) {
+                    if (stop) continue;
+                    const uint32_t ep = (uint32_t)(v[j] >> 32), fl = (uint32_t)(v[j] >> 30) & 3u;
+                    if (p - j < 0 || ep != epoch || fl == LB_NONE) {
+                        stop = true;  // not published yet: re-read from here
+                        continue;
+                    }
+                    excl += (uint32_t)(v[j] & 0x3fffffffu);
+                    ++used;
+                    if (fl == LB_INC) {
+                        done = true;
+                        stop = true;
+                    }
+                }
+                p -= used;
             }
             *(volatile uint64_t*)(status + ((uint64_t)seg * RADIX + tid) * tps + ts) =
                 lb_pack(epoch, LB_INC, excl + tile_cnt);
@@ -135,7 +158,8 @@ cudaError_t launch_onesweep(const uint64_t* in, uint64_t* out, uint64_t n, int n
     uint64_t tiles = (uint64_t)tps * nseg;
     cudaFuncSetAttribute(onesweep_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)ONESWEEP_SMEM);
-    onesweep_kernel<<<(unsigned)tiles, SORT_THREADS, ONESWEEP_SMEM, s>>>(in, out, n, tps, shift, hist, pass,
+    onesweep_kernel<<<(unsigned)tiles, SORT_THREADS, ONESWEEP_SMEM, s>>>(in, out, n, tps,
+                                                             (uint32_t)nseg, shift, hist, pass,
                                                              npass, status, ctr, epoch);
     return cudaGetLastError();
 }
