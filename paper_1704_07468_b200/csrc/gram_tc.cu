@@ -154,7 +154,8 @@ constexpr uint32_t GT_IDESC = (2u << 4)               // D format s32
 struct GramArgs {
     int64_t* Cm;        // [N][N] int64, upper entries Y > X updated
     int64_t N;
-    int kblocks;        // K / 128
+    const uint32_t* fill;  // filled columns of D (K = fill rounded up to 128)
+    uint32_t cap;          // columns of D (fill may overshoot; see light.cu)
     const int2* tiles;  // (row block of 128, col block of 256)
     int ntiles;
     int tma_epilogue;   // 1: TMA reduce-add into C (rows 16-byte aligned)
@@ -174,6 +175,8 @@ __global__ void __launch_bounds__(GT_THREADS, 1)
     uint32_t* tmem_slot = (uint32_t*)(bars + 2 * GT_STAGES + 4);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int kblocks = (int)((min(*a.fill, a.cap) + GT_KB - 1) / GT_KB);  // grid-uniform
+    if (kblocks == 0) return;
     if (threadIdx.x == 0) {
         for (int s = 0; s < GT_STAGES; ++s) {
             mbar_init(&full[s], 1);
@@ -203,7 +206,7 @@ __global__ void __launch_bounds__(GT_THREADS, 1)
             uint32_t stage = 0, phase = 0;
             for (int t = blockIdx.x; t < a.ntiles; t += gridDim.x) {
                 const int2 tl = a.tiles[t];
-                for (int kb = 0; kb < a.kblocks; ++kb) {
+                for (int kb = 0; kb < kblocks; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
                     unsigned char* sa = smem + (size_t)stage * GT_STAGE_BYTES;
                     unsigned char* sbm = sa + GT_A_BYTES;
@@ -230,7 +233,7 @@ __global__ void __launch_bounds__(GT_THREADS, 1)
                 mbar_wait(&tempty[acc], acc_phase ^ 1);
                 tc_fence_after();
                 const uint32_t dcol = tmem + acc * GT_N;
-                for (int kb = 0; kb < a.kblocks; ++kb) {
+                for (int kb = 0; kb < kblocks; ++kb) {
                     mbar_wait(&full[stage], phase);
                     tc_fence_after();
                     const uint32_t sa = smem_u32(smem + (size_t)stage * GT_STAGE_BYTES);
@@ -312,22 +315,26 @@ __global__ void __launch_bounds__(GT_THREADS, 1)
     }
 }
 
-// ---------------------------------------------------------------- D builder
-// D[x][r] = count of sequence x in heavy group r (buffer zeroed beforehand).
-__global__ void build_dense_kernel(SegmentOut so, const uint32_t* __restrict__ heavy,
-                                   uint32_t r0, uint32_t R, uint32_t ldd,
-                                   uint8_t* __restrict__ D) {
-    const int lane = threadIdx.x & 31;
-    const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
-    const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-    for (uint64_t r = warp; r < R; r += nwarps) {
-        const uint32_t gi = heavy[r0 + r];
-        const uint32_t a = so.gstart[gi], b = so.gend[gi];
-        for (uint32_t t = a + lane; t < b; t += 32) {
-            const uint32_t x = so.tseq[t] & 0x7fffffffu;
-            D[(uint64_t)x * ldd + r] = (uint8_t)so.tcnt[t];
-        }
+// ---------------------------------------------------------------- D reset
+// Zero the used columns [0, round_up(fill,128)) of every row, then reset fill:
+// D is all-zero again for the next accumulation.
+__global__ void dense_reset_kernel(uint8_t* __restrict__ D, int64_t n_pad, uint64_t ldd,
+                                   const uint32_t* fill) {
+    const uint64_t used = (min((uint64_t)*fill, ldd) + GT_KB - 1) / GT_KB * GT_KB;
+    const uint64_t per_row = used / 16;  // 16-byte stores
+    const uint64_t total = per_row * (uint64_t)n_pad;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t r = i / per_row, c = i - r * per_row;
+        *(uint4*)(D + r * ldd + c * 16) = make_uint4(0, 0, 0, 0);
     }
+}
+
+__global__ void fill_reset_kernel(uint32_t* fill, uint64_t ldd, uint64_t tile_macs,
+                                  unsigned long long* stats) {
+    const uint64_t k = (min((uint64_t)*fill, ldd) + GT_KB - 1) / GT_KB * GT_KB;
+    atomicAdd(&stats[ST_HEAVY_MACS], (unsigned long long)(tile_macs * k));
+    *fill = 0;
 }
 
 // ---------------------------------------------------------------- host side
@@ -349,8 +356,6 @@ static EncodeTiledFn get_encode() {
     return fn;
 }
 
-size_t gram_smem_bytes() { return GT_SMEM; }
-
 // Upper tiles (row block of 128 x col block of 256) that hold any Y > X entry.
 std::vector<int2> gram_tiles(int64_t n_pad) {
     std::vector<int2> t;
@@ -361,18 +366,9 @@ std::vector<int2> gram_tiles(int64_t n_pad) {
     return t;
 }
 
-cudaError_t launch_build_dense(SegmentOut so, const uint32_t* heavy, uint32_t r0, uint32_t R,
-                               uint32_t ldd, uint8_t* D, int sm_count, cudaStream_t s) {
-    if (R == 0) return cudaGetLastError();
-    uint64_t blocks = (R + 7) / 8;
-    if (blocks > (uint64_t)sm_count * 16) blocks = (uint64_t)sm_count * 16;
-    build_dense_kernel<<<(unsigned)blocks, 256, 0, s>>>(so, heavy, r0, R, ldd, D);
-    return cudaGetLastError();
-}
-
-cudaError_t launch_gram(const uint8_t* D, int64_t n_pad, uint32_t ldd, uint32_t kcols,
-                        int64_t* Cm, int64_t N, const int2* tiles, int ntiles, int sm_count,
-                        cudaStream_t s) {
+cudaError_t launch_gram_flush(uint8_t* D, int64_t n_pad, uint64_t ldd, uint32_t* dense_fill,
+                              int64_t* Cm, int64_t N, const int2* tiles, int ntiles,
+                              int sm_count, unsigned long long* stats, cudaStream_t s) {
     EncodeTiledFn enc = get_encode();
     if (!enc) return cudaErrorNotSupported;
     CUtensorMap map;
@@ -398,9 +394,15 @@ cudaError_t launch_gram(const uint8_t* D, int64_t n_pad, uint32_t ldd, uint32_t 
         if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
     }
     cudaFuncSetAttribute(gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GT_SMEM);
-    GramArgs a{Cm, N, (int)(kcols / GT_KB), tiles, ntiles, tma_epi ? 1 : 0};
+    GramArgs a{Cm, N, dense_fill, (uint32_t)ldd, tiles, ntiles, tma_epi ? 1 : 0};
     int grid = ntiles < sm_count ? ntiles : sm_count;
     gram_kernel<<<grid, GT_THREADS, GT_SMEM, s>>>(map, cmap, a);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    dense_reset_kernel<<<sm_count * 4, 256, 0, s>>>(D, n_pad, ldd, dense_fill);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    fill_reset_kernel<<<1, 1, 0, s>>>(dense_fill, ldd, (uint64_t)ntiles * GT_M * GT_N, stats);
     return cudaGetLastError();
 }
 

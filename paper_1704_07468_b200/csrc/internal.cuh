@@ -105,8 +105,7 @@ struct CorpusView {
 struct SegmentOut {
     uint32_t* tseq;          // [T] seq id | (group-head << 31)
     uint32_t* tcnt;          // [T] run length (count of the (key, seq) pair)
-    uint32_t* gstart;        // [G] first triple of each multi-sequence group
-    uint32_t* gend;          // [G] one past the last triple
+    uint32_t* gstart;        // [G+1] first triple of each multi-sequence group; [G] = T
     uint32_t* counts;        // [0] = T, [1] = G
 };
 
@@ -119,24 +118,25 @@ cudaError_t launch_encode(const CorpusView& cv, const uint8_t* kept, int nkept, 
 cudaError_t launch_onesweep(const uint64_t* in, uint64_t* out, uint64_t n, int nseg, int shift,
                             const uint32_t* hist, int pass, int npass, uint64_t* status,
                             uint32_t* ctr, uint32_t epoch, cudaStream_t s);
-cudaError_t launch_triples(const uint64_t* keys, uint64_t n, int nseg, int sb, int64_t N,
-                           int64_t* Cm, uint64_t* status, uint32_t* ctr, uint32_t epoch,
-                           SegmentOut so, unsigned long long* stats, cudaStream_t s);
-cudaError_t launch_groups(uint64_t max_triples, uint64_t* status, uint32_t* ctr, uint32_t epoch,
-                          SegmentOut so, unsigned long long* stats, cudaStream_t s);
-// Light pair updates; groups with >= heavy_min sequences (and counts <= 255) are
-// appended to heavy[] (count in *heavy_count) for the tensor-core Gram instead.
+// Chunked LSD pass (radix_hist + radix_scatter); hist: >= (target_ctas + nseg) * 256 u32.
+cudaError_t launch_radix_chunked(const uint64_t* in, uint64_t* out, uint64_t n, int nseg,
+                                 int shift, uint32_t* hist, int target_ctas, cudaStream_t s);
+cudaError_t launch_segment(const uint64_t* keys, uint64_t n, int nseg, int sb, int64_t N,
+                           int64_t* Cm, uint64_t* status_t, uint64_t* status_g, uint32_t* ctr,
+                           uint32_t epoch, SegmentOut so, unsigned long long* stats,
+                           cudaStream_t s);
+// Light pair updates; a group with >= heavy_min sequences (and counts <= 255)
+// instead claims column atomicAdd(dense_fill) of the dense count matrix
+// D[n_pad][ldd] (u8) and scatters its counts there, for the tensor-core Gram.
 cudaError_t launch_light(SegmentOut so, uint64_t max_groups, int64_t heavy_min, int64_t N,
-                         int64_t* Cm, uint32_t* heavy, uint32_t* heavy_count,
+                         int64_t* Cm, uint8_t* dense, uint64_t ldd, uint32_t* dense_fill,
                          unsigned long long* stats, int sm_count, cudaStream_t s);
-// Heavy path (gram_tc.cu)
-size_t gram_smem_bytes();
+// Heavy path (gram_tc.cu): C_m += D D^T over the *dense_fill filled columns
+// (count read on the device), then the used columns are zeroed and the fill reset.
 std::vector<int2> gram_tiles(int64_t n_pad);
-cudaError_t launch_build_dense(SegmentOut so, const uint32_t* heavy, uint32_t r0, uint32_t R,
-                               uint32_t ldd, uint8_t* D, int sm_count, cudaStream_t s);
-cudaError_t launch_gram(const uint8_t* D, int64_t n_pad, uint32_t ldd, uint32_t kcols,
-                        int64_t* Cm, int64_t N, const int2* tiles, int ntiles, int sm_count,
-                        cudaStream_t s);
+cudaError_t launch_gram_flush(uint8_t* D, int64_t n_pad, uint64_t ldd, uint32_t* dense_fill,
+                              int64_t* Cm, int64_t N, const int2* tiles, int ntiles,
+                              int sm_count, unsigned long long* stats, cudaStream_t s);
 cudaError_t launch_diag_closed_form(const int64_t* gofs, int64_t N, int64_t nmask, int64_t* Cm,
                                     cudaStream_t s);
 cudaError_t launch_epilogue(int64_t* C, int64_t N, int g, int k, int M, int64_t* Nm, int64_t* K,

@@ -6,22 +6,31 @@
 // since X_a < X_b; the epilogue mirrors it (reading A4). Integer adds
 // commute, so the atomic update order never changes the result.
 //
-// One warp per group: the warp walks rows a and its lanes take columns b.
+// One warp per group; its triples are held in registers 32 at a time and the
+// pairs are spread over the lanes (triangle table within a chunk, full 32 x 32
+// blocks across chunks), so every atomic instruction carries 32 updates.
 #include "internal.cuh"
 
 namespace gk {
 
 __global__ void __launch_bounds__(256) light_kernel(SegmentOut so, int64_t heavy_min, int64_t N,
-                                                    int64_t* Cm, uint32_t* heavy,
-                                                    uint32_t* heavy_count,
+                                                    int64_t* Cm, uint8_t* dense, uint64_t ldd,
+                                                    uint32_t* dense_fill,
                                                     unsigned long long* stats) {
+    // triangle table: pairs (a < b < 32) ordered by b, so the first n(n-1)/2
+    // entries are exactly the pairs of an n-triple chunk
+    __shared__ uint16_t s_tri[496];
+    for (int b = 1, q = 0; b < 32; ++b)
+        for (int a = 0; a < b; ++a, ++q)
+            if (q % blockDim.x == threadIdx.x) s_tri[q] = (uint16_t)(a | (b << 5));
+    __syncthreads();
     const uint32_t G = so.counts[1];
     const int lane = threadIdx.x & 31;
     const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
     const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
     unsigned long long pairs = 0, nheavy = 0;
     for (uint64_t gi = warp; gi < G; gi += nwarps) {
-        const uint32_t a0 = so.gstart[gi], b0 = so.gend[gi];
+        const uint32_t a0 = so.gstart[gi], b0 = so.gstart[gi + 1];
         const uint32_t s = b0 - a0;
         if ((int64_t)s >= heavy_min) {
             // dense tensor-core path if every count fits the u8 operand
@@ -29,19 +38,53 @@ __global__ void __launch_bounds__(256) light_kernel(SegmentOut so, int64_t heavy
             for (uint32_t t = a0 + lane; t < b0; t += 32) cmax = max(cmax, so.tcnt[t]);
             cmax = __reduce_max_sync(0xffffffffu, cmax);
             if (cmax <= 255u) {
-                if (lane == 0) heavy[atomicAdd(heavy_count, 1u)] = (uint32_t)gi;
-                ++nheavy;
-                continue;
+                // claim a column of the dense count matrix D and scatter the counts
+                uint32_t col = 0;
+                if (lane == 0) col = atomicAdd(dense_fill, 1u);
+                col = __shfl_sync(0xffffffffu, col, 0);
+                if (col < ldd) {  // (a full D falls back to pair updates below)
+                    for (uint32_t t = a0 + lane; t < b0; t += 32)
+                        dense[(uint64_t)(so.tseq[t] & 0x7fffffffu) * ldd + col] =
+                            (uint8_t)so.tcnt[t];
+                    ++nheavy;
+                    continue;
+                }
             }
         }
         pairs += (unsigned long long)s * (s - 1) / 2;
-        for (uint32_t a = a0; a + 1 < b0; ++a) {
-            const int64_t xa = so.tseq[a] & 0x7fffffffu;
-            const uint64_t ca = so.tcnt[a];
-            int64_t* row = Cm + xa * N;
-            for (uint32_t b = a + 1 + lane; b < b0; b += 32) {
-                const int64_t xb = so.tseq[b] & 0x7fffffffu;
-                atomicAdd((unsigned long long*)&row[xb], ca * so.tcnt[b]);
+        // the group's triples in 32-wide register chunks; pairs enumerated
+        // lane-parallel: within a chunk through the triangle table, across chunks
+        // as full 32 x 32 blocks (every lane busy on every atomic)
+        for (uint32_t A = a0; A < b0; A += 32) {
+            const uint32_t ia = A + lane;
+            const uint32_t xA = ia < b0 ? (so.tseq[ia] & 0x7fffffffu) : 0u;
+            const uint32_t cA = ia < b0 ? so.tcnt[ia] : 0u;
+            const uint32_t na = min(32u, b0 - A);
+            const uint32_t P = na * (na - 1) / 2;
+            for (uint32_t q0 = 0; q0 < P; q0 += 32) {
+                const uint32_t q = q0 + lane;
+                const uint32_t ab = q < P ? s_tri[q] : 0u;
+                const int a = ab & 31, b = ab >> 5;
+                const uint32_t xa = __shfl_sync(0xffffffffu, xA, a);
+                const uint32_t ca = __shfl_sync(0xffffffffu, cA, a);
+                const uint32_t xb = __shfl_sync(0xffffffffu, xA, b);
+                const uint32_t cb = __shfl_sync(0xffffffffu, cA, b);
+                if (q < P)
+                    atomicAdd((unsigned long long*)&Cm[(int64_t)xa * N + xb],
+                              (unsigned long long)ca * cb);
+            }
+            for (uint32_t B = A + 32; B < b0; B += 32) {
+                const uint32_t ib = B + lane;
+                const bool vb = ib < b0;
+                const uint32_t xB = vb ? (so.tseq[ib] & 0x7fffffffu) : 0u;
+                const uint32_t cB = vb ? so.tcnt[ib] : 0u;
+                for (uint32_t a = 0; a < na; ++a) {
+                    const uint32_t xa = __shfl_sync(0xffffffffu, xA, a);
+                    const uint32_t ca = __shfl_sync(0xffffffffu, cA, a);
+                    if (vb)
+                        atomicAdd((unsigned long long*)&Cm[(int64_t)xa * N + xB],
+                                  (unsigned long long)ca * cB);
+                }
             }
         }
     }
@@ -50,15 +93,13 @@ __global__ void __launch_bounds__(256) light_kernel(SegmentOut so, int64_t heavy
 }
 
 cudaError_t launch_light(SegmentOut so, uint64_t max_groups, int64_t heavy_min, int64_t N,
-                         int64_t* Cm, uint32_t* heavy, uint32_t* heavy_count,
+                         int64_t* Cm, uint8_t* dense, uint64_t ldd, uint32_t* dense_fill,
                          unsigned long long* stats, int sm_count, cudaStream_t s) {
-    cudaError_t e = heavy_count ? cudaMemsetAsync(heavy_count, 0, sizeof(uint32_t), s)
-                                : cudaSuccess;
-    if (e != cudaSuccess || max_groups == 0) return e;
+    if (max_groups == 0) return cudaGetLastError();
     uint64_t blocks = (max_groups + 7) / 8;
     uint64_t cap = (uint64_t)sm_count * 8;
     if (blocks > cap) blocks = cap;
-    light_kernel<<<(unsigned)blocks, 256, 0, s>>>(so, heavy_min, N, Cm, heavy, heavy_count,
+    light_kernel<<<(unsigned)blocks, 256, 0, s>>>(so, heavy_min, N, Cm, dense, ldd, dense_fill,
                                                   stats);
     return cudaGetLastError();
 }

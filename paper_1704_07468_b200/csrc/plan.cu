@@ -76,6 +76,7 @@ struct gakco_plan {
     int rank = 0, world = 1;
     int64_t heavy_min = 0, batch_keys = 0;
     bool timing = false;
+    int sort_mode = 0;  // 0: chunked two-kernel LSD pass, 1: onesweep (decoupled look-back)
     int sm_count = 148;
     std::string err;
 
@@ -87,6 +88,7 @@ struct gakco_plan {
     DevBuf codes, off, gofs, gmseq, keysA, keysB, hist, status, ctr, tseq, tcnt, gstart, gend,
         counts, kept, stats, flags, kdiag, Cscr, Nmscr, Kscr, Knscr, heavy, hcount, dense, tiles;
     int64_t tiles_npad = -1;
+    uint64_t dense_ldd = 0;
     int ntiles = 0;
     uint32_t epoch = 1;
     uint32_t ctr_next = 0;
@@ -261,6 +263,10 @@ extern "C" gakco_status gakco_set_option(gakco_plan* p, int option, int64_t valu
             if (value < 0) return p->fail(GAKCO_E_ARG, "batch keys must be >= 0");
             p->batch_keys = value;
             return GAKCO_OK;
+        case GAKCO_OPT_SORT:
+            if (value < 0 || value > 1) return p->fail(GAKCO_E_ARG, "sort must be 0 or 1");
+            p->sort_mode = (int)value;
+            return GAKCO_OK;
         case GAKCO_OPT_TIMING:
             p->timing = value != 0;
             return GAKCO_OK;
@@ -385,7 +391,9 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
     const bool heavy_on = heavy_min < (int64_t)1 << 40 && N >= 2;
 
     // batch size (keys cap; with the Gram on, s32 exactness: masks * n_max^2 < 2^31)
-    uint64_t bk = p->batch_keys > 0 ? (uint64_t)p->batch_keys : (1ull << 26);
+    // default: ~4M keys (32 MB per key buffer) so encode -> sort -> segment of a
+    // batch stays resident in the 126 MB L2
+    uint64_t bk = p->batch_keys > 0 ? (uint64_t)p->batch_keys : (4ull << 20);
     if (bk > (1ull << 30) - 1) bk = (1ull << 30) - 1;
     uint64_t bmax_masks = std::max<uint64_t>(1, n ? bk / n : mine.size());
     if (heavy_on && nmax > 0) {
@@ -399,14 +407,17 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
     CK(p->ensure(p->keysB, cap_keys * 8, s));
     CK(p->ensure(p->tseq, cap_keys * 4, s));
     CK(p->ensure(p->tcnt, cap_keys * 4, s));
-    CK(p->ensure(p->gstart, (cap_keys / 2 + 1) * 4, s));
-    CK(p->ensure(p->gend, (cap_keys / 2 + 1) * 4, s));
+    CK(p->ensure(p->gstart, (cap_keys / 2 + 2) * 4, s));
     CK(p->ensure(p->counts, 16, s));
-    CK(p->ensure(p->hist, std::min<uint64_t>(bmax_masks, mine.size() + 1) * MAXPASS * RADIX * 4, s));
+    CK(p->ensure(p->hist, std::max<uint64_t>(std::min<uint64_t>(bmax_masks, mine.size() + 1) *
+                                                 MAXPASS * RADIX * 4,
+                                             (uint64_t)(3 * p->sm_count + 64 + bmax_masks) *
+                                                 RADIX * 4),
+                 s));
     {
         uint64_t tps = (n + SORT_TILE - 1) / SORT_TILE;
         uint64_t st_sort = std::min<uint64_t>(bmax_masks, mine.size() + 1) * RADIX * tps;
-        uint64_t st_seg = cap_keys / SEG_TILE + 2;
+        uint64_t st_seg = 2 * (cap_keys / SEG_TILE + 2);  // two look-back arrays
         CK(p->ensure(p->status, std::max(st_sort, st_seg) * 8, s, /*zero=*/true));
     }
     if (p->ctr.cap == 0) {
@@ -420,11 +431,18 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
     const int64_t light_limit = gram_ok ? heavy_min : INT64_MAX;
     uint64_t rcap = 0;
     if (gram_ok) {
-        CK(p->ensure(p->heavy, (cap_keys / 2 + 1) * 4, s));
-        CK(p->ensure(p->hcount, 16, s));
-        // dense chunk: n_pad rows x rcap u8 columns, at most ~1 GB
-        rcap = std::max<uint64_t>(128, ((1024ull << 20) / (uint64_t)n_pad) / 128 * 128);
-        CK(p->ensure(p->dense, (size_t)n_pad * rcap, s));
+        CK(p->ensure(p->hcount, 16, s, /*zero=*/true));
+        // dense count matrix D: n_pad rows x rcap u8 columns (<= 4 GB, and no more
+        // columns than heavy groups can exist), accumulated over batches of a level
+        const uint64_t most = (uint64_t)mine.size() * n / (uint64_t)heavy_min + 128;
+        rcap = std::min<uint64_t>((4096ull << 20) / (uint64_t)n_pad, most);
+        rcap = std::max<uint64_t>(128, (rcap + 127) / 128 * 128);
+        if ((size_t)n_pad * rcap > p->dense.cap) p->dense_ldd = 0;
+        CK(p->ensure(p->dense, (size_t)n_pad * rcap, s, /*zero=*/true));
+        if (p->dense_ldd != rcap) {  // new geometry: start from an all-zero buffer
+            CK(cudaMemsetAsync(p->dense.p, 0, (size_t)n_pad * rcap, s));
+            p->dense_ldd = rcap;
+        }
         if (p->tiles_npad != n_pad) {
             std::vector<int2> t = gram_tiles(n_pad);
             CK(p->ensure(p->tiles, t.size() * sizeof(int2), s));
@@ -438,9 +456,30 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
     CorpusView cv{(const uint8_t*)p->codes.p, (const int64_t*)p->off.p, (const int64_t*)p->gofs.p,
                   (const uint32_t*)p->gmseq.p, N, n};
     SegmentOut so{(uint32_t*)p->tseq.p, (uint32_t*)p->tcnt.p, (uint32_t*)p->gstart.p,
-                  (uint32_t*)p->gend.p, (uint32_t*)p->counts.p};
-    int64_t passkeys = 0, heavy_macs = 0;
+                  (uint32_t*)p->counts.p};
+    int64_t passkeys = 0;
     const size_t nn = (size_t)N * N;
+
+    // Heavy groups of consecutive batches of one level accumulate as columns of D;
+    // the Gram runs ("flush") at a level change, when D could overflow (a bound,
+    // so no host read-back is needed), or when the s32 sums could reach 2^31.
+    uint64_t dense_bound = 0, dense_masks = 0;
+    int dense_m = -1;
+    const uint64_t mask_lim =
+        gram_ok ? std::max<uint64_t>(1, (uint64_t)INT32_MAX / ((uint64_t)nmax * nmax)) : 0;
+    auto flush = [&]() -> gakco_status {
+        if (dense_m < 0 || dense_bound == 0) return GAKCO_OK;
+        cudaEvent_t ah = nullptr;
+        p->stage_begin(s, &ah);
+        p->launches += 2;  // + reset kernels
+        LK(launch_gram_flush((uint8_t*)p->dense.p, n_pad, rcap, (uint32_t*)p->hcount.p,
+                             C + (size_t)dense_m * nn, N, (const int2*)p->tiles.p, p->ntiles,
+                             p->sm_count, stats, s));
+        p->stage_end(s, S_HEAVY, ah);
+        dense_bound = 0;
+        dense_masks = 0;
+        return GAKCO_OK;
+    };
 
     size_t pos = 0;
     while (pos < mine.size()) {
@@ -452,22 +491,41 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
         const int npass = (kb + RADIX_BITS - 1) / RADIX_BITS;
         int64_t* Cm = C + (size_t)m * nn;
         cudaEvent_t a = nullptr;
+        if (gram_ok && n > 0) {
+            const uint64_t bnd = (uint64_t)nmask * n / (uint64_t)heavy_min + 1;
+            if (dense_m != m || dense_bound + bnd > rcap || dense_masks + nmask > mask_lim) {
+                gakco_status fs = flush();
+                if (fs != GAKCO_OK) return fs;
+            }
+            dense_m = m;
+            dense_bound += bnd;
+            dense_masks += nmask;
+        }
 
         if (n > 0) {
             p->stage_begin(s, &a);
-            CK(cudaMemsetAsync(p->hist.p, 0, (size_t)nmask * MAXPASS * RADIX * 4, s));
+            const bool onesweep = p->sort_mode == 1;
+            if (onesweep) CK(cudaMemsetAsync(p->hist.p, 0, (size_t)nmask * MAXPASS * RADIX * 4, s));
             LK(launch_encode(cv, (const uint8_t*)p->kept.p + pos * GMAX, g - m, p->sigma, sb,
-                             nmask, npass, (uint64_t*)p->keysA.p, (uint32_t*)p->hist.p, s));
+                             nmask, onesweep ? npass : 0, (uint64_t*)p->keysA.p,
+                             (uint32_t*)p->hist.p, s));
             p->stage_end(s, S_ENCODE, a);
 
             p->stage_begin(s, &a);
             uint64_t* in = (uint64_t*)p->keysA.p;
             uint64_t* outk = (uint64_t*)p->keysB.p;
             for (int q = 0; q < npass; ++q) {
-                uint32_t* c;
-                CK(p->next_ctr(s, &c));
-                LK(launch_onesweep(in, outk, n, nmask, sb + RADIX_BITS * q, (const uint32_t*)p->hist.p,
-                                   q, npass, (uint64_t*)p->status.p, c, p->epoch++, s));
+                if (onesweep) {
+                    uint32_t* c;
+                    CK(p->next_ctr(s, &c));
+                    LK(launch_onesweep(in, outk, n, nmask, sb + RADIX_BITS * q,
+                                       (const uint32_t*)p->hist.p, q, npass,
+                                       (uint64_t*)p->status.p, c, p->epoch++, s));
+                } else {
+                    p->launches += 1;  // two kernels
+                    LK(launch_radix_chunked(in, outk, n, nmask, sb + RADIX_BITS * q,
+                                            (uint32_t*)p->hist.p, 3 * p->sm_count, s));
+                }
                 std::swap(in, outk);
             }
             passkeys += (int64_t)npass * nmask * (int64_t)n;
@@ -476,45 +534,28 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
             p->stage_begin(s, &a);
             uint32_t* c1;
             CK(p->next_ctr(s, &c1));
-            LK(launch_triples(in, n, nmask, sb, N, Cm, (uint64_t*)p->status.p, c1, p->epoch++, so,
-                              stats, s));
-            uint32_t* c2;
-            CK(p->next_ctr(s, &c2));
-            LK(launch_groups(n * nmask, (uint64_t*)p->status.p, c2, p->epoch++, so, stats, s));
+            const uint64_t seg_tiles = n * nmask / SEG_TILE + 2;
+            LK(launch_segment(in, n, nmask, sb, N, Cm, (uint64_t*)p->status.p,
+                              (uint64_t*)p->status.p + seg_tiles, c1, p->epoch++, so, stats, s));
             p->stage_end(s, S_SEGMENT, a);
 
             p->stage_begin(s, &a);
-            LK(launch_light(so, n * nmask / 2 + 1, light_limit, N, Cm, (uint32_t*)p->heavy.p,
-                            (uint32_t*)p->hcount.p, stats, p->sm_count, s));
+            LK(launch_light(so, n * nmask / 2 + 1, light_limit, N, Cm, (uint8_t*)p->dense.p,
+                            rcap, (uint32_t*)p->hcount.p, stats, p->sm_count, s));
             p->stage_end(s, S_LIGHT, a);
-
-            if (gram_ok) {
-                uint32_t R = 0;
-                CK(cudaMemcpyAsync(&R, p->hcount.p, sizeof(uint32_t), cudaMemcpyDeviceToHost, s));
-                CK(cudaStreamSynchronize(s));
-                p->stage_begin(s, &a);
-                for (uint64_t r0 = 0; r0 < R; r0 += rcap) {
-                    const uint32_t rc = (uint32_t)std::min<uint64_t>(rcap, R - r0);
-                    const uint32_t ldd = (rc + 127) / 128 * 128;
-                    CK(cudaMemsetAsync(p->dense.p, 0, (size_t)n_pad * ldd, s));
-                    LK(launch_build_dense(so, (const uint32_t*)p->heavy.p, (uint32_t)r0, rc, ldd,
-                                          (uint8_t*)p->dense.p, p->sm_count, s));
-                    LK(launch_gram((const uint8_t*)p->dense.p, n_pad, ldd, ldd, Cm, N,
-                                   (const int2*)p->tiles.p, p->ntiles, p->sm_count, s));
-                    heavy_macs += (int64_t)p->ntiles * 128 * 256 * (int64_t)ldd;
-                }
-                p->stage_end(s, S_HEAVY, a);
-            }
         }
         LK(launch_diag_closed_form((const int64_t*)p->gofs.p, N, nmask, Cm, s));
         pos = end;
+    }
+    {
+        gakco_status fs = flush();
+        if (fs != GAKCO_OK) return fs;
     }
     p->last_masks = (int64_t)mine.size();
     p->host_stats = gakco_stats{};
     p->host_stats.masks = (int64_t)mine.size();
     p->host_stats.keys = (int64_t)mine.size() * (int64_t)n;
     p->host_stats.sort_passes = passkeys;
-    p->host_stats.heavy_macs = heavy_macs;
     p->after_accumulate = true;
     return GAKCO_OK;
 #undef CK
@@ -643,6 +684,7 @@ extern "C" gakco_status gakco_get_stats(gakco_plan* p, gakco_stats* out) {
         r.groups_multi = (int64_t)d[ST_GROUPS];
         r.light_pairs = (int64_t)d[ST_LIGHT_PAIRS];
         r.heavy_groups = (int64_t)d[ST_HEAVY_GROUPS];
+        r.heavy_macs = (int64_t)d[ST_HEAVY_MACS];
     }
     double* ms[S_NSTAGE] = {&r.ms_encode, &r.ms_sort, &r.ms_segment,
                             &r.ms_light,  &r.ms_heavy, &r.ms_epilogue};

@@ -16,6 +16,8 @@
 //      (segment, digit, tile)) and looks back for the exclusive prefix;
 //   4. it reorders the tile by digit in shared memory and writes each digit's run
 //      contiguously to  seg*n + digit_base[d] + prefix[d] + local offset.
+#include <algorithm>
+
 #include "internal.cuh"
 
 namespace gk {
@@ -161,6 +163,173 @@ cudaError_t launch_onesweep(const uint64_t* in, uint64_t* out, uint64_t n, int n
     onesweep_kernel<<<(unsigned)tiles, SORT_THREADS, ONESWEEP_SMEM, s>>>(in, out, n, tps,
                                                              (uint32_t)nseg, shift, hist, pass,
                                                              npass, status, ctr, epoch);
+    return cudaGetLastError();
+}
+
+// ============================================================================
+// Chunked LSD pass (no look-back chain): the same stable 8-bit pass, split in
+// two kernels so that no tile ever waits on another:
+//   radix_hist:    CTA (seg, c) counts the pass digit over its chunk of L keys;
+//   radix_scatter: CTA (seg, c) sums the chunk histograms of its segment (digit
+//                  totals -> digit bases; chunks < c -> its prefix), then walks
+//                  its chunk in 4096-key tiles IN ORDER, ranking each tile
+//                  stably (warp match + per-warp counters), reordering it by
+//                  digit in shared memory and writing each digit run to
+//                  seg*n + base[d] + prefix[d] + running[d] + local offset.
+// Batches are sized to stay resident in the 126 MB L2, so the second read of a
+// chunk, and the next pass's reads of this pass's output, hit in L2.
+// ============================================================================
+constexpr int RS_THREADS = SORT_THREADS;  // 512
+constexpr int RS_WARPS = RS_THREADS / 32;
+
+__global__ void __launch_bounds__(RS_THREADS) radix_hist_kernel(
+    const uint64_t* __restrict__ in, uint64_t n, uint32_t cps, uint64_t L, int shift,
+    uint32_t* __restrict__ hist) {
+    __shared__ uint32_t s_h[RS_WARPS][RADIX];
+    const int tid = threadIdx.x, w = tid >> 5;
+    for (int i = tid; i < RS_WARPS * RADIX; i += RS_THREADS) (&s_h[0][0])[i] = 0;
+    __syncthreads();
+    const uint32_t seg = blockIdx.x / cps, c = blockIdx.x - seg * cps;
+    const uint64_t lo = (uint64_t)c * L;
+    const uint64_t hi = min(n, lo + L);
+    const uint64_t* p = in + (uint64_t)seg * n;
+    if (lo < hi) {
+        // 16-byte loads on the even-aligned body, scalars on the edges
+        uint64_t a = lo, b = hi;
+        const uint64_t base = (uint64_t)seg * n;
+        if ((base + a) & 1) {
+            if (tid == 0) atomicAdd(&s_h[0][(p[a] >> shift) & 0xff], 1u);
+            ++a;
+        }
+        if ((b - a) & 1) {
+            if (tid == 0) atomicAdd(&s_h[0][(p[b - 1] >> shift) & 0xff], 1u);
+            --b;
+        }
+        const ulonglong2* v = (const ulonglong2*)(p + a);
+        const uint64_t nv = (b - a) / 2;
+        for (uint64_t i = tid; i < nv; i += RS_THREADS) {
+            const ulonglong2 q = v[i];
+            atomicAdd(&s_h[w][(q.x >> shift) & 0xff], 1u);
+            atomicAdd(&s_h[w][(q.y >> shift) & 0xff], 1u);
+        }
+    }
+    __syncthreads();
+    if (tid < RADIX) {
+        uint32_t s = 0;
+        for (int ww = 0; ww < RS_WARPS; ++ww) s += s_h[ww][tid];
+        hist[((uint64_t)seg * cps + c) * RADIX + tid] = s;
+    }
+}
+
+__global__ void __launch_bounds__(RS_THREADS) radix_scatter_kernel(
+    const uint64_t* __restrict__ in, uint64_t* __restrict__ out, uint64_t n, uint32_t cps,
+    uint64_t L, int shift, const uint32_t* __restrict__ hist) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    uint64_t* s_keys = (uint64_t*)smem;                                  // [SORT_TILE]
+    int64_t* s_run = (int64_t*)(s_keys + SORT_TILE);                     // [RADIX]
+    uint32_t(*s_whist)[RADIX] = (uint32_t(*)[RADIX])(s_run + RADIX);     // [WARPS][RADIX]
+    uint32_t* s_doff = &s_whist[RS_WARPS][0];                            // [RADIX]
+    uint32_t* s_cnt = s_doff + RADIX;                                    // [RADIX]
+    uint32_t* s_w = s_cnt + RADIX;                                       // [8]
+
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const uint32_t seg = blockIdx.x / cps, c = blockIdx.x - seg * cps;
+    const uint64_t lo = (uint64_t)c * L;
+    const uint64_t hi = min(n, lo + L);
+    const uint64_t seg_base = (uint64_t)seg * n;
+
+    // digit totals of the segment and this chunk's prefix (all chunks < c)
+    uint32_t tot = 0, pre = 0;
+    if (tid < RADIX) {
+        const uint32_t* h = hist + (uint64_t)seg * cps * RADIX + tid;
+        for (uint32_t cc = 0; cc < cps; ++cc) {
+            const uint32_t v = h[(uint64_t)cc * RADIX];
+            tot += v;
+            pre += cc < c ? v : 0u;
+        }
+    }
+    const uint32_t dbase = scan256_excl(tot, s_w);
+    if (tid < RADIX) s_run[tid] = (int64_t)dbase + pre;
+    __syncthreads();
+
+    const uint32_t lt = lanemask_lt();
+    for (uint64_t t0 = lo; t0 < hi; t0 += SORT_TILE) {
+        const uint32_t cnt = (uint32_t)min((uint64_t)SORT_TILE, hi - t0);
+        for (int i = tid; i < RS_WARPS * RADIX; i += RS_THREADS) (&s_whist[0][0])[i] = 0;
+        __syncthreads();
+        uint64_t keys[SORT_ITEMS];
+        uint32_t rank[SORT_ITEMS];
+#pragma unroll
+        for (int i = 0; i < SORT_ITEMS; ++i) {
+            const uint32_t idx = w * SORT_ITEMS * 32 + i * 32 + lane;
+            keys[i] = idx < cnt ? in[seg_base + t0 + idx] : 0ull;
+        }
+#pragma unroll
+        for (int i = 0; i < SORT_ITEMS; ++i) {
+            const uint32_t idx = w * SORT_ITEMS * 32 + i * 32 + lane;
+            const bool valid = idx < cnt;
+            const uint32_t d = (uint32_t)(keys[i] >> shift) & 0xffu;
+            const uint32_t vmask = __ballot_sync(0xffffffffu, valid);
+            const uint32_t peers = __match_any_sync(0xffffffffu, d) & vmask;
+            const uint32_t prior = valid ? s_whist[w][d] : 0u;
+            __syncwarp();
+            if (valid && lane == __ffs(peers) - 1) s_whist[w][d] = prior + __popc(peers);
+            __syncwarp();
+            rank[i] = prior + __popc(peers & lt);
+        }
+        __syncthreads();
+        uint32_t tcnt = 0;
+        if (tid < RADIX) {
+            uint32_t sum = 0;
+            for (int ww = 0; ww < RS_WARPS; ++ww) {
+                const uint32_t v = s_whist[ww][tid];
+                s_whist[ww][tid] = sum;
+                sum += v;
+            }
+            tcnt = sum;
+            s_cnt[tid] = sum;
+        }
+        const uint32_t doff = scan256_excl(tcnt, s_w);
+        if (tid < RADIX) s_doff[tid] = doff;
+        __syncthreads();
+#pragma unroll
+        for (int i = 0; i < SORT_ITEMS; ++i) {
+            const uint32_t idx = w * SORT_ITEMS * 32 + i * 32 + lane;
+            if (idx < cnt) {
+                const uint32_t d = (uint32_t)(keys[i] >> shift) & 0xffu;
+                s_keys[s_doff[d] + s_whist[w][d] + rank[i]] = keys[i];
+            }
+        }
+        __syncthreads();
+        for (uint32_t j = tid; j < cnt; j += RS_THREADS) {
+            const uint64_t k = s_keys[j];
+            const uint32_t d = (uint32_t)(k >> shift) & 0xffu;
+            out[seg_base + (uint64_t)(s_run[d] + (int64_t)(j - s_doff[d]))] = k;
+        }
+        __syncthreads();
+        if (tid < RADIX) s_run[tid] += s_cnt[tid];
+        // (the loop-top __syncthreads orders this before the next tile's reads)
+    }
+}
+
+constexpr size_t RS_SMEM = SORT_TILE * 8 + RADIX * 8 + RS_WARPS * RADIX * 4 + 2 * RADIX * 4 + 16 * 4;
+
+cudaError_t launch_radix_chunked(const uint64_t* in, uint64_t* out, uint64_t n, int nseg,
+                                 int shift, uint32_t* hist, int target_ctas, cudaStream_t s) {
+    if (n == 0 || nseg == 0) return cudaGetLastError();
+    // chunks per segment: fill ~target_ctas CTAs, whole 4096-key tiles per chunk
+    uint64_t tiles = (n + SORT_TILE - 1) / SORT_TILE;
+    uint64_t cps = std::max<uint64_t>(1, std::min<uint64_t>(tiles, (target_ctas + nseg - 1) / nseg));
+    uint64_t L = (tiles + cps - 1) / cps * SORT_TILE;
+    cps = (n + L - 1) / L;
+    const unsigned grid = (unsigned)(cps * nseg);
+    radix_hist_kernel<<<grid, RS_THREADS, 0, s>>>(in, n, (uint32_t)cps, L, shift, hist);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    cudaFuncSetAttribute(radix_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)RS_SMEM);
+    radix_scatter_kernel<<<grid, RS_THREADS, RS_SMEM, s>>>(in, out, n, (uint32_t)cps, L, shift,
+                                                           hist);
     return cudaGetLastError();
 }
 

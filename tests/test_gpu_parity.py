@@ -116,6 +116,19 @@ def test_batch_size_invariance(gk, oracle_lib):
     ref = oracle_lib.compute(cp, 7, 5, 2)
     for bk in (1, 4700, 3 * 4700 + 5, 1 << 20):
         assert_parity(run(gk, cp, 7, 5, 2, batch_keys=bk), ref)
+        assert_parity(run(gk, cp, 7, 5, 2, batch_keys=bk, sort=1), ref)
+
+
+def test_sort_modes_ragged(gk, oracle_lib):
+    """The chunked LSD pass and the onesweep pass give identical results on
+    segments spanning many tiles, with ragged tails and odd alignments."""
+    rng = np.random.default_rng(104)
+    seqs = [rng.integers(0, 20, size=int(rng.integers(0, 3000))) for _ in range(37)]
+    cp = sc.from_sequences(20, seqs)
+    ref = oracle_lib.compute(cp, 8, 4, 4)
+    for bk in (0, 50001):
+        assert_parity(run(gk, cp, 8, 4, 4, batch_keys=bk, sort=0), ref)
+        assert_parity(run(gk, cp, 8, 4, 4, batch_keys=bk, sort=1), ref)
 
 
 def test_edge_cases(gk, oracle_lib):
