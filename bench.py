@@ -46,6 +46,10 @@ def args_():
     ap.add_argument("--cpu-seconds", type=float, default=15.0,
                     help="target seconds of oracle work per CPU sample")
     ap.add_argument("--heavy-min", type=int, default=0)
+    ap.add_argument("--batch-keys", type=int, default=0)
+    ap.add_argument("--sort", type=int, default=None, choices=[0, 1])
+    ap.add_argument("--no-timing", action="store_true",
+                    help="no per-stage events (roofline then uses the last timed stages)")
     return ap.parse_args()
 
 
@@ -226,6 +230,12 @@ def run_ours(a):
     plan.set_option(gakco.GAKCO_OPT_TIMING, 1)
     if a.heavy_min:
         plan.set_option(gakco.GAKCO_OPT_HEAVY_MIN_SEQS, a.heavy_min)
+    if a.batch_keys:
+        plan.set_option(gakco.GAKCO_OPT_BATCH_KEYS, a.batch_keys)
+    if a.sort is not None:
+        plan.set_option(gakco.GAKCO_OPT_SORT, a.sort)
+    if a.no_timing:
+        plan.set_option(gakco.GAKCO_OPT_TIMING, 0)
     C = torch.zeros((M + 1, N, N), dtype=torch.int64, device=dev)
     Nm = torch.empty_like(C) if rank == 0 else None
     K = torch.empty((N, N), dtype=torch.int64, device=dev) if rank == 0 else None
@@ -325,6 +335,8 @@ def run_ours(a):
     pk = peaks()
     model = stage_model(last, cfg, N)
     per_step = {k[3:]: v / a.steps for k, v in stage_ms.items()}
+    if not any(per_step.values()):  # --no-timing: stage split unavailable
+        per_step = {"sort": ms_per_step}
     dom = max(per_step, key=lambda s: per_step[s])
     bound, algo = model[dom]
     t_dom = per_step[dom] / 1e3

@@ -401,7 +401,8 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
         bmax_masks = std::max<uint64_t>(1, std::min(bmax_masks, lim));
     }
     // a single mask whose n_max^2 exceeds 2^31 would need the light path only
-    const bool gram_ok = heavy_on && (uint64_t)nmax * (uint64_t)nmax <= (uint64_t)INT32_MAX;
+    const bool gram_ok =
+        heavy_on && nmax > 0 && (uint64_t)nmax * (uint64_t)nmax <= (uint64_t)INT32_MAX;
     const uint64_t cap_keys = std::max<uint64_t>(1, std::min<uint64_t>(bmax_masks, mine.size()) * n);
     CK(p->ensure(p->keysA, cap_keys * 8, s));
     CK(p->ensure(p->keysB, cap_keys * 8, s));

@@ -253,6 +253,17 @@ __global__ void __launch_bounds__(RS_THREADS) radix_scatter_kernel(
     __syncthreads();
 
     const uint32_t lt = lanemask_lt();
+    // register double buffer: the next tile's keys are in flight while this one
+    // is ranked and scattered
+    uint64_t nxt[SORT_ITEMS];
+    {
+        const uint32_t cnt0 = (uint32_t)min((uint64_t)SORT_TILE, hi > lo ? hi - lo : 0);
+#pragma unroll
+        for (int i = 0; i < SORT_ITEMS; ++i) {
+            const uint32_t idx = w * SORT_ITEMS * 32 + i * 32 + lane;
+            nxt[i] = idx < cnt0 ? in[seg_base + lo + idx] : 0ull;
+        }
+    }
     for (uint64_t t0 = lo; t0 < hi; t0 += SORT_TILE) {
         const uint32_t cnt = (uint32_t)min((uint64_t)SORT_TILE, hi - t0);
         for (int i = tid; i < RS_WARPS * RADIX; i += RS_THREADS) (&s_whist[0][0])[i] = 0;
@@ -260,9 +271,15 @@ __global__ void __launch_bounds__(RS_THREADS) radix_scatter_kernel(
         uint64_t keys[SORT_ITEMS];
         uint32_t rank[SORT_ITEMS];
 #pragma unroll
-        for (int i = 0; i < SORT_ITEMS; ++i) {
-            const uint32_t idx = w * SORT_ITEMS * 32 + i * 32 + lane;
-            keys[i] = idx < cnt ? in[seg_base + t0 + idx] : 0ull;
+        for (int i = 0; i < SORT_ITEMS; ++i) keys[i] = nxt[i];
+        if (t0 + SORT_TILE < hi) {
+            const uint64_t t1 = t0 + SORT_TILE;
+            const uint32_t cnt1 = (uint32_t)min((uint64_t)SORT_TILE, hi - t1);
+#pragma unroll
+            for (int i = 0; i < SORT_ITEMS; ++i) {
+                const uint32_t idx = w * SORT_ITEMS * 32 + i * 32 + lane;
+                nxt[i] = idx < cnt1 ? in[seg_base + t1 + idx] : 0ull;
+            }
         }
 #pragma unroll
         for (int i = 0; i < SORT_ITEMS; ++i) {
