@@ -71,6 +71,14 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, u
         "l"((uint64_t)map), "r"(smem_u32(bar)), "r"(x), "r"(y)
         : "memory");
 }
+__device__ __forceinline__ void tma_load_3d(void* dst, const CUtensorMap* map, uint64_t* bar,
+                                            int x, int y, int z) {
+    asm volatile(
+        "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(smem_u32(dst)),
+        "l"((uint64_t)map), "r"(smem_u32(bar)), "r"(x), "r"(y), "r"(z)
+        : "memory");
+}
 __device__ __forceinline__ void tc_fence_after() {
     asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
 }
@@ -211,10 +219,9 @@ __global__ void __launch_bounds__(GT_THREADS, 1)
                     unsigned char* sa = smem + (size_t)stage * GT_STAGE_BYTES;
                     unsigned char* sbm = sa + GT_A_BYTES;
                     mbar_expect_tx(&full[stage], GT_STAGE_BYTES);
-                    tma_load_2d(sa, &dmap, &full[stage], kb * GT_KB, tl.x * GT_M);
-                    tma_load_2d(sbm, &dmap, &full[stage], kb * GT_KB, tl.y * GT_N);
-                    tma_load_2d(sbm + GT_A_BYTES, &dmap, &full[stage], kb * GT_KB,
-                                tl.y * GT_N + GT_M);
+                    tma_load_3d(sa, &dmap, &full[stage], 0, tl.x * GT_M, kb);
+                    tma_load_3d(sbm, &dmap, &full[stage], 0, tl.y * GT_N, kb);
+                    tma_load_3d(sbm + GT_A_BYTES, &dmap, &full[stage], 0, tl.y * GT_N + GT_M, kb);
                     if (++stage == GT_STAGES) {
                         stage = 0;
                         phase ^= 1;
@@ -320,14 +327,12 @@ __global__ void __launch_bounds__(GT_THREADS, 1)
 // D is all-zero again for the next accumulation.
 __global__ void dense_reset_kernel(uint8_t* __restrict__ D, int64_t n_pad, uint64_t ldd,
                                    const uint32_t* fill) {
-    const uint64_t used = (min((uint64_t)*fill, ldd) + GT_KB - 1) / GT_KB * GT_KB;
-    const uint64_t per_row = used / 16;  // 16-byte stores
-    const uint64_t total = per_row * (uint64_t)n_pad;
+    // the used slabs [0, ceil(fill/128)) are one contiguous range of bytes
+    const uint64_t slabs = (min((uint64_t)*fill, ldd) + GT_KB - 1) / GT_KB;
+    const uint64_t total = slabs * (uint64_t)n_pad * GT_KB / 16;  // 16-byte stores
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total;
-         i += (uint64_t)gridDim.x * blockDim.x) {
-        const uint64_t r = i / per_row, c = i - r * per_row;
-        *(uint4*)(D + r * ldd + c * 16) = make_uint4(0, 0, 0, 0);
-    }
+         i += (uint64_t)gridDim.x * blockDim.x)
+        ((uint4*)D)[i] = make_uint4(0, 0, 0, 0);
 }
 
 __global__ void fill_reset_kernel(uint32_t* fill, uint64_t ldd, uint64_t tile_macs,
@@ -372,11 +377,12 @@ cudaError_t launch_gram_flush(uint8_t* D, int64_t n_pad, uint64_t ldd, uint32_t*
     EncodeTiledFn enc = get_encode();
     if (!enc) return cudaErrorNotSupported;
     CUtensorMap map;
-    cuuint64_t dims[2] = {ldd, (cuuint64_t)n_pad};
-    cuuint64_t strides[1] = {ldd};
-    cuuint32_t box[2] = {GT_KB, GT_M};
-    cuuint32_t estr[2] = {1, 1};
-    CUresult r = enc(&map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, (void*)D, dims, strides, box, estr,
+    // D as slabs: [ldd/128][n_pad][128] u8 -> 3-D map, box = 128 B x 128 rows x 1 slab
+    cuuint64_t dims[3] = {(cuuint64_t)GT_KB, (cuuint64_t)n_pad, ldd / GT_KB};
+    cuuint64_t strides[2] = {(cuuint64_t)GT_KB, (cuuint64_t)n_pad * GT_KB};
+    cuuint32_t box[3] = {GT_KB, GT_M, 1};
+    cuuint32_t estr[3] = {1, 1, 1};
+    CUresult r = enc(&map, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, (void*)D, dims, strides, box, estr,
                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;

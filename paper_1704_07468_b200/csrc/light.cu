@@ -15,7 +15,7 @@ namespace gk {
 
 __global__ void __launch_bounds__(256) light_kernel(SegmentOut so, int64_t heavy_min, int64_t N,
                                                     int64_t* Cm, uint8_t* dense, uint64_t ldd,
-                                                    uint32_t* dense_fill,
+                                                    uint64_t n_pad, uint32_t* dense_fill,
                                                     unsigned long long* stats) {
     // triangle table: pairs (a < b < 32) ordered by b, so the first n(n-1)/2
     // entries are exactly the pairs of an n-triple chunk
@@ -43,9 +43,12 @@ __global__ void __launch_bounds__(256) light_kernel(SegmentOut so, int64_t heavy
                 if (lane == 0) col = atomicAdd(dense_fill, 1u);
                 col = __shfl_sync(0xffffffffu, col, 0);
                 if (col < ldd) {  // (a full D falls back to pair updates below)
+                    // D is stored as slabs of 128 columns: [col/128][row][col%128], so
+                    // the 128 groups of a slab write into the same 128-byte lines
+                    uint8_t* slab = dense + (uint64_t)(col >> 7) * (uint64_t)n_pad * 128u +
+                                    (col & 127u);
                     for (uint32_t t = a0 + lane; t < b0; t += 32)
-                        dense[(uint64_t)(so.tseq[t] & 0x7fffffffu) * ldd + col] =
-                            (uint8_t)so.tcnt[t];
+                        slab[(uint64_t)(so.tseq[t] & 0x7fffffffu) * 128u] = (uint8_t)so.tcnt[t];
                     ++nheavy;
                     continue;
                 }
@@ -93,13 +96,15 @@ __global__ void __launch_bounds__(256) light_kernel(SegmentOut so, int64_t heavy
 }
 
 cudaError_t launch_light(SegmentOut so, uint64_t max_groups, int64_t heavy_min, int64_t N,
-                         int64_t* Cm, uint8_t* dense, uint64_t ldd, uint32_t* dense_fill,
+                         int64_t* Cm, uint8_t* dense, uint64_t ldd, uint64_t n_pad,
+                         uint32_t* dense_fill,
                          unsigned long long* stats, int sm_count, cudaStream_t s) {
     if (max_groups == 0) return cudaGetLastError();
     uint64_t blocks = (max_groups + 7) / 8;
     uint64_t cap = (uint64_t)sm_count * 8;
     if (blocks > cap) blocks = cap;
-    light_kernel<<<(unsigned)blocks, 256, 0, s>>>(so, heavy_min, N, Cm, dense, ldd, dense_fill,
+    light_kernel<<<(unsigned)blocks, 256, 0, s>>>(so, heavy_min, N, Cm, dense, ldd, n_pad,
+                                                  dense_fill,
                                                   stats);
     return cudaGetLastError();
 }

@@ -391,9 +391,9 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
     const bool heavy_on = heavy_min < (int64_t)1 << 40 && N >= 2;
 
     // batch size (keys cap; with the Gram on, s32 exactness: masks * n_max^2 < 2^31)
-    // default: ~4M keys (32 MB per key buffer) so encode -> sort -> segment of a
-    // batch stays resident in the 126 MB L2
-    uint64_t bk = p->batch_keys > 0 ? (uint64_t)p->batch_keys : (4ull << 20);
+    // default: up to 64M keys (512 MB per key buffer): large launches measured
+    // faster than L2-sized (4M-key) batches for every stage
+    uint64_t bk = p->batch_keys > 0 ? (uint64_t)p->batch_keys : (64ull << 20);
     if (bk > (1ull << 30) - 1) bk = (1ull << 30) - 1;
     uint64_t bmax_masks = std::max<uint64_t>(1, n ? bk / n : mine.size());
     if (heavy_on && nmax > 0) {
@@ -542,7 +542,8 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
 
             p->stage_begin(s, &a);
             LK(launch_light(so, n * nmask / 2 + 1, light_limit, N, Cm, (uint8_t*)p->dense.p,
-                            rcap, (uint32_t*)p->hcount.p, stats, p->sm_count, s));
+                            rcap, (uint64_t)n_pad, (uint32_t*)p->hcount.p, stats, p->sm_count,
+                            s));
             p->stage_end(s, S_LIGHT, a);
         }
         LK(launch_diag_closed_form((const int64_t*)p->gofs.p, N, nmask, Cm, s));
