@@ -85,6 +85,53 @@ __device__ __forceinline__ uint32_t lookback_one(uint64_t* status, uint32_t t, u
     return excl;
 }
 
+// Warp-cooperative decoupled look-back (all 32 lanes of ONE warp call it): the
+// lanes read 32 predecessors' statuses at once, so each L2 round trip consumes up
+// to 32 tiles; returns the exclusive prefix (to every lane).
+__device__ __forceinline__ uint32_t lookback_warp(uint64_t* status, uint32_t t, uint32_t agg,
+                                                  uint32_t epoch) {
+    const int lane = threadIdx.x & 31;
+    if (t == 0) {
+        if (lane == 0) *(volatile uint64_t*)(status) = lb_pack(epoch, LB_INC, agg);
+        return 0;
+    }
+    if (lane == 0) *(volatile uint64_t*)(status + t) = lb_pack(epoch, LB_AGG, agg);
+    uint32_t excl = 0;
+    int64_t p = (int64_t)t - 1;
+    while (true) {
+        const int64_t q = p - lane;
+        const uint64_t v = q >= 0 ? *(volatile const uint64_t*)(status + q)
+                                  : lb_pack(epoch, LB_INC, 0);
+        const uint32_t ep = (uint32_t)(v >> 32), fl = (uint32_t)(v >> 30) & 3u;
+        const bool ready = ep == epoch && fl != LB_NONE;
+        const uint32_t incm = __ballot_sync(0xffffffffu, ready && fl == LB_INC);
+        const uint32_t notready = __ballot_sync(0xffffffffu, !ready);
+        const int first = incm ? __ffs(incm) - 1 : 31;  // nearest inclusive (or the window)
+        const uint32_t need = first == 31 ? 0xffffffffu : ((2u << first) - 1u);
+        if (notready & need) continue;  // a needed predecessor has not published: re-read
+        uint32_t val = lane <= first ? (uint32_t)(v & 0x3fffffffu) : 0u;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) val += __shfl_xor_sync(0xffffffffu, val, o);
+        excl += val;
+        if (incm) break;
+        p -= 32;
+    }
+    if (lane == 0) *(volatile uint64_t*)(status + t) = lb_pack(epoch, LB_INC, excl + agg);
+    return excl;
+}
+
+// Lanes of the warp holding the same 8-bit digit d (ballot multisplit: 8 votes
+// instead of one match.any, which stalls on the MIO pipe).
+__device__ __forceinline__ uint32_t digit_peers(uint32_t d, uint32_t valid_mask) {
+    uint32_t peers = valid_mask;
+#pragma unroll
+    for (int b = 0; b < 8; ++b) {
+        const uint32_t bal = __ballot_sync(0xffffffffu, (d >> b) & 1u);
+        peers &= ((d >> b) & 1u) ? bal : ~bal;
+    }
+    return peers;
+}
+
 // Device counters of gakco_stats (int64 slots).
 enum { ST_KEYS = 0, ST_PASSKEYS, ST_TRIPLES, ST_GROUPS, ST_LIGHT_PAIRS, ST_HEAVY_GROUPS,
        ST_HEAVY_MACS, ST_COUNT };

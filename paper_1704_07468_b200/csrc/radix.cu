@@ -66,7 +66,7 @@ __global__ void __launch_bounds__(SORT_THREADS) onesweep_kernel(
         bool valid = idx < cnt;
         uint32_t d = (uint32_t)(keys[i] >> shift) & 0xffu;
         uint32_t vmask = __ballot_sync(0xffffffffu, valid);
-        uint32_t peers = __match_any_sync(0xffffffffu, d) & vmask;
+        uint32_t peers = digit_peers(d, vmask);
         uint32_t prior = valid ? s_whist[w][d] : 0u;
         __syncwarp();
         if (valid && lane == __ffs(peers) - 1) s_whist[w][d] = prior + __popc(peers);
@@ -287,7 +287,7 @@ __global__ void __launch_bounds__(RS_THREADS) radix_scatter_kernel(
             const bool valid = idx < cnt;
             const uint32_t d = (uint32_t)(keys[i] >> shift) & 0xffu;
             const uint32_t vmask = __ballot_sync(0xffffffffu, valid);
-            const uint32_t peers = __match_any_sync(0xffffffffu, d) & vmask;
+            const uint32_t peers = digit_peers(d, vmask);
             const uint32_t prior = valid ? s_whist[w][d] : 0u;
             __syncwarp();
             if (valid && lane == __ffs(peers) - 1) s_whist[w][d] = prior + __popc(peers);

@@ -102,8 +102,13 @@ __global__ void __launch_bounds__(SEG_THREADS) segment_kernel(
     uint32_t agg_t, agg_g;
     const uint32_t off_t = scan256_excl(__popc(emit_t), s_w, &agg_t);
     const uint32_t off_g = scan256_excl(__popc(emit_g), s_w, &agg_g);
-    if (tid == 0) s_pt = lookback_one(status_t, t, agg_t, epoch);
-    if (tid == 32) s_pg = lookback_one(status_g, t, agg_g, epoch);
+    if (tid < 32) {
+        const uint32_t e = lookback_warp(status_t, t, agg_t, epoch);
+        if (tid == 0) s_pt = e;
+    } else if (tid < 64) {
+        const uint32_t e = lookback_warp(status_g, t, agg_g, epoch);
+        if (tid == 32) s_pg = e;
+    }
     __syncthreads();
     uint32_t ti = s_pt + off_t, gi = s_pg + off_g;
 #pragma unroll
