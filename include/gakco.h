@@ -78,6 +78,8 @@ typedef struct {
     int64_t heavy_macs;     /* u8 multiply-accumulates issued by the Gram */
     int64_t launches;       /* kernels launched by the last accumulate + finalize */
     double ms_encode, ms_sort, ms_segment, ms_light, ms_heavy, ms_epilogue;
+    /* kernel launches per stage (same stages as the ms_* fields) */
+    int64_t n_encode, n_sort, n_segment, n_light, n_heavy, n_epilogue;
 } gakco_stats;
 
 /* Create a plan for alphabet size sigma (1..255), g-mer length g (1..32),

@@ -138,12 +138,16 @@ struct gakco_plan {
         }
         return ev_pool[ev_used++];
     }
+    int64_t stage_launches[S_NSTAGE] = {0, 0, 0, 0, 0, 0};
+    int64_t launches_at_begin = 0;
     void stage_begin(cudaStream_t s, cudaEvent_t* a) {
+        launches_at_begin = launches;
         if (!timing) return;
         *a = ev();
         cudaEventRecord(*a, s);
     }
     void stage_end(cudaStream_t s, int stage, cudaEvent_t a) {
+        stage_launches[stage] += launches - launches_at_begin;
         if (!timing) return;
         cudaEvent_t b = ev();
         cudaEventRecord(b, s);
@@ -296,6 +300,7 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
         CK(x);       \
     } while (0)
     p->launches = 0;
+    for (int64_t& v : p->stage_launches) v = 0;
     if (!codes && N > 0) return p->fail(GAKCO_E_ARG, "codes is NULL");
     if (!offsets || !C) return p->fail(GAKCO_E_ARG, "offsets or C is NULL");
     if (N < 1 || N >= ((int64_t)1 << 31)) return p->fail(GAKCO_E_ARG, "N must be in [1, 2^31)");
@@ -592,6 +597,7 @@ static gakco_status finalize_impl(gakco_plan* p, int64_t* C, int64_t N, int64_t*
         p->evs.clear();
         p->ev_used = 0;
         p->launches = 0;
+        for (int64_t& v : p->stage_launches) v = 0;
     }
     p->after_accumulate = false;
     p->last_stream = s;
@@ -676,6 +682,9 @@ extern "C" gakco_status gakco_get_stats(gakco_plan* p, gakco_stats* out) {
     DeviceGuard dg(p->device);
     gakco_stats r = p->host_stats;
     r.launches = p->launches;
+    int64_t* nl[S_NSTAGE] = {&r.n_encode, &r.n_sort, &r.n_segment,
+                             &r.n_light,  &r.n_heavy, &r.n_epilogue};
+    for (int i = 0; i < S_NSTAGE; ++i) *nl[i] = p->stage_launches[i];
     if (p->stats.p) {
         unsigned long long d[ST_COUNT];
         cudaError_t e = cudaMemcpyAsync(d, p->stats.p, sizeof d, cudaMemcpyDeviceToHost,

@@ -171,6 +171,25 @@ def test_shard_emulation(gk, oracle_lib):
                        "Knorm": Kn.cpu().numpy()}, ref)
 
 
+def test_shard_rule_matches_library(gk):
+    """gakco_set_shard(r, P) accumulates exactly the masks parallel.shard_masks
+    lists (checked against the literal Algorithm 1 reference per shard)."""
+    from tests.test_multirank import _partial_C
+    from paper_1704_07468_b200 import parallel
+    rng = np.random.default_rng(105)
+    cp = sc.random_small(rng, 4, n_max=6, l_max=30)
+    g, k, M, N = 6, 3, 3, cp.n_seq
+    for world in (3, 5):
+        for rank in range(world):
+            C = torch.zeros((M + 1, N, N), dtype=torch.int64, device="cuda")
+            plan = gk.Plan(cp.sigma, g, k, M)
+            plan.set_shard(rank, world)
+            plan.accumulate(cp.codes if cp.codes.size else np.zeros(1, np.uint8), cp.offsets, N, C)
+            plan.close()
+            ref = _partial_C(cp, g, M, parallel.shard_masks(g, M, rank, world))
+            assert np.array_equal(C.cpu().numpy(), ref)
+
+
 def test_host_buffers_e2e(gk, oracle_lib):
     """Host (pinned) inputs and host outputs through gakco_kernel (the e2e path)."""
     cp = sc.make("tiny")

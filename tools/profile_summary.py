@@ -1,0 +1,126 @@
+"""Summarise ncu outputs into profiles/ (run here, on the CPU box).
+
+    python tools/profile_summary.py --launches gpurun_out/launches.csv \
+        --report gpurun_out/prof.ncu-rep --tag r01_dna --config dna
+
+Writes profiles/<tag>_launches.md (per-kernel launch count, summed device time
+and share of the step, from the `--metrics gpu__time_duration.sum` pass) and
+profiles/<tag>_ncu.md (per-launch duration, DRAM bytes, throughputs from the
+`--set full` capture), and merges per-stage DRAM traffic into
+profiles/ncu_traffic.json (read by bench.py for roofline.traffic).
+"""
+import argparse
+import collections
+import csv
+import io
+import json
+import os
+import subprocess
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+STAGE = {"encode_kernel": "encode", "radix_hist_kernel": "sort", "radix_scatter_kernel": "sort",
+         "onesweep_kernel": "sort", "segment_kernel": "segment", "light_kernel": "light",
+         "gram_kernel": "heavy", "dense_reset_kernel": "heavy", "fill_reset_kernel": "heavy",
+         "epilogue_kernel": "epilogue", "kdiag_kernel": "epilogue",
+         "diag_closed_form_kernel": "light", "gmer_index_kernel": "encode",
+         "check_codes_kernel": "encode"}
+
+
+def short(name):
+    n = name.split("(")[0].strip()
+    n = n.split("::")[-1]
+    return n.split("<")[0]
+
+
+def launches(path, tag, out_dir):
+    text = open(path).read()
+    i = text.find('"ID"')
+    rows = list(csv.reader(io.StringIO(text[i:])))
+    hdr = rows[0]
+    ki, vi, ui = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Metric Unit")
+    per = collections.OrderedDict()
+    total = 0.0
+    for r in rows[1:]:
+        if len(r) <= vi:
+            continue
+        try:
+            v = float(r[vi].replace(",", ""))
+        except ValueError:
+            continue
+        unit = r[ui]
+        us = v / 1e3 if unit == "nsecond" else (v * 1e3 if unit == "msecond" else v)
+        k = short(r[ki])
+        c = per.setdefault(k, [0, 0.0])
+        c[0] += 1
+        c[1] += us
+        total += us
+    lines = [f"# {tag}: kernel launch list (ncu gpu__time_duration.sum, --clock-control none)",
+             "", "Cold-cache, serialised replay: compare SHARES, not absolute times.", "",
+             "| kernel | stage | launches | sum (us) | share |", "|---|---|---|---|---|"]
+    for k, (n, us) in sorted(per.items(), key=lambda kv: -kv[1][1]):
+        lines.append(f"| {k} | {STAGE.get(k, 'torch/other')} | {n} | {us:.1f} | "
+                     f"{100 * us / total:.1f}% |")
+    lines.append(f"| **total** | | {sum(n for n, _ in per.values())} | {total:.1f} | 100% |")
+    with open(os.path.join(out_dir, f"{tag}_launches.md"), "w") as f:
+        f.write("\n".join(lines) + "\n")
+    return per
+
+
+METRICS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
+           "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
+           "sm__throughput.avg.pct_of_peak_sustained_elapsed",
+           "lts__t_sectors.sum.pct_of_peak_sustained_elapsed",
+           "sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed",
+           "sm__warps_active.avg.pct_of_peak_sustained_active", "launch__grid_size",
+           "launch__registers_per_thread"]
+
+
+def report(path, tag, config, out_dir):
+    raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv", "--metrics",
+                          ",".join(METRICS)], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(raw)))
+    hdr, units = rows[0], rows[1]
+    idx = {h: i for i, h in enumerate(hdr)}
+    lines = [f"# {tag}: ncu --set full capture (per launch)", "",
+             "| kernel | " + " | ".join(f"{m.split('.')[0]} [{units[idx[m]]}]"
+                                        for m in METRICS if m in idx) + " |",
+             "|---|" + "---|" * sum(1 for m in METRICS if m in idx)]
+    traffic = {}
+    for r in rows[2:]:
+        k = short(r[idx["Kernel Name"]])
+        lines.append(f"| {k} | " + " | ".join(r[idx[m]] for m in METRICS if m in idx) + " |")
+        try:
+            mult = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+            rb = float(r[idx["dram__bytes_read.sum"]]) * mult[units[idx["dram__bytes_read.sum"]]]
+            wb = float(r[idx["dram__bytes_write.sum"]]) * mult[units[idx["dram__bytes_write.sum"]]]
+            traffic.setdefault(STAGE.get(k, k), []).append(rb + wb)
+        except (KeyError, ValueError):
+            pass
+    with open(os.path.join(out_dir, f"{tag}_ncu.md"), "w") as f:
+        f.write("\n".join(lines) + "\n")
+    tp = os.path.join(out_dir, "ncu_traffic.json")
+    allt = json.load(open(tp)) if os.path.exists(tp) else {}
+    allt.setdefault(config, {})
+    for st, v in traffic.items():
+        allt[config][st] = {"dram_bytes_per_launch_mean": sum(v) / len(v), "launches": len(v),
+                            "source": os.path.basename(path)}
+    json.dump(allt, open(tp, "w"), indent=1)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--launches")
+    ap.add_argument("--report")
+    ap.add_argument("--tag", required=True)
+    ap.add_argument("--config", default="dna")
+    a = ap.parse_args()
+    out = os.path.join(ROOT, "profiles")
+    os.makedirs(out, exist_ok=True)
+    if a.launches:
+        launches(a.launches, a.tag, out)
+    if a.report:
+        report(a.report, a.tag, a.config, out)
+
+
+if __name__ == "__main__":
+    main()
