@@ -29,64 +29,96 @@ __global__ void __launch_bounds__(256) light_kernel(SegmentOut so, int64_t heavy
     const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
     const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
     unsigned long long pairs = 0, nheavy = 0;
-    for (uint64_t gi = warp; gi < G; gi += nwarps) {
-        const uint32_t a0 = so.gstart[gi], b0 = so.gstart[gi + 1];
-        const uint32_t s = b0 - a0;
-        if ((int64_t)s >= heavy_min) {
-            // dense tensor-core path if every count fits the u8 operand
-            uint32_t cmax = 0;
-            for (uint32_t t = a0 + lane; t < b0; t += 32) cmax = max(cmax, so.tcnt[t]);
-            cmax = __reduce_max_sync(0xffffffffu, cmax);
-            if (cmax <= 255u) {
-                // claim a column of the dense count matrix D and scatter the counts
-                uint32_t col = 0;
-                if (lane == 0) col = atomicAdd(dense_fill, 1u);
-                col = __shfl_sync(0xffffffffu, col, 0);
-                if (col < ldd) {  // (a full D falls back to pair updates below)
-                    // D is stored as slabs of 128 columns: [col/128][row][col%128], so
-                    // the 128 groups of a slab write into the same 128-byte lines
-                    uint8_t* slab = dense + (uint64_t)(col >> 7) * (uint64_t)n_pad * 128u +
-                                    (col & 127u);
-                    for (uint32_t t = a0 + lane; t < b0; t += 32)
-                        slab[(uint64_t)(so.tseq[t] & 0x7fffffffu) * 128u] = (uint8_t)so.tcnt[t];
-                    ++nheavy;
-                    continue;
+    // A warp takes 32 consecutive groups at a time: one coalesced load brings all
+    // their bounds (gstart[G] == T closes the last group), and the first 32
+    // triples of the next group are loaded while the current one is processed.
+    for (uint64_t base = warp * 32; base < G; base += nwarps * 32) {
+        const uint32_t ng = (uint32_t)min((uint64_t)32, (uint64_t)G - base);
+        const uint32_t my_start = lane <= ng ? so.gstart[base + lane] : 0u;
+        const uint32_t last_end = __shfl_sync(0xffffffffu, my_start, ng);  // lane ng (<= 32)
+        const uint32_t my_end_lo = __shfl_down_sync(0xffffffffu, my_start, 1);
+        const uint32_t ge31 = (ng == 32) ? so.gstart[base + 32] : last_end;
+        const uint32_t my_end = lane == 31 ? ge31 : my_end_lo;
+        // prefetch group 0's first chunk
+        uint32_t pa0 = __shfl_sync(0xffffffffu, my_start, 0);
+        uint32_t pb0 = __shfl_sync(0xffffffffu, my_end, 0);
+        uint32_t pX = 0, pC = 0;
+        if (pa0 + lane < pb0) {
+            pX = so.tseq[pa0 + lane] & 0x7fffffffu;
+            pC = so.tcnt[pa0 + lane];
+        }
+        for (uint32_t j = 0; j < ng; ++j) {
+            const uint32_t a0 = pa0, b0 = pb0;
+            const uint32_t xA0 = pX, cA0 = pC;
+            if (j + 1 < ng) {  // prefetch the next group's first chunk
+                pa0 = __shfl_sync(0xffffffffu, my_start, j + 1);
+                pb0 = __shfl_sync(0xffffffffu, my_end, j + 1);
+                pX = pC = 0;
+                if (pa0 + lane < pb0) {
+                    pX = so.tseq[pa0 + lane] & 0x7fffffffu;
+                    pC = so.tcnt[pa0 + lane];
                 }
             }
-        }
-        pairs += (unsigned long long)s * (s - 1) / 2;
-        // the group's triples in 32-wide register chunks; pairs enumerated
-        // lane-parallel: within a chunk through the triangle table, across chunks
-        // as full 32 x 32 blocks (every lane busy on every atomic)
-        for (uint32_t A = a0; A < b0; A += 32) {
-            const uint32_t ia = A + lane;
-            const uint32_t xA = ia < b0 ? (so.tseq[ia] & 0x7fffffffu) : 0u;
-            const uint32_t cA = ia < b0 ? so.tcnt[ia] : 0u;
-            const uint32_t na = min(32u, b0 - A);
-            const uint32_t P = na * (na - 1) / 2;
-            for (uint32_t q0 = 0; q0 < P; q0 += 32) {
-                const uint32_t q = q0 + lane;
-                const uint32_t ab = q < P ? s_tri[q] : 0u;
-                const int a = ab & 31, b = ab >> 5;
-                const uint32_t xa = __shfl_sync(0xffffffffu, xA, a);
-                const uint32_t ca = __shfl_sync(0xffffffffu, cA, a);
-                const uint32_t xb = __shfl_sync(0xffffffffu, xA, b);
-                const uint32_t cb = __shfl_sync(0xffffffffu, cA, b);
-                if (q < P)
-                    atomicAdd((unsigned long long*)&Cm[(int64_t)xa * N + xb],
-                              (unsigned long long)ca * cb);
+            const uint32_t s = b0 - a0;
+            if ((int64_t)s >= heavy_min) {
+                // dense tensor-core path if every count fits the u8 operand
+                uint32_t cmax = cA0;
+                for (uint32_t t = a0 + 32 + lane; t < b0; t += 32) cmax = max(cmax, so.tcnt[t]);
+                cmax = __reduce_max_sync(0xffffffffu, cmax);
+                if (cmax <= 255u) {
+                    // claim a column of the dense count matrix D and scatter the counts
+                    uint32_t col = 0;
+                    if (lane == 0) col = atomicAdd(dense_fill, 1u);
+                    col = __shfl_sync(0xffffffffu, col, 0);
+                    if (col < ldd) {  // (a full D falls back to pair updates below)
+                        // D is stored as slabs of 128 columns: [col/128][row][col%128],
+                        // so the 128 groups of a slab write into the same 128-byte lines
+                        uint8_t* slab = dense + (uint64_t)(col >> 7) * n_pad * 128u + (col & 127u);
+                        if (lane < s) slab[(uint64_t)xA0 * 128u] = (uint8_t)cA0;
+                        for (uint32_t t = a0 + 32 + lane; t < b0; t += 32)
+                            slab[(uint64_t)(so.tseq[t] & 0x7fffffffu) * 128u] = (uint8_t)so.tcnt[t];
+                        ++nheavy;
+                        continue;
+                    }
+                }
             }
-            for (uint32_t B = A + 32; B < b0; B += 32) {
-                const uint32_t ib = B + lane;
-                const bool vb = ib < b0;
-                const uint32_t xB = vb ? (so.tseq[ib] & 0x7fffffffu) : 0u;
-                const uint32_t cB = vb ? so.tcnt[ib] : 0u;
-                for (uint32_t a = 0; a < na; ++a) {
+            pairs += (unsigned long long)s * (s - 1) / 2;
+            // the group's triples in 32-wide register chunks; pairs enumerated
+            // lane-parallel: within a chunk through the triangle table, across
+            // chunks as full 32 x 32 blocks (every lane busy on every atomic)
+            for (uint32_t A = a0; A < b0; A += 32) {
+                uint32_t xA = xA0, cA = cA0;
+                if (A != a0) {
+                    const uint32_t ia = A + lane;
+                    xA = ia < b0 ? (so.tseq[ia] & 0x7fffffffu) : 0u;
+                    cA = ia < b0 ? so.tcnt[ia] : 0u;
+                }
+                const uint32_t na = min(32u, b0 - A);
+                const uint32_t P = na * (na - 1) / 2;
+                for (uint32_t q0 = 0; q0 < P; q0 += 32) {
+                    const uint32_t q = q0 + lane;
+                    const uint32_t ab = q < P ? s_tri[q] : 0u;
+                    const int a = ab & 31, b = ab >> 5;
                     const uint32_t xa = __shfl_sync(0xffffffffu, xA, a);
                     const uint32_t ca = __shfl_sync(0xffffffffu, cA, a);
-                    if (vb)
-                        atomicAdd((unsigned long long*)&Cm[(int64_t)xa * N + xB],
-                                  (unsigned long long)ca * cB);
+                    const uint32_t xb = __shfl_sync(0xffffffffu, xA, b);
+                    const uint32_t cb = __shfl_sync(0xffffffffu, cA, b);
+                    if (q < P)
+                        atomicAdd((unsigned long long*)&Cm[(int64_t)xa * N + xb],
+                                  (unsigned long long)ca * cb);
+                }
+                for (uint32_t B = A + 32; B < b0; B += 32) {
+                    const uint32_t ib = B + lane;
+                    const bool vb = ib < b0;
+                    const uint32_t xB = vb ? (so.tseq[ib] & 0x7fffffffu) : 0u;
+                    const uint32_t cB = vb ? so.tcnt[ib] : 0u;
+                    for (uint32_t a = 0; a < na; ++a) {
+                        const uint32_t xa = __shfl_sync(0xffffffffu, xA, a);
+                        const uint32_t ca = __shfl_sync(0xffffffffu, cA, a);
+                        if (vb)
+                            atomicAdd((unsigned long long*)&Cm[(int64_t)xa * N + xB],
+                                      (unsigned long long)ca * cB);
+                    }
                 }
             }
         }
@@ -100,7 +132,7 @@ cudaError_t launch_light(SegmentOut so, uint64_t max_groups, int64_t heavy_min, 
                          uint32_t* dense_fill,
                          unsigned long long* stats, int sm_count, cudaStream_t s) {
     if (max_groups == 0) return cudaGetLastError();
-    uint64_t blocks = (max_groups + 7) / 8;
+    uint64_t blocks = (max_groups + 255) / 256;  // 8 warps x 32 groups per block-round
     uint64_t cap = (uint64_t)sm_count * 8;
     if (blocks > cap) blocks = cap;
     light_kernel<<<(unsigned)blocks, 256, 0, s>>>(so, heavy_min, N, Cm, dense, ldd, n_pad,

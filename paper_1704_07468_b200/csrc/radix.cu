@@ -230,7 +230,9 @@ __global__ void __launch_bounds__(RS_THREADS) radix_scatter_kernel(
     uint32_t(*s_whist)[RADIX] = (uint32_t(*)[RADIX])(s_run + RADIX);     // [WARPS][RADIX]
     uint32_t* s_doff = &s_whist[RS_WARPS][0];                            // [RADIX]
     uint32_t* s_cnt = s_doff + RADIX;                                    // [RADIX]
-    uint32_t* s_w = s_cnt + RADIX;                                       // [8]
+    uint32_t* s_w = s_cnt + RADIX;                                       // [16]
+    uint32_t* s_match = s_w + 16;                                        // [WARPS][RADIX]
+    for (int i = threadIdx.x; i < RS_WARPS * RADIX; i += RS_THREADS) s_match[i] = 0u;
 
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
     const uint32_t seg = blockIdx.x / cps, c = blockIdx.x - seg * cps;
@@ -281,16 +283,24 @@ __global__ void __launch_bounds__(RS_THREADS) radix_scatter_kernel(
                 nxt[i] = idx < cnt1 ? in[seg_base + t1 + idx] : 0ull;
             }
         }
+        // stable in-warp ranking: lanes with the same digit find each other with a
+        // shared-memory atomicOr of their lane bit (one ATOMS per key), the
+        // lowest peer advances the warp's digit counter and clears the bin
+        uint32_t* mbin = s_match + w * RADIX;
 #pragma unroll
         for (int i = 0; i < SORT_ITEMS; ++i) {
             const uint32_t idx = w * SORT_ITEMS * 32 + i * 32 + lane;
             const bool valid = idx < cnt;
             const uint32_t d = (uint32_t)(keys[i] >> shift) & 0xffu;
-            const uint32_t vmask = __ballot_sync(0xffffffffu, valid);
-            const uint32_t peers = digit_peers(d, vmask);
+            if (valid) atomicOr(&mbin[d], 1u << lane);
+            __syncwarp();
+            const uint32_t peers = valid ? mbin[d] : 0u;
             const uint32_t prior = valid ? s_whist[w][d] : 0u;
             __syncwarp();
-            if (valid && lane == __ffs(peers) - 1) s_whist[w][d] = prior + __popc(peers);
+            if (valid && lane == __ffs(peers) - 1) {
+                s_whist[w][d] = prior + __popc(peers);
+                mbin[d] = 0u;
+            }
             __syncwarp();
             rank[i] = prior + __popc(peers & lt);
         }
@@ -329,7 +339,8 @@ __global__ void __launch_bounds__(RS_THREADS) radix_scatter_kernel(
     }
 }
 
-constexpr size_t RS_SMEM = SORT_TILE * 8 + RADIX * 8 + RS_WARPS * RADIX * 4 + 2 * RADIX * 4 + 16 * 4;
+constexpr size_t RS_SMEM = SORT_TILE * 8 + RADIX * 8 + 2 * RS_WARPS * RADIX * 4 +
+                           2 * RADIX * 4 + 16 * 4;
 
 cudaError_t launch_radix_chunked(const uint64_t* in, uint64_t* out, uint64_t n, int nseg,
                                  int shift, uint32_t* hist, int target_ctas, cudaStream_t s) {

@@ -48,7 +48,8 @@ def launches(path, tag, out_dir):
         except ValueError:
             continue
         unit = r[ui]
-        us = v / 1e3 if unit == "nsecond" else (v * 1e3 if unit == "msecond" else v)
+        us = (v / 1e3 if unit in ("ns", "nsecond") else
+              v * 1e3 if unit in ("ms", "msecond") else v)
         k = short(r[ki])
         c = per.setdefault(k, [0, 0.0])
         c[0] += 1
