@@ -177,9 +177,12 @@ cudaError_t launch_segment(const uint64_t* keys, uint64_t n, int nseg, int sb, i
 // matrix D (u8, slabs of 128 columns: byte (c/128)*n_pad*128 + row*128 + c%128)
 // and scatters its counts there, for the tensor-core Gram.
 cudaError_t launch_light(SegmentOut so, uint64_t max_groups, int64_t heavy_min, int64_t N,
-                         int64_t* Cm, uint8_t* dense, uint64_t ldd, uint64_t n_pad,
+                         uint32_t* acc, uint8_t* dense, uint64_t ldd, uint64_t n_pad,
                          uint32_t* dense_fill, unsigned long long* stats, int sm_count,
                          cudaStream_t s);
+// acc: u32 strictly-upper packed triangle (N(N-1)/2); flush adds it into C_m, zeroes it.
+cudaError_t launch_light_flush(uint32_t* acc, int64_t N, int64_t* Cm, int sm_count,
+                               cudaStream_t s);
 // Heavy path (gram_tc.cu): C_m += D D^T over the *dense_fill filled columns
 // (count read on the device), then the used columns are zeroed and the fill reset.
 std::vector<int2> gram_tiles(int64_t n_pad);

@@ -4,7 +4,10 @@
 // For a group (one masked key) whose sorted triples are (X_1,c_1) < ... < (X_s,c_s),
 // every unordered pair a < b adds c_a*c_b to C_m(X_a, X_b) — the upper triangle,
 // since X_a < X_b; the epilogue mirrors it (reading A4). Integer adds
-// commute, so the atomic update order never changes the result.
+// commute, so the atomic update order never changes the result. The adds go to
+// a u32 strictly-upper packed accumulator (half the footprint of int64 rows, L2
+// resident for N <= ~5500) that light_flush adds into C_m; the host flushes
+// before masks * n_max^2 could reach 2^32 (per mask an entry grows <= n_X n_Y).
 //
 // One warp per group; its triples are held in registers 32 at a time and the
 // pairs are spread over the lanes (triangle table within a chunk, full 32 x 32
@@ -13,8 +16,13 @@
 
 namespace gk {
 
+// Strictly-upper packed index of (x, y), x < y: rows of N-1, N-2, ... entries.
+__device__ __forceinline__ uint64_t tri_index(uint32_t x, uint32_t y, int64_t N) {
+    return (uint64_t)x * (uint64_t)(N - 1) - (uint64_t)x * (x - 1) / 2 + (y - x - 1);
+}
+
 __global__ void __launch_bounds__(256) light_kernel(SegmentOut so, int64_t heavy_min, int64_t N,
-                                                    int64_t* Cm, uint8_t* dense, uint64_t ldd,
+                                                    uint32_t* acc, uint8_t* dense, uint64_t ldd,
                                                     uint64_t n_pad, uint32_t* dense_fill,
                                                     unsigned long long* stats) {
     // triangle table: pairs (a < b < 32) ordered by b, so the first n(n-1)/2
@@ -103,9 +111,7 @@ __global__ void __launch_bounds__(256) light_kernel(SegmentOut so, int64_t heavy
                     const uint32_t ca = __shfl_sync(0xffffffffu, cA, a);
                     const uint32_t xb = __shfl_sync(0xffffffffu, xA, b);
                     const uint32_t cb = __shfl_sync(0xffffffffu, cA, b);
-                    if (q < P)
-                        atomicAdd((unsigned long long*)&Cm[(int64_t)xa * N + xb],
-                                  (unsigned long long)ca * cb);
+                    if (q < P) atomicAdd(&acc[tri_index(xa, xb, N)], ca * cb);
                 }
                 for (uint32_t B = A + 32; B < b0; B += 32) {
                     const uint32_t ib = B + lane;
@@ -115,9 +121,7 @@ __global__ void __launch_bounds__(256) light_kernel(SegmentOut so, int64_t heavy
                     for (uint32_t a = 0; a < na; ++a) {
                         const uint32_t xa = __shfl_sync(0xffffffffu, xA, a);
                         const uint32_t ca = __shfl_sync(0xffffffffu, cA, a);
-                        if (vb)
-                            atomicAdd((unsigned long long*)&Cm[(int64_t)xa * N + xB],
-                                      (unsigned long long)ca * cB);
+                        if (vb) atomicAdd(&acc[tri_index(xa, xB, N)], ca * cB);
                     }
                 }
             }
@@ -128,16 +132,40 @@ __global__ void __launch_bounds__(256) light_kernel(SegmentOut so, int64_t heavy
 }
 
 cudaError_t launch_light(SegmentOut so, uint64_t max_groups, int64_t heavy_min, int64_t N,
-                         int64_t* Cm, uint8_t* dense, uint64_t ldd, uint64_t n_pad,
+                         uint32_t* acc, uint8_t* dense, uint64_t ldd, uint64_t n_pad,
                          uint32_t* dense_fill,
                          unsigned long long* stats, int sm_count, cudaStream_t s) {
     if (max_groups == 0) return cudaGetLastError();
     uint64_t blocks = (max_groups + 255) / 256;  // 8 warps x 32 groups per block-round
     uint64_t cap = (uint64_t)sm_count * 8;
     if (blocks > cap) blocks = cap;
-    light_kernel<<<(unsigned)blocks, 256, 0, s>>>(so, heavy_min, N, Cm, dense, ldd, n_pad,
+    light_kernel<<<(unsigned)blocks, 256, 0, s>>>(so, heavy_min, N, acc, dense, ldd, n_pad,
                                                   dense_fill,
                                                   stats);
+    return cudaGetLastError();
+}
+
+// C_m(X,Y) += acc[(X,Y)] for every X < Y, and acc is zeroed again (one pass over
+// the packed triangle; rows of C are read-modify-written contiguously).
+__global__ void light_flush_kernel(uint32_t* __restrict__ acc, int64_t N, int64_t* __restrict__ Cm) {
+    for (int64_t x = blockIdx.x; x < N - 1; x += gridDim.x) {
+        uint32_t* row = acc + tri_index((uint32_t)x, (uint32_t)x + 1, N);
+        int64_t* crow = Cm + x * N;
+        for (int64_t y = x + 1 + threadIdx.x; y < N; y += blockDim.x) {
+            const uint32_t v = row[y - x - 1];
+            if (v) {
+                crow[y] += v;
+                row[y - x - 1] = 0u;
+            }
+        }
+    }
+}
+
+cudaError_t launch_light_flush(uint32_t* acc, int64_t N, int64_t* Cm, int sm_count,
+                               cudaStream_t s) {
+    if (N < 2) return cudaGetLastError();
+    int64_t blocks = N - 1 < (int64_t)sm_count * 16 ? N - 1 : (int64_t)sm_count * 16;
+    light_flush_kernel<<<(unsigned)blocks, 256, 0, s>>>(acc, N, Cm);
     return cudaGetLastError();
 }
 

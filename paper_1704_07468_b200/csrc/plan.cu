@@ -86,7 +86,8 @@ struct gakco_plan {
     std::vector<int> key_bits;  // per level
 
     DevBuf codes, off, gofs, gmseq, keysA, keysB, hist, status, ctr, tseq, tcnt, gstart, gend,
-        counts, kept, stats, flags, kdiag, Cscr, Nmscr, Kscr, Knscr, heavy, hcount, dense, tiles;
+        counts, kept, stats, flags, kdiag, Cscr, Nmscr, Kscr, Knscr, heavy, hcount, dense, tiles,
+        lightacc;
     int64_t tiles_npad = -1;
     uint64_t dense_ldd = 0;
     int ntiles = 0;
@@ -242,7 +243,7 @@ extern "C" void gakco_destroy(gakco_plan* p) {
                       &p->hist,  &p->status, &p->ctr,  &p->tseq,   &p->tcnt,  &p->gstart,
                       &p->gend,  &p->counts, &p->kept, &p->stats,  &p->flags, &p->kdiag,
                       &p->Cscr,  &p->Nmscr, &p->Kscr,  &p->Knscr, &p->heavy, &p->hcount,
-                      &p->dense, &p->tiles};
+                      &p->dense, &p->tiles, &p->lightacc};
     for (DevBuf* b : bufs)
         if (b->p) cudaFree(b->p);
     for (cudaEvent_t e : p->ev_pool) cudaEventDestroy(e);
@@ -343,6 +344,8 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
         if (nn * (unsigned __int128)binom64(g, p->k) > (unsigned __int128)INT64_MAX)
             return p->fail(GAKCO_E_RANGE, "K may overflow int64");
     }
+    if ((uint64_t)nmax * (uint64_t)nmax > (uint64_t)UINT32_MAX)
+        return p->fail(GAKCO_E_RANGE, "a sequence has more than 65535 g-mers (u32 pair sums)");
     const int sb = (N <= 1) ? 0 : 64 - __builtin_clzll((unsigned long long)(N - 1));
     for (int m = 0; m <= M; ++m)
         if (p->key_bits[m] + sb > 64)
@@ -486,6 +489,24 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
         dense_masks = 0;
         return GAKCO_OK;
     };
+    // Light updates accumulate in a u32 packed strictly-upper triangle, added into
+    // C_m at a level change or before masks * n_max^2 could reach 2^32.
+    const uint64_t ntri = (uint64_t)N * (uint64_t)(N - 1) / 2;
+    CK(p->ensure(p->lightacc, ntri * 4 + 16, s, /*zero=*/true));
+    uint64_t light_masks = 0;
+    int light_m = -1;
+    const uint64_t light_lim =
+        nmax > 0 ? std::max<uint64_t>(1, (uint64_t)UINT32_MAX / ((uint64_t)nmax * nmax)) : 1;
+    auto lflush = [&]() -> gakco_status {
+        if (light_m < 0 || light_masks == 0) return GAKCO_OK;
+        cudaEvent_t al = nullptr;
+        p->stage_begin(s, &al);
+        LK(launch_light_flush((uint32_t*)p->lightacc.p, N, C + (size_t)light_m * nn, p->sm_count,
+                              s));
+        p->stage_end(s, S_LIGHT, al);
+        light_masks = 0;
+        return GAKCO_OK;
+    };
 
     size_t pos = 0;
     while (pos < mine.size()) {
@@ -506,6 +527,14 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
             dense_m = m;
             dense_bound += bnd;
             dense_masks += nmask;
+        }
+        if (n > 0) {
+            if (light_m != m || light_masks + nmask > light_lim) {
+                gakco_status fs = lflush();
+                if (fs != GAKCO_OK) return fs;
+            }
+            light_m = m;
+            light_masks += nmask;
         }
 
         if (n > 0) {
@@ -546,7 +575,8 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
             p->stage_end(s, S_SEGMENT, a);
 
             p->stage_begin(s, &a);
-            LK(launch_light(so, n * nmask / 2 + 1, light_limit, N, Cm, (uint8_t*)p->dense.p,
+            LK(launch_light(so, n * nmask / 2 + 1, light_limit, N, (uint32_t*)p->lightacc.p,
+                            (uint8_t*)p->dense.p,
                             rcap, (uint64_t)n_pad, (uint32_t*)p->hcount.p, stats, p->sm_count,
                             s));
             p->stage_end(s, S_LIGHT, a);
@@ -556,6 +586,8 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
     }
     {
         gakco_status fs = flush();
+        if (fs != GAKCO_OK) return fs;
+        fs = lflush();
         if (fs != GAKCO_OK) return fs;
     }
     p->last_masks = (int64_t)mine.size();
