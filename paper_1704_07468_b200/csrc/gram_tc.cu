@@ -322,24 +322,99 @@ __global__ void __launch_bounds__(GT_THREADS, 1)
     }
 }
 
-// ---------------------------------------------------------------- D reset
-// Zero the used columns [0, round_up(fill,128)) of every row, then reset fill:
-// D is all-zero again for the next accumulation.
-__global__ void dense_reset_kernel(uint8_t* __restrict__ D, int64_t n_pad, uint64_t ldd,
-                                   const uint32_t* fill) {
-    // the used slabs [0, ceil(fill/128)) are one contiguous range of bytes
-    const uint64_t slabs = (min((uint64_t)*fill, ldd) + GT_KB - 1) / GT_KB;
-    const uint64_t total = slabs * (uint64_t)n_pad * GT_KB / 16;  // 16-byte stores
-    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total;
-         i += (uint64_t)gridDim.x * blockDim.x)
-        ((uint4*)D)[i] = make_uint4(0, 0, 0, 0);
+// ---------------------------------------------------------------- D build
+// A slab = 128 columns (groups) x n_pad rows, stored [row][128 B]. One CTA builds
+// BD_ROWS rows of one slab in shared memory (zero, scatter the groups' counts for
+// the rows in range, then 16-byte coalesced stores), so D is written once with
+// full lines and never needs a separate zeroing pass. Columns [prev, fill) are
+// this batch's (prev = fill[1], a multiple of 128); unused columns of the last
+// slab are written as zeros.
+// Work item = 32 columns (a quarter slab) x up to BD_ROWS rows: every group's
+// triples are read once, and each row's 32 bytes go out as two 16-byte stores
+// (whole 32-byte sectors at a 128-byte stride).
+constexpr int BD_ROWS = 2048;
+constexpr int BD_COLS = 32;
+constexpr int BD_STRIDE = 32;  // smem row stride (40 to spread banks measured slower)
+constexpr int BD_THREADS = 512;
+
+__global__ void __launch_bounds__(BD_THREADS) build_dense_kernel(
+    SegmentOut so, const uint2* __restrict__ heavy_list, const uint32_t* fill,
+    uint8_t* __restrict__ D, int64_t n_pad, uint64_t ldd) {
+    extern __shared__ __align__(16) unsigned char sb[];  // [BD_ROWS][BD_COLS]
+    const uint64_t f0 = fill[1];
+    const uint64_t f1 = min((uint64_t)fill[0], ldd);
+    if (f1 <= f0) return;
+    // quarter slabs of every slab this batch touches (whole slabs, so columns up
+    // to the next multiple of 128 are written as zeros, never left stale)
+    const uint64_t q0 = f0 / BD_COLS, q1 = (f1 + GT_KB - 1) / GT_KB * (GT_KB / BD_COLS);
+    const uint64_t nchunks = (uint64_t)(n_pad + BD_ROWS - 1) / BD_ROWS;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (uint64_t wk = blockIdx.x; wk < (q1 - q0) * nchunks; wk += gridDim.x) {
+        const uint64_t qs = q0 + wk / nchunks;
+        const int64_t r0 = (int64_t)(wk % nchunks) * BD_ROWS;
+        const int64_t rows = min((int64_t)BD_ROWS, n_pad - r0);
+        for (int i = threadIdx.x; i < rows * BD_STRIDE / 8; i += BD_THREADS)
+            ((uint64_t*)sb)[i] = 0ull;
+        __syncthreads();
+        // warp w fills columns w and w + 16 of the quarter slab
+        uint2 bnd[BD_COLS * 32 / BD_THREADS];
+#pragma unroll
+        for (int k = 0; k < BD_COLS * 32 / BD_THREADS; ++k) {
+            const uint64_t col = qs * BD_COLS + warp + k * (BD_THREADS / 32);
+            bnd[k] = col < f1 ? heavy_list[col] : make_uint2(0, 0);
+        }
+#pragma unroll
+        for (int k = 0; k < BD_COLS * 32 / BD_THREADS; ++k) {
+            const int c = warp + k * (BD_THREADS / 32);
+            for (uint32_t t = bnd[k].x + lane; t < bnd[k].y; t += 32) {
+                const int64_t x = (int64_t)(so.tseq[t] & 0x7fffffffu) - r0;
+                if (x >= 0 && x < rows) sb[x * BD_STRIDE + c] = (uint8_t)so.tcnt[t];
+            }
+        }
+        __syncthreads();
+        // row r of the quarter slab -> D + (slab*n_pad + r0 + r)*128 + quarter*32
+        const uint64_t slab = qs / (GT_KB / BD_COLS), quarter = qs % (GT_KB / BD_COLS);
+        uint8_t* dst = D + (slab * (uint64_t)n_pad + (uint64_t)r0) * GT_KB + quarter * BD_COLS;
+        for (int i = threadIdx.x; i < rows * 2; i += BD_THREADS) {
+            const int r = i >> 1, h = i & 1;
+            const uint64_t* src = (const uint64_t*)(sb + r * BD_STRIDE + h * 16);
+            const uint64_t lo = src[0], hi = src[1];
+            *(uint4*)(dst + (uint64_t)r * GT_KB + h * 16) =
+                make_uint4((uint32_t)lo, (uint32_t)(lo >> 32), (uint32_t)hi, (uint32_t)(hi >> 32));
+        }
+        __syncthreads();
+    }
 }
 
+// After a batch's build: fill rounded up to whole slabs; the next batch starts there.
+__global__ void fill_round_kernel(uint32_t* fill, uint64_t ldd) {
+    uint64_t f = min((uint64_t)fill[0], ldd);
+    f = min((f + GT_KB - 1) / GT_KB * GT_KB, ldd);
+    fill[0] = (uint32_t)f;
+    fill[1] = (uint32_t)f;
+}
+
+// After a Gram flush: count the issued MACs and reset the fill.
 __global__ void fill_reset_kernel(uint32_t* fill, uint64_t ldd, uint64_t tile_macs,
                                   unsigned long long* stats) {
-    const uint64_t k = (min((uint64_t)*fill, ldd) + GT_KB - 1) / GT_KB * GT_KB;
+    const uint64_t k = (min((uint64_t)fill[0], ldd) + GT_KB - 1) / GT_KB * GT_KB;
     atomicAdd(&stats[ST_HEAVY_MACS], (unsigned long long)(tile_macs * k));
-    *fill = 0;
+    fill[0] = 0;
+    fill[1] = 0;
+}
+
+cudaError_t launch_build_dense(SegmentOut so, const uint2* heavy_list, uint32_t* dense_fill,
+                               uint8_t* D, int64_t n_pad, uint64_t ldd, int sm_count,
+                               cudaStream_t s) {
+    const size_t smem = (size_t)BD_ROWS * BD_STRIDE;  // 64 KB: 3 CTAs per SM
+    cudaFuncSetAttribute(build_dense_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    build_dense_kernel<<<sm_count * 3, BD_THREADS, smem, s>>>(so, heavy_list, dense_fill, D,
+                                                              n_pad, ldd);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    fill_round_kernel<<<1, 1, 0, s>>>(dense_fill, ldd);
+    return cudaGetLastError();
 }
 
 // ---------------------------------------------------------------- host side
@@ -404,9 +479,6 @@ cudaError_t launch_gram_flush(uint8_t* D, int64_t n_pad, uint64_t ldd, uint32_t*
     int grid = ntiles < sm_count ? ntiles : sm_count;
     gram_kernel<<<grid, GT_THREADS, GT_SMEM, s>>>(map, cmap, a);
     cudaError_t e = cudaGetLastError();
-    if (e != cudaSuccess) return e;
-    dense_reset_kernel<<<sm_count * 4, 256, 0, s>>>(D, n_pad, ldd, dense_fill);
-    e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     fill_reset_kernel<<<1, 1, 0, s>>>(dense_fill, ldd, (uint64_t)ntiles * GT_M * GT_N, stats);
     return cudaGetLastError();

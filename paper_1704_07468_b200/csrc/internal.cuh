@@ -177,9 +177,16 @@ cudaError_t launch_segment(const uint64_t* keys, uint64_t n, int nseg, int sb, i
 // matrix D (u8, slabs of 128 columns: byte (c/128)*n_pad*128 + row*128 + c%128)
 // and scatters its counts there, for the tensor-core Gram.
 cudaError_t launch_light(SegmentOut so, uint64_t max_groups, int64_t heavy_min, int64_t N,
-                         uint32_t* acc, uint8_t* dense, uint64_t ldd, uint64_t n_pad,
+                         uint32_t* acc, uint2* heavy_list, uint64_t ldd,
                          uint32_t* dense_fill, unsigned long long* stats, int sm_count,
                          cudaStream_t s);
+// Fill the D slabs of the columns claimed by this batch ([prev, fill) with
+// prev = dense_fill[1], a multiple of 128) from the batch's triples, in shared
+// memory, with full-line stores; then round dense_fill[0] up to a multiple of 128
+// and set dense_fill[1] = dense_fill[0].
+cudaError_t launch_build_dense(SegmentOut so, const uint2* heavy_list, uint32_t* dense_fill,
+                               uint8_t* D, int64_t n_pad, uint64_t ldd, int sm_count,
+                               cudaStream_t s);
 // acc: u32 strictly-upper packed triangle (N(N-1)/2); flush adds it into C_m, zeroes it.
 cudaError_t launch_light_flush(uint32_t* acc, int64_t N, int64_t* Cm, int sm_count,
                                cudaStream_t s);

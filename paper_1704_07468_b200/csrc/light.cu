@@ -22,8 +22,8 @@ __device__ __forceinline__ uint64_t tri_index(uint32_t x, uint32_t y, int64_t N)
 }
 
 __global__ void __launch_bounds__(256) light_kernel(SegmentOut so, int64_t heavy_min, int64_t N,
-                                                    uint32_t* acc, uint8_t* dense, uint64_t ldd,
-                                                    uint64_t n_pad, uint32_t* dense_fill,
+                                                    uint32_t* acc, uint2* heavy_list,
+                                                    uint64_t ldd, uint32_t* dense_fill,
                                                     unsigned long long* stats) {
     // triangle table: pairs (a < b < 32) ordered by b, so the first n(n-1)/2
     // entries are exactly the pairs of an n-triple chunk
@@ -74,17 +74,12 @@ __global__ void __launch_bounds__(256) light_kernel(SegmentOut so, int64_t heavy
                 for (uint32_t t = a0 + 32 + lane; t < b0; t += 32) cmax = max(cmax, so.tcnt[t]);
                 cmax = __reduce_max_sync(0xffffffffu, cmax);
                 if (cmax <= 255u) {
-                    // claim a column of the dense count matrix D and scatter the counts
+                    // claim a column of the dense count matrix D; build_dense fills it
                     uint32_t col = 0;
                     if (lane == 0) col = atomicAdd(dense_fill, 1u);
                     col = __shfl_sync(0xffffffffu, col, 0);
                     if (col < ldd) {  // (a full D falls back to pair updates below)
-                        // D is stored as slabs of 128 columns: [col/128][row][col%128],
-                        // so the 128 groups of a slab write into the same 128-byte lines
-                        uint8_t* slab = dense + (uint64_t)(col >> 7) * n_pad * 128u + (col & 127u);
-                        if (lane < s) slab[(uint64_t)xA0 * 128u] = (uint8_t)cA0;
-                        for (uint32_t t = a0 + 32 + lane; t < b0; t += 32)
-                            slab[(uint64_t)(so.tseq[t] & 0x7fffffffu) * 128u] = (uint8_t)so.tcnt[t];
+                        if (lane == 0) heavy_list[col] = make_uint2(a0, b0);
                         ++nheavy;
                         continue;
                     }
@@ -132,16 +127,15 @@ __global__ void __launch_bounds__(256) light_kernel(SegmentOut so, int64_t heavy
 }
 
 cudaError_t launch_light(SegmentOut so, uint64_t max_groups, int64_t heavy_min, int64_t N,
-                         uint32_t* acc, uint8_t* dense, uint64_t ldd, uint64_t n_pad,
-                         uint32_t* dense_fill,
-                         unsigned long long* stats, int sm_count, cudaStream_t s) {
+                         uint32_t* acc, uint2* heavy_list, uint64_t ldd,
+                         uint32_t* dense_fill, unsigned long long* stats, int sm_count,
+                         cudaStream_t s) {
     if (max_groups == 0) return cudaGetLastError();
     uint64_t blocks = (max_groups + 255) / 256;  // 8 warps x 32 groups per block-round
     uint64_t cap = (uint64_t)sm_count * 8;
     if (blocks > cap) blocks = cap;
-    light_kernel<<<(unsigned)blocks, 256, 0, s>>>(so, heavy_min, N, acc, dense, ldd, n_pad,
-                                                  dense_fill,
-                                                  stats);
+    light_kernel<<<(unsigned)blocks, 256, 0, s>>>(so, heavy_min, N, acc, heavy_list, ldd,
+                                                  dense_fill, stats);
     return cudaGetLastError();
 }
 

@@ -443,15 +443,13 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
         CK(p->ensure(p->hcount, 16, s, /*zero=*/true));
         // dense count matrix D: n_pad rows x rcap u8 columns (<= 4 GB, and no more
         // columns than heavy groups can exist), accumulated over batches of a level
-        const uint64_t most = (uint64_t)mine.size() * n / (uint64_t)heavy_min + 128;
+        // (every batch rounds its columns up to whole 128-column slabs)
+        const uint64_t most =
+            (uint64_t)mine.size() * n / (uint64_t)heavy_min + 128 * (mine.size() + 1);
         rcap = std::min<uint64_t>((4096ull << 20) / (uint64_t)n_pad, most);
         rcap = std::max<uint64_t>(128, (rcap + 127) / 128 * 128);
-        if ((size_t)n_pad * rcap > p->dense.cap) p->dense_ldd = 0;
-        CK(p->ensure(p->dense, (size_t)n_pad * rcap, s, /*zero=*/true));
-        if (p->dense_ldd != rcap) {  // new geometry: start from an all-zero buffer
-            CK(cudaMemsetAsync(p->dense.p, 0, (size_t)n_pad * rcap, s));
-            p->dense_ldd = rcap;
-        }
+        CK(p->ensure(p->dense, (size_t)n_pad * rcap, s));
+        CK(p->ensure(p->heavy, rcap * sizeof(uint2), s));
         if (p->tiles_npad != n_pad) {
             std::vector<int2> t = gram_tiles(n_pad);
             CK(p->ensure(p->tiles, t.size() * sizeof(int2), s));
@@ -480,7 +478,7 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
         if (dense_m < 0 || dense_bound == 0) return GAKCO_OK;
         cudaEvent_t ah = nullptr;
         p->stage_begin(s, &ah);
-        p->launches += 2;  // + reset kernels
+        p->launches += 1;  // + fill_reset
         LK(launch_gram_flush((uint8_t*)p->dense.p, n_pad, rcap, (uint32_t*)p->hcount.p,
                              C + (size_t)dense_m * nn, N, (const int2*)p->tiles.p, p->ntiles,
                              p->sm_count, stats, s));
@@ -519,7 +517,7 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
         int64_t* Cm = C + (size_t)m * nn;
         cudaEvent_t a = nullptr;
         if (gram_ok && n > 0) {
-            const uint64_t bnd = (uint64_t)nmask * n / (uint64_t)heavy_min + 1;
+            const uint64_t bnd = (uint64_t)nmask * n / (uint64_t)heavy_min + 128;
             if (dense_m != m || dense_bound + bnd > rcap || dense_masks + nmask > mask_lim) {
                 gakco_status fs = flush();
                 if (fs != GAKCO_OK) return fs;
@@ -576,10 +574,16 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
 
             p->stage_begin(s, &a);
             LK(launch_light(so, n * nmask / 2 + 1, light_limit, N, (uint32_t*)p->lightacc.p,
-                            (uint8_t*)p->dense.p,
-                            rcap, (uint64_t)n_pad, (uint32_t*)p->hcount.p, stats, p->sm_count,
-                            s));
+                            (uint2*)p->heavy.p, rcap, (uint32_t*)p->hcount.p, stats,
+                            p->sm_count, s));
             p->stage_end(s, S_LIGHT, a);
+            if (gram_ok) {
+                p->stage_begin(s, &a);
+                p->launches += 1;  // + fill_round
+                LK(launch_build_dense(so, (const uint2*)p->heavy.p, (uint32_t*)p->hcount.p,
+                                      (uint8_t*)p->dense.p, n_pad, rcap, p->sm_count, s));
+                p->stage_end(s, S_HEAVY, a);
+            }
         }
         LK(launch_diag_closed_form((const int64_t*)p->gofs.p, N, nmask, Cm, s));
         pos = end;
