@@ -48,6 +48,7 @@ def args_():
     ap.add_argument("--heavy-min", type=int, default=0)
     ap.add_argument("--batch-keys", type=int, default=0)
     ap.add_argument("--sort", type=int, default=None, choices=[0, 1])
+    ap.add_argument("--sort-ctas", type=int, default=0)
     ap.add_argument("--no-timing", action="store_true",
                     help="no per-stage events (roofline then uses the last timed stages)")
     return ap.parse_args()
@@ -234,6 +235,8 @@ def run_ours(a):
         plan.set_option(gakco.GAKCO_OPT_BATCH_KEYS, a.batch_keys)
     if a.sort is not None:
         plan.set_option(gakco.GAKCO_OPT_SORT, a.sort)
+    if a.sort_ctas:
+        plan.set_option(gakco.GAKCO_OPT_SORT_CTAS_PER_SM, a.sort_ctas)
     if a.no_timing:
         plan.set_option(gakco.GAKCO_OPT_TIMING, 0)
     C = torch.zeros((M + 1, N, N), dtype=torch.int64, device=dev)

@@ -62,8 +62,9 @@ typedef enum {
                                      a huge value = never (all light); 2 = all heavy */
     GAKCO_OPT_BATCH_KEYS = 2,     /* max keys (masks x g-mers) per batch; 0 = auto */
     GAKCO_OPT_TIMING = 3,         /* 1 = record per-stage CUDA events (gakco_get_stats) */
-    GAKCO_OPT_SORT = 4            /* LSD pass kernel: 0 = chunked two-kernel pass (default),
+    GAKCO_OPT_SORT = 4,           /* LSD pass kernel: 0 = chunked two-kernel pass (default),
                                      1 = onesweep with decoupled look-back */
+    GAKCO_OPT_SORT_CTAS_PER_SM = 5 /* chunked pass grid size in CTAs per SM (default 2) */
 } gakco_option;
 
 /* Counters of the last gakco_accumulate (algorithmic units). */

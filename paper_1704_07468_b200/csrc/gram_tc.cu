@@ -20,6 +20,8 @@
 #include <cuda.h>
 #include <string.h>
 
+#include <algorithm>
+
 #include "internal.cuh"
 
 namespace gk {
@@ -167,6 +169,7 @@ struct GramArgs {
     const int2* tiles;  // (row block of 128, col block of 256)
     int ntiles;
     int tma_epilogue;   // 1: TMA reduce-add into C (rows 16-byte aligned)
+    int ksplit;         // K slices per output tile
 };
 
 __global__ void __launch_bounds__(GT_THREADS, 1)
@@ -185,6 +188,10 @@ __global__ void __launch_bounds__(GT_THREADS, 1)
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int kblocks = (int)((min(*a.fill, a.cap) + GT_KB - 1) / GT_KB);  // grid-uniform
     if (kblocks == 0) return;
+    // work unit u = (tile u / ksplit, K slice u % ksplit): split-K keeps every SM
+    // busy when there are few output tiles (small N); slices add up in C
+    const int kper = (kblocks + a.ksplit - 1) / a.ksplit;
+    const int nunits = a.ntiles * a.ksplit;
     if (threadIdx.x == 0) {
         for (int s = 0; s < GT_STAGES; ++s) {
             mbar_init(&full[s], 1);
@@ -212,9 +219,10 @@ __global__ void __launch_bounds__(GT_THREADS, 1)
         if (lane == 0) {
             asm volatile("prefetch.tensormap [%0];" ::"l"((uint64_t)&dmap) : "memory");
             uint32_t stage = 0, phase = 0;
-            for (int t = blockIdx.x; t < a.ntiles; t += gridDim.x) {
-                const int2 tl = a.tiles[t];
-                for (int kb = 0; kb < kblocks; ++kb) {
+            for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
+                const int2 tl = a.tiles[u / a.ksplit];
+                const int klo = (u % a.ksplit) * kper, khi = min(kblocks, klo + kper);
+                for (int kb = klo; kb < khi; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
                     unsigned char* sa = smem + (size_t)stage * GT_STAGE_BYTES;
                     unsigned char* sbm = sa + GT_A_BYTES;
@@ -234,13 +242,16 @@ __global__ void __launch_bounds__(GT_THREADS, 1)
         if (lane == 0) {
             uint32_t stage = 0, phase = 0;
             int it = 0;
-            for (int t = blockIdx.x; t < a.ntiles; t += gridDim.x, ++it) {
+            for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
+                const int klo = (u % a.ksplit) * kper, khi = min(kblocks, klo + kper);
+                if (klo >= khi) continue;  // empty K slice: skipped by every role
                 const int acc = it & 1;
                 const uint32_t acc_phase = (it >> 1) & 1;
+                ++it;
                 mbar_wait(&tempty[acc], acc_phase ^ 1);
                 tc_fence_after();
                 const uint32_t dcol = tmem + acc * GT_N;
-                for (int kb = 0; kb < kblocks; ++kb) {
+                for (int kb = klo; kb < khi; ++kb) {
                     mbar_wait(&full[stage], phase);
                     tc_fence_after();
                     const uint32_t sa = smem_u32(smem + (size_t)stage * GT_STAGE_BYTES);
@@ -248,7 +259,7 @@ __global__ void __launch_bounds__(GT_THREADS, 1)
 #pragma unroll
                     for (int kk = 0; kk < GT_KB / 32; ++kk)
                         tc_mma_u8(dcol, sw128_desc(sa + kk * 32), sw128_desc(sbm + kk * 32),
-                                  GT_IDESC, (kb | kk) != 0);
+                                  GT_IDESC, (kb != klo || kk != 0) ? 1u : 0u);
                     tc_commit(&empty[stage]);
                     if (++stage == GT_STAGES) {
                         stage = 0;
@@ -264,10 +275,13 @@ __global__ void __launch_bounds__(GT_THREADS, 1)
         // bulk reduce-add into C_m (coalesced, asynchronous, exact u64 adds).
         int it = 0, buf = 0;
         const int row = warp * 32 + lane;
-        for (int t = blockIdx.x; t < a.ntiles; t += gridDim.x, ++it) {
+        for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
+            const int klo = (u % a.ksplit) * kper, khi = min(kblocks, klo + kper);
+            if (klo >= khi) continue;
             const int acc = it & 1;
             const uint32_t acc_phase = (it >> 1) & 1;
-            const int2 tl = a.tiles[t];
+            ++it;
+            const int2 tl = a.tiles[u / a.ksplit];
             mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
             const int64_t x = (int64_t)tl.x * GT_M + row;
@@ -304,7 +318,8 @@ __global__ void __launch_bounds__(GT_THREADS, 1)
                         const int64_t xx = (int64_t)tl.x * GT_M + e / GT_EC;
                         const int64_t yy = y0 + c + e % GT_EC;
                         const uint64_t val = s64[e];
-                        if (val && xx < a.N && yy < a.N) a.Cm[xx * a.N + yy] += (int64_t)val;
+                        if (val && xx < a.N && yy < a.N)  // atomic: K slices share tiles
+                            atomicAdd((unsigned long long*)&a.Cm[xx * a.N + yy], val);
                     }
                 }
                 buf ^= 1;
@@ -475,8 +490,10 @@ cudaError_t launch_gram_flush(uint8_t* D, int64_t n_pad, uint64_t ldd, uint32_t*
         if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
     }
     cudaFuncSetAttribute(gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GT_SMEM);
-    GramArgs a{Cm, N, dense_fill, (uint32_t)ldd, tiles, ntiles, tma_epi ? 1 : 0};
-    int grid = ntiles < sm_count ? ntiles : sm_count;
+    // split K so that there are >= ~2 work units per SM when tiles are few
+    const int ksplit = std::max(1, std::min(16, (2 * sm_count) / std::max(1, ntiles)));
+    GramArgs a{Cm, N, dense_fill, (uint32_t)ldd, tiles, ntiles, tma_epi ? 1 : 0, ksplit};
+    int grid = ntiles * ksplit < sm_count ? ntiles * ksplit : sm_count;
     gram_kernel<<<grid, GT_THREADS, GT_SMEM, s>>>(map, cmap, a);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;

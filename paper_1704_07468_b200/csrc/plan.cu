@@ -77,6 +77,7 @@ struct gakco_plan {
     int64_t heavy_min = 0, batch_keys = 0;
     bool timing = false;
     int sort_mode = 0;  // 0: chunked two-kernel LSD pass, 1: onesweep (decoupled look-back)
+    int sort_ctas_per_sm = 3;  // chunked pass grid = this x SMs (measured best of 1..4)
     int sm_count = 148;
     std::string err;
 
@@ -272,6 +273,10 @@ extern "C" gakco_status gakco_set_option(gakco_plan* p, int option, int64_t valu
             if (value < 0 || value > 1) return p->fail(GAKCO_E_ARG, "sort must be 0 or 1");
             p->sort_mode = (int)value;
             return GAKCO_OK;
+        case GAKCO_OPT_SORT_CTAS_PER_SM:
+            if (value < 1 || value > 16) return p->fail(GAKCO_E_ARG, "1..16");
+            p->sort_ctas_per_sm = (int)value;
+            return GAKCO_OK;
         case GAKCO_OPT_TIMING:
             p->timing = value != 0;
             return GAKCO_OK;
@@ -420,7 +425,8 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
     CK(p->ensure(p->counts, 16, s));
     CK(p->ensure(p->hist, std::max<uint64_t>(std::min<uint64_t>(bmax_masks, mine.size() + 1) *
                                                  MAXPASS * RADIX * 4,
-                                             (uint64_t)(3 * p->sm_count + 64 + bmax_masks) *
+                                             (uint64_t)(p->sort_ctas_per_sm * p->sm_count + 64 +
+                                                        bmax_masks) *
                                                  RADIX * 4),
                  s));
     {
@@ -557,7 +563,8 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
                 } else {
                     p->launches += 1;  // two kernels
                     LK(launch_radix_chunked(in, outk, n, nmask, sb + RADIX_BITS * q,
-                                            (uint32_t*)p->hist.p, 3 * p->sm_count, s));
+                                            (uint32_t*)p->hist.p, p->sort_ctas_per_sm * p->sm_count,
+                                            s));
                 }
                 std::swap(in, outk);
             }

@@ -31,6 +31,7 @@ GAKCO_OPT_HEAVY_MIN_SEQS = 1
 GAKCO_OPT_BATCH_KEYS = 2
 GAKCO_OPT_TIMING = 3
 GAKCO_OPT_SORT = 4
+GAKCO_OPT_SORT_CTAS_PER_SM = 5
 
 EXPORTS = ("gakco_create", "gakco_set_shard", "gakco_set_option", "gakco_accumulate",
            "gakco_finalize", "gakco_kernel", "gakco_get_stats", "gakco_num_masks",
