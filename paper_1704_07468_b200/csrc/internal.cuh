@@ -152,7 +152,7 @@ struct CorpusView {
 struct SegmentOut {
     uint32_t* tseq;          // [T] seq id | (group-head << 31)
     uint32_t* tcnt;          // [T] run length (count of the (key, seq) pair)
-    uint32_t* gstart;        // [G+1] first triple of each multi-sequence group; [G] = T
+    uint2* groups;           // [G] triple range [x, y) of each multi-sequence group
     uint32_t* counts;        // [0] = T, [1] = G
 };
 
@@ -168,10 +168,10 @@ cudaError_t launch_onesweep(const uint64_t* in, uint64_t* out, uint64_t n, int n
 // Chunked LSD pass (radix_hist + radix_scatter); hist: >= (target_ctas + nseg) * 256 u32.
 cudaError_t launch_radix_chunked(const uint64_t* in, uint64_t* out, uint64_t n, int nseg,
                                  int shift, uint32_t* hist, int target_ctas, cudaStream_t s);
+// counters: 2 u32 (triples, groups) reserved per tile; zeroed by the launcher.
 cudaError_t launch_segment(const uint64_t* keys, uint64_t n, int nseg, int sb, int64_t N,
-                           int64_t* Cm, uint64_t* status_t, uint64_t* status_g, uint32_t* ctr,
-                           uint32_t epoch, SegmentOut so, unsigned long long* stats,
-                           cudaStream_t s);
+                           int64_t* Cm, uint32_t* counters, SegmentOut so,
+                           unsigned long long* stats, cudaStream_t s);
 // Light pair updates; a group with >= heavy_min sequences (and counts <= 255)
 // instead claims column c = atomicAdd(dense_fill) (< ldd) of the dense count
 // matrix D (u8, slabs of 128 columns: byte (c/128)*n_pad*128 + row*128 + c%128)

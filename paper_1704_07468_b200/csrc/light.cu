@@ -37,16 +37,13 @@ __global__ void __launch_bounds__(256) light_kernel(SegmentOut so, int64_t heavy
     const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
     const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
     unsigned long long pairs = 0, nheavy = 0;
-    // A warp takes 32 consecutive groups at a time: one coalesced load brings all
-    // their bounds (gstart[G] == T closes the last group), and the first 32
-    // triples of the next group are loaded while the current one is processed.
+    // A warp takes 32 groups at a time: one coalesced load brings all their
+    // triple ranges, and the first 32 triples of the next group are loaded while
+    // the current one is processed.
     for (uint64_t base = warp * 32; base < G; base += nwarps * 32) {
         const uint32_t ng = (uint32_t)min((uint64_t)32, (uint64_t)G - base);
-        const uint32_t my_start = lane <= ng ? so.gstart[base + lane] : 0u;
-        const uint32_t last_end = __shfl_sync(0xffffffffu, my_start, ng);  // lane ng (<= 32)
-        const uint32_t my_end_lo = __shfl_down_sync(0xffffffffu, my_start, 1);
-        const uint32_t ge31 = (ng == 32) ? so.gstart[base + 32] : last_end;
-        const uint32_t my_end = lane == 31 ? ge31 : my_end_lo;
+        const uint2 rg = lane < ng ? so.groups[base + lane] : make_uint2(0u, 0u);
+        const uint32_t my_start = rg.x, my_end = rg.y;
         // prefetch group 0's first chunk
         uint32_t pa0 = __shfl_sync(0xffffffffu, my_start, 0);
         uint32_t pb0 = __shfl_sync(0xffffffffu, my_end, 0);

@@ -421,7 +421,7 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
     CK(p->ensure(p->keysB, cap_keys * 8, s));
     CK(p->ensure(p->tseq, cap_keys * 4, s));
     CK(p->ensure(p->tcnt, cap_keys * 4, s));
-    CK(p->ensure(p->gstart, (cap_keys / 2 + 2) * 4, s));
+    CK(p->ensure(p->gstart, (cap_keys / 2 + 2) * sizeof(uint2), s));  // group ranges
     CK(p->ensure(p->counts, 16, s));
     CK(p->ensure(p->hist, std::max<uint64_t>(std::min<uint64_t>(bmax_masks, mine.size() + 1) *
                                                  MAXPASS * RADIX * 4,
@@ -468,7 +468,7 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
     }
     CorpusView cv{(const uint8_t*)p->codes.p, (const int64_t*)p->off.p, (const int64_t*)p->gofs.p,
                   (const uint32_t*)p->gmseq.p, N, n};
-    SegmentOut so{(uint32_t*)p->tseq.p, (uint32_t*)p->tcnt.p, (uint32_t*)p->gstart.p,
+    SegmentOut so{(uint32_t*)p->tseq.p, (uint32_t*)p->tcnt.p, (uint2*)p->gstart.p,
                   (uint32_t*)p->counts.p};
     int64_t passkeys = 0;
     const size_t nn = (size_t)N * N;
@@ -572,11 +572,7 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
             p->stage_end(s, S_SORT, a);
 
             p->stage_begin(s, &a);
-            uint32_t* c1;
-            CK(p->next_ctr(s, &c1));
-            const uint64_t seg_tiles = n * nmask / SEG_TILE + 2;
-            LK(launch_segment(in, n, nmask, sb, N, Cm, (uint64_t*)p->status.p,
-                              (uint64_t*)p->status.p + seg_tiles, c1, p->epoch++, so, stats, s));
+            LK(launch_segment(in, n, nmask, sb, N, Cm, so.counts, so, stats, s));
             p->stage_end(s, S_SEGMENT, a);
 
             p->stage_begin(s, &a);

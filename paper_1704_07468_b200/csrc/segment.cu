@@ -7,31 +7,39 @@
 // count) TRIPLE; a run of equal key bits is one GROUP, whose triples list the
 // sequences sharing the (g-m)-mer in ascending order.
 //
-// One pass, one kernel (ordered compaction with decoupled look-back):
+// One kernel, no inter-tile ordering: a tile emits the groups that START in it
+// (a group running past the tile end is finished by its owner, which scans the
+// tail), at offsets reserved with one atomicAdd per tile; group order in the
+// output is arbitrary (integer sums commute), each group's triples are
+// contiguous and in sequence order.
 //  * every triple with count >= 2 adds count^2 - count to C_m(X,X) (the
 //    within-sequence repeat part of sum_key c_X(key)^2; the other part, one per
 //    g-mer per mask, is added in closed form by launch_diag_closed_form —
-//    DESIGN.md reading A3: singletons still count on the diagonal);
-//  * only triples of groups with >= 2 distinct sequences are emitted (the only
-//    groups that touch off-diagonal entries), as seq | group-head<<31 and count;
-//  * the first emitted triple of each such group is recorded in gstart[]; a
-//    group's triples are [gstart[g], gstart[g+1]) (gstart[G] == T).
+//    DESIGN.md reading A3: singletons still count on the diagonal) — by the tile
+//    holding the triple's first key;
+//  * only groups with >= 2 distinct sequences are emitted (the only groups that
+//    touch off-diagonal entries): triples as seq | group-head<<31 and count,
+//    groups as [first, last+1) triple ranges.
 #include "internal.cuh"
 
 namespace gk {
 
 __global__ void __launch_bounds__(SEG_THREADS) segment_kernel(
     const uint64_t* __restrict__ keys, uint64_t n, uint64_t total, int sb, int64_t N,
-    int64_t* Cm, uint64_t* status_t, uint64_t* status_g, uint32_t* ctr, uint32_t epoch,
-    SegmentOut so, unsigned long long* stats) {
+    int64_t* Cm, uint32_t* counters, SegmentOut so, unsigned long long* stats) {
     __shared__ uint32_t s_w[8];
-    __shared__ uint32_t s_tile, s_pt, s_pg;
-    const int tid = threadIdx.x;
-    if (tid == 0) s_tile = atomicAdd(ctr, 1u);
-    __syncthreads();
-    const uint32_t t = s_tile;
-    const uint64_t base = (uint64_t)t * SEG_TILE + (uint64_t)tid * SEG_ITEMS;
+    __shared__ uint32_t s_gpos[SEG_TILE];
+    __shared__ uint32_t s_first_gh, s_base_t, s_base_g, s_tail;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint64_t tile0 = (uint64_t)blockIdx.x * SEG_TILE;
+    const uint64_t base = tile0 + (uint64_t)tid * SEG_ITEMS;
+    const uint64_t tile_end = min(tile0 + SEG_TILE, total);
     const uint64_t seqmask = (1ull << sb) - 1ull;
+    if (tid == 0) {
+        s_first_gh = 0xffffffffu;
+        s_tail = 0;
+    }
+    __syncthreads();
 
     uint64_t cur[SEG_ITEMS];
     if (base + SEG_ITEMS <= total) {
@@ -46,9 +54,9 @@ __global__ void __launch_bounds__(SEG_THREADS) segment_kernel(
 #pragma unroll
         for (int i = 0; i < SEG_ITEMS; ++i) cur[i] = base + i < total ? keys[base + i] : 0ull;
     }
-    uint64_t prev = (base < total && base % n != 0) ? keys[base - 1] : 0ull;
+    const uint64_t prev = (base < total && base % n != 0) ? keys[base - 1] : 0ull;
 
-    uint32_t emit_t = 0, emit_g = 0, gh_bits = 0;
+    uint32_t th_bits = 0, gh_bits = 0, multi_bits = 0;
     uint32_t cnt[SEG_ITEMS];
 #pragma unroll
     for (int i = 0; i < SEG_ITEMS; ++i) {
@@ -92,55 +100,120 @@ __global__ void __launch_bounds__(SEG_THREADS) segment_kernel(
             const int64_t x = (int64_t)(c0 & seqmask);
             atomicAdd((unsigned long long*)&Cm[x * N + x], (unsigned long long)c * c - c);
         }
-        const bool multi = !gh || (j < seg_end && (nk >> sb) == (c0 >> sb));
-        if (multi) {
-            emit_t |= 1u << i;
-            if (gh) emit_g |= 1u << i;
+        th_bits |= 1u << i;
+        if (!gh || (j < seg_end && (nk >> sb) == (c0 >> sb))) multi_bits |= 1u << i;
+        if (gh) {
+            gh_bits |= 1u << i;
+            atomicMin(&s_first_gh, (uint32_t)(idx - tile0));
         }
-        if (gh) gh_bits |= 1u << i;
+    }
+    __syncthreads();
+    // keys before the tile's first group head belong to a group owned by an
+    // earlier tile: not emitted here
+    const uint32_t fgh = s_first_gh;
+    uint32_t emit_t = 0, emit_g = 0;
+#pragma unroll
+    for (int i = 0; i < SEG_ITEMS; ++i) {
+        const bool own = fgh != 0xffffffffu && (uint32_t)(base + i - tile0) >= fgh;
+        if (own && ((th_bits & multi_bits) >> i & 1u)) {
+            emit_t |= 1u << i;
+            if ((gh_bits >> i) & 1u) emit_g |= 1u << i;
+        }
     }
     uint32_t agg_t, agg_g;
     const uint32_t off_t = scan256_excl(__popc(emit_t), s_w, &agg_t);
     const uint32_t off_g = scan256_excl(__popc(emit_g), s_w, &agg_g);
-    if (tid < 32) {
-        const uint32_t e = lookback_warp(status_t, t, agg_t, epoch);
-        if (tid == 0) s_pt = e;
-    } else if (tid < 64) {
-        const uint32_t e = lookback_warp(status_g, t, agg_g, epoch);
-        if (tid == 32) s_pg = e;
+
+    // the last group starting here may run past the tile: count its tail triples
+    const bool has_gh = fgh != 0xffffffffu;
+    const bool crossing = has_gh && tile_end < total && tile_end % n != 0 &&
+                          (keys[tile_end] >> sb) == (keys[tile_end - 1] >> sb);
+    uint64_t gend_key = tile_end;  // one past the crossing group's last key
+    if (crossing && warp == 0) {
+        const uint64_t gkey = keys[tile_end - 1] >> sb;
+        const uint64_t seg_end = (tile_end / n + 1) * n;
+        uint32_t nt = 0;
+        uint64_t e = tile_end;
+        uint64_t last = keys[tile_end - 1];
+        while (true) {
+            const uint64_t q = e + lane;
+            const uint64_t kk = q < seg_end ? keys[q] : ~0ull;
+            const bool in = q < seg_end && (kk >> sb) == gkey;
+            const uint32_t inm = __ballot_sync(0xffffffffu, in);
+            const uint64_t pk = __shfl_up_sync(0xffffffffu, kk, 1);
+            const uint64_t pv = lane == 0 ? last : pk;
+            nt += __popc(__ballot_sync(0xffffffffu, in && kk != pv));
+            const uint32_t run = ~inm ? __ffs(~inm) - 1 : 32;  // leading in-group lanes
+            if (run < 32) {
+                gend_key = e + run;
+                break;
+            }
+            last = __shfl_sync(0xffffffffu, kk, 31);
+            e += 32;
+        }
+        if (lane == 0) s_tail = nt;
     }
     __syncthreads();
-    uint32_t ti = s_pt + off_t, gi = s_pg + off_g;
+    const uint32_t tail = s_tail;
+    if (tid == 0) {
+        s_base_t = atomicAdd(&counters[0], agg_t + tail);
+        s_base_g = atomicAdd(&counters[1], agg_g);
+        if (agg_t + tail) atomicAdd(&stats[ST_TRIPLES], (unsigned long long)(agg_t + tail));
+        if (agg_g) atomicAdd(&stats[ST_GROUPS], (unsigned long long)agg_g);
+    }
+    __syncthreads();
+    uint32_t ti = s_base_t + off_t, gl = off_g;
 #pragma unroll
     for (int i = 0; i < SEG_ITEMS; ++i) {
         if (emit_t & (1u << i)) {
             const uint32_t x = (uint32_t)(cur[i] & seqmask);
             so.tseq[ti] = x | (((gh_bits >> i) & 1u) << 31);
             so.tcnt[ti] = cnt[i];
-            if (emit_g & (1u << i)) so.gstart[gi++] = ti;
+            if (emit_g & (1u << i)) s_gpos[gl++] = ti;
             ++ti;
         }
     }
-    if (base < total && base + SEG_ITEMS >= total) {  // the thread holding the last key
-        so.counts[0] = s_pt + agg_t;
-        so.counts[1] = s_pg + agg_g;
-        so.gstart[s_pg + agg_g] = s_pt + agg_t;        // sentinel gstart[G] = T
-    }
-    if (tid == 0) {
-        atomicAdd(&stats[ST_TRIPLES], (unsigned long long)agg_t);
-        atomicAdd(&stats[ST_GROUPS], (unsigned long long)agg_g);
+    __syncthreads();
+    // group ranges: a group runs to the next group's first triple (or the end of
+    // this tile's triples, its tail included)
+    const uint32_t tend = s_base_t + agg_t + tail;
+    for (uint32_t g = tid; g < agg_g; g += SEG_THREADS)
+        so.groups[s_base_g + g] = make_uint2(s_gpos[g], g + 1 < agg_g ? s_gpos[g + 1] : tend);
+    // tail triples of the crossing group (warp 0), after this tile's triples
+    if (tail && warp == 0) {
+        const uint64_t seg_end = (tile_end / n + 1) * n;
+        uint32_t w = s_base_t + agg_t;
+        uint64_t last = keys[tile_end - 1];
+        for (uint64_t e = tile_end; e < gend_key; e += 32) {
+            const uint64_t q = e + lane;
+            const bool in = q < gend_key;
+            const uint64_t kk = in ? keys[q] : 0ull;
+            const uint64_t pk = __shfl_up_sync(0xffffffffu, kk, 1);
+            const uint64_t pv = lane == 0 ? last : pk;
+            const bool head = in && kk != pv;
+            const uint32_t hm = __ballot_sync(0xffffffffu, head);
+            if (head) {
+                uint64_t r = q + 1;
+                while (r < seg_end && keys[r] == kk) ++r;
+                const uint32_t pos = w + __popc(hm & lanemask_lt());
+                so.tseq[pos] = (uint32_t)(kk & seqmask);
+                so.tcnt[pos] = (uint32_t)(r - q);
+            }
+            w += __popc(hm);
+            last = __shfl_sync(0xffffffffu, kk, 31);
+        }
     }
 }
 
 cudaError_t launch_segment(const uint64_t* keys, uint64_t n, int nseg, int sb, int64_t N,
-                           int64_t* Cm, uint64_t* status_t, uint64_t* status_g, uint32_t* ctr,
-                           uint32_t epoch, SegmentOut so, unsigned long long* stats,
-                           cudaStream_t s) {
+                           int64_t* Cm, uint32_t* counters, SegmentOut so,
+                           unsigned long long* stats, cudaStream_t s) {
+    cudaError_t e = cudaMemsetAsync(counters, 0, 2 * sizeof(uint32_t), s);
     uint64_t total = n * (uint64_t)nseg;
-    if (total == 0) return cudaMemsetAsync(so.counts, 0, 2 * sizeof(uint32_t), s);
+    if (e != cudaSuccess || total == 0) return e;
     uint64_t tiles = (total + SEG_TILE - 1) / SEG_TILE;
-    segment_kernel<<<(unsigned)tiles, SEG_THREADS, 0, s>>>(keys, n, total, sb, N, Cm, status_t,
-                                                           status_g, ctr, epoch, so, stats);
+    segment_kernel<<<(unsigned)tiles, SEG_THREADS, 0, s>>>(keys, n, total, sb, N, Cm, counters, so,
+                                                           stats);
     return cudaGetLastError();
 }
 
