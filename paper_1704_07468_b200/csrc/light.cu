@@ -44,26 +44,59 @@ __global__ void __launch_bounds__(256) light_kernel(SegmentOut so, int64_t heavy
         const uint32_t ng = (uint32_t)min((uint64_t)32, (uint64_t)G - base);
         const uint2 rg = lane < ng ? so.groups[base + lane] : make_uint2(0u, 0u);
         const uint32_t my_start = rg.x, my_end = rg.y;
-        // prefetch group 0's first chunk
-        uint32_t pa0 = __shfl_sync(0xffffffffu, my_start, 0);
-        uint32_t pb0 = __shfl_sync(0xffffffffu, my_end, 0);
-        uint32_t pX = 0, pC = 0;
-        if (pa0 + lane < pb0) {
-            pX = so.tseq[pa0 + lane] & 0x7fffffffu;
-            pC = so.tcnt[pa0 + lane];
+        const uint32_t my_s = my_end - my_start;
+
+        // (1) small light groups (s <= 32) of the batch: their pairs are flattened
+        // into one index space, so every lane does one pair update per round
+        // whatever the group sizes (no lane idles on a 2-sequence group).
+        const bool flat = lane < ng && my_s <= 32 && (int64_t)my_s < heavy_min;
+        const uint32_t P = flat ? my_s * (my_s - 1) / 2 : 0u;
+        uint32_t incl = P;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t t = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += t;
         }
-        for (uint32_t j = 0; j < ng; ++j) {
+        const uint32_t excl = incl - P;
+        const uint32_t Ptot = __shfl_sync(0xffffffffu, incl, 31);
+        pairs += lane == 0 ? Ptot : 0u;
+        for (uint32_t q0 = 0; q0 < Ptot; q0 += 32) {
+            const uint32_t q = q0 + lane;
+            // group of pair q: the last lane j with excl_j <= q
+            int j = 0;
+#pragma unroll
+            for (int step = 16; step > 0; step >>= 1) {
+                const uint32_t e = __shfl_sync(0xffffffffu, excl, j + step);
+                if (e <= q) j += step;
+            }
+            const uint32_t ej = __shfl_sync(0xffffffffu, excl, j);
+            const uint32_t sj = __shfl_sync(0xffffffffu, my_start, j);
+            if (q < Ptot) {
+                const uint32_t ab = s_tri[q - ej];
+                const uint32_t ta = sj + (ab & 31), tb = sj + (ab >> 5);
+                const uint32_t xa = so.tseq[ta] & 0x7fffffffu, xb = so.tseq[tb] & 0x7fffffffu;
+                atomicAdd(&acc[tri_index(xa, xb, N)], so.tcnt[ta] * so.tcnt[tb]);
+            }
+        }
+
+        // (2) the other groups one by one (big light groups and heavy candidates)
+        uint32_t todo = __ballot_sync(0xffffffffu, lane < ng && !flat);
+        uint32_t pa0 = 0, pb0 = 0, pX = 0, pC = 0;
+        auto prefetch = [&](uint32_t jj) {
+            pa0 = __shfl_sync(0xffffffffu, my_start, jj);
+            pb0 = __shfl_sync(0xffffffffu, my_end, jj);
+            pX = pC = 0;
+            if (pa0 + lane < pb0) {
+                pX = so.tseq[pa0 + lane] & 0x7fffffffu;
+                pC = so.tcnt[pa0 + lane];
+            }
+        };
+        if (todo) prefetch(__ffs(todo) - 1);
+        while (todo) {
+            todo &= todo - 1;
             const uint32_t a0 = pa0, b0 = pb0;
             const uint32_t xA0 = pX, cA0 = pC;
-            if (j + 1 < ng) {  // prefetch the next group's first chunk
-                pa0 = __shfl_sync(0xffffffffu, my_start, j + 1);
-                pb0 = __shfl_sync(0xffffffffu, my_end, j + 1);
-                pX = pC = 0;
-                if (pa0 + lane < pb0) {
-                    pX = so.tseq[pa0 + lane] & 0x7fffffffu;
-                    pC = so.tcnt[pa0 + lane];
-                }
-            }
+            if (todo) prefetch(__ffs(todo) - 1);  // the next group's first chunk
             const uint32_t s = b0 - a0;
             if ((int64_t)s >= heavy_min) {
                 // dense tensor-core path if every count fits the u8 operand
