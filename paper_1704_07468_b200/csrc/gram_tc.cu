@@ -378,10 +378,29 @@ __global__ void __launch_bounds__(BD_THREADS) build_dense_kernel(
             const uint64_t col = qs * BD_COLS + warp + k * (BD_THREADS / 32);
             bnd[k] = col < f1 ? heavy_list[col] : make_uint2(0, 0);
         }
+        // the first 4 x 32 triples of both columns are loaded before any is used
+        // (8 independent loads in flight per lane); longer groups continue below
+        constexpr int NK = BD_COLS * 32 / BD_THREADS;
+        uint32_t xs[NK][4], cs[NK][4];
 #pragma unroll
-        for (int k = 0; k < BD_COLS * 32 / BD_THREADS; ++k) {
+        for (int k = 0; k < NK; ++k)
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const uint32_t t = bnd[k].x + u * 32 + lane;
+                const bool v = t < bnd[k].y;
+                xs[k][u] = v ? so.tseq[t] & 0x7fffffffu : 0xffffffffu;
+                cs[k][u] = v ? so.tcnt[t] : 0u;
+            }
+#pragma unroll
+        for (int k = 0; k < NK; ++k) {
             const int c = warp + k * (BD_THREADS / 32);
-            for (uint32_t t = bnd[k].x + lane; t < bnd[k].y; t += 32) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int64_t x = (int64_t)xs[k][u] - r0;
+                if (xs[k][u] != 0xffffffffu && x >= 0 && x < rows)
+                    sb[x * BD_STRIDE + c] = (uint8_t)cs[k][u];
+            }
+            for (uint32_t t = bnd[k].x + 128 + lane; t < bnd[k].y; t += 32) {
                 const int64_t x = (int64_t)(so.tseq[t] & 0x7fffffffu) - r0;
                 if (x >= 0 && x < rows) sb[x * BD_STRIDE + c] = (uint8_t)so.tcnt[t];
             }
