@@ -328,6 +328,24 @@ def run_ours(a):
                "api": "gakco_kernel(host pinned codes/offsets -> host K, Knorm)" if world == 1
                else "gakco_accumulate(host inputs) + NCCL reduce + gakco_finalize(host K, Knorm)"}
 
+    # ---- K-only fast path (NEXT-1): K = C_{g-k} from the level-(g-k) masks only
+    k_only = None
+    if world == 1 and cfg.M >= cfg.g - cfg.k:
+        from math import comb
+        for _ in range(2):
+            plan.kernel_k(codes_d, offs_h, N, K, Kn, stream)
+        kt = []
+        for i in range(a.steps):
+            flush.fill_(i)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            plan.kernel_k(codes_d, offs_h, N, K, Kn, stream)
+            e1.record(stream)
+            torch.cuda.synchronize(dev)
+            kt.append(e0.elapsed_time(e1))
+        k_only = {"ms_per_step": sum(kt) / len(kt), "masks": comb(cfg.g, cfg.g - cfg.k),
+                  "outputs": "K, Knorm (device)", "api": "gakco_kernel_k"}
+
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
@@ -382,7 +400,7 @@ def run_ours(a):
            "scaling": "strong", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
            "config": config_dict(a.config, cfg, cp, masks, n, world),
            "roofline": roof, "stages": stages, "gpu_launches": int(launches),
-           "clocks": clocks, "e2e": e2e,
+           "clocks": clocks, "e2e": e2e, "k_only": k_only,
            "counters": {k: v for k, v in last.items() if not k.startswith("ms_")}}
     if world == 1 and not a.no_cpu_baseline:
         import oracle

@@ -121,6 +121,14 @@ gakco_status gakco_kernel(gakco_plan* plan, const uint8_t* codes, const int64_t*
                           int64_t N, int64_t* C, int64_t* Nm, int64_t* K, double* Knorm,
                           void* cuda_stream);
 
+/* K-only fast path. Because C(g-j, g-k-j) = C(g-j, k) =
+ * h_j, Eq. 8 at m = g-k is exactly Eq. 7: K = C_{g-k}. So K
+ * needs only the C(g, g-k) masks of level g-k — no other level and no Eq. 9.
+ * Requires M >= g-k (the paper's M = g-k; GAKCO_E_ARG otherwise). Writes K and/or
+ * Knorm (either may be NULL, host or device pointers). Shard setting ignored. */
+gakco_status gakco_kernel_k(gakco_plan* plan, const uint8_t* codes, const int64_t* offsets,
+                            int64_t N, int64_t* K, double* Knorm, void* cuda_stream);
+
 /* Counters and (if GAKCO_OPT_TIMING) stage times of the last accumulate /
  * finalize. Synchronises the plan's last stream. */
 gakco_status gakco_get_stats(gakco_plan* plan, gakco_stats* out);

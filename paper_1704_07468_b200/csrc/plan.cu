@@ -293,8 +293,11 @@ extern "C" int64_t gakco_num_masks(const gakco_plan* p, int shard_only) {
 }
 
 // ----------------------------------------------------------------------------
+// only_level >= 0: process only the masks of that level, accumulated into the
+// single N x N matrix C (used by the K-only path, K = C_{g-k}).
 static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const int64_t* offsets,
-                                    int64_t N, int64_t* C, cudaStream_t s, int rank, int world) {
+                                    int64_t N, int64_t* C, cudaStream_t s, int rank, int world,
+                                    int only_level = -1) {
 #define CK(x)                                          \
     do {                                               \
         cudaError_t e_ = (x);                          \
@@ -386,7 +389,8 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
     // this shard's masks, in processing order
     std::vector<int> mine;
     for (size_t i = 0; i < p->mask_level.size(); ++i)
-        if ((int)(i % world) == rank) mine.push_back((int)i);
+        if ((int)(i % world) == rank && (only_level < 0 || p->mask_level[i] == only_level))
+            mine.push_back((int)i);
     std::vector<uint8_t> kept_h(mine.size() * GMAX + GMAX, 0);
     for (size_t i = 0; i < mine.size(); ++i)
         std::memcpy(&kept_h[i * GMAX], p->mask_kept[mine[i]].data(), GMAX);
@@ -472,6 +476,9 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
                   (uint32_t*)p->counts.p};
     int64_t passkeys = 0;
     const size_t nn = (size_t)N * N;
+    auto level_ptr = [&](int m) -> int64_t* {
+        return only_level >= 0 ? C : C + (size_t)m * nn;
+    };
 
     // Heavy groups of consecutive batches of one level accumulate as columns of D;
     // the Gram runs ("flush") at a level change, when D could overflow (a bound,
@@ -486,7 +493,7 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
         p->stage_begin(s, &ah);
         p->launches += 1;  // + fill_reset
         LK(launch_gram_flush((uint8_t*)p->dense.p, n_pad, rcap, (uint32_t*)p->hcount.p,
-                             C + (size_t)dense_m * nn, N, (const int2*)p->tiles.p, p->ntiles,
+                             level_ptr(dense_m), N, (const int2*)p->tiles.p, p->ntiles,
                              p->sm_count, stats, s));
         p->stage_end(s, S_HEAVY, ah);
         dense_bound = 0;
@@ -505,7 +512,7 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
         if (light_m < 0 || light_masks == 0) return GAKCO_OK;
         cudaEvent_t al = nullptr;
         p->stage_begin(s, &al);
-        LK(launch_light_flush((uint32_t*)p->lightacc.p, N, C + (size_t)light_m * nn, p->sm_count,
+        LK(launch_light_flush((uint32_t*)p->lightacc.p, N, level_ptr(light_m), p->sm_count,
                               s));
         p->stage_end(s, S_LIGHT, al);
         light_masks = 0;
@@ -520,7 +527,7 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
         const int nmask = (int)(end - pos);
         const int kb = p->key_bits[m];
         const int npass = (kb + RADIX_BITS - 1) / RADIX_BITS;
-        int64_t* Cm = C + (size_t)m * nn;
+        int64_t* Cm = level_ptr(m);
         cudaEvent_t a = nullptr;
         if (gram_ok && n > 0) {
             const uint64_t bnd = (uint64_t)nmask * n / (uint64_t)heavy_min + 128;
@@ -616,8 +623,11 @@ extern "C" gakco_status gakco_accumulate(gakco_plan* p, const uint8_t* codes,
     return accumulate_impl(p, codes, offsets, N, C, (cudaStream_t)stream, p->rank, p->world);
 }
 
+// k_only: C is the single level g-k and K = C_{g-k} (the epilogue runs with
+// g = k = 1, M = 0, i.e. K = N_0 = C_0, and Nm is not produced).
 static gakco_status finalize_impl(gakco_plan* p, int64_t* C, int64_t N, int64_t* Nm, int64_t* K,
-                                  double* Knorm, cudaStream_t s, bool keep_events) {
+                                  double* Knorm, cudaStream_t s, bool keep_events,
+                                  bool k_only = false) {
 #define CK(x)                                          \
     do {                                               \
         cudaError_t e_ = (x);                          \
@@ -641,7 +651,8 @@ static gakco_status finalize_impl(gakco_plan* p, int64_t* C, int64_t N, int64_t*
     p->after_accumulate = false;
     p->last_stream = s;
     const size_t nn = (size_t)N * N;
-    const int M = p->M;
+    const int M = k_only ? 0 : p->M;
+    if (k_only) Nm = nullptr;
     int64_t* dNm = Nm;
     int64_t* dK = K;
     double* dKn = Knorm;
@@ -664,7 +675,8 @@ static gakco_status finalize_impl(gakco_plan* p, int64_t* C, int64_t N, int64_t*
     CK(cudaMemsetAsync(p->flags.p, 0, sizeof(int), s));
     cudaEvent_t a = nullptr;
     p->stage_begin(s, &a);
-    LK(launch_epilogue(C, N, p->g, p->k, M, dNm, dK, dKn, (int64_t*)p->kdiag.p, (int*)p->flags.p,
+    LK(launch_epilogue(C, N, k_only ? 1 : p->g, k_only ? 1 : p->k, M, dNm, dK, dKn,
+                       (int64_t*)p->kdiag.p, (int*)p->flags.p,
                        s));
     p->stage_end(s, S_EPILOGUE, a);
     if (hNm) CK(cudaMemcpyAsync(Nm, dNm, (M + 1) * nn * 8, cudaMemcpyDeviceToHost, s));
@@ -714,6 +726,27 @@ extern "C" gakco_status gakco_kernel(gakco_plan* p, const uint8_t* codes, const 
         if (e != cudaSuccess) return p->cuda_fail(e, "copy C to host");
     }
     return GAKCO_OK;
+}
+
+extern "C" gakco_status gakco_kernel_k(gakco_plan* p, const uint8_t* codes,
+                                       const int64_t* offsets, int64_t N, int64_t* K,
+                                       double* Knorm, void* stream) {
+    if (!p) return GAKCO_E_ARG;
+    if (N < 1 || N >= ((int64_t)1 << 31)) return p->fail(GAKCO_E_ARG, "N must be in [1, 2^31)");
+    if (p->M < p->g - p->k)
+        return p->fail(GAKCO_E_ARG, "K-only path needs M >= g-k (K = C_{g-k})");
+    if (!K && !Knorm) return p->fail(GAKCO_E_ARG, "K and Knorm are both NULL");
+    DeviceGuard dg(p->device);
+    cudaStream_t s = (cudaStream_t)stream;
+    const size_t bytes = (size_t)N * N * 8;
+    cudaError_t e = p->ensure(p->Cscr, bytes, s);
+    if (e != cudaSuccess) return p->cuda_fail(e, "C scratch");
+    int64_t* dC = (int64_t*)p->Cscr.p;
+    e = cudaMemsetAsync(dC, 0, bytes, s);
+    if (e != cudaSuccess) return p->cuda_fail(e, "memset C");
+    gakco_status st = accumulate_impl(p, codes, offsets, N, dC, s, 0, 1, p->g - p->k);
+    if (st != GAKCO_OK) return st;
+    return finalize_impl(p, dC, N, nullptr, K, Knorm, s, true, /*k_only=*/true);
 }
 
 extern "C" gakco_status gakco_get_stats(gakco_plan* p, gakco_stats* out) {

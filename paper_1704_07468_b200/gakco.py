@@ -34,8 +34,8 @@ GAKCO_OPT_SORT = 4
 GAKCO_OPT_SORT_CTAS_PER_SM = 5
 
 EXPORTS = ("gakco_create", "gakco_set_shard", "gakco_set_option", "gakco_accumulate",
-           "gakco_finalize", "gakco_kernel", "gakco_get_stats", "gakco_num_masks",
-           "gakco_last_error", "gakco_status_string", "gakco_destroy")
+           "gakco_finalize", "gakco_kernel", "gakco_kernel_k", "gakco_get_stats",
+           "gakco_num_masks", "gakco_last_error", "gakco_status_string", "gakco_destroy")
 
 
 class gakco_stats(ctypes.Structure):
@@ -73,6 +73,7 @@ def lib():
         L.gakco_accumulate.argtypes = [P, P, P, i64, P, P]
         L.gakco_finalize.argtypes = [P, P, i64, P, P, P, P]
         L.gakco_kernel.argtypes = [P, P, P, i64, P, P, P, P, P]
+        L.gakco_kernel_k.argtypes = [P, P, P, i64, P, P, P]
         L.gakco_get_stats.argtypes = [P, ctypes.POINTER(gakco_stats)]
         L.gakco_num_masks.argtypes = [P, ci]
         L.gakco_num_masks.restype = i64
@@ -83,7 +84,7 @@ def lib():
         L.gakco_destroy.argtypes = [P]
         L.gakco_destroy.restype = None
         for f in ("gakco_create", "gakco_set_shard", "gakco_set_option", "gakco_accumulate",
-                  "gakco_finalize", "gakco_kernel", "gakco_get_stats"):
+                  "gakco_finalize", "gakco_kernel", "gakco_kernel_k", "gakco_get_stats"):
             getattr(L, f).restype = ci
         _lib = L
     return _lib
@@ -148,6 +149,11 @@ def gakco_kernel(plan, codes, offsets, N, C=None, Nm=None, K=None, Knorm=None, s
                                     _ptr(K), _ptr(Knorm), _stream(stream)))
 
 
+def gakco_kernel_k(plan, codes, offsets, N, K=None, Knorm=None, stream=None):
+    _check(plan, lib().gakco_kernel_k(plan, _ptr(codes), _ptr(offsets), N, _ptr(K), _ptr(Knorm),
+                                      _stream(stream)))
+
+
 def gakco_get_stats(plan):
     s = gakco_stats()
     _check(plan, lib().gakco_get_stats(plan, ctypes.byref(s)))
@@ -185,6 +191,9 @@ class Plan:
 
     def kernel(self, codes, offsets, N, C=None, Nm=None, K=None, Knorm=None, stream=None):
         gakco_kernel(self.h, codes, offsets, N, C, Nm, K, Knorm, stream)
+
+    def kernel_k(self, codes, offsets, N, K=None, Knorm=None, stream=None):
+        gakco_kernel_k(self.h, codes, offsets, N, K, Knorm, stream)
 
     def stats(self):
         return gakco_get_stats(self.h)

@@ -207,6 +207,45 @@ def test_host_buffers_e2e(gk, oracle_lib):
     assert_knorm(Kn.numpy(), ref["Knorm"])
 
 
+def test_k_only_fast_path(gk, oracle_lib):
+    """NEXT-1: gakco_kernel_k (level g-k masks only) gives the oracle's K and
+    Knorm; refused when M < g-k."""
+    rng = np.random.default_rng(106)
+    cases = [(sc.make("tiny"), 7, 5)]
+    for _ in range(10):
+        sigma = int(rng.choice([2, 4, 20]))
+        g = int(rng.integers(1, 10))
+        k = int(rng.integers(1, g + 1))
+        cases.append((sc.random_small(rng, sigma, n_max=60, l_max=100), g, k))
+    for cp, g, k in cases:
+        ref = oracle_lib.compute(cp, g, k, g - k)
+        N = cp.n_seq
+        K = torch.empty((N, N), dtype=torch.int64, device="cuda")
+        Kn = torch.empty((N, N), dtype=torch.float64, device="cuda")
+        plan = gk.Plan(cp.sigma, g, k, g - k)
+        plan.kernel_k(cp.codes if cp.codes.size else np.zeros(1, np.uint8), cp.offsets, N, K, Kn)
+        plan.close()
+        assert np.array_equal(K.cpu().numpy(), ref["K"])
+        assert_knorm(Kn.cpu().numpy(), ref["Knorm"])
+    plan = gk.Plan(4, 7, 5, 1)
+    with pytest.raises(gk.GakcoError):
+        plan.kernel_k(cases[0][0].codes, cases[0][0].offsets, 50, K, Kn)
+    plan.close()
+
+
+def test_k_only_dna_digest(gk):
+    """K-only on the full DNA config matches the oracle's committed K digest."""
+    gold = _golden("dna")
+    cfg = sc.CONFIGS["dna"]
+    cp = sc.make("dna")
+    N = cp.n_seq
+    K = torch.empty((N, N), dtype=torch.int64, device="cuda")
+    plan = gk.Plan(cfg.sigma, cfg.g, cfg.k, cfg.M)
+    plan.kernel_k(cp.codes, cp.offsets, N, K, None)
+    plan.close()
+    assert refs.digest_np(K.cpu().numpy()) == int(gold["digests"]["K"])
+
+
 def test_errors(gk):
     with pytest.raises(gk.GakcoError) as e:
         gk.Plan(4, 3, 4, 0)
