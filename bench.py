@@ -135,18 +135,27 @@ def oracle_sample(cp, cfg, seconds, threads):
     suffix = np.cumsum(n[::-1])[::-1]             # sum_{y>=x} n_y
     row_work = n * suffix                          # window steps of row x (y >= x)
     total = row_work.sum()
-    t0 = time.perf_counter()
-    oracle.digests(cp, cfg.g, cfg.k, cfg.M, threads=threads, row_begin=0, row_end=1, rows=False)
-    t1 = time.perf_counter() - t0
-    # calibration includes the K(X,X) pass (N pairs); subtract it from the per-row rate
-    rate = max(row_work[0], 1.0) / max(t1, 1e-4)
-    target = rate * seconds
-    r = int(np.searchsorted(np.cumsum(row_work), target)) + 1
-    r = max(1, min(cp.n_seq, r))
-    t0 = time.perf_counter()
-    oracle.digests(cp, cfg.g, cfg.k, cfg.M, threads=threads, row_begin=0, row_end=r, rows=False)
-    dt = time.perf_counter() - t0
-    frac = row_work[:r].sum() / total
+    cum = np.cumsum(row_work)
+
+    def run(r):
+        t0 = time.perf_counter()
+        oracle.digests(cp, cfg.g, cfg.k, cfg.M, threads=threads, row_begin=0, row_end=r,
+                       rows=False)
+        return time.perf_counter() - t0
+
+    # calibrate on a growing row count (each run also pays the K(X,X) pass), then
+    # size the sample so that it takes about `seconds`
+    r = max(1, min(cp.n_seq, threads))
+    dt = run(r)
+    while dt < 0.1 * seconds and r < cp.n_seq:
+        r = min(cp.n_seq, r * 4)
+        dt = run(r)
+    if dt < 0.5 * seconds and r < cp.n_seq:
+        rate = cum[r - 1] / max(dt, 1e-6)
+        r = int(np.searchsorted(cum, rate * seconds)) + 1
+        r = max(1, min(cp.n_seq, r))
+        dt = run(r)
+    frac = cum[r - 1] / total
     return dt, frac, r
 
 
