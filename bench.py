@@ -206,15 +206,18 @@ def config_dict(name, cfg, cp, masks, n, world):
 # ----------------------------------------------------------------- GPU arm
 def stage_model(stats, cfg, N):
     """Algorithmic bytes / ops per stage: unit x count."""
+    # composites are 8 B, or 4 B where key + sequence bits fit 32 (keys32)
     keys, passes = stats["keys"], stats["sort_passes"]
+    k32, p32 = stats.get("keys32", 0), stats.get("sort_passes32", 0)
+    kbytes = 8.0 * (keys - k32) + 4.0 * k32
     trip, grp = stats["triples"], stats["groups_multi"]
     M = cfg.M
     epi = N * N * ((M + 1) * 4 + (M + 1) * 4 + (M + 1) * 8 + 16) + N * (M + 1) * 8
     return {
-        "encode": ("hbm", 12.0 * keys),            # write 8 B key + read 4 B seq id
-        "sort": ("hbm", 16.0 * passes),            # read + write 8 B per key per pass
-        "segment": ("hbm", 8.0 * keys + 16.0 * trip + 8.0 * grp),
-        "light": ("hbm", 16.0 * stats["light_pairs"]),  # int64 read-modify-write per update
+        "encode": ("hbm", kbytes + 4.0 * keys),    # write the key + read the 4 B seq id
+        "sort": ("hbm", 16.0 * (passes - p32) + 8.0 * p32),  # read + write per key per pass
+        "segment": ("hbm", kbytes + 8.0 * trip + 8.0 * grp),  # read keys; write triples, groups
+        "light": ("hbm", 8.0 * stats["light_pairs"]),  # u32 read-modify-write per update
         "heavy": ("tensor", 2.0 * stats["heavy_macs"]),
         "epilogue": ("hbm", float(epi)),
     }

@@ -81,6 +81,8 @@ typedef struct {
     double ms_encode, ms_sort, ms_segment, ms_light, ms_heavy, ms_epilogue;
     /* kernel launches per stage (same stages as the ms_* fields) */
     int64_t n_encode, n_sort, n_segment, n_light, n_heavy, n_epilogue;
+    int64_t keys32;         /* of `keys`, those carried as 32-bit composites */
+    int64_t sort_passes32;  /* of `sort_passes`, those over 32-bit composites */
 } gakco_stats;
 
 /* Create a plan for alphabet size sigma (1..255), g-mer length g (1..32),

@@ -52,9 +52,11 @@ cudaError_t launch_check_codes(const uint8_t* codes, int64_t len, int sigma, int
 
 // grid.y = mask within the batch; grid.x strides over g-mers.
 // kept[b*GMAX + r] = r-th kept position of mask b (ascending).
+// K = uint32_t when the composite fits 32 bits (half the key traffic downstream).
+template <typename K>
 __global__ void __launch_bounds__(256) encode_kernel(CorpusView cv, const uint8_t* __restrict__ kept,
                                                      int nkept, int sigma, int sb, int npass,
-                                                     uint64_t* __restrict__ out,
+                                                     K* __restrict__ out,
                                                      uint32_t* __restrict__ hist) {
     __shared__ uint32_t sh[MAXPASS][RADIX];
     __shared__ uint8_t sk[GMAX];
@@ -63,7 +65,7 @@ __global__ void __launch_bounds__(256) encode_kernel(CorpusView cv, const uint8_
     if (threadIdx.x < GMAX) sk[threadIdx.x] = kept[b * GMAX + threadIdx.x];
     __syncthreads();
     const uint64_t n = cv.n;
-    uint64_t* o = out + (uint64_t)b * n;
+    K* o = out + (uint64_t)b * n;
     for (uint64_t j = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; j < n;
          j += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t x = cv.gm_seq[j];
@@ -71,7 +73,7 @@ __global__ void __launch_bounds__(256) encode_kernel(CorpusView cv, const uint8_
         uint64_t key = 0;
         for (int r = 0; r < nkept; ++r) key = key * (uint64_t)sigma + p[sk[r]];
         const uint64_t comp = (key << sb) | x;
-        o[j] = comp;
+        o[j] = (K)comp;
         for (int q = 0; q < npass; ++q) atomicAdd(&sh[q][(comp >> (sb + RADIX_BITS * q)) & 0xff], 1u);
     }
     __syncthreads();
@@ -82,12 +84,18 @@ __global__ void __launch_bounds__(256) encode_kernel(CorpusView cv, const uint8_
 }
 
 cudaError_t launch_encode(const CorpusView& cv, const uint8_t* kept, int nkept, int sigma, int sb,
-                          int nmask, int npass, uint64_t* out, uint32_t* hist, cudaStream_t s) {
+                          int nmask, int npass, void* out, bool k64, uint32_t* hist,
+                          cudaStream_t s) {
     if (cv.n == 0 || nmask == 0) return cudaGetLastError();
     uint64_t blocks = (cv.n + 256 * 8 - 1) / (256 * 8);
     if (blocks > 1024) blocks = 1024;
     dim3 grid((unsigned)blocks, (unsigned)nmask);
-    encode_kernel<<<grid, 256, 0, s>>>(cv, kept, nkept, sigma, sb, npass, out, hist);
+    if (k64)
+        encode_kernel<uint64_t><<<grid, 256, 0, s>>>(cv, kept, nkept, sigma, sb, npass,
+                                                     (uint64_t*)out, hist);
+    else
+        encode_kernel<uint32_t><<<grid, 256, 0, s>>>(cv, kept, nkept, sigma, sb, npass,
+                                                     (uint32_t*)out, hist);
     return cudaGetLastError();
 }
 

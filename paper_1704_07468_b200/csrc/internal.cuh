@@ -160,16 +160,18 @@ struct SegmentOut {
 cudaError_t launch_gmer_index(const int64_t* gofs, int64_t N, uint32_t* gm_seq, cudaStream_t s);
 cudaError_t launch_check_codes(const uint8_t* codes, int64_t len, int sigma, int* flags,
                                cudaStream_t s);
+// Keys are u64, or u32 (k64 = false) when key bits + sequence bits <= 32.
 cudaError_t launch_encode(const CorpusView& cv, const uint8_t* kept, int nkept, int sigma, int sb,
-                          int nmask, int npass, uint64_t* out, uint32_t* hist, cudaStream_t s);
+                          int nmask, int npass, void* out, bool k64, uint32_t* hist,
+                          cudaStream_t s);
 cudaError_t launch_onesweep(const uint64_t* in, uint64_t* out, uint64_t n, int nseg, int shift,
                             const uint32_t* hist, int pass, int npass, uint64_t* status,
                             uint32_t* ctr, uint32_t epoch, cudaStream_t s);
 // Chunked LSD pass (radix_hist + radix_scatter); hist: >= (target_ctas + nseg) * 256 u32.
-cudaError_t launch_radix_chunked(const uint64_t* in, uint64_t* out, uint64_t n, int nseg,
+cudaError_t launch_radix_chunked(const void* in, void* out, bool k64, uint64_t n, int nseg,
                                  int shift, uint32_t* hist, int target_ctas, cudaStream_t s);
 // counters: 2 u32 (triples, groups) reserved per tile; zeroed by the launcher.
-cudaError_t launch_segment(const uint64_t* keys, uint64_t n, int nseg, int sb, int64_t N,
+cudaError_t launch_segment(const void* keys, bool k64, uint64_t n, int nseg, int sb, int64_t N,
                            int64_t* Cm, uint32_t* counters, SegmentOut so,
                            unsigned long long* stats, cudaStream_t s);
 // Light pair updates; a group with >= heavy_min sequences (and counts <= 255)

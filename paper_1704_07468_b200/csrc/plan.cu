@@ -474,7 +474,7 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
                   (const uint32_t*)p->gmseq.p, N, n};
     SegmentOut so{(uint32_t*)p->tseq.p, (uint32_t*)p->tcnt.p, (uint2*)p->gstart.p,
                   (uint32_t*)p->counts.p};
-    int64_t passkeys = 0;
+    int64_t passkeys = 0, keys32 = 0, passkeys32 = 0;
     const size_t nn = (size_t)N * N;
     auto level_ptr = [&](int m) -> int64_t* {
         return only_level >= 0 ? C : C + (size_t)m * nn;
@@ -551,35 +551,41 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
         if (n > 0) {
             p->stage_begin(s, &a);
             const bool onesweep = p->sort_mode == 1;
+            // 32-bit composites when key + sequence bits fit (half the key traffic)
+            const bool k64 = onesweep || kb + sb > 32;
             if (onesweep) CK(cudaMemsetAsync(p->hist.p, 0, (size_t)nmask * MAXPASS * RADIX * 4, s));
             LK(launch_encode(cv, (const uint8_t*)p->kept.p + pos * GMAX, g - m, p->sigma, sb,
-                             nmask, onesweep ? npass : 0, (uint64_t*)p->keysA.p,
-                             (uint32_t*)p->hist.p, s));
+                             nmask, onesweep ? npass : 0, p->keysA.p, k64, (uint32_t*)p->hist.p,
+                             s));
             p->stage_end(s, S_ENCODE, a);
 
             p->stage_begin(s, &a);
-            uint64_t* in = (uint64_t*)p->keysA.p;
-            uint64_t* outk = (uint64_t*)p->keysB.p;
+            void* in = p->keysA.p;
+            void* outk = p->keysB.p;
             for (int q = 0; q < npass; ++q) {
                 if (onesweep) {
                     uint32_t* c;
                     CK(p->next_ctr(s, &c));
-                    LK(launch_onesweep(in, outk, n, nmask, sb + RADIX_BITS * q,
-                                       (const uint32_t*)p->hist.p, q, npass,
+                    LK(launch_onesweep((const uint64_t*)in, (uint64_t*)outk, n, nmask,
+                                       sb + RADIX_BITS * q, (const uint32_t*)p->hist.p, q, npass,
                                        (uint64_t*)p->status.p, c, p->epoch++, s));
                 } else {
                     p->launches += 1;  // two kernels
-                    LK(launch_radix_chunked(in, outk, n, nmask, sb + RADIX_BITS * q,
+                    LK(launch_radix_chunked(in, outk, k64, n, nmask, sb + RADIX_BITS * q,
                                             (uint32_t*)p->hist.p, p->sort_ctas_per_sm * p->sm_count,
                                             s));
                 }
                 std::swap(in, outk);
             }
             passkeys += (int64_t)npass * nmask * (int64_t)n;
+            if (!k64) {
+                keys32 += (int64_t)nmask * (int64_t)n;
+                passkeys32 += (int64_t)npass * nmask * (int64_t)n;
+            }
             p->stage_end(s, S_SORT, a);
 
             p->stage_begin(s, &a);
-            LK(launch_segment(in, n, nmask, sb, N, Cm, so.counts, so, stats, s));
+            LK(launch_segment(in, k64, n, nmask, sb, N, Cm, so.counts, so, stats, s));
             p->stage_end(s, S_SEGMENT, a);
 
             p->stage_begin(s, &a);
@@ -609,6 +615,8 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
     p->host_stats.masks = (int64_t)mine.size();
     p->host_stats.keys = (int64_t)mine.size() * (int64_t)n;
     p->host_stats.sort_passes = passkeys;
+    p->host_stats.keys32 = keys32;
+    p->host_stats.sort_passes32 = passkeys32;
     p->after_accumulate = true;
     return GAKCO_OK;
 #undef CK

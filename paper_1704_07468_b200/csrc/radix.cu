@@ -182,9 +182,11 @@ cudaError_t launch_onesweep(const uint64_t* in, uint64_t* out, uint64_t n, int n
 constexpr int RS_THREADS = SORT_THREADS;  // 512
 constexpr int RS_WARPS = RS_THREADS / 32;
 
+template <typename K>
 __global__ void __launch_bounds__(RS_THREADS) radix_hist_kernel(
-    const uint64_t* __restrict__ in, uint64_t n, uint32_t cps, uint64_t L, int shift,
+    const K* __restrict__ in, uint64_t n, uint32_t cps, uint64_t L, int shift,
     uint32_t* __restrict__ hist) {
+    constexpr int E = 16 / sizeof(K);  // keys per 16-byte load
     __shared__ uint32_t s_h[RS_WARPS][RADIX];
     const int tid = threadIdx.x, w = tid >> 5;
     for (int i = tid; i < RS_WARPS * RADIX; i += RS_THREADS) (&s_h[0][0])[i] = 0;
@@ -192,26 +194,24 @@ __global__ void __launch_bounds__(RS_THREADS) radix_hist_kernel(
     const uint32_t seg = blockIdx.x / cps, c = blockIdx.x - seg * cps;
     const uint64_t lo = (uint64_t)c * L;
     const uint64_t hi = min(n, lo + L);
-    const uint64_t* p = in + (uint64_t)seg * n;
+    const K* p = in + (uint64_t)seg * n;
     if (lo < hi) {
-        // 16-byte loads on the even-aligned body, scalars on the edges
-        uint64_t a = lo, b = hi;
-        const uint64_t base = (uint64_t)seg * n;
-        if ((base + a) & 1) {
-            if (tid == 0) atomicAdd(&s_h[0][(p[a] >> shift) & 0xff], 1u);
+        // 16-byte loads on the aligned body, scalars on the edges
+        uint64_t a = lo;
+        while (a < hi && ((uintptr_t)(p + a) & 15)) {
+            if (tid == 0) atomicAdd(&s_h[0][(uint32_t)(p[a] >> shift) & 0xff], 1u);
             ++a;
         }
-        if ((b - a) & 1) {
-            if (tid == 0) atomicAdd(&s_h[0][(p[b - 1] >> shift) & 0xff], 1u);
-            --b;
-        }
-        const ulonglong2* v = (const ulonglong2*)(p + a);
-        const uint64_t nv = (b - a) / 2;
+        const uint64_t nv = (hi - a) / E;
+        const uint4* v = (const uint4*)(p + a);
         for (uint64_t i = tid; i < nv; i += RS_THREADS) {
-            const ulonglong2 q = v[i];
-            atomicAdd(&s_h[w][(q.x >> shift) & 0xff], 1u);
-            atomicAdd(&s_h[w][(q.y >> shift) & 0xff], 1u);
+            const uint4 q = v[i];
+            const K* kq = (const K*)&q;
+#pragma unroll
+            for (int e = 0; e < E; ++e) atomicAdd(&s_h[w][(uint32_t)(kq[e] >> shift) & 0xff], 1u);
         }
+        for (uint64_t i = a + nv * E + tid; i < hi; i += RS_THREADS)
+            atomicAdd(&s_h[w][(uint32_t)(p[i] >> shift) & 0xff], 1u);
     }
     __syncthreads();
     if (tid < RADIX) {
@@ -221,12 +221,13 @@ __global__ void __launch_bounds__(RS_THREADS) radix_hist_kernel(
     }
 }
 
+template <typename K>
 __global__ void __launch_bounds__(RS_THREADS) radix_scatter_kernel(
-    const uint64_t* __restrict__ in, uint64_t* __restrict__ out, uint64_t n, uint32_t cps,
+    const K* __restrict__ in, K* __restrict__ out, uint64_t n, uint32_t cps,
     uint64_t L, int shift, const uint32_t* __restrict__ hist) {
     extern __shared__ __align__(16) unsigned char smem[];
-    uint64_t* s_keys = (uint64_t*)smem;                                  // [SORT_TILE]
-    int64_t* s_run = (int64_t*)(s_keys + SORT_TILE);                     // [RADIX]
+    K* s_keys = (K*)smem;                                                // [SORT_TILE]
+    int64_t* s_run = (int64_t*)(smem + SORT_TILE * sizeof(K));           // [RADIX]
     uint32_t(*s_whist)[RADIX] = (uint32_t(*)[RADIX])(s_run + RADIX);     // [WARPS][RADIX]
     uint32_t* s_doff = &s_whist[RS_WARPS][0];                            // [RADIX]
     uint32_t* s_cnt = s_doff + RADIX;                                    // [RADIX]
@@ -257,20 +258,20 @@ __global__ void __launch_bounds__(RS_THREADS) radix_scatter_kernel(
     const uint32_t lt = lanemask_lt();
     // register double buffer: the next tile's keys are in flight while this one
     // is ranked and scattered
-    uint64_t nxt[SORT_ITEMS];
+    K nxt[SORT_ITEMS];
     {
         const uint32_t cnt0 = (uint32_t)min((uint64_t)SORT_TILE, hi > lo ? hi - lo : 0);
 #pragma unroll
         for (int i = 0; i < SORT_ITEMS; ++i) {
             const uint32_t idx = w * SORT_ITEMS * 32 + i * 32 + lane;
-            nxt[i] = idx < cnt0 ? in[seg_base + lo + idx] : 0ull;
+            nxt[i] = idx < cnt0 ? in[seg_base + lo + idx] : (K)0;
         }
     }
     for (uint64_t t0 = lo; t0 < hi; t0 += SORT_TILE) {
         const uint32_t cnt = (uint32_t)min((uint64_t)SORT_TILE, hi - t0);
         for (int i = tid; i < RS_WARPS * RADIX; i += RS_THREADS) (&s_whist[0][0])[i] = 0;
         __syncthreads();
-        uint64_t keys[SORT_ITEMS];
+        K keys[SORT_ITEMS];
         uint32_t rank[SORT_ITEMS];
 #pragma unroll
         for (int i = 0; i < SORT_ITEMS; ++i) keys[i] = nxt[i];
@@ -280,7 +281,7 @@ __global__ void __launch_bounds__(RS_THREADS) radix_scatter_kernel(
 #pragma unroll
             for (int i = 0; i < SORT_ITEMS; ++i) {
                 const uint32_t idx = w * SORT_ITEMS * 32 + i * 32 + lane;
-                nxt[i] = idx < cnt1 ? in[seg_base + t1 + idx] : 0ull;
+                nxt[i] = idx < cnt1 ? in[seg_base + t1 + idx] : (K)0;
             }
         }
         // stable in-warp ranking: lanes with the same digit find each other with a
@@ -329,7 +330,7 @@ __global__ void __launch_bounds__(RS_THREADS) radix_scatter_kernel(
         }
         __syncthreads();
         for (uint32_t j = tid; j < cnt; j += RS_THREADS) {
-            const uint64_t k = s_keys[j];
+            const K k = s_keys[j];
             const uint32_t d = (uint32_t)(k >> shift) & 0xffu;
             out[seg_base + (uint64_t)(s_run[d] + (int64_t)(j - s_doff[d]))] = k;
         }
@@ -339,26 +340,38 @@ __global__ void __launch_bounds__(RS_THREADS) radix_scatter_kernel(
     }
 }
 
-constexpr size_t RS_SMEM = SORT_TILE * 8 + RADIX * 8 + 2 * RS_WARPS * RADIX * 4 +
-                           2 * RADIX * 4 + 16 * 4;
+template <typename K>
+constexpr size_t rs_smem() {
+    return SORT_TILE * sizeof(K) + RADIX * 8 + 2 * RS_WARPS * RADIX * 4 + 2 * RADIX * 4 + 16 * 4;
+}
 
-cudaError_t launch_radix_chunked(const uint64_t* in, uint64_t* out, uint64_t n, int nseg,
-                                 int shift, uint32_t* hist, int target_ctas, cudaStream_t s) {
-    if (n == 0 || nseg == 0) return cudaGetLastError();
+template <typename K>
+static cudaError_t radix_chunked(const K* in, K* out, uint64_t n, int nseg, int shift,
+                                 uint32_t* hist, int target_ctas, cudaStream_t s) {
     // chunks per segment: fill ~target_ctas CTAs, whole 4096-key tiles per chunk
     uint64_t tiles = (n + SORT_TILE - 1) / SORT_TILE;
     uint64_t cps = std::max<uint64_t>(1, std::min<uint64_t>(tiles, (target_ctas + nseg - 1) / nseg));
     uint64_t L = (tiles + cps - 1) / cps * SORT_TILE;
     cps = (n + L - 1) / L;
     const unsigned grid = (unsigned)(cps * nseg);
-    radix_hist_kernel<<<grid, RS_THREADS, 0, s>>>(in, n, (uint32_t)cps, L, shift, hist);
+    radix_hist_kernel<K><<<grid, RS_THREADS, 0, s>>>(in, n, (uint32_t)cps, L, shift, hist);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    cudaFuncSetAttribute(radix_scatter_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)RS_SMEM);
-    radix_scatter_kernel<<<grid, RS_THREADS, RS_SMEM, s>>>(in, out, n, (uint32_t)cps, L, shift,
-                                                           hist);
+    cudaFuncSetAttribute(radix_scatter_kernel<K>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)rs_smem<K>());
+    radix_scatter_kernel<K><<<grid, RS_THREADS, rs_smem<K>(), s>>>(in, out, n, (uint32_t)cps, L,
+                                                                   shift, hist);
     return cudaGetLastError();
+}
+
+cudaError_t launch_radix_chunked(const void* in, void* out, bool k64, uint64_t n, int nseg,
+                                 int shift, uint32_t* hist, int target_ctas, cudaStream_t s) {
+    if (n == 0 || nseg == 0) return cudaGetLastError();
+    if (k64)
+        return radix_chunked<uint64_t>((const uint64_t*)in, (uint64_t*)out, n, nseg, shift, hist,
+                                       target_ctas, s);
+    return radix_chunked<uint32_t>((const uint32_t*)in, (uint32_t*)out, n, nseg, shift, hist,
+                                   target_ctas, s);
 }
 
 }  // namespace gk

@@ -24,8 +24,9 @@
 
 namespace gk {
 
+template <typename K>
 __global__ void __launch_bounds__(SEG_THREADS) segment_kernel(
-    const uint64_t* __restrict__ keys, uint64_t n, uint64_t total, int sb, int64_t N,
+    const K* __restrict__ keys, uint64_t n, uint64_t total, int sb, int64_t N,
     int64_t* Cm, uint32_t* counters, SegmentOut so, unsigned long long* stats) {
     __shared__ uint32_t s_w[8];
     __shared__ uint32_t s_gpos[SEG_TILE];
@@ -41,28 +42,30 @@ __global__ void __launch_bounds__(SEG_THREADS) segment_kernel(
     }
     __syncthreads();
 
-    uint64_t cur[SEG_ITEMS];
+    K cur[SEG_ITEMS];
     if (base + SEG_ITEMS <= total) {
-        const ulonglong2* v = (const ulonglong2*)(keys + base);
+        constexpr int NV = SEG_ITEMS * sizeof(K) / 16;
+        const uint4* v = (const uint4*)(keys + base);
 #pragma unroll
-        for (int i = 0; i < SEG_ITEMS / 2; ++i) {
-            ulonglong2 q = v[i];
-            cur[2 * i] = q.x;
-            cur[2 * i + 1] = q.y;
+        for (int i = 0; i < NV; ++i) {
+            const uint4 q = v[i];
+            const K* kq = (const K*)&q;
+#pragma unroll
+            for (int e = 0; e < 16 / (int)sizeof(K); ++e) cur[i * (16 / sizeof(K)) + e] = kq[e];
         }
     } else {
 #pragma unroll
-        for (int i = 0; i < SEG_ITEMS; ++i) cur[i] = base + i < total ? keys[base + i] : 0ull;
+        for (int i = 0; i < SEG_ITEMS; ++i) cur[i] = base + i < total ? keys[base + i] : (K)0;
     }
-    const uint64_t prev = (base < total && base % n != 0) ? keys[base - 1] : 0ull;
+    const K prev = (base < total && base % n != 0) ? keys[base - 1] : (K)0;
 
     uint32_t th_bits = 0, gh_bits = 0, multi_bits = 0;
     uint32_t cnt[SEG_ITEMS];
 #pragma unroll
     for (int i = 0; i < SEG_ITEMS; ++i) {
         const uint64_t idx = base + i;
-        const uint64_t c0 = cur[i];
-        const uint64_t p0 = i == 0 ? prev : cur[i - 1];
+        const K c0 = cur[i];
+        const K p0 = i == 0 ? prev : cur[i - 1];
         cnt[i] = 0;
         if (idx >= total) continue;
         const bool first = (idx % n) == 0;
@@ -71,7 +74,7 @@ __global__ void __launch_bounds__(SEG_THREADS) segment_kernel(
         // run end j and the key that follows it
         const uint64_t seg_end = (idx / n + 1) * n;
         uint64_t j = idx + 1;
-        uint64_t nk = ~c0;
+        K nk = (K)~c0;
         bool found = false;
 #pragma unroll
         for (int k = i + 1; k < SEG_ITEMS; ++k) {
@@ -86,7 +89,7 @@ __global__ void __launch_bounds__(SEG_THREADS) segment_kernel(
         }
         if (!found && j < seg_end) {
             while (j < seg_end) {
-                const uint64_t kk = keys[j];
+                const K kk = keys[j];
                 if (kk != c0) {
                     nk = kk;
                     break;
@@ -130,18 +133,18 @@ __global__ void __launch_bounds__(SEG_THREADS) segment_kernel(
                           (keys[tile_end] >> sb) == (keys[tile_end - 1] >> sb);
     uint64_t gend_key = tile_end;  // one past the crossing group's last key
     if (crossing && warp == 0) {
-        const uint64_t gkey = keys[tile_end - 1] >> sb;
+        const K gkey = keys[tile_end - 1] >> sb;
         const uint64_t seg_end = (tile_end / n + 1) * n;
         uint32_t nt = 0;
         uint64_t e = tile_end;
-        uint64_t last = keys[tile_end - 1];
+        K last = keys[tile_end - 1];
         while (true) {
             const uint64_t q = e + lane;
-            const uint64_t kk = q < seg_end ? keys[q] : ~0ull;
+            const K kk = q < seg_end ? keys[q] : (K)~(K)0;
             const bool in = q < seg_end && (kk >> sb) == gkey;
             const uint32_t inm = __ballot_sync(0xffffffffu, in);
-            const uint64_t pk = __shfl_up_sync(0xffffffffu, kk, 1);
-            const uint64_t pv = lane == 0 ? last : pk;
+            const K pk = __shfl_up_sync(0xffffffffu, kk, 1);
+            const K pv = lane == 0 ? last : pk;
             nt += __popc(__ballot_sync(0xffffffffu, in && kk != pv));
             const uint32_t run = ~inm ? __ffs(~inm) - 1 : 32;  // leading in-group lanes
             if (run < 32) {
@@ -183,13 +186,13 @@ __global__ void __launch_bounds__(SEG_THREADS) segment_kernel(
     if (tail && warp == 0) {
         const uint64_t seg_end = (tile_end / n + 1) * n;
         uint32_t w = s_base_t + agg_t;
-        uint64_t last = keys[tile_end - 1];
+        K last = keys[tile_end - 1];
         for (uint64_t e = tile_end; e < gend_key; e += 32) {
             const uint64_t q = e + lane;
             const bool in = q < gend_key;
-            const uint64_t kk = in ? keys[q] : 0ull;
-            const uint64_t pk = __shfl_up_sync(0xffffffffu, kk, 1);
-            const uint64_t pv = lane == 0 ? last : pk;
+            const K kk = in ? keys[q] : (K)0;
+            const K pk = __shfl_up_sync(0xffffffffu, kk, 1);
+            const K pv = lane == 0 ? last : pk;
             const bool head = in && kk != pv;
             const uint32_t hm = __ballot_sync(0xffffffffu, head);
             if (head) {
@@ -205,15 +208,19 @@ __global__ void __launch_bounds__(SEG_THREADS) segment_kernel(
     }
 }
 
-cudaError_t launch_segment(const uint64_t* keys, uint64_t n, int nseg, int sb, int64_t N,
+cudaError_t launch_segment(const void* keys, bool k64, uint64_t n, int nseg, int sb, int64_t N,
                            int64_t* Cm, uint32_t* counters, SegmentOut so,
                            unsigned long long* stats, cudaStream_t s) {
     cudaError_t e = cudaMemsetAsync(counters, 0, 2 * sizeof(uint32_t), s);
     uint64_t total = n * (uint64_t)nseg;
     if (e != cudaSuccess || total == 0) return e;
     uint64_t tiles = (total + SEG_TILE - 1) / SEG_TILE;
-    segment_kernel<<<(unsigned)tiles, SEG_THREADS, 0, s>>>(keys, n, total, sb, N, Cm, counters, so,
-                                                           stats);
+    if (k64)
+        segment_kernel<uint64_t><<<(unsigned)tiles, SEG_THREADS, 0, s>>>(
+            (const uint64_t*)keys, n, total, sb, N, Cm, counters, so, stats);
+    else
+        segment_kernel<uint32_t><<<(unsigned)tiles, SEG_THREADS, 0, s>>>(
+            (const uint32_t*)keys, n, total, sb, N, Cm, counters, so, stats);
     return cudaGetLastError();
 }
 
