@@ -64,7 +64,10 @@ typedef enum {
     GAKCO_OPT_TIMING = 3,         /* 1 = record per-stage CUDA events (gakco_get_stats) */
     GAKCO_OPT_SORT = 4,           /* LSD pass kernel: 0 = chunked two-kernel pass (default),
                                      1 = onesweep with decoupled look-back */
-    GAKCO_OPT_SORT_CTAS_PER_SM = 5 /* chunked pass grid size in CTAs per SM (default 2) */
+    GAKCO_OPT_SORT_CTAS_PER_SM = 5, /* chunked pass grid size in CTAs per SM (default 3) */
+    GAKCO_OPT_LIGHT_BINS = 6      /* light updates binned by accumulator block (ablation /
+                                     test knob): <= 0 = never (default; measured slower on
+                                     Scale), > 0 = always, with this many cells per block */
 } gakco_option;
 
 /* Counters of the last gakco_accumulate (algorithmic units). */

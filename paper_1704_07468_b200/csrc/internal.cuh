@@ -178,10 +178,20 @@ cudaError_t launch_segment(const void* keys, bool k64, uint64_t n, int nseg, int
 // instead claims column c = atomicAdd(dense_fill) (< ldd) of the dense count
 // matrix D (u8, slabs of 128 columns: byte (c/128)*n_pad*128 + row*128 + c%128)
 // and scatters its counts there, for the tensor-core Gram.
+// Record buckets for light updates when the accumulator is much larger than L2:
+// nb buckets of cap u32 records, bucket b covering accumulator cells
+// [b*block_cells, (b+1)*block_cells); nb = 0 disables binning.
+struct LightBins {
+    uint32_t* rec;
+    uint32_t* cnt;
+    uint64_t cap;
+    uint64_t block_cells;
+    int nb;
+};
 cudaError_t launch_light(SegmentOut so, uint64_t max_groups, int64_t heavy_min, int64_t N,
                          uint32_t* acc, uint2* heavy_list, uint64_t ldd,
-                         uint32_t* dense_fill, unsigned long long* stats, int sm_count,
-                         cudaStream_t s);
+                         uint32_t* dense_fill, LightBins bins, unsigned long long* stats,
+                         int sm_count, cudaStream_t s);
 // Fill the D slabs of the columns claimed by this batch ([prev, fill) with
 // prev = dense_fill[1], a multiple of 128) from the batch's triples, in shared
 // memory, with full-line stores; then round dense_fill[0] up to a multiple of 128

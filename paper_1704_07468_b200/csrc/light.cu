@@ -21,9 +21,60 @@ __device__ __forceinline__ uint64_t tri_index(uint32_t x, uint32_t y, int64_t N)
     return (uint64_t)x * (uint64_t)(N - 1) - (uint64_t)x * (x - 1) / 2 + (y - x - 1);
 }
 
+// One pair update acc[idx] += val, called by all 32 lanes (valid marks real
+// updates). With binning on (large N: the accumulator is far bigger than L2),
+// small updates become 4-byte records (cell offset << 4 | val) appended to the
+// bucket of their accumulator block, to be applied block by block while the
+// block is L2-resident (apply_bins_kernel); anything else is a direct atomic.
+__device__ __forceinline__ void pair_add(uint32_t* acc, const LightBins& bn, bool valid,
+                                         uint64_t idx, uint32_t val) {
+    if (bn.nb == 0) {
+        if (valid) atomicAdd(&acc[idx], val);
+        return;
+    }
+    const uint32_t b = valid ? (uint32_t)(idx / bn.block_cells) : 0xffffffffu;
+    const bool rec = valid && val < 16u;
+    if (valid && !rec) atomicAdd(&acc[idx], val);
+    const uint32_t peers = __match_any_sync(0xffffffffu, rec ? b : 0xffffffffu);
+    if (rec) {
+        const int lane = threadIdx.x & 31;
+        const int leader = __ffs(peers) - 1;
+        uint32_t base = 0;
+        if (lane == leader) base = atomicAdd(&bn.cnt[b], (uint32_t)__popc(peers));
+        base = __shfl_sync(peers, base, leader);
+        const uint64_t pos = (uint64_t)base + __popc(peers & lanemask_lt());
+        if (pos < bn.cap)
+            bn.rec[(uint64_t)b * bn.cap + pos] =
+                ((uint32_t)(idx - (uint64_t)b * bn.block_cells) << 4) | val;
+        else
+            atomicAdd(&acc[idx], val);  // bucket full
+    }
+}
+
+__global__ void apply_bins_kernel(uint32_t* __restrict__ acc, LightBins bn, int b) {
+    const uint64_t c = min((uint64_t)bn.cnt[b], bn.cap);
+    const uint32_t* r = bn.rec + (uint64_t)b * bn.cap;
+    uint32_t* a = acc + (uint64_t)b * bn.block_cells;
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < c;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t v = r[i];
+        atomicAdd(&a[v >> 4], v & 15u);
+    }
+}
+
+cudaError_t launch_apply_bins(uint32_t* acc, LightBins bn, int sm_count, cudaStream_t s) {
+    for (int b = 0; b < bn.nb; ++b) {  // one block at a time: L2-resident atomics
+        apply_bins_kernel<<<sm_count * 8, 256, 0, s>>>(acc, bn, b);
+        cudaError_t e = cudaGetLastError();
+        if (e != cudaSuccess) return e;
+    }
+    return cudaMemsetAsync(bn.cnt, 0, bn.nb * sizeof(uint32_t), s);
+}
+
 __global__ void __launch_bounds__(256) light_kernel(SegmentOut so, int64_t heavy_min, int64_t N,
                                                     uint32_t* acc, uint2* heavy_list,
                                                     uint64_t ldd, uint32_t* dense_fill,
+                                                    LightBins bn,
                                                     unsigned long long* stats) {
     // triangle table: pairs (a < b < 32) ordered by b, so the first n(n-1)/2
     // entries are exactly the pairs of an n-triple chunk
@@ -71,12 +122,16 @@ __global__ void __launch_bounds__(256) light_kernel(SegmentOut so, int64_t heavy
             }
             const uint32_t ej = __shfl_sync(0xffffffffu, excl, j);
             const uint32_t sj = __shfl_sync(0xffffffffu, my_start, j);
+            uint64_t idx = 0;
+            uint32_t val = 0;
             if (q < Ptot) {
                 const uint32_t ab = s_tri[q - ej];
                 const uint32_t ta = sj + (ab & 31), tb = sj + (ab >> 5);
                 const uint32_t xa = so.tseq[ta] & 0x7fffffffu, xb = so.tseq[tb] & 0x7fffffffu;
-                atomicAdd(&acc[tri_index(xa, xb, N)], so.tcnt[ta] * so.tcnt[tb]);
+                idx = tri_index(xa, xb, N);
+                val = so.tcnt[ta] * so.tcnt[tb];
             }
+            pair_add(acc, bn, q < Ptot, idx, val);
         }
 
         // (2) the other groups one by one (big light groups and heavy candidates)
@@ -136,7 +191,7 @@ __global__ void __launch_bounds__(256) light_kernel(SegmentOut so, int64_t heavy
                     const uint32_t ca = __shfl_sync(0xffffffffu, cA, a);
                     const uint32_t xb = __shfl_sync(0xffffffffu, xA, b);
                     const uint32_t cb = __shfl_sync(0xffffffffu, cA, b);
-                    if (q < P) atomicAdd(&acc[tri_index(xa, xb, N)], ca * cb);
+                    pair_add(acc, bn, q < P, q < P ? tri_index(xa, xb, N) : 0, ca * cb);
                 }
                 for (uint32_t B = A + 32; B < b0; B += 32) {
                     const uint32_t ib = B + lane;
@@ -146,7 +201,7 @@ __global__ void __launch_bounds__(256) light_kernel(SegmentOut so, int64_t heavy
                     for (uint32_t a = 0; a < na; ++a) {
                         const uint32_t xa = __shfl_sync(0xffffffffu, xA, a);
                         const uint32_t ca = __shfl_sync(0xffffffffu, cA, a);
-                        if (vb) atomicAdd(&acc[tri_index(xa, xB, N)], ca * cB);
+                        pair_add(acc, bn, vb, vb ? tri_index(xa, xB, N) : 0, ca * cB);
                     }
                 }
             }
@@ -158,15 +213,17 @@ __global__ void __launch_bounds__(256) light_kernel(SegmentOut so, int64_t heavy
 
 cudaError_t launch_light(SegmentOut so, uint64_t max_groups, int64_t heavy_min, int64_t N,
                          uint32_t* acc, uint2* heavy_list, uint64_t ldd,
-                         uint32_t* dense_fill, unsigned long long* stats, int sm_count,
-                         cudaStream_t s) {
+                         uint32_t* dense_fill, LightBins bins, unsigned long long* stats,
+                         int sm_count, cudaStream_t s) {
     if (max_groups == 0) return cudaGetLastError();
     uint64_t blocks = (max_groups + 255) / 256;  // 8 warps x 32 groups per block-round
     uint64_t cap = (uint64_t)sm_count * 8;
     if (blocks > cap) blocks = cap;
     light_kernel<<<(unsigned)blocks, 256, 0, s>>>(so, heavy_min, N, acc, heavy_list, ldd,
-                                                  dense_fill, stats);
-    return cudaGetLastError();
+                                                  dense_fill, bins, stats);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess || bins.nb == 0) return e;
+    return launch_apply_bins(acc, bins, sm_count, s);
 }
 
 // C_m(X,Y) += acc[(X,Y)] for every X < Y, and acc is zeroed again (one pass over

@@ -78,6 +78,7 @@ struct gakco_plan {
     bool timing = false;
     int sort_mode = 0;  // 0: chunked two-kernel LSD pass, 1: onesweep (decoupled look-back)
     int sort_ctas_per_sm = 3;  // chunked pass grid = this x SMs (measured best of 1..4)
+    int64_t light_bins = 0;    // 0 auto, < 0 off, > 0 forced block size in cells
     int sm_count = 148;
     std::string err;
 
@@ -88,7 +89,7 @@ struct gakco_plan {
 
     DevBuf codes, off, gofs, gmseq, keysA, keysB, hist, status, ctr, tseq, tcnt, gstart, gend,
         counts, kept, stats, flags, kdiag, Cscr, Nmscr, Kscr, Knscr, heavy, hcount, dense, tiles,
-        lightacc;
+        lightacc, binrec, bincnt;
     int64_t tiles_npad = -1;
     uint64_t dense_ldd = 0;
     int ntiles = 0;
@@ -244,7 +245,7 @@ extern "C" void gakco_destroy(gakco_plan* p) {
                       &p->hist,  &p->status, &p->ctr,  &p->tseq,   &p->tcnt,  &p->gstart,
                       &p->gend,  &p->counts, &p->kept, &p->stats,  &p->flags, &p->kdiag,
                       &p->Cscr,  &p->Nmscr, &p->Kscr,  &p->Knscr, &p->heavy, &p->hcount,
-                      &p->dense, &p->tiles, &p->lightacc};
+                      &p->dense, &p->tiles, &p->lightacc, &p->binrec, &p->bincnt};
     for (DevBuf* b : bufs)
         if (b->p) cudaFree(b->p);
     for (cudaEvent_t e : p->ev_pool) cudaEventDestroy(e);
@@ -272,6 +273,9 @@ extern "C" gakco_status gakco_set_option(gakco_plan* p, int option, int64_t valu
         case GAKCO_OPT_SORT:
             if (value < 0 || value > 1) return p->fail(GAKCO_E_ARG, "sort must be 0 or 1");
             p->sort_mode = (int)value;
+            return GAKCO_OK;
+        case GAKCO_OPT_LIGHT_BINS:
+            p->light_bins = value;
             return GAKCO_OK;
         case GAKCO_OPT_SORT_CTAS_PER_SM:
             if (value < 1 || value > 16) return p->fail(GAKCO_E_ARG, "1..16");
@@ -504,6 +508,27 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
     // C_m at a level change or before masks * n_max^2 could reach 2^32.
     const uint64_t ntri = (uint64_t)N * (uint64_t)(N - 1) / 2;
     CK(p->ensure(p->lightacc, ntri * 4 + 16, s, /*zero=*/true));
+    // light-update binning when the accumulator is far larger than L2 (Scale:
+    // 800 MB): records per 64 MB block, applied block by block (light.cu)
+    LightBins bins{nullptr, nullptr, 0, 0, 0};
+    {
+        uint64_t bc = 0;
+        // auto mode leaves binning OFF: measured 2.3x slower than direct atomics on
+        // Scale (match.any + record traffic cost more than the DRAM RMW saved)
+        if (p->light_bins > 0) bc = (uint64_t)p->light_bins;  // forced (tests, ablation)
+        if (bc > 0 && ntri > 0) {
+            bc = std::min<uint64_t>(bc, (1ull << 28) - 1);  // offset field: 28 bits
+            const int nb = (int)((ntri + bc - 1) / bc);
+            const uint64_t total_rec = std::max<uint64_t>(1ull << 20, std::min<uint64_t>(512ull << 20, ntri * 4));
+            // (forced mode is a test knob: tiny buckets also exercise the overflow path)
+            const uint64_t cap =
+                p->light_bins > 0 ? 64 : std::max<uint64_t>(1024, total_rec / nb);
+            CK(p->ensure(p->binrec, cap * nb * 4, s));
+            CK(p->ensure(p->bincnt, nb * 4 + 16, s, /*zero=*/true));
+            CK(cudaMemsetAsync(p->bincnt.p, 0, nb * 4, s));
+            bins = LightBins{(uint32_t*)p->binrec.p, (uint32_t*)p->bincnt.p, cap, bc, nb};
+        }
+    }
     uint64_t light_masks = 0;
     int light_m = -1;
     const uint64_t light_lim =
@@ -590,7 +615,7 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
 
             p->stage_begin(s, &a);
             LK(launch_light(so, n * nmask / 2 + 1, light_limit, N, (uint32_t*)p->lightacc.p,
-                            (uint2*)p->heavy.p, rcap, (uint32_t*)p->hcount.p, stats,
+                            (uint2*)p->heavy.p, rcap, (uint32_t*)p->hcount.p, bins, stats,
                             p->sm_count, s));
             p->stage_end(s, S_LIGHT, a);
             if (gram_ok) {

@@ -110,6 +110,20 @@ def test_heavy_light_equivalence(gk, oracle_lib):
         assert_parity(run(gk, cp, g, k, M), ref)
 
 
+def test_light_binning(gk, oracle_lib):
+    """Binned light updates (forced, tiny accumulator blocks so records span many
+    buckets and some buckets overflow to direct atomics) == oracle."""
+    rng = np.random.default_rng(107)
+    for _ in range(6):
+        sigma = int(rng.choice([2, 4, 20]))
+        g = int(rng.integers(2, 9))
+        k = int(rng.integers(1, g + 1))
+        cp = sc.random_small(rng, sigma, n_max=120, l_max=80)
+        ref = oracle_lib.compute(cp, g, k, g - k)
+        for cells in (7, 1000):
+            assert_parity(run(gk, cp, g, k, g - k, light_bins=cells, heavy_min_seqs=1 << 50), ref)
+
+
 def test_batch_size_invariance(gk, oracle_lib):
     """Different mask batch sizes give identical results (integer sums)."""
     cp = sc.make("tiny")
