@@ -103,6 +103,9 @@ gakco_status gakco_set_option(gakco_plan* plan, int option, int64_t value);
 
 /* Add this shard's contribution to C: for each of its masks, every pair of
  * sequences sharing a masked key adds count_X*count_Y.
+ * A code >= sigma gives GAKCO_E_SYMBOL: here if codes is a host pointer; for a
+ * device pointer the check runs on the device (no host sync) and the error is
+ * returned by the next gakco_finalize (C is then meaningless).
  *   codes    uint8[offsets[N]] symbol codes (host or device pointer)
  *   offsets  int64[N+1], offsets[0] = 0, non-decreasing (host or device)
  *   C        int64[(M+1)*N*N] DEVICE pointer; the UPPER triangle (Y >= X,

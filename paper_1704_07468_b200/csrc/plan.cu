@@ -107,6 +107,7 @@ struct gakco_plan {
     bool after_accumulate = false;
 
     std::vector<int64_t> h_off, h_gofs;
+    std::vector<uint8_t> kept_h;
 
     gakco_status fail(gakco_status s, const std::string& msg) {
         err = msg;
@@ -365,16 +366,15 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
 
     // corpus to device (+ symbol check)
     CK(p->ensure(p->codes, (size_t)L + 16, s));
-    CK(p->ensure(p->flags, 64, s));
-    CK(cudaMemsetAsync(p->flags.p, 0, sizeof(int), s));
+    CK(p->ensure(p->flags, 64, s, /*zero=*/true));
     if (L > 0) {
         if (is_device_ptr(codes)) {
+            // device codes are checked on the device without a host sync; a bad code
+            // sets flags[1] and is reported (GAKCO_E_SYMBOL) by gakco_finalize. The
+            // path stays memory-safe meanwhile (keys only index 256-bin digits).
             CK(cudaMemcpyAsync(p->codes.p, codes, L, cudaMemcpyDeviceToDevice, s));
-            LK(launch_check_codes((const uint8_t*)p->codes.p, L, p->sigma, (int*)p->flags.p, s));
-            int fl = 0;
-            CK(cudaMemcpyAsync(&fl, p->flags.p, sizeof(int), cudaMemcpyDeviceToHost, s));
-            CK(cudaStreamSynchronize(s));
-            if (fl & EF_BAD_SYMBOL) return p->fail(GAKCO_E_SYMBOL, "a code is >= sigma");
+            LK(launch_check_codes((const uint8_t*)p->codes.p, L, p->sigma,
+                                  (int*)p->flags.p + 1, s));
         } else {
             for (int64_t i = 0; i < L; ++i)
                 if (codes[i] >= p->sigma) return p->fail(GAKCO_E_SYMBOL, "a code is >= sigma");
@@ -395,12 +395,14 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
     for (size_t i = 0; i < p->mask_level.size(); ++i)
         if ((int)(i % world) == rank && (only_level < 0 || p->mask_level[i] == only_level))
             mine.push_back((int)i);
-    std::vector<uint8_t> kept_h(mine.size() * GMAX + GMAX, 0);
+    // (pageable host staging: cudaMemcpyAsync returns once the source is copied,
+    // so the member buffers can be reused without a stream sync)
+    std::vector<uint8_t>& kept_h = p->kept_h;
+    kept_h.assign(mine.size() * GMAX + GMAX, 0);
     for (size_t i = 0; i < mine.size(); ++i)
         std::memcpy(&kept_h[i * GMAX], p->mask_kept[mine[i]].data(), GMAX);
     CK(p->ensure(p->kept, kept_h.size(), s));
     CK(cudaMemcpyAsync(p->kept.p, kept_h.data(), kept_h.size(), cudaMemcpyHostToDevice, s));
-    CK(cudaStreamSynchronize(s));  // kept_h / h_* are pageable host staging
 
     // heavy / light threshold: a group of s sequences costs ~s^2/2 scattered
     // updates on the light path and ~N_pad^2/2 u8 MACs on the Gram; with the
@@ -704,7 +706,7 @@ static gakco_status finalize_impl(gakco_plan* p, int64_t* C, int64_t N, int64_t*
         dKn = (double*)p->Knscr.p;
     }
     CK(p->ensure(p->kdiag, N * 8, s));
-    CK(p->ensure(p->flags, 64, s));
+    CK(p->ensure(p->flags, 64, s, /*zero=*/true));
     CK(cudaMemsetAsync(p->flags.p, 0, sizeof(int), s));
     cudaEvent_t a = nullptr;
     p->stage_begin(s, &a);
@@ -715,11 +717,13 @@ static gakco_status finalize_impl(gakco_plan* p, int64_t* C, int64_t N, int64_t*
     if (hNm) CK(cudaMemcpyAsync(Nm, dNm, (M + 1) * nn * 8, cudaMemcpyDeviceToHost, s));
     if (hK) CK(cudaMemcpyAsync(K, dK, nn * 8, cudaMemcpyDeviceToHost, s));
     if (hKn) CK(cudaMemcpyAsync(Knorm, dKn, nn * 8, cudaMemcpyDeviceToHost, s));
-    int fl = 0;
-    CK(cudaMemcpyAsync(&fl, p->flags.p, sizeof(int), cudaMemcpyDeviceToHost, s));
+    int fl[2] = {0, 0};
+    CK(cudaMemcpyAsync(fl, p->flags.p, 2 * sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemsetAsync((int*)p->flags.p + 1, 0, sizeof(int), s));  // symbol flag consumed
     CK(cudaStreamSynchronize(s));
-    if (fl & EF_NEGATIVE_N) return p->fail(GAKCO_E_INTERNAL, "negative N_m after Eq. 9");
-    if (fl & EF_K_MISMATCH) return p->fail(GAKCO_E_INTERNAL, "K != C_{g-k}");
+    if (fl[1] & EF_BAD_SYMBOL) return p->fail(GAKCO_E_SYMBOL, "a code is >= sigma");
+    if (fl[0] & EF_NEGATIVE_N) return p->fail(GAKCO_E_INTERNAL, "negative N_m after Eq. 9");
+    if (fl[0] & EF_K_MISMATCH) return p->fail(GAKCO_E_INTERNAL, "K != C_{g-k}");
     return GAKCO_OK;
 #undef CK
 #undef LK

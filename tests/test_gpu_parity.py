@@ -270,6 +270,14 @@ def test_errors(gk):
     with pytest.raises(gk.GakcoError) as e:
         gk.kernel_matrix(bad, cp.offsets, 4, 3, 2, 1)
     assert e.value.status == gk.GAKCO_E_SYMBOL
+    # device codes: checked on the device, reported by finalize; the plan recovers
+    plan = gk.Plan(4, 3, 2, 1)
+    with pytest.raises(gk.GakcoError) as e:
+        gk.kernel_matrix(torch.from_numpy(bad).cuda(), cp.offsets, 4, 3, 2, 1, plan=plan)
+    assert e.value.status == gk.GAKCO_E_SYMBOL
+    ok = gk.kernel_matrix(torch.from_numpy(cp.codes).cuda(), cp.offsets, 4, 3, 2, 1, plan=plan)
+    assert ok["K"][0, 0].item() == 2 * 3  # two 3-mers, h_0 = C(3,2) = 3, one self-pair each
+    plan.close()
     with pytest.raises(gk.GakcoError) as e:
         gk.kernel_matrix(cp.codes, np.array([0, 5, 4]), 4, 3, 2, 1)
     assert e.value.status == gk.GAKCO_E_ARG
