@@ -47,7 +47,8 @@ def args_():
                     help="target seconds of oracle work per CPU sample")
     ap.add_argument("--heavy-min", type=int, default=0)
     ap.add_argument("--batch-keys", type=int, default=0)
-    ap.add_argument("--sort", type=int, default=None, choices=[0, 1])
+    ap.add_argument("--sort", type=int, default=None, choices=[-1, 0, 1, 2],
+                    help="grouping: -1 auto, 0 chunked LSD sort, 1 onesweep LSD, 2 hash partition")
     ap.add_argument("--sort-ctas", type=int, default=0)
     ap.add_argument("--no-timing", action="store_true",
                     help="no per-stage events (roofline then uses the last timed stages)")
@@ -213,9 +214,18 @@ def stage_model(stats, cfg, N):
     trip, grp = stats["triples"], stats["groups_multi"]
     M = cfg.M
     epi = N * N * ((M + 1) * 4 + (M + 1) * 4 + (M + 1) * 8 + 16) + N * (M + 1) * 8
+    if stats.get("grouping", 0) == 2:
+        # hash partition (bucket.cu): the count pass recomputes keys from the packed
+        # windows (ALU work, windows re-read once per CTA mask group: L2);
+        # the scatter pass writes every composite once; group reads it once
+        enc = ("alu", float(keys))
+        srt = ("hbm", kbytes)
+    else:
+        enc = ("hbm", kbytes + 4.0 * keys)     # write the key + read the 4 B seq id
+        srt = ("hbm", 16.0 * (passes - p32) + 8.0 * p32)  # read + write per key per pass
     return {
-        "encode": ("hbm", kbytes + 4.0 * keys),    # write the key + read the 4 B seq id
-        "sort": ("hbm", 16.0 * (passes - p32) + 8.0 * p32),  # read + write per key per pass
+        "encode": enc,
+        "sort": srt,
         "segment": ("hbm", kbytes + 8.0 * trip + 8.0 * grp),  # read keys; write triples, groups
         "light": ("hbm", 8.0 * stats["light_pairs"]),  # u32 read-modify-write per update
         "heavy": ("tensor", 2.0 * stats["heavy_macs"]),
@@ -369,13 +379,17 @@ def run_ours(a):
     per_step = {k[3:]: v / a.steps for k, v in stage_ms.items()}
     if not any(per_step.values()):  # --no-timing: stage split unavailable
         per_step = {"sort": ms_per_step}
-    dom = max(per_step, key=lambda s: per_step[s])
+    dom = max((s_ for s_ in per_step if model[s_][0] != "alu") or per_step,
+              key=lambda s_: per_step[s_])
     bound, algo = model[dom]
     t_dom = per_step[dom] / 1e3
     stages = {}
     for s_, ms in per_step.items():
         b_, alg = model[s_]
-        if ms > 0:
+        if ms > 0 and b_ == "alu":
+            stages[s_] = {"ms": round(ms, 4), "bound": b_,
+                          "Gkeys/s": round(alg / (ms / 1e3) / 1e9, 2)}
+        elif ms > 0:
             stages[s_] = {"ms": round(ms, 4), "bound": b_,
                           ("GB/s" if b_ == "hbm" else "TOPS"):
                               round(alg / (ms / 1e3) / (1e9 if b_ == "hbm" else 1e12), 2)}

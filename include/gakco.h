@@ -62,8 +62,12 @@ typedef enum {
                                      a huge value = never (all light); 2 = all heavy */
     GAKCO_OPT_BATCH_KEYS = 2,     /* max keys (masks x g-mers) per batch; 0 = auto */
     GAKCO_OPT_TIMING = 3,         /* 1 = record per-stage CUDA events (gakco_get_stats) */
-    GAKCO_OPT_SORT = 4,           /* LSD pass kernel: 0 = chunked two-kernel pass (default),
-                                     1 = onesweep with decoupled look-back */
+    GAKCO_OPT_SORT = 4,           /* grouping of masked keys: -1 = automatic (default: hash
+                                     partition when it applies, else 0), 0 = LSD radix sort,
+                                     chunked two-kernel passes, 1 = LSD onesweep with
+                                     decoupled look-back, 2 = hash partition + shared-memory
+                                     hash grouping (falls back to 0 where it does not apply:
+                                     g*ceil(log2 sigma) > 64 or > 16M g-mers) */
     GAKCO_OPT_SORT_CTAS_PER_SM = 5, /* chunked pass grid size in CTAs per SM (default 3) */
     GAKCO_OPT_LIGHT_BINS = 6      /* light updates binned by accumulator block (ablation /
                                      test knob): <= 0 = never (default; measured slower on
@@ -86,6 +90,8 @@ typedef struct {
     int64_t n_encode, n_sort, n_segment, n_light, n_heavy, n_epilogue;
     int64_t keys32;         /* of `keys`, those carried as 32-bit composites */
     int64_t sort_passes32;  /* of `sort_passes`, those over 32-bit composites */
+    int64_t grouping;       /* path of the last accumulate: 0 chunked LSD sort,
+                               1 onesweep LSD sort, 2 hash partition (bucket.cu) */
 } gakco_stats;
 
 /* Create a plan for alphabet size sigma (1..255), g-mer length g (1..32),

@@ -156,6 +156,47 @@ struct SegmentOut {
     uint32_t* counts;        // [0] = T, [1] = G
 };
 
+// ---- hash-partition grouping (bucket.cu) ----
+constexpr int BK_SUB_TILE = 4096;  // g-mers per sub-tile of the partition passes
+// Per mask: how its key is formed from the packed g-mer window w (symbol r of the
+// g-mer at bits [bits*(g-1-r), bits*(g-r)) of w).
+struct MaskDesc {
+    uint8_t nkept, nrun, pad0, pad1;
+    uint8_t kept_sh[GMAX];   // HORNER: shift of the r-th kept symbol
+    uint8_t run_src[GMAX];   // RUNS: maximal runs of kept positions, as bit fields
+    uint8_t run_len[GMAX];
+    uint8_t run_dst[GMAX];
+};
+struct BkArgs {
+    const uint64_t* win;      // [n] packed g-mer windows
+    const uint32_t* gm_seq;   // [n] sequence of each g-mer
+    uint64_t n;               // g-mers per mask
+    const MaskDesc* desc;     // [nmask] this batch's masks
+    int nmask, mb;            // masks in the batch, masks per CTA of the passes
+    uint32_t nb, nchunks;     // buckets per mask, g-mer chunks per mask
+    uint64_t T;               // g-mers per chunk
+    int bits, sb;             // bits per symbol in w, sequence-id bits (>= 1)
+    int runs;                 // 1: RUNS keys, 0: HORNER keys
+    uint32_t sigma;
+    uint32_t* H;              // [nmask][nchunks][nb] chunk histograms -> prefixes
+    uint32_t* tot;            // [nmask][nb] bucket sizes
+    uint32_t* bbase;          // [nmask][nb+1] bucket starts within the mask
+};
+struct BkScratch {            // big-bucket tables (entry offset 2*start; occ at start)
+    uint64_t* tab;
+    uint32_t* tcnt;
+    uint32_t* gs;
+    uint32_t* occ;
+};
+cudaError_t launch_windows(const CorpusView& cv, int g, int bits, uint64_t* win, int sm_count,
+                           cudaStream_t s);
+int bk_masks_per_cta(uint32_t nb);
+cudaError_t launch_bucket_count(const BkArgs& a, bool k64, cudaStream_t s);
+cudaError_t launch_bucket_scatter(const BkArgs& a, void* out, bool k64, cudaStream_t s);
+cudaError_t launch_bucket_group(const BkArgs& a, const void* keys, bool k64, int64_t N,
+                                int64_t* Cm, SegmentOut so, BkScratch sc,
+                                unsigned long long* stats, int sm_count, cudaStream_t s);
+
 // ---- launchers (each returns cudaGetLastError()) ----
 cudaError_t launch_gmer_index(const int64_t* gofs, int64_t N, uint32_t* gm_seq, cudaStream_t s);
 cudaError_t launch_check_codes(const uint8_t* codes, int64_t len, int sigma, int* flags,

@@ -1,9 +1,9 @@
 // light.cu — group -> C_m update for groups with few sequences (countAndUpdate,
 // second half; Algorithm 1 lines 15-17).
 //
-// For a group (one masked key) whose sorted triples are (X_1,c_1) < ... < (X_s,c_s),
-// every unordered pair a < b adds c_a*c_b to C_m(X_a, X_b) — the upper triangle,
-// since X_a < X_b; the epilogue mirrors it (reading A4). Integer adds
+// For a group (one masked key) with triples (X_1,c_1), ..., (X_s,c_s) (distinct X,
+// in any order), every unordered pair adds c_a*c_b to C_m(min(X_a,X_b), max(..)) —
+// the upper triangle; the epilogue mirrors it (reading A4). Integer adds
 // commute, so the atomic update order never changes the result. The adds go to
 // a u32 strictly-upper packed accumulator (half the footprint of int64 rows, L2
 // resident for N <= ~5500) that light_flush adds into C_m; the host flushes
@@ -128,7 +128,7 @@ __global__ void __launch_bounds__(256) light_kernel(SegmentOut so, int64_t heavy
                 const uint32_t ab = s_tri[q - ej];
                 const uint32_t ta = sj + (ab & 31), tb = sj + (ab >> 5);
                 const uint32_t xa = so.tseq[ta] & 0x7fffffffu, xb = so.tseq[tb] & 0x7fffffffu;
-                idx = tri_index(xa, xb, N);
+                idx = tri_index(min(xa, xb), max(xa, xb), N);
                 val = so.tcnt[ta] * so.tcnt[tb];
             }
             pair_add(acc, bn, q < Ptot, idx, val);
@@ -191,7 +191,8 @@ __global__ void __launch_bounds__(256) light_kernel(SegmentOut so, int64_t heavy
                     const uint32_t ca = __shfl_sync(0xffffffffu, cA, a);
                     const uint32_t xb = __shfl_sync(0xffffffffu, xA, b);
                     const uint32_t cb = __shfl_sync(0xffffffffu, cA, b);
-                    pair_add(acc, bn, q < P, q < P ? tri_index(xa, xb, N) : 0, ca * cb);
+                    pair_add(acc, bn, q < P, q < P ? tri_index(min(xa, xb), max(xa, xb), N) : 0,
+                             ca * cb);
                 }
                 for (uint32_t B = A + 32; B < b0; B += 32) {
                     const uint32_t ib = B + lane;
@@ -201,7 +202,8 @@ __global__ void __launch_bounds__(256) light_kernel(SegmentOut so, int64_t heavy
                     for (uint32_t a = 0; a < na; ++a) {
                         const uint32_t xa = __shfl_sync(0xffffffffu, xA, a);
                         const uint32_t ca = __shfl_sync(0xffffffffu, cA, a);
-                        pair_add(acc, bn, vb, vb ? tri_index(xa, xB, N) : 0, ca * cB);
+                        pair_add(acc, bn, vb, vb ? tri_index(min(xa, xB), max(xa, xB), N) : 0,
+                                 ca * cB);
                     }
                 }
             }

@@ -76,7 +76,10 @@ struct gakco_plan {
     int rank = 0, world = 1;
     int64_t heavy_min = 0, batch_keys = 0;
     bool timing = false;
-    int sort_mode = 0;  // 0: chunked two-kernel LSD pass, 1: onesweep (decoupled look-back)
+    // grouping: -1 auto (hash partition when it applies, else chunked LSD),
+    // 0 chunked two-kernel LSD pass, 1 onesweep LSD (decoupled look-back),
+    // 2 hash partition + shared-memory hash grouping (bucket.cu)
+    int sort_mode = -1;
     int sort_ctas_per_sm = 3;  // chunked pass grid = this x SMs (measured best of 1..4)
     int64_t light_bins = 0;    // 0 auto, < 0 off, > 0 forced block size in cells
     int sm_count = 148;
@@ -89,7 +92,7 @@ struct gakco_plan {
 
     DevBuf codes, off, gofs, gmseq, keysA, keysB, hist, status, ctr, tseq, tcnt, gstart, gend,
         counts, kept, stats, flags, kdiag, Cscr, Nmscr, Kscr, Knscr, heavy, hcount, dense, tiles,
-        lightacc, binrec, bincnt;
+        lightacc, binrec, bincnt, win, bkH, bktot, bkbase, bkdesc, bktab, bktcnt, bkgs, bkocc;
     int64_t tiles_npad = -1;
     uint64_t dense_ldd = 0;
     int ntiles = 0;
@@ -144,6 +147,7 @@ struct gakco_plan {
     }
     int64_t stage_launches[S_NSTAGE] = {0, 0, 0, 0, 0, 0};
     int64_t launches_at_begin = 0;
+    int last_grouping = 0;
     void stage_begin(cudaStream_t s, cudaEvent_t* a) {
         launches_at_begin = launches;
         if (!timing) return;
@@ -246,7 +250,9 @@ extern "C" void gakco_destroy(gakco_plan* p) {
                       &p->hist,  &p->status, &p->ctr,  &p->tseq,   &p->tcnt,  &p->gstart,
                       &p->gend,  &p->counts, &p->kept, &p->stats,  &p->flags, &p->kdiag,
                       &p->Cscr,  &p->Nmscr, &p->Kscr,  &p->Knscr, &p->heavy, &p->hcount,
-                      &p->dense, &p->tiles, &p->lightacc, &p->binrec, &p->bincnt};
+                      &p->dense, &p->tiles, &p->lightacc, &p->binrec, &p->bincnt,
+                      &p->win,   &p->bkH,   &p->bktot, &p->bkbase, &p->bkdesc, &p->bktab,
+                      &p->bktcnt, &p->bkgs, &p->bkocc};
     for (DevBuf* b : bufs)
         if (b->p) cudaFree(b->p);
     for (cudaEvent_t e : p->ev_pool) cudaEventDestroy(e);
@@ -272,7 +278,7 @@ extern "C" gakco_status gakco_set_option(gakco_plan* p, int option, int64_t valu
             p->batch_keys = value;
             return GAKCO_OK;
         case GAKCO_OPT_SORT:
-            if (value < 0 || value > 1) return p->fail(GAKCO_E_ARG, "sort must be 0 or 1");
+            if (value < -1 || value > 2) return p->fail(GAKCO_E_ARG, "sort must be -1..2");
             p->sort_mode = (int)value;
             return GAKCO_OK;
         case GAKCO_OPT_LIGHT_BINS:
@@ -364,6 +370,21 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
         if (p->key_bits[m] + sb > 64)
             return p->fail(GAKCO_E_RANGE, "masked key + sequence id exceed 64 bits");
 
+    // grouping: hash partition (bucket.cu) when the g-mer window packs into 64 bits,
+    // a mask has <= 16M g-mers (<= 16384 buckets of ~1024 keys) and every level's
+    // key + sequence id fits 64 bits; otherwise the LSD radix sort (radix.cu)
+    int bits = 1;
+    while ((1 << bits) < p->sigma) ++bits;
+    const int sbh = std::max(sb, 1);
+    bool hash_mode = (p->sort_mode == -1 || p->sort_mode == 2) && n > 0 && g * bits <= 64 &&
+                     n <= (16384ull << 10);
+    std::vector<int> level_runs(M + 1, 0);
+    for (int m = 0; m <= M && hash_mode; ++m) {
+        if ((g - m) * bits + sbh <= 64) level_runs[m] = 1;
+        else if (p->key_bits[m] + sbh > 64) hash_mode = false;
+    }
+    p->last_grouping = hash_mode ? 2 : (p->sort_mode == 1 ? 1 : 0);
+
     // corpus to device (+ symbol check)
     CK(p->ensure(p->codes, (size_t)L + 16, s));
     CK(p->ensure(p->flags, 64, s, /*zero=*/true));
@@ -416,7 +437,8 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
     // batch size (keys cap; with the Gram on, s32 exactness: masks * n_max^2 < 2^31)
     // default: up to 64M keys (512 MB per key buffer): large launches measured
     // faster than L2-sized (4M-key) batches for every stage
-    uint64_t bk = p->batch_keys > 0 ? (uint64_t)p->batch_keys : (64ull << 20);
+    uint64_t bk = p->batch_keys > 0 ? (uint64_t)p->batch_keys
+                                    : (hash_mode ? (32ull << 20) : (64ull << 20));
     if (bk > (1ull << 30) - 1) bk = (1ull << 30) - 1;
     uint64_t bmax_masks = std::max<uint64_t>(1, n ? bk / n : mine.size());
     if (heavy_on && nmax > 0) {
@@ -453,6 +475,40 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
     CK(cudaMemsetAsync(p->stats.p, 0, ST_COUNT * 8, s));
     unsigned long long* stats = (unsigned long long*)p->stats.p;
 
+    // hash-partition buffers: packed windows, mask descriptors, big-bucket scratch
+    std::vector<MaskDesc> desc_h;
+    if (hash_mode) {
+        CK(p->ensure(p->win, n * 8, s));
+        CK(p->ensure(p->bktab, cap_keys * 2 * 8, s));
+        CK(p->ensure(p->bktcnt, cap_keys * 2 * 4, s));
+        CK(p->ensure(p->bkgs, cap_keys * 2 * 4, s));
+        CK(p->ensure(p->bkocc, cap_keys * 4, s));
+        desc_h.resize(mine.size() + 1);
+        std::memset(desc_h.data(), 0, desc_h.size() * sizeof(MaskDesc));
+        for (size_t i = 0; i < mine.size(); ++i) {
+            const int m = p->mask_level[mine[i]];
+            const uint8_t* kept = p->mask_kept[mine[i]].data();
+            MaskDesc& d = desc_h[i];
+            d.nkept = (uint8_t)(g - m);
+            for (int r = 0; r < g - m; ++r) d.kept_sh[r] = (uint8_t)(bits * (g - 1 - kept[r]));
+            // maximal runs of consecutive kept positions -> bit fields of w
+            int r = 0, nrun = 0;
+            while (r < g - m) {
+                int e = r;
+                while (e + 1 < g - m && kept[e + 1] == kept[e] + 1) ++e;
+                d.run_src[nrun] = (uint8_t)(bits * (g - 1 - kept[e]));
+                d.run_len[nrun] = (uint8_t)(bits * (e - r + 1));
+                d.run_dst[nrun] = (uint8_t)(bits * (g - m - 1 - e));
+                ++nrun;
+                r = e + 1;
+            }
+            d.nrun = (uint8_t)nrun;
+        }
+        CK(p->ensure(p->bkdesc, desc_h.size() * sizeof(MaskDesc), s));
+        CK(cudaMemcpyAsync(p->bkdesc.p, desc_h.data(), desc_h.size() * sizeof(MaskDesc),
+                           cudaMemcpyHostToDevice, s));
+    }
+
     const int64_t light_limit = gram_ok ? heavy_min : INT64_MAX;
     uint64_t rcap = 0;
     if (gram_ok) {
@@ -481,6 +537,12 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
     SegmentOut so{(uint32_t*)p->tseq.p, (uint32_t*)p->tcnt.p, (uint2*)p->gstart.p,
                   (uint32_t*)p->counts.p};
     int64_t passkeys = 0, keys32 = 0, passkeys32 = 0;
+    if (hash_mode) {
+        cudaEvent_t a0 = nullptr;
+        p->stage_begin(s, &a0);
+        LK(launch_windows(cv, g, bits, (uint64_t*)p->win.p, p->sm_count, s));
+        p->stage_end(s, S_ENCODE, a0);
+    }
     const size_t nn = (size_t)N * N;
     auto level_ptr = [&](int m) -> int64_t* {
         return only_level >= 0 ? C : C + (size_t)m * nn;
@@ -575,7 +637,46 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
             light_masks += nmask;
         }
 
-        if (n > 0) {
+        if (n > 0 && hash_mode) {
+            // hash partition: count -> (column / bucket scans + scatter) -> group
+            const bool k64 = (level_runs[m] ? (g - m) * bits : kb) + sbh > 32;
+            BkArgs ba{};
+            ba.win = (const uint64_t*)p->win.p;
+            ba.gm_seq = (const uint32_t*)p->gmseq.p;
+            ba.n = n;
+            ba.desc = (const MaskDesc*)p->bkdesc.p + pos;
+            ba.nmask = nmask;
+            ba.nb = (uint32_t)std::min<uint64_t>(16384, std::max<uint64_t>(1, (n + 1023) / 1024));
+            uint64_t T = BK_SUB_TILE;
+            while (((n + T - 1) / T) * ba.nb > std::max<uint64_t>(n / 4, ba.nb) && T < (1ull << 22))
+                T *= 2;
+            ba.T = T;
+            ba.nchunks = (uint32_t)((n + T - 1) / T);
+            ba.mb = bk_masks_per_cta(ba.nb);
+            ba.bits = bits;
+            ba.sb = sbh;
+            ba.runs = level_runs[m];
+            ba.sigma = (uint32_t)p->sigma;
+            CK(p->ensure(p->bkH, (size_t)nmask * ba.nchunks * ba.nb * 4, s));
+            CK(p->ensure(p->bktot, (size_t)nmask * ba.nb * 4, s));
+            CK(p->ensure(p->bkbase, (size_t)nmask * (ba.nb + 1) * 4, s));
+            ba.H = (uint32_t*)p->bkH.p;
+            ba.tot = (uint32_t*)p->bktot.p;
+            ba.bbase = (uint32_t*)p->bkbase.p;
+            p->stage_begin(s, &a);
+            LK(launch_bucket_count(ba, k64, s));
+            p->stage_end(s, S_ENCODE, a);
+            p->stage_begin(s, &a);
+            p->launches += 2;  // colscan + bscan
+            LK(launch_bucket_scatter(ba, p->keysA.p, k64, s));
+            p->stage_end(s, S_SORT, a);
+            if (!k64) keys32 += (int64_t)nmask * (int64_t)n;
+            p->stage_begin(s, &a);
+            BkScratch bs{(uint64_t*)p->bktab.p, (uint32_t*)p->bktcnt.p, (uint32_t*)p->bkgs.p,
+                         (uint32_t*)p->bkocc.p};
+            LK(launch_bucket_group(ba, p->keysA.p, k64, N, Cm, so, bs, stats, p->sm_count, s));
+            p->stage_end(s, S_SEGMENT, a);
+        } else if (n > 0) {
             p->stage_begin(s, &a);
             const bool onesweep = p->sort_mode == 1;
             // 32-bit composites when key + sequence bits fit (half the key traffic)
@@ -615,6 +716,8 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
             LK(launch_segment(in, k64, n, nmask, sb, N, Cm, so.counts, so, stats, s));
             p->stage_end(s, S_SEGMENT, a);
 
+        }
+        if (n > 0) {
             p->stage_begin(s, &a);
             LK(launch_light(so, n * nmask / 2 + 1, light_limit, N, (uint32_t*)p->lightacc.p,
                             (uint2*)p->heavy.p, rcap, (uint32_t*)p->hcount.p, bins, stats,
@@ -644,6 +747,7 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
     p->host_stats.sort_passes = passkeys;
     p->host_stats.keys32 = keys32;
     p->host_stats.sort_passes32 = passkeys32;
+    p->host_stats.grouping = p->last_grouping;
     p->after_accumulate = true;
     return GAKCO_OK;
 #undef CK

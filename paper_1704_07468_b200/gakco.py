@@ -46,7 +46,7 @@ class gakco_stats(ctypes.Structure):
             "ms_encode", "ms_sort", "ms_segment", "ms_light", "ms_heavy", "ms_epilogue")] + [
         (n, ctypes.c_int64) for n in (
             "n_encode", "n_sort", "n_segment", "n_light", "n_heavy", "n_epilogue", "keys32",
-            "sort_passes32")]
+            "sort_passes32", "grouping")]
 
     def as_dict(self):
         return {n: getattr(self, n) for n, _ in self._fields_}

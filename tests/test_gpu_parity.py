@@ -145,6 +145,54 @@ def test_sort_modes_ragged(gk, oracle_lib):
         assert_parity(run(gk, cp, 8, 4, 4, batch_keys=bk, sort=1), ref)
 
 
+def test_grouping_modes(gk, oracle_lib):
+    """Hash-partition grouping (bucket.cu, GAKCO_OPT_SORT 2, the default where it
+    applies) == chunked LSD sort (0) == onesweep LSD sort (1) == oracle; the stats
+    report which path ran."""
+    rng = np.random.default_rng(108)
+    for it in range(10):
+        sigma = int(rng.choice([2, 4, 20, 36]))
+        g = int(rng.integers(2, 11))
+        k = int(rng.integers(1, g + 1))
+        M = int(rng.integers(0, g + 1))
+        cp = sc.random_small(rng, sigma, n_max=200, l_max=300)
+        ref = oracle_lib.compute(cp, g, k, M)
+        for mode in (0, 1, 2):
+            r = run(gk, cp, g, k, M, sort=mode)
+            assert_parity(r, ref)
+            if r["stats"]["keys"] > 0:
+                assert r["stats"]["grouping"] == mode
+        assert run(gk, cp, g, k, M)["stats"]["grouping"] in (0, 2)
+
+
+def test_hash_big_buckets(gk, oracle_lib):
+    """Buckets far above the shared-memory capacity (4096 keys) take the
+    global-table path: few distinct keys (Σ = 2, g = 4; Σ = 1) over many g-mers,
+    mixed with ordinary buckets (Σ = 4 background)."""
+    rng = np.random.default_rng(109)
+    cases = [
+        (sc.from_sequences(2, [rng.integers(0, 2, size=3000) for _ in range(12)]), 4, 2, 2),
+        (sc.from_sequences(1, [[0] * 2500, [0] * 1800, [0] * 3]), 5, 3, 2),
+        (sc.from_sequences(4, [[0] * 6000] + [rng.integers(0, 4, size=2000) for _ in range(20)]),
+         6, 3, 3),
+    ]
+    for cp, g, k, M in cases:
+        ref = oracle_lib.compute(cp, g, k, M)
+        for hm in (0, 1 << 50):
+            assert_parity(run(gk, cp, g, k, M, sort=2, heavy_min_seqs=hm), ref)
+
+
+def test_hash_batch_size_invariance(gk, oracle_lib):
+    """Hash grouping over different mask batch sizes (bucket counts, chunk sizes
+    and masks per CTA change with the batch) gives identical results."""
+    rng = np.random.default_rng(110)
+    seqs = [rng.integers(0, 20, size=int(rng.integers(0, 2500))) for _ in range(41)]
+    cp = sc.from_sequences(20, seqs)
+    ref = oracle_lib.compute(cp, 8, 4, 4)
+    for bk in (1, 50001, 1 << 22):
+        assert_parity(run(gk, cp, 8, 4, 4, batch_keys=bk, sort=2), ref)
+
+
 def test_edge_cases(gk, oracle_lib):
     cases = [
         (sc.from_sequences(4, [[0, 1, 2, 3, 0, 1]]), 3, 2, 1),      # N = 1
@@ -311,6 +359,22 @@ def test_full_config_digests(gk, name):
     # Knorm: reference recomputed from the verified K with the oracle's formula
     import oracle
     assert_knorm(r["Knorm"].cpu().numpy(), oracle.normalize(K))
+
+
+def test_dna_digests_lsd_sort(gk):
+    """The LSD radix-sort grouping (GAKCO_OPT_SORT 0) on the full DNA config also
+    matches the committed digests (the default there is the hash partition)."""
+    gold = _golden("dna")
+    cfg = sc.CONFIGS["dna"]
+    cp = sc.make("dna")
+    plan = gk.Plan(cfg.sigma, cfg.g, cfg.k, cfg.M)
+    plan.set_option(gk.GAKCO_OPT_SORT, 0)
+    r = gk.kernel_matrix(cp.codes, cp.offsets, cfg.sigma, cfg.g, cfg.k, cfg.M, plan=plan)
+    assert plan.stats()["grouping"] == 0
+    plan.close()
+    assert refs.digest_np(r["K"].cpu().numpy()) == int(gold["digests"]["K"])
+    for m in range(cfg.M + 1):
+        assert refs.digest_np(r["C"][m].cpu().numpy()) == int(gold["digests"][f"C{m}"])
 
 
 @pytest.mark.parametrize("name", ["text", "scale"])
