@@ -62,8 +62,8 @@ typedef enum {
                                      a huge value = never (all light); 2 = all heavy */
     GAKCO_OPT_BATCH_KEYS = 2,     /* max keys (masks x g-mers) per batch; 0 = auto */
     GAKCO_OPT_TIMING = 3,         /* 1 = record per-stage CUDA events (gakco_get_stats) */
-    GAKCO_OPT_SORT = 4,           /* grouping of masked keys: -1 = automatic (default: hash
-                                     partition when it applies, else 0), 0 = LSD radix sort,
+    GAKCO_OPT_SORT = 4,           /* grouping of masked keys: -1 = automatic (default; = 0,
+                                     measured fastest), 0 = LSD radix sort,
                                      chunked two-kernel passes, 1 = LSD onesweep with
                                      decoupled look-back, 2 = hash partition + shared-memory
                                      hash grouping (falls back to 0 where it does not apply:

@@ -1,6 +1,7 @@
 // bucket.cu — grouping of masked g-mers by hash partition + shared-memory hash
-// tables (the default grouping; the LSD radix sort + run-length pass of radix.cu /
-// segment.cu is the alternative, GAKCO_OPT_SORT 0/1).
+// tables (GAKCO_OPT_SORT 2; the NEXT-4 ablation of SURVEY.md §8f against the LSD
+// radix sort + run-length pass of radix.cu / segment.cu, which is the default:
+// measured faster).
 //
 // What it computes is exactly what Algorithm 1 lines 13-15
 // compute with removePosition -> sort -> countAndUpdate: for every mask, the groups
@@ -215,31 +216,26 @@ __global__ void __launch_bounds__(1024) bk_bscan_kernel(BkArgs a) {
 }
 
 // ---------------------------------------------------------------- group
-constexpr int GR_THREADS = 512;
-constexpr int GR_ITEMS = 8;
-constexpr int GR_CAP = GR_THREADS * GR_ITEMS;  // keys of a bucket grouped in smem
-constexpr int GR_HMAX = 2 * GR_CAP;            // table slots (load <= 1/2)
 constexpr uint64_t EMPTY = ~0ull;
 constexpr int CNT_BITS = 13;                   // smem triple entry: tag << 13 | count
-constexpr size_t GR_SMEM = (size_t)GR_HMAX * 8 + (size_t)GR_HMAX * 4;
 
-__device__ __forceinline__ uint32_t slot_hash(uint64_t v, int lg) {
+// slot in [0, H) of a 64-bit value (H need not be a power of two)
+__device__ __forceinline__ uint32_t slot_of(uint64_t v, uint32_t H) {
     v ^= v >> 31;
     v *= 0xD6E8FEB86659FD93ull;
     v ^= v >> 32;
-    return (uint32_t)(v >> (64 - lg)) ;
+    return (uint32_t)(((v & 0xffffffffull) * (uint64_t)H) >> 32);
 }
 
 // Per-CTA bookkeeping shared by the smem and the global-table paths: given the
 // per-slot distinct-sequence counts gs[0..H), reserve the triple / group ranges
 // of the groups with gs >= 2, write the group ranges, and turn gs into the
 // per-group write cursor (0xffffffff for groups that are not emitted).
-template <typename SlotArr>
-__device__ __forceinline__ void emit_groups(SlotArr gs, uint32_t H, uint32_t* s_w,
+__device__ __forceinline__ void emit_groups(uint32_t* gs, uint32_t H, uint32_t* s_w,
                                             uint32_t* s_base, SegmentOut so,
                                             unsigned long long& n_t, unsigned long long& n_g) {
     const uint32_t per = (H + blockDim.x - 1) / blockDim.x;
-    const uint32_t lo = threadIdx.x * per, hi = min(H, lo + per);
+    const uint32_t lo = min(H, threadIdx.x * per), hi = min(H, lo + per);
     uint32_t nt = 0, ng = 0;
     for (uint32_t i = lo; i < hi; ++i) {
         const uint32_t s = gs[i];
@@ -272,18 +268,9 @@ __device__ __forceinline__ void emit_groups(SlotArr gs, uint32_t H, uint32_t* s_
     __syncthreads();
 }
 
-// Global-table path for a bucket larger than GR_CAP (rare: skewed keys). Tables
-// live in scratch at entry offset 4*start (the bucket's own region; H <= 4c).
-// Global-table path for a bucket larger than GR_CAP (rare: skewed keys). Tables
+// Global-table path for a bucket larger than GV_CAP (rare: skewed keys). Tables
 // of H = 2c slots live in scratch at entry offset 2*start (the bucket's own
 // region, disjoint from every other bucket's).
-__device__ __forceinline__ uint32_t slot_mod(uint64_t v, uint32_t H) {
-    v ^= v >> 31;
-    v *= 0xD6E8FEB86659FD93ull;
-    v ^= v >> 32;
-    return (uint32_t)(((v >> 32) * (uint64_t)H) >> 32);
-}
-
 template <typename K>
 __device__ void group_big(const K* keys, uint64_t start, uint32_t c, int sb, int64_t N,
                           int64_t* Cm, SegmentOut so, BkScratch sc, uint32_t* s_w,
@@ -302,7 +289,7 @@ __device__ void group_big(const K* keys, uint64_t start, uint32_t c, int sb, int
     __syncthreads();
     for (uint32_t i = threadIdx.x; i < c; i += blockDim.x) {
         const uint64_t key = (uint64_t)keys[start + i] >> sb;
-        uint32_t h = slot_mod(key, H);
+        uint32_t h = slot_of(key, H);
         while (true) {
             const uint64_t v = *(volatile uint64_t*)&tab[h];
             if (v == key) break;
@@ -318,13 +305,18 @@ __device__ void group_big(const K* keys, uint64_t start, uint32_t c, int sb, int
     for (uint32_t i = threadIdx.x; i < H; i += blockDim.x) tab[i] = EMPTY;
     __syncthreads();
     for (uint32_t i = threadIdx.x; i < c; i += blockDim.x) {
-        const uint64_t tag = ((uint64_t)occ[i] << 32) | ((uint64_t)keys[start + i] & seqmask);
-        uint32_t h = slot_mod(tag, H);
+        const uint32_t g = occ[i];
+        const uint64_t tag = ((uint64_t)g << 32) | ((uint64_t)keys[start + i] & seqmask);
+        uint32_t h = slot_of(tag, H);
         while (true) {
             uint64_t v = *(volatile uint64_t*)&tab[h];
             if (v == EMPTY) {
                 v = atomicCAS((unsigned long long*)&tab[h], EMPTY, tag);
-                if (v == EMPTY) v = tag;
+                if (v == EMPTY) {
+                    atomicAdd(&tcnt[h], 1u);
+                    atomicAdd(&gs[g], 1u);  // a new distinct sequence of group g
+                    break;
+                }
             }
             if (v == tag) {
                 atomicAdd(&tcnt[h], 1u);
@@ -334,42 +326,57 @@ __device__ void group_big(const K* keys, uint64_t start, uint32_t c, int sb, int
         }
     }
     __syncthreads();
-    for (uint32_t i = threadIdx.x; i < H; i += blockDim.x) {
-        const uint64_t v = tab[i];
-        if (v == EMPTY) continue;
-        atomicAdd(&gs[(uint32_t)(v >> 32)], 1u);
-        const uint64_t cc = tcnt[i];
-        if (cc >= 2) {
-            const int64_t x = (int64_t)(v & 0xffffffffull);
-            atomicAdd((unsigned long long*)&Cm[x * N + x], (unsigned long long)(cc * cc - cc));
-        }
-    }
-    __syncthreads();
     emit_groups(gs, H, s_w, s_base, so, n_t, n_g);
     for (uint32_t i = threadIdx.x; i < H; i += blockDim.x) {
         const uint64_t v = tab[i];
         if (v == EMPTY) continue;
+        const uint32_t x = (uint32_t)(v & 0xffffffffull);
+        const uint64_t cc = tcnt[i];
+        if (cc >= 2)
+            atomicAdd((unsigned long long*)&Cm[(int64_t)x * N + x], (unsigned long long)(cc * cc - cc));
         const uint32_t g = (uint32_t)(v >> 32);
         if (*(volatile uint32_t*)&gs[g] == 0xffffffffu) continue;
         const uint32_t pos = atomicAdd(&gs[g], 1u);
-        so.tseq[pos] = (uint32_t)(v & 0xffffffffull);
-        so.tcnt[pos] = tcnt[i];
+        so.tseq[pos] = x;
+        so.tcnt[pos] = (uint32_t)cc;
     }
     __syncthreads();
 }
 
+// One CTA per bucket (grid-stride over the batch's buckets). Shared memory:
+// the bucket's composites, a table of H ~ 1.5c slots, per-slot group counters.
+//   (1) key -> group slot g (table of keys); g kept per key;
+//   (2) table reused for (g, seq) -> count; a new (g, seq) bumps gs[g], the
+//       number of distinct sequences of group g;
+//   (3) groups with gs >= 2 get CTA-local triple offsets and group indices
+//       (warp-aggregated shared atomics), then one global reservation;
+//   (4) one pass over the slots: group ranges out; every triple: repeats
+//       c^2 - c on the diagonal, (seq, count) out at its group's cursor.
+// gs packs (distinct seqs << 12 | cursor) after (3); GV_CAP < 4096.
+constexpr int GV_THREADS = 256;
+constexpr int GV_CAP = 2048;      // keys of a bucket grouped in smem (mean ~1024)
+constexpr int GV_HMAX = GV_CAP * 3 / 2;
+static_assert(GV_CAP < 4096 && GV_CAP < (1 << CNT_BITS), "12-bit cursor / group fields");
+constexpr size_t GV_SMEM = (size_t)GV_HMAX * 8 + (size_t)GV_HMAX * 4 * 2 + (size_t)GV_CAP * 8 +
+                           (size_t)GV_CAP * 2;
+
 template <typename K>
-__global__ void __launch_bounds__(GR_THREADS, 2) bk_group_kernel(
+__global__ void __launch_bounds__(GV_THREADS, 3) bk_group_kernel(
     const K* __restrict__ keys, BkArgs a, int64_t N, int64_t* Cm, SegmentOut so,
     BkScratch sc, unsigned long long* stats) {
     extern __shared__ __align__(16) unsigned char smem[];
-    uint64_t* tab = (uint64_t*)smem;                      // [GR_HMAX]
-    uint32_t* gs = (uint32_t*)(smem + GR_HMAX * 8);       // [GR_HMAX]
+    uint64_t* tab = (uint64_t*)smem;                                  // [GV_HMAX]
+    uint32_t* gs = (uint32_t*)(tab + GV_HMAX);                        // [GV_HMAX]
+    uint32_t* gl = gs + GV_HMAX;                                      // [GV_HMAX]
+    K* kc = (K*)(gl + GV_HMAX);                                       // [GV_CAP]
+    uint16_t* ks = (uint16_t*)((unsigned char*)(gl + GV_HMAX) + GV_CAP * 8);  // [GV_CAP]
     __shared__ uint32_t s_w[32];
-    __shared__ uint32_t s_base[2];
+    __shared__ uint32_t s_cnt[2], s_base[2];
     const int sb = a.sb;
+    const int lane = threadIdx.x & 31;
     const uint64_t seqmask = (1ull << sb) - 1ull;
     const uint32_t nbt = (uint32_t)a.nmask * a.nb;
+    const uint32_t lt = lanemask_lt();
     unsigned long long n_t = 0, n_g = 0;
     for (uint32_t wb = blockIdx.x; wb < nbt; wb += gridDim.x) {
         const uint32_t m = wb / a.nb, b = wb - m * a.nb;
@@ -377,33 +384,22 @@ __global__ void __launch_bounds__(GR_THREADS, 2) bk_group_kernel(
         const uint32_t lo = bb[b], c = bb[b + 1] - lo;  // block-uniform
         if (c < 2) continue;  // one g-mer: count 1, no pair, no repeat
         const uint64_t start = (uint64_t)m * a.n + lo;
-        if (c > (uint32_t)GR_CAP) {
+        if (c > (uint32_t)GV_CAP) {
             group_big<K>(keys, start, c, sb, N, Cm, so, sc, s_w, s_base, n_t, n_g);
             continue;
         }
-        int lg = 9;
-        while ((1u << lg) < 2u * c) ++lg;
-        const uint32_t H = 1u << lg;
-        K comp[GR_ITEMS];
-#pragma unroll
-        for (int i = 0; i < GR_ITEMS; ++i) {
-            const uint32_t idx = (uint32_t)i * GR_THREADS + threadIdx.x;
-            comp[i] = idx < c ? keys[start + idx] : (K)0;
-        }
-        for (uint32_t i = threadIdx.x; i < H; i += GR_THREADS) {
+        const uint32_t H = max(64u, (3u * c / 2u + 31u) & ~31u);
+        for (uint32_t i = threadIdx.x; i < c; i += GV_THREADS) kc[i] = keys[start + i];
+        for (uint32_t i = threadIdx.x; i < H; i += GV_THREADS) {
             tab[i] = EMPTY;
             gs[i] = 0u;
         }
+        if (threadIdx.x < 2) s_cnt[threadIdx.x] = 0u;
         __syncthreads();
         // (1) key -> group slot
-        uint32_t slot[GR_ITEMS];
-#pragma unroll
-        for (int i = 0; i < GR_ITEMS; ++i) {
-            const uint32_t idx = (uint32_t)i * GR_THREADS + threadIdx.x;
-            slot[i] = 0;
-            if (idx >= c) continue;
-            const uint64_t key = (uint64_t)comp[i] >> sb;
-            uint32_t h = slot_hash(key, lg);
+        for (uint32_t i = threadIdx.x; i < c; i += GV_THREADS) {
+            const uint64_t key = (uint64_t)kc[i] >> sb;
+            uint32_t h = slot_of(key, H);
             while (true) {
                 const uint64_t v = *(volatile uint64_t*)&tab[h];
                 if (v == key) break;
@@ -411,57 +407,95 @@ __global__ void __launch_bounds__(GR_THREADS, 2) bk_group_kernel(
                     const uint64_t old = atomicCAS((unsigned long long*)&tab[h], EMPTY, key);
                     if (old == EMPTY || old == key) break;
                 }
-                h = (h + 1) & (H - 1);
+                h = h + 1 == H ? 0 : h + 1;
             }
-            slot[i] = h;
+            ks[i] = (uint16_t)h;
         }
         __syncthreads();
-        for (uint32_t i = threadIdx.x; i < H; i += GR_THREADS) tab[i] = EMPTY;
+        for (uint32_t i = threadIdx.x; i < H; i += GV_THREADS) tab[i] = EMPTY;
         __syncthreads();
         // (2) (group slot, seq) -> count: entry = tag << 13 | count
-#pragma unroll
-        for (int i = 0; i < GR_ITEMS; ++i) {
-            const uint32_t idx = (uint32_t)i * GR_THREADS + threadIdx.x;
-            if (idx >= c) continue;
-            const uint64_t tag = ((uint64_t)slot[i] << 31) | ((uint64_t)comp[i] & seqmask);
-            uint32_t h = slot_hash(tag, lg);
+        for (uint32_t i = threadIdx.x; i < c; i += GV_THREADS) {
+            const uint32_t g = ks[i];
+            const uint64_t tag = ((uint64_t)g << 31) | ((uint64_t)kc[i] & seqmask);
+            uint32_t h = slot_of(tag, H);
             while (true) {
                 uint64_t v = *(volatile uint64_t*)&tab[h];
                 if (v == EMPTY) {
                     v = atomicCAS((unsigned long long*)&tab[h], EMPTY, (tag << CNT_BITS) | 1ull);
-                    if (v == EMPTY) break;
+                    if (v == EMPTY) {
+                        atomicAdd(&gs[g], 1u);
+                        break;
+                    }
                 }
                 if ((v >> CNT_BITS) == tag) {
                     atomicAdd((unsigned long long*)&tab[h], 1ull);
                     break;
                 }
-                h = (h + 1) & (H - 1);
+                h = h + 1 == H ? 0 : h + 1;
             }
         }
         __syncthreads();
-        // (3) distinct sequences per group; within-sequence repeats on the diagonal
-        for (uint32_t i = threadIdx.x; i < H; i += GR_THREADS) {
-            const uint64_t v = tab[i];
-            if (v == EMPTY) continue;
-            atomicAdd(&gs[(uint32_t)(v >> (CNT_BITS + 31))], 1u);
-            const uint64_t cc = v & ((1ull << CNT_BITS) - 1ull);
-            if (cc >= 2) {
-                const int64_t x = (int64_t)((v >> CNT_BITS) & 0x7fffffffull);
-                atomicAdd((unsigned long long*)&Cm[x * N + x], (unsigned long long)(cc * cc - cc));
+        // (3) CTA-local offsets of the multi-sequence groups (warp-aggregated)
+        for (uint32_t i0 = 0; i0 < H; i0 += GV_THREADS) {
+            const uint32_t i = i0 + threadIdx.x;
+            const uint32_t s = i < H ? gs[i] : 0u;
+            const bool em = s >= 2;
+            const uint32_t bal = __ballot_sync(0xffffffffu, em);
+            uint32_t inc = em ? s : 0u;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t t = __shfl_up_sync(0xffffffffu, inc, o);
+                if (lane >= o) inc += t;
+            }
+            const uint32_t wt = __shfl_sync(0xffffffffu, inc, 31);
+            uint32_t bt = 0, bg = 0;
+            if (lane == 0 && bal) {
+                bt = atomicAdd(&s_cnt[0], wt);
+                bg = atomicAdd(&s_cnt[1], (uint32_t)__popc(bal));
+            }
+            bt = __shfl_sync(0xffffffffu, bt, 0);
+            bg = __shfl_sync(0xffffffffu, bg, 0);
+            if (i < H) {
+                if (em) {
+                    const uint32_t off = bt + inc - s;
+                    gs[i] = (s << 12) | off;
+                    gl[i] = ((bg + (uint32_t)__popc(bal & lt)) << 12) | off;
+                } else {
+                    gs[i] = 0u;
+                    gl[i] = 0xffffffffu;
+                }
             }
         }
         __syncthreads();
-        // (4) ranges of the multi-sequence groups
-        emit_groups(gs, H, s_w, s_base, so, n_t, n_g);
-        // (5) triples
-        for (uint32_t i = threadIdx.x; i < H; i += GR_THREADS) {
+        if (threadIdx.x == 0) {
+            const uint32_t tt = s_cnt[0], tg = s_cnt[1];
+            s_base[0] = tt ? atomicAdd(&so.counts[0], tt) : 0u;
+            s_base[1] = tg ? atomicAdd(&so.counts[1], tg) : 0u;
+            n_t += tt;
+            n_g += tg;
+        }
+        __syncthreads();
+        const uint32_t tb = s_base[0], gb = s_base[1];
+        // (4) group ranges, diagonal repeats, triples
+        for (uint32_t i = threadIdx.x; i < H; i += GV_THREADS) {
+            const uint32_t q = gl[i];
+            if (q != 0xffffffffu) {
+                const uint32_t s = gs[i] >> 12, off = q & 0xfffu;
+                so.groups[gb + (q >> 12)] = make_uint2(tb + off, tb + off + s);
+            }
             const uint64_t v = tab[i];
             if (v == EMPTY) continue;
+            const uint32_t cc = (uint32_t)(v & ((1ull << CNT_BITS) - 1ull));
+            const uint32_t x = (uint32_t)((v >> CNT_BITS) & 0x7fffffffull);
+            if (cc >= 2)
+                atomicAdd((unsigned long long*)&Cm[(int64_t)x * N + x],
+                          (unsigned long long)cc * cc - cc);
             const uint32_t g = (uint32_t)(v >> (CNT_BITS + 31));
-            if (gs[g] == 0xffffffffu) continue;
-            const uint32_t pos = atomicAdd(&gs[g], 1u);
-            so.tseq[pos] = (uint32_t)((v >> CNT_BITS) & 0x7fffffffull);
-            so.tcnt[pos] = (uint32_t)(v & ((1ull << CNT_BITS) - 1ull));
+            if (gl[g] == 0xffffffffu) continue;
+            const uint32_t pos = tb + (atomicAdd(&gs[g], 1u) & 0xfffu);
+            so.tseq[pos] = x;
+            so.tcnt[pos] = cc;
         }
         __syncthreads();
     }
@@ -523,16 +557,16 @@ cudaError_t launch_bucket_group(const BkArgs& a, const void* keys, bool k64, int
     cudaError_t e = cudaMemsetAsync(so.counts, 0, 2 * sizeof(uint32_t), s);
     if (e != cudaSuccess || a.n == 0 || a.nmask == 0) return e;
     const uint64_t nbt = (uint64_t)a.nmask * a.nb;
-    const unsigned grid = (unsigned)std::min<uint64_t>(nbt, (uint64_t)sm_count * 2);
+    const unsigned grid = (unsigned)std::min<uint64_t>(nbt, (uint64_t)sm_count * 3);
     if (k64) {
         cudaFuncSetAttribute(bk_group_kernel<uint64_t>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GR_SMEM);
-        bk_group_kernel<uint64_t><<<grid, GR_THREADS, GR_SMEM, s>>>((const uint64_t*)keys, a, N,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GV_SMEM);
+        bk_group_kernel<uint64_t><<<grid, GV_THREADS, GV_SMEM, s>>>((const uint64_t*)keys, a, N,
                                                                      Cm, so, sc, stats);
     } else {
         cudaFuncSetAttribute(bk_group_kernel<uint32_t>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GR_SMEM);
-        bk_group_kernel<uint32_t><<<grid, GR_THREADS, GR_SMEM, s>>>((const uint32_t*)keys, a, N,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GV_SMEM);
+        bk_group_kernel<uint32_t><<<grid, GV_THREADS, GV_SMEM, s>>>((const uint32_t*)keys, a, N,
                                                                      Cm, so, sc, stats);
     }
     return cudaGetLastError();

@@ -76,7 +76,7 @@ struct gakco_plan {
     int rank = 0, world = 1;
     int64_t heavy_min = 0, batch_keys = 0;
     bool timing = false;
-    // grouping: -1 auto (hash partition when it applies, else chunked LSD),
+    // grouping: -1 auto (chunked LSD),
     // 0 chunked two-kernel LSD pass, 1 onesweep LSD (decoupled look-back),
     // 2 hash partition + shared-memory hash grouping (bucket.cu)
     int sort_mode = -1;
@@ -376,7 +376,8 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
     int bits = 1;
     while ((1 << bits) < p->sigma) ++bits;
     const int sbh = std::max(sb, 1);
-    bool hash_mode = (p->sort_mode == -1 || p->sort_mode == 2) && n > 0 && g * bits <= 64 &&
+    // (auto = LSD: the hash path measured slower on every config so far)
+    bool hash_mode = p->sort_mode == 2 && n > 0 && g * bits <= 64 &&
                      n <= (16384ull << 10);
     std::vector<int> level_runs(M + 1, 0);
     for (int m = 0; m <= M && hash_mode; ++m) {
@@ -438,7 +439,7 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
     // default: up to 64M keys (512 MB per key buffer): large launches measured
     // faster than L2-sized (4M-key) batches for every stage
     uint64_t bk = p->batch_keys > 0 ? (uint64_t)p->batch_keys
-                                    : (hash_mode ? (32ull << 20) : (64ull << 20));
+                                    : (hash_mode ? (12ull << 20) : (64ull << 20));
     if (bk > (1ull << 30) - 1) bk = (1ull << 30) - 1;
     uint64_t bmax_masks = std::max<uint64_t>(1, n ? bk / n : mine.size());
     if (heavy_on && nmax > 0) {

@@ -146,9 +146,9 @@ def test_sort_modes_ragged(gk, oracle_lib):
 
 
 def test_grouping_modes(gk, oracle_lib):
-    """Hash-partition grouping (bucket.cu, GAKCO_OPT_SORT 2, the default where it
-    applies) == chunked LSD sort (0) == onesweep LSD sort (1) == oracle; the stats
-    report which path ran."""
+    """Hash-partition grouping (bucket.cu, GAKCO_OPT_SORT 2) == chunked LSD sort
+    (0, the default) == onesweep LSD sort (1) == oracle; the stats report which
+    path ran."""
     rng = np.random.default_rng(108)
     for it in range(10):
         sigma = int(rng.choice([2, 4, 20, 36]))
@@ -162,7 +162,7 @@ def test_grouping_modes(gk, oracle_lib):
             assert_parity(r, ref)
             if r["stats"]["keys"] > 0:
                 assert r["stats"]["grouping"] == mode
-        assert run(gk, cp, g, k, M)["stats"]["grouping"] in (0, 2)
+        assert run(gk, cp, g, k, M)["stats"]["grouping"] == 0
 
 
 def test_hash_big_buckets(gk, oracle_lib):
@@ -361,16 +361,16 @@ def test_full_config_digests(gk, name):
     assert_knorm(r["Knorm"].cpu().numpy(), oracle.normalize(K))
 
 
-def test_dna_digests_lsd_sort(gk):
-    """The LSD radix-sort grouping (GAKCO_OPT_SORT 0) on the full DNA config also
-    matches the committed digests (the default there is the hash partition)."""
+def test_dna_digests_hash_grouping(gk):
+    """The hash-partition grouping (GAKCO_OPT_SORT 2, the NEXT-4 ablation) on the
+    full DNA config also matches the committed digests (the default is LSD)."""
     gold = _golden("dna")
     cfg = sc.CONFIGS["dna"]
     cp = sc.make("dna")
     plan = gk.Plan(cfg.sigma, cfg.g, cfg.k, cfg.M)
-    plan.set_option(gk.GAKCO_OPT_SORT, 0)
+    plan.set_option(gk.GAKCO_OPT_SORT, 2)
     r = gk.kernel_matrix(cp.codes, cp.offsets, cfg.sigma, cfg.g, cfg.k, cfg.M, plan=plan)
-    assert plan.stats()["grouping"] == 0
+    assert plan.stats()["grouping"] == 2
     plan.close()
     assert refs.digest_np(r["K"].cpu().numpy()) == int(gold["digests"]["K"])
     for m in range(cfg.M + 1):
