@@ -50,6 +50,8 @@ def args_():
     ap.add_argument("--sort", type=int, default=None, choices=[-1, 0, 1, 2],
                     help="grouping: -1 auto, 0 chunked LSD sort, 1 onesweep LSD, 2 hash partition")
     ap.add_argument("--sort-ctas", type=int, default=0)
+    ap.add_argument("--gram-pair", type=int, default=None, choices=[0, 1],
+                    help="heavy Gram kernel: 1 CTA pairs (default), 0 one SM per tile")
     ap.add_argument("--no-timing", action="store_true",
                     help="no per-stage events (roofline then uses the last timed stages)")
     return ap.parse_args()
@@ -259,6 +261,8 @@ def run_ours(a):
         plan.set_option(gakco.GAKCO_OPT_SORT, a.sort)
     if a.sort_ctas:
         plan.set_option(gakco.GAKCO_OPT_SORT_CTAS_PER_SM, a.sort_ctas)
+    if a.gram_pair is not None:
+        plan.set_option(gakco.GAKCO_OPT_GRAM_PAIR, a.gram_pair)
     if a.no_timing:
         plan.set_option(gakco.GAKCO_OPT_TIMING, 0)
     C = torch.zeros((M + 1, N, N), dtype=torch.int64, device=dev)

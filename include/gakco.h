@@ -69,9 +69,12 @@ typedef enum {
                                      hash grouping (falls back to 0 where it does not apply:
                                      g*ceil(log2 sigma) > 64 or > 16M g-mers) */
     GAKCO_OPT_SORT_CTAS_PER_SM = 5, /* chunked pass grid size in CTAs per SM (default 3) */
-    GAKCO_OPT_LIGHT_BINS = 6      /* light updates binned by accumulator block (ablation /
+    GAKCO_OPT_LIGHT_BINS = 6,     /* light updates binned by accumulator block (ablation /
                                      test knob): <= 0 = never (default; measured slower on
                                      Scale), > 0 = always, with this many cells per block */
+    GAKCO_OPT_GRAM_PAIR = 7       /* heavy-group Gram kernel: 1 = CTA pairs (tcgen05
+                                     cta_group::2, 256 x 512 tiles; default), 0 = one SM per
+                                     128 x 256 tile */
 } gakco_option;
 
 /* Counters of the last gakco_accumulate (algorithmic units). */

@@ -249,6 +249,11 @@ std::vector<int2> gram_tiles(int64_t n_pad);
 cudaError_t launch_gram_flush(uint8_t* D, int64_t n_pad, uint64_t ldd, uint32_t* dense_fill,
                               int64_t* Cm, int64_t N, const int2* tiles, int ntiles,
                               int sm_count, unsigned long long* stats, cudaStream_t s);
+// CTA-pair variant (gram2.cu): 256 x 512 pair tiles, n_pad a multiple of 512.
+std::vector<int2> gram2_tiles(int64_t n_pad);
+cudaError_t launch_gram2_flush(uint8_t* D, int64_t n_pad, uint64_t ldd, uint32_t* dense_fill,
+                               int64_t* Cm, int64_t N, const int2* tiles, int ntiles,
+                               int sm_count, unsigned long long* stats, cudaStream_t s);
 cudaError_t launch_diag_closed_form(const int64_t* gofs, int64_t N, int64_t nmask, int64_t* Cm,
                                     cudaStream_t s);
 cudaError_t launch_epilogue(int64_t* C, int64_t N, int g, int k, int M, int64_t* Nm, int64_t* K,

@@ -82,6 +82,7 @@ struct gakco_plan {
     int sort_mode = -1;
     int sort_ctas_per_sm = 3;  // chunked pass grid = this x SMs (measured best of 1..4)
     int64_t light_bins = 0;    // 0 auto, < 0 off, > 0 forced block size in cells
+    int gram_pair = 1;         // 1: CTA-pair Gram (gram2.cu), 0: one-SM Gram (gram_tc.cu)
     int sm_count = 148;
     std::string err;
 
@@ -94,6 +95,7 @@ struct gakco_plan {
         counts, kept, stats, flags, kdiag, Cscr, Nmscr, Kscr, Knscr, heavy, hcount, dense, tiles,
         lightacc, binrec, bincnt, win, bkH, bktot, bkbase, bkdesc, bktab, bktcnt, bkgs, bkocc;
     int64_t tiles_npad = -1;
+    int tiles_pair = -1;
     uint64_t dense_ldd = 0;
     int ntiles = 0;
     uint32_t epoch = 1;
@@ -288,6 +290,10 @@ extern "C" gakco_status gakco_set_option(gakco_plan* p, int option, int64_t valu
             if (value < 1 || value > 16) return p->fail(GAKCO_E_ARG, "1..16");
             p->sort_ctas_per_sm = (int)value;
             return GAKCO_OK;
+        case GAKCO_OPT_GRAM_PAIR:
+            if (value < 0 || value > 1) return p->fail(GAKCO_E_ARG, "gram pair must be 0 or 1");
+            p->gram_pair = (int)value;
+            return GAKCO_OK;
         case GAKCO_OPT_TIMING:
             p->timing = value != 0;
             return GAKCO_OK;
@@ -430,7 +436,7 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
     // updates on the light path and ~N_pad^2/2 u8 MACs on the Gram; with the
     // measured rates (~1.1e11 updates/s, ~1.5e15 MAC/s) they break even near
     // s = 0.0085 N_pad.
-    const int64_t n_pad = (N + 255) / 256 * 256;
+    const int64_t n_pad = p->gram_pair ? (N + 511) / 512 * 512 : (N + 255) / 256 * 256;
     int64_t heavy_min = p->heavy_min;
     if (heavy_min == 0) heavy_min = std::max<int64_t>(16, (int64_t)(0.0085 * (double)n_pad + 0.999));
     const bool heavy_on = heavy_min < (int64_t)1 << 40 && N >= 2;
@@ -523,14 +529,15 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
         rcap = std::max<uint64_t>(128, (rcap + 127) / 128 * 128);
         CK(p->ensure(p->dense, (size_t)n_pad * rcap, s));
         CK(p->ensure(p->heavy, rcap * sizeof(uint2), s));
-        if (p->tiles_npad != n_pad) {
-            std::vector<int2> t = gram_tiles(n_pad);
+        if (p->tiles_npad != n_pad || p->tiles_pair != p->gram_pair) {
+            std::vector<int2> t = p->gram_pair ? gram2_tiles(n_pad) : gram_tiles(n_pad);
             CK(p->ensure(p->tiles, t.size() * sizeof(int2), s));
             CK(cudaMemcpyAsync(p->tiles.p, t.data(), t.size() * sizeof(int2),
                                cudaMemcpyHostToDevice, s));
             CK(cudaStreamSynchronize(s));
             p->ntiles = (int)t.size();
             p->tiles_npad = n_pad;
+            p->tiles_pair = p->gram_pair;
         }
     }
     CorpusView cv{(const uint8_t*)p->codes.p, (const int64_t*)p->off.p, (const int64_t*)p->gofs.p,
@@ -561,9 +568,14 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
         cudaEvent_t ah = nullptr;
         p->stage_begin(s, &ah);
         p->launches += 1;  // + fill_reset
-        LK(launch_gram_flush((uint8_t*)p->dense.p, n_pad, rcap, (uint32_t*)p->hcount.p,
-                             level_ptr(dense_m), N, (const int2*)p->tiles.p, p->ntiles,
-                             p->sm_count, stats, s));
+        if (p->gram_pair)
+            LK(launch_gram2_flush((uint8_t*)p->dense.p, n_pad, rcap, (uint32_t*)p->hcount.p,
+                                  level_ptr(dense_m), N, (const int2*)p->tiles.p, p->ntiles,
+                                  p->sm_count, stats, s));
+        else
+            LK(launch_gram_flush((uint8_t*)p->dense.p, n_pad, rcap, (uint32_t*)p->hcount.p,
+                                 level_ptr(dense_m), N, (const int2*)p->tiles.p, p->ntiles,
+                                 p->sm_count, stats, s));
         p->stage_end(s, S_HEAVY, ah);
         dense_bound = 0;
         dense_masks = 0;

@@ -33,6 +33,7 @@ GAKCO_OPT_TIMING = 3
 GAKCO_OPT_SORT = 4
 GAKCO_OPT_SORT_CTAS_PER_SM = 5
 GAKCO_OPT_LIGHT_BINS = 6
+GAKCO_OPT_GRAM_PAIR = 7
 
 EXPORTS = ("gakco_create", "gakco_set_shard", "gakco_set_option", "gakco_accumulate",
            "gakco_finalize", "gakco_kernel", "gakco_kernel_k", "gakco_get_stats",

@@ -106,6 +106,7 @@ def test_heavy_light_equivalence(gk, oracle_lib):
         ref = oracle_lib.compute(cp, g, k, M)
         heavy = run(gk, cp, g, k, M, heavy_min_seqs=2)
         assert_parity(heavy, ref)
+        assert_parity(run(gk, cp, g, k, M, heavy_min_seqs=2, gram_pair=0), ref)
         assert_parity(run(gk, cp, g, k, M, heavy_min_seqs=1 << 50), ref)
         assert_parity(run(gk, cp, g, k, M), ref)
 
