@@ -50,6 +50,8 @@ def args_():
     ap.add_argument("--sort", type=int, default=None, choices=[-1, 0, 1, 2],
                     help="grouping: -1 auto, 0 chunked LSD sort, 1 onesweep LSD, 2 hash partition")
     ap.add_argument("--sort-ctas", type=int, default=0)
+    ap.add_argument("--light-flat", type=int, default=0,
+                    help="light groups of <= this many sequences share a warp (1..32)")
     ap.add_argument("--gram-pair", type=int, default=None, choices=[0, 1],
                     help="heavy Gram kernel: 1 CTA pairs (default), 0 one SM per tile")
     ap.add_argument("--no-timing", action="store_true",
@@ -231,6 +233,8 @@ def stage_model(stats, cfg, N):
         "segment": ("hbm", kbytes + 8.0 * trip + 8.0 * grp),  # read keys; write triples, groups
         "light": ("hbm", 8.0 * stats["light_pairs"]),  # u32 read-modify-write per update
         "heavy": ("tensor", 2.0 * stats["heavy_macs"]),
+        # one n_pad-byte u8 column per heavy group, written once
+        "dense": ("hbm", float(stats["heavy_groups"]) * float(stats.get("n_pad", 0))),
         "epilogue": ("hbm", float(epi)),
     }
 
@@ -261,6 +265,8 @@ def run_ours(a):
         plan.set_option(gakco.GAKCO_OPT_SORT, a.sort)
     if a.sort_ctas:
         plan.set_option(gakco.GAKCO_OPT_SORT_CTAS_PER_SM, a.sort_ctas)
+    if a.light_flat:
+        plan.set_option(gakco.GAKCO_OPT_LIGHT_FLAT, a.light_flat)
     if a.gram_pair is not None:
         plan.set_option(gakco.GAKCO_OPT_GRAM_PAIR, a.gram_pair)
     if a.no_timing:

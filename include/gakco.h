@@ -72,9 +72,12 @@ typedef enum {
     GAKCO_OPT_LIGHT_BINS = 6,     /* light updates binned by accumulator block (ablation /
                                      test knob): <= 0 = never (default; measured slower on
                                      Scale), > 0 = always, with this many cells per block */
-    GAKCO_OPT_GRAM_PAIR = 7       /* heavy-group Gram kernel: 1 = CTA pairs (tcgen05
+    GAKCO_OPT_GRAM_PAIR = 7,      /* heavy-group Gram kernel: 1 = CTA pairs (tcgen05
                                      cta_group::2, 256 x 512 tiles; default), 0 = one SM per
                                      128 x 256 tile */
+    GAKCO_OPT_LIGHT_FLAT = 8      /* light groups of <= this many sequences (1..32, default
+                                     8) have their pairs flattened across a warp; bigger
+                                     ones are enumerated from registers, one group per warp */
 } gakco_option;
 
 /* Counters of the last gakco_accumulate (algorithmic units). */
@@ -88,13 +91,17 @@ typedef struct {
     int64_t heavy_groups;   /* groups sent to the tensor-core Gram */
     int64_t heavy_macs;     /* u8 multiply-accumulates issued by the Gram */
     int64_t launches;       /* kernels launched by the last accumulate + finalize */
-    double ms_encode, ms_sort, ms_segment, ms_light, ms_heavy, ms_epilogue;
+    double ms_encode, ms_sort, ms_segment, ms_light, ms_heavy, ms_epilogue;  /* ms_heavy:
+                               the Gram flushes; building D is ms_dense */
     /* kernel launches per stage (same stages as the ms_* fields) */
     int64_t n_encode, n_sort, n_segment, n_light, n_heavy, n_epilogue;
     int64_t keys32;         /* of `keys`, those carried as 32-bit composites */
     int64_t sort_passes32;  /* of `sort_passes`, those over 32-bit composites */
     int64_t grouping;       /* path of the last accumulate: 0 chunked LSD sort,
                                1 onesweep LSD sort, 2 hash partition (bucket.cu) */
+    double ms_dense;        /* building the dense u8 count columns of heavy groups */
+    int64_t n_dense;
+    int64_t n_pad;          /* rows of the dense count matrix (0: no tensor-core Gram) */
 } gakco_stats;
 
 /* Create a plan for alphabet size sigma (1..255), g-mer length g (1..32),

@@ -12,10 +12,19 @@
 // through a shared-memory transpose so both writes are coalesced.
 // Invariant checks: N_m >= 0, K == C_{g-k} when M >= g-k.
 #include <math.h>
+#include <string.h>
 
 #include "internal.cuh"
 
 namespace gk {
+
+// Coefficients, computed on the host (launch_epilogue) and passed by value:
+//   e9[m][j] = C(g-j, m-j)  (Eq. 9 recursion, j < m)
+//   h[m]     = C(g-m, k) for m <= min(M, g-k), else 0  (Eq. 6-7)
+struct EpiCoef {
+    int64_t e9[GMAX + 1][GMAX + 1];
+    int64_t h[GMAX + 1];
+};
 
 struct EpiArgs {
     int64_t* C;
@@ -28,21 +37,11 @@ struct EpiArgs {
     int* flags;
 };
 
-__device__ __forceinline__ void binom_table(int64_t (*t)[GMAX + 1], int g) {
-    // Pascal's triangle rows 0..g, filled by thread 0 (tiny).
-    if (threadIdx.x == 0 && threadIdx.y == 0) {
-        for (int n = 0; n <= g; ++n)
-            for (int r = 0; r <= GMAX; ++r)
-                t[n][r] = (r == 0) ? 1 : (r > n ? 0 : (r == n ? 1 : t[n - 1][r - 1] + t[n - 1][r]));
-    }
-    __syncthreads();
-}
-
 // Per-entry math. prof[m] = C_m(X,Y) in, N_m(X,Y) out. Returns K(X,Y).
 // Loops run to the compile-time bound MM (guarded by M) so prof stays in registers.
 template <int MM, typename P>
-__device__ __forceinline__ int64_t entry(P prof, const int64_t (*bt)[GMAX + 1], int g,
-                                         int k, int M, int* bad) {
+__device__ __forceinline__ int64_t entry(P prof, const EpiCoef& cf, int g, int k, int M,
+                                         int* bad) {
     int64_t cgk = 0;
 #pragma unroll
     for (int m = 0; m <= MM; ++m)
@@ -52,29 +51,26 @@ __device__ __forceinline__ int64_t entry(P prof, const int64_t (*bt)[GMAX + 1], 
         if (m > M) break;
         int64_t v = prof[m];
 #pragma unroll
-        for (int j = 0; j < m; ++j) v -= bt[g - j][m - j] * prof[j];  // prof[j] is N_j now
+        for (int j = 0; j < m; ++j) v -= cf.e9[m][j] * prof[j];  // prof[j] is N_j now
         if (v < 0) *bad |= EF_NEGATIVE_N;
         prof[m] = v;
     }
     int64_t K = 0;
-    const int top = M < g - k ? M : g - k;
 #pragma unroll
     for (int m = 0; m <= MM; ++m)
-        if (m <= top) K += bt[g - m][k] * prof[m];
+        if (m <= M) K += cf.h[m] * prof[m];
     if (M >= g - k && K != cgk) *bad |= EF_K_MISMATCH;
     return K;
 }
 
-__global__ void kdiag_kernel(EpiArgs a) {
-    __shared__ int64_t bt[GMAX + 1][GMAX + 1];
-    binom_table(bt, a.g);
+__global__ void kdiag_kernel(EpiArgs a, const __grid_constant__ EpiCoef cf) {
     const int64_t nn = a.N * a.N;
     int bad = 0;
     for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < a.N;
          x += (int64_t)gridDim.x * blockDim.x) {
         int64_t prof[GMAX + 1];
         for (int m = 0; m <= a.M; ++m) prof[m] = a.C[m * nn + x * a.N + x];
-        a.kdiag[x] = entry<GMAX>(prof, bt, a.g, a.k, a.M, &bad);
+        a.kdiag[x] = entry<GMAX>(prof, cf, a.g, a.k, a.M, &bad);
     }
     if (bad) atomicOr(a.flags, bad);
 }
@@ -88,12 +84,11 @@ __device__ __forceinline__ double knorm(int64_t kxy, int64_t kxx, int64_t kyy, b
 // blockDim (32, 8); grid (tiles, tiles); block (bx=bj, by=bi) works iff bi <= bj.
 // MM bounds M so the per-thread profiles stay in registers.
 template <int MM>
-__global__ void __launch_bounds__(256) epilogue_kernel(EpiArgs a) {
-    __shared__ int64_t bt[GMAX + 1][GMAX + 1];
+__global__ void __launch_bounds__(256) epilogue_kernel(EpiArgs a,
+                                                       const __grid_constant__ EpiCoef cf) {
     __shared__ int64_t st[32][33];
     const int bi = blockIdx.y, bj = blockIdx.x;
     if (bi > bj) return;
-    binom_table(bt, a.g);
     const int tx = threadIdx.x, ty = threadIdx.y;
     const int64_t N = a.N, nn = N * N;
     const int M = a.M;
@@ -118,7 +113,7 @@ __global__ void __launch_bounds__(256) epilogue_kernel(EpiArgs a) {
             for (int m = 0; m <= MM; ++m)
                 if (m <= M) a.C[m * nn + X * N + Y] = prof[q][m];
         }
-        kv[q] = entry<MM>(prof[q], bt, a.g, a.k, M, &bad);  // prof now holds N_m
+        kv[q] = entry<MM>(prof[q], cf, a.g, a.k, M, &bad);  // prof now holds N_m
         if (a.Nm) {
 #pragma unroll
             for (int m = 0; m <= MM; ++m)
@@ -177,15 +172,25 @@ __global__ void __launch_bounds__(256) epilogue_kernel(EpiArgs a) {
 cudaError_t launch_epilogue(int64_t* C, int64_t N, int g, int k, int M, int64_t* Nm, int64_t* K,
                             double* Knorm, int64_t* kdiag, int* flags, cudaStream_t s) {
     EpiArgs a{C, N, g, k, M, Nm, K, Knorm, kdiag, flags};
+    EpiCoef cf;
+    memset(&cf, 0, sizeof cf);
+    int64_t bt[GMAX + 1][GMAX + 1];  // Pascal's triangle
+    for (int n = 0; n <= GMAX; ++n)
+        for (int r = 0; r <= GMAX; ++r)
+            bt[n][r] = (r == 0) ? 1 : (r > n ? 0 : (r == n ? 1 : bt[n - 1][r - 1] + bt[n - 1][r]));
+    for (int m = 0; m <= M && m <= GMAX; ++m) {
+        for (int j = 0; j < m; ++j) cf.e9[m][j] = bt[g - j][m - j];
+        cf.h[m] = (m <= g - k) ? bt[g - m][k] : 0;
+    }
     int64_t blocks = (N + 255) / 256;
-    kdiag_kernel<<<(int)(blocks < 1024 ? blocks : 1024), 256, 0, s>>>(a);
+    kdiag_kernel<<<(int)(blocks < 1024 ? blocks : 1024), 256, 0, s>>>(a, cf);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     const unsigned tiles = (unsigned)((N + 31) / 32);
     if (M <= 7)
-        epilogue_kernel<7><<<dim3(tiles, tiles), dim3(32, 8), 0, s>>>(a);
+        epilogue_kernel<7><<<dim3(tiles, tiles), dim3(32, 8), 0, s>>>(a, cf);
     else
-        epilogue_kernel<GMAX><<<dim3(tiles, tiles), dim3(32, 8), 0, s>>>(a);
+        epilogue_kernel<GMAX><<<dim3(tiles, tiles), dim3(32, 8), 0, s>>>(a, cf);
     return cudaGetLastError();
 }
 

@@ -299,8 +299,10 @@ cudaError_t launch_gram2_flush(uint8_t* D, int64_t n_pad, uint64_t ldd, uint32_t
     if (me != cudaSuccess) return me;
     cudaFuncSetAttribute(gram2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G2_SMEM);
     const int pairs = std::max(1, sm_count / 2);
-    // split K so that there are >= ~4 work units per pair
-    const int ksplit = std::max(1, std::min(16, (4 * pairs) / std::max(1, ntiles)));
+    // split K only as far as it fills the machine: the smallest split whose last
+    // wave keeps >= 90% of the workers busy (one wave of whole-K tiles streams
+    // each K slab of D from DRAM once, shared through L2 by all tiles)
+    const int ksplit = gram_ksplit(ntiles, pairs);
     Gram2Args a{Cm, N, dense_fill, (uint32_t)ldd, tiles, ntiles, tma_epi, ksplit};
     const int units = ntiles * ksplit;
     const int grid = 2 * std::min(pairs, units);

@@ -304,6 +304,107 @@ __global__ void __launch_bounds__(BD_THREADS) build_dense_kernel(
     }
 }
 
+// Build v2: work item = one whole slab (128 columns) x BD2_ROWS rows, so every
+// 128-byte line of D is written once, in full, by one CTA (16-byte stores). The
+// slab is assembled in shared memory with 4-byte words XOR-swizzled by row (the
+// scatter of one column over many rows then spreads over all banks). A group's
+// triples are in ascending sequence order on the sort path (sorted = 1): a warp
+// brackets the row range with one round of 32 samples and scans only that part;
+// otherwise (hash grouping) it scans the whole group with a row filter.
+constexpr int BD2_ROWS = 512;
+constexpr int BD2_THREADS = 512;
+constexpr size_t BD2_SMEM = (size_t)BD2_ROWS * GT_KB;  // 64 KB
+
+__device__ __forceinline__ uint32_t bd2_off(uint32_t r, uint32_t cc) {
+    return r * GT_KB + ((((cc >> 2) ^ (r & 31u)) << 2) | (cc & 3u));
+}
+
+__global__ void __launch_bounds__(BD2_THREADS) build_dense2_kernel(
+    SegmentOut so, const uint2* __restrict__ heavy_list, const uint32_t* fill,
+    uint8_t* __restrict__ D, int64_t n_pad, uint64_t ldd, int sorted) {
+    extern __shared__ __align__(16) unsigned char sb[];  // [BD2_ROWS][128], swizzled words
+    const uint64_t f0 = fill[1];
+    const uint64_t f1 = min((uint64_t)fill[0], ldd);
+    if (f1 <= f0) return;
+    const uint64_t s0 = f0 / GT_KB, s1 = (f1 + GT_KB - 1) / GT_KB;
+    const uint64_t nrc = (uint64_t)(n_pad + BD2_ROWS - 1) / BD2_ROWS;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (uint64_t wk = blockIdx.x; wk < (s1 - s0) * nrc; wk += gridDim.x) {
+        const uint64_t slab = s0 + wk / nrc;
+        const uint32_t r0 = (uint32_t)(wk % nrc) * BD2_ROWS;
+        const uint32_t rows = (uint32_t)min((int64_t)BD2_ROWS, n_pad - (int64_t)r0);
+        for (uint32_t i = threadIdx.x; i < rows * (GT_KB / 16); i += BD2_THREADS)
+            ((uint4*)sb)[i] = make_uint4(0u, 0u, 0u, 0u);
+        __syncthreads();
+        // warp w fills columns w + 16 j (j < 8); the 8 columns' loads are issued
+        // together at every step (one latency per step, not per column)
+        constexpr int CPW = GT_KB / (BD2_THREADS / 32);  // 8 columns per warp
+        uint32_t lo[CPW], hi[CPW];
+        {
+            const uint64_t col = slab * GT_KB + warp + (BD2_THREADS / 32) * (lane & (CPW - 1));
+            const uint2 bnd = (lane < CPW && col < f1) ? heavy_list[col] : make_uint2(0u, 0u);
+#pragma unroll
+            for (int j = 0; j < CPW; ++j) {
+                lo[j] = __shfl_sync(0xffffffffu, bnd.x, j);
+                hi[j] = __shfl_sync(0xffffffffu, bnd.y, j);
+            }
+        }
+        if (sorted) {
+            // one round of 32 samples per column brackets the rows [r0, r0 + rows)
+            uint32_t xs[CPW];
+#pragma unroll
+            for (int j = 0; j < CPW; ++j) {
+                const uint32_t len = hi[j] - lo[j];
+                xs[j] = len > 64 ? so.tseq[lo[j] + (uint32_t)(((uint64_t)len * lane) >> 5)] & 0x7fffffffu
+                                 : 0u;
+            }
+#pragma unroll
+            for (int j = 0; j < CPW; ++j) {
+                const uint32_t len = hi[j] - lo[j];
+                if (len <= 64) continue;  // warp-uniform
+                const uint32_t below = __ballot_sync(0xffffffffu, xs[j] < r0);
+                const uint32_t inside = __ballot_sync(0xffffffffu, xs[j] < r0 + rows);
+                const int lb = below ? 31 - __clz(below) : -1;
+                const int ib = inside ? 31 - __clz(inside) : -1;
+                const uint32_t nlo = lb < 0 ? lo[j] : lo[j] + (uint32_t)(((uint64_t)len * lb) >> 5);
+                const uint32_t nhi =
+                    ib == 31 ? hi[j] : lo[j] + (uint32_t)(((uint64_t)len * (ib + 1)) >> 5);
+                lo[j] = nlo;
+                hi[j] = ib < 0 ? nlo : nhi;
+            }
+        }
+        uint32_t todo = 0;
+#pragma unroll
+        for (int j = 0; j < CPW; ++j) todo = max(todo, hi[j] - lo[j]);
+        for (uint32_t o = lane; o < todo; o += 32) {
+            uint32_t xv[CPW], cv[CPW];
+#pragma unroll
+            for (int j = 0; j < CPW; ++j) {
+                const uint32_t t = lo[j] + o;
+                xv[j] = t < hi[j] ? so.tseq[t] & 0x7fffffffu : 0xffffffffu;
+                cv[j] = t < hi[j] ? so.tcnt[t] : 0u;
+            }
+#pragma unroll
+            for (int j = 0; j < CPW; ++j)
+                if (xv[j] >= r0 && xv[j] < r0 + rows)
+                    sb[bd2_off(xv[j] - r0, warp + (BD2_THREADS / 32) * j)] = (uint8_t)cv[j];
+        }
+        __syncthreads();
+        uint4* dst = (uint4*)(D + (slab * (uint64_t)n_pad + r0) * GT_KB);
+        for (uint32_t i = threadIdx.x; i < rows * (GT_KB / 16); i += BD2_THREADS) {
+            const uint32_t r = i >> 3, q = i & 7;
+            const uint32_t* w = (const uint32_t*)(sb + r * GT_KB);
+            uint4 v;
+            v.x = w[(4 * q + 0) ^ (r & 31u)];
+            v.y = w[(4 * q + 1) ^ (r & 31u)];
+            v.z = w[(4 * q + 2) ^ (r & 31u)];
+            v.w = w[(4 * q + 3) ^ (r & 31u)];
+            dst[i] = v;
+        }
+        __syncthreads();
+    }
+}
+
 // After a batch's build: fill rounded up to whole slabs; the next batch starts there.
 __global__ void fill_round_kernel(uint32_t* fill, uint64_t ldd) {
     uint64_t f = min((uint64_t)fill[0], ldd);
@@ -322,13 +423,12 @@ __global__ void fill_reset_kernel(uint32_t* fill, uint64_t ldd, uint64_t tile_ma
 }
 
 cudaError_t launch_build_dense(SegmentOut so, const uint2* heavy_list, uint32_t* dense_fill,
-                               uint8_t* D, int64_t n_pad, uint64_t ldd, int sm_count,
+                               uint8_t* D, int64_t n_pad, uint64_t ldd, int sorted, int sm_count,
                                cudaStream_t s) {
-    const size_t smem = (size_t)BD_ROWS * BD_STRIDE;  // 64 KB: 3 CTAs per SM
-    cudaFuncSetAttribute(build_dense_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
-    build_dense_kernel<<<sm_count * 3, BD_THREADS, smem, s>>>(so, heavy_list, dense_fill, D,
-                                                              n_pad, ldd);
+    cudaFuncSetAttribute(build_dense2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)BD2_SMEM);
+    build_dense2_kernel<<<sm_count * 3, BD2_THREADS, BD2_SMEM, s>>>(so, heavy_list, dense_fill,
+                                                                    D, n_pad, ldd, sorted);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     fill_round_kernel<<<1, 1, 0, s>>>(dense_fill, ldd);
@@ -406,8 +506,10 @@ cudaError_t launch_gram_flush(uint8_t* D, int64_t n_pad, uint64_t ldd, uint32_t*
     cudaError_t me = gram_maps(D, n_pad, ldd, Cm, N, GT_EC, &map, &cmap, &tma_epi);
     if (me != cudaSuccess) return me;
     cudaFuncSetAttribute(gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GT_SMEM);
-    // split K so that there are >= ~2 work units per SM when tiles are few
-    const int ksplit = std::max(1, std::min(16, (2 * sm_count) / std::max(1, ntiles)));
+    // split K only as far as it fills the machine: the smallest split whose last
+    // wave keeps >= 90% of the workers busy (one wave of whole-K tiles streams
+    // each K slab of D from DRAM once, shared through L2 by all tiles)
+    const int ksplit = gram_ksplit(ntiles, sm_count);
     GramArgs a{Cm, N, dense_fill, (uint32_t)ldd, tiles, ntiles, tma_epi ? 1 : 0, ksplit};
     int grid = ntiles * ksplit < sm_count ? ntiles * ksplit : sm_count;
     gram_kernel<<<grid, GT_THREADS, GT_SMEM, s>>>(map, cmap, a);

@@ -231,14 +231,15 @@ struct LightBins {
 };
 cudaError_t launch_light(SegmentOut so, uint64_t max_groups, int64_t heavy_min, int64_t N,
                          uint32_t* acc, uint2* heavy_list, uint64_t ldd,
-                         uint32_t* dense_fill, LightBins bins, unsigned long long* stats,
-                         int sm_count, cudaStream_t s);
+                         uint32_t* dense_fill, LightBins bins, uint32_t flat_max,
+                         unsigned long long* stats, int sm_count, cudaStream_t s);
 // Fill the D slabs of the columns claimed by this batch ([prev, fill) with
 // prev = dense_fill[1], a multiple of 128) from the batch's triples, in shared
 // memory, with full-line stores; then round dense_fill[0] up to a multiple of 128
 // and set dense_fill[1] = dense_fill[0].
+// sorted = 1: each group's triples are in ascending sequence order (LSD path).
 cudaError_t launch_build_dense(SegmentOut so, const uint2* heavy_list, uint32_t* dense_fill,
-                               uint8_t* D, int64_t n_pad, uint64_t ldd, int sm_count,
+                               uint8_t* D, int64_t n_pad, uint64_t ldd, int sorted, int sm_count,
                                cudaStream_t s);
 // acc: u32 strictly-upper packed triangle (N(N-1)/2); flush adds it into C_m, zeroes it.
 cudaError_t launch_light_flush(uint32_t* acc, int64_t N, int64_t* Cm, int sm_count,
@@ -246,6 +247,23 @@ cudaError_t launch_light_flush(uint32_t* acc, int64_t N, int64_t* Cm, int sm_cou
 // Heavy path (gram_tc.cu): C_m += D D^T over the *dense_fill filled columns
 // (count read on the device), then the used columns are zeroed and the fill reset.
 std::vector<int2> gram_tiles(int64_t n_pad);
+// K split of a Gram flush: smallest ks in 1..16 with tiles*ks / (waves*workers) >= 0.9
+inline int gram_ksplit(int ntiles, int workers) {
+    if (ntiles <= 0 || workers <= 0) return 1;
+    int best = 1;
+    double best_eff = 0.0;
+    for (int ks = 1; ks <= 16; ++ks) {
+        const long units = (long)ntiles * ks;
+        const long waves = (units + workers - 1) / workers;
+        const double eff = (double)units / (double)(waves * workers);
+        if (eff >= 0.9) return ks;
+        if (eff > best_eff + 1e-9) {
+            best_eff = eff;
+            best = ks;
+        }
+    }
+    return best;
+}
 cudaError_t launch_gram_flush(uint8_t* D, int64_t n_pad, uint64_t ldd, uint32_t* dense_fill,
                               int64_t* Cm, int64_t N, const int2* tiles, int ntiles,
                               int sm_count, unsigned long long* stats, cudaStream_t s);

@@ -74,7 +74,7 @@ cudaError_t launch_apply_bins(uint32_t* acc, LightBins bn, int sm_count, cudaStr
 __global__ void __launch_bounds__(256) light_kernel(SegmentOut so, int64_t heavy_min, int64_t N,
                                                     uint32_t* acc, uint2* heavy_list,
                                                     uint64_t ldd, uint32_t* dense_fill,
-                                                    LightBins bn,
+                                                    LightBins bn, uint32_t flat_max,
                                                     unsigned long long* stats) {
     // triangle table: pairs (a < b < 32) ordered by b, so the first n(n-1)/2
     // entries are exactly the pairs of an n-triple chunk
@@ -97,10 +97,12 @@ __global__ void __launch_bounds__(256) light_kernel(SegmentOut so, int64_t heavy
         const uint32_t my_start = rg.x, my_end = rg.y;
         const uint32_t my_s = my_end - my_start;
 
-        // (1) small light groups (s <= 32) of the batch: their pairs are flattened
-        // into one index space, so every lane does one pair update per round
-        // whatever the group sizes (no lane idles on a 2-sequence group).
-        const bool flat = lane < ng && my_s <= 32 && (int64_t)my_s < heavy_min;
+        // (1) small light groups (s <= flat_max <= 32) of the batch: their pairs are
+        // flattened into one index space, so every lane does one pair update per
+        // round whatever the group sizes (no lane idles on a 2-sequence group);
+        // the triples are gathered per pair, so bigger groups go to (2), which
+        // loads each group's triples once into registers.
+        const bool flat = lane < ng && my_s <= flat_max && (int64_t)my_s < heavy_min;
         const uint32_t P = flat ? my_s * (my_s - 1) / 2 : 0u;
         uint32_t incl = P;
 #pragma unroll
@@ -215,14 +217,14 @@ __global__ void __launch_bounds__(256) light_kernel(SegmentOut so, int64_t heavy
 
 cudaError_t launch_light(SegmentOut so, uint64_t max_groups, int64_t heavy_min, int64_t N,
                          uint32_t* acc, uint2* heavy_list, uint64_t ldd,
-                         uint32_t* dense_fill, LightBins bins, unsigned long long* stats,
-                         int sm_count, cudaStream_t s) {
+                         uint32_t* dense_fill, LightBins bins, uint32_t flat_max,
+                         unsigned long long* stats, int sm_count, cudaStream_t s) {
     if (max_groups == 0) return cudaGetLastError();
     uint64_t blocks = (max_groups + 255) / 256;  // 8 warps x 32 groups per block-round
     uint64_t cap = (uint64_t)sm_count * 8;
     if (blocks > cap) blocks = cap;
     light_kernel<<<(unsigned)blocks, 256, 0, s>>>(so, heavy_min, N, acc, heavy_list, ldd,
-                                                  dense_fill, bins, stats);
+                                                  dense_fill, bins, flat_max, stats);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess || bins.nb == 0) return e;
     return launch_apply_bins(acc, bins, sm_count, s);

@@ -30,7 +30,7 @@ struct DevBuf {
     size_t cap = 0;
 };
 
-enum Stage { S_ENCODE = 0, S_SORT, S_SEGMENT, S_LIGHT, S_HEAVY, S_EPILOGUE, S_NSTAGE };
+enum Stage { S_ENCODE = 0, S_SORT, S_SEGMENT, S_LIGHT, S_HEAVY, S_EPILOGUE, S_DENSE, S_NSTAGE };
 
 struct DeviceGuard {
     int prev = -1;
@@ -83,6 +83,7 @@ struct gakco_plan {
     int sort_ctas_per_sm = 3;  // chunked pass grid = this x SMs (measured best of 1..4)
     int64_t light_bins = 0;    // 0 auto, < 0 off, > 0 forced block size in cells
     int gram_pair = 1;         // 1: CTA-pair Gram (gram2.cu), 0: one-SM Gram (gram_tc.cu)
+    int light_flat = 8;        // light groups of <= this many sequences share warps
     int sm_count = 148;
     std::string err;
 
@@ -147,7 +148,7 @@ struct gakco_plan {
         }
         return ev_pool[ev_used++];
     }
-    int64_t stage_launches[S_NSTAGE] = {0, 0, 0, 0, 0, 0};
+    int64_t stage_launches[S_NSTAGE] = {0, 0, 0, 0, 0, 0, 0};
     int64_t launches_at_begin = 0;
     int last_grouping = 0;
     void stage_begin(cudaStream_t s, cudaEvent_t* a) {
@@ -294,6 +295,10 @@ extern "C" gakco_status gakco_set_option(gakco_plan* p, int option, int64_t valu
             if (value < 0 || value > 1) return p->fail(GAKCO_E_ARG, "gram pair must be 0 or 1");
             p->gram_pair = (int)value;
             return GAKCO_OK;
+        case GAKCO_OPT_LIGHT_FLAT:
+            if (value < 1 || value > 32) return p->fail(GAKCO_E_ARG, "light flat must be 1..32");
+            p->light_flat = (int)value;
+            return GAKCO_OK;
         case GAKCO_OPT_TIMING:
             p->timing = value != 0;
             return GAKCO_OK;
@@ -438,7 +443,7 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
     // s = 0.0085 N_pad.
     const int64_t n_pad = p->gram_pair ? (N + 511) / 512 * 512 : (N + 255) / 256 * 256;
     int64_t heavy_min = p->heavy_min;
-    if (heavy_min == 0) heavy_min = std::max<int64_t>(16, (int64_t)(0.0085 * (double)n_pad + 0.999));
+    if (heavy_min == 0) heavy_min = std::max<int64_t>(16, (int64_t)(0.012 * (double)n_pad + 0.999));
     const bool heavy_on = heavy_min < (int64_t)1 << 40 && N >= 2;
 
     // batch size (keys cap; with the Gram on, s32 exactness: masks * n_max^2 < 2^31)
@@ -733,15 +738,16 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
         if (n > 0) {
             p->stage_begin(s, &a);
             LK(launch_light(so, n * nmask / 2 + 1, light_limit, N, (uint32_t*)p->lightacc.p,
-                            (uint2*)p->heavy.p, rcap, (uint32_t*)p->hcount.p, bins, stats,
-                            p->sm_count, s));
+                            (uint2*)p->heavy.p, rcap, (uint32_t*)p->hcount.p, bins,
+                            (uint32_t)p->light_flat, stats, p->sm_count, s));
             p->stage_end(s, S_LIGHT, a);
             if (gram_ok) {
                 p->stage_begin(s, &a);
                 p->launches += 1;  // + fill_round
                 LK(launch_build_dense(so, (const uint2*)p->heavy.p, (uint32_t*)p->hcount.p,
-                                      (uint8_t*)p->dense.p, n_pad, rcap, p->sm_count, s));
-                p->stage_end(s, S_HEAVY, a);
+                                      (uint8_t*)p->dense.p, n_pad, rcap, hash_mode ? 0 : 1,
+                                      p->sm_count, s));
+                p->stage_end(s, S_DENSE, a);
             }
         }
         LK(launch_diag_closed_form((const int64_t*)p->gofs.p, N, nmask, Cm, s));
@@ -761,6 +767,7 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
     p->host_stats.keys32 = keys32;
     p->host_stats.sort_passes32 = passkeys32;
     p->host_stats.grouping = p->last_grouping;
+    p->host_stats.n_pad = gram_ok ? n_pad : 0;
     p->after_accumulate = true;
     return GAKCO_OK;
 #undef CK
@@ -908,8 +915,8 @@ extern "C" gakco_status gakco_get_stats(gakco_plan* p, gakco_stats* out) {
     DeviceGuard dg(p->device);
     gakco_stats r = p->host_stats;
     r.launches = p->launches;
-    int64_t* nl[S_NSTAGE] = {&r.n_encode, &r.n_sort, &r.n_segment,
-                             &r.n_light,  &r.n_heavy, &r.n_epilogue};
+    int64_t* nl[S_NSTAGE] = {&r.n_encode, &r.n_sort,     &r.n_segment, &r.n_light,
+                             &r.n_heavy,  &r.n_epilogue, &r.n_dense};
     for (int i = 0; i < S_NSTAGE; ++i) *nl[i] = p->stage_launches[i];
     if (p->stats.p) {
         unsigned long long d[ST_COUNT];
@@ -923,8 +930,8 @@ extern "C" gakco_status gakco_get_stats(gakco_plan* p, gakco_stats* out) {
         r.heavy_groups = (int64_t)d[ST_HEAVY_GROUPS];
         r.heavy_macs = (int64_t)d[ST_HEAVY_MACS];
     }
-    double* ms[S_NSTAGE] = {&r.ms_encode, &r.ms_sort, &r.ms_segment,
-                            &r.ms_light,  &r.ms_heavy, &r.ms_epilogue};
+    double* ms[S_NSTAGE] = {&r.ms_encode, &r.ms_sort,     &r.ms_segment, &r.ms_light,
+                            &r.ms_heavy,  &r.ms_epilogue, &r.ms_dense};
     for (auto& se : p->evs) {
         float t = 0;
         cudaEventSynchronize(se.second.second);

@@ -34,6 +34,7 @@ GAKCO_OPT_SORT = 4
 GAKCO_OPT_SORT_CTAS_PER_SM = 5
 GAKCO_OPT_LIGHT_BINS = 6
 GAKCO_OPT_GRAM_PAIR = 7
+GAKCO_OPT_LIGHT_FLAT = 8
 
 EXPORTS = ("gakco_create", "gakco_set_shard", "gakco_set_option", "gakco_accumulate",
            "gakco_finalize", "gakco_kernel", "gakco_kernel_k", "gakco_get_stats",
@@ -47,7 +48,8 @@ class gakco_stats(ctypes.Structure):
             "ms_encode", "ms_sort", "ms_segment", "ms_light", "ms_heavy", "ms_epilogue")] + [
         (n, ctypes.c_int64) for n in (
             "n_encode", "n_sort", "n_segment", "n_light", "n_heavy", "n_epilogue", "keys32",
-            "sort_passes32", "grouping")]
+            "sort_passes32", "grouping")] + [("ms_dense", ctypes.c_double)] + [
+        (n, ctypes.c_int64) for n in ("n_dense", "n_pad")]
 
     def as_dict(self):
         return {n: getattr(self, n) for n, _ in self._fields_}

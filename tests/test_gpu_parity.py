@@ -111,6 +111,20 @@ def test_heavy_light_equivalence(gk, oracle_lib):
         assert_parity(run(gk, cp, g, k, M), ref)
 
 
+def test_light_flat_threshold(gk, oracle_lib):
+    """Light groups enumerated flattened across a warp (s <= flat) or from
+    registers one group per warp: every threshold gives the oracle's result."""
+    rng = np.random.default_rng(111)
+    for _ in range(6):
+        sigma = int(rng.choice([2, 4, 20]))
+        g = int(rng.integers(3, 9))
+        k = int(rng.integers(1, g + 1))
+        cp = sc.random_small(rng, sigma, n_max=150, l_max=90)
+        ref = oracle_lib.compute(cp, g, k, g - k)
+        for flat in (1, 5, 32):
+            assert_parity(run(gk, cp, g, k, g - k, light_flat=flat, heavy_min_seqs=1 << 50), ref)
+
+
 def test_light_binning(gk, oracle_lib):
     """Binned light updates (forced, tiny accumulator blocks so records span many
     buckets and some buckets overflow to direct atomics) == oracle."""
