@@ -153,6 +153,22 @@ gakco_status gakco_kernel(gakco_plan* plan, const uint8_t* codes, const int64_t*
 gakco_status gakco_kernel_k(gakco_plan* plan, const uint8_t* codes, const int64_t* offsets,
                             int64_t N, int64_t* K, double* Knorm, void* cuda_stream);
 
+/* Rectangular train x test kernel. The corpus holds the NA
+ * training sequences first, then the NB = N - NA test sequences. Computes the
+ * NA x NB block (rows = train, columns = test) of C_m, N_m, K and Knorm of the
+ * concatenated corpus — what the SVM decision function needs, K(x_i, x) (Eq. 1,
+ * P:66; the paper concatenates train and test into one N x N matrix) —
+ * without any train x train or test x test pair update, plus Kdiag[X] = K(X,X) for
+ * all N sequences (the normalisation of Knorm). Knorm(X,Y) = K(X,Y) /
+ * sqrt(K(X,X) K(Y,Y)) as in the full path.
+ *   N >= 2, 1 <= NA <= N - 1; C, Nm: int64[(M+1)*NA*NB]; K: int64[NA*NB];
+ *   Knorm: fp64[NA*NB]; Kdiag: int64[N]; row-major, [m][X][Y - NA].
+ * Any output may be NULL (not returned; C NULL = plan scratch) and host or device.
+ * Errors as gakco_kernel; shard setting ignored. */
+gakco_status gakco_kernel_rect(gakco_plan* plan, const uint8_t* codes, const int64_t* offsets,
+                               int64_t N, int64_t NA, int64_t* C, int64_t* Nm, int64_t* K,
+                               double* Knorm, int64_t* Kdiag, void* cuda_stream);
+
 /* Counters and (if GAKCO_OPT_TIMING) stage times of the last accumulate /
  * finalize. Synchronises the plan's last stream. */
 gakco_status gakco_get_stats(gakco_plan* plan, gakco_stats* out);

@@ -185,6 +185,37 @@ def pair_outputs(nm_rows: np.ndarray, g: int, k: int) -> dict:
     return {"C": C, "K": K}
 
 
+def normalize_rect(K: np.ndarray, kd_rows: np.ndarray, kd_cols: np.ndarray) -> np.ndarray:
+    """K(X,Y)/sqrt(K(X,X)K(Y,Y)) for a rectangular block (reading A5): 0 where a
+    diagonal is <= 0; computed as (double)K / sqrt((double)Kxx * (double)Kyy)."""
+    out = np.zeros(K.shape, dtype=np.float64)
+    for i in range(K.shape[0]):
+        for j in range(K.shape[1]):
+            a, b = int(kd_rows[i]), int(kd_cols[j])
+            if a > 0 and b > 0:
+                out[i, j] = float(K[i, j]) / np.sqrt(float(a) * float(b))
+    return out
+
+
+def rect(corpus, NA: int, g: int, k: int, M: int, threads: int | None = None) -> dict:
+    """Train x test block: rows X < NA, columns Y = NA..N-1 of
+    the concatenated corpus's C_m, N_m, K, Knorm (the same definitions as compute():
+    Def. 1 / Eq. 5 histograms per pair, Eq. 8, Eq. 6-7, reading A5), and
+    Kdiag[X] = K(X,X) for all N (Eq. 1 needs K(x_i, x))."""
+    N = int(np.asarray(corpus.offsets).size - 1)
+    NB = N - NA
+    X = np.repeat(np.arange(NA, dtype=np.int64), NB)
+    Y = np.tile(np.arange(NA, N, dtype=np.int64), NA)
+    nm = pairs(corpus, g, M, X, Y, threads)
+    po = pair_outputs(nm, g, k)
+    d = np.arange(N, dtype=np.int64)
+    kd = pair_outputs(pairs(corpus, g, M, d, d, threads), g, k)["K"]
+    K = po["K"].reshape(NA, NB)
+    return {"C": po["C"].T.reshape(M + 1, NA, NB).copy(),
+            "Nm": nm.T.reshape(M + 1, NA, NB).copy(),
+            "K": K, "Knorm": normalize_rect(K, kd[:NA], kd[NA:]), "Kdiag": kd}
+
+
 def digests(corpus, g: int, k: int, M: int, threads: int | None = None,
             row_begin: int = 0, row_end: int | None = None, rows: bool = True):
     """Digests of C_0..C_M, N_0..N_M, K, Knorm without materialising them."""

@@ -272,8 +272,8 @@ __device__ __forceinline__ void emit_groups(uint32_t* gs, uint32_t H, uint32_t* 
 // of H = 2c slots live in scratch at entry offset 2*start (the bucket's own
 // region, disjoint from every other bucket's).
 template <typename K>
-__device__ void group_big(const K* keys, uint64_t start, uint32_t c, int sb, int64_t N,
-                          int64_t* Cm, SegmentOut so, BkScratch sc, uint32_t* s_w,
+__device__ void group_big(const K* keys, uint64_t start, uint32_t c, int sb, int64_t dstride,
+                          int64_t* diag, SegmentOut so, BkScratch sc, uint32_t* s_w,
                           uint32_t* s_base, unsigned long long& n_t, unsigned long long& n_g) {
     const uint32_t H = 2u * c;
     uint64_t* tab = sc.tab + 2 * start;
@@ -333,7 +333,7 @@ __device__ void group_big(const K* keys, uint64_t start, uint32_t c, int sb, int
         const uint32_t x = (uint32_t)(v & 0xffffffffull);
         const uint64_t cc = tcnt[i];
         if (cc >= 2)
-            atomicAdd((unsigned long long*)&Cm[(int64_t)x * N + x], (unsigned long long)(cc * cc - cc));
+            atomicAdd((unsigned long long*)&diag[(int64_t)x * dstride], (unsigned long long)(cc * cc - cc));
         const uint32_t g = (uint32_t)(v >> 32);
         if (*(volatile uint32_t*)&gs[g] == 0xffffffffu) continue;
         const uint32_t pos = atomicAdd(&gs[g], 1u);
@@ -362,7 +362,7 @@ constexpr size_t GV_SMEM = (size_t)GV_HMAX * 8 + (size_t)GV_HMAX * 4 * 2 + (size
 
 template <typename K>
 __global__ void __launch_bounds__(GV_THREADS, 3) bk_group_kernel(
-    const K* __restrict__ keys, BkArgs a, int64_t N, int64_t* Cm, SegmentOut so,
+    const K* __restrict__ keys, BkArgs a, int64_t dstride, int64_t* diag, SegmentOut so,
     BkScratch sc, unsigned long long* stats) {
     extern __shared__ __align__(16) unsigned char smem[];
     uint64_t* tab = (uint64_t*)smem;                                  // [GV_HMAX]
@@ -385,7 +385,7 @@ __global__ void __launch_bounds__(GV_THREADS, 3) bk_group_kernel(
         if (c < 2) continue;  // one g-mer: count 1, no pair, no repeat
         const uint64_t start = (uint64_t)m * a.n + lo;
         if (c > (uint32_t)GV_CAP) {
-            group_big<K>(keys, start, c, sb, N, Cm, so, sc, s_w, s_base, n_t, n_g);
+            group_big<K>(keys, start, c, sb, dstride, diag, so, sc, s_w, s_base, n_t, n_g);
             continue;
         }
         const uint32_t H = max(64u, (3u * c / 2u + 31u) & ~31u);
@@ -489,7 +489,7 @@ __global__ void __launch_bounds__(GV_THREADS, 3) bk_group_kernel(
             const uint32_t cc = (uint32_t)(v & ((1ull << CNT_BITS) - 1ull));
             const uint32_t x = (uint32_t)((v >> CNT_BITS) & 0x7fffffffull);
             if (cc >= 2)
-                atomicAdd((unsigned long long*)&Cm[(int64_t)x * N + x],
+                atomicAdd((unsigned long long*)&diag[(int64_t)x * dstride],
                           (unsigned long long)cc * cc - cc);
             const uint32_t g = (uint32_t)(v >> (CNT_BITS + 31));
             if (gl[g] == 0xffffffffu) continue;
@@ -551,8 +551,8 @@ cudaError_t launch_bucket_scatter(const BkArgs& a, void* out, bool k64, cudaStre
     return cudaGetLastError();
 }
 
-cudaError_t launch_bucket_group(const BkArgs& a, const void* keys, bool k64, int64_t N,
-                                int64_t* Cm, SegmentOut so, BkScratch sc,
+cudaError_t launch_bucket_group(const BkArgs& a, const void* keys, bool k64, int64_t dstride,
+                                int64_t* diag, SegmentOut so, BkScratch sc,
                                 unsigned long long* stats, int sm_count, cudaStream_t s) {
     cudaError_t e = cudaMemsetAsync(so.counts, 0, 2 * sizeof(uint32_t), s);
     if (e != cudaSuccess || a.n == 0 || a.nmask == 0) return e;
@@ -561,13 +561,13 @@ cudaError_t launch_bucket_group(const BkArgs& a, const void* keys, bool k64, int
     if (k64) {
         cudaFuncSetAttribute(bk_group_kernel<uint64_t>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GV_SMEM);
-        bk_group_kernel<uint64_t><<<grid, GV_THREADS, GV_SMEM, s>>>((const uint64_t*)keys, a, N,
-                                                                     Cm, so, sc, stats);
+        bk_group_kernel<uint64_t><<<grid, GV_THREADS, GV_SMEM, s>>>((const uint64_t*)keys, a, dstride,
+                                                                     diag, so, sc, stats);
     } else {
         cudaFuncSetAttribute(bk_group_kernel<uint32_t>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GV_SMEM);
-        bk_group_kernel<uint32_t><<<grid, GV_THREADS, GV_SMEM, s>>>((const uint32_t*)keys, a, N,
-                                                                     Cm, so, sc, stats);
+        bk_group_kernel<uint32_t><<<grid, GV_THREADS, GV_SMEM, s>>>((const uint32_t*)keys, a, dstride,
+                                                                     diag, so, sc, stats);
     }
     return cudaGetLastError();
 }

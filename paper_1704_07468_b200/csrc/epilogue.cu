@@ -169,9 +169,51 @@ __global__ void __launch_bounds__(256) epilogue_kernel(EpiArgs a,
     }
 }
 
-cudaError_t launch_epilogue(int64_t* C, int64_t N, int g, int k, int M, int64_t* Nm, int64_t* K,
-                            double* Knorm, int64_t* kdiag, int* flags, cudaStream_t s) {
-    EpiArgs a{C, N, g, k, M, Nm, K, Knorm, kdiag, flags};
+// ---------------------------------------------------------------- rectangular
+// Train x test block: rows X < NA (train), columns Y = NA + j
+// (test). C is [M+1][NA][NB] (every entry accumulated), Dg [M+1][N] the diagonals
+// C_m(X,X) of all N sequences; kdiag[X] = K(X,X) for all N (normalisation).
+__global__ void kdiag_rect_kernel(const int64_t* __restrict__ Dg, int64_t N, int g, int k, int M,
+                                  int64_t* kdiag, int* flags, const __grid_constant__ EpiCoef cf) {
+    int bad = 0;
+    for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < N;
+         x += (int64_t)gridDim.x * blockDim.x) {
+        int64_t prof[GMAX + 1];
+        for (int m = 0; m <= M; ++m) prof[m] = Dg[m * N + x];
+        kdiag[x] = entry<GMAX>(prof, cf, g, k, M, &bad);
+    }
+    if (bad) atomicOr(flags, bad);
+}
+
+template <int MM>
+__global__ void __launch_bounds__(256) epilogue_rect_kernel(
+    const int64_t* __restrict__ C, int64_t NA, int64_t NB, int g, int k, int M, int64_t* Nm,
+    int64_t* K, double* Knorm, const int64_t* __restrict__ kdiag, int* flags,
+    const __grid_constant__ EpiCoef cf) {
+    const int64_t cells = NA * NB;
+    int bad = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < cells;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        int64_t prof[MM + 1];
+#pragma unroll
+        for (int m = 0; m <= MM; ++m)
+            if (m <= M) prof[m] = C[m * cells + i];
+        const int64_t kv = entry<MM>(prof, cf, g, k, M, &bad);
+        if (Nm) {
+#pragma unroll
+            for (int m = 0; m <= MM; ++m)
+                if (m <= M) Nm[m * cells + i] = prof[m];
+        }
+        if (K) K[i] = kv;
+        if (Knorm) {
+            const int64_t x = i / NB, y = NA + (i - x * NB);
+            Knorm[i] = knorm(kv, kdiag[x], kdiag[y], false);
+        }
+    }
+    if (bad) atomicOr(flags, bad);
+}
+
+static EpiCoef make_coef(int g, int k, int M) {
     EpiCoef cf;
     memset(&cf, 0, sizeof cf);
     int64_t bt[GMAX + 1][GMAX + 1];  // Pascal's triangle
@@ -182,6 +224,34 @@ cudaError_t launch_epilogue(int64_t* C, int64_t N, int g, int k, int M, int64_t*
         for (int j = 0; j < m; ++j) cf.e9[m][j] = bt[g - j][m - j];
         cf.h[m] = (m <= g - k) ? bt[g - m][k] : 0;
     }
+    return cf;
+}
+
+cudaError_t launch_epilogue_rect(const int64_t* C, const int64_t* Dg, int64_t N, int64_t NA, int g,
+                                 int k, int M, int64_t* Nm, int64_t* K, double* Knorm,
+                                 int64_t* kdiag, int* flags, int sm_count, cudaStream_t s) {
+    const EpiCoef cf = make_coef(g, k, M);
+    int64_t blocks = (N + 255) / 256;
+    kdiag_rect_kernel<<<(int)(blocks < 1024 ? blocks : 1024), 256, 0, s>>>(Dg, N, g, k, M, kdiag,
+                                                                         flags, cf);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    const int64_t NB = N - NA;
+    if (NA * NB == 0) return cudaGetLastError();
+    const int grid = sm_count * 8;
+    if (M <= 7)
+        epilogue_rect_kernel<7><<<grid, 256, 0, s>>>(C, NA, NB, g, k, M, Nm, K, Knorm, kdiag,
+                                                     flags, cf);
+    else
+        epilogue_rect_kernel<GMAX><<<grid, 256, 0, s>>>(C, NA, NB, g, k, M, Nm, K, Knorm, kdiag,
+                                                        flags, cf);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_epilogue(int64_t* C, int64_t N, int g, int k, int M, int64_t* Nm, int64_t* K,
+                            double* Knorm, int64_t* kdiag, int* flags, cudaStream_t s) {
+    EpiArgs a{C, N, g, k, M, Nm, K, Knorm, kdiag, flags};
+    const EpiCoef cf = make_coef(g, k, M);
     int64_t blocks = (N + 255) / 256;
     kdiag_kernel<<<(int)(blocks < 1024 ? blocks : 1024), 256, 0, s>>>(a, cf);
     cudaError_t e = cudaGetLastError();

@@ -98,8 +98,10 @@ __device__ __forceinline__ void tc_commit_pair(uint64_t* b) {
 }
 
 struct Gram2Args {
-    int64_t* Cm;
-    int64_t N;
+    int64_t* Cm;        // [nrows][ncols]
+    int64_t nrows, ncols;
+    int64_t brow0;      // first row of D that is column 0 of the output (B operand)
+    int rect;           // 1: rectangular block, every entry; 0: Y > X only
     const uint32_t* fill;
     uint32_t cap;
     const int2* tiles;  // (row block of 256, col block of 512)
@@ -157,7 +159,7 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(G2_THREADS, 1)
                 const int2 tl = a.tiles[u / a.ksplit];
                 const int klo = (u % a.ksplit) * kper, khi = min(kblocks, klo + kper);
                 const int arow = tl.x * G2_TM + (int)rank * G2_M;
-                const int b0 = tl.y * G2_TN + (int)rank * 128;  // N half 0: my 128 rows
+                const int b0 = (int)a.brow0 + tl.y * G2_TN + (int)rank * 128;  // N half 0
                 for (int kb = klo; kb < khi; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
                     unsigned char* sa = smem + (size_t)stage * G2_STAGE_BYTES;
@@ -234,8 +236,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(G2_THREADS, 1)
                 for (int j2 = 0; j2 < G2_EC / 2; ++j2) {
                     const int ch = (j2 + lane) & (G2_EC / 2 - 1);
                     const int64_t y = y0 + c + 2 * ch;
-                    const uint64_t lo = (y > x) ? (uint64_t)v[2 * ch] : 0ull;
-                    const uint64_t hi = (y + 1 > x) ? (uint64_t)v[2 * ch + 1] : 0ull;
+                    const uint64_t lo = (a.rect || y > x) ? (uint64_t)v[2 * ch] : 0ull;
+                    const uint64_t hi = (a.rect || y + 1 > x) ? (uint64_t)v[2 * ch + 1] : 0ull;
                     *(ulonglong2*)(sb + row * (G2_EC * 8) + ch * 16) = make_ulonglong2(lo, hi);
                 }
                 if (a.tma_epilogue) {
@@ -253,8 +255,8 @@ __global__ void __cluster_dims__(2, 1, 1) __launch_bounds__(G2_THREADS, 1)
                         const int64_t xx = xrow0 + e / G2_EC;
                         const int64_t yy = y0 + c + e % G2_EC;
                         const uint64_t val = s64[e];
-                        if (val && xx < a.N && yy < a.N)
-                            atomicAdd((unsigned long long*)&a.Cm[xx * a.N + yy], val);
+                        if (val && xx < a.nrows && yy < a.ncols)
+                            atomicAdd((unsigned long long*)&a.Cm[xx * a.ncols + yy], val);
                     }
                 }
                 buf ^= 1;
@@ -284,18 +286,30 @@ std::vector<int2> gram2_tiles(int64_t n_pad) {
     return t;
 }
 
-cudaError_t gram_maps(uint8_t* D, int64_t n_pad, uint64_t ldd, int64_t* Cm, int64_t N, int ec,
-                      CUtensorMap* map, CUtensorMap* cmap, int* tma_epi);
+cudaError_t gram_maps(uint8_t* D, int64_t n_pad, uint64_t ldd, int64_t* Cm, int64_t nrows,
+                      int64_t ncols, int ec, CUtensorMap* map, CUtensorMap* cmap, int* tma_epi);
+
+// Rectangular block (rows [0, NA) x columns [NA, NA + NB) of D D^T): every pair tile.
+std::vector<int2> gram2_tiles_rect(int64_t NA, int64_t NB) {
+    std::vector<int2> t;
+    const int rb = (int)((NA + G2_TM - 1) / G2_TM), cb = (int)((NB + G2_TN - 1) / G2_TN);
+    for (int i = 0; i < rb; ++i)
+        for (int j = 0; j < cb; ++j) t.push_back(make_int2(i, j));
+    return t;
+}
 void launch_fill_reset(uint32_t* dense_fill, uint64_t ldd, uint64_t tile_macs,
                        unsigned long long* stats, cudaStream_t s);
 
 cudaError_t launch_gram2_flush(uint8_t* D, int64_t n_pad, uint64_t ldd, uint32_t* dense_fill,
                                int64_t* Cm, int64_t N, const int2* tiles, int ntiles,
-                               int sm_count, unsigned long long* stats, cudaStream_t s) {
+                               int sm_count, unsigned long long* stats, cudaStream_t s,
+                               int64_t NA) {
     if (n_pad % G2_TN != 0) return cudaErrorInvalidValue;
+    const bool rect = NA > 0;
+    const int64_t nrows = rect ? NA : N, ncols = rect ? N - NA : N;
     CUtensorMap map, cmap;
     int tma_epi = 0;
-    cudaError_t me = gram_maps(D, n_pad, ldd, Cm, N, G2_EC, &map, &cmap, &tma_epi);
+    cudaError_t me = gram_maps(D, n_pad, ldd, Cm, nrows, ncols, G2_EC, &map, &cmap, &tma_epi);
     if (me != cudaSuccess) return me;
     cudaFuncSetAttribute(gram2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)G2_SMEM);
     const int pairs = std::max(1, sm_count / 2);
@@ -303,7 +317,8 @@ cudaError_t launch_gram2_flush(uint8_t* D, int64_t n_pad, uint64_t ldd, uint32_t
     // wave keeps >= 90% of the workers busy (one wave of whole-K tiles streams
     // each K slab of D from DRAM once, shared through L2 by all tiles)
     const int ksplit = gram_ksplit(ntiles, pairs);
-    Gram2Args a{Cm, N, dense_fill, (uint32_t)ldd, tiles, ntiles, tma_epi, ksplit};
+    Gram2Args a{Cm, nrows, ncols, rect ? NA : 0, rect ? 1 : 0, dense_fill, (uint32_t)ldd, tiles,
+                ntiles, tma_epi, ksplit};
     const int units = ntiles * ksplit;
     const int grid = 2 * std::min(pairs, units);
     gram2_kernel<<<grid, G2_THREADS, G2_SMEM, s>>>(map, cmap, a);

@@ -467,8 +467,8 @@ std::vector<int2> gram_tiles(int64_t n_pad) {
 // Tensor maps of a flush: D (u8 slabs [ldd/128][n_pad][128], box 128 B x 128 rows,
 // 128B swizzle) and C_m (u64 view, box ec columns x 128 rows) for the TMA
 // reduce-add epilogue; *tma_epi = 0 when C_m rows are not 16-byte aligned.
-cudaError_t gram_maps(uint8_t* D, int64_t n_pad, uint64_t ldd, int64_t* Cm, int64_t N, int ec,
-                      CUtensorMap* map, CUtensorMap* cmap, int* tma_epi) {
+cudaError_t gram_maps(uint8_t* D, int64_t n_pad, uint64_t ldd, int64_t* Cm, int64_t nrows,
+                      int64_t ncols, int ec, CUtensorMap* map, CUtensorMap* cmap, int* tma_epi) {
     EncodeTiledFn enc = get_encode();
     if (!enc) return cudaErrorNotSupported;
     cuuint64_t dims[3] = {(cuuint64_t)GT_KB, (cuuint64_t)n_pad, ldd / GT_KB};
@@ -480,9 +480,9 @@ cudaError_t gram_maps(uint8_t* D, int64_t n_pad, uint64_t ldd, int64_t* Cm, int6
                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) return cudaErrorInvalidValue;
     memset(cmap, 0, sizeof *cmap);
-    *tma_epi = (N % 2 == 0) && (((uintptr_t)Cm & 15) == 0);
-    cuuint64_t cdims[2] = {(cuuint64_t)N, (cuuint64_t)N};
-    cuuint64_t cstr[1] = {(cuuint64_t)N * 8};
+    *tma_epi = (ncols % 2 == 0) && (((uintptr_t)Cm & 15) == 0);
+    cuuint64_t cdims[2] = {(cuuint64_t)ncols, (cuuint64_t)nrows};
+    cuuint64_t cstr[1] = {(cuuint64_t)ncols * 8};
     cuuint32_t cbox[2] = {(cuuint32_t)ec, GT_M};
     if (*tma_epi) {
         r = enc(cmap, CU_TENSOR_MAP_DATA_TYPE_UINT64, 2, (void*)Cm, cdims, cstr, cbox, estr,
@@ -503,7 +503,7 @@ cudaError_t launch_gram_flush(uint8_t* D, int64_t n_pad, uint64_t ldd, uint32_t*
                               int sm_count, unsigned long long* stats, cudaStream_t s) {
     CUtensorMap map, cmap;
     int tma_epi = 0;
-    cudaError_t me = gram_maps(D, n_pad, ldd, Cm, N, GT_EC, &map, &cmap, &tma_epi);
+    cudaError_t me = gram_maps(D, n_pad, ldd, Cm, N, N, GT_EC, &map, &cmap, &tma_epi);
     if (me != cudaSuccess) return me;
     cudaFuncSetAttribute(gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GT_SMEM);
     // split K only as far as it fills the machine: the smallest split whose last

@@ -193,8 +193,8 @@ cudaError_t launch_windows(const CorpusView& cv, int g, int bits, uint64_t* win,
 int bk_masks_per_cta(uint32_t nb);
 cudaError_t launch_bucket_count(const BkArgs& a, bool k64, cudaStream_t s);
 cudaError_t launch_bucket_scatter(const BkArgs& a, void* out, bool k64, cudaStream_t s);
-cudaError_t launch_bucket_group(const BkArgs& a, const void* keys, bool k64, int64_t N,
-                                int64_t* Cm, SegmentOut so, BkScratch sc,
+cudaError_t launch_bucket_group(const BkArgs& a, const void* keys, bool k64, int64_t dstride,
+                                int64_t* diag, SegmentOut so, BkScratch sc,
                                 unsigned long long* stats, int sm_count, cudaStream_t s);
 
 // ---- launchers (each returns cudaGetLastError()) ----
@@ -212,8 +212,9 @@ cudaError_t launch_onesweep(const uint64_t* in, uint64_t* out, uint64_t n, int n
 cudaError_t launch_radix_chunked(const void* in, void* out, bool k64, uint64_t n, int nseg,
                                  int shift, uint32_t* hist, int target_ctas, cudaStream_t s);
 // counters: 2 u32 (triples, groups) reserved per tile; zeroed by the launcher.
-cudaError_t launch_segment(const void* keys, bool k64, uint64_t n, int nseg, int sb, int64_t N,
-                           int64_t* Cm, uint32_t* counters, SegmentOut so,
+// diag[X * dstride] receives the within-sequence repeat term of C_m(X,X)
+cudaError_t launch_segment(const void* keys, bool k64, uint64_t n, int nseg, int sb,
+                           int64_t dstride, int64_t* diag, uint32_t* counters, SegmentOut so,
                            unsigned long long* stats, cudaStream_t s);
 // Light pair updates; a group with >= heavy_min sequences (and counts <= 255)
 // instead claims column c = atomicAdd(dense_fill) (< ldd) of the dense count
@@ -232,7 +233,10 @@ struct LightBins {
 cudaError_t launch_light(SegmentOut so, uint64_t max_groups, int64_t heavy_min, int64_t N,
                          uint32_t* acc, uint2* heavy_list, uint64_t ldd,
                          uint32_t* dense_fill, LightBins bins, uint32_t flat_max,
-                         unsigned long long* stats, int sm_count, cudaStream_t s);
+                         int64_t NA, unsigned long long* stats, int sm_count, cudaStream_t s);
+// rectangular accumulator (NA x NB, row-major) -> C_m (NA x NB), zeroed
+cudaError_t launch_light_flush_rect(uint32_t* acc, uint64_t cells, int64_t* Cm, int sm_count,
+                                    cudaStream_t s);
 // Fill the D slabs of the columns claimed by this batch ([prev, fill) with
 // prev = dense_fill[1], a multiple of 128) from the batch's triples, in shared
 // memory, with full-line stores; then round dense_fill[0] up to a multiple of 128
@@ -268,12 +272,21 @@ cudaError_t launch_gram_flush(uint8_t* D, int64_t n_pad, uint64_t ldd, uint32_t*
                               int64_t* Cm, int64_t N, const int2* tiles, int ntiles,
                               int sm_count, unsigned long long* stats, cudaStream_t s);
 // CTA-pair variant (gram2.cu): 256 x 512 pair tiles, n_pad a multiple of 512.
+// NA > 0: rectangular block C_m[X][Y - NA] += (D D^T)[X][Y], X < NA <= Y (C_m is NA x
+// (N - NA)), over the tiles of gram2_tiles_rect.
 std::vector<int2> gram2_tiles(int64_t n_pad);
+std::vector<int2> gram2_tiles_rect(int64_t NA, int64_t NB);
 cudaError_t launch_gram2_flush(uint8_t* D, int64_t n_pad, uint64_t ldd, uint32_t* dense_fill,
                                int64_t* Cm, int64_t N, const int2* tiles, int ntiles,
-                               int sm_count, unsigned long long* stats, cudaStream_t s);
-cudaError_t launch_diag_closed_form(const int64_t* gofs, int64_t N, int64_t nmask, int64_t* Cm,
-                                    cudaStream_t s);
+                               int sm_count, unsigned long long* stats, cudaStream_t s,
+                               int64_t NA = 0);
+cudaError_t launch_diag_closed_form(const int64_t* gofs, int64_t N, int64_t nmask, int64_t* diag,
+                                    int64_t dstride, cudaStream_t s);
+// Rectangular epilogue: C [M+1][NA][N-NA], Dg [M+1][N] diagonals -> Nm, K, Knorm
+// [.][NA][N-NA] and kdiag[N] = K(X,X).
+cudaError_t launch_epilogue_rect(const int64_t* C, const int64_t* Dg, int64_t N, int64_t NA, int g,
+                                 int k, int M, int64_t* Nm, int64_t* K, double* Knorm,
+                                 int64_t* kdiag, int* flags, int sm_count, cudaStream_t s);
 cudaError_t launch_epilogue(int64_t* C, int64_t N, int g, int k, int M, int64_t* Nm, int64_t* K,
                             double* Knorm, int64_t* kdiag, int* flags, cudaStream_t s);
 

@@ -21,6 +21,21 @@ __device__ __forceinline__ uint64_t tri_index(uint32_t x, uint32_t y, int64_t N)
     return (uint64_t)x * (uint64_t)(N - 1) - (uint64_t)x * (x - 1) / 2 + (y - x - 1);
 }
 
+// Accumulator cell of the unordered pair {x, y} (x != y): the strictly-upper
+// packed triangle (full mode, NA = 0), or, in rectangular mode (NA > 0: sequences
+// [0, NA) are the rows, [NA, N) the columns), row-major NA x (N - NA) for a
+// cross pair; a pair inside one set is not a cell (*ok = false).
+__device__ __forceinline__ uint64_t pair_cell(uint32_t x, uint32_t y, int64_t N, int64_t NA,
+                                              bool* ok) {
+    const uint32_t lo = min(x, y), hi = max(x, y);
+    if (NA == 0) {
+        *ok = true;
+        return tri_index(lo, hi, N);
+    }
+    *ok = (int64_t)lo < NA && (int64_t)hi >= NA;
+    return (uint64_t)lo * (uint64_t)(N - NA) + (uint64_t)((int64_t)hi - NA);
+}
+
 // One pair update acc[idx] += val, called by all 32 lanes (valid marks real
 // updates). With binning on (large N: the accumulator is far bigger than L2),
 // small updates become 4-byte records (cell offset << 4 | val) appended to the
@@ -75,7 +90,7 @@ __global__ void __launch_bounds__(256) light_kernel(SegmentOut so, int64_t heavy
                                                     uint32_t* acc, uint2* heavy_list,
                                                     uint64_t ldd, uint32_t* dense_fill,
                                                     LightBins bn, uint32_t flat_max,
-                                                    unsigned long long* stats) {
+                                                    int64_t NA, unsigned long long* stats) {
     // triangle table: pairs (a < b < 32) ordered by b, so the first n(n-1)/2
     // entries are exactly the pairs of an n-triple chunk
     __shared__ uint16_t s_tri[496];
@@ -126,14 +141,15 @@ __global__ void __launch_bounds__(256) light_kernel(SegmentOut so, int64_t heavy
             const uint32_t sj = __shfl_sync(0xffffffffu, my_start, j);
             uint64_t idx = 0;
             uint32_t val = 0;
+            bool ok = false;
             if (q < Ptot) {
                 const uint32_t ab = s_tri[q - ej];
                 const uint32_t ta = sj + (ab & 31), tb = sj + (ab >> 5);
                 const uint32_t xa = so.tseq[ta] & 0x7fffffffu, xb = so.tseq[tb] & 0x7fffffffu;
-                idx = tri_index(min(xa, xb), max(xa, xb), N);
+                idx = pair_cell(xa, xb, N, NA, &ok);
                 val = so.tcnt[ta] * so.tcnt[tb];
             }
-            pair_add(acc, bn, q < Ptot, idx, val);
+            pair_add(acc, bn, ok, idx, val);
         }
 
         // (2) the other groups one by one (big light groups and heavy candidates)
@@ -193,8 +209,9 @@ __global__ void __launch_bounds__(256) light_kernel(SegmentOut so, int64_t heavy
                     const uint32_t ca = __shfl_sync(0xffffffffu, cA, a);
                     const uint32_t xb = __shfl_sync(0xffffffffu, xA, b);
                     const uint32_t cb = __shfl_sync(0xffffffffu, cA, b);
-                    pair_add(acc, bn, q < P, q < P ? tri_index(min(xa, xb), max(xa, xb), N) : 0,
-                             ca * cb);
+                    bool ok = false;
+                    const uint64_t idx = q < P ? pair_cell(xa, xb, N, NA, &ok) : 0;
+                    pair_add(acc, bn, ok && q < P, idx, ca * cb);
                 }
                 for (uint32_t B = A + 32; B < b0; B += 32) {
                     const uint32_t ib = B + lane;
@@ -204,8 +221,9 @@ __global__ void __launch_bounds__(256) light_kernel(SegmentOut so, int64_t heavy
                     for (uint32_t a = 0; a < na; ++a) {
                         const uint32_t xa = __shfl_sync(0xffffffffu, xA, a);
                         const uint32_t ca = __shfl_sync(0xffffffffu, cA, a);
-                        pair_add(acc, bn, vb, vb ? tri_index(min(xa, xB), max(xa, xB), N) : 0,
-                                 ca * cB);
+                        bool ok = false;
+                        const uint64_t idx = vb ? pair_cell(xa, xB, N, NA, &ok) : 0;
+                        pair_add(acc, bn, ok && vb, idx, ca * cB);
                     }
                 }
             }
@@ -218,13 +236,13 @@ __global__ void __launch_bounds__(256) light_kernel(SegmentOut so, int64_t heavy
 cudaError_t launch_light(SegmentOut so, uint64_t max_groups, int64_t heavy_min, int64_t N,
                          uint32_t* acc, uint2* heavy_list, uint64_t ldd,
                          uint32_t* dense_fill, LightBins bins, uint32_t flat_max,
-                         unsigned long long* stats, int sm_count, cudaStream_t s) {
+                         int64_t NA, unsigned long long* stats, int sm_count, cudaStream_t s) {
     if (max_groups == 0) return cudaGetLastError();
     uint64_t blocks = (max_groups + 255) / 256;  // 8 warps x 32 groups per block-round
     uint64_t cap = (uint64_t)sm_count * 8;
     if (blocks > cap) blocks = cap;
     light_kernel<<<(unsigned)blocks, 256, 0, s>>>(so, heavy_min, N, acc, heavy_list, ldd,
-                                                  dense_fill, bins, flat_max, stats);
+                                                  dense_fill, bins, flat_max, NA, stats);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess || bins.nb == 0) return e;
     return launch_apply_bins(acc, bins, sm_count, s);
@@ -246,6 +264,26 @@ __global__ void light_flush_kernel(uint32_t* __restrict__ acc, int64_t N, int64_
     }
 }
 
+// Rectangular mode: C_m[X][Y - NA] += acc[X][Y - NA] (row-major NA x NB), zeroed.
+__global__ void light_flush_rect_kernel(uint32_t* __restrict__ acc, uint64_t cells,
+                                        int64_t* __restrict__ Cm) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < cells;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t v = acc[i];
+        if (v) {
+            Cm[i] += v;
+            acc[i] = 0u;
+        }
+    }
+}
+
+cudaError_t launch_light_flush_rect(uint32_t* acc, uint64_t cells, int64_t* Cm, int sm_count,
+                                    cudaStream_t s) {
+    if (cells == 0) return cudaGetLastError();
+    light_flush_rect_kernel<<<sm_count * 8, 256, 0, s>>>(acc, cells, Cm);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_light_flush(uint32_t* acc, int64_t N, int64_t* Cm, int sm_count,
                                cudaStream_t s) {
     if (N < 2) return cudaGetLastError();
@@ -255,19 +293,19 @@ cudaError_t launch_light_flush(uint32_t* acc, int64_t N, int64_t* Cm, int sm_cou
 }
 
 // Closed-form diagonal part: every g-mer of X matches itself under every mask, so
-// each of the nmask masks adds n_X = gofs[X+1]-gofs[X] to C_m(X,X).
+// each of the nmask masks adds n_X = gofs[X+1]-gofs[X] to C_m(X,X) = diag[X*dstride].
 __global__ void diag_closed_form_kernel(const int64_t* __restrict__ gofs, int64_t N, int64_t nmask,
-                                        int64_t* Cm) {
+                                        int64_t* diag, int64_t dstride) {
     for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < N;
          x += (int64_t)gridDim.x * blockDim.x)
-        Cm[x * N + x] += nmask * (gofs[x + 1] - gofs[x]);
+        diag[x * dstride] += nmask * (gofs[x + 1] - gofs[x]);
 }
 
-cudaError_t launch_diag_closed_form(const int64_t* gofs, int64_t N, int64_t nmask, int64_t* Cm,
-                                    cudaStream_t s) {
+cudaError_t launch_diag_closed_form(const int64_t* gofs, int64_t N, int64_t nmask, int64_t* diag,
+                                    int64_t dstride, cudaStream_t s) {
     int64_t blocks = (N + 255) / 256;
     diag_closed_form_kernel<<<(int)(blocks < 1024 ? blocks : 1024), 256, 0, s>>>(gofs, N, nmask,
-                                                                                 Cm);
+                                                                                 diag, dstride);
     return cudaGetLastError();
 }
 

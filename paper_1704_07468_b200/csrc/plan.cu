@@ -92,11 +92,12 @@ struct gakco_plan {
     std::vector<std::array<uint8_t, GMAX>> mask_kept;
     std::vector<int> key_bits;  // per level
 
-    DevBuf codes, off, gofs, gmseq, keysA, keysB, hist, status, ctr, tseq, tcnt, gstart, gend,
+    DevBuf Dgscr, Kdscr, codes, off, gofs, gmseq, keysA, keysB, hist, status, ctr, tseq, tcnt, gstart, gend,
         counts, kept, stats, flags, kdiag, Cscr, Nmscr, Kscr, Knscr, heavy, hcount, dense, tiles,
         lightacc, binrec, bincnt, win, bkH, bktot, bkbase, bkdesc, bktab, bktcnt, bkgs, bkocc;
     int64_t tiles_npad = -1;
     int tiles_pair = -1;
+    int64_t tiles_na = -1;
     uint64_t dense_ldd = 0;
     int ntiles = 0;
     uint32_t epoch = 1;
@@ -249,7 +250,7 @@ extern "C" gakco_status gakco_create(int sigma, int g, int k, int M, int device,
 extern "C" void gakco_destroy(gakco_plan* p) {
     if (!p) return;
     DeviceGuard dg(p->device);
-    DevBuf* bufs[] = {&p->codes, &p->off,   &p->gofs,  &p->gmseq,  &p->keysA, &p->keysB,
+    DevBuf* bufs[] = {&p->Dgscr, &p->Kdscr, &p->codes, &p->off,   &p->gofs,  &p->gmseq,  &p->keysA, &p->keysB,
                       &p->hist,  &p->status, &p->ctr,  &p->tseq,   &p->tcnt,  &p->gstart,
                       &p->gend,  &p->counts, &p->kept, &p->stats,  &p->flags, &p->kdiag,
                       &p->Cscr,  &p->Nmscr, &p->Kscr,  &p->Knscr, &p->heavy, &p->hcount,
@@ -319,7 +320,8 @@ extern "C" int64_t gakco_num_masks(const gakco_plan* p, int shard_only) {
 // single N x N matrix C (used by the K-only path, K = C_{g-k}).
 static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const int64_t* offsets,
                                     int64_t N, int64_t* C, cudaStream_t s, int rank, int world,
-                                    int only_level = -1) {
+                                    int only_level = -1, int64_t NA = 0,
+                                    int64_t* Dg = nullptr) {
 #define CK(x)                                          \
     do {                                               \
         cudaError_t e_ = (x);                          \
@@ -441,7 +443,11 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
     // updates on the light path and ~N_pad^2/2 u8 MACs on the Gram; with the
     // measured rates (~1.1e11 updates/s, ~1.5e15 MAC/s) they break even near
     // s = 0.0085 N_pad.
-    const int64_t n_pad = p->gram_pair ? (N + 511) / 512 * 512 : (N + 255) / 256 * 256;
+    // rectangular mode (NA > 0): rows [0, NA) x columns [NA, N) only; C is
+    // [levels][NA][N - NA], the diagonals C_m(X,X) go to Dg [levels][N]
+    const bool rect = NA > 0;
+    const bool gpair = p->gram_pair || rect;
+    const int64_t n_pad = gpair ? (N + 511) / 512 * 512 : (N + 255) / 256 * 256;
     int64_t heavy_min = p->heavy_min;
     if (heavy_min == 0) heavy_min = std::max<int64_t>(16, (int64_t)(0.012 * (double)n_pad + 0.999));
     const bool heavy_on = heavy_min < (int64_t)1 << 40 && N >= 2;
@@ -534,15 +540,18 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
         rcap = std::max<uint64_t>(128, (rcap + 127) / 128 * 128);
         CK(p->ensure(p->dense, (size_t)n_pad * rcap, s));
         CK(p->ensure(p->heavy, rcap * sizeof(uint2), s));
-        if (p->tiles_npad != n_pad || p->tiles_pair != p->gram_pair) {
-            std::vector<int2> t = p->gram_pair ? gram2_tiles(n_pad) : gram_tiles(n_pad);
+        const int tkey = rect ? 2 : (gpair ? 1 : 0);
+        if (p->tiles_npad != n_pad || p->tiles_pair != tkey || (rect && p->tiles_na != NA)) {
+            std::vector<int2> t = rect ? gram2_tiles_rect(NA, N - NA)
+                                       : (gpair ? gram2_tiles(n_pad) : gram_tiles(n_pad));
             CK(p->ensure(p->tiles, t.size() * sizeof(int2), s));
             CK(cudaMemcpyAsync(p->tiles.p, t.data(), t.size() * sizeof(int2),
                                cudaMemcpyHostToDevice, s));
             CK(cudaStreamSynchronize(s));
             p->ntiles = (int)t.size();
             p->tiles_npad = n_pad;
-            p->tiles_pair = p->gram_pair;
+            p->tiles_pair = tkey;
+            p->tiles_na = NA;
         }
     }
     CorpusView cv{(const uint8_t*)p->codes.p, (const int64_t*)p->off.p, (const int64_t*)p->gofs.p,
@@ -556,9 +565,15 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
         LK(launch_windows(cv, g, bits, (uint64_t*)p->win.p, p->sm_count, s));
         p->stage_end(s, S_ENCODE, a0);
     }
-    const size_t nn = (size_t)N * N;
+    const size_t nn = rect ? (size_t)NA * (size_t)(N - NA) : (size_t)N * N;
     auto level_ptr = [&](int m) -> int64_t* {
         return only_level >= 0 ? C : C + (size_t)m * nn;
+    };
+    // C_m(X,X) lives at diag_ptr(m)[X * dstride]
+    const int64_t dstride = rect ? 1 : N + 1;
+    auto diag_ptr = [&](int m) -> int64_t* {
+        if (!rect) return level_ptr(m);
+        return only_level >= 0 ? Dg : Dg + (size_t)m * N;
     };
 
     // Heavy groups of consecutive batches of one level accumulate as columns of D;
@@ -573,10 +588,10 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
         cudaEvent_t ah = nullptr;
         p->stage_begin(s, &ah);
         p->launches += 1;  // + fill_reset
-        if (p->gram_pair)
+        if (gpair)
             LK(launch_gram2_flush((uint8_t*)p->dense.p, n_pad, rcap, (uint32_t*)p->hcount.p,
                                   level_ptr(dense_m), N, (const int2*)p->tiles.p, p->ntiles,
-                                  p->sm_count, stats, s));
+                                  p->sm_count, stats, s, NA));
         else
             LK(launch_gram_flush((uint8_t*)p->dense.p, n_pad, rcap, (uint32_t*)p->hcount.p,
                                  level_ptr(dense_m), N, (const int2*)p->tiles.p, p->ntiles,
@@ -588,7 +603,8 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
     };
     // Light updates accumulate in a u32 packed strictly-upper triangle, added into
     // C_m at a level change or before masks * n_max^2 could reach 2^32.
-    const uint64_t ntri = (uint64_t)N * (uint64_t)(N - 1) / 2;
+    const uint64_t ntri =
+        rect ? (uint64_t)NA * (uint64_t)(N - NA) : (uint64_t)N * (uint64_t)(N - 1) / 2;
     CK(p->ensure(p->lightacc, ntri * 4 + 16, s, /*zero=*/true));
     // light-update binning when the accumulator is far larger than L2 (Scale:
     // 800 MB): records per 64 MB block, applied block by block (light.cu)
@@ -597,7 +613,7 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
         uint64_t bc = 0;
         // auto mode leaves binning OFF: measured 2.3x slower than direct atomics on
         // Scale (match.any + record traffic cost more than the DRAM RMW saved)
-        if (p->light_bins > 0) bc = (uint64_t)p->light_bins;  // forced (tests, ablation)
+        if (p->light_bins > 0 && !rect) bc = (uint64_t)p->light_bins;  // forced (tests, ablation)
         if (bc > 0 && ntri > 0) {
             bc = std::min<uint64_t>(bc, (1ull << 28) - 1);  // offset field: 28 bits
             const int nb = (int)((ntri + bc - 1) / bc);
@@ -619,8 +635,12 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
         if (light_m < 0 || light_masks == 0) return GAKCO_OK;
         cudaEvent_t al = nullptr;
         p->stage_begin(s, &al);
-        LK(launch_light_flush((uint32_t*)p->lightacc.p, N, level_ptr(light_m), p->sm_count,
-                              s));
+        if (rect)
+            LK(launch_light_flush_rect((uint32_t*)p->lightacc.p, ntri, level_ptr(light_m),
+                                       p->sm_count, s));
+        else
+            LK(launch_light_flush((uint32_t*)p->lightacc.p, N, level_ptr(light_m), p->sm_count,
+                                  s));
         p->stage_end(s, S_LIGHT, al);
         light_masks = 0;
         return GAKCO_OK;
@@ -635,6 +655,7 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
         const int kb = p->key_bits[m];
         const int npass = (kb + RADIX_BITS - 1) / RADIX_BITS;
         int64_t* Cm = level_ptr(m);
+        int64_t* Dm = diag_ptr(m);  // C_m(X,X) at Dm[X * dstride]
         cudaEvent_t a = nullptr;
         if (gram_ok && n > 0) {
             const uint64_t bnd = (uint64_t)nmask * n / (uint64_t)heavy_min + 128;
@@ -692,7 +713,8 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
             p->stage_begin(s, &a);
             BkScratch bs{(uint64_t*)p->bktab.p, (uint32_t*)p->bktcnt.p, (uint32_t*)p->bkgs.p,
                          (uint32_t*)p->bkocc.p};
-            LK(launch_bucket_group(ba, p->keysA.p, k64, N, Cm, so, bs, stats, p->sm_count, s));
+            LK(launch_bucket_group(ba, p->keysA.p, k64, dstride, Dm, so, bs, stats, p->sm_count,
+                                   s));
             p->stage_end(s, S_SEGMENT, a);
         } else if (n > 0) {
             p->stage_begin(s, &a);
@@ -731,7 +753,7 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
             p->stage_end(s, S_SORT, a);
 
             p->stage_begin(s, &a);
-            LK(launch_segment(in, k64, n, nmask, sb, N, Cm, so.counts, so, stats, s));
+            LK(launch_segment(in, k64, n, nmask, sb, dstride, Dm, so.counts, so, stats, s));
             p->stage_end(s, S_SEGMENT, a);
 
         }
@@ -739,7 +761,7 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
             p->stage_begin(s, &a);
             LK(launch_light(so, n * nmask / 2 + 1, light_limit, N, (uint32_t*)p->lightacc.p,
                             (uint2*)p->heavy.p, rcap, (uint32_t*)p->hcount.p, bins,
-                            (uint32_t)p->light_flat, stats, p->sm_count, s));
+                            (uint32_t)p->light_flat, NA, stats, p->sm_count, s));
             p->stage_end(s, S_LIGHT, a);
             if (gram_ok) {
                 p->stage_begin(s, &a);
@@ -750,7 +772,7 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
                 p->stage_end(s, S_DENSE, a);
             }
         }
-        LK(launch_diag_closed_form((const int64_t*)p->gofs.p, N, nmask, Cm, s));
+        LK(launch_diag_closed_form((const int64_t*)p->gofs.p, N, nmask, Dm, dstride, s));
         pos = end;
     }
     {
@@ -908,6 +930,89 @@ extern "C" gakco_status gakco_kernel_k(gakco_plan* p, const uint8_t* codes,
     gakco_status st = accumulate_impl(p, codes, offsets, N, dC, s, 0, 1, p->g - p->k);
     if (st != GAKCO_OK) return st;
     return finalize_impl(p, dC, N, nullptr, K, Knorm, s, true, /*k_only=*/true);
+}
+
+// Rectangular train x test block: sequences [0, NA) are the
+// training set X_i, [NA, N) the test set; outputs are the NA x (N - NA) block of
+// C_m / N_m / K / Knorm of the concatenated corpus (the paper concatenates
+// train and test into one N x N problem), without the train x train and test x
+// test pair updates, plus K(X,X) of all N sequences (normalisation; Eq. 1).
+extern "C" gakco_status gakco_kernel_rect(gakco_plan* p, const uint8_t* codes,
+                                          const int64_t* offsets, int64_t N, int64_t NA,
+                                          int64_t* C, int64_t* Nm, int64_t* K, double* Knorm,
+                                          int64_t* Kdiag, void* stream) {
+#define CK(x)                                               \
+    do {                                                    \
+        cudaError_t e_ = (x);                               \
+        if (e_ != cudaSuccess) return p->cuda_fail(e_, #x); \
+    } while (0)
+    if (!p) return GAKCO_E_ARG;
+    if (N < 2 || N >= ((int64_t)1 << 31)) return p->fail(GAKCO_E_ARG, "N must be in [2, 2^31)");
+    if (NA < 1 || NA >= N) return p->fail(GAKCO_E_ARG, "NA must be in [1, N-1]");
+    DeviceGuard dg(p->device);
+    cudaStream_t s = (cudaStream_t)stream;
+    const int64_t NB = N - NA;
+    const int M = p->M;
+    const size_t cells = (size_t)NA * (size_t)NB;
+    const size_t cbytes = (size_t)(M + 1) * cells * 8;
+    int64_t* dC = C;
+    const bool hC = C && !is_device_ptr(C);
+    if (!C || hC) {
+        CK(p->ensure(p->Cscr, cbytes, s));
+        dC = (int64_t*)p->Cscr.p;
+    }
+    CK(p->ensure(p->Dgscr, (size_t)(M + 1) * N * 8, s));
+    int64_t* Dg = (int64_t*)p->Dgscr.p;
+    CK(cudaMemsetAsync(dC, 0, cbytes, s));
+    CK(cudaMemsetAsync(Dg, 0, (size_t)(M + 1) * N * 8, s));
+    gakco_status st = accumulate_impl(p, codes, offsets, N, dC, s, 0, 1, -1, NA, Dg);
+    if (st != GAKCO_OK) return st;
+    // outputs: device pointers written in place, host ones through plan scratch
+    int64_t* dNm = Nm;
+    int64_t* dK = K;
+    double* dKn = Knorm;
+    int64_t* dKd = Kdiag;
+    const bool hNm = Nm && !is_device_ptr(Nm), hK = K && !is_device_ptr(K),
+               hKn = Knorm && !is_device_ptr(Knorm), hKd = Kdiag && !is_device_ptr(Kdiag);
+    if (hNm) {
+        CK(p->ensure(p->Nmscr, cbytes, s));
+        dNm = (int64_t*)p->Nmscr.p;
+    }
+    if (hK) {
+        CK(p->ensure(p->Kscr, cells * 8, s));
+        dK = (int64_t*)p->Kscr.p;
+    }
+    if (hKn) {
+        CK(p->ensure(p->Knscr, cells * 8, s));
+        dKn = (double*)p->Knscr.p;
+    }
+    if (!Kdiag || hKd) {
+        CK(p->ensure(p->Kdscr, N * 8, s));
+        dKd = (int64_t*)p->Kdscr.p;
+    }
+    CK(p->ensure(p->flags, 64, s, /*zero=*/true));
+    CK(cudaMemsetAsync(p->flags.p, 0, sizeof(int), s));
+    cudaEvent_t a = nullptr;
+    p->after_accumulate = false;
+    p->stage_begin(s, &a);
+    ++p->launches;
+    CK(launch_epilogue_rect(dC, Dg, N, NA, p->g, p->k, M, dNm, dK, dKn, dKd, (int*)p->flags.p,
+                            p->sm_count, s));
+    p->stage_end(s, S_EPILOGUE, a);
+    if (hC) CK(cudaMemcpyAsync(C, dC, cbytes, cudaMemcpyDeviceToHost, s));
+    if (hNm) CK(cudaMemcpyAsync(Nm, dNm, cbytes, cudaMemcpyDeviceToHost, s));
+    if (hK) CK(cudaMemcpyAsync(K, dK, cells * 8, cudaMemcpyDeviceToHost, s));
+    if (hKn) CK(cudaMemcpyAsync(Knorm, dKn, cells * 8, cudaMemcpyDeviceToHost, s));
+    if (hKd) CK(cudaMemcpyAsync(Kdiag, dKd, N * 8, cudaMemcpyDeviceToHost, s));
+    int fl[2] = {0, 0};
+    CK(cudaMemcpyAsync(fl, p->flags.p, 2 * sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemsetAsync((int*)p->flags.p + 1, 0, sizeof(int), s));
+    CK(cudaStreamSynchronize(s));
+    if (fl[1] & EF_BAD_SYMBOL) return p->fail(GAKCO_E_SYMBOL, "a code is >= sigma");
+    if (fl[0] & EF_NEGATIVE_N) return p->fail(GAKCO_E_INTERNAL, "negative N_m after Eq. 9");
+    if (fl[0] & EF_K_MISMATCH) return p->fail(GAKCO_E_INTERNAL, "K != C_{g-k}");
+    return GAKCO_OK;
+#undef CK
 }
 
 extern "C" gakco_status gakco_get_stats(gakco_plan* p, gakco_stats* out) {

@@ -26,8 +26,8 @@ namespace gk {
 
 template <typename K>
 __global__ void __launch_bounds__(SEG_THREADS) segment_kernel(
-    const K* __restrict__ keys, uint64_t n, uint64_t total, int sb, int64_t N,
-    int64_t* Cm, uint32_t* counters, SegmentOut so, unsigned long long* stats) {
+    const K* __restrict__ keys, uint64_t n, uint64_t total, int sb, int64_t dstride,
+    int64_t* diag, uint32_t* counters, SegmentOut so, unsigned long long* stats) {
     __shared__ uint32_t s_w[8];
     __shared__ uint32_t s_gpos[SEG_TILE];
     __shared__ uint32_t s_first_gh, s_base_t, s_base_g, s_tail;
@@ -101,7 +101,7 @@ __global__ void __launch_bounds__(SEG_THREADS) segment_kernel(
         cnt[i] = c;
         if (c >= 2) {
             const int64_t x = (int64_t)(c0 & seqmask);
-            atomicAdd((unsigned long long*)&Cm[x * N + x], (unsigned long long)c * c - c);
+            atomicAdd((unsigned long long*)&diag[x * dstride], (unsigned long long)c * c - c);
         }
         th_bits |= 1u << i;
         if (!gh || (j < seg_end && (nk >> sb) == (c0 >> sb))) multi_bits |= 1u << i;
@@ -208,8 +208,8 @@ __global__ void __launch_bounds__(SEG_THREADS) segment_kernel(
     }
 }
 
-cudaError_t launch_segment(const void* keys, bool k64, uint64_t n, int nseg, int sb, int64_t N,
-                           int64_t* Cm, uint32_t* counters, SegmentOut so,
+cudaError_t launch_segment(const void* keys, bool k64, uint64_t n, int nseg, int sb,
+                           int64_t dstride, int64_t* diag, uint32_t* counters, SegmentOut so,
                            unsigned long long* stats, cudaStream_t s) {
     cudaError_t e = cudaMemsetAsync(counters, 0, 2 * sizeof(uint32_t), s);
     uint64_t total = n * (uint64_t)nseg;
@@ -217,10 +217,10 @@ cudaError_t launch_segment(const void* keys, bool k64, uint64_t n, int nseg, int
     uint64_t tiles = (total + SEG_TILE - 1) / SEG_TILE;
     if (k64)
         segment_kernel<uint64_t><<<(unsigned)tiles, SEG_THREADS, 0, s>>>(
-            (const uint64_t*)keys, n, total, sb, N, Cm, counters, so, stats);
+            (const uint64_t*)keys, n, total, sb, dstride, diag, counters, so, stats);
     else
         segment_kernel<uint32_t><<<(unsigned)tiles, SEG_THREADS, 0, s>>>(
-            (const uint32_t*)keys, n, total, sb, N, Cm, counters, so, stats);
+            (const uint32_t*)keys, n, total, sb, dstride, diag, counters, so, stats);
     return cudaGetLastError();
 }
 

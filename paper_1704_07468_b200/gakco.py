@@ -37,7 +37,8 @@ GAKCO_OPT_GRAM_PAIR = 7
 GAKCO_OPT_LIGHT_FLAT = 8
 
 EXPORTS = ("gakco_create", "gakco_set_shard", "gakco_set_option", "gakco_accumulate",
-           "gakco_finalize", "gakco_kernel", "gakco_kernel_k", "gakco_get_stats",
+           "gakco_finalize", "gakco_kernel", "gakco_kernel_k", "gakco_kernel_rect",
+           "gakco_get_stats",
            "gakco_num_masks", "gakco_last_error", "gakco_status_string", "gakco_destroy")
 
 
@@ -79,6 +80,7 @@ def lib():
         L.gakco_finalize.argtypes = [P, P, i64, P, P, P, P]
         L.gakco_kernel.argtypes = [P, P, P, i64, P, P, P, P, P]
         L.gakco_kernel_k.argtypes = [P, P, P, i64, P, P, P]
+        L.gakco_kernel_rect.argtypes = [P, P, P, i64, i64, P, P, P, P, P, P]
         L.gakco_get_stats.argtypes = [P, ctypes.POINTER(gakco_stats)]
         L.gakco_num_masks.argtypes = [P, ci]
         L.gakco_num_masks.restype = i64
@@ -89,7 +91,8 @@ def lib():
         L.gakco_destroy.argtypes = [P]
         L.gakco_destroy.restype = None
         for f in ("gakco_create", "gakco_set_shard", "gakco_set_option", "gakco_accumulate",
-                  "gakco_finalize", "gakco_kernel", "gakco_kernel_k", "gakco_get_stats"):
+                  "gakco_finalize", "gakco_kernel", "gakco_kernel_k", "gakco_kernel_rect",
+                  "gakco_get_stats"):
             getattr(L, f).restype = ci
         _lib = L
     return _lib
@@ -154,6 +157,13 @@ def gakco_kernel(plan, codes, offsets, N, C=None, Nm=None, K=None, Knorm=None, s
                                     _ptr(K), _ptr(Knorm), _stream(stream)))
 
 
+def gakco_kernel_rect(plan, codes, offsets, N, NA, C=None, Nm=None, K=None, Knorm=None,
+                      Kdiag=None, stream=None):
+    _check(plan, lib().gakco_kernel_rect(plan, _ptr(codes), _ptr(offsets), N, NA, _ptr(C),
+                                         _ptr(Nm), _ptr(K), _ptr(Knorm), _ptr(Kdiag),
+                                         _stream(stream)))
+
+
 def gakco_kernel_k(plan, codes, offsets, N, K=None, Knorm=None, stream=None):
     _check(plan, lib().gakco_kernel_k(plan, _ptr(codes), _ptr(offsets), N, _ptr(K), _ptr(Knorm),
                                       _stream(stream)))
@@ -200,6 +210,10 @@ class Plan:
     def kernel_k(self, codes, offsets, N, K=None, Knorm=None, stream=None):
         gakco_kernel_k(self.h, codes, offsets, N, K, Knorm, stream)
 
+    def kernel_rect(self, codes, offsets, N, NA, C=None, Nm=None, K=None, Knorm=None,
+                    Kdiag=None, stream=None):
+        gakco_kernel_rect(self.h, codes, offsets, N, NA, C, Nm, K, Knorm, Kdiag, stream)
+
     def stats(self):
         return gakco_get_stats(self.h)
 
@@ -243,6 +257,36 @@ def kernel_matrix(codes, offsets, sigma, g, k, M=None, device=0, plan=None, outp
             s = stream or torch.cuda.current_stream(dev)
             plan.kernel(codes_c, off_c, N, C, Nm, K, Kn, stream=s)
         return {"C": C, "Nm": Nm, "K": K, "Knorm": Kn}
+    finally:
+        if own:
+            plan.close()
+
+
+def kernel_matrix_rect(codes, offsets, NA, sigma, g, k, M=None, device=0, plan=None, stream=None):
+    """Train x test block (NEXT-2): the corpus holds the NA training sequences, then
+    the test sequences. Returns device tensors C, Nm (M+1, NA, NB), K, Knorm (NA, NB)
+    and Kdiag (N,)."""
+    import torch
+    M = g - k if M is None else M
+    N = int(offsets.shape[0]) - 1
+    NB = N - NA
+    dev = torch.device("cuda", device)
+    own = plan is None
+    plan = plan or Plan(sigma, g, k, M, device)
+    try:
+        C = torch.empty((M + 1, NA, NB), dtype=torch.int64, device=dev)
+        Nm = torch.empty((M + 1, NA, NB), dtype=torch.int64, device=dev)
+        K = torch.empty((NA, NB), dtype=torch.int64, device=dev)
+        Kn = torch.empty((NA, NB), dtype=torch.float64, device=dev)
+        Kd = torch.empty((N,), dtype=torch.int64, device=dev)
+        codes_c = np.ascontiguousarray(codes, dtype=np.uint8) if isinstance(codes, np.ndarray) else codes
+        off_c = np.ascontiguousarray(offsets, dtype=np.int64) if isinstance(offsets, np.ndarray) else offsets
+        if isinstance(codes_c, np.ndarray) and codes_c.size == 0:
+            codes_c = np.zeros(1, dtype=np.uint8)
+        with torch.cuda.device(dev):
+            s = stream or torch.cuda.current_stream(dev)
+            plan.kernel_rect(codes_c, off_c, N, NA, C, Nm, K, Kn, Kd, stream=s)
+        return {"C": C, "Nm": Nm, "K": K, "Knorm": Kn, "Kdiag": Kd}
     finally:
         if own:
             plan.close()

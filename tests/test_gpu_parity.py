@@ -433,3 +433,54 @@ def test_large_config_sampled_pairs(gk, oracle_lib, name):
     got = r["Knorm"][torch.as_tensor(sub, device=K.device)][:, torch.as_tensor(sub, device=K.device)]
     assert_knorm(got.cpu().numpy(), ref)
     assert np.array_equal(Kd[d], po["K"][160:200])
+
+
+def _run_rect(gk, cp, NA, g, k, M, **opts):
+    plan = gk.Plan(cp.sigma, g, k, M)
+    for opt, val in opts.items():
+        plan.set_option(getattr(gk, "GAKCO_OPT_" + opt.upper()), val)
+    r = gk.kernel_matrix_rect(cp.codes, cp.offsets, NA, cp.sigma, g, k, M, plan=plan)
+    plan.close()
+    return {key: v.cpu().numpy() for key, v in r.items()}
+
+
+def _assert_rect(got, ref):
+    for key in ("C", "Nm", "K", "Kdiag"):
+        assert np.array_equal(got[key], ref[key]), key
+    np.testing.assert_allclose(got["Knorm"], ref["Knorm"], rtol=KNORM_RTOL, atol=0)
+
+
+def test_rect_train_test(gk, oracle_lib):
+    """NEXT-2: the train x test block through gakco_kernel_rect == the oracle's
+    block (pair-by-pair histograms), over splits, alphabets and the light, heavy
+    (tensor-core Gram, rectangular tiles) and default paths."""
+    rng = np.random.default_rng(112)
+    for it in range(12):
+        sigma = int(rng.choice([2, 4, 20, 36]))
+        g = int(rng.integers(2, 10))
+        k = int(rng.integers(1, g + 1))
+        M = int(rng.integers(0, g + 1))
+        cp = sc.random_small(rng, sigma, n_max=120, l_max=100)
+        N = cp.n_seq
+        if N < 2:
+            continue
+        NA = int(rng.integers(1, N))
+        ref = oracle_lib.rect(cp, NA, g, k, M)
+        _assert_rect(_run_rect(gk, cp, NA, g, k, M), ref)
+        _assert_rect(_run_rect(gk, cp, NA, g, k, M, heavy_min_seqs=2), ref)
+        _assert_rect(_run_rect(gk, cp, NA, g, k, M, heavy_min_seqs=1 << 50), ref)
+
+
+def test_rect_is_block_of_full_dna(gk):
+    """At the DNA config's full size (bench launch configuration), the rectangular
+    block equals the block of the full-matrix path (whose K is digest-verified in
+    test_full_config_digests), for an uneven split (tiles ragged on both sides)."""
+    cfg = sc.CONFIGS["dna"]
+    cp = sc.make("dna")
+    NA = 2731
+    full = gk.kernel_matrix(cp.codes, cp.offsets, cfg.sigma, cfg.g, cfg.k, cfg.M)
+    r = gk.kernel_matrix_rect(cp.codes, cp.offsets, NA, cfg.sigma, cfg.g, cfg.k, cfg.M)
+    assert torch.equal(r["K"], full["K"][:NA, NA:])
+    assert torch.equal(r["C"], full["C"][:, :NA, NA:])
+    assert torch.equal(r["Kdiag"], full["K"].diagonal())
+    assert torch.equal(r["Knorm"], full["Knorm"][:NA, NA:])

@@ -253,3 +253,27 @@ def test_overflow_is_an_error(oracle_lib):
     Nm = np.full((2, 1, 1), 2 ** 62, dtype=np.int64)
     with pytest.raises(RuntimeError):
         oracle_lib.cumulative(Nm, 3)
+
+
+def test_rect_is_block_of_full(oracle_lib):
+    """NEXT-2 oracle: the train x test block assembled pair by pair equals the
+    corresponding block of the full oracle on the concatenated corpus (every
+    output, incl. Knorm from the full diagonal), for several splits."""
+    rng = np.random.default_rng(31)
+    for _ in range(6):
+        sigma = int(rng.choice([2, 4, 20]))
+        g = int(rng.integers(2, 8))
+        k = int(rng.integers(1, g + 1))
+        M = int(rng.integers(0, g + 1))
+        cp = sc.random_small(rng, sigma, n_max=14, l_max=30)
+        N = cp.n_seq
+        if N < 2:
+            continue
+        full = oracle_lib.compute(cp, g, k, M)
+        for NA in sorted({1, N // 2, N - 1}):
+            r = oracle_lib.rect(cp, NA, g, k, M)
+            assert np.array_equal(r["C"], full["C"][:, :NA, NA:])
+            assert np.array_equal(r["Nm"], full["Nm"][:, :NA, NA:])
+            assert np.array_equal(r["K"], full["K"][:NA, NA:])
+            assert np.array_equal(r["Kdiag"], np.diag(full["K"]))
+            np.testing.assert_allclose(r["Knorm"], full["Knorm"][:NA, NA:], rtol=1e-15, atol=0)
