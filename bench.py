@@ -52,6 +52,8 @@ def args_():
     ap.add_argument("--sort-ctas", type=int, default=0)
     ap.add_argument("--light-flat", type=int, default=0,
                     help="light groups of <= this many sequences share a warp (1..32)")
+    ap.add_argument("--relabel", type=int, default=None, choices=[-1, 0, 1],
+                    help="light accumulator relabelling: -1 auto, 0 off, 1 on")
     ap.add_argument("--gram-pair", type=int, default=None, choices=[0, 1],
                     help="heavy Gram kernel: 1 CTA pairs (default), 0 one SM per tile")
     ap.add_argument("--no-timing", action="store_true",
@@ -267,6 +269,8 @@ def run_ours(a):
         plan.set_option(gakco.GAKCO_OPT_SORT_CTAS_PER_SM, a.sort_ctas)
     if a.light_flat:
         plan.set_option(gakco.GAKCO_OPT_LIGHT_FLAT, a.light_flat)
+    if a.relabel is not None:
+        plan.set_option(gakco.GAKCO_OPT_LIGHT_RELABEL, a.relabel)
     if a.gram_pair is not None:
         plan.set_option(gakco.GAKCO_OPT_GRAM_PAIR, a.gram_pair)
     if a.no_timing:

@@ -75,9 +75,12 @@ typedef enum {
     GAKCO_OPT_GRAM_PAIR = 7,      /* heavy-group Gram kernel: 1 = CTA pairs (tcgen05
                                      cta_group::2, 256 x 512 tiles; default), 0 = one SM per
                                      128 x 256 tile */
-    GAKCO_OPT_LIGHT_FLAT = 8      /* light groups of <= this many sequences (1..32, default
+    GAKCO_OPT_LIGHT_FLAT = 8,     /* light groups of <= this many sequences (1..32, default
                                      8) have their pairs flattened across a warp; bigger
                                      ones are enumerated from registers, one group per warp */
+    GAKCO_OPT_LIGHT_RELABEL = 9   /* light accumulator sequence relabelling (locality; results
+                                     unchanged): -1 = automatic (default: when the packed
+                                     triangle exceeds 96 MB), 0 = off, 1 = on */
 } gakco_option;
 
 /* Counters of the last gakco_accumulate (algorithmic units). */

@@ -233,7 +233,17 @@ struct LightBins {
 cudaError_t launch_light(SegmentOut so, uint64_t max_groups, int64_t heavy_min, int64_t N,
                          uint32_t* acc, uint2* heavy_list, uint64_t ldd,
                          uint32_t* dense_fill, LightBins bins, uint32_t flat_max,
-                         int64_t NA, unsigned long long* stats, int sm_count, cudaStream_t s);
+                         int64_t NA, const uint32_t* perm, unsigned long long* stats,
+                         int sm_count, cudaStream_t s);
+// Light accumulator relabelled by perm (sequence -> accumulator index): flush it into
+// C_m (original order) and zero it.
+cudaError_t launch_light_flush_perm(uint32_t* acc, int64_t N, int64_t* Cm, const uint32_t* perm,
+                                    int sm_count, cudaStream_t s);
+// Clusters of sequences for the relabelling: union of every X with its best partner
+// argmax_Y C(X,Y) (C upper triangle); parent[X] <- root. iota: [N] = 0..N-1.
+cudaError_t launch_cluster_roots(const int64_t* C, int64_t N, unsigned long long* best,
+                                 uint32_t* parent, const uint32_t* iota, int sm_count,
+                                 cudaStream_t s);
 // rectangular accumulator (NA x NB, row-major) -> C_m (NA x NB), zeroed
 cudaError_t launch_light_flush_rect(uint32_t* acc, uint64_t cells, int64_t* Cm, int sm_count,
                                     cudaStream_t s);

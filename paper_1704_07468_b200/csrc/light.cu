@@ -26,7 +26,11 @@ __device__ __forceinline__ uint64_t tri_index(uint32_t x, uint32_t y, int64_t N)
 // [0, NA) are the rows, [NA, N) the columns), row-major NA x (N - NA) for a
 // cross pair; a pair inside one set is not a cell (*ok = false).
 __device__ __forceinline__ uint64_t pair_cell(uint32_t x, uint32_t y, int64_t N, int64_t NA,
-                                              bool* ok) {
+                                              bool* ok, const uint32_t* perm = nullptr) {
+    if (perm) {  // relabelled accumulator (full mode only): cell of {perm[x], perm[y]}
+        x = perm[x];
+        y = perm[y];
+    }
     const uint32_t lo = min(x, y), hi = max(x, y);
     if (NA == 0) {
         *ok = true;
@@ -90,7 +94,8 @@ __global__ void __launch_bounds__(256) light_kernel(SegmentOut so, int64_t heavy
                                                     uint32_t* acc, uint2* heavy_list,
                                                     uint64_t ldd, uint32_t* dense_fill,
                                                     LightBins bn, uint32_t flat_max,
-                                                    int64_t NA, unsigned long long* stats) {
+                                                    int64_t NA, const uint32_t* perm,
+                                                    unsigned long long* stats) {
     // triangle table: pairs (a < b < 32) ordered by b, so the first n(n-1)/2
     // entries are exactly the pairs of an n-triple chunk
     __shared__ uint16_t s_tri[496];
@@ -146,7 +151,7 @@ __global__ void __launch_bounds__(256) light_kernel(SegmentOut so, int64_t heavy
                 const uint32_t ab = s_tri[q - ej];
                 const uint32_t ta = sj + (ab & 31), tb = sj + (ab >> 5);
                 const uint32_t xa = so.tseq[ta] & 0x7fffffffu, xb = so.tseq[tb] & 0x7fffffffu;
-                idx = pair_cell(xa, xb, N, NA, &ok);
+                idx = pair_cell(xa, xb, N, NA, &ok, perm);
                 val = so.tcnt[ta] * so.tcnt[tb];
             }
             pair_add(acc, bn, ok, idx, val);
@@ -210,7 +215,7 @@ __global__ void __launch_bounds__(256) light_kernel(SegmentOut so, int64_t heavy
                     const uint32_t xb = __shfl_sync(0xffffffffu, xA, b);
                     const uint32_t cb = __shfl_sync(0xffffffffu, cA, b);
                     bool ok = false;
-                    const uint64_t idx = q < P ? pair_cell(xa, xb, N, NA, &ok) : 0;
+                    const uint64_t idx = q < P ? pair_cell(xa, xb, N, NA, &ok, perm) : 0;
                     pair_add(acc, bn, ok && q < P, idx, ca * cb);
                 }
                 for (uint32_t B = A + 32; B < b0; B += 32) {
@@ -222,7 +227,7 @@ __global__ void __launch_bounds__(256) light_kernel(SegmentOut so, int64_t heavy
                         const uint32_t xa = __shfl_sync(0xffffffffu, xA, a);
                         const uint32_t ca = __shfl_sync(0xffffffffu, cA, a);
                         bool ok = false;
-                        const uint64_t idx = vb ? pair_cell(xa, xB, N, NA, &ok) : 0;
+                        const uint64_t idx = vb ? pair_cell(xa, xB, N, NA, &ok, perm) : 0;
                         pair_add(acc, bn, ok && vb, idx, ca * cB);
                     }
                 }
@@ -236,13 +241,14 @@ __global__ void __launch_bounds__(256) light_kernel(SegmentOut so, int64_t heavy
 cudaError_t launch_light(SegmentOut so, uint64_t max_groups, int64_t heavy_min, int64_t N,
                          uint32_t* acc, uint2* heavy_list, uint64_t ldd,
                          uint32_t* dense_fill, LightBins bins, uint32_t flat_max,
-                         int64_t NA, unsigned long long* stats, int sm_count, cudaStream_t s) {
+                         int64_t NA, const uint32_t* perm, unsigned long long* stats,
+                         int sm_count, cudaStream_t s) {
     if (max_groups == 0) return cudaGetLastError();
     uint64_t blocks = (max_groups + 255) / 256;  // 8 warps x 32 groups per block-round
     uint64_t cap = (uint64_t)sm_count * 8;
     if (blocks > cap) blocks = cap;
     light_kernel<<<(unsigned)blocks, 256, 0, s>>>(so, heavy_min, N, acc, heavy_list, ldd,
-                                                  dense_fill, bins, flat_max, NA, stats);
+                                                  dense_fill, bins, flat_max, NA, perm, stats);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess || bins.nb == 0) return e;
     return launch_apply_bins(acc, bins, sm_count, s);
@@ -262,6 +268,107 @@ __global__ void light_flush_kernel(uint32_t* __restrict__ acc, int64_t N, int64_
             }
         }
     }
+}
+
+// Relabelled accumulator: C_m(X,Y) += acc[cell{perm[X], perm[Y]}] for X < Y, read
+// row by row of C_m (coalesced int64 adds; the acc reads gather). The caller zeroes
+// acc afterwards (one memset).
+__global__ void light_flush_perm_kernel(const uint32_t* __restrict__ acc, int64_t N,
+                                        int64_t* __restrict__ Cm,
+                                        const uint32_t* __restrict__ perm) {
+    for (int64_t x = blockIdx.x; x < N - 1; x += gridDim.x) {
+        const uint32_t px = perm[x];
+        int64_t* crow = Cm + x * N;
+        for (int64_t y = x + 1 + threadIdx.x; y < N; y += blockDim.x) {
+            const uint32_t py = perm[y];
+            const uint32_t v = acc[tri_index(min(px, py), max(px, py), N)];
+            if (v) crow[y] += v;
+        }
+    }
+}
+
+cudaError_t launch_light_flush_perm(uint32_t* acc, int64_t N, int64_t* Cm, const uint32_t* perm,
+                                    int sm_count, cudaStream_t s) {
+    if (N < 2) return cudaGetLastError();
+    int64_t blocks = N - 1 < (int64_t)sm_count * 16 ? N - 1 : (int64_t)sm_count * 16;
+    light_flush_perm_kernel<<<(unsigned)blocks, 256, 0, s>>>(acc, N, Cm, perm);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    return cudaMemsetAsync(acc, 0, (size_t)N * (size_t)(N - 1) / 2 * 4, s);
+}
+
+// ---- sequence relabelling for the light accumulator (locality) ----
+// best[X] = max over Y != X of (C(X,Y) << 32 | Y) for C(X,Y) > 0 (upper triangle read
+// once; both endpoints updated): the partner sharing the most matches with X.
+__global__ void best_partner_kernel(const int64_t* __restrict__ C, int64_t N,
+                                    unsigned long long* best) {
+    for (int64_t x = blockIdx.x; x < N - 1; x += gridDim.x) {
+        const int64_t* row = C + x * N;
+        unsigned long long mine = 0ull;
+        for (int64_t y = x + 1 + threadIdx.x; y < N; y += blockDim.x) {
+            const int64_t v = row[y];
+            if (v > 0) {
+                const unsigned long long vc = (unsigned long long)min(v, (int64_t)0xffffffff);
+                mine = max(mine, (vc << 32) | (unsigned long long)y);
+                atomicMax(&best[y], (vc << 32) | (unsigned long long)x);
+            }
+        }
+        for (int o = 16; o > 0; o >>= 1) mine = max(mine, __shfl_xor_sync(0xffffffffu, mine, o));
+        if ((threadIdx.x & 31) == 0 && mine) atomicMax(&best[x], mine);
+    }
+}
+
+__device__ __forceinline__ uint32_t uf_find(uint32_t* parent, uint32_t x) {
+    while (true) {
+        const uint32_t p = parent[x];
+        if (p == x) return x;
+        const uint32_t gp = parent[p];
+        if (gp != p) atomicCAS(&parent[x], p, gp);  // path halving
+        x = p;
+    }
+}
+
+// union(X, best partner of X), lock-free (the larger root is hooked under the smaller)
+__global__ void best_union_kernel(const unsigned long long* __restrict__ best, int64_t N,
+                                  uint32_t* parent) {
+    for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < N;
+         x += (int64_t)gridDim.x * blockDim.x) {
+        const unsigned long long b = best[x];
+        if (!b) continue;
+        uint32_t a = (uint32_t)x, c = (uint32_t)(b & 0xffffffffull);
+        while (true) {
+            a = uf_find(parent, a);
+            c = uf_find(parent, c);
+            if (a == c) break;
+            if (a < c) {
+                const uint32_t t = a;
+                a = c;
+                c = t;
+            }
+            if (atomicCAS(&parent[a], a, c) == a) break;
+        }
+    }
+}
+
+__global__ void uf_roots_kernel(uint32_t* parent, int64_t N) {
+    for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < N;
+         x += (int64_t)gridDim.x * blockDim.x)
+        parent[x] = uf_find(parent, (uint32_t)x);
+}
+
+cudaError_t launch_cluster_roots(const int64_t* C, int64_t N, unsigned long long* best,
+                                 uint32_t* parent, const uint32_t* iota, int sm_count,
+                                 cudaStream_t s) {
+    cudaError_t e = cudaMemsetAsync(best, 0, N * sizeof(unsigned long long), s);
+    if (e != cudaSuccess) return e;
+    e = cudaMemcpyAsync(parent, iota, N * sizeof(uint32_t), cudaMemcpyDeviceToDevice, s);
+    if (e != cudaSuccess) return e;
+    const int64_t rows = N - 1 < (int64_t)sm_count * 16 ? N - 1 : (int64_t)sm_count * 16;
+    if (rows > 0) best_partner_kernel<<<(unsigned)rows, 256, 0, s>>>(C, N, best);
+    const int blocks = (int)((N + 255) / 256 < 1024 ? (N + 255) / 256 : 1024);
+    best_union_kernel<<<blocks, 256, 0, s>>>(best, N, parent);
+    uf_roots_kernel<<<blocks, 256, 0, s>>>(parent, N);
+    return cudaGetLastError();
 }
 
 // Rectangular mode: C_m[X][Y - NA] += acc[X][Y - NA] (row-major NA x NB), zeroed.

@@ -84,6 +84,7 @@ struct gakco_plan {
     int64_t light_bins = 0;    // 0 auto, < 0 off, > 0 forced block size in cells
     int gram_pair = 1;         // 1: CTA-pair Gram (gram2.cu), 0: one-SM Gram (gram_tc.cu)
     int light_flat = 8;        // light groups of <= this many sequences share warps
+    int light_relabel = -1;    // -1 auto (accumulator >> L2), 0 off, 1 on
     int sm_count = 148;
     std::string err;
 
@@ -92,7 +93,7 @@ struct gakco_plan {
     std::vector<std::array<uint8_t, GMAX>> mask_kept;
     std::vector<int> key_bits;  // per level
 
-    DevBuf Dgscr, Kdscr, codes, off, gofs, gmseq, keysA, keysB, hist, status, ctr, tseq, tcnt, gstart, gend,
+    DevBuf perm, iota, best, parent, Dgscr, Kdscr, codes, off, gofs, gmseq, keysA, keysB, hist, status, ctr, tseq, tcnt, gstart, gend,
         counts, kept, stats, flags, kdiag, Cscr, Nmscr, Kscr, Knscr, heavy, hcount, dense, tiles,
         lightacc, binrec, bincnt, win, bkH, bktot, bkbase, bkdesc, bktab, bktcnt, bkgs, bkocc;
     int64_t tiles_npad = -1;
@@ -250,7 +251,7 @@ extern "C" gakco_status gakco_create(int sigma, int g, int k, int M, int device,
 extern "C" void gakco_destroy(gakco_plan* p) {
     if (!p) return;
     DeviceGuard dg(p->device);
-    DevBuf* bufs[] = {&p->Dgscr, &p->Kdscr, &p->codes, &p->off,   &p->gofs,  &p->gmseq,  &p->keysA, &p->keysB,
+    DevBuf* bufs[] = {&p->perm, &p->iota, &p->best, &p->parent, &p->Dgscr, &p->Kdscr, &p->codes, &p->off,   &p->gofs,  &p->gmseq,  &p->keysA, &p->keysB,
                       &p->hist,  &p->status, &p->ctr,  &p->tseq,   &p->tcnt,  &p->gstart,
                       &p->gend,  &p->counts, &p->kept, &p->stats,  &p->flags, &p->kdiag,
                       &p->Cscr,  &p->Nmscr, &p->Kscr,  &p->Knscr, &p->heavy, &p->hcount,
@@ -299,6 +300,10 @@ extern "C" gakco_status gakco_set_option(gakco_plan* p, int option, int64_t valu
         case GAKCO_OPT_LIGHT_FLAT:
             if (value < 1 || value > 32) return p->fail(GAKCO_E_ARG, "light flat must be 1..32");
             p->light_flat = (int)value;
+            return GAKCO_OK;
+        case GAKCO_OPT_LIGHT_RELABEL:
+            if (value < -1 || value > 1) return p->fail(GAKCO_E_ARG, "relabel must be -1..1");
+            p->light_relabel = (int)value;
             return GAKCO_OK;
         case GAKCO_OPT_TIMING:
             p->timing = value != 0;
@@ -627,6 +632,44 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
             bins = LightBins{(uint32_t*)p->binrec.p, (uint32_t*)p->bincnt.p, cap, bc, nb};
         }
     }
+    // Sequence relabelling of the light accumulator (locality): when the
+    // packed triangle is far larger than L2, the sequences are reordered after the
+    // first level by clusters of best partners (argmax_Y C_m(X,Y)), so pairs that
+    // share many keys (families) update nearby cells; the flush maps back.
+    const bool relabel = !rect && bins.nb == 0 && N >= 2 &&
+                         (p->light_relabel == 1 ||
+                          (p->light_relabel == -1 && ntri * 4 > (96ull << 20)));
+    bool perm_active = false;
+    if (relabel) {
+        CK(p->ensure(p->perm, N * 4, s));
+        CK(p->ensure(p->iota, N * 4, s));
+        CK(p->ensure(p->best, N * 8, s));
+        CK(p->ensure(p->parent, N * 4, s));
+        std::vector<uint32_t> io(N);
+        for (int64_t i = 0; i < N; ++i) io[i] = (uint32_t)i;
+        CK(cudaMemcpyAsync(p->iota.p, io.data(), N * 4, cudaMemcpyHostToDevice, s));
+        CK(cudaStreamSynchronize(s));  // io is a local buffer
+    }
+    auto make_perm = [&](int m_done) -> gakco_status {
+        cudaEvent_t ar = nullptr;
+        p->stage_begin(s, &ar);
+        p->launches += 3;
+        CK(launch_cluster_roots(level_ptr(m_done), N, (unsigned long long*)p->best.p,
+                                (uint32_t*)p->parent.p, (const uint32_t*)p->iota.p,
+                                p->sm_count, s));
+        p->stage_end(s, S_LIGHT, ar);
+        std::vector<uint32_t> root(N), order(N), pm(N);
+        CK(cudaMemcpyAsync(root.data(), p->parent.p, N * 4, cudaMemcpyDeviceToHost, s));
+        CK(cudaStreamSynchronize(s));
+        for (int64_t i = 0; i < N; ++i) order[i] = (uint32_t)i;
+        std::stable_sort(order.begin(), order.end(),
+                         [&](uint32_t a, uint32_t b) { return root[a] < root[b]; });
+        for (int64_t i = 0; i < N; ++i) pm[order[i]] = (uint32_t)i;
+        CK(cudaMemcpyAsync(p->perm.p, pm.data(), N * 4, cudaMemcpyHostToDevice, s));
+        CK(cudaStreamSynchronize(s));  // pm is a local buffer
+        perm_active = true;
+        return GAKCO_OK;
+    };
     uint64_t light_masks = 0;
     int light_m = -1;
     const uint64_t light_lim =
@@ -638,6 +681,9 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
         if (rect)
             LK(launch_light_flush_rect((uint32_t*)p->lightacc.p, ntri, level_ptr(light_m),
                                        p->sm_count, s));
+        else if (perm_active)
+            LK(launch_light_flush_perm((uint32_t*)p->lightacc.p, N, level_ptr(light_m),
+                                       (const uint32_t*)p->perm.p, p->sm_count, s));
         else
             LK(launch_light_flush((uint32_t*)p->lightacc.p, N, level_ptr(light_m), p->sm_count,
                                   s));
@@ -669,8 +715,15 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
         }
         if (n > 0) {
             if (light_m != m || light_masks + nmask > light_lim) {
+                const int done = light_m;
                 gakco_status fs = lflush();
                 if (fs != GAKCO_OK) return fs;
+                if (relabel && !perm_active && done >= 0 && done != m) {
+                    // level `done` is complete in C: its Gram flush was issued at this level
+                    // change by the heavy block above, its light flush just now
+                    fs = make_perm(done);
+                    if (fs != GAKCO_OK) return fs;
+                }
             }
             light_m = m;
             light_masks += nmask;
@@ -761,7 +814,9 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
             p->stage_begin(s, &a);
             LK(launch_light(so, n * nmask / 2 + 1, light_limit, N, (uint32_t*)p->lightacc.p,
                             (uint2*)p->heavy.p, rcap, (uint32_t*)p->hcount.p, bins,
-                            (uint32_t)p->light_flat, NA, stats, p->sm_count, s));
+                            (uint32_t)p->light_flat, NA,
+                            perm_active ? (const uint32_t*)p->perm.p : nullptr, stats,
+                            p->sm_count, s));
             p->stage_end(s, S_LIGHT, a);
             if (gram_ok) {
                 p->stage_begin(s, &a);

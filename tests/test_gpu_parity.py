@@ -125,6 +125,24 @@ def test_light_flat_threshold(gk, oracle_lib):
             assert_parity(run(gk, cp, g, k, g - k, light_flat=flat, heavy_min_seqs=1 << 50), ref)
 
 
+def test_light_relabel(gk, oracle_lib):
+    """Light accumulator relabelled after the first level by best-partner clusters
+    (forced on; automatic only for accumulators far beyond L2) == oracle, on
+    family-structured and random corpora, M >= 1 so later levels use the labels."""
+    rng = np.random.default_rng(113)
+    cases = [(sc.gen_families(7, 90, 6, 60, 30, 60, sigma=20), 6, 3, 3),
+             (sc.gen_families(8, 150, 10, 80, 80, 80, sigma=4), 8, 5, 3)]
+    for _ in range(4):
+        sigma = int(rng.choice([2, 4, 20]))
+        g = int(rng.integers(3, 9))
+        k = int(rng.integers(1, g))
+        cases.append((sc.random_small(rng, sigma, n_max=120, l_max=90), g, k, g - k))
+    for cp, g, k, M in cases:
+        ref = oracle_lib.compute(cp, g, k, M)
+        assert_parity(run(gk, cp, g, k, M, light_relabel=1), ref)
+        assert_parity(run(gk, cp, g, k, M, light_relabel=1, heavy_min_seqs=1 << 50), ref)
+
+
 def test_light_binning(gk, oracle_lib):
     """Binned light updates (forced, tiny accumulator blocks so records span many
     buckets and some buckets overflow to direct atomics) == oracle."""
