@@ -68,7 +68,7 @@ typedef enum {
                                      decoupled look-back, 2 = hash partition + shared-memory
                                      hash grouping (falls back to 0 where it does not apply:
                                      g*ceil(log2 sigma) > 64 or > 16M g-mers) */
-    GAKCO_OPT_SORT_CTAS_PER_SM = 5, /* chunked pass grid size in CTAs per SM (default 3) */
+    GAKCO_OPT_SORT_CTAS_PER_SM = 5, /* chunked pass grid size in CTAs per SM (default 4) */
     GAKCO_OPT_LIGHT_BINS = 6,     /* light updates binned by accumulator block (ablation /
                                      test knob): <= 0 = never (default; measured slower on
                                      Scale), > 0 = always, with this many cells per block */

@@ -80,7 +80,7 @@ struct gakco_plan {
     // 0 chunked two-kernel LSD pass, 1 onesweep LSD (decoupled look-back),
     // 2 hash partition + shared-memory hash grouping (bucket.cu)
     int sort_mode = -1;
-    int sort_ctas_per_sm = 3;  // chunked pass grid = this x SMs (measured best of 1..4)
+    int sort_ctas_per_sm = 4;  // chunked pass grid = this x SMs (2 resident: 2 full waves; measured best of 2..4)
     int64_t light_bins = 0;    // 0 auto, < 0 off, > 0 forced block size in cells
     int gram_pair = 1;         // 1: CTA-pair Gram (gram2.cu), 0: one-SM Gram (gram_tc.cu)
     int light_flat = 8;        // light groups of <= this many sequences share warps
