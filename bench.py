@@ -54,6 +54,8 @@ def args_():
                     help="light groups of <= this many sequences share a warp (1..32)")
     ap.add_argument("--relabel", type=int, default=None, choices=[-1, 0, 1],
                     help="light accumulator relabelling: -1 auto, 0 off, 1 on")
+    ap.add_argument("--fp4", type=int, default=None, choices=[-1, 0, 1],
+                    help="heavy Gram operands: -1 auto (e2m1 where exact), 0 u8, 1 e2m1")
     ap.add_argument("--gram-pair", type=int, default=None, choices=[0, 1],
                     help="heavy Gram kernel: 1 CTA pairs (default), 0 one SM per tile")
     ap.add_argument("--no-timing", action="store_true",
@@ -271,6 +273,8 @@ def run_ours(a):
         plan.set_option(gakco.GAKCO_OPT_LIGHT_FLAT, a.light_flat)
     if a.relabel is not None:
         plan.set_option(gakco.GAKCO_OPT_LIGHT_RELABEL, a.relabel)
+    if a.fp4 is not None:
+        plan.set_option(gakco.GAKCO_OPT_GRAM_FP4, a.fp4)
     if a.gram_pair is not None:
         plan.set_option(gakco.GAKCO_OPT_GRAM_PAIR, a.gram_pair)
     if a.no_timing:
@@ -427,12 +431,16 @@ def run_ours(a):
                 "peak_source": pk["source"] + " hbm_gbs"}
     else:
         achieved = algo / t_dom / 1e12 if t_dom > 0 else 0.0
-        peak = pk["bf16_tflops"] * 2.0  # int8 = 2x bf16 (nominal 4.5 vs 2.25 PFLOP/s)
+        # int8 = 2x bf16 (nominal 4.5 vs 2.25 PFLOP/s); e2m1 (kind::mxf4) = 4x (9 vs 2.25)
+        ratio = 4.0 if last.get("gram_fp4", 0) else 2.0
+        peak = pk["bf16_tflops"] * ratio
         roof = {"bound": "tensor", "kernel": dom, "achieved": achieved, "peak": peak,
                 "unit": "TFLOP/s", "frac": achieved / peak, "traffic": traffic,
                 "algorithmic_ops_per_launch": algo / nl, "launches_per_step": nl,
                 "avg_launch_ms": per_step[dom] / nl,
-                "peak_source": pk["source"] + " bf16_tflops x2 (int8 nominal ratio)"}
+                "peak_source": pk["source"] + (" bf16_tflops x4 (e2m1 nominal ratio)"
+                                               if ratio == 4.0 else
+                                               " bf16_tflops x2 (int8 nominal ratio)")}
 
     out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
            "warmup": a.warmup, "ms_per_step": ms_per_step,

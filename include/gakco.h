@@ -78,9 +78,14 @@ typedef enum {
     GAKCO_OPT_LIGHT_FLAT = 8,     /* light groups of <= this many sequences (1..32, default
                                      8) have their pairs flattened across a warp; bigger
                                      ones are enumerated from registers, one group per warp */
-    GAKCO_OPT_LIGHT_RELABEL = 9   /* light accumulator sequence relabelling (locality; results
+    GAKCO_OPT_LIGHT_RELABEL = 9,  /* light accumulator sequence relabelling (locality; results
                                      unchanged): -1 = automatic (default: when the packed
                                      triangle exceeds 96 MB), 0 = off, 1 = on */
+    GAKCO_OPT_GRAM_FP4 = 10       /* heavy-group Gram operands: -1 = automatic (default: e2m1
+                                     counts, kind::mxf4 block-scaled with unit scales, when one
+                                     mask's n_max^2 < 2^24 keeps the f32 sums exact; groups
+                                     with a count > 4 stay light), 0 = u8 (kind::i8), 1 = e2m1
+                                     where exact */
 } gakco_option;
 
 /* Counters of the last gakco_accumulate (algorithmic units). */
@@ -105,6 +110,7 @@ typedef struct {
     double ms_dense;        /* building the dense u8 count columns of heavy groups */
     int64_t n_dense;
     int64_t n_pad;          /* rows of the dense count matrix (0: no tensor-core Gram) */
+    int64_t gram_fp4;       /* 1: the Gram ran on e2m1 counts (kind::mxf4), 0: u8 (kind::i8) */
 } gakco_stats;
 
 /* Create a plan for alphabet size sigma (1..255), g-mer length g (1..32),

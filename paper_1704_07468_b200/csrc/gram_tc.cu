@@ -319,14 +319,22 @@ __device__ __forceinline__ uint32_t bd2_off(uint32_t r, uint32_t cc) {
     return r * GT_KB + ((((cc >> 2) ^ (r & 31u)) << 2) | (cc & 3u));
 }
 
+// FP4 = true: e2m1 codes packed two per byte (slab = 256 columns = 128 bytes per row;
+// count c in 1..4 -> code 2, 4, 5, 6; the light path keeps counts > 4).
+__device__ __forceinline__ uint32_t e2m1_code(uint32_t c) {
+    return c <= 2 ? 2 * c : c + 2;  // 0->0, 1->2 (1.0), 2->4 (2.0), 3->5 (3.0), 4->6 (4.0)
+}
+
+template <bool FP4>
 __global__ void __launch_bounds__(BD2_THREADS) build_dense2_kernel(
     SegmentOut so, const uint2* __restrict__ heavy_list, const uint32_t* fill,
     uint8_t* __restrict__ D, int64_t n_pad, uint64_t ldd, int sorted) {
     extern __shared__ __align__(16) unsigned char sb[];  // [BD2_ROWS][128], swizzled words
+    constexpr uint32_t SC = FP4 ? 2 * GT_KB : GT_KB;     // columns per slab
     const uint64_t f0 = fill[1];
     const uint64_t f1 = min((uint64_t)fill[0], ldd);
     if (f1 <= f0) return;
-    const uint64_t s0 = f0 / GT_KB, s1 = (f1 + GT_KB - 1) / GT_KB;
+    const uint64_t s0 = f0 / SC, s1 = (f1 + SC - 1) / SC;
     const uint64_t nrc = (uint64_t)(n_pad + BD2_ROWS - 1) / BD2_ROWS;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     for (uint64_t wk = blockIdx.x; wk < (s1 - s0) * nrc; wk += gridDim.x) {
@@ -336,12 +344,14 @@ __global__ void __launch_bounds__(BD2_THREADS) build_dense2_kernel(
         for (uint32_t i = threadIdx.x; i < rows * (GT_KB / 16); i += BD2_THREADS)
             ((uint4*)sb)[i] = make_uint4(0u, 0u, 0u, 0u);
         __syncthreads();
-        // warp w fills columns w + 16 j (j < 8); the 8 columns' loads are issued
-        // together at every step (one latency per step, not per column)
-        constexpr int CPW = GT_KB / (BD2_THREADS / 32);  // 8 columns per warp
+        // warp w fills columns w + 16 j (j < 8) of each 128-column half; the 8
+        // columns' loads are issued together at every step (one latency per step)
+        constexpr int CPW = GT_KB / (BD2_THREADS / 32);  // 8 columns per warp per half
+#pragma unroll 1
+        for (uint32_t half = 0; half < SC / GT_KB; ++half) {
         uint32_t lo[CPW], hi[CPW];
         {
-            const uint64_t col = slab * GT_KB + warp + (BD2_THREADS / 32) * (lane & (CPW - 1));
+            const uint64_t col = slab * SC + half * GT_KB + warp + (BD2_THREADS / 32) * (lane & (CPW - 1));
             const uint2 bnd = (lane < CPW && col < f1) ? heavy_list[col] : make_uint2(0u, 0u);
 #pragma unroll
             for (int j = 0; j < CPW; ++j) {
@@ -386,11 +396,20 @@ __global__ void __launch_bounds__(BD2_THREADS) build_dense2_kernel(
             }
 #pragma unroll
             for (int j = 0; j < CPW; ++j)
-                if (xv[j] >= r0 && xv[j] < r0 + rows)
-                    sb[bd2_off(xv[j] - r0, warp + (BD2_THREADS / 32) * j)] = (uint8_t)cv[j];
+                if (xv[j] >= r0 && xv[j] < r0 + rows) {
+                    const uint32_t cc = half * GT_KB + warp + (BD2_THREADS / 32) * j;
+                    if (FP4) {  // nibble cc & 1 of byte cc / 2 (a word is shared by 8 columns)
+                        const uint32_t r = xv[j] - r0;
+                        uint32_t* wp = (uint32_t*)(sb + r * GT_KB) + (((cc >> 3) ^ (r & 31u)));
+                        atomicOr(wp, e2m1_code(cv[j]) << (((cc >> 1) & 3u) * 8 + (cc & 1u) * 4));
+                    } else {
+                        sb[bd2_off(xv[j] - r0, cc)] = (uint8_t)cv[j];
+                    }
+                }
         }
+        }  // half
         __syncthreads();
-        uint4* dst = (uint4*)(D + (slab * (uint64_t)n_pad + r0) * GT_KB);
+        uint4* dst = (uint4*)(D + (slab * (uint64_t)n_pad + r0) * GT_KB);  // 128 B rows
         for (uint32_t i = threadIdx.x; i < rows * (GT_KB / 16); i += BD2_THREADS) {
             const uint32_t r = i >> 3, q = i & 7;
             const uint32_t* w = (const uint32_t*)(sb + r * GT_KB);
@@ -405,33 +424,41 @@ __global__ void __launch_bounds__(BD2_THREADS) build_dense2_kernel(
     }
 }
 
-// After a batch's build: fill rounded up to whole slabs; the next batch starts there.
-__global__ void fill_round_kernel(uint32_t* fill, uint64_t ldd) {
+// After a batch's build: fill rounded up to whole slabs (sc columns); the next batch
+// starts there.
+__global__ void fill_round_kernel(uint32_t* fill, uint64_t ldd, uint32_t sc) {
     uint64_t f = min((uint64_t)fill[0], ldd);
-    f = min((f + GT_KB - 1) / GT_KB * GT_KB, ldd);
+    f = min((f + sc - 1) / sc * sc, ldd);
     fill[0] = (uint32_t)f;
     fill[1] = (uint32_t)f;
 }
 
-// After a Gram flush: count the issued MACs and reset the fill.
+// After a Gram flush: count the issued MACs (K rounded to sc columns) and reset the fill.
 __global__ void fill_reset_kernel(uint32_t* fill, uint64_t ldd, uint64_t tile_macs,
-                                  unsigned long long* stats) {
-    const uint64_t k = (min((uint64_t)fill[0], ldd) + GT_KB - 1) / GT_KB * GT_KB;
+                                  unsigned long long* stats, uint32_t sc) {
+    const uint64_t k = (min((uint64_t)fill[0], ldd) + sc - 1) / sc * sc;
     atomicAdd(&stats[ST_HEAVY_MACS], (unsigned long long)(tile_macs * k));
     fill[0] = 0;
     fill[1] = 0;
 }
 
 cudaError_t launch_build_dense(SegmentOut so, const uint2* heavy_list, uint32_t* dense_fill,
-                               uint8_t* D, int64_t n_pad, uint64_t ldd, int sorted, int sm_count,
-                               cudaStream_t s) {
-    cudaFuncSetAttribute(build_dense2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)BD2_SMEM);
-    build_dense2_kernel<<<sm_count * 3, BD2_THREADS, BD2_SMEM, s>>>(so, heavy_list, dense_fill,
-                                                                    D, n_pad, ldd, sorted);
+                               uint8_t* D, int64_t n_pad, uint64_t ldd, int sorted, int fp4,
+                               int sm_count, cudaStream_t s) {
+    if (fp4) {
+        cudaFuncSetAttribute(build_dense2_kernel<true>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)BD2_SMEM);
+        build_dense2_kernel<true><<<sm_count * 3, BD2_THREADS, BD2_SMEM, s>>>(
+            so, heavy_list, dense_fill, D, n_pad, ldd, sorted);
+    } else {
+        cudaFuncSetAttribute(build_dense2_kernel<false>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)BD2_SMEM);
+        build_dense2_kernel<false><<<sm_count * 3, BD2_THREADS, BD2_SMEM, s>>>(
+            so, heavy_list, dense_fill, D, n_pad, ldd, sorted);
+    }
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    fill_round_kernel<<<1, 1, 0, s>>>(dense_fill, ldd);
+    fill_round_kernel<<<1, 1, 0, s>>>(dense_fill, ldd, fp4 ? 2 * GT_KB : GT_KB);
     return cudaGetLastError();
 }
 
@@ -495,7 +522,12 @@ cudaError_t gram_maps(uint8_t* D, int64_t n_pad, uint64_t ldd, int64_t* Cm, int6
 
 void launch_fill_reset(uint32_t* dense_fill, uint64_t ldd, uint64_t tile_macs,
                        unsigned long long* stats, cudaStream_t s) {
-    fill_reset_kernel<<<1, 1, 0, s>>>(dense_fill, ldd, tile_macs, stats);
+    fill_reset_kernel<<<1, 1, 0, s>>>(dense_fill, ldd, tile_macs, stats, GT_KB);
+}
+
+void launch_fill_reset4(uint32_t* dense_fill, uint64_t ldd, uint64_t tile_macs,
+                        unsigned long long* stats, cudaStream_t s) {
+    fill_reset_kernel<<<1, 1, 0, s>>>(dense_fill, ldd, tile_macs, stats, 2 * GT_KB);
 }
 
 cudaError_t launch_gram_flush(uint8_t* D, int64_t n_pad, uint64_t ldd, uint32_t* dense_fill,
@@ -515,7 +547,8 @@ cudaError_t launch_gram_flush(uint8_t* D, int64_t n_pad, uint64_t ldd, uint32_t*
     gram_kernel<<<grid, GT_THREADS, GT_SMEM, s>>>(map, cmap, a);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    fill_reset_kernel<<<1, 1, 0, s>>>(dense_fill, ldd, (uint64_t)ntiles * GT_M * GT_N, stats);
+    fill_reset_kernel<<<1, 1, 0, s>>>(dense_fill, ldd, (uint64_t)ntiles * GT_M * GT_N, stats,
+                                      GT_KB);
     return cudaGetLastError();
 }
 

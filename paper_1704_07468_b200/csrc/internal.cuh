@@ -233,8 +233,8 @@ struct LightBins {
 cudaError_t launch_light(SegmentOut so, uint64_t max_groups, int64_t heavy_min, int64_t N,
                          uint32_t* acc, uint2* heavy_list, uint64_t ldd,
                          uint32_t* dense_fill, LightBins bins, uint32_t flat_max,
-                         int64_t NA, const uint32_t* perm, unsigned long long* stats,
-                         int sm_count, cudaStream_t s);
+                         int64_t NA, const uint32_t* perm, uint32_t heavy_cmax,
+                         unsigned long long* stats, int sm_count, cudaStream_t s);
 // Light accumulator relabelled by perm (sequence -> accumulator index): flush it into
 // C_m (original order) and zero it.
 cudaError_t launch_light_flush_perm(uint32_t* acc, int64_t N, int64_t* Cm, const uint32_t* perm,
@@ -253,8 +253,8 @@ cudaError_t launch_light_flush_rect(uint32_t* acc, uint64_t cells, int64_t* Cm, 
 // and set dense_fill[1] = dense_fill[0].
 // sorted = 1: each group's triples are in ascending sequence order (LSD path).
 cudaError_t launch_build_dense(SegmentOut so, const uint2* heavy_list, uint32_t* dense_fill,
-                               uint8_t* D, int64_t n_pad, uint64_t ldd, int sorted, int sm_count,
-                               cudaStream_t s);
+                               uint8_t* D, int64_t n_pad, uint64_t ldd, int sorted, int fp4,
+                               int sm_count, cudaStream_t s);
 // acc: u32 strictly-upper packed triangle (N(N-1)/2); flush adds it into C_m, zeroes it.
 cudaError_t launch_light_flush(uint32_t* acc, int64_t N, int64_t* Cm, int sm_count,
                                cudaStream_t s);
@@ -286,6 +286,14 @@ cudaError_t launch_gram_flush(uint8_t* D, int64_t n_pad, uint64_t ldd, uint32_t*
 // (N - NA)), over the tiles of gram2_tiles_rect.
 std::vector<int2> gram2_tiles(int64_t n_pad);
 std::vector<int2> gram2_tiles_rect(int64_t NA, int64_t NB);
+// e2m1 (kind::mxf4) variant: 256 x 256 pair tiles, D packed 4-bit (slabs of 256
+// columns), f32 accumulation (exact below 2^24 per entry and flush)
+std::vector<int2> gram4_tiles(int64_t n_pad);
+std::vector<int2> gram4_tiles_rect(int64_t NA, int64_t NB);
+cudaError_t launch_gram4_flush(uint8_t* D, int64_t n_pad, uint64_t ldd, uint32_t* dense_fill,
+                               int64_t* Cm, int64_t N, const int2* tiles, int ntiles,
+                               int sm_count, unsigned long long* stats, cudaStream_t s,
+                               int64_t NA);
 cudaError_t launch_gram2_flush(uint8_t* D, int64_t n_pad, uint64_t ldd, uint32_t* dense_fill,
                                int64_t* Cm, int64_t N, const int2* tiles, int ntiles,
                                int sm_count, unsigned long long* stats, cudaStream_t s,

@@ -95,6 +95,7 @@ __global__ void __launch_bounds__(256) light_kernel(SegmentOut so, int64_t heavy
                                                     uint64_t ldd, uint32_t* dense_fill,
                                                     LightBins bn, uint32_t flat_max,
                                                     int64_t NA, const uint32_t* perm,
+                                                    uint32_t heavy_cmax,
                                                     unsigned long long* stats) {
     // triangle table: pairs (a < b < 32) ordered by b, so the first n(n-1)/2
     // entries are exactly the pairs of an n-triple chunk
@@ -181,7 +182,7 @@ __global__ void __launch_bounds__(256) light_kernel(SegmentOut so, int64_t heavy
                 uint32_t cmax = cA0;
                 for (uint32_t t = a0 + 32 + lane; t < b0; t += 32) cmax = max(cmax, so.tcnt[t]);
                 cmax = __reduce_max_sync(0xffffffffu, cmax);
-                if (cmax <= 255u) {
+                if (cmax <= heavy_cmax) {
                     // claim a column of the dense count matrix D; build_dense fills it
                     uint32_t col = 0;
                     if (lane == 0) col = atomicAdd(dense_fill, 1u);
@@ -241,14 +242,15 @@ __global__ void __launch_bounds__(256) light_kernel(SegmentOut so, int64_t heavy
 cudaError_t launch_light(SegmentOut so, uint64_t max_groups, int64_t heavy_min, int64_t N,
                          uint32_t* acc, uint2* heavy_list, uint64_t ldd,
                          uint32_t* dense_fill, LightBins bins, uint32_t flat_max,
-                         int64_t NA, const uint32_t* perm, unsigned long long* stats,
-                         int sm_count, cudaStream_t s) {
+                         int64_t NA, const uint32_t* perm, uint32_t heavy_cmax,
+                         unsigned long long* stats, int sm_count, cudaStream_t s) {
     if (max_groups == 0) return cudaGetLastError();
     uint64_t blocks = (max_groups + 255) / 256;  // 8 warps x 32 groups per block-round
     uint64_t cap = (uint64_t)sm_count * 8;
     if (blocks > cap) blocks = cap;
     light_kernel<<<(unsigned)blocks, 256, 0, s>>>(so, heavy_min, N, acc, heavy_list, ldd,
-                                                  dense_fill, bins, flat_max, NA, perm, stats);
+                                                  dense_fill, bins, flat_max, NA, perm,
+                                                  heavy_cmax, stats);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess || bins.nb == 0) return e;
     return launch_apply_bins(acc, bins, sm_count, s);

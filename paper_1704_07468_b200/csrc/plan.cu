@@ -85,6 +85,7 @@ struct gakco_plan {
     int gram_pair = 1;         // 1: CTA-pair Gram (gram2.cu), 0: one-SM Gram (gram_tc.cu)
     int light_flat = 8;        // light groups of <= this many sequences share warps
     int light_relabel = -1;    // -1 auto (accumulator >> L2), 0 off, 1 on
+    int gram_fp4 = -1;         // -1 auto (e2m1 Gram when exact), 0 u8 / kind::i8, 1 e2m1
     int sm_count = 148;
     std::string err;
 
@@ -305,6 +306,10 @@ extern "C" gakco_status gakco_set_option(gakco_plan* p, int option, int64_t valu
             if (value < -1 || value > 1) return p->fail(GAKCO_E_ARG, "relabel must be -1..1");
             p->light_relabel = (int)value;
             return GAKCO_OK;
+        case GAKCO_OPT_GRAM_FP4:
+            if (value < -1 || value > 1) return p->fail(GAKCO_E_ARG, "gram fp4 must be -1..1");
+            p->gram_fp4 = (int)value;
+            return GAKCO_OK;
         case GAKCO_OPT_TIMING:
             p->timing = value != 0;
             return GAKCO_OK;
@@ -453,8 +458,16 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
     const bool rect = NA > 0;
     const bool gpair = p->gram_pair || rect;
     const int64_t n_pad = gpair ? (N + 511) / 512 * 512 : (N + 255) / 256 * 256;
+    // e2m1 Gram (kind::mxf4, gram2.cu): counts <= 4 exact in e2m1, f32 sums exact
+    // below 2^24, so it applies while one mask's n_max^2 stays below 2^24; groups
+    // with a count > 4 stay on the light path
+    const bool fp4 = gpair && p->gram_fp4 != 0 && nmax > 0 &&
+                     (uint64_t)nmax * (uint64_t)nmax < (1ull << 24);
+    const uint64_t exact_lim = fp4 ? (1ull << 24) - 1 : (uint64_t)INT32_MAX;
+    const uint64_t slab_cols = fp4 ? 256 : 128;
     int64_t heavy_min = p->heavy_min;
-    if (heavy_min == 0) heavy_min = std::max<int64_t>(16, (int64_t)(0.012 * (double)n_pad + 0.999));
+    if (heavy_min == 0)
+        heavy_min = std::max<int64_t>(16, (int64_t)((fp4 ? 0.008 : 0.012) * (double)n_pad + 0.999));
     const bool heavy_on = heavy_min < (int64_t)1 << 40 && N >= 2;
 
     // batch size (keys cap; with the Gram on, s32 exactness: masks * n_max^2 < 2^31)
@@ -465,7 +478,7 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
     if (bk > (1ull << 30) - 1) bk = (1ull << 30) - 1;
     uint64_t bmax_masks = std::max<uint64_t>(1, n ? bk / n : mine.size());
     if (heavy_on && nmax > 0) {
-        uint64_t lim = (uint64_t)(INT32_MAX / ((uint64_t)nmax * (uint64_t)nmax));
+        uint64_t lim = exact_lim / ((uint64_t)nmax * (uint64_t)nmax);
         bmax_masks = std::max<uint64_t>(1, std::min(bmax_masks, lim));
     }
     // a single mask whose n_max^2 exceeds 2^31 would need the light path only
@@ -541,14 +554,15 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
         // (every batch rounds its columns up to whole 128-column slabs)
         const uint64_t most =
             (uint64_t)mine.size() * n / (uint64_t)heavy_min + 128 * (mine.size() + 1);
-        rcap = std::min<uint64_t>((4096ull << 20) / (uint64_t)n_pad, most);
-        rcap = std::max<uint64_t>(128, (rcap + 127) / 128 * 128);
-        CK(p->ensure(p->dense, (size_t)n_pad * rcap, s));
+        rcap = std::min<uint64_t>((4096ull << 20) * (fp4 ? 2 : 1) / (uint64_t)n_pad, most);
+        rcap = std::max<uint64_t>(slab_cols, (rcap + slab_cols - 1) / slab_cols * slab_cols);
+        CK(p->ensure(p->dense, (size_t)n_pad * rcap / (fp4 ? 2 : 1), s));
         CK(p->ensure(p->heavy, rcap * sizeof(uint2), s));
-        const int tkey = rect ? 2 : (gpair ? 1 : 0);
+        const int tkey = (rect ? 2 : (gpair ? 1 : 0)) + (fp4 ? 4 : 0);
         if (p->tiles_npad != n_pad || p->tiles_pair != tkey || (rect && p->tiles_na != NA)) {
-            std::vector<int2> t = rect ? gram2_tiles_rect(NA, N - NA)
-                                       : (gpair ? gram2_tiles(n_pad) : gram_tiles(n_pad));
+            std::vector<int2> t = fp4 ? (rect ? gram4_tiles_rect(NA, N - NA) : gram4_tiles(n_pad))
+                                  : rect ? gram2_tiles_rect(NA, N - NA)
+                                         : (gpair ? gram2_tiles(n_pad) : gram_tiles(n_pad));
             CK(p->ensure(p->tiles, t.size() * sizeof(int2), s));
             CK(cudaMemcpyAsync(p->tiles.p, t.data(), t.size() * sizeof(int2),
                                cudaMemcpyHostToDevice, s));
@@ -587,13 +601,17 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
     uint64_t dense_bound = 0, dense_masks = 0;
     int dense_m = -1;
     const uint64_t mask_lim =
-        gram_ok ? std::max<uint64_t>(1, (uint64_t)INT32_MAX / ((uint64_t)nmax * nmax)) : 0;
+        gram_ok ? std::max<uint64_t>(1, exact_lim / ((uint64_t)nmax * nmax)) : 0;
     auto flush = [&]() -> gakco_status {
         if (dense_m < 0 || dense_bound == 0) return GAKCO_OK;
         cudaEvent_t ah = nullptr;
         p->stage_begin(s, &ah);
         p->launches += 1;  // + fill_reset
-        if (gpair)
+        if (fp4)
+            LK(launch_gram4_flush((uint8_t*)p->dense.p, n_pad, rcap, (uint32_t*)p->hcount.p,
+                                  level_ptr(dense_m), N, (const int2*)p->tiles.p, p->ntiles,
+                                  p->sm_count, stats, s, NA));
+        else if (gpair)
             LK(launch_gram2_flush((uint8_t*)p->dense.p, n_pad, rcap, (uint32_t*)p->hcount.p,
                                   level_ptr(dense_m), N, (const int2*)p->tiles.p, p->ntiles,
                                   p->sm_count, stats, s, NA));
@@ -704,7 +722,7 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
         int64_t* Dm = diag_ptr(m);  // C_m(X,X) at Dm[X * dstride]
         cudaEvent_t a = nullptr;
         if (gram_ok && n > 0) {
-            const uint64_t bnd = (uint64_t)nmask * n / (uint64_t)heavy_min + 128;
+            const uint64_t bnd = (uint64_t)nmask * n / (uint64_t)heavy_min + slab_cols;
             if (dense_m != m || dense_bound + bnd > rcap || dense_masks + nmask > mask_lim) {
                 gakco_status fs = flush();
                 if (fs != GAKCO_OK) return fs;
@@ -815,14 +833,15 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
             LK(launch_light(so, n * nmask / 2 + 1, light_limit, N, (uint32_t*)p->lightacc.p,
                             (uint2*)p->heavy.p, rcap, (uint32_t*)p->hcount.p, bins,
                             (uint32_t)p->light_flat, NA,
-                            perm_active ? (const uint32_t*)p->perm.p : nullptr, stats,
-                            p->sm_count, s));
+                            perm_active ? (const uint32_t*)p->perm.p : nullptr,
+                            fp4 ? 4u : 255u, stats, p->sm_count, s));
             p->stage_end(s, S_LIGHT, a);
             if (gram_ok) {
                 p->stage_begin(s, &a);
                 p->launches += 1;  // + fill_round
                 LK(launch_build_dense(so, (const uint2*)p->heavy.p, (uint32_t*)p->hcount.p,
                                       (uint8_t*)p->dense.p, n_pad, rcap, hash_mode ? 0 : 1,
+                                      fp4 ? 1 : 0,
                                       p->sm_count, s));
                 p->stage_end(s, S_DENSE, a);
             }
@@ -845,6 +864,7 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
     p->host_stats.sort_passes32 = passkeys32;
     p->host_stats.grouping = p->last_grouping;
     p->host_stats.n_pad = gram_ok ? n_pad : 0;
+    p->host_stats.gram_fp4 = gram_ok && fp4 ? 1 : 0;
     p->after_accumulate = true;
     return GAKCO_OK;
 #undef CK

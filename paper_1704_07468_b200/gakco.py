@@ -36,6 +36,7 @@ GAKCO_OPT_LIGHT_BINS = 6
 GAKCO_OPT_GRAM_PAIR = 7
 GAKCO_OPT_LIGHT_FLAT = 8
 GAKCO_OPT_LIGHT_RELABEL = 9
+GAKCO_OPT_GRAM_FP4 = 10
 
 EXPORTS = ("gakco_create", "gakco_set_shard", "gakco_set_option", "gakco_accumulate",
            "gakco_finalize", "gakco_kernel", "gakco_kernel_k", "gakco_kernel_rect",
@@ -51,7 +52,7 @@ class gakco_stats(ctypes.Structure):
         (n, ctypes.c_int64) for n in (
             "n_encode", "n_sort", "n_segment", "n_light", "n_heavy", "n_epilogue", "keys32",
             "sort_passes32", "grouping")] + [("ms_dense", ctypes.c_double)] + [
-        (n, ctypes.c_int64) for n in ("n_dense", "n_pad")]
+        (n, ctypes.c_int64) for n in ("n_dense", "n_pad", "gram_fp4")]
 
     def as_dict(self):
         return {n: getattr(self, n) for n, _ in self._fields_}

@@ -107,6 +107,8 @@ def test_heavy_light_equivalence(gk, oracle_lib):
         heavy = run(gk, cp, g, k, M, heavy_min_seqs=2)
         assert_parity(heavy, ref)
         assert_parity(run(gk, cp, g, k, M, heavy_min_seqs=2, gram_pair=0), ref)
+        assert_parity(run(gk, cp, g, k, M, heavy_min_seqs=2, gram_fp4=0), ref)
+        assert_parity(run(gk, cp, g, k, M, heavy_min_seqs=2, gram_fp4=1), ref)
         assert_parity(run(gk, cp, g, k, M, heavy_min_seqs=1 << 50), ref)
         assert_parity(run(gk, cp, g, k, M), ref)
 
@@ -486,6 +488,7 @@ def test_rect_train_test(gk, oracle_lib):
         ref = oracle_lib.rect(cp, NA, g, k, M)
         _assert_rect(_run_rect(gk, cp, NA, g, k, M), ref)
         _assert_rect(_run_rect(gk, cp, NA, g, k, M, heavy_min_seqs=2), ref)
+        _assert_rect(_run_rect(gk, cp, NA, g, k, M, heavy_min_seqs=2, gram_fp4=0), ref)
         _assert_rect(_run_rect(gk, cp, NA, g, k, M, heavy_min_seqs=1 << 50), ref)
 
 
