@@ -81,11 +81,14 @@ typedef enum {
     GAKCO_OPT_LIGHT_RELABEL = 9,  /* light accumulator sequence relabelling (locality; results
                                      unchanged): -1 = automatic (default: when the packed
                                      triangle exceeds 96 MB), 0 = off, 1 = on */
-    GAKCO_OPT_GRAM_FP4 = 10       /* heavy-group Gram operands: -1 = automatic (default: e2m1
+    GAKCO_OPT_GRAM_FP4 = 10,      /* heavy-group Gram operands: -1 = automatic (default: e2m1
                                      counts, kind::mxf4 block-scaled with unit scales, when one
                                      mask's n_max^2 < 2^24 keeps the f32 sums exact; groups
                                      with a count > 4 stay light), 0 = u8 (kind::i8), 1 = e2m1
                                      where exact */
+    GAKCO_OPT_PIPELINE = 11       /* 1 (default): light updates, dense build and Gram of batch b
+                                     run on a second stream while batch b+1 is encoded, sorted
+                                     and segmented (double-buffered triples); 0: one stream */
 } gakco_option;
 
 /* Counters of the last gakco_accumulate (algorithmic units). */

@@ -86,6 +86,11 @@ struct gakco_plan {
     int light_flat = 8;        // light groups of <= this many sequences share warps
     int light_relabel = -1;    // -1 auto (accumulator >> L2), 0 off, 1 on
     int gram_fp4 = -1;         // -1 auto (e2m1 Gram when exact), 0 u8 / kind::i8, 1 e2m1
+    int pipeline = 1;          // light / dense / Gram of batch b on an aux stream, overlapping
+                               // encode / sort / segment of batch b+1 (double-buffered triples)
+    cudaStream_t aux = nullptr;
+    cudaEvent_t ev_seg[2] = {nullptr, nullptr}, ev_light[2] = {nullptr, nullptr},
+                ev_join = nullptr;
     int sm_count = 148;
     std::string err;
 
@@ -94,7 +99,7 @@ struct gakco_plan {
     std::vector<std::array<uint8_t, GMAX>> mask_kept;
     std::vector<int> key_bits;  // per level
 
-    DevBuf perm, iota, best, parent, Dgscr, Kdscr, codes, off, gofs, gmseq, keysA, keysB, hist, status, ctr, tseq, tcnt, gstart, gend,
+    DevBuf tseq2, tcnt2, gstart2, counts2, perm, iota, best, parent, Dgscr, Kdscr, codes, off, gofs, gmseq, keysA, keysB, hist, status, ctr, tseq, tcnt, gstart, gend,
         counts, kept, stats, flags, kdiag, Cscr, Nmscr, Kscr, Knscr, heavy, hcount, dense, tiles,
         lightacc, binrec, bincnt, win, bkH, bktot, bkbase, bkdesc, bktab, bktcnt, bkgs, bkocc;
     int64_t tiles_npad = -1;
@@ -252,7 +257,7 @@ extern "C" gakco_status gakco_create(int sigma, int g, int k, int M, int device,
 extern "C" void gakco_destroy(gakco_plan* p) {
     if (!p) return;
     DeviceGuard dg(p->device);
-    DevBuf* bufs[] = {&p->perm, &p->iota, &p->best, &p->parent, &p->Dgscr, &p->Kdscr, &p->codes, &p->off,   &p->gofs,  &p->gmseq,  &p->keysA, &p->keysB,
+    DevBuf* bufs[] = {&p->tseq2, &p->tcnt2, &p->gstart2, &p->counts2, &p->perm, &p->iota, &p->best, &p->parent, &p->Dgscr, &p->Kdscr, &p->codes, &p->off,   &p->gofs,  &p->gmseq,  &p->keysA, &p->keysB,
                       &p->hist,  &p->status, &p->ctr,  &p->tseq,   &p->tcnt,  &p->gstart,
                       &p->gend,  &p->counts, &p->kept, &p->stats,  &p->flags, &p->kdiag,
                       &p->Cscr,  &p->Nmscr, &p->Kscr,  &p->Knscr, &p->heavy, &p->hcount,
@@ -262,6 +267,9 @@ extern "C" void gakco_destroy(gakco_plan* p) {
     for (DevBuf* b : bufs)
         if (b->p) cudaFree(b->p);
     for (cudaEvent_t e : p->ev_pool) cudaEventDestroy(e);
+    for (cudaEvent_t e : {p->ev_seg[0], p->ev_seg[1], p->ev_light[0], p->ev_light[1], p->ev_join})
+        if (e) cudaEventDestroy(e);
+    if (p->aux) cudaStreamDestroy(p->aux);
     delete p;
 }
 
@@ -309,6 +317,10 @@ extern "C" gakco_status gakco_set_option(gakco_plan* p, int option, int64_t valu
         case GAKCO_OPT_GRAM_FP4:
             if (value < -1 || value > 1) return p->fail(GAKCO_E_ARG, "gram fp4 must be -1..1");
             p->gram_fp4 = (int)value;
+            return GAKCO_OK;
+        case GAKCO_OPT_PIPELINE:
+            if (value < 0 || value > 1) return p->fail(GAKCO_E_ARG, "pipeline must be 0 or 1");
+            p->pipeline = (int)value;
             return GAKCO_OK;
         case GAKCO_OPT_TIMING:
             p->timing = value != 0;
@@ -491,6 +503,24 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
     CK(p->ensure(p->tcnt, cap_keys * 4, s));
     CK(p->ensure(p->gstart, (cap_keys / 2 + 2) * sizeof(uint2), s));  // group ranges
     CK(p->ensure(p->counts, 16, s));
+    // two-stream pipeline: light / dense / Gram on `s2` consume batch b's triples while
+    // `s` encodes, sorts and segments batch b+1 into the other triple buffer
+    const bool pipe = p->pipeline != 0;
+    if (pipe) {
+        CK(p->ensure(p->tseq2, cap_keys * 4, s));
+        CK(p->ensure(p->tcnt2, cap_keys * 4, s));
+        CK(p->ensure(p->gstart2, (cap_keys / 2 + 2) * sizeof(uint2), s));
+        CK(p->ensure(p->counts2, 16, s));
+        if (!p->aux) {
+            CK(cudaStreamCreateWithFlags(&p->aux, cudaStreamNonBlocking));
+            for (int i = 0; i < 2; ++i) {
+                CK(cudaEventCreateWithFlags(&p->ev_seg[i], cudaEventDisableTiming));
+                CK(cudaEventCreateWithFlags(&p->ev_light[i], cudaEventDisableTiming));
+            }
+            CK(cudaEventCreateWithFlags(&p->ev_join, cudaEventDisableTiming));
+        }
+    }
+    cudaStream_t s2 = pipe ? p->aux : s;
     CK(p->ensure(p->hist, std::max<uint64_t>(std::min<uint64_t>(bmax_masks, mine.size() + 1) *
                                                  MAXPASS * RADIX * 4,
                                              (uint64_t)(p->sort_ctas_per_sm * p->sm_count + 64 +
@@ -575,8 +605,12 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
     }
     CorpusView cv{(const uint8_t*)p->codes.p, (const int64_t*)p->off.p, (const int64_t*)p->gofs.p,
                   (const uint32_t*)p->gmseq.p, N, n};
-    SegmentOut so{(uint32_t*)p->tseq.p, (uint32_t*)p->tcnt.p, (uint2*)p->gstart.p,
-                  (uint32_t*)p->counts.p};
+    SegmentOut so1{(uint32_t*)p->tseq.p, (uint32_t*)p->tcnt.p, (uint2*)p->gstart.p,
+                   (uint32_t*)p->counts.p};
+    SegmentOut so2 = pipe ? SegmentOut{(uint32_t*)p->tseq2.p, (uint32_t*)p->tcnt2.p,
+                                       (uint2*)p->gstart2.p, (uint32_t*)p->counts2.p}
+                          : so1;
+    int64_t batch_no = 0;
     int64_t passkeys = 0, keys32 = 0, passkeys32 = 0;
     if (hash_mode) {
         cudaEvent_t a0 = nullptr;
@@ -605,21 +639,21 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
     auto flush = [&]() -> gakco_status {
         if (dense_m < 0 || dense_bound == 0) return GAKCO_OK;
         cudaEvent_t ah = nullptr;
-        p->stage_begin(s, &ah);
+        p->stage_begin(s2, &ah);
         p->launches += 1;  // + fill_reset
         if (fp4)
             LK(launch_gram4_flush((uint8_t*)p->dense.p, n_pad, rcap, (uint32_t*)p->hcount.p,
                                   level_ptr(dense_m), N, (const int2*)p->tiles.p, p->ntiles,
-                                  p->sm_count, stats, s, NA));
+                                  p->sm_count, stats, s2, NA));
         else if (gpair)
             LK(launch_gram2_flush((uint8_t*)p->dense.p, n_pad, rcap, (uint32_t*)p->hcount.p,
                                   level_ptr(dense_m), N, (const int2*)p->tiles.p, p->ntiles,
-                                  p->sm_count, stats, s, NA));
+                                  p->sm_count, stats, s2, NA));
         else
             LK(launch_gram_flush((uint8_t*)p->dense.p, n_pad, rcap, (uint32_t*)p->hcount.p,
                                  level_ptr(dense_m), N, (const int2*)p->tiles.p, p->ntiles,
-                                 p->sm_count, stats, s));
-        p->stage_end(s, S_HEAVY, ah);
+                                 p->sm_count, stats, s2));
+        p->stage_end(s2, S_HEAVY, ah);
         dense_bound = 0;
         dense_masks = 0;
         return GAKCO_OK;
@@ -669,6 +703,7 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
         CK(cudaStreamSynchronize(s));  // io is a local buffer
     }
     auto make_perm = [&](int m_done) -> gakco_status {
+        CK(cudaStreamSynchronize(s2));  // C of level m_done complete (light + Gram flushes)
         cudaEvent_t ar = nullptr;
         p->stage_begin(s, &ar);
         p->launches += 3;
@@ -695,21 +730,25 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
     auto lflush = [&]() -> gakco_status {
         if (light_m < 0 || light_masks == 0) return GAKCO_OK;
         cudaEvent_t al = nullptr;
-        p->stage_begin(s, &al);
+        p->stage_begin(s2, &al);
         if (rect)
             LK(launch_light_flush_rect((uint32_t*)p->lightacc.p, ntri, level_ptr(light_m),
-                                       p->sm_count, s));
+                                       p->sm_count, s2));
         else if (perm_active)
             LK(launch_light_flush_perm((uint32_t*)p->lightacc.p, N, level_ptr(light_m),
-                                       (const uint32_t*)p->perm.p, p->sm_count, s));
+                                       (const uint32_t*)p->perm.p, p->sm_count, s2));
         else
             LK(launch_light_flush((uint32_t*)p->lightacc.p, N, level_ptr(light_m), p->sm_count,
-                                  s));
-        p->stage_end(s, S_LIGHT, al);
+                                  s2));
+        p->stage_end(s2, S_LIGHT, al);
         light_masks = 0;
         return GAKCO_OK;
     };
 
+    if (pipe) {  // everything enqueued on s so far (uploads, zeroing) precedes s2's work
+        CK(cudaEventRecord(p->ev_join, s));
+        CK(cudaStreamWaitEvent(s2, p->ev_join, 0));
+    }
     size_t pos = 0;
     while (pos < mine.size()) {
         const int m = p->mask_level[mine[pos]];
@@ -747,6 +786,13 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
             light_masks += nmask;
         }
 
+        // triple buffer of this batch; its previous user (batch_no - 2) must be done
+        const int bi = (int)(batch_no & 1);
+        const SegmentOut so = bi ? so2 : so1;
+        auto wait_buf = [&]() -> gakco_status {
+            if (pipe && batch_no >= 2) CK(cudaStreamWaitEvent(s, p->ev_light[bi], 0));
+            return GAKCO_OK;
+        };
         if (n > 0 && hash_mode) {
             // hash partition: count -> (column / bucket scans + scatter) -> group
             const bool k64 = (level_runs[m] ? (g - m) * bits : kb) + sbh > 32;
@@ -784,6 +830,10 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
             p->stage_begin(s, &a);
             BkScratch bs{(uint64_t*)p->bktab.p, (uint32_t*)p->bktcnt.p, (uint32_t*)p->bkgs.p,
                          (uint32_t*)p->bkocc.p};
+            {
+                gakco_status ws = wait_buf();
+                if (ws != GAKCO_OK) return ws;
+            }
             LK(launch_bucket_group(ba, p->keysA.p, k64, dstride, Dm, so, bs, stats, p->sm_count,
                                    s));
             p->stage_end(s, S_SEGMENT, a);
@@ -823,28 +873,38 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
             }
             p->stage_end(s, S_SORT, a);
 
+            {
+                gakco_status ws = wait_buf();
+                if (ws != GAKCO_OK) return ws;
+            }
             p->stage_begin(s, &a);
             LK(launch_segment(in, k64, n, nmask, sb, dstride, Dm, so.counts, so, stats, s));
             p->stage_end(s, S_SEGMENT, a);
 
         }
         if (n > 0) {
-            p->stage_begin(s, &a);
+            // light and dense build of this batch on s2, after its segment on s
+            if (pipe) {
+                CK(cudaEventRecord(p->ev_seg[bi], s));
+                CK(cudaStreamWaitEvent(s2, p->ev_seg[bi], 0));
+            }
+            p->stage_begin(s2, &a);
             LK(launch_light(so, n * nmask / 2 + 1, light_limit, N, (uint32_t*)p->lightacc.p,
                             (uint2*)p->heavy.p, rcap, (uint32_t*)p->hcount.p, bins,
                             (uint32_t)p->light_flat, NA,
                             perm_active ? (const uint32_t*)p->perm.p : nullptr,
-                            fp4 ? 4u : 255u, stats, p->sm_count, s));
-            p->stage_end(s, S_LIGHT, a);
+                            fp4 ? 4u : 255u, stats, p->sm_count, s2));
+            p->stage_end(s2, S_LIGHT, a);
             if (gram_ok) {
-                p->stage_begin(s, &a);
+                p->stage_begin(s2, &a);
                 p->launches += 1;  // + fill_round
                 LK(launch_build_dense(so, (const uint2*)p->heavy.p, (uint32_t*)p->hcount.p,
                                       (uint8_t*)p->dense.p, n_pad, rcap, hash_mode ? 0 : 1,
-                                      fp4 ? 1 : 0,
-                                      p->sm_count, s));
-                p->stage_end(s, S_DENSE, a);
+                                      fp4 ? 1 : 0, p->sm_count, s2));
+                p->stage_end(s2, S_DENSE, a);
             }
+            if (pipe) CK(cudaEventRecord(p->ev_light[bi], s2));
+            ++batch_no;
         }
         LK(launch_diag_closed_form((const int64_t*)p->gofs.p, N, nmask, Dm, dstride, s));
         pos = end;
@@ -854,6 +914,10 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
         if (fs != GAKCO_OK) return fs;
         fs = lflush();
         if (fs != GAKCO_OK) return fs;
+    }
+    if (pipe) {  // the caller's stream sees every s2 kernel as done
+        CK(cudaEventRecord(p->ev_join, s2));
+        CK(cudaStreamWaitEvent(s, p->ev_join, 0));
     }
     p->last_masks = (int64_t)mine.size();
     p->host_stats = gakco_stats{};

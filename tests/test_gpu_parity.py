@@ -160,12 +160,15 @@ def test_light_binning(gk, oracle_lib):
 
 
 def test_batch_size_invariance(gk, oracle_lib):
-    """Different mask batch sizes give identical results (integer sums)."""
+    """Different mask batch sizes give identical results (integer sums), with the
+    two-stream batch pipeline (default) and on one stream."""
     cp = sc.make("tiny")
     ref = oracle_lib.compute(cp, 7, 5, 2)
     for bk in (1, 4700, 3 * 4700 + 5, 1 << 20):
         assert_parity(run(gk, cp, 7, 5, 2, batch_keys=bk), ref)
         assert_parity(run(gk, cp, 7, 5, 2, batch_keys=bk, sort=1), ref)
+        assert_parity(run(gk, cp, 7, 5, 2, batch_keys=bk, pipeline=0), ref)
+        assert_parity(run(gk, cp, 7, 5, 2, batch_keys=bk, heavy_min_seqs=2), ref)
 
 
 def test_sort_modes_ragged(gk, oracle_lib):
