@@ -264,8 +264,8 @@ __global__ void light_flush_kernel(uint32_t* __restrict__ acc, int64_t N, int64_
         int64_t* crow = Cm + x * N;
         for (int64_t y = x + 1 + threadIdx.x; y < N; y += blockDim.x) {
             const uint32_t v = row[y - x - 1];
-            if (v) {
-                crow[y] += v;
+            if (v) {  // atomic: a Gram flush of the same level may run on another stream
+                atomicAdd((unsigned long long*)&crow[y], (unsigned long long)v);
                 row[y - x - 1] = 0u;
             }
         }
@@ -284,7 +284,7 @@ __global__ void light_flush_perm_kernel(const uint32_t* __restrict__ acc, int64_
         for (int64_t y = x + 1 + threadIdx.x; y < N; y += blockDim.x) {
             const uint32_t py = perm[y];
             const uint32_t v = acc[tri_index(min(px, py), max(px, py), N)];
-            if (v) crow[y] += v;
+            if (v) atomicAdd((unsigned long long*)&crow[y], (unsigned long long)v);
         }
     }
 }
@@ -380,7 +380,7 @@ __global__ void light_flush_rect_kernel(uint32_t* __restrict__ acc, uint64_t cel
          i += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t v = acc[i];
         if (v) {
-            Cm[i] += v;
+            atomicAdd((unsigned long long*)&Cm[i], (unsigned long long)v);
             acc[i] = 0u;
         }
     }

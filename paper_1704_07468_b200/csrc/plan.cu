@@ -88,9 +88,10 @@ struct gakco_plan {
     int gram_fp4 = -1;         // -1 auto (e2m1 Gram when exact), 0 u8 / kind::i8, 1 e2m1
     int pipeline = 1;          // light / dense / Gram of batch b on an aux stream, overlapping
                                // encode / sort / segment of batch b+1 (double-buffered triples)
-    cudaStream_t aux = nullptr;
+    cudaStream_t aux = nullptr, aux2 = nullptr;  // light + dense; Gram flushes
     cudaEvent_t ev_seg[2] = {nullptr, nullptr}, ev_light[2] = {nullptr, nullptr},
-                ev_join = nullptr;
+                ev_join = nullptr, ev_join2 = nullptr, ev_build = nullptr,
+                ev_gram[2] = {nullptr, nullptr};
     int sm_count = 148;
     std::string err;
 
@@ -99,7 +100,7 @@ struct gakco_plan {
     std::vector<std::array<uint8_t, GMAX>> mask_kept;
     std::vector<int> key_bits;  // per level
 
-    DevBuf tseq2, tcnt2, gstart2, counts2, perm, iota, best, parent, Dgscr, Kdscr, codes, off, gofs, gmseq, keysA, keysB, hist, status, ctr, tseq, tcnt, gstart, gend,
+    DevBuf dense2, heavy2, hcount2, tseq2, tcnt2, gstart2, counts2, perm, iota, best, parent, Dgscr, Kdscr, codes, off, gofs, gmseq, keysA, keysB, hist, status, ctr, tseq, tcnt, gstart, gend,
         counts, kept, stats, flags, kdiag, Cscr, Nmscr, Kscr, Knscr, heavy, hcount, dense, tiles,
         lightacc, binrec, bincnt, win, bkH, bktot, bkbase, bkdesc, bktab, bktcnt, bkgs, bkocc;
     int64_t tiles_npad = -1;
@@ -257,7 +258,7 @@ extern "C" gakco_status gakco_create(int sigma, int g, int k, int M, int device,
 extern "C" void gakco_destroy(gakco_plan* p) {
     if (!p) return;
     DeviceGuard dg(p->device);
-    DevBuf* bufs[] = {&p->tseq2, &p->tcnt2, &p->gstart2, &p->counts2, &p->perm, &p->iota, &p->best, &p->parent, &p->Dgscr, &p->Kdscr, &p->codes, &p->off,   &p->gofs,  &p->gmseq,  &p->keysA, &p->keysB,
+    DevBuf* bufs[] = {&p->dense2, &p->heavy2, &p->hcount2, &p->tseq2, &p->tcnt2, &p->gstart2, &p->counts2, &p->perm, &p->iota, &p->best, &p->parent, &p->Dgscr, &p->Kdscr, &p->codes, &p->off,   &p->gofs,  &p->gmseq,  &p->keysA, &p->keysB,
                       &p->hist,  &p->status, &p->ctr,  &p->tseq,   &p->tcnt,  &p->gstart,
                       &p->gend,  &p->counts, &p->kept, &p->stats,  &p->flags, &p->kdiag,
                       &p->Cscr,  &p->Nmscr, &p->Kscr,  &p->Knscr, &p->heavy, &p->hcount,
@@ -267,9 +268,11 @@ extern "C" void gakco_destroy(gakco_plan* p) {
     for (DevBuf* b : bufs)
         if (b->p) cudaFree(b->p);
     for (cudaEvent_t e : p->ev_pool) cudaEventDestroy(e);
-    for (cudaEvent_t e : {p->ev_seg[0], p->ev_seg[1], p->ev_light[0], p->ev_light[1], p->ev_join})
+    for (cudaEvent_t e : {p->ev_seg[0], p->ev_seg[1], p->ev_light[0], p->ev_light[1], p->ev_join,
+                          p->ev_join2, p->ev_build, p->ev_gram[0], p->ev_gram[1]})
         if (e) cudaEventDestroy(e);
     if (p->aux) cudaStreamDestroy(p->aux);
+    if (p->aux2) cudaStreamDestroy(p->aux2);
     delete p;
 }
 
@@ -513,14 +516,21 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
         CK(p->ensure(p->counts2, 16, s));
         if (!p->aux) {
             CK(cudaStreamCreateWithFlags(&p->aux, cudaStreamNonBlocking));
+            CK(cudaStreamCreateWithFlags(&p->aux2, cudaStreamNonBlocking));
             for (int i = 0; i < 2; ++i) {
                 CK(cudaEventCreateWithFlags(&p->ev_seg[i], cudaEventDisableTiming));
                 CK(cudaEventCreateWithFlags(&p->ev_light[i], cudaEventDisableTiming));
+                CK(cudaEventCreateWithFlags(&p->ev_gram[i], cudaEventDisableTiming));
             }
             CK(cudaEventCreateWithFlags(&p->ev_join, cudaEventDisableTiming));
+            CK(cudaEventCreateWithFlags(&p->ev_join2, cudaEventDisableTiming));
+            CK(cudaEventCreateWithFlags(&p->ev_build, cudaEventDisableTiming));
         }
     }
     cudaStream_t s2 = pipe ? p->aux : s;
+    // Gram flushes on s3 (tensor pipe), concurrent with the next columns' light
+    // updates and dense build on s2 (L2 atomics / stores) into the other D slot
+    cudaStream_t s3 = pipe ? p->aux2 : s;
     CK(p->ensure(p->hist, std::max<uint64_t>(std::min<uint64_t>(bmax_masks, mine.size() + 1) *
                                                  MAXPASS * RADIX * 4,
                                              (uint64_t)(p->sort_ctas_per_sm * p->sm_count + 64 +
@@ -579,6 +589,7 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
     uint64_t rcap = 0;
     if (gram_ok) {
         CK(p->ensure(p->hcount, 16, s, /*zero=*/true));
+        if (pipe) CK(p->ensure(p->hcount2, 16, s, /*zero=*/true));
         // dense count matrix D: n_pad rows x rcap u8 columns (<= 4 GB, and no more
         // columns than heavy groups can exist), accumulated over batches of a level
         // (every batch rounds its columns up to whole 128-column slabs)
@@ -588,6 +599,10 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
         rcap = std::max<uint64_t>(slab_cols, (rcap + slab_cols - 1) / slab_cols * slab_cols);
         CK(p->ensure(p->dense, (size_t)n_pad * rcap / (fp4 ? 2 : 1), s));
         CK(p->ensure(p->heavy, rcap * sizeof(uint2), s));
+        if (pipe) {
+            CK(p->ensure(p->dense2, (size_t)n_pad * rcap / (fp4 ? 2 : 1), s));
+            CK(p->ensure(p->heavy2, rcap * sizeof(uint2), s));
+        }
         const int tkey = (rect ? 2 : (gpair ? 1 : 0)) + (fp4 ? 4 : 0);
         if (p->tiles_npad != n_pad || p->tiles_pair != tkey || (rect && p->tiles_na != NA)) {
             std::vector<int2> t = fp4 ? (rect ? gram4_tiles_rect(NA, N - NA) : gram4_tiles(n_pad))
@@ -634,26 +649,39 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
     // so no host read-back is needed), or when the s32 sums could reach 2^31.
     uint64_t dense_bound = 0, dense_masks = 0;
     int dense_m = -1;
+    // D slot being filled (the Gram of the other slot may still be running on s3)
+    int dslot = 0;
+    bool slot_used[2] = {false, false};
+    auto dense_p = [&]() { return (uint8_t*)(dslot ? p->dense2.p : p->dense.p); };
+    auto heavy_p = [&]() { return (uint2*)(dslot ? p->heavy2.p : p->heavy.p); };
+    auto hcount_p = [&]() { return (uint32_t*)(dslot ? p->hcount2.p : p->hcount.p); };
     const uint64_t mask_lim =
         gram_ok ? std::max<uint64_t>(1, exact_lim / ((uint64_t)nmax * nmax)) : 0;
     auto flush = [&]() -> gakco_status {
         if (dense_m < 0 || dense_bound == 0) return GAKCO_OK;
+        if (pipe) {  // every build of this slot (s2) precedes its Gram (s3)
+            CK(cudaEventRecord(p->ev_build, s2));
+            CK(cudaStreamWaitEvent(s3, p->ev_build, 0));
+        }
         cudaEvent_t ah = nullptr;
-        p->stage_begin(s2, &ah);
+        p->stage_begin(s3, &ah);
         p->launches += 1;  // + fill_reset
         if (fp4)
-            LK(launch_gram4_flush((uint8_t*)p->dense.p, n_pad, rcap, (uint32_t*)p->hcount.p,
-                                  level_ptr(dense_m), N, (const int2*)p->tiles.p, p->ntiles,
-                                  p->sm_count, stats, s2, NA));
+            LK(launch_gram4_flush(dense_p(), n_pad, rcap, hcount_p(), level_ptr(dense_m), N,
+                                  (const int2*)p->tiles.p, p->ntiles, p->sm_count, stats, s3, NA));
         else if (gpair)
-            LK(launch_gram2_flush((uint8_t*)p->dense.p, n_pad, rcap, (uint32_t*)p->hcount.p,
-                                  level_ptr(dense_m), N, (const int2*)p->tiles.p, p->ntiles,
-                                  p->sm_count, stats, s2, NA));
+            LK(launch_gram2_flush(dense_p(), n_pad, rcap, hcount_p(), level_ptr(dense_m), N,
+                                  (const int2*)p->tiles.p, p->ntiles, p->sm_count, stats, s3, NA));
         else
-            LK(launch_gram_flush((uint8_t*)p->dense.p, n_pad, rcap, (uint32_t*)p->hcount.p,
-                                 level_ptr(dense_m), N, (const int2*)p->tiles.p, p->ntiles,
-                                 p->sm_count, stats, s2));
-        p->stage_end(s2, S_HEAVY, ah);
+            LK(launch_gram_flush(dense_p(), n_pad, rcap, hcount_p(), level_ptr(dense_m), N,
+                                 (const int2*)p->tiles.p, p->ntiles, p->sm_count, stats, s3));
+        p->stage_end(s3, S_HEAVY, ah);
+        if (pipe) {  // switch D slots; the next user of the other slot waits for its Gram
+            CK(cudaEventRecord(p->ev_gram[dslot], s3));
+            slot_used[dslot] = true;
+            dslot ^= 1;
+            if (slot_used[dslot]) CK(cudaStreamWaitEvent(s2, p->ev_gram[dslot], 0));
+        }
         dense_bound = 0;
         dense_masks = 0;
         return GAKCO_OK;
@@ -704,6 +732,7 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
     }
     auto make_perm = [&](int m_done) -> gakco_status {
         CK(cudaStreamSynchronize(s2));  // C of level m_done complete (light + Gram flushes)
+        CK(cudaStreamSynchronize(s3));
         cudaEvent_t ar = nullptr;
         p->stage_begin(s, &ar);
         p->launches += 3;
@@ -745,9 +774,10 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
         return GAKCO_OK;
     };
 
-    if (pipe) {  // everything enqueued on s so far (uploads, zeroing) precedes s2's work
+    if (pipe) {  // everything enqueued on s so far (uploads, zeroing) precedes s2/s3 work
         CK(cudaEventRecord(p->ev_join, s));
         CK(cudaStreamWaitEvent(s2, p->ev_join, 0));
+        CK(cudaStreamWaitEvent(s3, p->ev_join, 0));
     }
     size_t pos = 0;
     while (pos < mine.size()) {
@@ -890,7 +920,7 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
             }
             p->stage_begin(s2, &a);
             LK(launch_light(so, n * nmask / 2 + 1, light_limit, N, (uint32_t*)p->lightacc.p,
-                            (uint2*)p->heavy.p, rcap, (uint32_t*)p->hcount.p, bins,
+                            heavy_p(), rcap, hcount_p(), bins,
                             (uint32_t)p->light_flat, NA,
                             perm_active ? (const uint32_t*)p->perm.p : nullptr,
                             fp4 ? 4u : 255u, stats, p->sm_count, s2));
@@ -898,8 +928,8 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
             if (gram_ok) {
                 p->stage_begin(s2, &a);
                 p->launches += 1;  // + fill_round
-                LK(launch_build_dense(so, (const uint2*)p->heavy.p, (uint32_t*)p->hcount.p,
-                                      (uint8_t*)p->dense.p, n_pad, rcap, hash_mode ? 0 : 1,
+                LK(launch_build_dense(so, heavy_p(), hcount_p(), dense_p(), n_pad, rcap,
+                                      hash_mode ? 0 : 1,
                                       fp4 ? 1 : 0, p->sm_count, s2));
                 p->stage_end(s2, S_DENSE, a);
             }
@@ -915,9 +945,11 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
         fs = lflush();
         if (fs != GAKCO_OK) return fs;
     }
-    if (pipe) {  // the caller's stream sees every s2 kernel as done
+    if (pipe) {  // the caller's stream sees every s2 / s3 kernel as done
         CK(cudaEventRecord(p->ev_join, s2));
         CK(cudaStreamWaitEvent(s, p->ev_join, 0));
+        CK(cudaEventRecord(p->ev_join2, s3));
+        CK(cudaStreamWaitEvent(s, p->ev_join2, 0));
     }
     p->last_masks = (int64_t)mine.size();
     p->host_stats = gakco_stats{};
