@@ -424,6 +424,86 @@ __global__ void __launch_bounds__(BD2_THREADS) build_dense2_kernel(
     }
 }
 
+// Build v3 (sorted triples, the sort path): one CTA per slab, walking its row
+// chunks in order. Each warp owns SC/16 columns and keeps, per column, a cursor into
+// the column's triples (ascending sequence): a row chunk consumes exactly the
+// triples below its end, so every triple is read once and a chunk costs one round
+// of loads for all the warp's columns (v2 re-brackets every (slab, chunk) item).
+template <bool FP4>
+__global__ void __launch_bounds__(BD2_THREADS) build_dense3_kernel(
+    SegmentOut so, const uint2* __restrict__ heavy_list, const uint32_t* fill,
+    uint8_t* __restrict__ D, int64_t n_pad, uint64_t ldd) {
+    extern __shared__ __align__(16) unsigned char sb[];  // [BD2_ROWS][128], swizzled words
+    constexpr uint32_t SC = FP4 ? 2 * GT_KB : GT_KB;     // columns per slab
+    constexpr int NW = BD2_THREADS / 32;
+    constexpr int CPW = SC / NW;                         // columns per warp (16 or 8)
+    const uint64_t f0 = fill[1];
+    const uint64_t f1 = min((uint64_t)fill[0], ldd);
+    if (f1 <= f0) return;
+    const uint64_t s0 = f0 / SC, s1 = (f1 + SC - 1) / SC;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (uint64_t slab = s0 + blockIdx.x; slab < s1; slab += gridDim.x) {
+        uint32_t cur[CPW], end[CPW];
+        {
+            const uint64_t col = slab * SC + warp + NW * (lane % CPW);
+            const uint2 bnd = (lane < CPW && col < f1) ? heavy_list[col] : make_uint2(0u, 0u);
+#pragma unroll
+            for (int j = 0; j < CPW; ++j) {
+                cur[j] = __shfl_sync(0xffffffffu, bnd.x, j);
+                end[j] = __shfl_sync(0xffffffffu, bnd.y, j);
+            }
+        }
+        for (int64_t r0 = 0; r0 < n_pad; r0 += BD2_ROWS) {
+            const uint32_t rows = (uint32_t)min((int64_t)BD2_ROWS, n_pad - r0);
+            const uint32_t rend = (uint32_t)r0 + rows;
+            for (uint32_t i = threadIdx.x; i < rows * (GT_KB / 16); i += BD2_THREADS)
+                ((uint4*)sb)[i] = make_uint4(0u, 0u, 0u, 0u);
+            __syncthreads();
+            bool more = true;
+            while (more) {  // usually one round: a column rarely has > 32 triples per chunk
+                uint32_t xv[CPW], cv[CPW];
+#pragma unroll
+                for (int j = 0; j < CPW; ++j) {
+                    const uint32_t t = cur[j] + lane;
+                    xv[j] = t < end[j] ? so.tseq[t] & 0x7fffffffu : 0xffffffffu;
+                    cv[j] = t < end[j] ? so.tcnt[t] : 0u;
+                }
+                more = false;
+#pragma unroll
+                for (int j = 0; j < CPW; ++j) {
+                    const bool in = xv[j] < rend;  // (>= r0: earlier triples were consumed)
+                    if (in) {
+                        const uint32_t cc = warp + NW * j;
+                        const uint32_t r = xv[j] - (uint32_t)r0;
+                        if (FP4) {
+                            uint32_t* wp = (uint32_t*)(sb + r * GT_KB) + ((cc >> 3) ^ (r & 31u));
+                            atomicOr(wp, e2m1_code(cv[j]) << (((cc >> 1) & 3u) * 8 + (cc & 1u) * 4));
+                        } else {
+                            sb[bd2_off(r, cc)] = (uint8_t)cv[j];
+                        }
+                    }
+                    const uint32_t used = __popc(__ballot_sync(0xffffffffu, in));
+                    cur[j] += used;
+                    more |= used == 32 && cur[j] < end[j];
+                }
+            }
+            __syncthreads();
+            uint4* dst = (uint4*)(D + (slab * (uint64_t)n_pad + (uint64_t)r0) * GT_KB);
+            for (uint32_t i = threadIdx.x; i < rows * (GT_KB / 16); i += BD2_THREADS) {
+                const uint32_t r = i >> 3, q = i & 7;
+                const uint32_t* w = (const uint32_t*)(sb + r * GT_KB);
+                uint4 v;
+                v.x = w[(4 * q + 0) ^ (r & 31u)];
+                v.y = w[(4 * q + 1) ^ (r & 31u)];
+                v.z = w[(4 * q + 2) ^ (r & 31u)];
+                v.w = w[(4 * q + 3) ^ (r & 31u)];
+                dst[i] = v;
+            }
+            __syncthreads();
+        }
+    }
+}
+
 // After a batch's build: fill rounded up to whole slabs (sc columns); the next batch
 // starts there.
 __global__ void fill_round_kernel(uint32_t* fill, uint64_t ldd, uint32_t sc) {
@@ -445,7 +525,19 @@ __global__ void fill_reset_kernel(uint32_t* fill, uint64_t ldd, uint64_t tile_ma
 cudaError_t launch_build_dense(SegmentOut so, const uint2* heavy_list, uint32_t* dense_fill,
                                uint8_t* D, int64_t n_pad, uint64_t ldd, int sorted, int fp4,
                                int sm_count, cudaStream_t s) {
-    if (fp4) {
+    if (sorted) {
+        if (fp4) {
+            cudaFuncSetAttribute(build_dense3_kernel<true>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)BD2_SMEM);
+            build_dense3_kernel<true><<<sm_count * 3, BD2_THREADS, BD2_SMEM, s>>>(
+                so, heavy_list, dense_fill, D, n_pad, ldd);
+        } else {
+            cudaFuncSetAttribute(build_dense3_kernel<false>,
+                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)BD2_SMEM);
+            build_dense3_kernel<false><<<sm_count * 3, BD2_THREADS, BD2_SMEM, s>>>(
+                so, heavy_list, dense_fill, D, n_pad, ldd);
+        }
+    } else if (fp4) {
         cudaFuncSetAttribute(build_dense2_kernel<true>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)BD2_SMEM);
         build_dense2_kernel<true><<<sm_count * 3, BD2_THREADS, BD2_SMEM, s>>>(
