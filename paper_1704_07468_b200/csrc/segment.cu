@@ -57,7 +57,10 @@ __global__ void __launch_bounds__(SEG_THREADS) segment_kernel(
 #pragma unroll
         for (int i = 0; i < SEG_ITEMS; ++i) cur[i] = base + i < total ? keys[base + i] : (K)0;
     }
-    const K prev = (base < total && base % n != 0) ? keys[base - 1] : (K)0;
+    // segment (mask) bounds of this thread's first item: one 64-bit division per
+    // thread; consecutive items cross at most one boundary each (n >= 1)
+    uint64_t seg_lo = base < total ? base / n * n : 0, seg_hi = seg_lo + n;
+    const K prev = (base < total && base != seg_lo) ? keys[base - 1] : (K)0;
 
     uint32_t th_bits = 0, gh_bits = 0, multi_bits = 0;
     uint32_t cnt[SEG_ITEMS];
@@ -68,11 +71,15 @@ __global__ void __launch_bounds__(SEG_THREADS) segment_kernel(
         const K p0 = i == 0 ? prev : cur[i - 1];
         cnt[i] = 0;
         if (idx >= total) continue;
-        const bool first = (idx % n) == 0;
+        if (idx >= seg_hi) {
+            seg_lo = seg_hi;
+            seg_hi += n;
+        }
+        const bool first = idx == seg_lo;
         if (!first && p0 == c0) continue;  // not a triple head
         const bool gh = first || (p0 >> sb) != (c0 >> sb);
         // run end j and the key that follows it
-        const uint64_t seg_end = (idx / n + 1) * n;
+        const uint64_t seg_end = seg_hi;
         uint64_t j = idx + 1;
         K nk = (K)~c0;
         bool found = false;
