@@ -40,7 +40,7 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
 
 // Exclusive scan of one value per thread over the first 256 threads of the block.
 // Must be reached by every thread of the block (threads >= 256 pass 0; their
-// result is meaningless). s_w: 8 words of shared scratch.
+// result is meaningless). s_w: 9 words of shared scratch.
 __device__ __forceinline__ uint32_t scan256_excl(uint32_t v, uint32_t* s_w, uint32_t* total = nullptr) {
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
     uint32_t inc = v;
@@ -51,12 +51,21 @@ __device__ __forceinline__ uint32_t scan256_excl(uint32_t v, uint32_t* s_w, uint
     }
     if (w < 8 && lane == 31) s_w[w] = inc;
     __syncthreads();
-    uint32_t wp = 0, tot = 0;
-    for (int i = 0; i < 8; ++i) {
-        if (i < w) wp += s_w[i];
-        tot += s_w[i];
+    if (w == 0) {  // exclusive prefix of the 8 warp totals (s_w[0..7]) and the total (s_w[8])
+        const uint32_t x = lane < 8 ? s_w[lane] : 0u;
+        uint32_t y = x;
+#pragma unroll
+        for (int o = 1; o < 8; o <<= 1) {
+            const uint32_t t = __shfl_up_sync(0xffffffffu, y, o);
+            if (lane >= o) y += t;
+        }
+        __syncwarp();
+        if (lane < 8) s_w[lane] = y - x;
+        if (lane == 7) s_w[8] = y;
     }
-    if (total) *total = tot;
+    __syncthreads();
+    const uint32_t wp = w < 8 ? s_w[w] : 0u;
+    if (total) *total = s_w[8];
     __syncthreads();
     return wp + inc - v;
 }

@@ -36,7 +36,7 @@ __global__ void __launch_bounds__(SORT_THREADS) onesweep_kernel(
     uint32_t(*s_whist)[RADIX] = (uint32_t(*)[RADIX])(s_goff + RADIX);     // [WARPS][RADIX]
     uint32_t* s_doff = &s_whist[WARPS][0];                                // [RADIX]
     uint32_t* s_w = s_doff + RADIX;                                       // [8]
-    uint32_t& s_tile = s_w[8];
+    uint32_t& s_tile = s_w[12];
 
     const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
     if (tid == 0) s_tile = atomicAdd(ctr, 1u);

@@ -28,7 +28,7 @@ template <typename K>
 __global__ void __launch_bounds__(SEG_THREADS) segment_kernel(
     const K* __restrict__ keys, uint64_t n, uint64_t total, int sb, int64_t dstride,
     int64_t* diag, uint32_t* counters, SegmentOut so, unsigned long long* stats) {
-    __shared__ uint32_t s_w[8];
+    __shared__ uint32_t s_w[16];
     __shared__ uint32_t s_gpos[SEG_TILE];
     __shared__ uint32_t s_first_gh, s_base_t, s_base_g, s_tail;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
