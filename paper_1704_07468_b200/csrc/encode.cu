@@ -83,6 +83,65 @@ __global__ void __launch_bounds__(256) encode_kernel(CorpusView cv, const uint8_
     }
 }
 
+// Encode from packed g-mer windows (bucket.cu's window_kernel: the g codes of
+// g-mer j as bits-wide fields of win[j], first position most significant): the
+// same mixed-radix key, symbols extracted with shifts instead of byte loads, and
+// EM masks per CTA share each thread's window and sequence-id loads.
+// grid: (g-mer tiles, ceil(nmask / EM)); kept_sh[b*GMAX + r] = bits*(g-1-kept_r).
+constexpr int EW_THREADS = 256;
+constexpr int EW_ITEMS = 8;
+constexpr int EW_MASKS = 8;
+template <typename K>
+__global__ void __launch_bounds__(EW_THREADS) encode_win_kernel(
+    const uint64_t* __restrict__ win, const uint32_t* __restrict__ gm_seq, uint64_t n,
+    const uint8_t* __restrict__ kept_sh, int nkept, uint32_t sigma, int bits, int sb, int nmask,
+    K* __restrict__ out) {
+    __shared__ uint8_t sh[EW_MASKS][GMAX];
+    const int b0 = blockIdx.y * EW_MASKS;
+    const int nm = min(EW_MASKS, nmask - b0);
+    for (int i = threadIdx.x; i < nm * GMAX; i += EW_THREADS)
+        sh[i / GMAX][i % GMAX] = kept_sh[(b0 + i / GMAX) * GMAX + i % GMAX];
+    __syncthreads();
+    const uint64_t symmask = (1ull << bits) - 1ull;
+    const uint64_t j0 = (uint64_t)blockIdx.x * EW_THREADS * EW_ITEMS + threadIdx.x;
+    uint64_t w[EW_ITEMS];
+    uint32_t x[EW_ITEMS];
+#pragma unroll
+    for (int i = 0; i < EW_ITEMS; ++i) {
+        const uint64_t j = j0 + (uint64_t)i * EW_THREADS;
+        w[i] = j < n ? win[j] : 0ull;
+        x[i] = j < n ? gm_seq[j] : 0u;
+    }
+    for (int mm = 0; mm < nm; ++mm) {
+        K* o = out + (uint64_t)(b0 + mm) * n;
+#pragma unroll
+        for (int i = 0; i < EW_ITEMS; ++i) {
+            const uint64_t j = j0 + (uint64_t)i * EW_THREADS;
+            if (j >= n) continue;
+            uint64_t key = 0;
+            for (int r = 0; r < nkept; ++r) key = key * sigma + ((w[i] >> sh[mm][r]) & symmask);
+            o[j] = (K)((key << sb) | x[i]);
+        }
+    }
+}
+
+cudaError_t launch_encode_win(const uint64_t* win, const uint32_t* gm_seq, uint64_t n,
+                              const uint8_t* kept_sh, int nkept, int sigma, int bits, int sb,
+                              int nmask, void* out, bool k64, cudaStream_t s) {
+    if (n == 0 || nmask == 0) return cudaGetLastError();
+    dim3 grid((unsigned)((n + EW_THREADS * EW_ITEMS - 1) / (EW_THREADS * EW_ITEMS)),
+              (unsigned)((nmask + EW_MASKS - 1) / EW_MASKS));
+    if (k64)
+        encode_win_kernel<uint64_t><<<grid, EW_THREADS, 0, s>>>(win, gm_seq, n, kept_sh, nkept,
+                                                                (uint32_t)sigma, bits, sb, nmask,
+                                                                (uint64_t*)out);
+    else
+        encode_win_kernel<uint32_t><<<grid, EW_THREADS, 0, s>>>(win, gm_seq, n, kept_sh, nkept,
+                                                                (uint32_t)sigma, bits, sb, nmask,
+                                                                (uint32_t*)out);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_encode(const CorpusView& cv, const uint8_t* kept, int nkept, int sigma, int sb,
                           int nmask, int npass, void* out, bool k64, uint32_t* hist,
                           cudaStream_t s) {

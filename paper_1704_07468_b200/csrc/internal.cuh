@@ -214,6 +214,11 @@ cudaError_t launch_check_codes(const uint8_t* codes, int64_t len, int sigma, int
 cudaError_t launch_encode(const CorpusView& cv, const uint8_t* kept, int nkept, int sigma, int sb,
                           int nmask, int npass, void* out, bool k64, uint32_t* hist,
                           cudaStream_t s);
+// Encode from packed windows (win[j]: g codes, bits each, first most significant);
+// kept_sh[b*GMAX + r] = bits*(g-1-kept_r) of mask b.
+cudaError_t launch_encode_win(const uint64_t* win, const uint32_t* gm_seq, uint64_t n,
+                              const uint8_t* kept_sh, int nkept, int sigma, int bits, int sb,
+                              int nmask, void* out, bool k64, cudaStream_t s);
 cudaError_t launch_onesweep(const uint64_t* in, uint64_t* out, uint64_t n, int nseg, int shift,
                             const uint32_t* hist, int pass, int npass, uint64_t* status,
                             uint32_t* ctr, uint32_t epoch, cudaStream_t s);

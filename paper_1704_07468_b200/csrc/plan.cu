@@ -100,7 +100,7 @@ struct gakco_plan {
     std::vector<std::array<uint8_t, GMAX>> mask_kept;
     std::vector<int> key_bits;  // per level
 
-    DevBuf dense2, heavy2, hcount2, tseq2, tcnt2, gstart2, counts2, perm, iota, best, parent, Dgscr, Kdscr, codes, off, gofs, gmseq, keysA, keysB, hist, status, ctr, tseq, tcnt, gstart, gend,
+    DevBuf keptsh, dense2, heavy2, hcount2, tseq2, tcnt2, gstart2, counts2, perm, iota, best, parent, Dgscr, Kdscr, codes, off, gofs, gmseq, keysA, keysB, hist, status, ctr, tseq, tcnt, gstart, gend,
         counts, kept, stats, flags, kdiag, Cscr, Nmscr, Kscr, Knscr, heavy, hcount, dense, tiles,
         lightacc, binrec, bincnt, win, bkH, bktot, bkbase, bkdesc, bktab, bktcnt, bkgs, bkocc;
     int64_t tiles_npad = -1;
@@ -258,7 +258,7 @@ extern "C" gakco_status gakco_create(int sigma, int g, int k, int M, int device,
 extern "C" void gakco_destroy(gakco_plan* p) {
     if (!p) return;
     DeviceGuard dg(p->device);
-    DevBuf* bufs[] = {&p->dense2, &p->heavy2, &p->hcount2, &p->tseq2, &p->tcnt2, &p->gstart2, &p->counts2, &p->perm, &p->iota, &p->best, &p->parent, &p->Dgscr, &p->Kdscr, &p->codes, &p->off,   &p->gofs,  &p->gmseq,  &p->keysA, &p->keysB,
+    DevBuf* bufs[] = {&p->keptsh, &p->dense2, &p->heavy2, &p->hcount2, &p->tseq2, &p->tcnt2, &p->gstart2, &p->counts2, &p->perm, &p->iota, &p->best, &p->parent, &p->Dgscr, &p->Kdscr, &p->codes, &p->off,   &p->gofs,  &p->gmseq,  &p->keysA, &p->keysB,
                       &p->hist,  &p->status, &p->ctr,  &p->tseq,   &p->tcnt,  &p->gstart,
                       &p->gend,  &p->counts, &p->kept, &p->stats,  &p->flags, &p->kdiag,
                       &p->Cscr,  &p->Nmscr, &p->Kscr,  &p->Knscr, &p->heavy, &p->hcount,
@@ -627,7 +627,22 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
                           : so1;
     int64_t batch_no = 0;
     int64_t passkeys = 0, keys32 = 0, passkeys32 = 0;
-    if (hash_mode) {
+    // encode from packed g-mer windows when g * bits <= 64 (LSD path, not onesweep,
+    // whose encoder also counts the digit histograms)
+    const bool use_win = !hash_mode && n > 0 && g * bits <= 64 && p->sort_mode != 1;
+    if (use_win) {
+        CK(p->ensure(p->win, n * 8, s));
+        std::vector<uint8_t> ksh(mine.size() * GMAX + GMAX, 0);
+        for (size_t i = 0; i < mine.size(); ++i) {
+            const int mm = p->mask_level[mine[i]];
+            for (int r = 0; r < g - mm; ++r)
+                ksh[i * GMAX + r] = (uint8_t)(bits * (g - 1 - p->mask_kept[mine[i]][r]));
+        }
+        CK(p->ensure(p->keptsh, ksh.size(), s));
+        CK(cudaMemcpyAsync(p->keptsh.p, ksh.data(), ksh.size(), cudaMemcpyHostToDevice, s));
+        CK(cudaStreamSynchronize(s));  // ksh is a local buffer
+    }
+    if (hash_mode || use_win) {
         cudaEvent_t a0 = nullptr;
         p->stage_begin(s, &a0);
         LK(launch_windows(cv, g, bits, (uint64_t*)p->win.p, p->sm_count, s));
@@ -873,9 +888,14 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
             // 32-bit composites when key + sequence bits fit (half the key traffic)
             const bool k64 = onesweep || kb + sb > 32;
             if (onesweep) CK(cudaMemsetAsync(p->hist.p, 0, (size_t)nmask * MAXPASS * RADIX * 4, s));
-            LK(launch_encode(cv, (const uint8_t*)p->kept.p + pos * GMAX, g - m, p->sigma, sb,
-                             nmask, onesweep ? npass : 0, p->keysA.p, k64, (uint32_t*)p->hist.p,
-                             s));
+            if (use_win)
+                LK(launch_encode_win((const uint64_t*)p->win.p, (const uint32_t*)p->gmseq.p, n,
+                                     (const uint8_t*)p->keptsh.p + pos * GMAX, g - m, p->sigma,
+                                     bits, sb, nmask, p->keysA.p, k64, s));
+            else
+                LK(launch_encode(cv, (const uint8_t*)p->kept.p + pos * GMAX, g - m, p->sigma, sb,
+                                 nmask, onesweep ? npass : 0, p->keysA.p, k64,
+                                 (uint32_t*)p->hist.p, s));
             p->stage_end(s, S_ENCODE, a);
 
             p->stage_begin(s, &a);
