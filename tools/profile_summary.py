@@ -18,12 +18,18 @@ import os
 import subprocess
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-STAGE = {"encode_kernel": "encode", "radix_hist_kernel": "sort", "radix_scatter_kernel": "sort",
+STAGE = {"encode_kernel": "encode", "encode_win_kernel": "encode", "window_kernel": "encode",
+         "radix_hist_kernel": "sort", "radix_scatter_kernel": "sort",
          "onesweep_kernel": "sort", "segment_kernel": "segment", "light_kernel": "light",
-         "gram_kernel": "heavy", "dense_reset_kernel": "heavy", "fill_reset_kernel": "heavy",
-         "epilogue_kernel": "epilogue", "kdiag_kernel": "epilogue",
+         "light_flush_kernel": "light", "light_flush_perm_kernel": "light",
+         "best_partner_kernel": "light", "best_union_kernel": "light", "uf_roots_kernel": "light",
+         "gram_kernel": "heavy", "gram2_kernel": "heavy", "gram4_kernel": "heavy",
+         "fill_reset_kernel": "heavy", "build_dense_kernel": "dense",
+         "build_dense2_kernel": "dense", "build_dense3_kernel": "dense",
+         "fill_round_kernel": "dense", "epilogue_kernel": "epilogue", "kdiag_kernel": "epilogue",
          "diag_closed_form_kernel": "light", "gmer_index_kernel": "encode",
-         "check_codes_kernel": "encode"}
+         "check_codes_kernel": "encode", "bk_pass_kernel": "encode", "bk_colscan_kernel": "sort",
+         "bk_bscan_kernel": "sort", "bk_group_kernel": "segment"}
 
 
 def short(name):
