@@ -430,7 +430,7 @@ __global__ void __launch_bounds__(BD2_THREADS) build_dense2_kernel(
 // triples below its end, so every triple is read once and a chunk costs one round
 // of loads for all the warp's columns (v2 re-brackets every (slab, chunk) item).
 template <bool FP4>
-__global__ void __launch_bounds__(BD2_THREADS) build_dense3_kernel(
+__global__ void __launch_bounds__(BD2_THREADS, 3) build_dense3_kernel(
     SegmentOut so, const uint2* __restrict__ heavy_list, const uint32_t* fill,
     uint8_t* __restrict__ D, int64_t n_pad, uint64_t ldd) {
     extern __shared__ __align__(16) unsigned char sb[];  // [BD2_ROWS][128], swizzled words

@@ -34,6 +34,8 @@ STAGE = {"encode_kernel": "encode", "encode_win_kernel": "encode", "window_kerne
 
 def short(name):
     n = name.split("(")[0].strip()
+    if n.startswith("void "):
+        n = n[5:]
     n = n.split("::")[-1]
     return n.split("<")[0]
 
