@@ -158,8 +158,42 @@ __global__ void __launch_bounds__(256) light_kernel(SegmentOut so, int64_t heavy
             pair_add(acc, bn, ok, idx, val);
         }
 
-        // (2) the other groups one by one (big light groups and heavy candidates)
-        uint32_t todo = __ballot_sync(0xffffffffu, lane < ng && !flat);
+        // (1b) heavy candidates among the 32 groups: counts checked per group, then one
+        // atomicAdd claims all their dense columns (a claim per group would serialise
+        // every warp on the fill counter)
+        uint32_t got = 0;
+        {
+            uint32_t cand = __ballot_sync(0xffffffffu, lane < ng && !flat && (int64_t)my_s >= heavy_min);
+            uint32_t claim = 0;
+            while (cand) {
+                const int jj = __ffs(cand) - 1;
+                cand &= cand - 1;
+                const uint32_t a0 = __shfl_sync(0xffffffffu, my_start, jj);
+                const uint32_t b0 = __shfl_sync(0xffffffffu, my_end, jj);
+                uint32_t cmax = 0;
+                for (uint32_t t = a0 + lane; t < b0; t += 32) cmax = max(cmax, so.tcnt[t]);
+                cmax = __reduce_max_sync(0xffffffffu, cmax);
+                if (cmax <= heavy_cmax) claim |= 1u << jj;
+            }
+            if (claim) {
+                uint32_t base = 0;
+                if (lane == 0) base = atomicAdd(dense_fill, (uint32_t)__popc(claim));
+                base = __shfl_sync(0xffffffffu, base, 0);
+                bool mine = false;
+                if ((claim >> lane) & 1u) {
+                    const uint64_t col = (uint64_t)base + __popc(claim & lanemask_lt());
+                    if (col < ldd) {  // (a full D: the group stays on the light path)
+                        heavy_list[col] = make_uint2(my_start, my_end);
+                        mine = true;
+                    }
+                }
+                got = __ballot_sync(0xffffffffu, mine);
+                nheavy += lane == 0 ? __popc(got) : 0u;
+            }
+        }
+
+        // (2) the other groups one by one (big light groups)
+        uint32_t todo = __ballot_sync(0xffffffffu, lane < ng && !flat) & ~got;
         uint32_t pa0 = 0, pb0 = 0, pX = 0, pC = 0;
         auto prefetch = [&](uint32_t jj) {
             pa0 = __shfl_sync(0xffffffffu, my_start, jj);
@@ -177,23 +211,6 @@ __global__ void __launch_bounds__(256) light_kernel(SegmentOut so, int64_t heavy
             const uint32_t xA0 = pX, cA0 = pC;
             if (todo) prefetch(__ffs(todo) - 1);  // the next group's first chunk
             const uint32_t s = b0 - a0;
-            if ((int64_t)s >= heavy_min) {
-                // dense tensor-core path if every count fits the u8 operand
-                uint32_t cmax = cA0;
-                for (uint32_t t = a0 + 32 + lane; t < b0; t += 32) cmax = max(cmax, so.tcnt[t]);
-                cmax = __reduce_max_sync(0xffffffffu, cmax);
-                if (cmax <= heavy_cmax) {
-                    // claim a column of the dense count matrix D; build_dense fills it
-                    uint32_t col = 0;
-                    if (lane == 0) col = atomicAdd(dense_fill, 1u);
-                    col = __shfl_sync(0xffffffffu, col, 0);
-                    if (col < ldd) {  // (a full D falls back to pair updates below)
-                        if (lane == 0) heavy_list[col] = make_uint2(a0, b0);
-                        ++nheavy;
-                        continue;
-                    }
-                }
-            }
             pairs += (unsigned long long)s * (s - 1) / 2;
             // the group's triples in 32-wide register chunks; pairs enumerated
             // lane-parallel: within a chunk through the triangle table, across
