@@ -222,15 +222,15 @@ __global__ void __launch_bounds__(RS_THREADS) radix_hist_kernel(
 }
 
 template <typename K>
-__global__ void __launch_bounds__(RS_THREADS) radix_scatter_kernel(
+__global__ void __launch_bounds__(RS_THREADS, 2) radix_scatter_kernel(
     const K* __restrict__ in, K* __restrict__ out, uint64_t n, uint32_t cps,
     uint64_t L, int shift, const uint32_t* __restrict__ hist) {
     extern __shared__ __align__(16) unsigned char smem[];
     K* s_keys = (K*)smem;                                                // [SORT_TILE]
     int64_t* s_run = (int64_t*)(smem + SORT_TILE * sizeof(K));           // [RADIX]
-    uint32_t(*s_whist)[RADIX] = (uint32_t(*)[RADIX])(s_run + RADIX);     // [WARPS][RADIX]
-    uint32_t* s_doff = &s_whist[RS_WARPS][0];                            // [RADIX]
-    uint32_t* s_cnt = s_doff + RADIX;                                    // [RADIX]
+    int64_t* s_goff = s_run + RADIX;                                     // [RADIX]
+    uint32_t(*s_whist)[RADIX] = (uint32_t(*)[RADIX])(s_goff + RADIX);    // [WARPS][RADIX]
+    uint32_t* s_cnt = &s_whist[RS_WARPS][0];                             // [RADIX]
     uint32_t* s_w = s_cnt + RADIX;                                       // [16]
     uint32_t* s_match = s_w + 16;                                        // [WARPS][RADIX]
     for (int i = threadIdx.x; i < RS_WARPS * RADIX; i += RS_THREADS) s_match[i] = 0u;
@@ -308,31 +308,38 @@ __global__ void __launch_bounds__(RS_THREADS) radix_scatter_kernel(
         __syncthreads();
         uint32_t tcnt = 0;
         if (tid < RADIX) {
-            uint32_t sum = 0;
+#pragma unroll
+            for (int ww = 0; ww < RS_WARPS; ++ww) tcnt += s_whist[ww][tid];
+            s_cnt[tid] = tcnt;
+        }
+        const uint32_t doff = scan256_excl(tcnt, s_w);
+        if (tid < RADIX) {
+            // s_whist[w][d] <- tile position of warp w's first digit-d key; s_goff[d] <-
+            // global position of tile index 0 as if it were digit d (so that tile index
+            // j of digit d goes to s_goff[d] + j): one lookup per key below
+            uint32_t sum = doff;
+#pragma unroll
             for (int ww = 0; ww < RS_WARPS; ++ww) {
                 const uint32_t v = s_whist[ww][tid];
                 s_whist[ww][tid] = sum;
                 sum += v;
             }
-            tcnt = sum;
-            s_cnt[tid] = sum;
+            s_goff[tid] = s_run[tid] - (int64_t)doff;
         }
-        const uint32_t doff = scan256_excl(tcnt, s_w);
-        if (tid < RADIX) s_doff[tid] = doff;
         __syncthreads();
 #pragma unroll
         for (int i = 0; i < SORT_ITEMS; ++i) {
             const uint32_t idx = w * SORT_ITEMS * 32 + i * 32 + lane;
             if (idx < cnt) {
                 const uint32_t d = (uint32_t)(keys[i] >> shift) & 0xffu;
-                s_keys[s_doff[d] + s_whist[w][d] + rank[i]] = keys[i];
+                s_keys[s_whist[w][d] + rank[i]] = keys[i];
             }
         }
         __syncthreads();
         for (uint32_t j = tid; j < cnt; j += RS_THREADS) {
             const K k = s_keys[j];
             const uint32_t d = (uint32_t)(k >> shift) & 0xffu;
-            out[seg_base + (uint64_t)(s_run[d] + (int64_t)(j - s_doff[d]))] = k;
+            out[seg_base + (uint64_t)(s_goff[d] + (int64_t)j)] = k;
         }
         __syncthreads();
         if (tid < RADIX) s_run[tid] += s_cnt[tid];
@@ -342,7 +349,7 @@ __global__ void __launch_bounds__(RS_THREADS) radix_scatter_kernel(
 
 template <typename K>
 constexpr size_t rs_smem() {
-    return SORT_TILE * sizeof(K) + RADIX * 8 + 2 * RS_WARPS * RADIX * 4 + 2 * RADIX * 4 + 16 * 4;
+    return SORT_TILE * sizeof(K) + 2 * RADIX * 8 + 2 * RS_WARPS * RADIX * 4 + RADIX * 4 + 16 * 4;
 }
 
 template <typename K>
