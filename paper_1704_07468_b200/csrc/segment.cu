@@ -30,6 +30,7 @@ __global__ void __launch_bounds__(SEG_THREADS) segment_kernel(
     int64_t* diag, uint32_t* counters, SegmentOut so, unsigned long long* stats) {
     __shared__ uint32_t s_w[16];
     __shared__ uint32_t s_gpos[SEG_TILE];
+    __shared__ uint32_t s_tx[SEG_TILE], s_tc[SEG_TILE];  // the tile's triples, staged
     __shared__ uint32_t s_first_gh, s_base_t, s_base_g, s_tail;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint64_t tile0 = (uint64_t)blockIdx.x * SEG_TILE;
@@ -172,18 +173,23 @@ __global__ void __launch_bounds__(SEG_THREADS) segment_kernel(
         if (agg_g) atomicAdd(&stats[ST_GROUPS], (unsigned long long)agg_g);
     }
     __syncthreads();
-    uint32_t ti = s_base_t + off_t, gl = off_g;
+    // triples staged in shared memory, then written with coalesced stores
+    uint32_t li = off_t, gl = off_g;
 #pragma unroll
     for (int i = 0; i < SEG_ITEMS; ++i) {
         if (emit_t & (1u << i)) {
             const uint32_t x = (uint32_t)(cur[i] & seqmask);
-            so.tseq[ti] = x | (((gh_bits >> i) & 1u) << 31);
-            so.tcnt[ti] = cnt[i];
-            if (emit_g & (1u << i)) s_gpos[gl++] = ti;
-            ++ti;
+            s_tx[li] = x | (((gh_bits >> i) & 1u) << 31);
+            s_tc[li] = cnt[i];
+            if (emit_g & (1u << i)) s_gpos[gl++] = s_base_t + li;
+            ++li;
         }
     }
     __syncthreads();
+    for (uint32_t j = tid; j < agg_t; j += SEG_THREADS) {
+        so.tseq[s_base_t + j] = s_tx[j];
+        so.tcnt[s_base_t + j] = s_tc[j];
+    }
     // group ranges: a group runs to the next group's first triple (or the end of
     // this tile's triples, its tail included)
     const uint32_t tend = s_base_t + agg_t + tail;
