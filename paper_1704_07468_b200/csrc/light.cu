@@ -12,6 +12,8 @@
 // One warp per group; its triples are held in registers 32 at a time and the
 // pairs are spread over the lanes (triangle table within a chunk, full 32 x 32
 // blocks across chunks), so every atomic instruction carries 32 updates.
+#include <algorithm>
+
 #include "internal.cuh"
 
 namespace gk {
@@ -369,6 +371,35 @@ __global__ void best_union_kernel(const unsigned long long* __restrict__ best, i
     }
 }
 
+// union(X, Y) for every pair sharing at least a quarter of the matches of X's or Y's
+// best partner (and >= 2): joins whole families, not only best-partner chains
+__global__ void thresh_union_kernel(const int64_t* __restrict__ C, int64_t N,
+                                    const unsigned long long* __restrict__ best,
+                                    uint32_t* parent) {
+    for (int64_t x = blockIdx.x; x < N - 1; x += gridDim.x) {
+        const uint64_t bx = best[x] >> 32;
+        const int64_t* row = C + x * N;
+        for (int64_t y = x + 1 + threadIdx.x; y < N; y += blockDim.x) {
+            const int64_t v = row[y];
+            if (v < 2) continue;
+            const uint64_t by = best[y] >> 32;
+            if ((uint64_t)v * 4 < bx && (uint64_t)v * 4 < by) continue;
+            uint32_t a = (uint32_t)x, c = (uint32_t)y;
+            while (true) {
+                a = uf_find(parent, a);
+                c = uf_find(parent, c);
+                if (a == c) break;
+                if (a < c) {
+                    const uint32_t t = a;
+                    a = c;
+                    c = t;
+                }
+                if (atomicCAS(&parent[a], a, c) == a) break;
+            }
+        }
+    }
+}
+
 __global__ void uf_roots_kernel(uint32_t* parent, int64_t N) {
     for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < N;
          x += (int64_t)gridDim.x * blockDim.x)
@@ -386,6 +417,7 @@ cudaError_t launch_cluster_roots(const int64_t* C, int64_t N, unsigned long long
     if (rows > 0) best_partner_kernel<<<(unsigned)rows, 256, 0, s>>>(C, N, best);
     const int blocks = (int)((N + 255) / 256 < 1024 ? (N + 255) / 256 : 1024);
     best_union_kernel<<<blocks, 256, 0, s>>>(best, N, parent);
+    if (rows > 0) thresh_union_kernel<<<(unsigned)rows, 256, 0, s>>>(C, N, best, parent);
     uf_roots_kernel<<<blocks, 256, 0, s>>>(parent, N);
     return cudaGetLastError();
 }

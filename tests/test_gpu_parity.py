@@ -133,7 +133,9 @@ def test_light_relabel(gk, oracle_lib):
     family-structured and random corpora, M >= 1 so later levels use the labels."""
     rng = np.random.default_rng(113)
     cases = [(sc.gen_families(7, 90, 6, 60, 30, 60, sigma=20), 6, 3, 3),
-             (sc.gen_families(8, 150, 10, 80, 80, 80, sigma=4), 8, 5, 3)]
+             (sc.gen_families(8, 150, 10, 80, 80, 80, sigma=4), 8, 5, 3),
+             (sc.gen_families(9, 400, 4, 100, 100, 100, sigma=20), 7, 4, 3),
+             (sc.gen_families(10, 300, 150, 60, 60, 60, sigma=20), 6, 3, 3)]
     for _ in range(4):
         sigma = int(rng.choice([2, 4, 20]))
         g = int(rng.integers(3, 9))
