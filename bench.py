@@ -58,6 +58,8 @@ def args_():
                     help="heavy Gram operands: -1 auto (e2m1 where exact), 0 u8, 1 e2m1")
     ap.add_argument("--pipeline", type=int, default=None, choices=[0, 1],
                     help="two-stream batch pipeline (default 1)")
+    ap.add_argument("--level-order", type=int, default=None, choices=[0, 1],
+                    help="0: levels m = 0..M (default), 1: m = M..0")
     ap.add_argument("--gram-pair", type=int, default=None, choices=[0, 1],
                     help="heavy Gram kernel: 1 CTA pairs (default), 0 one SM per tile")
     ap.add_argument("--no-timing", action="store_true",
@@ -281,6 +283,8 @@ def run_ours(a):
         plan.set_option(gakco.GAKCO_OPT_GRAM_FP4, a.fp4)
     if a.pipeline is not None:
         plan.set_option(gakco.GAKCO_OPT_PIPELINE, a.pipeline)
+    if a.level_order is not None:
+        plan.set_option(gakco.GAKCO_OPT_LEVEL_ORDER, a.level_order)
     if a.gram_pair is not None:
         plan.set_option(gakco.GAKCO_OPT_GRAM_PAIR, a.gram_pair)
     C = torch.zeros((M + 1, N, N), dtype=torch.int64, device=dev)

@@ -86,9 +86,13 @@ typedef enum {
                                      mask's n_max^2 < 2^24 keeps the f32 sums exact; groups
                                      with a count > 4 stay light), 0 = u8 (kind::i8), 1 = e2m1
                                      where exact */
-    GAKCO_OPT_PIPELINE = 11       /* 1 (default): light updates, dense build and Gram of batch b
+    GAKCO_OPT_PIPELINE = 11,      /* 1 (default): light updates, dense build and Gram of batch b
                                      run on a second stream while batch b+1 is encoded, sorted
                                      and segmented (double-buffered triples); 0: one stream */
+    GAKCO_OPT_LEVEL_ORDER = 12    /* 0 (default): levels processed m = 0..M; 1: m = M..0 (the
+                                     top level's Gram overlaps the rest: Protein 8.0 -> 7.8 ms
+                                     but DNA 9.26 -> 9.51 ms; ascending whenever the light
+                                     accumulator is relabelled) */
 } gakco_option;
 
 /* Counters of the last gakco_accumulate (algorithmic units). */

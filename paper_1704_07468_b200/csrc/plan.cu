@@ -85,6 +85,7 @@ struct gakco_plan {
     int gram_pair = 1;         // 1: CTA-pair Gram (gram2.cu), 0: one-SM Gram (gram_tc.cu)
     int light_flat = 8;        // light groups of <= this many sequences share warps
     int light_relabel = -1;    // -1 auto (accumulator >> L2), 0 off, 1 on
+    int level_order_desc = 0;  // process levels m = M..0 (1) or 0..M (0, measured faster on DNA)
     int gram_fp4 = -1;         // -1 auto (e2m1 Gram when exact), 0 u8 / kind::i8, 1 e2m1
     int pipeline = 1;          // light / dense / Gram of batch b on an aux stream, overlapping
                                // encode / sort / segment of batch b+1 (double-buffered triples)
@@ -325,6 +326,10 @@ extern "C" gakco_status gakco_set_option(gakco_plan* p, int option, int64_t valu
             if (value < 0 || value > 1) return p->fail(GAKCO_E_ARG, "pipeline must be 0 or 1");
             p->pipeline = (int)value;
             return GAKCO_OK;
+        case GAKCO_OPT_LEVEL_ORDER:
+            if (value < 0 || value > 1) return p->fail(GAKCO_E_ARG, "level order must be 0 or 1");
+            p->level_order_desc = (int)value;
+            return GAKCO_OK;
         case GAKCO_OPT_TIMING:
             p->timing = value != 0;
             return GAKCO_OK;
@@ -450,11 +455,23 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
     CK(p->ensure(p->gmseq, n * sizeof(uint32_t), s));
     LK(launch_gmer_index((const int64_t*)p->gofs.p, N, (uint32_t*)p->gmseq.p, s));
 
-    // this shard's masks, in processing order
+    // this shard's masks, in processing order: levels ascending (default) or, with
+    // GAKCO_OPT_LEVEL_ORDER, descending so the top level's long tensor-bound Gram
+    // flushes overlap the lower levels' light and sort work (any order gives the
+    // same integer sums); ascending whenever the light accumulator is relabelled
+    // (the clustering reads the first, cheapest level)
+    const bool relabel_pre =
+        NA == 0 && p->light_bins <= 0 && N >= 2 &&
+        (p->light_relabel == 1 ||
+         (p->light_relabel == -1 && (uint64_t)N * (uint64_t)(N - 1) / 2 * 4 > (96ull << 20)));
     std::vector<int> mine;
     for (size_t i = 0; i < p->mask_level.size(); ++i)
         if ((int)(i % world) == rank && (only_level < 0 || p->mask_level[i] == only_level))
             mine.push_back((int)i);
+    if (!relabel_pre && p->level_order_desc)
+        std::stable_sort(mine.begin(), mine.end(), [&](int a, int b) {
+            return p->mask_level[a] > p->mask_level[b];
+        });
     // (pageable host staging: cudaMemcpyAsync returns once the source is copied,
     // so the member buffers can be reused without a stream sync)
     std::vector<uint8_t>& kept_h = p->kept_h;

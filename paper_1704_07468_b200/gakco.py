@@ -38,6 +38,7 @@ GAKCO_OPT_LIGHT_FLAT = 8
 GAKCO_OPT_LIGHT_RELABEL = 9
 GAKCO_OPT_GRAM_FP4 = 10
 GAKCO_OPT_PIPELINE = 11
+GAKCO_OPT_LEVEL_ORDER = 12
 
 EXPORTS = ("gakco_create", "gakco_set_shard", "gakco_set_option", "gakco_accumulate",
            "gakco_finalize", "gakco_kernel", "gakco_kernel_k", "gakco_kernel_rect",

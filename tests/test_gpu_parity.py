@@ -170,6 +170,7 @@ def test_batch_size_invariance(gk, oracle_lib):
         assert_parity(run(gk, cp, 7, 5, 2, batch_keys=bk), ref)
         assert_parity(run(gk, cp, 7, 5, 2, batch_keys=bk, sort=1), ref)
         assert_parity(run(gk, cp, 7, 5, 2, batch_keys=bk, pipeline=0), ref)
+        assert_parity(run(gk, cp, 7, 5, 2, batch_keys=bk, level_order=0), ref)
         assert_parity(run(gk, cp, 7, 5, 2, batch_keys=bk, heavy_min_seqs=2), ref)
 
 
