@@ -1,4 +1,7 @@
-// gram_tc.cu — heavy groups as a dense count Gram on the 5th-gen tensor cores.
+// gram_tc.cu — heavy groups as a dense count Gram on the 5th-gen tensor cores:
+// the one-SM u8 Gram (GAKCO_OPT_GRAM_PAIR 0; the default CTA-pair kernels are in
+// gram2.cu), the dense-column builders (build_dense3 / build_dense2), the fill
+// counters, and the TMA maps shared with gram2.cu.
 //
 // countAndUpdate adds c_X(key)*c_Y(key) to C_m(X,Y) for every
 // pair of sequences sharing a key. For the R keys ("heavy groups", many
@@ -222,88 +225,6 @@ __global__ void __launch_bounds__(GT_THREADS, 1)
 }
 
 // ---------------------------------------------------------------- D build
-// A slab = 128 columns (groups) x n_pad rows, stored [row][128 B]. One CTA builds
-// BD_ROWS rows of one slab in shared memory (zero, scatter the groups' counts for
-// the rows in range, then 16-byte coalesced stores), so D is written once with
-// full lines and never needs a separate zeroing pass. Columns [prev, fill) are
-// this batch's (prev = fill[1], a multiple of 128); unused columns of the last
-// slab are written as zeros.
-// Work item = 32 columns (a quarter slab) x up to BD_ROWS rows: every group's
-// triples are read once, and each row's 32 bytes go out as two 16-byte stores
-// (whole 32-byte sectors at a 128-byte stride).
-constexpr int BD_ROWS = 2048;
-constexpr int BD_COLS = 32;
-constexpr int BD_STRIDE = 32;  // smem row stride (40 to spread banks measured slower)
-constexpr int BD_THREADS = 512;
-
-__global__ void __launch_bounds__(BD_THREADS) build_dense_kernel(
-    SegmentOut so, const uint2* __restrict__ heavy_list, const uint32_t* fill,
-    uint8_t* __restrict__ D, int64_t n_pad, uint64_t ldd) {
-    extern __shared__ __align__(16) unsigned char sb[];  // [BD_ROWS][BD_COLS]
-    const uint64_t f0 = fill[1];
-    const uint64_t f1 = min((uint64_t)fill[0], ldd);
-    if (f1 <= f0) return;
-    // quarter slabs of every slab this batch touches (whole slabs, so columns up
-    // to the next multiple of 128 are written as zeros, never left stale)
-    const uint64_t q0 = f0 / BD_COLS, q1 = (f1 + GT_KB - 1) / GT_KB * (GT_KB / BD_COLS);
-    const uint64_t nchunks = (uint64_t)(n_pad + BD_ROWS - 1) / BD_ROWS;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    for (uint64_t wk = blockIdx.x; wk < (q1 - q0) * nchunks; wk += gridDim.x) {
-        const uint64_t qs = q0 + wk / nchunks;
-        const int64_t r0 = (int64_t)(wk % nchunks) * BD_ROWS;
-        const int64_t rows = min((int64_t)BD_ROWS, n_pad - r0);
-        for (int i = threadIdx.x; i < rows * BD_STRIDE / 8; i += BD_THREADS)
-            ((uint64_t*)sb)[i] = 0ull;
-        __syncthreads();
-        // warp w fills columns w and w + 16 of the quarter slab
-        uint2 bnd[BD_COLS * 32 / BD_THREADS];
-#pragma unroll
-        for (int k = 0; k < BD_COLS * 32 / BD_THREADS; ++k) {
-            const uint64_t col = qs * BD_COLS + warp + k * (BD_THREADS / 32);
-            bnd[k] = col < f1 ? heavy_list[col] : make_uint2(0, 0);
-        }
-        // the first 4 x 32 triples of both columns are loaded before any is used
-        // (8 independent loads in flight per lane); longer groups continue below
-        constexpr int NK = BD_COLS * 32 / BD_THREADS;
-        uint32_t xs[NK][4], cs[NK][4];
-#pragma unroll
-        for (int k = 0; k < NK; ++k)
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const uint32_t t = bnd[k].x + u * 32 + lane;
-                const bool v = t < bnd[k].y;
-                xs[k][u] = v ? so.tseq[t] & 0x7fffffffu : 0xffffffffu;
-                cs[k][u] = v ? so.tcnt[t] : 0u;
-            }
-#pragma unroll
-        for (int k = 0; k < NK; ++k) {
-            const int c = warp + k * (BD_THREADS / 32);
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const int64_t x = (int64_t)xs[k][u] - r0;
-                if (xs[k][u] != 0xffffffffu && x >= 0 && x < rows)
-                    sb[x * BD_STRIDE + c] = (uint8_t)cs[k][u];
-            }
-            for (uint32_t t = bnd[k].x + 128 + lane; t < bnd[k].y; t += 32) {
-                const int64_t x = (int64_t)(so.tseq[t] & 0x7fffffffu) - r0;
-                if (x >= 0 && x < rows) sb[x * BD_STRIDE + c] = (uint8_t)so.tcnt[t];
-            }
-        }
-        __syncthreads();
-        // row r of the quarter slab -> D + (slab*n_pad + r0 + r)*128 + quarter*32
-        const uint64_t slab = qs / (GT_KB / BD_COLS), quarter = qs % (GT_KB / BD_COLS);
-        uint8_t* dst = D + (slab * (uint64_t)n_pad + (uint64_t)r0) * GT_KB + quarter * BD_COLS;
-        for (int i = threadIdx.x; i < rows * 2; i += BD_THREADS) {
-            const int r = i >> 1, h = i & 1;
-            const uint64_t* src = (const uint64_t*)(sb + r * BD_STRIDE + h * 16);
-            const uint64_t lo = src[0], hi = src[1];
-            *(uint4*)(dst + (uint64_t)r * GT_KB + h * 16) =
-                make_uint4((uint32_t)lo, (uint32_t)(lo >> 32), (uint32_t)hi, (uint32_t)(hi >> 32));
-        }
-        __syncthreads();
-    }
-}
-
 // Build v2: work item = one whole slab (128 columns) x BD2_ROWS rows, so every
 // 128-byte line of D is written once, in full, by one CTA (16-byte stores). The
 // slab is assembled in shared memory with 4-byte words XOR-swizzled by row (the
