@@ -113,6 +113,34 @@ __global__ void __launch_bounds__(256) epilogue_kernel(EpiArgs a,
             for (int m = 0; m <= MM; ++m)
                 if (m <= M) a.C[m * nn + X * N + Y] = prof[q][m];
         }
+    }
+    // off-diagonal tile: C mirrored into tile (bj, bi) while prof still holds C
+    // (transposed through shared memory: coalesced rows on both sides)
+    if (!diag_tile) {
+        for (int o = 0; o <= M; ++o) {
+            __syncthreads();
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                int64_t v = 0;
+#pragma unroll
+                for (int m = 0; m <= MM; ++m)
+                    if (m == o) v = prof[q][m];
+                st[ty + 8 * q][tx] = v;
+            }
+            __syncthreads();
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int r = ty + 8 * q;
+                const int64_t X = (int64_t)bj * 32 + r, Y = (int64_t)bi * 32 + tx;
+                if (X < N && Y < N) a.C[o * nn + X * N + Y] = st[tx][r];
+            }
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        if (!ok[q]) continue;
+        const int r = ty + 8 * q;
+        const int64_t X = (int64_t)bi * 32 + r, Y = (int64_t)bj * 32 + tx;
         kv[q] = entry<MM>(prof[q], cf, a.g, a.k, M, &bad);  // prof now holds N_m
         if (a.Nm) {
 #pragma unroll
@@ -124,12 +152,11 @@ __global__ void __launch_bounds__(256) epilogue_kernel(EpiArgs a,
     }
     if (bad) atomicOr(a.flags, bad);
     if (diag_tile) return;
-    // transposed writes of tile (bj, bi): C mirror, Nm, K, Knorm
+    // transposed writes of tile (bj, bi): Nm, K, Knorm (the C mirror went out above)
     const int nout = 2 * (M + 1) + 2;
-    for (int o = 0; o < nout; ++o) {
+    for (int o = M + 1; o < nout; ++o) {
         bool has;
-        if (o <= M) has = true;                        // C_m mirror (needs original C_m)
-        else if (o <= 2 * M + 1) has = a.Nm != nullptr;
+        if (o <= 2 * M + 1) has = a.Nm != nullptr;
         else if (o == 2 * M + 2) has = a.K != nullptr;
         else has = a.Knorm != nullptr;
         if (!has) continue;
@@ -140,8 +167,7 @@ __global__ void __launch_bounds__(256) epilogue_kernel(EpiArgs a,
             if (!ok[q]) continue;
             const int64_t X = (int64_t)bi * 32 + r, Y = (int64_t)bj * 32 + tx;
             int64_t v;
-            if (o <= M) v = a.C[o * nn + X * N + Y];
-            else if (o <= 2 * M + 1) {
+            if (o <= 2 * M + 1) {
                 v = 0;
 #pragma unroll
                 for (int m = 0; m <= MM; ++m)
@@ -161,8 +187,7 @@ __global__ void __launch_bounds__(256) epilogue_kernel(EpiArgs a,
             const int64_t X = (int64_t)bj * 32 + r, Y = (int64_t)bi * 32 + tx;
             if (X >= N || Y >= N) continue;
             const int64_t v = st[tx][r];
-            if (o <= M) a.C[o * nn + X * N + Y] = v;
-            else if (o <= 2 * M + 1) a.Nm[(o - M - 1) * nn + X * N + Y] = v;
+            if (o <= 2 * M + 1) a.Nm[(o - M - 1) * nn + X * N + Y] = v;
             else if (o == 2 * M + 2) a.K[X * N + Y] = v;
             else a.Knorm[X * N + Y] = __longlong_as_double(v);
         }
