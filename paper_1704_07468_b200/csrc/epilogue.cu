@@ -39,9 +39,9 @@ struct EpiArgs {
 
 // Per-entry math. prof[m] = C_m(X,Y) in, N_m(X,Y) out. Returns K(X,Y).
 // Loops run to the compile-time bound MM (guarded by M) so prof stays in registers.
-template <int MM, typename P>
-__device__ __forceinline__ int64_t entry(P prof, const EpiCoef& cf, int g, int k, int M,
-                                         int* bad) {
+template <int MM>
+__device__ __forceinline__ int64_t entry(int64_t (&prof)[MM + 1], const EpiCoef& cf, int g, int k,
+                                         int M, int* bad) {
     int64_t cgk = 0;
 #pragma unroll
     for (int m = 0; m <= MM; ++m)
@@ -117,16 +117,12 @@ __global__ void __launch_bounds__(256) epilogue_kernel(EpiArgs a,
     // off-diagonal tile: C mirrored into tile (bj, bi) while prof still holds C
     // (transposed through shared memory: coalesced rows on both sides)
     if (!diag_tile) {
-        for (int o = 0; o <= M; ++o) {
+#pragma unroll
+        for (int o = 0; o <= MM; ++o) {  // static indices keep prof in registers
+            if (o > M) break;
             __syncthreads();
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                int64_t v = 0;
-#pragma unroll
-                for (int m = 0; m <= MM; ++m)
-                    if (m == o) v = prof[q][m];
-                st[ty + 8 * q][tx] = v;
-            }
+            for (int q = 0; q < 4; ++q) st[ty + 8 * q][tx] = prof[q][o];
             __syncthreads();
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
@@ -152,33 +148,34 @@ __global__ void __launch_bounds__(256) epilogue_kernel(EpiArgs a,
     }
     if (bad) atomicOr(a.flags, bad);
     if (diag_tile) return;
-    // transposed writes of tile (bj, bi): Nm, K, Knorm (the C mirror went out above)
-    const int nout = 2 * (M + 1) + 2;
-    for (int o = M + 1; o < nout; ++o) {
-        bool has;
-        if (o <= 2 * M + 1) has = a.Nm != nullptr;
-        else if (o == 2 * M + 2) has = a.K != nullptr;
-        else has = a.Knorm != nullptr;
-        if (!has) continue;
+    // transposed writes of tile (bj, bi): Nm (static level index, prof stays in
+    // registers), then K and Knorm (the C mirror went out above)
+    if (a.Nm) {
+#pragma unroll
+        for (int o = 0; o <= MM; ++o) {
+            if (o > M) break;
+            __syncthreads();
+#pragma unroll
+            for (int q = 0; q < 4; ++q) st[ty + 8 * q][tx] = prof[q][o];
+            __syncthreads();
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const int r = ty + 8 * q;
+                const int64_t X = (int64_t)bj * 32 + r, Y = (int64_t)bi * 32 + tx;
+                if (X < N && Y < N) a.Nm[o * nn + X * N + Y] = st[tx][r];
+            }
+        }
+    }
+    for (int o = 0; o < 2; ++o) {
+        if (o == 0 ? a.K == nullptr : a.Knorm == nullptr) continue;
         __syncthreads();
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
             const int r = ty + 8 * q;
             if (!ok[q]) continue;
             const int64_t X = (int64_t)bi * 32 + r, Y = (int64_t)bj * 32 + tx;
-            int64_t v;
-            if (o <= 2 * M + 1) {
-                v = 0;
-#pragma unroll
-                for (int m = 0; m <= MM; ++m)
-                    if (m == o - M - 1) v = prof[q][m];
-            }
-            else if (o == 2 * M + 2) v = kv[q];
-            else {
-                double d = knorm(kv[q], a.kdiag[X], a.kdiag[Y], false);
-                v = __double_as_longlong(d);
-            }
-            st[r][tx] = v;
+            st[r][tx] = o == 0 ? kv[q]
+                               : __double_as_longlong(knorm(kv[q], a.kdiag[X], a.kdiag[Y], false));
         }
         __syncthreads();
 #pragma unroll
@@ -187,8 +184,7 @@ __global__ void __launch_bounds__(256) epilogue_kernel(EpiArgs a,
             const int64_t X = (int64_t)bj * 32 + r, Y = (int64_t)bi * 32 + tx;
             if (X >= N || Y >= N) continue;
             const int64_t v = st[tx][r];
-            if (o <= 2 * M + 1) a.Nm[(o - M - 1) * nn + X * N + Y] = v;
-            else if (o == 2 * M + 2) a.K[X * N + Y] = v;
+            if (o == 0) a.K[X * N + Y] = v;
             else a.Knorm[X * N + Y] = __longlong_as_double(v);
         }
     }
