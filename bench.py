@@ -461,15 +461,18 @@ def run_ours(a):
         else:
             ach = algo_ / t_ / 1e12 if t_ > 0 else 0.0
             # int8 = 2x bf16 (nominal 4.5 vs 2.25 PFLOP/s); e2m1 (kind::mxf4) = 4x (9 vs 2.25)
-            ratio = 4.0 if last.get("gram_fp4", 0) else 2.0
+            # the e2m1 / u8 levels mix (GAKCO_OPT_GRAM_FP4 per level): the peak is the
+            # rate at which this MAC mix would run at the two nominal peaks
+            macs = float(last.get("heavy_macs", 0) or 0)
+            f4 = float(last.get("heavy_macs_fp4", 0) or 0) / macs if macs > 0 else 0.0
+            ratio = 1.0 / (f4 / 4.0 + (1.0 - f4) / 2.0)
             peak_ = pk["bf16_tflops"] * ratio
             r = {"bound": "tensor", "kernel": st, "achieved": ach, "peak": peak_,
                  "unit": "TFLOP/s", "frac": ach / peak_, "traffic": traffic_,
                  "algorithmic_ops_per_launch": algo_ / nl_, "launches_per_step": nl_,
-                 "avg_launch_ms": per_step[st] / nl_,
-                 "peak_source": pk["source"] + (" bf16_tflops x4 (e2m1 nominal ratio)"
-                                                if ratio == 4.0 else
-                                                " bf16_tflops x2 (int8 nominal ratio)")}
+                 "avg_launch_ms": per_step[st] / nl_, "e2m1_mac_share": round(f4, 4),
+                 "peak_source": pk["source"] + " bf16_tflops x %.3g (e2m1 x4, int8 x2 nominal "
+                                               "ratios, weighted by the MAC mix)" % ratio}
         if st in limiter:
             r["limiter"] = limiter[st]
         return r

@@ -81,10 +81,13 @@ typedef enum {
     GAKCO_OPT_LIGHT_RELABEL = 9,  /* light accumulator sequence relabelling (locality; results
                                      unchanged): -1 = automatic (default: when the packed
                                      triangle exceeds 96 MB), 0 = off, 1 = on */
-    GAKCO_OPT_GRAM_FP4 = 10,      /* heavy-group Gram operands: -1 = automatic (default: e2m1
-                                     counts, kind::mxf4 block-scaled with unit scales, when one
-                                     mask's n_max^2 < 2^24 keeps the f32 sums exact; groups
-                                     with a count > 4 stay light), 0 = u8 (kind::i8), 1 = e2m1
+    GAKCO_OPT_GRAM_FP4 = 10,      /* heavy-group Gram operands, per level m: -1 = automatic
+                                     (default): e2m1 counts (kind::mxf4 block-scaled, unit
+                                     scales) when one mask's n_max^2 < 2^24 keeps the f32 sums
+                                     exact AND n_max * p_max^(g-m) <= 1/8 (p_max: share of the
+                                     most frequent symbol), so counts > 4 -- which e2m1 cannot
+                                     hold and which stay on the light path -- are rare; else u8
+                                     (kind::i8). 0 = u8 at every level, 1 = e2m1 at every level
                                      where exact */
     GAKCO_OPT_PIPELINE = 11,      /* 1 (default): light updates, dense build and Gram of batch b
                                      run on a second stream while batch b+1 is encoded, sorted
@@ -117,7 +120,9 @@ typedef struct {
     double ms_dense;        /* building the dense u8 count columns of heavy groups */
     int64_t n_dense;
     int64_t n_pad;          /* rows of the dense count matrix (0: no tensor-core Gram) */
-    int64_t gram_fp4;       /* 1: the Gram ran on e2m1 counts (kind::mxf4), 0: u8 (kind::i8) */
+    int64_t gram_fp4;       /* bit m set: level m's Gram ran on e2m1 counts (kind::mxf4);
+                               clear: u8 (kind::i8). Chosen per level (GAKCO_OPT_GRAM_FP4) */
+    int64_t heavy_macs_fp4; /* the part of heavy_macs issued as e2m1 (kind::mxf4) */
 } gakco_stats;
 
 /* Create a plan for alphabet size sigma (1..255), g-mer length g (1..32),

@@ -40,6 +40,32 @@ __global__ void check_codes_kernel(const uint8_t* __restrict__ codes, int64_t le
     if (__syncthreads_or(bad) && threadIdx.x == 0) atomicOr(flags, EF_BAD_SYMBOL);
 }
 
+// symbol histogram (hist[256], zeroed by the caller), for the per-level choice of
+// the Gram operand format in plan.cu (the most frequent symbol bounds how often one
+// masked key repeats inside a sequence)
+__global__ void symbol_hist_kernel(const uint8_t* __restrict__ codes, int64_t len,
+                                   unsigned long long* __restrict__ hist) {
+    __shared__ uint32_t h[256];
+    for (int i = threadIdx.x; i < 256; i += blockDim.x) h[i] = 0;
+    __syncthreads();
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < len;
+         i += (int64_t)gridDim.x * blockDim.x)
+        atomicAdd(&h[codes[i]], 1u);
+    __syncthreads();
+    for (int i = threadIdx.x; i < 256; i += blockDim.x)
+        if (h[i]) atomicAdd(&hist[i], (unsigned long long)h[i]);
+}
+
+cudaError_t launch_symbol_hist(const uint8_t* codes, int64_t len, unsigned long long* hist,
+                               int sm_count, cudaStream_t s) {
+    if (len > 0) {
+        int64_t blocks = (len + 1023) / 1024;
+        const int64_t cap = (int64_t)sm_count * 4;
+        symbol_hist_kernel<<<(int)(blocks < cap ? blocks : cap), 256, 0, s>>>(codes, len, hist);
+    }
+    return cudaGetLastError();
+}
+
 cudaError_t launch_check_codes(const uint8_t* codes, int64_t len, int sigma, int* flags,
                                cudaStream_t s) {
     if (len > 0) {

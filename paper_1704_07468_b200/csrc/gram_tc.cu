@@ -436,9 +436,10 @@ __global__ void fill_round_kernel(uint32_t* fill, uint64_t ldd, uint32_t sc) {
 
 // After a Gram flush: count the issued MACs (K rounded to sc columns) and reset the fill.
 __global__ void fill_reset_kernel(uint32_t* fill, uint64_t ldd, uint64_t tile_macs,
-                                  unsigned long long* stats, uint32_t sc) {
+                                  unsigned long long* stats, uint32_t sc, int e2m1) {
     const uint64_t k = (min((uint64_t)fill[0], ldd) + sc - 1) / sc * sc;
     atomicAdd(&stats[ST_HEAVY_MACS], (unsigned long long)(tile_macs * k));
+    if (e2m1) atomicAdd(&stats[ST_HEAVY_MACS4], (unsigned long long)(tile_macs * k));
     fill[0] = 0;
     fill[1] = 0;
 }
@@ -535,12 +536,12 @@ cudaError_t gram_maps(uint8_t* D, int64_t n_pad, uint64_t ldd, int64_t* Cm, int6
 
 void launch_fill_reset(uint32_t* dense_fill, uint64_t ldd, uint64_t tile_macs,
                        unsigned long long* stats, cudaStream_t s) {
-    fill_reset_kernel<<<1, 1, 0, s>>>(dense_fill, ldd, tile_macs, stats, GT_KB);
+    fill_reset_kernel<<<1, 1, 0, s>>>(dense_fill, ldd, tile_macs, stats, GT_KB, 0);
 }
 
 void launch_fill_reset4(uint32_t* dense_fill, uint64_t ldd, uint64_t tile_macs,
                         unsigned long long* stats, cudaStream_t s) {
-    fill_reset_kernel<<<1, 1, 0, s>>>(dense_fill, ldd, tile_macs, stats, 2 * GT_KB);
+    fill_reset_kernel<<<1, 1, 0, s>>>(dense_fill, ldd, tile_macs, stats, 2 * GT_KB, 1);
 }
 
 cudaError_t launch_gram_flush(uint8_t* D, int64_t n_pad, uint64_t ldd, uint32_t* dense_fill,
@@ -561,7 +562,7 @@ cudaError_t launch_gram_flush(uint8_t* D, int64_t n_pad, uint64_t ldd, uint32_t*
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     fill_reset_kernel<<<1, 1, 0, s>>>(dense_fill, ldd, (uint64_t)ntiles * GT_M * GT_N, stats,
-                                      GT_KB);
+                                      GT_KB, 0);
     return cudaGetLastError();
 }
 

@@ -143,7 +143,7 @@ __device__ __forceinline__ uint32_t digit_peers(uint32_t d, uint32_t valid_mask)
 
 // Device counters of gakco_stats (int64 slots).
 enum { ST_KEYS = 0, ST_PASSKEYS, ST_TRIPLES, ST_GROUPS, ST_LIGHT_PAIRS, ST_HEAVY_GROUPS,
-       ST_HEAVY_MACS, ST_COUNT };
+       ST_HEAVY_MACS, ST_HEAVY_MACS4, ST_COUNT };
 
 // Error flags raised by kernels (bit mask in a device int).
 enum { EF_NEGATIVE_N = 1, EF_K_MISMATCH = 2, EF_BAD_SYMBOL = 4 };
@@ -208,6 +208,8 @@ cudaError_t launch_bucket_group(const BkArgs& a, const void* keys, bool k64, int
 
 // ---- launchers (each returns cudaGetLastError()) ----
 cudaError_t launch_gmer_index(const int64_t* gofs, int64_t N, uint32_t* gm_seq, cudaStream_t s);
+cudaError_t launch_symbol_hist(const uint8_t* codes, int64_t len, unsigned long long* hist,
+                               int sm_count, cudaStream_t s);
 cudaError_t launch_check_codes(const uint8_t* codes, int64_t len, int sigma, int* flags,
                                cudaStream_t s);
 // Keys are u64, or u32 (k64 = false) when key bits + sequence bits <= 32.

@@ -14,6 +14,7 @@
 #include <algorithm>
 #include <array>
 #include <climits>
+#include <cmath>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -102,13 +103,14 @@ struct gakco_plan {
     std::vector<int> key_bits;  // per level
 
     DevBuf keptsh, dense2, heavy2, hcount2, tseq2, tcnt2, gstart2, counts2, perm, iota, best, parent, Dgscr, Kdscr, codes, off, gofs, gmseq, keysA, keysB, hist, status, ctr, tseq, tcnt, gstart, gend,
-        counts, kept, stats, flags, kdiag, Cscr, Nmscr, Kscr, Knscr, heavy, hcount, dense, tiles,
+        counts, kept, stats, flags, kdiag, Cscr, Nmscr, Kscr, Knscr, heavy, hcount, dense, tiles, tiles4, symhist,
         lightacc, binrec, bincnt, win, bkH, bktot, bkbase, bkdesc, bktab, bktcnt, bkgs, bkocc;
     int64_t tiles_npad = -1;
     int tiles_pair = -1;
     int64_t tiles_na = -1;
+    int64_t tiles4_npad = -1, tiles4_na = -1;
     uint64_t dense_ldd = 0;
-    int ntiles = 0;
+    int ntiles = 0, ntiles4 = 0;
     uint32_t epoch = 1;
     uint32_t ctr_next = 0;
     static constexpr uint32_t CTR_SLOTS = 4096;
@@ -263,7 +265,7 @@ extern "C" void gakco_destroy(gakco_plan* p) {
                       &p->hist,  &p->status, &p->ctr,  &p->tseq,   &p->tcnt,  &p->gstart,
                       &p->gend,  &p->counts, &p->kept, &p->stats,  &p->flags, &p->kdiag,
                       &p->Cscr,  &p->Nmscr, &p->Kscr,  &p->Knscr, &p->heavy, &p->hcount,
-                      &p->dense, &p->tiles, &p->lightacc, &p->binrec, &p->bincnt,
+                      &p->dense, &p->tiles, &p->tiles4, &p->symhist, &p->lightacc, &p->binrec, &p->bincnt,
                       &p->win,   &p->bkH,   &p->bktot, &p->bkbase, &p->bkdesc, &p->bktab,
                       &p->bktcnt, &p->bkgs, &p->bkocc};
     for (DevBuf* b : bufs)
@@ -429,7 +431,11 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
     }
     p->last_grouping = hash_mode ? 2 : (p->sort_mode == 1 ? 1 : 0);
 
-    // corpus to device (+ symbol check)
+    // corpus to device (+ symbol check). The symbol histogram feeds the per-level
+    // Gram operand format (auto e2m1 below); counted only when that choice is open.
+    const bool need_hist = p->gram_fp4 == -1 && (p->gram_pair || NA > 0) && nmax > 0 &&
+                           (uint64_t)nmax * (uint64_t)nmax < (1ull << 24);
+    std::vector<unsigned long long> hist(256, 0);
     CK(p->ensure(p->codes, (size_t)L + 16, s));
     CK(p->ensure(p->flags, 64, s, /*zero=*/true));
     if (L > 0) {
@@ -440,9 +446,19 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
             CK(cudaMemcpyAsync(p->codes.p, codes, L, cudaMemcpyDeviceToDevice, s));
             LK(launch_check_codes((const uint8_t*)p->codes.p, L, p->sigma,
                                   (int*)p->flags.p + 1, s));
+            if (need_hist) {
+                CK(p->ensure(p->symhist, 256 * 8, s));
+                CK(cudaMemsetAsync(p->symhist.p, 0, 256 * 8, s));
+                LK(launch_symbol_hist((const uint8_t*)p->codes.p, L,
+                                      (unsigned long long*)p->symhist.p, p->sm_count, s));
+                CK(cudaMemcpyAsync(hist.data(), p->symhist.p, 256 * 8, cudaMemcpyDeviceToHost, s));
+                CK(cudaStreamSynchronize(s));
+            }
         } else {
-            for (int64_t i = 0; i < L; ++i)
+            for (int64_t i = 0; i < L; ++i) {
                 if (codes[i] >= p->sigma) return p->fail(GAKCO_E_SYMBOL, "a code is >= sigma");
+                hist[codes[i]] += 1;
+            }
             CK(cudaMemcpyAsync(p->codes.p, codes, L, cudaMemcpyHostToDevice, s));
         }
     }
@@ -492,15 +508,41 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
     const int64_t n_pad = gpair ? (N + 511) / 512 * 512 : (N + 255) / 256 * 256;
     // e2m1 Gram (kind::mxf4, gram2.cu): counts <= 4 exact in e2m1, f32 sums exact
     // below 2^24, so it applies while one mask's n_max^2 stays below 2^24; groups
-    // with a count > 4 stay on the light path
-    const bool fp4 = gpair && p->gram_fp4 != 0 && nmax > 0 &&
-                     (uint64_t)nmax * (uint64_t)nmax < (1ull << 24);
-    const uint64_t exact_lim = fp4 ? (1ull << 24) - 1 : (uint64_t)INT32_MAX;
-    const uint64_t slab_cols = fp4 ? 256 : 128;
-    int64_t heavy_min = p->heavy_min;
-    if (heavy_min == 0)
-        heavy_min = std::max<int64_t>(16, (int64_t)((fp4 ? 0.008 : 0.012) * (double)n_pad + 0.999));
-    const bool heavy_on = heavy_min < (int64_t)1 << 40 && N >= 2;
+    // with a count > 4 stay on the light path. Chosen per level: in auto mode only
+    // where even the most frequent masked key is rare within one sequence,
+    // n_max * p_max^(g-m) <= 1/8 with p_max the most frequent symbol's share (i.i.d.
+    // reading: counts > 4 then have Poisson tail < 3e-7 per sequence); levels with
+    // few effective keys (large m on DNA, Zipf text) use u8, whose counts reach 255.
+    const bool fp4_any_ok = gpair && p->gram_fp4 != 0 && nmax > 0 &&
+                            (uint64_t)nmax * (uint64_t)nmax < (1ull << 24);
+    double pmax = 1.0;
+    if (L > 0) {
+        unsigned long long hm = 0;
+        for (int c = 0; c < 256; ++c) hm = std::max(hm, hist[c]);
+        if (hm > 0) pmax = (double)hm / (double)L;
+    }
+    std::vector<char> fp4_lv(M + 1, 0);
+    bool fp4_any = false;
+    for (int m = 0; m <= M; ++m) {
+        if (!fp4_any_ok) break;
+        const double rep_ = (double)nmax * std::pow(pmax, (double)(g - m));
+        fp4_lv[m] = p->gram_fp4 == 1 || rep_ <= 0.125;
+    }
+    for (size_t i = 0; i < mine.size(); ++i) fp4_any |= fp4_lv[p->mask_level[mine[i]]] != 0;
+    auto exact_lim_of = [&](int m) -> uint64_t {
+        return fp4_lv[m] ? (1ull << 24) - 1 : (uint64_t)INT32_MAX;
+    };
+    auto slab_cols_of = [&](int m) -> uint64_t { return fp4_lv[m] ? 256 : 128; };
+    auto heavy_min_of = [&](int m) -> int64_t {
+        if (p->heavy_min != 0) return p->heavy_min;
+        return std::max<int64_t>(16, (int64_t)((fp4_lv[m] ? 0.008 : 0.012) * (double)n_pad + 0.999));
+    };
+    int64_t heavy_min_lo = INT64_MAX;
+    for (size_t i = 0; i < mine.size(); ++i)
+        heavy_min_lo = std::min(heavy_min_lo, heavy_min_of(p->mask_level[mine[i]]));
+    if (mine.empty()) heavy_min_lo = p->heavy_min != 0 ? p->heavy_min : 16;
+    const uint64_t exact_lim = fp4_any ? (1ull << 24) - 1 : (uint64_t)INT32_MAX;
+    const bool heavy_on = heavy_min_lo < (int64_t)1 << 40 && N >= 2;
 
     // batch size (keys cap; with the Gram on, s32 exactness: masks * n_max^2 < 2^31)
     // default: up to 64M keys (512 MB per key buffer): large launches measured
@@ -602,8 +644,9 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
                            cudaMemcpyHostToDevice, s));
     }
 
-    const int64_t light_limit = gram_ok ? heavy_min : INT64_MAX;
-    uint64_t rcap = 0;
+    // per level: groups of >= heavy_min_of(m) sequences go to the Gram
+    auto light_limit_of = [&](int m) -> int64_t { return gram_ok ? heavy_min_of(m) : INT64_MAX; };
+    uint64_t rcap8 = 0, rcap4 = 0;  // D columns of a u8 / e2m1 level (same bytes)
     if (gram_ok) {
         CK(p->ensure(p->hcount, 16, s, /*zero=*/true));
         if (pipe) CK(p->ensure(p->hcount2, 16, s, /*zero=*/true));
@@ -611,20 +654,33 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
         // columns than heavy groups can exist), accumulated over batches of a level
         // (every batch rounds its columns up to whole 128-column slabs)
         const uint64_t most =
-            (uint64_t)mine.size() * n / (uint64_t)heavy_min + 128 * (mine.size() + 1);
-        rcap = std::min<uint64_t>((4096ull << 20) * (fp4 ? 2 : 1) / (uint64_t)n_pad, most);
-        rcap = std::max<uint64_t>(slab_cols, (rcap + slab_cols - 1) / slab_cols * slab_cols);
-        CK(p->ensure(p->dense, (size_t)n_pad * rcap / (fp4 ? 2 : 1), s));
-        CK(p->ensure(p->heavy, rcap * sizeof(uint2), s));
+            (uint64_t)mine.size() * n / (uint64_t)heavy_min_lo + 256 * (mine.size() + 1);
+        rcap8 = std::min<uint64_t>((4096ull << 20) / (uint64_t)n_pad, most);
+        rcap8 = std::max<uint64_t>(128, (rcap8 + 127) / 128 * 128);
+        rcap4 = fp4_any ? std::min<uint64_t>(2 * rcap8, std::max<uint64_t>(256, (most + 255) / 256 * 256)) : 0;
+        rcap4 = rcap4 / 256 * 256;
+        const uint64_t dbytes = std::max<uint64_t>((uint64_t)n_pad * rcap8, (uint64_t)n_pad * rcap4 / 2);
+        const uint64_t hcols = std::max(rcap8, rcap4);
+        CK(p->ensure(p->dense, dbytes, s));
+        CK(p->ensure(p->heavy, hcols * sizeof(uint2), s));
         if (pipe) {
-            CK(p->ensure(p->dense2, (size_t)n_pad * rcap / (fp4 ? 2 : 1), s));
-            CK(p->ensure(p->heavy2, rcap * sizeof(uint2), s));
+            CK(p->ensure(p->dense2, dbytes, s));
+            CK(p->ensure(p->heavy2, hcols * sizeof(uint2), s));
         }
-        const int tkey = (rect ? 2 : (gpair ? 1 : 0)) + (fp4 ? 4 : 0);
+        if (fp4_any && (p->tiles4_npad != n_pad || (rect && p->tiles4_na != NA))) {
+            std::vector<int2> t = rect ? gram4_tiles_rect(NA, N - NA) : gram4_tiles(n_pad);
+            CK(p->ensure(p->tiles4, t.size() * sizeof(int2), s));
+            CK(cudaMemcpyAsync(p->tiles4.p, t.data(), t.size() * sizeof(int2),
+                               cudaMemcpyHostToDevice, s));
+            CK(cudaStreamSynchronize(s));
+            p->ntiles4 = (int)t.size();
+            p->tiles4_npad = n_pad;
+            p->tiles4_na = rect ? NA : -1;
+        }
+        const int tkey = rect ? 2 : (gpair ? 1 : 0);
         if (p->tiles_npad != n_pad || p->tiles_pair != tkey || (rect && p->tiles_na != NA)) {
-            std::vector<int2> t = fp4 ? (rect ? gram4_tiles_rect(NA, N - NA) : gram4_tiles(n_pad))
-                                  : rect ? gram2_tiles_rect(NA, N - NA)
-                                         : (gpair ? gram2_tiles(n_pad) : gram_tiles(n_pad));
+            std::vector<int2> t = rect ? gram2_tiles_rect(NA, N - NA)
+                                       : (gpair ? gram2_tiles(n_pad) : gram_tiles(n_pad));
             CK(p->ensure(p->tiles, t.size() * sizeof(int2), s));
             CK(cudaMemcpyAsync(p->tiles.p, t.data(), t.size() * sizeof(int2),
                                cudaMemcpyHostToDevice, s));
@@ -687,8 +743,11 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
     auto dense_p = [&]() { return (uint8_t*)(dslot ? p->dense2.p : p->dense.p); };
     auto heavy_p = [&]() { return (uint2*)(dslot ? p->heavy2.p : p->heavy.p); };
     auto hcount_p = [&]() { return (uint32_t*)(dslot ? p->hcount2.p : p->hcount.p); };
-    const uint64_t mask_lim =
-        gram_ok ? std::max<uint64_t>(1, exact_lim / ((uint64_t)nmax * nmax)) : 0;
+    auto mask_lim_of = [&](int m) -> uint64_t {
+        return gram_ok ? std::max<uint64_t>(1, exact_lim_of(m) / ((uint64_t)nmax * nmax)) : 0;
+    };
+    auto rcap_of = [&](int m) -> uint64_t { return fp4_lv[m] ? rcap4 : rcap8; };
+    int64_t fp4_used = 0;  // levels whose Gram ran on e2m1
     auto flush = [&]() -> gakco_status {
         if (dense_m < 0 || dense_bound == 0) return GAKCO_OK;
         if (pipe) {  // every build of this slot (s2) precedes its Gram (s3)
@@ -698,10 +757,12 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
         cudaEvent_t ah = nullptr;
         p->stage_begin(s3, &ah);
         p->launches += 1;  // + fill_reset
-        if (fp4)
+        const uint64_t rcap = rcap_of(dense_m);
+        if (fp4_lv[dense_m]) {
+            fp4_used |= 1ll << dense_m;
             LK(launch_gram4_flush(dense_p(), n_pad, rcap, hcount_p(), level_ptr(dense_m), N,
-                                  (const int2*)p->tiles.p, p->ntiles, p->sm_count, stats, s3, NA));
-        else if (gpair)
+                                  (const int2*)p->tiles4.p, p->ntiles4, p->sm_count, stats, s3, NA));
+        } else if (gpair)
             LK(launch_gram2_flush(dense_p(), n_pad, rcap, hcount_p(), level_ptr(dense_m), N,
                                   (const int2*)p->tiles.p, p->ntiles, p->sm_count, stats, s3, NA));
         else
@@ -823,8 +884,9 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
         int64_t* Dm = diag_ptr(m);  // C_m(X,X) at Dm[X * dstride]
         cudaEvent_t a = nullptr;
         if (gram_ok && n > 0) {
-            const uint64_t bnd = (uint64_t)nmask * n / (uint64_t)heavy_min + slab_cols;
-            if (dense_m != m || dense_bound + bnd > rcap || dense_masks + nmask > mask_lim) {
+            const uint64_t bnd = (uint64_t)nmask * n / (uint64_t)heavy_min_of(m) + slab_cols_of(m);
+            if (dense_m != m || dense_bound + bnd > rcap_of(m) ||
+                dense_masks + nmask > mask_lim_of(m)) {
                 gakco_status fs = flush();
                 if (fs != GAKCO_OK) return fs;
             }
@@ -956,18 +1018,18 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
                 CK(cudaStreamWaitEvent(s2, p->ev_seg[bi], 0));
             }
             p->stage_begin(s2, &a);
-            LK(launch_light(so, n * nmask / 2 + 1, light_limit, N, (uint32_t*)p->lightacc.p,
-                            heavy_p(), rcap, hcount_p(), bins,
+            LK(launch_light(so, n * nmask / 2 + 1, light_limit_of(m), N, (uint32_t*)p->lightacc.p,
+                            heavy_p(), rcap_of(m), hcount_p(), bins,
                             (uint32_t)p->light_flat, NA,
                             perm_active ? (const uint32_t*)p->perm.p : nullptr,
-                            fp4 ? 4u : 255u, stats, p->sm_count, s2));
+                            fp4_lv[m] ? 4u : 255u, stats, p->sm_count, s2));
             p->stage_end(s2, S_LIGHT, a);
             if (gram_ok) {
                 p->stage_begin(s2, &a);
                 p->launches += 1;  // + fill_round
-                LK(launch_build_dense(so, heavy_p(), hcount_p(), dense_p(), n_pad, rcap,
+                LK(launch_build_dense(so, heavy_p(), hcount_p(), dense_p(), n_pad, rcap_of(m),
                                       hash_mode ? 0 : 1,
-                                      fp4 ? 1 : 0, p->sm_count, s2));
+                                      fp4_lv[m] ? 1 : 0, p->sm_count, s2));
                 p->stage_end(s2, S_DENSE, a);
             }
             if (pipe) CK(cudaEventRecord(p->ev_light[bi], s2));
@@ -997,7 +1059,7 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
     p->host_stats.sort_passes32 = passkeys32;
     p->host_stats.grouping = p->last_grouping;
     p->host_stats.n_pad = gram_ok ? n_pad : 0;
-    p->host_stats.gram_fp4 = gram_ok && fp4 ? 1 : 0;
+    p->host_stats.gram_fp4 = gram_ok ? fp4_used : 0;
     p->after_accumulate = true;
     return GAKCO_OK;
 #undef CK
@@ -1242,6 +1304,7 @@ extern "C" gakco_status gakco_get_stats(gakco_plan* p, gakco_stats* out) {
         r.light_pairs = (int64_t)d[ST_LIGHT_PAIRS];
         r.heavy_groups = (int64_t)d[ST_HEAVY_GROUPS];
         r.heavy_macs = (int64_t)d[ST_HEAVY_MACS];
+        r.heavy_macs_fp4 = (int64_t)d[ST_HEAVY_MACS4];
     }
     double* ms[S_NSTAGE] = {&r.ms_encode, &r.ms_sort,     &r.ms_segment, &r.ms_light,
                             &r.ms_heavy,  &r.ms_epilogue, &r.ms_dense};

@@ -54,7 +54,7 @@ class gakco_stats(ctypes.Structure):
         (n, ctypes.c_int64) for n in (
             "n_encode", "n_sort", "n_segment", "n_light", "n_heavy", "n_epilogue", "keys32",
             "sort_passes32", "grouping")] + [("ms_dense", ctypes.c_double)] + [
-        (n, ctypes.c_int64) for n in ("n_dense", "n_pad", "gram_fp4")]
+        (n, ctypes.c_int64) for n in ("n_dense", "n_pad", "gram_fp4", "heavy_macs_fp4")]
 
     def as_dict(self):
         return {n: getattr(self, n) for n, _ in self._fields_}

@@ -113,6 +113,46 @@ def test_heavy_light_equivalence(gk, oracle_lib):
         assert_parity(run(gk, cp, g, k, M), ref)
 
 
+def _fp4_levels(cp, g, M):
+    """The documented auto policy (include/gakco.h GAKCO_OPT_GRAM_FP4): level m uses
+    e2m1 when n_max * p_max^(g-m) <= 1/8."""
+    lens = np.diff(cp.offsets)
+    nmax = int(max(0, (lens - g + 1).max())) if len(lens) else 0
+    pmax = np.bincount(cp.codes, minlength=256).max() / max(1, len(cp.codes))
+    return sum(1 << m for m in range(M + 1) if nmax * pmax ** (g - m) <= 0.125)
+
+
+def test_gram_format_per_level(gk, oracle_lib):
+    """Auto Gram operand format is chosen per level: e2m1 where keys are rare within a
+    sequence, u8 where counts > 4 are common (few effective keys: high m on DNA, Zipf
+    text). Mixed plans keep parity; host and device codes choose the same formats."""
+    import torch
+    rng = np.random.default_rng(131)
+    dna = sc.uniform(300, 90, 4, 5)
+    zipf = sc.gen_text(7, 260, 60, 120)
+    for cp, g, k, M in [(dna, 8, 2, 6), (zipf, 6, 1, 5)]:
+        ref = oracle_lib.compute(cp, g, k, M)
+        want = _fp4_levels(cp, g, M)
+        assert 0 < want < (1 << (M + 1)) - 1  # a mixed plan
+        r = run(gk, cp, g, k, M, heavy_min_seqs=2)
+        assert_parity(r, ref)
+        assert r["stats"]["gram_fp4"] == want
+        assert 0 < r["stats"]["heavy_macs_fp4"] < r["stats"]["heavy_macs"]
+        # device-resident codes: histogram on the device, same choice
+        plan = gk.Plan(cp.sigma, g, k, M)
+        plan.set_option(gk.GAKCO_OPT_HEAVY_MIN_SEQS, 2)
+        rd = gk.kernel_matrix(torch.from_numpy(cp.codes).cuda(), cp.offsets, cp.sigma, g, k,
+                              M, plan=plan)
+        assert plan.stats()["gram_fp4"] == want
+        plan.close()
+        assert np.array_equal(rd["C"].cpu().numpy(), ref["C"])
+        # forced formats
+        assert run(gk, cp, g, k, M, heavy_min_seqs=2, gram_fp4=0)["stats"]["gram_fp4"] == 0
+        assert run(gk, cp, g, k, M, heavy_min_seqs=2, gram_fp4=1)["stats"]["gram_fp4"] == \
+            (1 << (M + 1)) - 1
+    del rng
+
+
 def test_light_flat_threshold(gk, oracle_lib):
     """Light groups enumerated flattened across a warp (s <= flat) or from
     registers one group per warp: every threshold gives the oracle's result."""
