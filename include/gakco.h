@@ -62,12 +62,14 @@ typedef enum {
                                      a huge value = never (all light); 2 = all heavy */
     GAKCO_OPT_BATCH_KEYS = 2,     /* max keys (masks x g-mers) per batch; 0 = auto */
     GAKCO_OPT_TIMING = 3,         /* 1 = record per-stage CUDA events (gakco_get_stats) */
-    GAKCO_OPT_SORT = 4,           /* grouping of masked keys: -1 = automatic (default; = 0,
+    GAKCO_OPT_SORT = 4,           /* grouping of masked keys: -1 = automatic (default; = 3,
                                      measured fastest), 0 = LSD radix sort,
-                                     chunked two-kernel passes, 1 = LSD onesweep with
+                                     chunked two-kernel passes (v1), 1 = LSD onesweep with
                                      decoupled look-back, 2 = hash partition + shared-memory
-                                     hash grouping (falls back to 0 where it does not apply:
-                                     g*ceil(log2 sigma) > 64 or > 16M g-mers) */
+                                     hash grouping (falls back to the LSD sort where it does
+                                     not apply: g*ceil(log2 sigma) > 64 or > 16M g-mers),
+                                     3/4/5 = chunked LSD v2 (tiles streamed by bulk copies;
+                                     ranking by shared atomicOr match / match.any / ballots) */
     GAKCO_OPT_SORT_CTAS_PER_SM = 5, /* chunked pass grid size in CTAs per SM (default 4) */
     GAKCO_OPT_LIGHT_BINS = 6,     /* light updates binned by accumulator block (ablation /
                                      test knob): <= 0 = never (default; measured slower on

@@ -225,6 +225,9 @@ cudaError_t launch_onesweep(const uint64_t* in, uint64_t* out, uint64_t n, int n
                             const uint32_t* hist, int pass, int npass, uint64_t* status,
                             uint32_t* ctr, uint32_t epoch, cudaStream_t s);
 // Chunked LSD pass (radix_hist + radix_scatter); hist: >= (target_ctas + nseg) * 256 u32.
+cudaError_t launch_radix_chunked2(const void* in, void* out, bool k64, uint64_t n, int nseg,
+                                  int shift, uint32_t* hist, int target_ctas, int rank_mode,
+                                  cudaStream_t s);
 cudaError_t launch_radix_chunked(const void* in, void* out, bool k64, uint64_t n, int nseg,
                                  int shift, uint32_t* hist, int target_ctas, cudaStream_t s);
 // counters: 2 u32 (triples, groups) reserved per tile; zeroed by the launcher.

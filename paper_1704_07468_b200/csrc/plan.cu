@@ -298,7 +298,7 @@ extern "C" gakco_status gakco_set_option(gakco_plan* p, int option, int64_t valu
             p->batch_keys = value;
             return GAKCO_OK;
         case GAKCO_OPT_SORT:
-            if (value < -1 || value > 2) return p->fail(GAKCO_E_ARG, "sort must be -1..2");
+            if (value < -1 || value > 5) return p->fail(GAKCO_E_ARG, "sort must be -1..5");
             p->sort_mode = (int)value;
             return GAKCO_OK;
         case GAKCO_OPT_LIGHT_BINS:
@@ -559,8 +559,9 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
     const bool gram_ok =
         heavy_on && nmax > 0 && (uint64_t)nmax * (uint64_t)nmax <= (uint64_t)INT32_MAX;
     const uint64_t cap_keys = std::max<uint64_t>(1, std::min<uint64_t>(bmax_masks, mine.size()) * n);
-    CK(p->ensure(p->keysA, cap_keys * 8, s));
-    CK(p->ensure(p->keysB, cap_keys * 8, s));
+    // (+ slack: the bulk copies of radix_scatter2 read whole 16-byte words)
+    CK(p->ensure(p->keysA, cap_keys * 8 + 64, s));
+    CK(p->ensure(p->keysB, cap_keys * 8 + 64, s));
     CK(p->ensure(p->tseq, cap_keys * 4, s));
     CK(p->ensure(p->tcnt, cap_keys * 4, s));
     CK(p->ensure(p->gstart, (cap_keys / 2 + 2) * sizeof(uint2), s));  // group ranges
@@ -989,9 +990,16 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
                                        (uint64_t*)p->status.p, c, p->epoch++, s));
                 } else {
                     p->launches += 1;  // two kernels
-                    LK(launch_radix_chunked(in, outk, k64, n, nmask, sb + RADIX_BITS * q,
-                                            (uint32_t*)p->hist.p, p->sort_ctas_per_sm * p->sm_count,
-                                            s));
+                    // auto: the v2 pass (bulk-copied tiles, atomicOr-match ranking)
+                    if (p->sort_mode >= 3 || p->sort_mode == -1)
+                        LK(launch_radix_chunked2(in, outk, k64, n, nmask, sb + RADIX_BITS * q,
+                                                 (uint32_t*)p->hist.p,
+                                                 p->sort_ctas_per_sm * p->sm_count,
+                                                 p->sort_mode >= 3 ? p->sort_mode - 3 : 0, s));
+                    else
+                        LK(launch_radix_chunked(in, outk, k64, n, nmask, sb + RADIX_BITS * q,
+                                                (uint32_t*)p->hist.p,
+                                                p->sort_ctas_per_sm * p->sm_count, s));
                 }
                 std::swap(in, outk);
             }

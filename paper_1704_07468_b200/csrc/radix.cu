@@ -19,6 +19,7 @@
 #include <algorithm>
 
 #include "internal.cuh"
+#include "tc_ptx.cuh"
 
 namespace gk {
 
@@ -369,6 +370,282 @@ static cudaError_t radix_chunked(const K* in, K* out, uint64_t n, int nseg, int 
     radix_scatter_kernel<K><<<grid, RS_THREADS, rs_smem<K>(), s>>>(in, out, n, (uint32_t)cps, L,
                                                                    shift, hist);
     return cudaGetLastError();
+}
+
+// ============================================================================
+// radix_scatter2: the same chunked stable pass, restructured for instruction
+// count and latency (the v1 kernel issues ~4 warp instructions per key, spills,
+// and its shared atomicOr match serialises per lane: ncu 29 wavefronts per ATOMS):
+//   * 256 threads, 16 keys per thread, tiles of 4096 keys;
+//   * the next tile streams into shared memory with one cp.async.bulk (TMA 1D,
+//     mbarrier completion) while this one is ranked: no prefetch registers;
+//   * full tiles take a branch-free path (only a chunk's last tile is partial);
+//   * ranking by the shared atomicOr match (RANK = 0, default), match.any (1) or
+//     ballot multisplit (2) -- measured on Text: 112 / 145 / 124 ms per step's sort;
+//     a merged 64-bit {count | mask} bin (one atomic fewer) compiled to a CAS loop
+//     and took 251 ms;
+//     the per-warp digit counters are read-modify-written by the lowest peer;
+//   * the tile is reordered in place (its input buffer) and written out per digit
+//     run; each warp clears its own counters, so a tile needs 6 barriers.
+// ============================================================================
+constexpr int RS2_THREADS = 256;
+constexpr int RS2_WARPS = RS2_THREADS / 32;
+constexpr int RS2_ITEMS = 16;
+constexpr int RS2_TILE = RS2_THREADS * RS2_ITEMS;  // 4096 keys
+
+template <typename K>
+__host__ __device__ constexpr size_t rs2_buf_bytes() {
+    return RS2_TILE * sizeof(K) + 32;  // + alignment slack of the bulk copy
+}
+template <typename K>
+constexpr size_t rs2_smem() {
+    return 2 * rs2_buf_bytes<K>() + 2 * RADIX * 8 + 2 * RS2_WARPS * RADIX * 4 + RADIX * 4 +
+           16 * 4 + 2 * 8;
+}
+
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                         uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+        ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+// issue the bulk copy of keys [g0, g0 + cnt) (16-byte aligned window); returns the
+// element offset of key g0 inside the buffer
+template <typename K>
+__device__ __forceinline__ uint32_t rs2_issue(K* buf, const K* in, uint64_t g0, uint32_t cnt,
+                                              uint64_t* bar) {
+    const uintptr_t a0 = (uintptr_t)(in + g0), a1 = (uintptr_t)(in + g0 + cnt);
+    const uintptr_t b0 = a0 & ~(uintptr_t)15, b1 = (a1 + 15) & ~(uintptr_t)15;
+    const uint32_t bytes = (uint32_t)(b1 - b0);
+    mbar_expect_tx(bar, bytes);
+    bulk_g2s(buf, (const void*)b0, bytes, bar);
+    return (uint32_t)((a0 - b0) / sizeof(K));
+}
+
+template <typename K, int RANK, bool FULL>
+__device__ __forceinline__ void rs2_rank(const K (&keys)[RS2_ITEMS], uint32_t (&rank)[RS2_ITEMS],
+                                         int shift, uint32_t cnt, uint32_t* whist,
+                                         uint32_t* mbin, int w, int lane) {
+    const uint32_t lt = lanemask_lt();
+    if (RANK == 1) {
+        // all match.any first (independent: in flight together), then the counter chain
+#pragma unroll
+        for (int i = 0; i < RS2_ITEMS; ++i) {
+            const uint32_t idx = (uint32_t)(w * RS2_ITEMS * 32 + i * 32 + lane);
+            uint32_t d = (uint32_t)(keys[i] >> shift) & 0xffu;
+            if (!FULL && idx >= cnt) d = 0x100u;  // invalid lanes only match each other
+            rank[i] = __match_any_sync(0xffffffffu, d);
+        }
+#pragma unroll
+        for (int i = 0; i < RS2_ITEMS; ++i) {
+            const uint32_t idx = (uint32_t)(w * RS2_ITEMS * 32 + i * 32 + lane);
+            const bool valid = FULL || idx < cnt;
+            const uint32_t d = (uint32_t)(keys[i] >> shift) & 0xffu;
+            const uint32_t peers = rank[i];
+            const uint32_t prior = valid ? whist[d] : 0u;
+            __syncwarp();
+            if (valid && (peers & lt) == 0u) whist[d] = prior + __popc(peers);
+            __syncwarp();
+            rank[i] = prior + __popc(peers & lt);
+        }
+    } else if (RANK == 2) {
+        // ballot multisplit: peers from 8 votes, no shared atomics
+#pragma unroll
+        for (int i = 0; i < RS2_ITEMS; ++i) {
+            const uint32_t idx = (uint32_t)(w * RS2_ITEMS * 32 + i * 32 + lane);
+            const bool valid = FULL || idx < cnt;
+            const uint32_t d = (uint32_t)(keys[i] >> shift) & 0xffu;
+            const uint32_t peers = digit_peers(d, __ballot_sync(0xffffffffu, valid));
+            const uint32_t prior = valid ? whist[d] : 0u;
+            __syncwarp();
+            if (valid && (peers & lt) == 0u) whist[d] = prior + __popc(peers);
+            __syncwarp();
+            rank[i] = prior + __popc(peers & lt);
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < RS2_ITEMS; ++i) {
+            const uint32_t idx = (uint32_t)(w * RS2_ITEMS * 32 + i * 32 + lane);
+            const bool valid = FULL || idx < cnt;
+            const uint32_t d = (uint32_t)(keys[i] >> shift) & 0xffu;
+            if (valid) atomicOr(&mbin[d], 1u << lane);
+            __syncwarp();
+            const uint32_t peers = valid ? mbin[d] : 0u;
+            const uint32_t prior = valid ? whist[d] : 0u;
+            __syncwarp();
+            if (valid && (peers & lt) == 0u) {
+                whist[d] = prior + __popc(peers);
+                mbin[d] = 0u;
+            }
+            __syncwarp();
+            rank[i] = prior + __popc(peers & lt);
+        }
+    }
+}
+
+template <typename K, int RANK>
+__global__ void __launch_bounds__(RS2_THREADS, (sizeof(K) == 8 ? 2 : 3)) radix_scatter2_kernel(
+    const K* __restrict__ in, K* __restrict__ out, uint64_t n, uint32_t cps, uint64_t L,
+    int shift, const uint32_t* __restrict__ hist) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    K* const buf0 = (K*)smem;
+    K* const buf1 = (K*)(smem + rs2_buf_bytes<K>());
+    unsigned char* q = smem + 2 * rs2_buf_bytes<K>();
+    int64_t* s_run = (int64_t*)q;                                        // [RADIX]
+    int64_t* s_goff = s_run + RADIX;                                     // [RADIX]
+    uint32_t(*s_whist)[RADIX] = (uint32_t(*)[RADIX])(s_goff + RADIX);    // [WARPS][RADIX]
+    uint32_t* s_match = &s_whist[RS2_WARPS][0];                          // [WARPS][RADIX]
+    uint32_t* s_cnt = s_match + RS2_WARPS * RADIX;                       // [RADIX]
+    uint32_t* s_w = s_cnt + RADIX;                                       // [16]
+    uint64_t* s_bar = (uint64_t*)(s_w + 16);                             // [2]
+
+    const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+    const uint32_t seg = blockIdx.x / cps, c = blockIdx.x - seg * cps;
+    const uint64_t lo = (uint64_t)c * L;
+    const uint64_t hi = min(n, lo + L);
+    const uint64_t seg_base = (uint64_t)seg * n;
+    const K* src = in + seg_base;
+    const uint32_t ntile = hi > lo ? (uint32_t)((hi - lo + RS2_TILE - 1) / RS2_TILE) : 0u;
+
+    for (int i = tid; i < 2 * RS2_WARPS * RADIX; i += RS2_THREADS) (&s_whist[0][0])[i] = 0u;
+    if (tid == 0) {
+        mbar_init(&s_bar[0], 1);
+        mbar_init(&s_bar[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        for (uint32_t t = 0; t < 2 && t < ntile; ++t) {
+            const uint64_t g0 = lo + (uint64_t)t * RS2_TILE;
+            rs2_issue(t ? buf1 : buf0, src, g0, (uint32_t)min((uint64_t)RS2_TILE, hi - g0),
+                      &s_bar[t]);
+        }
+    }
+    // digit totals of the segment and this chunk's prefix (all chunks < c)
+    uint32_t tot = 0, pre = 0;
+    {
+        const uint32_t* h = hist + (uint64_t)seg * cps * RADIX + tid;
+        for (uint32_t cc = 0; cc < cps; ++cc) {
+            const uint32_t v = h[(uint64_t)cc * RADIX];
+            tot += v;
+            pre += cc < c ? v : 0u;
+        }
+    }
+    const uint32_t dbase = scan256_excl(tot, s_w);  // (its barriers also publish the inits)
+    s_run[tid] = (int64_t)dbase + pre;
+    // element offset of a tile's first key inside its buffer (16-byte aligned copies)
+    auto delta_of = [&](uint32_t t) -> uint32_t {
+        return (uint32_t)((((uintptr_t)(src + lo + (uint64_t)t * RS2_TILE)) & 15) / sizeof(K));
+    };
+    __syncthreads();
+
+    uint32_t* whist = s_whist[w];
+    uint32_t* mbin = s_match + w * RADIX;
+    for (uint32_t t = 0; t < ntile; ++t) {
+        const int b = (int)(t & 1u);
+        const uint64_t t0 = lo + (uint64_t)t * RS2_TILE;
+        const uint32_t cnt = (uint32_t)min((uint64_t)RS2_TILE, hi - t0);
+        K* buf = b ? buf1 : buf0;
+        mbar_wait(&s_bar[b], (t >> 1) & 1u);
+        const K* kin = buf + delta_of(t);
+        K keys[RS2_ITEMS];
+        uint32_t rank[RS2_ITEMS];
+#pragma unroll
+        for (int i = 0; i < RS2_ITEMS; ++i) {
+            const uint32_t idx = (uint32_t)(w * RS2_ITEMS * 32 + i * 32 + lane);
+            keys[i] = (cnt == RS2_TILE || idx < cnt) ? kin[idx] : (K)0;
+        }
+        if (cnt == RS2_TILE)
+            rs2_rank<K, RANK, true>(keys, rank, shift, cnt, whist, mbin, w, lane);
+        else
+            rs2_rank<K, RANK, false>(keys, rank, shift, cnt, whist, mbin, w, lane);
+        __syncthreads();  // (A) every warp's counters final; every key of buf read
+        // the other buffer's copy for tile t + 1 was issued long ago; this buffer's
+        // next tile (t + 2) can stream in once the reorder below is written out,
+        // which (C) orders; issue it there
+        uint32_t tcnt = 0;
+#pragma unroll
+        for (int ww = 0; ww < RS2_WARPS; ++ww) tcnt += s_whist[ww][tid];
+        s_cnt[tid] = tcnt;
+        const uint32_t doff = scan256_excl(tcnt, s_w);
+        {
+            uint32_t sum = doff;
+#pragma unroll
+            for (int ww = 0; ww < RS2_WARPS; ++ww) {
+                const uint32_t v = s_whist[ww][tid];
+                s_whist[ww][tid] = sum;
+                sum += v;
+            }
+            s_goff[tid] = s_run[tid] - (int64_t)doff;
+            s_run[tid] += tcnt;
+        }
+        __syncthreads();  // (B)
+#pragma unroll
+        for (int i = 0; i < RS2_ITEMS; ++i) {
+            const uint32_t idx = (uint32_t)(w * RS2_ITEMS * 32 + i * 32 + lane);
+            if (cnt == RS2_TILE || idx < cnt) {
+                const uint32_t d = (uint32_t)(keys[i] >> shift) & 0xffu;
+                buf[whist[d] + rank[i]] = keys[i];
+            }
+        }
+        __syncwarp();
+        // this warp's counters are no longer read by anyone: clear for the next tile
+#pragma unroll
+        for (int j = 0; j < RADIX / 32; ++j) whist[j * 32 + lane] = 0u;
+        __syncthreads();  // (C) tile reordered in buf
+        for (uint32_t j = tid; j < cnt; j += RS2_THREADS) {
+            const K k = buf[j];
+            const uint32_t d = (uint32_t)(k >> shift) & 0xffu;
+            out[seg_base + (uint64_t)(s_goff[d] + (int64_t)j)] = k;
+        }
+        if (t + 2 < ntile) {
+            // buf is free once every thread has written its share out
+            __syncthreads();  // (D)
+            const uint64_t g2 = lo + (uint64_t)(t + 2) * RS2_TILE;
+            if (tid == 0) {
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                rs2_issue(buf, src, g2, (uint32_t)min((uint64_t)RS2_TILE, hi - g2), &s_bar[b]);
+            }
+        }
+        // (the next tile's barrier A orders s_goff / s_cnt reuse)
+    }
+}
+
+template <typename K, int RANK>
+static cudaError_t radix_chunked2(const K* in, K* out, uint64_t n, int nseg, int shift,
+                                  uint32_t* hist, int target_ctas, cudaStream_t s) {
+    uint64_t tiles = (n + RS2_TILE - 1) / RS2_TILE;
+    uint64_t cps = std::max<uint64_t>(1, std::min<uint64_t>(tiles, (target_ctas + nseg - 1) / nseg));
+    uint64_t L = (tiles + cps - 1) / cps * RS2_TILE;
+    cps = (n + L - 1) / L;
+    const unsigned grid = (unsigned)(cps * nseg);
+    radix_hist_kernel<K><<<grid, RS_THREADS, 0, s>>>(in, n, (uint32_t)cps, L, shift, hist);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    cudaFuncSetAttribute(radix_scatter2_kernel<K, RANK>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rs2_smem<K>());
+    radix_scatter2_kernel<K, RANK><<<grid, RS2_THREADS, rs2_smem<K>(), s>>>(
+        in, out, n, (uint32_t)cps, L, shift, hist);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_radix_chunked2(const void* in, void* out, bool k64, uint64_t n, int nseg,
+                                  int shift, uint32_t* hist, int target_ctas, int rank_mode,
+                                  cudaStream_t s) {
+    if (n == 0 || nseg == 0) return cudaGetLastError();
+#define RS2_CASE(KT, R)                                                                  \
+    if (rank_mode == R)                                                                  \
+        return radix_chunked2<KT, R>((const KT*)in, (KT*)out, n, nseg, shift, hist, target_ctas, s);
+    if (k64) {
+        RS2_CASE(uint64_t, 1)
+        RS2_CASE(uint64_t, 2)
+        return radix_chunked2<uint64_t, 0>((const uint64_t*)in, (uint64_t*)out, n, nseg, shift,
+                                           hist, target_ctas, s);
+    }
+    RS2_CASE(uint32_t, 1)
+    RS2_CASE(uint32_t, 2)
+#undef RS2_CASE
+    return radix_chunked2<uint32_t, 0>((const uint32_t*)in, (uint32_t*)out, n, nseg, shift, hist,
+                                       target_ctas, s);
 }
 
 cudaError_t launch_radix_chunked(const void* in, void* out, bool k64, uint64_t n, int nseg,

@@ -209,21 +209,32 @@ def test_batch_size_invariance(gk, oracle_lib):
     for bk in (1, 4700, 3 * 4700 + 5, 1 << 20):
         assert_parity(run(gk, cp, 7, 5, 2, batch_keys=bk), ref)
         assert_parity(run(gk, cp, 7, 5, 2, batch_keys=bk, sort=1), ref)
+        assert_parity(run(gk, cp, 7, 5, 2, batch_keys=bk, sort=3), ref)
+        assert_parity(run(gk, cp, 7, 5, 2, batch_keys=bk, sort=4), ref)
         assert_parity(run(gk, cp, 7, 5, 2, batch_keys=bk, pipeline=0), ref)
         assert_parity(run(gk, cp, 7, 5, 2, batch_keys=bk, level_order=0), ref)
         assert_parity(run(gk, cp, 7, 5, 2, batch_keys=bk, heavy_min_seqs=2), ref)
 
 
 def test_sort_modes_ragged(gk, oracle_lib):
-    """The chunked LSD pass and the onesweep pass give identical results on
-    segments spanning many tiles, with ragged tails and odd alignments."""
+    """The chunked LSD passes (v1; v2 with bulk-copied tiles, atomicOr or match.any
+    ranking) and the onesweep pass give identical results on segments spanning many
+    tiles, with ragged tails and odd alignments (u32 and u64 composites)."""
     rng = np.random.default_rng(104)
     seqs = [rng.integers(0, 20, size=int(rng.integers(0, 3000))) for _ in range(37)]
     cp = sc.from_sequences(20, seqs)
     ref = oracle_lib.compute(cp, 8, 4, 4)
-    for bk in (0, 50001):
-        assert_parity(run(gk, cp, 8, 4, 4, batch_keys=bk, sort=0), ref)
-        assert_parity(run(gk, cp, 8, 4, 4, batch_keys=bk, sort=1), ref)
+    for bk in (0, 50001, 4097 * 3):
+        for mode in (0, 1, 3, 4, 5):
+            assert_parity(run(gk, cp, 8, 4, 4, batch_keys=bk, sort=mode), ref)
+    cp4 = sc.from_sequences(4, [rng.integers(0, 4, size=int(rng.integers(0, 5000)))
+                                for _ in range(23)])
+    ref4 = oracle_lib.compute(cp4, 6, 3, 3)
+    for bk in (0, 12289):
+        for mode in (0, 3, 4, 5):
+            r = run(gk, cp4, 6, 3, 3, batch_keys=bk, sort=mode)
+            assert r["stats"]["keys32"] > 0
+            assert_parity(r, ref4)
 
 
 def test_grouping_modes(gk, oracle_lib):
@@ -238,11 +249,11 @@ def test_grouping_modes(gk, oracle_lib):
         M = int(rng.integers(0, g + 1))
         cp = sc.random_small(rng, sigma, n_max=200, l_max=300)
         ref = oracle_lib.compute(cp, g, k, M)
-        for mode in (0, 1, 2):
+        for mode in (0, 1, 2, 3, 4, 5):
             r = run(gk, cp, g, k, M, sort=mode)
             assert_parity(r, ref)
             if r["stats"]["keys"] > 0:
-                assert r["stats"]["grouping"] == mode
+                assert r["stats"]["grouping"] == (mode if mode < 3 else 0)
         assert run(gk, cp, g, k, M)["stats"]["grouping"] == 0
 
 
