@@ -31,17 +31,15 @@ __global__ void __launch_bounds__(SEG_THREADS) segment_kernel(
     __shared__ uint32_t s_w[16];
     __shared__ uint32_t s_gpos[SEG_TILE];
     __shared__ uint32_t s_tx[SEG_TILE], s_tc[SEG_TILE];  // the tile's triples, staged
-    __shared__ uint32_t s_first_gh, s_base_t, s_base_g, s_tail;
+    __shared__ uint32_t s_first_gh, s_base_t, s_base_g, s_tail, s_gend_done;
+    __shared__ uint32_t s_wmin[SEG_THREADS / 32], s_beyond;
+    __shared__ unsigned long long s_gend;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint64_t tile0 = (uint64_t)blockIdx.x * SEG_TILE;
     const uint64_t base = tile0 + (uint64_t)tid * SEG_ITEMS;
+    const uint32_t lbase = (uint32_t)tid * SEG_ITEMS;  // tile-local index of item 0
     const uint64_t tile_end = min(tile0 + SEG_TILE, total);
     const uint64_t seqmask = (1ull << sb) - 1ull;
-    if (tid == 0) {
-        s_first_gh = 0xffffffffu;
-        s_tail = 0;
-    }
-    __syncthreads();
 
     K cur[SEG_ITEMS];
     if (base + SEG_ITEMS <= total) {
@@ -63,106 +61,134 @@ __global__ void __launch_bounds__(SEG_THREADS) segment_kernel(
     uint64_t seg_lo = base < total ? base / n * n : 0, seg_hi = seg_lo + n;
     const K prev = (base < total && base != seg_lo) ? keys[base - 1] : (K)0;
 
-    uint32_t th_bits = 0, gh_bits = 0, multi_bits = 0;
-    uint32_t cnt[SEG_ITEMS];
+    // 1. head flags: a triple head where the composite changes, a group head where
+    //    the key bits change (both at every segment start)
+    uint32_t th_bits = 0, gh_bits = 0;
 #pragma unroll
     for (int i = 0; i < SEG_ITEMS; ++i) {
         const uint64_t idx = base + i;
-        const K c0 = cur[i];
-        const K p0 = i == 0 ? prev : cur[i - 1];
-        cnt[i] = 0;
-        if (idx >= total) continue;
+        if (idx >= total) break;
         if (idx >= seg_hi) {
             seg_lo = seg_hi;
             seg_hi += n;
         }
+        const K c0 = cur[i];
+        const K p0 = i == 0 ? prev : cur[i - 1];
         const bool first = idx == seg_lo;
-        if (!first && p0 == c0) continue;  // not a triple head
-        const bool gh = first || (p0 >> sb) != (c0 >> sb);
-        // run end j and the key that follows it
-        const uint64_t seg_end = seg_hi;
-        uint64_t j = idx + 1;
-        K nk = (K)~c0;
-        bool found = false;
+        if (first || p0 != c0) th_bits |= 1u << i;
+        if (first || ((p0 ^ c0) >> sb) != 0) gh_bits |= 1u << i;
+    }
+    if (tid == 0) {
+        s_first_gh = 0xffffffffu;
+        s_tail = 0;
+        // first triple head at or after the tile end, tile-local (index << 1 | is a
+        // group head): a segment start, a key change, or the end of the crossing run
+        uint32_t b = (uint32_t)(tile_end - tile0) << 1 | 1u;
+        if (tile_end < total && tile_end % n != 0) {
+            const K lk = keys[tile_end - 1];
+            const uint64_t seg_end = (tile_end / n + 1) * n;
+            uint64_t q = tile_end;
+            while (q < seg_end && keys[q] == lk) ++q;
+            const bool g = q == seg_end || ((keys[q] ^ lk) >> sb) != 0;
+            b = (uint32_t)(q - tile0) << 1 | (g ? 1u : 0u);
+        }
+        s_beyond = b;
+    }
+    // 2. the first triple head after this thread's items: suffix minimum over the
+    //    later threads of the tile, then s_beyond
+    uint32_t mine = 0xffffffffu;
+    if (th_bits) {
+        const int f = __ffs(th_bits) - 1;
+        mine = (lbase + f) << 1 | ((gh_bits >> f) & 1u);
+    }
+    uint32_t suf = mine;
 #pragma unroll
-        for (int k = i + 1; k < SEG_ITEMS; ++k) {
-            if (!found && base + k < seg_end) {
-                if (cur[k] != c0) {
-                    found = true;
-                    nk = cur[k];
-                } else {
-                    ++j;
-                }
-            }
-        }
-        if (!found && j < seg_end) {
-            while (j < seg_end) {
-                const K kk = keys[j];
-                if (kk != c0) {
-                    nk = kk;
-                    break;
-                }
-                ++j;
-            }
-        }
-        const uint32_t c = (uint32_t)(j - idx);
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t v = __shfl_down_sync(0xffffffffu, suf, o);
+        if (lane + o < 32) suf = min(suf, v);
+    }
+    if (lane == 0) s_wmin[warp] = suf;
+    __syncthreads();
+    uint32_t nxt = __shfl_down_sync(0xffffffffu, suf, 1);
+    if (lane == 31) nxt = 0xffffffffu;
+    {
+        uint32_t later = s_beyond;
+#pragma unroll
+        for (int ww = 1; ww < SEG_THREADS / 32; ++ww)
+            if (ww > warp) later = min(later, s_wmin[ww]);
+        nxt = min(nxt, later);
+    }
+    // 3. backward over the items: run length = next head - head; a group head's
+    //    group is shared (>= 2 sequences) iff the next triple is not a group head
+    uint32_t multi_bits = 0;
+    uint32_t cnt[SEG_ITEMS];
+#pragma unroll
+    for (int i = SEG_ITEMS - 1; i >= 0; --i) {
+        cnt[i] = 0;
+        if (!((th_bits >> i) & 1u)) continue;
+        const uint32_t li = lbase + i;
+        const uint32_t c = (nxt >> 1) - li;
         cnt[i] = c;
+        const uint32_t gh = (gh_bits >> i) & 1u;
+        if (!gh || !(nxt & 1u)) multi_bits |= 1u << i;
         if (c >= 2) {
-            const int64_t x = (int64_t)(c0 & seqmask);
+            const int64_t x = (int64_t)(cur[i] & seqmask);
             atomicAdd((unsigned long long*)&diag[x * dstride], (unsigned long long)c * c - c);
         }
-        th_bits |= 1u << i;
-        if (!gh || (j < seg_end && (nk >> sb) == (c0 >> sb))) multi_bits |= 1u << i;
-        if (gh) {
-            gh_bits |= 1u << i;
-            atomicMin(&s_first_gh, (uint32_t)(idx - tile0));
-        }
+        nxt = li << 1 | gh;
     }
+    if (gh_bits) atomicMin(&s_first_gh, lbase + (__ffs(gh_bits) - 1));
     __syncthreads();
     // keys before the tile's first group head belong to a group owned by an
     // earlier tile: not emitted here
     const uint32_t fgh = s_first_gh;
     uint32_t emit_t = 0, emit_g = 0;
-#pragma unroll
-    for (int i = 0; i < SEG_ITEMS; ++i) {
-        const bool own = fgh != 0xffffffffu && (uint32_t)(base + i - tile0) >= fgh;
-        if (own && ((th_bits & multi_bits) >> i & 1u)) {
-            emit_t |= 1u << i;
-            if ((gh_bits >> i) & 1u) emit_g |= 1u << i;
-        }
+    if (fgh != 0xffffffffu) {
+        const uint32_t own = lbase >= fgh ? 0xffu : (fgh - lbase < SEG_ITEMS ? (0xffu << (fgh - lbase)) & 0xffu : 0u);
+        emit_t = th_bits & multi_bits & own;
+        emit_g = emit_t & gh_bits;
     }
     uint32_t agg_t, agg_g;
     const uint32_t off_t = scan256_excl(__popc(emit_t), s_w, &agg_t);
     const uint32_t off_g = scan256_excl(__popc(emit_g), s_w, &agg_g);
 
-    // the last group starting here may run past the tile: count its tail triples
-    const bool has_gh = fgh != 0xffffffffu;
-    const bool crossing = has_gh && tile_end < total && tile_end % n != 0 &&
-                          (keys[tile_end] >> sb) == (keys[tile_end - 1] >> sb);
-    uint64_t gend_key = tile_end;  // one past the crossing group's last key
-    if (crossing && warp == 0) {
-        const K gkey = keys[tile_end - 1] >> sb;
-        const uint64_t seg_end = (tile_end / n + 1) * n;
-        uint32_t nt = 0;
-        uint64_t e = tile_end;
-        K last = keys[tile_end - 1];
-        while (true) {
-            const uint64_t q = e + lane;
-            const K kk = q < seg_end ? keys[q] : (K)~(K)0;
-            const bool in = q < seg_end && (kk >> sb) == gkey;
-            const uint32_t inm = __ballot_sync(0xffffffffu, in);
-            const K pk = __shfl_up_sync(0xffffffffu, kk, 1);
-            const K pv = lane == 0 ? last : pk;
-            nt += __popc(__ballot_sync(0xffffffffu, in && kk != pv));
-            const uint32_t run = ~inm ? __ffs(~inm) - 1 : 32;  // leading in-group lanes
-            if (run < 32) {
-                gend_key = e + run;
+    // 4. the last group starting here may run past the tile: all threads scan its
+    //    tail in tile-sized chunks, counting its triple heads
+    const bool crossing = fgh != 0xffffffffu && tile_end < total && tile_end % n != 0 &&
+                          (((keys[tile_end] ^ keys[tile_end - 1]) >> sb) == 0);
+    uint64_t gend = tile_end;  // one past the crossing group's last key
+    K gkey = 0;
+    uint64_t seg_end_t = 0;
+    if (crossing) {  // (block-uniform)
+        gkey = keys[tile_end - 1] >> sb;
+        seg_end_t = (tile_end / n + 1) * n;
+        uint32_t heads = 0;
+        for (uint64_t e = tile_end;; e += SEG_TILE) {
+            if (tid == 0) {
+                s_gend = ~0ull;
+                s_gend_done = 0;
+            }
+            __syncthreads();
+            uint32_t h = 0;
+#pragma unroll
+            for (int i = 0; i < SEG_ITEMS; ++i) {
+                const uint64_t q = e + lbase + i;
+                const K kk = q < seg_end_t ? keys[q] : (K)~(K)0;
+                const bool in = q < seg_end_t && (kk >> sb) == gkey;
+                if (!in) {
+                    atomicMin(&s_gend, (unsigned long long)q);
+                    break;
+                }
+                h += kk != keys[q - 1];
+            }
+            if (h) atomicAdd(&s_tail, h);
+            __syncthreads();
+            if (s_gend != ~0ull) {
+                gend = s_gend;
                 break;
             }
-            last = __shfl_sync(0xffffffffu, kk, 31);
-            e += 32;
         }
-        if (lane == 0) s_tail = nt;
+        (void)heads;
     }
     __syncthreads();
     const uint32_t tail = s_tail;
@@ -173,7 +199,8 @@ __global__ void __launch_bounds__(SEG_THREADS) segment_kernel(
         if (agg_g) atomicAdd(&stats[ST_GROUPS], (unsigned long long)agg_g);
     }
     __syncthreads();
-    // triples staged in shared memory, then written with coalesced stores
+    const uint32_t base_t = s_base_t, base_g = s_base_g;
+    // 5. triples staged in shared memory, then written with coalesced stores
     uint32_t li = off_t, gl = off_g;
 #pragma unroll
     for (int i = 0; i < SEG_ITEMS; ++i) {
@@ -181,42 +208,48 @@ __global__ void __launch_bounds__(SEG_THREADS) segment_kernel(
             const uint32_t x = (uint32_t)(cur[i] & seqmask);
             s_tx[li] = x | (((gh_bits >> i) & 1u) << 31);
             s_tc[li] = cnt[i];
-            if (emit_g & (1u << i)) s_gpos[gl++] = s_base_t + li;
+            if (emit_g & (1u << i)) s_gpos[gl++] = base_t + li;
             ++li;
         }
     }
     __syncthreads();
     for (uint32_t j = tid; j < agg_t; j += SEG_THREADS) {
-        so.tseq[s_base_t + j] = s_tx[j];
-        so.tcnt[s_base_t + j] = s_tc[j];
+        so.tseq[base_t + j] = s_tx[j];
+        so.tcnt[base_t + j] = s_tc[j];
     }
     // group ranges: a group runs to the next group's first triple (or the end of
     // this tile's triples, its tail included)
-    const uint32_t tend = s_base_t + agg_t + tail;
+    const uint32_t tend = base_t + agg_t + tail;
     for (uint32_t g = tid; g < agg_g; g += SEG_THREADS)
-        so.groups[s_base_g + g] = make_uint2(s_gpos[g], g + 1 < agg_g ? s_gpos[g + 1] : tend);
-    // tail triples of the crossing group (warp 0), after this tile's triples
-    if (tail && warp == 0) {
-        const uint64_t seg_end = (tile_end / n + 1) * n;
-        uint32_t w = s_base_t + agg_t;
-        K last = keys[tile_end - 1];
-        for (uint64_t e = tile_end; e < gend_key; e += 32) {
-            const uint64_t q = e + lane;
-            const bool in = q < gend_key;
-            const K kk = in ? keys[q] : (K)0;
-            const K pk = __shfl_up_sync(0xffffffffu, kk, 1);
-            const K pv = lane == 0 ? last : pk;
-            const bool head = in && kk != pv;
-            const uint32_t hm = __ballot_sync(0xffffffffu, head);
-            if (head) {
-                uint64_t r = q + 1;
-                while (r < seg_end && keys[r] == kk) ++r;
-                const uint32_t pos = w + __popc(hm & lanemask_lt());
-                so.tseq[pos] = (uint32_t)(kk & seqmask);
-                so.tcnt[pos] = (uint32_t)(r - q);
+        so.groups[base_g + g] = make_uint2(s_gpos[g], g + 1 < agg_g ? s_gpos[g + 1] : tend);
+    // 6. tail triples of the crossing group, after this tile's triples, in order:
+    //    chunk by chunk, a block scan of the heads places them
+    if (tail) {  // (block-uniform)
+        uint32_t wpos = base_t + agg_t;
+        for (uint64_t e = tile_end; e < gend; e += SEG_TILE) {
+            uint32_t hb = 0;
+            K kv[SEG_ITEMS];
+#pragma unroll
+            for (int i = 0; i < SEG_ITEMS; ++i) {
+                const uint64_t q = e + lbase + i;
+                kv[i] = q < gend ? keys[q] : (K)0;
+                if (q < gend && kv[i] != keys[q - 1]) hb |= 1u << i;
             }
-            w += __popc(hm);
-            last = __shfl_sync(0xffffffffu, kk, 31);
+            uint32_t chunk_heads;
+            const uint32_t off = scan256_excl(__popc(hb), s_w, &chunk_heads);
+            uint32_t pos = wpos + off;
+#pragma unroll
+            for (int i = 0; i < SEG_ITEMS; ++i) {
+                if (hb & (1u << i)) {
+                    const uint64_t q = e + lbase + i;
+                    uint64_t r = q + 1;
+                    while (r < gend && keys[r] == kv[i]) ++r;
+                    so.tseq[pos] = (uint32_t)(kv[i] & seqmask);
+                    so.tcnt[pos] = (uint32_t)(r - q);
+                    ++pos;
+                }
+            }
+            wpos += chunk_heads;
         }
     }
 }
