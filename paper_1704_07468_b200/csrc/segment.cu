@@ -25,14 +25,14 @@
 namespace gk {
 
 template <typename K>
-__global__ void __launch_bounds__(SEG_THREADS) segment_kernel(
+__global__ void __launch_bounds__(SEG_THREADS, 5) segment_kernel(
     const K* __restrict__ keys, uint64_t n, uint64_t total, int sb, int64_t dstride,
     int64_t* diag, uint32_t* counters, SegmentOut so, unsigned long long* stats) {
     __shared__ uint32_t s_w[16];
     __shared__ uint32_t s_gpos[SEG_TILE];
     __shared__ uint32_t s_tx[SEG_TILE], s_tc[SEG_TILE];  // the tile's triples, staged
     __shared__ uint32_t s_first_gh, s_base_t, s_base_g, s_tail, s_gend_done;
-    __shared__ uint32_t s_wmin[SEG_THREADS / 32], s_beyond;
+    __shared__ uint32_t s_wmin[SEG_THREADS / 32], s_beyond, s_cross;
     __shared__ unsigned long long s_gend;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const uint64_t tile0 = (uint64_t)blockIdx.x * SEG_TILE;
@@ -55,6 +55,14 @@ __global__ void __launch_bounds__(SEG_THREADS) segment_kernel(
     } else {
 #pragma unroll
         for (int i = 0; i < SEG_ITEMS; ++i) cur[i] = base + i < total ? keys[base + i] : (K)0;
+    }
+    // the last warp also fetches the 32 keys after the tile (the run / group
+    // crossing its end), in flight together with the tile's own loads
+    const bool has_next = tile_end < total && tile_end % n != 0;
+    K ext = (K)0, lk = (K)0;
+    if (warp == SEG_THREADS / 32 - 1 && has_next) {
+        lk = keys[tile_end - 1];
+        ext = tile_end + lane < total ? keys[tile_end + lane] : (K)~lk;
     }
     // segment (mask) bounds of this thread's first item: one 64-bit division per
     // thread; consecutive items cross at most one boundary each (n >= 1)
@@ -81,18 +89,34 @@ __global__ void __launch_bounds__(SEG_THREADS) segment_kernel(
     if (tid == 0) {
         s_first_gh = 0xffffffffu;
         s_tail = 0;
+    }
+    if (warp == SEG_THREADS / 32 - 1) {
         // first triple head at or after the tile end, tile-local (index << 1 | is a
         // group head): a segment start, a key change, or the end of the crossing run
         uint32_t b = (uint32_t)(tile_end - tile0) << 1 | 1u;
-        if (tile_end < total && tile_end % n != 0) {
-            const K lk = keys[tile_end - 1];
+        bool cross = false;
+        if (has_next) {  // (warp-uniform)
             const uint64_t seg_end = (tile_end / n + 1) * n;
-            uint64_t q = tile_end;
-            while (q < seg_end && keys[q] == lk) ++q;
-            const bool g = q == seg_end || ((keys[q] ^ lk) >> sb) != 0;
-            b = (uint32_t)(q - tile0) << 1 | (g ? 1u : 0u);
+            cross = ((__shfl_sync(0xffffffffu, ext, 0) ^ lk) >> sb) == 0;
+            for (uint64_t e = tile_end;; e += 32) {
+                const uint64_t q = e + lane;
+                const K kk = e == tile_end ? ext : (q < seg_end ? keys[q] : (K)~lk);
+                const bool stop = q >= seg_end || kk != lk;
+                const uint32_t sm = __ballot_sync(0xffffffffu, stop);
+                if (sm) {
+                    const int j = __ffs(sm) - 1;
+                    const K kj = __shfl_sync(0xffffffffu, kk, j);
+                    const uint64_t qj = e + j;
+                    const bool g = qj >= seg_end || ((kj ^ lk) >> sb) != 0;
+                    b = (uint32_t)(qj - tile0) << 1 | (g ? 1u : 0u);
+                    break;
+                }
+            }
         }
-        s_beyond = b;
+        if (lane == 0) {
+            s_beyond = b;
+            s_cross = cross ? 1u : 0u;
+        }
     }
     // 2. the first triple head after this thread's items: suffix minimum over the
     //    later threads of the tile, then s_beyond
@@ -154,8 +178,7 @@ __global__ void __launch_bounds__(SEG_THREADS) segment_kernel(
 
     // 4. the last group starting here may run past the tile: all threads scan its
     //    tail in tile-sized chunks, counting its triple heads
-    const bool crossing = fgh != 0xffffffffu && tile_end < total && tile_end % n != 0 &&
-                          (((keys[tile_end] ^ keys[tile_end - 1]) >> sb) == 0);
+    const bool crossing = fgh != 0xffffffffu && s_cross != 0;
     uint64_t gend = tile_end;  // one past the crossing group's last key
     K gkey = 0;
     uint64_t seg_end_t = 0;
