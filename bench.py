@@ -47,9 +47,10 @@ def args_():
                     help="target seconds of oracle work per CPU sample")
     ap.add_argument("--heavy-min", type=int, default=0)
     ap.add_argument("--batch-keys", type=int, default=0)
-    ap.add_argument("--sort", type=int, default=None, choices=[-1, 0, 1, 2, 3, 4, 5],
+    ap.add_argument("--sort", type=int, default=None, choices=[-1, 0, 1, 2, 3, 4, 5, 6],
                     help="grouping: -1 auto, 0 chunked LSD sort, 1 onesweep LSD, 2 hash partition, "
-                         "3/4/5 chunked LSD v2 (bulk-copy tiles; atomicOr / match.any / ballot ranking)")
+                         "3/4/5 chunked LSD v2 (bulk-copy tiles; atomicOr / match.any / ballot ranking), "
+                         "6 mask trie (shared leading-position passes)")
     ap.add_argument("--sort-ctas", type=int, default=0)
     ap.add_argument("--light-flat", type=int, default=0,
                     help="light groups of <= this many sequences share a warp (1..32)")

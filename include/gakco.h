@@ -69,7 +69,11 @@ typedef enum {
                                      hash grouping (falls back to the LSD sort where it does
                                      not apply: g*ceil(log2 sigma) > 64 or > 16M g-mers),
                                      3/4/5 = chunked LSD v2 (tiles streamed by bulk copies;
-                                     ranking by shared atomicOr match / match.any / ballots) */
+                                     ranking by shared atomicOr match / match.any / ballots),
+                                     6 = mask trie: per-position stable passes over packed
+                                     windows + sequence ids, passes of common leading kept
+                                     positions shared between masks (auto when a mask has
+                                     >= 2M g-mers and g*ceil(log2 sigma) <= 64) */
     GAKCO_OPT_SORT_CTAS_PER_SM = 5, /* chunked pass grid size in CTAs per SM (default 4) */
     GAKCO_OPT_LIGHT_BINS = 6,     /* light updates binned by accumulator block (ablation /
                                      test knob): <= 0 = never (default; measured slower on
@@ -118,7 +122,8 @@ typedef struct {
     int64_t keys32;         /* of `keys`, those carried as 32-bit composites */
     int64_t sort_passes32;  /* of `sort_passes`, those over 32-bit composites */
     int64_t grouping;       /* path of the last accumulate: 0 chunked LSD sort,
-                               1 onesweep LSD sort, 2 hash partition (bucket.cu) */
+                               1 onesweep LSD sort, 2 hash partition (bucket.cu),
+                               3 mask trie */
     double ms_dense;        /* building the dense u8 count columns of heavy groups */
     int64_t n_dense;
     int64_t n_pad;          /* rows of the dense count matrix (0: no tensor-core Gram) */

@@ -225,13 +225,21 @@ cudaError_t launch_onesweep(const uint64_t* in, uint64_t* out, uint64_t n, int n
                             const uint32_t* hist, int pass, int npass, uint64_t* status,
                             uint32_t* ctr, uint32_t epoch, cudaStream_t s);
 // Chunked LSD pass (radix_hist + radix_scatter); hist: >= (target_ctas + nseg) * 256 u32.
+cudaError_t launch_trie_pass(const uint64_t* win, uint64_t* wout, const void* sin, void* sout,
+                             bool seq16, uint64_t n, int shift, uint32_t dmask, uint64_t omask,
+                             uint32_t* hist, int target_ctas, cudaStream_t s, int* nlaunch);
+cudaError_t launch_seq16(const uint32_t* a, uint16_t* b, uint64_t n, int sm_count,
+                         cudaStream_t s);
 cudaError_t launch_radix_chunked2(const void* in, void* out, bool k64, uint64_t n, int nseg,
                                   int shift, uint32_t* hist, int target_ctas, int rank_mode,
-                                  cudaStream_t s);
+                                  cudaStream_t s, int* nlaunch);
 cudaError_t launch_radix_chunked(const void* in, void* out, bool k64, uint64_t n, int nseg,
                                  int shift, uint32_t* hist, int target_ctas, cudaStream_t s);
 // counters: 2 u32 (triples, groups) reserved per tile; zeroed by the launcher.
 // diag[X * dstride] receives the within-sequence repeat term of C_m(X,X)
+cudaError_t launch_segment_soa(const uint64_t* w, const void* sq, bool seq16, uint64_t n,
+                               int nseg, int64_t dstride, int64_t* diag, uint32_t* counters,
+                               SegmentOut so, unsigned long long* stats, cudaStream_t s);
 cudaError_t launch_segment(const void* keys, bool k64, uint64_t n, int nseg, int sb,
                            int64_t dstride, int64_t* diag, uint32_t* counters, SegmentOut so,
                            unsigned long long* stats, cudaStream_t s);

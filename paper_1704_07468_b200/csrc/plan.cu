@@ -102,7 +102,7 @@ struct gakco_plan {
     std::vector<std::array<uint8_t, GMAX>> mask_kept;
     std::vector<int> key_bits;  // per level
 
-    DevBuf keptsh, dense2, heavy2, hcount2, tseq2, tcnt2, gstart2, counts2, perm, iota, best, parent, Dgscr, Kdscr, codes, off, gofs, gmseq, keysA, keysB, hist, status, ctr, tseq, tcnt, gstart, gend,
+    DevBuf trieS0, trieW, trieS, keptsh, dense2, heavy2, hcount2, tseq2, tcnt2, gstart2, counts2, perm, iota, best, parent, Dgscr, Kdscr, codes, off, gofs, gmseq, keysA, keysB, hist, status, ctr, tseq, tcnt, gstart, gend,
         counts, kept, stats, flags, kdiag, Cscr, Nmscr, Kscr, Knscr, heavy, hcount, dense, tiles, tiles4, symhist,
         lightacc, binrec, bincnt, win, bkH, bktot, bkbase, bkdesc, bktab, bktcnt, bkgs, bkocc;
     int64_t tiles_npad = -1;
@@ -265,7 +265,7 @@ extern "C" void gakco_destroy(gakco_plan* p) {
                       &p->hist,  &p->status, &p->ctr,  &p->tseq,   &p->tcnt,  &p->gstart,
                       &p->gend,  &p->counts, &p->kept, &p->stats,  &p->flags, &p->kdiag,
                       &p->Cscr,  &p->Nmscr, &p->Kscr,  &p->Knscr, &p->heavy, &p->hcount,
-                      &p->dense, &p->tiles, &p->tiles4, &p->symhist, &p->lightacc, &p->binrec, &p->bincnt,
+                      &p->dense, &p->tiles, &p->tiles4, &p->symhist, &p->trieS0, &p->trieW, &p->trieS, &p->lightacc, &p->binrec, &p->bincnt,
                       &p->win,   &p->bkH,   &p->bktot, &p->bkbase, &p->bkdesc, &p->bktab,
                       &p->bktcnt, &p->bkgs, &p->bkocc};
     for (DevBuf* b : bufs)
@@ -298,7 +298,7 @@ extern "C" gakco_status gakco_set_option(gakco_plan* p, int option, int64_t valu
             p->batch_keys = value;
             return GAKCO_OK;
         case GAKCO_OPT_SORT:
-            if (value < -1 || value > 5) return p->fail(GAKCO_E_ARG, "sort must be -1..5");
+            if (value < -1 || value > 6) return p->fail(GAKCO_E_ARG, "sort must be -1..6");
             p->sort_mode = (int)value;
             return GAKCO_OK;
         case GAKCO_OPT_LIGHT_BINS:
@@ -488,6 +488,26 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
         std::stable_sort(mine.begin(), mine.end(), [&](int a, int b) {
             return p->mask_level[a] > p->mask_level[b];
         });
+    // mask trie (GAKCO_OPT_SORT 6): within a level, masks in lexicographic order of
+    // their kept positions, so consecutive masks share the passes of their common
+    // leading positions
+    // (auto: the trie for masks of >= 2M g-mers, where its single-mask passes fill the
+    // machine -- Text 180 -> 151 ms, Scale 246 -> 238 ms; the batched LSD passes win
+    // below: DNA, Protein)
+    const bool trie = (p->sort_mode == 6 || (p->sort_mode == -1 && n >= (2ull << 20))) &&
+                      !hash_mode && n > 0 && g * bits <= 64;
+    if (trie) {
+        size_t a0 = 0;
+        while (a0 < mine.size()) {
+            size_t a1 = a0;
+            while (a1 < mine.size() && p->mask_level[mine[a1]] == p->mask_level[mine[a0]]) ++a1;
+            std::stable_sort(mine.begin() + a0, mine.begin() + a1, [&](int a, int b) {
+                return p->mask_kept[a] < p->mask_kept[b];
+            });
+            a0 = a1;
+        }
+        p->last_grouping = 3;
+    }
     // (pageable host staging: cudaMemcpyAsync returns once the source is copied,
     // so the member buffers can be reused without a stream sync)
     std::vector<uint8_t>& kept_h = p->kept_h;
@@ -594,7 +614,7 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
     CK(p->ensure(p->hist, std::max<uint64_t>(std::min<uint64_t>(bmax_masks, mine.size() + 1) *
                                                  MAXPASS * RADIX * 4,
                                              (uint64_t)(p->sort_ctas_per_sm * p->sm_count + 64 +
-                                                        bmax_masks) *
+                                                        2 * bmax_masks) *
                                                  RADIX * 4),
                  s));
     {
@@ -704,6 +724,21 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
     // encode from packed g-mer windows when g * bits <= 64 (LSD path, not onesweep,
     // whose encoder also counts the digit histograms)
     const bool use_win = !hash_mode && n > 0 && g * bits <= 64 && p->sort_mode != 1;
+    // trie buffers: root sequence ids (u16 when N <= 65536), one level of the pass
+    // stack per kept position (windows + ids); the batch's leaves go to keysA / keysB
+    const bool seq16 = N <= 65536;
+    const size_t ssz = seq16 ? 2 : 4;
+    std::array<int, GMAX> stack_pos{};
+    int stack_depth = 0;
+    if (trie) {
+        CK(p->ensure(p->trieS0, n * ssz + 64, s));
+        if (seq16)
+            LK(launch_seq16((const uint32_t*)p->gmseq.p, (uint16_t*)p->trieS0.p, n, p->sm_count, s));
+        else
+            CK(cudaMemcpyAsync(p->trieS0.p, p->gmseq.p, n * 4, cudaMemcpyDeviceToDevice, s));
+        CK(p->ensure(p->trieW, (size_t)g * n * 8 + 64, s));
+        CK(p->ensure(p->trieS, (size_t)g * n * ssz + 64, s));
+    }
     if (use_win) {
         CK(p->ensure(p->win, n * 8, s));
         std::vector<uint8_t> ksh(mine.size() * GMAX + GMAX, 0);
@@ -962,6 +997,54 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
             LK(launch_bucket_group(ba, p->keysA.p, k64, dstride, Dm, so, bs, stats, p->sm_count,
                                    s));
             p->stage_end(s, S_SEGMENT, a);
+        } else if (n > 0 && trie) {
+            // mask trie: pass t of a mask is a stable pass by the symbol at its t-th kept
+            // position (ascending); the passes of a common leading-position prefix are
+            // shared with the previous mask (stack), the last pass writes the masked
+            // windows to the mask's segment of the batch
+            const int kk = g - m;
+            const uint32_t dmask = (1u << bits) - 1u;
+            p->stage_begin(s, &a);
+            for (size_t j = pos; j < end; ++j) {
+                const uint8_t* kept = p->mask_kept[mine[j]].data();
+                uint64_t* wleaf = (uint64_t*)p->keysA.p + (j - pos) * n;
+                uint8_t* sleaf = (uint8_t*)p->keysB.p + (j - pos) * n * ssz;
+                if (kk == 0) {  // no kept position: one key, identity order
+                    CK(cudaMemsetAsync(wleaf, 0, n * 8, s));
+                    CK(cudaMemcpyAsync(sleaf, p->trieS0.p, n * ssz, cudaMemcpyDeviceToDevice, s));
+                    continue;
+                }
+                uint64_t kmask = 0;
+                for (int r = 0; r < kk; ++r) kmask |= (uint64_t)dmask << (bits * (g - 1 - kept[r]));
+                int d = 0;
+                while (d < stack_depth && d < kk - 1 && stack_pos[d] == kept[d]) ++d;
+                for (int t = d; t < kk; ++t) {
+                    const bool leaf = t == kk - 1;
+                    const uint64_t* wi = t == 0 ? (const uint64_t*)p->win.p
+                                                : (const uint64_t*)p->trieW.p + (size_t)(t - 1) * n;
+                    const void* si = t == 0 ? p->trieS0.p
+                                            : (const void*)((const uint8_t*)p->trieS.p + (size_t)(t - 1) * n * ssz);
+                    uint64_t* wo = leaf ? wleaf : (uint64_t*)p->trieW.p + (size_t)t * n;
+                    void* so_ = leaf ? (void*)sleaf : (void*)((uint8_t*)p->trieS.p + (size_t)t * n * ssz);
+                    int nl = 2;
+                    LK(launch_trie_pass(wi, wo, si, so_, seq16, n, bits * (g - 1 - kept[t]), dmask,
+                                        leaf ? kmask : ~0ull, (uint32_t*)p->hist.p,
+                                        p->sort_ctas_per_sm * p->sm_count, s, &nl));
+                    p->launches += nl - 1;  // hist (+ chunk scan) + scatter
+                    if (!leaf) stack_pos[t] = kept[t];
+                }
+                stack_depth = kk - 1;
+                passkeys += (int64_t)(kk - d) * (int64_t)n;
+            }
+            p->stage_end(s, S_SORT, a);
+            {
+                gakco_status ws = wait_buf();
+                if (ws != GAKCO_OK) return ws;
+            }
+            p->stage_begin(s, &a);
+            LK(launch_segment_soa((const uint64_t*)p->keysA.p, p->keysB.p, seq16, n, nmask, dstride,
+                                  Dm, so.counts, so, stats, s));
+            p->stage_end(s, S_SEGMENT, a);
         } else if (n > 0) {
             p->stage_begin(s, &a);
             const bool onesweep = p->sort_mode == 1;
@@ -989,14 +1072,19 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
                                        sb + RADIX_BITS * q, (const uint32_t*)p->hist.p, q, npass,
                                        (uint64_t*)p->status.p, c, p->epoch++, s));
                 } else {
-                    p->launches += 1;  // two kernels
                     // auto: the v2 pass (bulk-copied tiles, atomicOr-match ranking)
-                    if (p->sort_mode >= 3 || p->sort_mode == -1)
+                    const bool v2 = p->sort_mode >= 3 || p->sort_mode == -1;
+                    if (v2) {  // hist (+ a chunk scan when many chunks) + scatter
+                        int nl = 2;
                         LK(launch_radix_chunked2(in, outk, k64, n, nmask, sb + RADIX_BITS * q,
                                                  (uint32_t*)p->hist.p,
                                                  p->sort_ctas_per_sm * p->sm_count,
-                                                 p->sort_mode >= 3 ? p->sort_mode - 3 : 0, s));
-                    else
+                                                 p->sort_mode >= 3 ? p->sort_mode - 3 : 0, s, &nl));
+                        p->launches += nl - 1;
+                    } else {
+                        p->launches += 1;  // hist + scatter
+                    }
+                    if (!v2)
                         LK(launch_radix_chunked(in, outk, k64, n, nmask, sb + RADIX_BITS * q,
                                                 (uint32_t*)p->hist.p,
                                                 p->sort_ctas_per_sm * p->sm_count, s));

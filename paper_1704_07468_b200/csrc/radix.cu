@@ -17,6 +17,7 @@
 //   4. it reorders the tile by digit in shared memory and writes each digit's run
 //      contiguously to  seg*n + digit_base[d] + prefix[d] + local offset.
 #include <algorithm>
+#include <type_traits>
 
 #include "internal.cuh"
 #include "tc_ptx.cuh"
@@ -186,7 +187,7 @@ constexpr int RS_WARPS = RS_THREADS / 32;
 template <typename K>
 __global__ void __launch_bounds__(RS_THREADS) radix_hist_kernel(
     const K* __restrict__ in, uint64_t n, uint32_t cps, uint64_t L, int shift,
-    uint32_t* __restrict__ hist) {
+    uint32_t* __restrict__ hist, uint32_t dmask = 0xffu) {
     constexpr int E = 16 / sizeof(K);  // keys per 16-byte load
     __shared__ uint32_t s_h[RS_WARPS][RADIX];
     const int tid = threadIdx.x, w = tid >> 5;
@@ -200,7 +201,7 @@ __global__ void __launch_bounds__(RS_THREADS) radix_hist_kernel(
         // 16-byte loads on the aligned body, scalars on the edges
         uint64_t a = lo;
         while (a < hi && ((uintptr_t)(p + a) & 15)) {
-            if (tid == 0) atomicAdd(&s_h[0][(uint32_t)(p[a] >> shift) & 0xff], 1u);
+            if (tid == 0) atomicAdd(&s_h[0][(uint32_t)(p[a] >> shift) & dmask], 1u);
             ++a;
         }
         const uint64_t nv = (hi - a) / E;
@@ -209,10 +210,10 @@ __global__ void __launch_bounds__(RS_THREADS) radix_hist_kernel(
             const uint4 q = v[i];
             const K* kq = (const K*)&q;
 #pragma unroll
-            for (int e = 0; e < E; ++e) atomicAdd(&s_h[w][(uint32_t)(kq[e] >> shift) & 0xff], 1u);
+            for (int e = 0; e < E; ++e) atomicAdd(&s_h[w][(uint32_t)(kq[e] >> shift) & dmask], 1u);
         }
         for (uint64_t i = a + nv * E + tid; i < hi; i += RS_THREADS)
-            atomicAdd(&s_h[w][(uint32_t)(p[i] >> shift) & 0xff], 1u);
+            atomicAdd(&s_h[w][(uint32_t)(p[i] >> shift) & dmask], 1u);
     }
     __syncthreads();
     if (tid < RADIX) {
@@ -397,10 +398,20 @@ template <typename K>
 __host__ __device__ constexpr size_t rs2_buf_bytes() {
     return RS2_TILE * sizeof(K) + 32;  // + alignment slack of the bulk copy
 }
-template <typename K>
+// payload moved along with the keys (the mask-trie passes: sequence ids); NoPay: none
+struct NoPay {};
+template <typename P>
+__host__ __device__ constexpr bool rs2_haspay() {
+    return !std::is_same<P, NoPay>::value;
+}
+template <typename P>
+__host__ __device__ constexpr size_t rs2_pbuf_bytes() {
+    return rs2_haspay<P>() ? RS2_TILE * sizeof(P) + 32 : 0;
+}
+template <typename K, typename P = NoPay>
 constexpr size_t rs2_smem() {
-    return 2 * rs2_buf_bytes<K>() + 2 * RADIX * 8 + 2 * RS2_WARPS * RADIX * 4 + RADIX * 4 +
-           16 * 4 + 2 * 8;
+    return 2 * rs2_buf_bytes<K>() + 3 * rs2_pbuf_bytes<P>() + 2 * RADIX * 8 +
+           2 * RS2_WARPS * RADIX * 4 + RADIX * 4 + 16 * 4 + 2 * 8;
 }
 
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
@@ -414,19 +425,30 @@ __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t by
 // issue the bulk copy of keys [g0, g0 + cnt) (16-byte aligned window); returns the
 // element offset of key g0 inside the buffer
 template <typename K>
-__device__ __forceinline__ uint32_t rs2_issue(K* buf, const K* in, uint64_t g0, uint32_t cnt,
-                                              uint64_t* bar) {
+__device__ __forceinline__ uint32_t rs2_bytes(const K* in, uint64_t g0, uint32_t cnt) {
     const uintptr_t a0 = (uintptr_t)(in + g0), a1 = (uintptr_t)(in + g0 + cnt);
-    const uintptr_t b0 = a0 & ~(uintptr_t)15, b1 = (a1 + 15) & ~(uintptr_t)15;
-    const uint32_t bytes = (uint32_t)(b1 - b0);
+    return (uint32_t)(((a1 + 15) & ~(uintptr_t)15) - (a0 & ~(uintptr_t)15));
+}
+template <typename K>
+__device__ __forceinline__ void rs2_copy(K* buf, const K* in, uint64_t g0, uint32_t cnt,
+                                         uint64_t* bar) {
+    const uintptr_t a0 = (uintptr_t)(in + g0);
+    bulk_g2s(buf, (const void*)(a0 & ~(uintptr_t)15), rs2_bytes(in, g0, cnt), bar);
+}
+// one barrier completes the key copy and (with a payload) the payload copy
+template <typename K, typename P>
+__device__ __forceinline__ void rs2_issue(K* buf, const K* in, P* pbuf, const P* pin, uint64_t g0,
+                                          uint32_t cnt, uint64_t* bar) {
+    uint32_t bytes = rs2_bytes(in, g0, cnt);
+    if constexpr (rs2_haspay<P>()) bytes += rs2_bytes(pin, g0, cnt);
     mbar_expect_tx(bar, bytes);
-    bulk_g2s(buf, (const void*)b0, bytes, bar);
-    return (uint32_t)((a0 - b0) / sizeof(K));
+    rs2_copy(buf, in, g0, cnt, bar);
+    if constexpr (rs2_haspay<P>()) rs2_copy(pbuf, pin, g0, cnt, bar);
 }
 
 template <typename K, int RANK, bool FULL>
 __device__ __forceinline__ void rs2_rank(const K (&keys)[RS2_ITEMS], uint32_t (&rank)[RS2_ITEMS],
-                                         int shift, uint32_t cnt, uint32_t* whist,
+                                         int shift, uint32_t dmask, uint32_t cnt, uint32_t* whist,
                                          uint32_t* mbin, int w, int lane) {
     const uint32_t lt = lanemask_lt();
     if (RANK == 1) {
@@ -434,7 +456,7 @@ __device__ __forceinline__ void rs2_rank(const K (&keys)[RS2_ITEMS], uint32_t (&
 #pragma unroll
         for (int i = 0; i < RS2_ITEMS; ++i) {
             const uint32_t idx = (uint32_t)(w * RS2_ITEMS * 32 + i * 32 + lane);
-            uint32_t d = (uint32_t)(keys[i] >> shift) & 0xffu;
+            uint32_t d = (uint32_t)(keys[i] >> shift) & dmask;
             if (!FULL && idx >= cnt) d = 0x100u;  // invalid lanes only match each other
             rank[i] = __match_any_sync(0xffffffffu, d);
         }
@@ -442,7 +464,7 @@ __device__ __forceinline__ void rs2_rank(const K (&keys)[RS2_ITEMS], uint32_t (&
         for (int i = 0; i < RS2_ITEMS; ++i) {
             const uint32_t idx = (uint32_t)(w * RS2_ITEMS * 32 + i * 32 + lane);
             const bool valid = FULL || idx < cnt;
-            const uint32_t d = (uint32_t)(keys[i] >> shift) & 0xffu;
+            const uint32_t d = (uint32_t)(keys[i] >> shift) & dmask;
             const uint32_t peers = rank[i];
             const uint32_t prior = valid ? whist[d] : 0u;
             __syncwarp();
@@ -456,7 +478,7 @@ __device__ __forceinline__ void rs2_rank(const K (&keys)[RS2_ITEMS], uint32_t (&
         for (int i = 0; i < RS2_ITEMS; ++i) {
             const uint32_t idx = (uint32_t)(w * RS2_ITEMS * 32 + i * 32 + lane);
             const bool valid = FULL || idx < cnt;
-            const uint32_t d = (uint32_t)(keys[i] >> shift) & 0xffu;
+            const uint32_t d = (uint32_t)(keys[i] >> shift) & dmask;
             const uint32_t peers = digit_peers(d, __ballot_sync(0xffffffffu, valid));
             const uint32_t prior = valid ? whist[d] : 0u;
             __syncwarp();
@@ -469,7 +491,7 @@ __device__ __forceinline__ void rs2_rank(const K (&keys)[RS2_ITEMS], uint32_t (&
         for (int i = 0; i < RS2_ITEMS; ++i) {
             const uint32_t idx = (uint32_t)(w * RS2_ITEMS * 32 + i * 32 + lane);
             const bool valid = FULL || idx < cnt;
-            const uint32_t d = (uint32_t)(keys[i] >> shift) & 0xffu;
+            const uint32_t d = (uint32_t)(keys[i] >> shift) & dmask;
             if (valid) atomicOr(&mbin[d], 1u << lane);
             __syncwarp();
             const uint32_t peers = valid ? mbin[d] : 0u;
@@ -485,14 +507,19 @@ __device__ __forceinline__ void rs2_rank(const K (&keys)[RS2_ITEMS], uint32_t (&
     }
 }
 
-template <typename K, int RANK>
+template <typename K, typename P, int RANK>
 __global__ void __launch_bounds__(RS2_THREADS, (sizeof(K) == 8 ? 2 : 3)) radix_scatter2_kernel(
-    const K* __restrict__ in, K* __restrict__ out, uint64_t n, uint32_t cps, uint64_t L,
-    int shift, const uint32_t* __restrict__ hist) {
+    const K* __restrict__ in, K* __restrict__ out, const P* __restrict__ pin, P* __restrict__ pout,
+    uint64_t n, uint32_t cps, uint64_t L, int shift, uint32_t dmask,
+    const uint32_t* __restrict__ hist, K omask, int prescanned) {
+    constexpr bool HASP = rs2_haspay<P>();
     extern __shared__ __align__(16) unsigned char smem[];
     K* const buf0 = (K*)smem;
     K* const buf1 = (K*)(smem + rs2_buf_bytes<K>());
-    unsigned char* q = smem + 2 * rs2_buf_bytes<K>();
+    P* const pbuf0 = (P*)(smem + 2 * rs2_buf_bytes<K>());
+    P* const pbuf1 = (P*)(smem + 2 * rs2_buf_bytes<K>() + rs2_pbuf_bytes<P>());
+    P* const s_pout = (P*)(smem + 2 * rs2_buf_bytes<K>() + 2 * rs2_pbuf_bytes<P>());
+    unsigned char* q = smem + 2 * rs2_buf_bytes<K>() + 3 * rs2_pbuf_bytes<P>();
     int64_t* s_run = (int64_t*)q;                                        // [RADIX]
     int64_t* s_goff = s_run + RADIX;                                     // [RADIX]
     uint32_t(*s_whist)[RADIX] = (uint32_t(*)[RADIX])(s_goff + RADIX);    // [WARPS][RADIX]
@@ -507,6 +534,7 @@ __global__ void __launch_bounds__(RS2_THREADS, (sizeof(K) == 8 ? 2 : 3)) radix_s
     const uint64_t hi = min(n, lo + L);
     const uint64_t seg_base = (uint64_t)seg * n;
     const K* src = in + seg_base;
+    const P* psrc = HASP ? pin + seg_base : nullptr;
     const uint32_t ntile = hi > lo ? (uint32_t)((hi - lo + RS2_TILE - 1) / RS2_TILE) : 0u;
 
     for (int i = tid; i < 2 * RS2_WARPS * RADIX; i += RS2_THREADS) (&s_whist[0][0])[i] = 0u;
@@ -516,13 +544,18 @@ __global__ void __launch_bounds__(RS2_THREADS, (sizeof(K) == 8 ? 2 : 3)) radix_s
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         for (uint32_t t = 0; t < 2 && t < ntile; ++t) {
             const uint64_t g0 = lo + (uint64_t)t * RS2_TILE;
-            rs2_issue(t ? buf1 : buf0, src, g0, (uint32_t)min((uint64_t)RS2_TILE, hi - g0),
-                      &s_bar[t]);
+            rs2_issue(t ? buf1 : buf0, src, t ? pbuf1 : pbuf0, psrc, g0,
+                      (uint32_t)min((uint64_t)RS2_TILE, hi - g0), &s_bar[t]);
         }
     }
-    // digit totals of the segment and this chunk's prefix (all chunks < c)
-    uint32_t tot = 0, pre = 0;
-    {
+    // this chunk's digit offsets in its segment: hist_scan_kernel turned the chunk
+    // histograms into exclusive prefixes over chunks and appended the digit totals
+    // (few chunks: summed here, each CTA over its segment's chunk rows)
+    uint32_t pre = 0, tot = 0;
+    if (prescanned) {
+        pre = hist[((uint64_t)seg * cps + c) * RADIX + tid];
+        tot = hist[(uint64_t)gridDim.x * RADIX + (uint64_t)seg * RADIX + tid];
+    } else {
         const uint32_t* h = hist + (uint64_t)seg * cps * RADIX + tid;
         for (uint32_t cc = 0; cc < cps; ++cc) {
             const uint32_t v = h[(uint64_t)cc * RADIX];
@@ -530,11 +563,16 @@ __global__ void __launch_bounds__(RS2_THREADS, (sizeof(K) == 8 ? 2 : 3)) radix_s
             pre += cc < c ? v : 0u;
         }
     }
-    const uint32_t dbase = scan256_excl(tot, s_w);  // (its barriers also publish the inits)
+    const uint32_t dbase = scan256_excl(tot, s_w);
     s_run[tid] = (int64_t)dbase + pre;
     // element offset of a tile's first key inside its buffer (16-byte aligned copies)
     auto delta_of = [&](uint32_t t) -> uint32_t {
         return (uint32_t)((((uintptr_t)(src + lo + (uint64_t)t * RS2_TILE)) & 15) / sizeof(K));
+    };
+    auto pdelta_of = [&](uint32_t t) -> uint32_t {
+        return HASP ? (uint32_t)((((uintptr_t)(psrc + lo + (uint64_t)t * RS2_TILE)) & 15) /
+                                 sizeof(P))
+                    : 0u;
     };
     __syncthreads();
 
@@ -545,6 +583,7 @@ __global__ void __launch_bounds__(RS2_THREADS, (sizeof(K) == 8 ? 2 : 3)) radix_s
         const uint64_t t0 = lo + (uint64_t)t * RS2_TILE;
         const uint32_t cnt = (uint32_t)min((uint64_t)RS2_TILE, hi - t0);
         K* buf = b ? buf1 : buf0;
+        P* pbuf = b ? pbuf1 : pbuf0;
         mbar_wait(&s_bar[b], (t >> 1) & 1u);
         const K* kin = buf + delta_of(t);
         K keys[RS2_ITEMS];
@@ -555,13 +594,10 @@ __global__ void __launch_bounds__(RS2_THREADS, (sizeof(K) == 8 ? 2 : 3)) radix_s
             keys[i] = (cnt == RS2_TILE || idx < cnt) ? kin[idx] : (K)0;
         }
         if (cnt == RS2_TILE)
-            rs2_rank<K, RANK, true>(keys, rank, shift, cnt, whist, mbin, w, lane);
+            rs2_rank<K, RANK, true>(keys, rank, shift, dmask, cnt, whist, mbin, w, lane);
         else
-            rs2_rank<K, RANK, false>(keys, rank, shift, cnt, whist, mbin, w, lane);
+            rs2_rank<K, RANK, false>(keys, rank, shift, dmask, cnt, whist, mbin, w, lane);
         __syncthreads();  // (A) every warp's counters final; every key of buf read
-        // the other buffer's copy for tile t + 1 was issued long ago; this buffer's
-        // next tile (t + 2) can stream in once the reorder below is written out,
-        // which (C) orders; issue it there
         uint32_t tcnt = 0;
 #pragma unroll
         for (int ww = 0; ww < RS2_WARPS; ++ww) tcnt += s_whist[ww][tid];
@@ -579,12 +615,15 @@ __global__ void __launch_bounds__(RS2_THREADS, (sizeof(K) == 8 ? 2 : 3)) radix_s
             s_run[tid] += tcnt;
         }
         __syncthreads();  // (B)
+        const P* pk = HASP ? pbuf + pdelta_of(t) : nullptr;
 #pragma unroll
         for (int i = 0; i < RS2_ITEMS; ++i) {
             const uint32_t idx = (uint32_t)(w * RS2_ITEMS * 32 + i * 32 + lane);
             if (cnt == RS2_TILE || idx < cnt) {
-                const uint32_t d = (uint32_t)(keys[i] >> shift) & 0xffu;
-                buf[whist[d] + rank[i]] = keys[i];
+                const uint32_t d = (uint32_t)(keys[i] >> shift) & dmask;
+                const uint32_t pos = whist[d] + rank[i];
+                buf[pos] = keys[i];
+                if constexpr (HASP) s_pout[pos] = pk[idx];
             }
         }
         __syncwarp();
@@ -594,8 +633,10 @@ __global__ void __launch_bounds__(RS2_THREADS, (sizeof(K) == 8 ? 2 : 3)) radix_s
         __syncthreads();  // (C) tile reordered in buf
         for (uint32_t j = tid; j < cnt; j += RS2_THREADS) {
             const K k = buf[j];
-            const uint32_t d = (uint32_t)(k >> shift) & 0xffu;
-            out[seg_base + (uint64_t)(s_goff[d] + (int64_t)j)] = k;
+            const uint32_t d = (uint32_t)(k >> shift) & dmask;
+            const uint64_t dst = seg_base + (uint64_t)(s_goff[d] + (int64_t)j);
+            out[dst] = k & omask;  // (the trie's leaf pass applies the mask's key bits)
+            if constexpr (HASP) pout[dst] = s_pout[j];
         }
         if (t + 2 < ntile) {
             // buf is free once every thread has written its share out
@@ -603,49 +644,131 @@ __global__ void __launch_bounds__(RS2_THREADS, (sizeof(K) == 8 ? 2 : 3)) radix_s
             const uint64_t g2 = lo + (uint64_t)(t + 2) * RS2_TILE;
             if (tid == 0) {
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                rs2_issue(buf, src, g2, (uint32_t)min((uint64_t)RS2_TILE, hi - g2), &s_bar[b]);
+                rs2_issue(buf, src, pbuf, psrc, g2, (uint32_t)min((uint64_t)RS2_TILE, hi - g2),
+                          &s_bar[b]);
             }
+        } else if (HASP) {
+            __syncthreads();  // s_pout is rewritten by the next tile's reorder
         }
         // (the next tile's barrier A orders s_goff / s_cnt reuse)
     }
 }
 
-template <typename K, int RANK>
-static cudaError_t radix_chunked2(const K* in, K* out, uint64_t n, int nseg, int shift,
-                                  uint32_t* hist, int target_ctas, cudaStream_t s) {
+// chunk histograms [seg][chunk][digit] -> exclusive prefixes over the chunks of each
+// segment, in place; the segment's digit totals go after all chunk rows, at
+// [nseg * cps + seg][digit]. A warp per (segment, digit): its lanes load 32 chunks
+// per step, all steps' loads in flight before the carried warp scans.
+constexpr int HS_STEPS = 24;  // up to 768 chunks per segment in one round trip
+__global__ void __launch_bounds__(256) hist_scan_kernel(uint32_t* hist, uint32_t cps,
+                                                         uint32_t nseg) {
+    const int lane = threadIdx.x & 31;
+    const uint32_t wid = blockIdx.x * 8 + (threadIdx.x >> 5);  // (segment, digit)
+    if (wid >= nseg * RADIX) return;
+    const uint32_t seg = wid / RADIX, d = wid % RADIX;
+    uint32_t* h = hist + (uint64_t)seg * cps * RADIX + d;
+    uint32_t run = 0;
+    for (uint32_t c0 = 0; c0 < cps; c0 += 32 * HS_STEPS) {
+        uint32_t v[HS_STEPS];
+#pragma unroll
+        for (int k = 0; k < HS_STEPS; ++k) {
+            const uint32_t c = c0 + k * 32 + lane;
+            v[k] = c < cps ? h[(uint64_t)c * RADIX] : 0u;
+        }
+#pragma unroll
+        for (int k = 0; k < HS_STEPS; ++k) {
+            uint32_t inc = v[k];
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t t = __shfl_up_sync(0xffffffffu, inc, o);
+                if (lane >= o) inc += t;
+            }
+            const uint32_t c = c0 + k * 32 + lane;
+            if (c < cps) h[(uint64_t)c * RADIX] = run + inc - v[k];
+            run += __shfl_sync(0xffffffffu, inc, 31);
+        }
+    }
+    if (lane == 0) hist[((uint64_t)nseg * cps + seg) * RADIX + d] = run;
+}
+
+template <typename K, typename P, int RANK>
+static cudaError_t radix_chunked2(const K* in, K* out, const P* pin, P* pout, uint64_t n,
+                                  int nseg, int shift, uint32_t dmask, uint32_t* hist,
+                                  int target_ctas, cudaStream_t s, K omask = ~(K)0,
+                                  int* nlaunch = nullptr) {
     uint64_t tiles = (n + RS2_TILE - 1) / RS2_TILE;
     uint64_t cps = std::max<uint64_t>(1, std::min<uint64_t>(tiles, (target_ctas + nseg - 1) / nseg));
     uint64_t L = (tiles + cps - 1) / cps * RS2_TILE;
     cps = (n + L - 1) / L;
     const unsigned grid = (unsigned)(cps * nseg);
-    radix_hist_kernel<K><<<grid, RS_THREADS, 0, s>>>(in, n, (uint32_t)cps, L, shift, hist);
+    radix_hist_kernel<K><<<grid, RS_THREADS, 0, s>>>(in, n, (uint32_t)cps, L, shift, hist, dmask);
+    // many chunks per segment (the trie's single-segment passes): one scan launch
+    // instead of every CTA summing all of its segment's chunk rows
+    const int prescan = cps > 32 ? 1 : 0;
+    if (nlaunch) *nlaunch = 2 + prescan;
+    if (prescan)
+        hist_scan_kernel<<<(unsigned)(nseg * RADIX / 8), 256, 0, s>>>(hist, (uint32_t)cps,
+                                                                      (uint32_t)nseg);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    cudaFuncSetAttribute(radix_scatter2_kernel<K, RANK>,
-                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rs2_smem<K>());
-    radix_scatter2_kernel<K, RANK><<<grid, RS2_THREADS, rs2_smem<K>(), s>>>(
-        in, out, n, (uint32_t)cps, L, shift, hist);
+    cudaFuncSetAttribute(radix_scatter2_kernel<K, P, RANK>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rs2_smem<K, P>());
+    radix_scatter2_kernel<K, P, RANK><<<grid, RS2_THREADS, rs2_smem<K, P>(), s>>>(
+        in, out, pin, pout, n, (uint32_t)cps, L, shift, dmask, hist, omask, prescan);
+    return cudaGetLastError();
+}
+
+// one stable pass of the mask trie (trie.cu): packed windows + sequence ids
+// (a stable pass by the symbol at one kept position; omask = the mask's key bits on
+// the leaf pass, all ones otherwise)
+cudaError_t launch_trie_pass(const uint64_t* win, uint64_t* wout, const void* sin, void* sout,
+                             bool seq16, uint64_t n, int shift, uint32_t dmask, uint64_t omask,
+                             uint32_t* hist, int target_ctas, cudaStream_t s, int* nlaunch) {
+    if (n == 0) return cudaGetLastError();
+    if (seq16)
+        return radix_chunked2<uint64_t, uint16_t, 0>(win, wout, (const uint16_t*)sin,
+                                                     (uint16_t*)sout, n, 1, shift, dmask, hist,
+                                                     target_ctas, s, omask, nlaunch);
+    return radix_chunked2<uint64_t, uint32_t, 0>(win, wout, (const uint32_t*)sin, (uint32_t*)sout,
+                                                 n, 1, shift, dmask, hist, target_ctas, s, omask,
+                                                 nlaunch);
+}
+
+__global__ void seq16_kernel(const uint32_t* __restrict__ a, uint16_t* __restrict__ b,
+                             uint64_t n) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        b[i] = (uint16_t)a[i];
+}
+cudaError_t launch_seq16(const uint32_t* a, uint16_t* b, uint64_t n, int sm_count,
+                         cudaStream_t s) {
+    if (n == 0) return cudaGetLastError();
+    const uint64_t blocks = std::min<uint64_t>((n + 255) / 256, (uint64_t)sm_count * 8);
+    seq16_kernel<<<(unsigned)blocks, 256, 0, s>>>(a, b, n);
     return cudaGetLastError();
 }
 
 cudaError_t launch_radix_chunked2(const void* in, void* out, bool k64, uint64_t n, int nseg,
                                   int shift, uint32_t* hist, int target_ctas, int rank_mode,
-                                  cudaStream_t s) {
+                                  cudaStream_t s, int* nlaunch) {
     if (n == 0 || nseg == 0) return cudaGetLastError();
 #define RS2_CASE(KT, R)                                                                  \
     if (rank_mode == R)                                                                  \
-        return radix_chunked2<KT, R>((const KT*)in, (KT*)out, n, nseg, shift, hist, target_ctas, s);
+        return radix_chunked2<KT, NoPay, R>((const KT*)in, (KT*)out, nullptr, nullptr, n, nseg, \
+                                            shift, 0xffu, hist, target_ctas, s, ~(KT)0,    \
+                                            nlaunch);
     if (k64) {
         RS2_CASE(uint64_t, 1)
         RS2_CASE(uint64_t, 2)
-        return radix_chunked2<uint64_t, 0>((const uint64_t*)in, (uint64_t*)out, n, nseg, shift,
-                                           hist, target_ctas, s);
+        return radix_chunked2<uint64_t, NoPay, 0>((const uint64_t*)in, (uint64_t*)out, nullptr,
+                                                  nullptr, n, nseg, shift, 0xffu, hist,
+                                                  target_ctas, s, ~0ull, nlaunch);
     }
     RS2_CASE(uint32_t, 1)
     RS2_CASE(uint32_t, 2)
 #undef RS2_CASE
-    return radix_chunked2<uint32_t, 0>((const uint32_t*)in, (uint32_t*)out, n, nseg, shift, hist,
-                                       target_ctas, s);
+    return radix_chunked2<uint32_t, NoPay, 0>((const uint32_t*)in, (uint32_t*)out, nullptr,
+                                              nullptr, n, nseg, shift, 0xffu, hist, target_ctas,
+                                              s, ~0u, nlaunch);
 }
 
 cudaError_t launch_radix_chunked(const void* in, void* out, bool k64, uint64_t n, int nseg,

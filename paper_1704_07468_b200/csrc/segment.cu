@@ -24,10 +24,75 @@
 
 namespace gk {
 
+// Element access policies: composites (key bits << sb | seq, the LSD path) or the
+// mask trie's separate arrays (masked packed window, sequence id).
 template <typename K>
+struct SegComp {
+    using E = K;
+    const K* keys;
+    int sb;
+    __device__ E ld(uint64_t i) const { return keys[i]; }
+    __device__ void ld8(uint64_t base, E (&c)[SEG_ITEMS]) const {
+        constexpr int NV = SEG_ITEMS * sizeof(K) / 16;
+        const uint4* v = (const uint4*)(keys + base);
+#pragma unroll
+        for (int i = 0; i < NV; ++i) {
+            const uint4 q = v[i];
+            const K* kq = (const K*)&q;
+#pragma unroll
+            for (int e = 0; e < 16 / (int)sizeof(K); ++e) c[i * (16 / sizeof(K)) + e] = kq[e];
+        }
+    }
+    __device__ bool teq(E a, E b) const { return a == b; }
+    __device__ bool geq(E a, E b) const { return ((a ^ b) >> sb) == 0; }
+    __device__ uint32_t seq(E a) const { return (uint32_t)(a & ((1ull << sb) - 1ull)); }
+    __device__ E other(E a) const { return ~a; }  // differs in the key bits
+    __device__ E shfl(E a, int src) const { return __shfl_sync(0xffffffffu, a, src); }
+};
+
+struct SoaElem {
+    uint64_t w;
+    uint32_t s;
+};
+template <typename S>
+struct SegSoa {
+    using E = SoaElem;
+    const uint64_t* w;  // masked packed windows (the leaf pass applied the mask)
+    const S* sq;        // sequence ids
+    __device__ E ld(uint64_t i) const { return E{w[i], (uint32_t)sq[i]}; }
+    __device__ void ld8(uint64_t base, E (&c)[SEG_ITEMS]) const {
+        const uint4* v = (const uint4*)(w + base);
+#pragma unroll
+        for (int i = 0; i < SEG_ITEMS / 2; ++i) {
+            const uint4 q = v[i];
+            c[2 * i].w = (uint64_t)q.x | (uint64_t)q.y << 32;
+            c[2 * i + 1].w = (uint64_t)q.z | (uint64_t)q.w << 32;
+        }
+        const uint4* u = (const uint4*)(sq + base);
+        constexpr int NU = SEG_ITEMS * sizeof(S) / 16;
+#pragma unroll
+        for (int i = 0; i < NU; ++i) {
+            const uint4 q = u[i];
+            const S* sv = (const S*)&q;
+#pragma unroll
+            for (int e = 0; e < 16 / (int)sizeof(S); ++e)
+                c[i * (16 / sizeof(S)) + e].s = (uint32_t)sv[e];
+        }
+    }
+    __device__ bool teq(E a, E b) const { return a.w == b.w && a.s == b.s; }
+    __device__ bool geq(E a, E b) const { return a.w == b.w; }
+    __device__ uint32_t seq(E a) const { return a.s; }
+    __device__ E other(E a) const { return E{~a.w, a.s}; }
+    __device__ E shfl(E a, int src) const {
+        return E{__shfl_sync(0xffffffffu, a.w, src), __shfl_sync(0xffffffffu, a.s, src)};
+    }
+};
+
+template <typename Pol>
 __global__ void __launch_bounds__(SEG_THREADS, 5) segment_kernel(
-    const K* __restrict__ keys, uint64_t n, uint64_t total, int sb, int64_t dstride,
+    Pol pol, uint64_t n, uint64_t total, int64_t dstride,
     int64_t* diag, uint32_t* counters, SegmentOut so, unsigned long long* stats) {
+    using K = typename Pol::E;
     __shared__ uint32_t s_w[16];
     __shared__ uint32_t s_gpos[SEG_TILE];
     __shared__ uint32_t s_tx[SEG_TILE], s_tc[SEG_TILE];  // the tile's triples, staged
@@ -39,35 +104,26 @@ __global__ void __launch_bounds__(SEG_THREADS, 5) segment_kernel(
     const uint64_t base = tile0 + (uint64_t)tid * SEG_ITEMS;
     const uint32_t lbase = (uint32_t)tid * SEG_ITEMS;  // tile-local index of item 0
     const uint64_t tile_end = min(tile0 + SEG_TILE, total);
-    const uint64_t seqmask = (1ull << sb) - 1ull;
 
     K cur[SEG_ITEMS];
     if (base + SEG_ITEMS <= total) {
-        constexpr int NV = SEG_ITEMS * sizeof(K) / 16;
-        const uint4* v = (const uint4*)(keys + base);
-#pragma unroll
-        for (int i = 0; i < NV; ++i) {
-            const uint4 q = v[i];
-            const K* kq = (const K*)&q;
-#pragma unroll
-            for (int e = 0; e < 16 / (int)sizeof(K); ++e) cur[i * (16 / sizeof(K)) + e] = kq[e];
-        }
+        pol.ld8(base, cur);
     } else {
 #pragma unroll
-        for (int i = 0; i < SEG_ITEMS; ++i) cur[i] = base + i < total ? keys[base + i] : (K)0;
+        for (int i = 0; i < SEG_ITEMS; ++i) cur[i] = base + i < total ? pol.ld(base + i) : K{};
     }
     // the last warp also fetches the 32 keys after the tile (the run / group
     // crossing its end), in flight together with the tile's own loads
     const bool has_next = tile_end < total && tile_end % n != 0;
-    K ext = (K)0, lk = (K)0;
+    K ext{}, lk{};
     if (warp == SEG_THREADS / 32 - 1 && has_next) {
-        lk = keys[tile_end - 1];
-        ext = tile_end + lane < total ? keys[tile_end + lane] : (K)~lk;
+        lk = pol.ld(tile_end - 1);
+        ext = tile_end + lane < total ? pol.ld(tile_end + lane) : pol.other(lk);
     }
     // segment (mask) bounds of this thread's first item: one 64-bit division per
     // thread; consecutive items cross at most one boundary each (n >= 1)
     uint64_t seg_lo = base < total ? base / n * n : 0, seg_hi = seg_lo + n;
-    const K prev = (base < total && base != seg_lo) ? keys[base - 1] : (K)0;
+    const K prev = (base < total && base != seg_lo) ? pol.ld(base - 1) : K{};
 
     // 1. head flags: a triple head where the composite changes, a group head where
     //    the key bits change (both at every segment start)
@@ -83,8 +139,8 @@ __global__ void __launch_bounds__(SEG_THREADS, 5) segment_kernel(
         const K c0 = cur[i];
         const K p0 = i == 0 ? prev : cur[i - 1];
         const bool first = idx == seg_lo;
-        if (first || p0 != c0) th_bits |= 1u << i;
-        if (first || ((p0 ^ c0) >> sb) != 0) gh_bits |= 1u << i;
+        if (first || !pol.teq(p0, c0)) th_bits |= 1u << i;
+        if (first || !pol.geq(p0, c0)) gh_bits |= 1u << i;
     }
     if (tid == 0) {
         s_first_gh = 0xffffffffu;
@@ -97,17 +153,17 @@ __global__ void __launch_bounds__(SEG_THREADS, 5) segment_kernel(
         bool cross = false;
         if (has_next) {  // (warp-uniform)
             const uint64_t seg_end = (tile_end / n + 1) * n;
-            cross = ((__shfl_sync(0xffffffffu, ext, 0) ^ lk) >> sb) == 0;
+            cross = pol.geq(pol.shfl(ext, 0), lk);
             for (uint64_t e = tile_end;; e += 32) {
                 const uint64_t q = e + lane;
-                const K kk = e == tile_end ? ext : (q < seg_end ? keys[q] : (K)~lk);
-                const bool stop = q >= seg_end || kk != lk;
+                const K kk = e == tile_end ? ext : (q < seg_end ? pol.ld(q) : pol.other(lk));
+                const bool stop = q >= seg_end || !pol.teq(kk, lk);
                 const uint32_t sm = __ballot_sync(0xffffffffu, stop);
                 if (sm) {
                     const int j = __ffs(sm) - 1;
-                    const K kj = __shfl_sync(0xffffffffu, kk, j);
+                    const K kj = pol.shfl(kk, j);
                     const uint64_t qj = e + j;
-                    const bool g = qj >= seg_end || ((kj ^ lk) >> sb) != 0;
+                    const bool g = qj >= seg_end || !pol.geq(kj, lk);
                     b = (uint32_t)(qj - tile0) << 1 | (g ? 1u : 0u);
                     break;
                 }
@@ -156,7 +212,7 @@ __global__ void __launch_bounds__(SEG_THREADS, 5) segment_kernel(
         const uint32_t gh = (gh_bits >> i) & 1u;
         if (!gh || !(nxt & 1u)) multi_bits |= 1u << i;
         if (c >= 2) {
-            const int64_t x = (int64_t)(cur[i] & seqmask);
+            const int64_t x = (int64_t)pol.seq(cur[i]);
             atomicAdd((unsigned long long*)&diag[x * dstride], (unsigned long long)c * c - c);
         }
         nxt = li << 1 | gh;
@@ -180,10 +236,10 @@ __global__ void __launch_bounds__(SEG_THREADS, 5) segment_kernel(
     //    tail in tile-sized chunks, counting its triple heads
     const bool crossing = fgh != 0xffffffffu && s_cross != 0;
     uint64_t gend = tile_end;  // one past the crossing group's last key
-    K gkey = 0;
+    K gkey{};
     uint64_t seg_end_t = 0;
     if (crossing) {  // (block-uniform)
-        gkey = keys[tile_end - 1] >> sb;
+        gkey = pol.ld(tile_end - 1);
         seg_end_t = (tile_end / n + 1) * n;
         uint32_t heads = 0;
         for (uint64_t e = tile_end;; e += SEG_TILE) {
@@ -196,13 +252,12 @@ __global__ void __launch_bounds__(SEG_THREADS, 5) segment_kernel(
 #pragma unroll
             for (int i = 0; i < SEG_ITEMS; ++i) {
                 const uint64_t q = e + lbase + i;
-                const K kk = q < seg_end_t ? keys[q] : (K)~(K)0;
-                const bool in = q < seg_end_t && (kk >> sb) == gkey;
+                const bool in = q < seg_end_t && pol.geq(pol.ld(q), gkey);
                 if (!in) {
                     atomicMin(&s_gend, (unsigned long long)q);
                     break;
                 }
-                h += kk != keys[q - 1];
+                h += !pol.teq(pol.ld(q), pol.ld(q - 1));
             }
             if (h) atomicAdd(&s_tail, h);
             __syncthreads();
@@ -228,7 +283,7 @@ __global__ void __launch_bounds__(SEG_THREADS, 5) segment_kernel(
 #pragma unroll
     for (int i = 0; i < SEG_ITEMS; ++i) {
         if (emit_t & (1u << i)) {
-            const uint32_t x = (uint32_t)(cur[i] & seqmask);
+            const uint32_t x = pol.seq(cur[i]);
             s_tx[li] = x | (((gh_bits >> i) & 1u) << 31);
             s_tc[li] = cnt[i];
             if (emit_g & (1u << i)) s_gpos[gl++] = base_t + li;
@@ -255,8 +310,8 @@ __global__ void __launch_bounds__(SEG_THREADS, 5) segment_kernel(
 #pragma unroll
             for (int i = 0; i < SEG_ITEMS; ++i) {
                 const uint64_t q = e + lbase + i;
-                kv[i] = q < gend ? keys[q] : (K)0;
-                if (q < gend && kv[i] != keys[q - 1]) hb |= 1u << i;
+                kv[i] = q < gend ? pol.ld(q) : K{};
+                if (q < gend && !pol.teq(kv[i], pol.ld(q - 1))) hb |= 1u << i;
             }
             uint32_t chunk_heads;
             const uint32_t off = scan256_excl(__popc(hb), s_w, &chunk_heads);
@@ -266,8 +321,8 @@ __global__ void __launch_bounds__(SEG_THREADS, 5) segment_kernel(
                 if (hb & (1u << i)) {
                     const uint64_t q = e + lbase + i;
                     uint64_t r = q + 1;
-                    while (r < gend && keys[r] == kv[i]) ++r;
-                    so.tseq[pos] = (uint32_t)(kv[i] & seqmask);
+                    while (r < gend && pol.teq(pol.ld(r), kv[i])) ++r;
+                    so.tseq[pos] = pol.seq(kv[i]);
                     so.tcnt[pos] = (uint32_t)(r - q);
                     ++pos;
                 }
@@ -285,11 +340,32 @@ cudaError_t launch_segment(const void* keys, bool k64, uint64_t n, int nseg, int
     if (e != cudaSuccess || total == 0) return e;
     uint64_t tiles = (total + SEG_TILE - 1) / SEG_TILE;
     if (k64)
-        segment_kernel<uint64_t><<<(unsigned)tiles, SEG_THREADS, 0, s>>>(
-            (const uint64_t*)keys, n, total, sb, dstride, diag, counters, so, stats);
+        segment_kernel<SegComp<uint64_t>><<<(unsigned)tiles, SEG_THREADS, 0, s>>>(
+            SegComp<uint64_t>{(const uint64_t*)keys, sb}, n, total, dstride, diag, counters, so,
+            stats);
     else
-        segment_kernel<uint32_t><<<(unsigned)tiles, SEG_THREADS, 0, s>>>(
-            (const uint32_t*)keys, n, total, sb, dstride, diag, counters, so, stats);
+        segment_kernel<SegComp<uint32_t>><<<(unsigned)tiles, SEG_THREADS, 0, s>>>(
+            SegComp<uint32_t>{(const uint32_t*)keys, sb}, n, total, dstride, diag, counters, so,
+            stats);
+    return cudaGetLastError();
+}
+
+// the mask trie's leaves: masked packed windows + sequence ids (u16 or u32)
+cudaError_t launch_segment_soa(const uint64_t* w, const void* sq, bool seq16, uint64_t n,
+                               int nseg, int64_t dstride, int64_t* diag, uint32_t* counters,
+                               SegmentOut so, unsigned long long* stats, cudaStream_t s) {
+    cudaError_t e = cudaMemsetAsync(counters, 0, 2 * sizeof(uint32_t), s);
+    uint64_t total = n * (uint64_t)nseg;
+    if (e != cudaSuccess || total == 0) return e;
+    uint64_t tiles = (total + SEG_TILE - 1) / SEG_TILE;
+    if (seq16)
+        segment_kernel<SegSoa<uint16_t>><<<(unsigned)tiles, SEG_THREADS, 0, s>>>(
+            SegSoa<uint16_t>{w, (const uint16_t*)sq}, n, total, dstride, diag, counters, so,
+            stats);
+    else
+        segment_kernel<SegSoa<uint32_t>><<<(unsigned)tiles, SEG_THREADS, 0, s>>>(
+            SegSoa<uint32_t>{w, (const uint32_t*)sq}, n, total, dstride, diag, counters, so,
+            stats);
     return cudaGetLastError();
 }
 

@@ -211,6 +211,8 @@ def test_batch_size_invariance(gk, oracle_lib):
         assert_parity(run(gk, cp, 7, 5, 2, batch_keys=bk, sort=1), ref)
         assert_parity(run(gk, cp, 7, 5, 2, batch_keys=bk, sort=3), ref)
         assert_parity(run(gk, cp, 7, 5, 2, batch_keys=bk, sort=4), ref)
+        assert_parity(run(gk, cp, 7, 5, 2, batch_keys=bk, sort=6), ref)
+        assert_parity(run(gk, cp, 7, 5, 2, batch_keys=bk, sort=6, heavy_min_seqs=2), ref)
         assert_parity(run(gk, cp, 7, 5, 2, batch_keys=bk, pipeline=0), ref)
         assert_parity(run(gk, cp, 7, 5, 2, batch_keys=bk, level_order=0), ref)
         assert_parity(run(gk, cp, 7, 5, 2, batch_keys=bk, heavy_min_seqs=2), ref)
@@ -225,7 +227,7 @@ def test_sort_modes_ragged(gk, oracle_lib):
     cp = sc.from_sequences(20, seqs)
     ref = oracle_lib.compute(cp, 8, 4, 4)
     for bk in (0, 50001, 4097 * 3):
-        for mode in (0, 1, 3, 4, 5):
+        for mode in (0, 1, 3, 4, 5, 6):
             assert_parity(run(gk, cp, 8, 4, 4, batch_keys=bk, sort=mode), ref)
     cp4 = sc.from_sequences(4, [rng.integers(0, 4, size=int(rng.integers(0, 5000)))
                                 for _ in range(23)])
@@ -249,11 +251,11 @@ def test_grouping_modes(gk, oracle_lib):
         M = int(rng.integers(0, g + 1))
         cp = sc.random_small(rng, sigma, n_max=200, l_max=300)
         ref = oracle_lib.compute(cp, g, k, M)
-        for mode in (0, 1, 2, 3, 4, 5):
+        for mode in (0, 1, 2, 3, 4, 5, 6):
             r = run(gk, cp, g, k, M, sort=mode)
             assert_parity(r, ref)
             if r["stats"]["keys"] > 0:
-                assert r["stats"]["grouping"] == (mode if mode < 3 else 0)
+                assert r["stats"]["grouping"] == (mode if mode < 3 else (3 if mode == 6 else 0))
         assert run(gk, cp, g, k, M)["stats"]["grouping"] == 0
 
 
