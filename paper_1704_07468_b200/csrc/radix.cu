@@ -510,9 +510,12 @@ __device__ __forceinline__ void rs2_rank(const K (&keys)[RS2_ITEMS], uint32_t (&
 template <typename K, typename P, int RANK>
 __global__ void __launch_bounds__(RS2_THREADS, (sizeof(K) == 8 ? 2 : 3)) radix_scatter2_kernel(
     const K* __restrict__ in, K* __restrict__ out, const P* __restrict__ pin, P* __restrict__ pout,
-    uint64_t n, uint32_t cps, uint64_t L, int shift, uint32_t dmask,
-    const uint32_t* __restrict__ hist, K omask, int prescanned) {
+    uint64_t n, uint32_t cps, uint64_t L, int shift, uint32_t dmask_,
+    const uint32_t* __restrict__ hist, K omask_, int prescanned) {
     constexpr bool HASP = rs2_haspay<P>();
+    // (the plain LSD passes: full 8-bit digits, no output mask -- compile-time)
+    const uint32_t dmask = HASP ? dmask_ : 0xffu;
+    const K omask = HASP ? omask_ : ~(K)0;
     extern __shared__ __align__(16) unsigned char smem[];
     K* const buf0 = (K*)smem;
     K* const buf1 = (K*)(smem + rs2_buf_bytes<K>());
@@ -703,7 +706,7 @@ static cudaError_t radix_chunked2(const K* in, K* out, const P* pin, P* pout, ui
     radix_hist_kernel<K><<<grid, RS_THREADS, 0, s>>>(in, n, (uint32_t)cps, L, shift, hist, dmask);
     // many chunks per segment (the trie's single-segment passes): one scan launch
     // instead of every CTA summing all of its segment's chunk rows
-    const int prescan = cps > 32 ? 1 : 0;
+    const int prescan = cps > 128 ? 1 : 0;
     if (nlaunch) *nlaunch = 2 + prescan;
     if (prescan)
         hist_scan_kernel<<<(unsigned)(nseg * RADIX / 8), 256, 0, s>>>(hist, (uint32_t)cps,
