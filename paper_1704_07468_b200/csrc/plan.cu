@@ -82,6 +82,7 @@ struct gakco_plan {
     // 2 hash partition + shared-memory hash grouping (bucket.cu)
     int sort_mode = -1;
     int sort_ctas_per_sm = 4;  // chunked pass grid = this x SMs (2 resident: 2 full waves; measured best of 2..4)
+    int trie_ctas_per_sm = 2;  // trie passes (one mask each): one full wave (Text sort 91 -> 76 ms vs 4)
     int64_t light_bins = 0;    // 0 auto, < 0 off, > 0 forced block size in cells
     int gram_pair = 1;         // 1: CTA-pair Gram (gram2.cu), 0: one-SM Gram (gram_tc.cu)
     int light_flat = 8;        // light groups of <= this many sequences share warps
@@ -307,6 +308,7 @@ extern "C" gakco_status gakco_set_option(gakco_plan* p, int option, int64_t valu
         case GAKCO_OPT_SORT_CTAS_PER_SM:
             if (value < 1 || value > 16) return p->fail(GAKCO_E_ARG, "1..16");
             p->sort_ctas_per_sm = (int)value;
+            p->trie_ctas_per_sm = (int)value;
             return GAKCO_OK;
         case GAKCO_OPT_GRAM_PAIR:
             if (value < 0 || value > 1) return p->fail(GAKCO_E_ARG, "gram pair must be 0 or 1");
@@ -1029,7 +1031,7 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
                     int nl = 2;
                     LK(launch_trie_pass(wi, wo, si, so_, seq16, n, bits * (g - 1 - kept[t]), dmask,
                                         leaf ? kmask : ~0ull, (uint32_t*)p->hist.p,
-                                        p->sort_ctas_per_sm * p->sm_count, s, &nl));
+                                        p->trie_ctas_per_sm * p->sm_count, s, &nl));
                     p->launches += nl - 1;  // hist (+ chunk scan) + scatter
                     if (!leaf) stack_pos[t] = kept[t];
                 }
