@@ -74,9 +74,9 @@ typedef enum {
                                      windows + sequence ids, passes of common leading kept
                                      positions shared between masks (auto when a mask has
                                      >= 2M g-mers and g*ceil(log2 sigma) <= 64) */
-    GAKCO_OPT_SORT_CTAS_PER_SM = 5, /* chunked pass grid size in CTAs per SM (default 4 for the
-                                       batched LSD passes, 2 for the mask trie; setting it
-                                       sets both) */
+    GAKCO_OPT_SORT_CTAS_PER_SM = 5, /* chunked pass grid size in CTAs per SM (defaults: 4 for
+                                       the batched LSD passes on u64 composites, 8 on u32,
+                                       2 for the mask trie; setting it sets all three) */
     GAKCO_OPT_LIGHT_BINS = 6,     /* light updates binned by accumulator block (ablation /
                                      test knob): <= 0 = never (default; measured slower on
                                      Scale), > 0 = always, with this many cells per block */

@@ -83,6 +83,7 @@ struct gakco_plan {
     int sort_mode = -1;
     int sort_ctas_per_sm = 4;  // chunked pass grid = this x SMs (2 resident: 2 full waves; measured best of 2..4)
     int trie_ctas_per_sm = 2;  // trie passes (one mask each): one full wave (Text sort 91 -> 76 ms vs 4)
+    int sort32_ctas_per_sm = 8;  // u32 composites: more chunks per segment (DNA sort 1.60 -> 1.49 ms)
     int64_t light_bins = 0;    // 0 auto, < 0 off, > 0 forced block size in cells
     int gram_pair = 1;         // 1: CTA-pair Gram (gram2.cu), 0: one-SM Gram (gram_tc.cu)
     int light_flat = 8;        // light groups of <= this many sequences share warps
@@ -309,6 +310,7 @@ extern "C" gakco_status gakco_set_option(gakco_plan* p, int option, int64_t valu
             if (value < 1 || value > 16) return p->fail(GAKCO_E_ARG, "1..16");
             p->sort_ctas_per_sm = (int)value;
             p->trie_ctas_per_sm = (int)value;
+            p->sort32_ctas_per_sm = (int)value;
             return GAKCO_OK;
         case GAKCO_OPT_GRAM_PAIR:
             if (value < 0 || value > 1) return p->fail(GAKCO_E_ARG, "gram pair must be 0 or 1");
@@ -615,7 +617,8 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
     cudaStream_t s3 = pipe ? p->aux2 : s;
     CK(p->ensure(p->hist, std::max<uint64_t>(std::min<uint64_t>(bmax_masks, mine.size() + 1) *
                                                  MAXPASS * RADIX * 4,
-                                             (uint64_t)(p->sort_ctas_per_sm * p->sm_count + 64 +
+                                             (uint64_t)(std::max(p->sort_ctas_per_sm, p->sort32_ctas_per_sm) *
+                                                            p->sm_count + 64 +
                                                         2 * bmax_masks) *
                                                  RADIX * 4),
                  s));
@@ -1080,7 +1083,8 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
                         int nl = 2;
                         LK(launch_radix_chunked2(in, outk, k64, n, nmask, sb + RADIX_BITS * q,
                                                  (uint32_t*)p->hist.p,
-                                                 p->sort_ctas_per_sm * p->sm_count,
+                                                 (k64 ? p->sort_ctas_per_sm : p->sort32_ctas_per_sm) *
+                                                     p->sm_count,
                                                  p->sort_mode >= 3 ? p->sort_mode - 3 : 0, s, &nl));
                         p->launches += nl - 1;
                     } else {

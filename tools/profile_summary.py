@@ -29,15 +29,18 @@ STAGE = {"encode_kernel": "encode", "encode_win_kernel": "encode", "window_kerne
          "fill_round_kernel": "dense", "epilogue_kernel": "epilogue", "kdiag_kernel": "epilogue",
          "diag_closed_form_kernel": "light", "gmer_index_kernel": "encode",
          "check_codes_kernel": "encode", "bk_pass_kernel": "encode", "bk_colscan_kernel": "sort",
-         "bk_bscan_kernel": "sort", "bk_group_kernel": "segment"}
+         "bk_bscan_kernel": "sort", "bk_group_kernel": "segment",
+         "radix_scatter2_kernel": "sort", "hist_scan_kernel": "sort", "seq16_kernel": "sort",
+         "symbol_hist_kernel": "encode", "thresh_union_kernel": "light",
+         "light_flush_rect_kernel": "light", "fill_reset4_kernel": "heavy"}
 
 
 def short(name):
-    n = name.split("(")[0].strip()
+    n = name.strip()
     if n.startswith("void "):
         n = n[5:]
-    n = n.split("::")[-1]
-    return n.split("<")[0]
+    cut = min([i for i in (n.find("<"), n.find("(")) if i >= 0] or [len(n)])
+    return n[:cut].split("::")[-1]
 
 
 def launches(path, tag, out_dir):
