@@ -103,7 +103,16 @@ typedef enum {
     GAKCO_OPT_LEVEL_ORDER = 12    /* 0 (default): levels processed m = 0..M; 1: m = M..0 (the
                                      top level's Gram overlaps the rest: Protein 8.0 -> 7.8 ms
                                      but DNA 9.26 -> 9.51 ms; ascending whenever the light
-                                     accumulator is relabelled) */
+                                     accumulator is relabelled) */,
+    GAKCO_OPT_LIGHT_WINDOW = 13,  /* window Gram of cluster-local light groups: once the light
+                                     accumulator is relabelled (GAKCO_OPT_LIGHT_RELABEL), a
+                                     group whose labels lie in one window of 256 labels becomes
+                                     a u8 count column of that window's 256 x 256 block,
+                                     multiplied on the tensor cores (kind::i8) and added back
+                                     through the inverse labelling. -1 = automatic (default:
+                                     with relabelling), 0 = off, 1 = on (relabels) */
+    GAKCO_OPT_WINDOW_MIN = 14     /* smallest group (sequences) for the window Gram (default 9;
+                                     groups of <= GAKCO_OPT_LIGHT_FLAT sequences stay light) */
 } gakco_option;
 
 /* Counters of the last gakco_accumulate (algorithmic units). */
@@ -132,6 +141,8 @@ typedef struct {
     int64_t gram_fp4;       /* bit m set: level m's Gram ran on e2m1 counts (kind::mxf4);
                                clear: u8 (kind::i8). Chosen per level (GAKCO_OPT_GRAM_FP4) */
     int64_t heavy_macs_fp4; /* the part of heavy_macs issued as e2m1 (kind::mxf4) */
+    int64_t win_groups;     /* light groups sent to the window Gram (GAKCO_OPT_LIGHT_WINDOW) */
+    int64_t win_macs;       /* u8 multiply-accumulates issued by the window Gram */
 } gakco_stats;
 
 /* Create a plan for alphabet size sigma (1..255), g-mer length g (1..32),

@@ -57,6 +57,10 @@ struct GramArgs {
     int ntiles;
     int tma_epilogue;   // 1: TMA reduce-add into C (rows 16-byte aligned)
     int ksplit;         // K slices per output tile
+    // window mode (wfill != nullptr): D rows are windows of 256 labels, tile (2w + r,
+    // w) is rows r*128.. of window w against all its 256 rows, K = wfill[w] columns;
+    // the output is the window's block of wC ([nw * 256][256] int64, local columns)
+    const uint32_t* wfill;
 };
 
 __global__ void __launch_bounds__(GT_THREADS, 1)
@@ -73,8 +77,15 @@ __global__ void __launch_bounds__(GT_THREADS, 1)
     uint32_t* tmem_slot = (uint32_t*)(bars + 2 * GT_STAGES + 4);
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int kblocks = (int)((min(*a.fill, a.cap) + GT_KB - 1) / GT_KB);  // grid-uniform
-    if (kblocks == 0) return;
+    const bool wmode = a.wfill != nullptr;
+    const int kblocks0 = wmode ? 0 : (int)((min(*a.fill, a.cap) + GT_KB - 1) / GT_KB);
+    if (!wmode && kblocks0 == 0) return;  // (grid-uniform)
+    // K blocks of a tile: the flush's fill, or (window mode) its window's fill
+    auto kblocks_of = [&](int2 tl) -> int {
+        return wmode ? (int)((min(a.wfill[tl.y], a.cap) + GT_KB - 1) / GT_KB) : kblocks0;
+    };
+    const int kblocks = kblocks0;
+    (void)kblocks;
     // work unit u = (tile u / ksplit, K slice u % ksplit): split-K keeps every SM
     // busy when there are few output tiles (small N); slices add up in C
     const int kper = (kblocks + a.ksplit - 1) / a.ksplit;
@@ -108,7 +119,9 @@ __global__ void __launch_bounds__(GT_THREADS, 1)
             uint32_t stage = 0, phase = 0;
             for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
                 const int2 tl = a.tiles[u / a.ksplit];
-                const int klo = (u % a.ksplit) * kper, khi = min(kblocks, klo + kper);
+                const int kbt = kblocks_of(tl);
+                const int kpt = wmode ? kbt : kper;
+                const int klo = (u % a.ksplit) * kpt, khi = min(kbt, klo + kpt);
                 for (int kb = klo; kb < khi; ++kb) {
                     mbar_wait(&empty[stage], phase ^ 1);
                     unsigned char* sa = smem + (size_t)stage * GT_STAGE_BYTES;
@@ -130,7 +143,9 @@ __global__ void __launch_bounds__(GT_THREADS, 1)
             uint32_t stage = 0, phase = 0;
             int it = 0;
             for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
-                const int klo = (u % a.ksplit) * kper, khi = min(kblocks, klo + kper);
+                const int kbt = kblocks_of(a.tiles[u / a.ksplit]);
+                const int kpt = wmode ? kbt : kper;
+                const int klo = (u % a.ksplit) * kpt, khi = min(kbt, klo + kpt);
                 if (klo >= khi) continue;  // empty K slice: skipped by every role
                 const int acc = it & 1;
                 const uint32_t acc_phase = (it >> 1) & 1;
@@ -163,16 +178,20 @@ __global__ void __launch_bounds__(GT_THREADS, 1)
         int it = 0, buf = 0;
         const int row = warp * 32 + lane;
         for (int u = blockIdx.x; u < nunits; u += gridDim.x) {
-            const int klo = (u % a.ksplit) * kper, khi = min(kblocks, klo + kper);
+            const int2 tl = a.tiles[u / a.ksplit];
+            const int kbt = kblocks_of(tl);
+            const int kpt = wmode ? kbt : kper;
+            const int klo = (u % a.ksplit) * kpt, khi = min(kbt, klo + kpt);
             if (klo >= khi) continue;
             const int acc = it & 1;
             const uint32_t acc_phase = (it >> 1) & 1;
             ++it;
-            const int2 tl = a.tiles[u / a.ksplit];
             mbar_wait(&tfull[acc], acc_phase);
             tc_fence_after();
-            const int64_t x = (int64_t)tl.x * GT_M + row;
-            const int64_t y0 = (int64_t)tl.y * GT_N;
+            // (window mode: local coordinates inside the window's 256 x 256 block)
+            const int64_t x = wmode ? (int64_t)(tl.x - 2 * tl.y) * GT_M + row
+                                    : (int64_t)tl.x * GT_M + row;
+            const int64_t y0 = wmode ? 0 : (int64_t)tl.y * GT_N;
 #pragma unroll 1
             for (int c = 0; c < GT_N; c += GT_EC) {
                 uint32_t v[GT_EC];
@@ -193,6 +212,7 @@ __global__ void __launch_bounds__(GT_THREADS, 1)
                     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                     epi_bar();
                     if (threadIdx.x == 0) {
+                        // (window mode: output row = the window's D row, column local)
                         tma_reduce_add_2d(&cmap, sb, (int)(y0 + c), (int)(tl.x * GT_M));
                         asm volatile("cp.async.bulk.commit_group;" ::: "memory");
                     }
@@ -202,7 +222,7 @@ __global__ void __launch_bounds__(GT_THREADS, 1)
                     const uint64_t* s64 = (const uint64_t*)sb;
 #pragma unroll 4
                     for (int e = threadIdx.x; e < GT_M * GT_EC; e += 128) {
-                        const int64_t xx = (int64_t)tl.x * GT_M + e / GT_EC;
+                        const int64_t xx = (int64_t)tl.x * GT_M + e / GT_EC;  // (wC row)
                         const int64_t yy = y0 + c + e % GT_EC;
                         const uint64_t val = s64[e];
                         if (val && xx < a.N && yy < a.N)  // atomic: K slices share tiles
@@ -563,6 +583,133 @@ cudaError_t launch_gram_flush(uint8_t* D, int64_t n_pad, uint64_t ldd, uint32_t*
     if (e != cudaSuccess) return e;
     fill_reset_kernel<<<1, 1, 0, s>>>(dense_fill, ldd, (uint64_t)ntiles * GT_M * GT_N, stats,
                                       GT_KB, 0);
+    return cudaGetLastError();
+}
+
+// ---------------------------------------------------------------- window Gram
+// Window build: CTA (w, q) writes slabs q, q + WB_Q, ... of this batch's columns
+// [wa.fill[nw + w], wa.fill[w]) of window w (the batch start is slab-aligned): 128
+// columns x 256 rows of u8 counts assembled in shared memory (zeros elsewhere),
+// stored as one contiguous 32 KB block of wD [slab][nw * 256][128]. A warp takes 8
+// columns, their members gathered together (latency: list -> triple -> label).
+constexpr int WB_Q = 16;
+constexpr int WB_THREADS = 512;
+constexpr int WB_CPW = GT_KB / (WB_THREADS / 32);  // columns per warp per slab (8)
+
+__global__ void __launch_bounds__(WB_THREADS) window_build_kernel(SegmentOut so, WinArgs wa,
+                                                                 const uint32_t* __restrict__ perm,
+                                                                 uint8_t* __restrict__ wD) {
+    __shared__ __align__(16) uint8_t tile[WIN_ROWS * GT_KB];  // [row][col], 32 KB
+    const uint32_t w = blockIdx.x / WB_Q, q = blockIdx.x % WB_Q;
+    const uint32_t c1 = min(wa.fill[w], wa.cap), c0 = min(wa.fill[wa.nw + w], c1);
+    const uint32_t s0 = c0 / GT_KB, s1 = (c1 + GT_KB - 1) / GT_KB;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const uint32_t lab0 = w * WIN_STEP;
+    for (uint32_t sl = s0 + q; sl < s1; sl += WB_Q) {
+        uint4* t4 = (uint4*)tile;
+        for (int i = threadIdx.x; i < WIN_ROWS * GT_KB / 16; i += WB_THREADS) t4[i] = make_uint4(0, 0, 0, 0);
+        __syncthreads();
+        uint2 g[WB_CPW];
+#pragma unroll
+        for (int jj = 0; jj < WB_CPW; ++jj) {
+            const uint32_t col = sl * GT_KB + warp * WB_CPW + jj;
+            g[jj] = col < c1 ? wa.list[(uint64_t)w * wa.cap + col] : make_uint2(0u, 0u);
+        }
+#pragma unroll
+        for (int jj = 0; jj < WB_CPW; ++jj) {
+            const int j = warp * WB_CPW + jj;
+            for (uint32_t t = g[jj].x + lane; t < g[jj].y; t += 32) {
+                const uint32_t r = perm[so.tseq[t] & 0x7fffffffu] - lab0;
+                if (r < (uint32_t)WIN_ROWS)  // (a split group: its members in this window)
+                    tile[r * GT_KB + j] = (uint8_t)so.tcnt[t];
+            }
+        }
+        __syncthreads();
+        uint4* dst = (uint4*)(wD + ((uint64_t)sl * wa.nw * WIN_ROWS + (uint64_t)w * WIN_ROWS) * GT_KB);
+        for (int i = threadIdx.x; i < WIN_ROWS * GT_KB / 16; i += WB_THREADS) dst[i] = t4[i];
+        __syncthreads();
+    }
+}
+
+// after a build: the next batch starts at the next whole slab
+__global__ void window_round_kernel(WinArgs wa) {
+    for (uint32_t w = blockIdx.x * blockDim.x + threadIdx.x; w < wa.nw; w += gridDim.x * blockDim.x) {
+        const uint32_t f = min((min(wa.fill[w], wa.cap) + GT_KB - 1) / GT_KB * GT_KB, wa.cap);
+        wa.fill[w] = f;
+        wa.fill[wa.nw + w] = f;
+    }
+}
+
+cudaError_t launch_window_build(SegmentOut so, WinArgs wa, const uint32_t* perm, uint8_t* wD,
+                                int sm_count, cudaStream_t s) {
+    (void)sm_count;
+    if (wa.nw == 0) return cudaGetLastError();
+    window_build_kernel<<<wa.nw * WB_Q, WB_THREADS, 0, s>>>(so, wa, perm, wD);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    window_round_kernel<<<(wa.nw + 255) / 256, 256, 0, s>>>(wa);
+    return cudaGetLastError();
+}
+
+// MACs of a window flush (tiles of 128 x 256 over each window's columns), then the
+// fills (and batch starts) are cleared
+__global__ void window_reset_kernel(WinArgs wa, unsigned long long* stats) {
+    unsigned long long macs = 0;
+    for (uint32_t w = threadIdx.x; w < wa.nw; w += blockDim.x) {
+        const uint32_t k = (min(wa.fill[w], wa.cap) + GT_KB - 1) / GT_KB * GT_KB;
+        macs += (unsigned long long)k * 2 * GT_M * GT_N;
+        wa.fill[w] = 0;
+        wa.fill[wa.nw + w] = 0;
+    }
+    for (int o = 16; o > 0; o >>= 1) macs += __shfl_xor_sync(0xffffffffu, macs, o);
+    if ((threadIdx.x & 31) == 0 && macs) atomicAdd(&stats[ST_WIN_MACS], macs);
+}
+
+cudaError_t launch_window_gram(uint8_t* wD, WinArgs wa, int64_t* wC, const int2* tiles,
+                               int ntiles, int sm_count, unsigned long long* stats,
+                               cudaStream_t s) {
+    if (wa.nw == 0) return cudaGetLastError();
+    CUtensorMap map, cmap;
+    int tma_epi = 0;
+    const int64_t rows = (int64_t)wa.nw * WIN_ROWS;
+    cudaError_t me = gram_maps(wD, rows, wa.cap, wC, rows, WIN_ROWS, GT_EC, &map, &cmap, &tma_epi);
+    if (me != cudaSuccess) return me;
+    if (!tma_epi) return cudaErrorInvalidValue;  // (wC is 16-byte aligned, 256 columns)
+    cudaFuncSetAttribute(gram_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)GT_SMEM);
+    GramArgs a{wC, WIN_ROWS, nullptr, wa.cap, tiles, ntiles, 1, 1, wa.fill};
+    const int grid = ntiles < sm_count ? ntiles : sm_count;
+    gram_kernel<<<grid, GT_THREADS, GT_SMEM, s>>>(map, cmap, a);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    window_reset_kernel<<<1, 1024, 0, s>>>(wa, stats);
+    return cudaGetLastError();
+}
+
+// C_m(X, Y) += wC entries (local row < local col), X, Y = the original sequences of
+// the two labels (min, max: the upper triangle); wC is zeroed again.
+__global__ void window_flush_kernel(int64_t* __restrict__ wC, uint32_t nw,
+                                    const uint32_t* __restrict__ inv, int64_t N,
+                                    int64_t* __restrict__ Cm) {
+    const uint64_t total = (uint64_t)nw * WIN_ROWS * WIN_ROWS;
+    for (uint64_t e = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; e < total;
+         e += (uint64_t)gridDim.x * blockDim.x) {
+        const int64_t v = wC[e];
+        if (v == 0) continue;
+        wC[e] = 0;
+        const uint32_t w = (uint32_t)(e / (WIN_ROWS * WIN_ROWS));
+        const uint32_t r = (uint32_t)(e / WIN_ROWS % WIN_ROWS), c = (uint32_t)(e % WIN_ROWS);
+        const uint64_t lr = (uint64_t)w * WIN_STEP + r, lc = (uint64_t)w * WIN_STEP + c;
+        if (lr >= (uint64_t)N || lc >= (uint64_t)N) continue;
+        const uint32_t X = inv[lr], Y = inv[lc];
+        const uint32_t lo = min(X, Y), hi = max(X, Y);
+        atomicAdd((unsigned long long*)&Cm[(uint64_t)lo * N + hi], (unsigned long long)v);
+    }
+}
+
+cudaError_t launch_window_flush(int64_t* wC, uint32_t nw, const uint32_t* inv, int64_t N,
+                                int64_t* Cm, int sm_count, cudaStream_t s) {
+    if (nw == 0) return cudaGetLastError();
+    window_flush_kernel<<<sm_count * 8, 256, 0, s>>>(wC, nw, inv, N, Cm);
     return cudaGetLastError();
 }
 

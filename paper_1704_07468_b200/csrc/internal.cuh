@@ -143,7 +143,7 @@ __device__ __forceinline__ uint32_t digit_peers(uint32_t d, uint32_t valid_mask)
 
 // Device counters of gakco_stats (int64 slots).
 enum { ST_KEYS = 0, ST_PASSKEYS, ST_TRIPLES, ST_GROUPS, ST_LIGHT_PAIRS, ST_HEAVY_GROUPS,
-       ST_HEAVY_MACS, ST_HEAVY_MACS4, ST_COUNT };
+       ST_HEAVY_MACS, ST_HEAVY_MACS4, ST_WIN_GROUPS, ST_WIN_MACS, ST_COUNT };
 
 // Error flags raised by kernels (bit mask in a device int).
 enum { EF_NEGATIVE_N = 1, EF_K_MISMATCH = 2, EF_BAD_SYMBOL = 4 };
@@ -257,11 +257,31 @@ struct LightBins {
     uint64_t block_cells;
     int nb;
 };
+// Window Gram (relabelled accumulator): a light group whose relabelled members lie
+// in one window of 256 labels [128 w, 128 w + 256) becomes a u8 count column of that
+// window's dense block, multiplied on the tensor cores (gram_tc.cu); nw = 0: off.
+constexpr int WIN_ROWS = 256;   // labels per window
+constexpr int WIN_STEP = 128;   // window starts
+struct WinArgs {
+    uint32_t* fill;   // [2][nw] columns claimed per window; [1]: this batch's first
+    uint2* list;      // [nw][cap] triple range of each claimed group
+    uint32_t cap;     // columns per window
+    uint32_t nw;      // windows (0: the window path is off)
+    uint32_t wmin;    // smallest group (sequences) taken
+};
+cudaError_t launch_window_build(SegmentOut so, WinArgs wa, const uint32_t* perm, uint8_t* wD,
+                                int sm_count, cudaStream_t s);
+cudaError_t launch_window_gram(uint8_t* wD, WinArgs wa, int64_t* wC, const int2* tiles,
+                               int ntiles, int sm_count, unsigned long long* stats,
+                               cudaStream_t s);
+cudaError_t launch_window_flush(int64_t* wC, uint32_t nw, const uint32_t* inv, int64_t N,
+                                int64_t* Cm, int sm_count, cudaStream_t s);
 cudaError_t launch_light(SegmentOut so, uint64_t max_groups, int64_t heavy_min, int64_t N,
                          uint32_t* acc, uint2* heavy_list, uint64_t ldd,
                          uint32_t* dense_fill, LightBins bins, uint32_t flat_max,
                          int64_t NA, const uint32_t* perm, uint32_t heavy_cmax,
-                         unsigned long long* stats, int sm_count, cudaStream_t s);
+                         unsigned long long* stats, int sm_count, cudaStream_t s,
+                         WinArgs wa = WinArgs{nullptr, nullptr, 0, 0, 0});
 // Light accumulator relabelled by perm (sequence -> accumulator index): flush it into
 // C_m (original order) and zero it.
 cudaError_t launch_light_flush_perm(uint32_t* acc, int64_t N, int64_t* Cm, const uint32_t* perm,

@@ -98,7 +98,7 @@ __global__ void __launch_bounds__(256) light_kernel(SegmentOut so, int64_t heavy
                                                     LightBins bn, uint32_t flat_max,
                                                     int64_t NA, const uint32_t* perm,
                                                     uint32_t heavy_cmax,
-                                                    unsigned long long* stats) {
+                                                    unsigned long long* stats, WinArgs wa) {
     // triangle table: pairs (a < b < 32) ordered by b, so the first n(n-1)/2
     // entries are exactly the pairs of an n-triple chunk
     __shared__ uint16_t s_tri[496];
@@ -110,7 +110,7 @@ __global__ void __launch_bounds__(256) light_kernel(SegmentOut so, int64_t heavy
     const int lane = threadIdx.x & 31;
     const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
     const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-    unsigned long long pairs = 0, nheavy = 0;
+    unsigned long long pairs = 0, nheavy = 0, nwin = 0;
     // A warp takes 32 groups at a time: one coalesced load brings all their
     // triple ranges, and the first 32 triples of the next group are loaded while
     // the current one is processed.
@@ -194,6 +194,44 @@ __global__ void __launch_bounds__(256) light_kernel(SegmentOut so, int64_t heavy
             }
         }
 
+        // (1c) window candidates (relabelled accumulator): light groups of >= wmin
+        // sequences whose labels lie in one window of 256 become u8 count columns of
+        // that window's block (window Gram); counts > 255 or a full window: light.
+        // (Splitting groups that straddle windows -- their in-window pairs to the Gram,
+        // the rest light -- was measured: no gain on Scale.)
+        if (wa.nw) {
+            uint32_t cand = __ballot_sync(0xffffffffu, lane < ng && !flat &&
+                                                           (int64_t)my_s < heavy_min &&
+                                                           my_s >= wa.wmin) & ~got;
+            while (cand) {
+                const int jj = __ffs(cand) - 1;
+                cand &= cand - 1;
+                const uint32_t a0 = __shfl_sync(0xffffffffu, my_start, jj);
+                const uint32_t b0 = __shfl_sync(0xffffffffu, my_end, jj);
+                uint32_t lmin = 0xffffffffu, lmax = 0, cmax = 0;
+                for (uint32_t t = a0 + lane; t < b0; t += 32) {
+                    const uint32_t lb = perm[so.tseq[t] & 0x7fffffffu];
+                    lmin = min(lmin, lb);
+                    lmax = max(lmax, lb);
+                    cmax = max(cmax, so.tcnt[t]);
+                }
+                lmin = __reduce_min_sync(0xffffffffu, lmin);
+                lmax = __reduce_max_sync(0xffffffffu, lmax);
+                cmax = __reduce_max_sync(0xffffffffu, cmax);
+                const uint32_t w = lmin / WIN_STEP;
+                if (cmax <= 255u && lmax < w * WIN_STEP + WIN_ROWS) {
+                    uint32_t col = 0;
+                    if (lane == 0) col = atomicAdd(&wa.fill[w], 1u);
+                    col = __shfl_sync(0xffffffffu, col, 0);
+                    if (col < wa.cap) {
+                        if (lane == 0) wa.list[(uint64_t)w * wa.cap + col] = make_uint2(a0, b0);
+                        got |= 1u << jj;
+                        nwin += lane == 0 ? 1u : 0u;
+                    }
+                }
+            }
+        }
+
         // (2) the other groups one by one (big light groups)
         uint32_t todo = __ballot_sync(0xffffffffu, lane < ng && !flat) & ~got;
         uint32_t pa0 = 0, pb0 = 0, pX = 0, pC = 0;
@@ -256,20 +294,22 @@ __global__ void __launch_bounds__(256) light_kernel(SegmentOut so, int64_t heavy
     }
     if (lane == 0 && pairs) atomicAdd(&stats[ST_LIGHT_PAIRS], pairs);
     if (lane == 0 && nheavy) atomicAdd(&stats[ST_HEAVY_GROUPS], nheavy);
+    if (lane == 0 && nwin) atomicAdd(&stats[ST_WIN_GROUPS], nwin);
 }
 
 cudaError_t launch_light(SegmentOut so, uint64_t max_groups, int64_t heavy_min, int64_t N,
                          uint32_t* acc, uint2* heavy_list, uint64_t ldd,
                          uint32_t* dense_fill, LightBins bins, uint32_t flat_max,
                          int64_t NA, const uint32_t* perm, uint32_t heavy_cmax,
-                         unsigned long long* stats, int sm_count, cudaStream_t s) {
+                         unsigned long long* stats, int sm_count, cudaStream_t s,
+                         WinArgs wa) {
     if (max_groups == 0) return cudaGetLastError();
     uint64_t blocks = (max_groups + 255) / 256;  // 8 warps x 32 groups per block-round
     uint64_t cap = (uint64_t)sm_count * 8;
     if (blocks > cap) blocks = cap;
     light_kernel<<<(unsigned)blocks, 256, 0, s>>>(so, heavy_min, N, acc, heavy_list, ldd,
                                                   dense_fill, bins, flat_max, NA, perm,
-                                                  heavy_cmax, stats);
+                                                  heavy_cmax, stats, wa);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess || bins.nb == 0) return e;
     return launch_apply_bins(acc, bins, sm_count, s);

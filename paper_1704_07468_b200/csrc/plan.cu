@@ -88,6 +88,8 @@ struct gakco_plan {
     int gram_pair = 1;         // 1: CTA-pair Gram (gram2.cu), 0: one-SM Gram (gram_tc.cu)
     int light_flat = 8;        // light groups of <= this many sequences share warps
     int light_relabel = -1;    // -1 auto (accumulator >> L2), 0 off, 1 on
+    int light_window = -1;     // window Gram of cluster-local groups: -1 auto (with relabelling), 0 off, 1 on (relabels)
+    int64_t window_min = 9;    // smallest group (sequences) for the window Gram
     int level_order_desc = 0;  // process levels m = M..0 (1) or 0..M (0, measured faster on DNA)
     int gram_fp4 = -1;         // -1 auto (e2m1 Gram when exact), 0 u8 / kind::i8, 1 e2m1
     int pipeline = 1;          // light / dense / Gram of batch b on an aux stream, overlapping
@@ -104,7 +106,7 @@ struct gakco_plan {
     std::vector<std::array<uint8_t, GMAX>> mask_kept;
     std::vector<int> key_bits;  // per level
 
-    DevBuf trieS0, trieW, trieS, keptsh, dense2, heavy2, hcount2, tseq2, tcnt2, gstart2, counts2, perm, iota, best, parent, Dgscr, Kdscr, codes, off, gofs, gmseq, keysA, keysB, hist, status, ctr, tseq, tcnt, gstart, gend,
+    DevBuf wD, wlist, wfill, wC, winv, wtiles, trieS0, trieW, trieS, keptsh, dense2, heavy2, hcount2, tseq2, tcnt2, gstart2, counts2, perm, iota, best, parent, Dgscr, Kdscr, codes, off, gofs, gmseq, keysA, keysB, hist, status, ctr, tseq, tcnt, gstart, gend,
         counts, kept, stats, flags, kdiag, Cscr, Nmscr, Kscr, Knscr, heavy, hcount, dense, tiles, tiles4, symhist,
         lightacc, binrec, bincnt, win, bkH, bktot, bkbase, bkdesc, bktab, bktcnt, bkgs, bkocc;
     int64_t tiles_npad = -1;
@@ -267,7 +269,7 @@ extern "C" void gakco_destroy(gakco_plan* p) {
                       &p->hist,  &p->status, &p->ctr,  &p->tseq,   &p->tcnt,  &p->gstart,
                       &p->gend,  &p->counts, &p->kept, &p->stats,  &p->flags, &p->kdiag,
                       &p->Cscr,  &p->Nmscr, &p->Kscr,  &p->Knscr, &p->heavy, &p->hcount,
-                      &p->dense, &p->tiles, &p->tiles4, &p->symhist, &p->trieS0, &p->trieW, &p->trieS, &p->lightacc, &p->binrec, &p->bincnt,
+                      &p->dense, &p->tiles, &p->tiles4, &p->symhist, &p->trieS0, &p->trieW, &p->trieS, &p->wD, &p->wlist, &p->wfill, &p->wC, &p->winv, &p->wtiles, &p->lightacc, &p->binrec, &p->bincnt,
                       &p->win,   &p->bkH,   &p->bktot, &p->bkbase, &p->bkdesc, &p->bktab,
                       &p->bktcnt, &p->bkgs, &p->bkocc};
     for (DevBuf* b : bufs)
@@ -323,6 +325,14 @@ extern "C" gakco_status gakco_set_option(gakco_plan* p, int option, int64_t valu
         case GAKCO_OPT_LIGHT_RELABEL:
             if (value < -1 || value > 1) return p->fail(GAKCO_E_ARG, "relabel must be -1..1");
             p->light_relabel = (int)value;
+            return GAKCO_OK;
+        case GAKCO_OPT_LIGHT_WINDOW:
+            if (value < -1 || value > 1) return p->fail(GAKCO_E_ARG, "light window must be -1..1");
+            p->light_window = (int)value;
+            return GAKCO_OK;
+        case GAKCO_OPT_WINDOW_MIN:
+            if (value < 2) return p->fail(GAKCO_E_ARG, "window min must be >= 2");
+            p->window_min = value;
             return GAKCO_OK;
         case GAKCO_OPT_GRAM_FP4:
             if (value < -1 || value > 1) return p->fail(GAKCO_E_ARG, "gram fp4 must be -1..1");
@@ -851,8 +861,37 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
     // first level by clusters of best partners (argmax_Y C_m(X,Y)), so pairs that
     // share many keys (families) update nearby cells; the flush maps back.
     const bool relabel = !rect && bins.nb == 0 && N >= 2 &&
-                         (p->light_relabel == 1 ||
+                         (p->light_relabel == 1 || p->light_window == 1 ||
                           (p->light_relabel == -1 && ntri * 4 > (96ull << 20)));
+    // window Gram: once relabelled, groups whose labels lie in one
+    // window of 256 go to the tensor cores as u8 columns of that window's block
+    const bool win_on = relabel && p->light_window != 0 && n > 0;
+    WinArgs wa{nullptr, nullptr, 0, 0, 0};
+    int nwtiles = 0;
+    if (win_on) {
+        const uint32_t nw = (uint32_t)((N + WIN_STEP - 1) / WIN_STEP);
+        // columns per window: a few batches' claims, <= 64K, D <= 2 GB
+        uint64_t cap = std::min<uint64_t>(65536, (2048ull << 20) / ((uint64_t)nw * WIN_ROWS));
+        cap = std::max<uint64_t>(128, cap / 128 * 128);
+        CK(p->ensure(p->wD, cap * nw * WIN_ROWS, s));
+        CK(p->ensure(p->wlist, cap * nw * sizeof(uint2), s));
+        CK(p->ensure(p->wfill, 2 * nw * 4, s, /*zero=*/true));
+        CK(cudaMemsetAsync(p->wfill.p, 0, 2 * nw * 4, s));
+        CK(p->ensure(p->wC, (size_t)nw * WIN_ROWS * WIN_ROWS * 8, s, /*zero=*/true));
+        CK(cudaMemsetAsync(p->wC.p, 0, (size_t)nw * WIN_ROWS * WIN_ROWS * 8, s));
+        CK(p->ensure(p->winv, N * 4, s));
+        std::vector<int2> wt;
+        for (uint32_t w = 0; w < nw; ++w) {
+            wt.push_back(make_int2((int)(2 * w), (int)w));
+            wt.push_back(make_int2((int)(2 * w + 1), (int)w));
+        }
+        CK(p->ensure(p->wtiles, wt.size() * sizeof(int2), s));
+        CK(cudaMemcpyAsync(p->wtiles.p, wt.data(), wt.size() * sizeof(int2), cudaMemcpyHostToDevice, s));
+        CK(cudaStreamSynchronize(s));  // wt is a local buffer
+        nwtiles = (int)wt.size();
+        wa = WinArgs{(uint32_t*)p->wfill.p, (uint2*)p->wlist.p, (uint32_t)cap, nw,
+                     (uint32_t)std::max<int64_t>(p->window_min, (int64_t)p->light_flat + 1)};
+    }
     bool perm_active = false;
     if (relabel) {
         CK(p->ensure(p->perm, N * 4, s));
@@ -882,7 +921,9 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
                          [&](uint32_t a, uint32_t b) { return root[a] < root[b]; });
         for (int64_t i = 0; i < N; ++i) pm[order[i]] = (uint32_t)i;
         CK(cudaMemcpyAsync(p->perm.p, pm.data(), N * 4, cudaMemcpyHostToDevice, s));
-        CK(cudaStreamSynchronize(s));  // pm is a local buffer
+        if (win_on)  // label -> sequence, for the window flush
+            CK(cudaMemcpyAsync(p->winv.p, order.data(), N * 4, cudaMemcpyHostToDevice, s));
+        CK(cudaStreamSynchronize(s));  // pm / order are local buffers
         perm_active = true;
         return GAKCO_OK;
     };
@@ -890,6 +931,26 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
     int light_m = -1;
     const uint64_t light_lim =
         nmax > 0 ? std::max<uint64_t>(1, (uint64_t)UINT32_MAX / ((uint64_t)nmax * nmax)) : 1;
+    // window Gram of the pending window columns (every few batches, and before the
+    // window block is added into C_m); s32 sums exact: a batch spans <= (2^31-1)/n_max^2
+    // masks and a Gram <= WIN_BATCHES batches (the accumulation before is int64)
+    int win_pending = 0;
+    uint64_t win_masks = 0;
+    constexpr int WIN_BATCHES = 4;
+    const uint64_t win_lim =
+        nmax > 0 ? std::max<uint64_t>(1, (uint64_t)INT32_MAX / ((uint64_t)nmax * nmax)) : 1;
+    auto wgram = [&]() -> gakco_status {
+        if (win_pending == 0) return GAKCO_OK;
+        cudaEvent_t aw = nullptr;
+        p->stage_begin(s2, &aw);
+        p->launches += 1;  // + reset
+        LK(launch_window_gram((uint8_t*)p->wD.p, wa, (int64_t*)p->wC.p, (const int2*)p->wtiles.p,
+                              nwtiles, p->sm_count, stats, s2));
+        p->stage_end(s2, S_HEAVY, aw);
+        win_pending = 0;
+        win_masks = 0;
+        return GAKCO_OK;
+    };
     auto lflush = [&]() -> gakco_status {
         if (light_m < 0 || light_masks == 0) return GAKCO_OK;
         cudaEvent_t al = nullptr;
@@ -897,9 +958,16 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
         if (rect)
             LK(launch_light_flush_rect((uint32_t*)p->lightacc.p, ntri, level_ptr(light_m),
                                        p->sm_count, s2));
-        else if (perm_active)
+        else if (perm_active) {
             LK(launch_light_flush_perm((uint32_t*)p->lightacc.p, N, level_ptr(light_m),
                                        (const uint32_t*)p->perm.p, p->sm_count, s2));
+            if (win_on) {
+                gakco_status ws = wgram();
+                if (ws != GAKCO_OK) return ws;
+                LK(launch_window_flush((int64_t*)p->wC.p, wa.nw, (const uint32_t*)p->winv.p, N,
+                                       level_ptr(light_m), p->sm_count, s2));
+            }
+        }
         else
             LK(launch_light_flush((uint32_t*)p->lightacc.p, N, level_ptr(light_m), p->sm_count,
                                   s2));
@@ -1124,8 +1192,25 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
                             heavy_p(), rcap_of(m), hcount_p(), bins,
                             (uint32_t)p->light_flat, NA,
                             perm_active ? (const uint32_t*)p->perm.p : nullptr,
-                            fp4_lv[m] ? 4u : 255u, stats, p->sm_count, s2));
+                            fp4_lv[m] ? 4u : 255u, stats, p->sm_count, s2,
+                            perm_active && win_on ? wa : WinArgs{nullptr, nullptr, 0, 0, 0}));
             p->stage_end(s2, S_LIGHT, a);
+            if (perm_active && win_on) {  // this batch's window columns (+ the Gram every few)
+                if (win_masks + nmask > win_lim) {  // s32 exactness of the next Gram
+                    gakco_status ws = wgram();
+                    if (ws != GAKCO_OK) return ws;
+                }
+                win_masks += nmask;
+                p->stage_begin(s2, &a);
+                p->launches += 1;  // + round
+                LK(launch_window_build(so, wa, (const uint32_t*)p->perm.p, (uint8_t*)p->wD.p,
+                                       p->sm_count, s2));
+                p->stage_end(s2, S_DENSE, a);
+                if (++win_pending >= WIN_BATCHES) {
+                    gakco_status ws = wgram();
+                    if (ws != GAKCO_OK) return ws;
+                }
+            }
             if (gram_ok) {
                 p->stage_begin(s2, &a);
                 p->launches += 1;  // + fill_round
@@ -1407,6 +1492,8 @@ extern "C" gakco_status gakco_get_stats(gakco_plan* p, gakco_stats* out) {
         r.heavy_groups = (int64_t)d[ST_HEAVY_GROUPS];
         r.heavy_macs = (int64_t)d[ST_HEAVY_MACS];
         r.heavy_macs_fp4 = (int64_t)d[ST_HEAVY_MACS4];
+        r.win_groups = (int64_t)d[ST_WIN_GROUPS];
+        r.win_macs = (int64_t)d[ST_WIN_MACS];
     }
     double* ms[S_NSTAGE] = {&r.ms_encode, &r.ms_sort,     &r.ms_segment, &r.ms_light,
                             &r.ms_heavy,  &r.ms_epilogue, &r.ms_dense};

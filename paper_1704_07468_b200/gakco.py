@@ -39,6 +39,8 @@ GAKCO_OPT_LIGHT_RELABEL = 9
 GAKCO_OPT_GRAM_FP4 = 10
 GAKCO_OPT_PIPELINE = 11
 GAKCO_OPT_LEVEL_ORDER = 12
+GAKCO_OPT_LIGHT_WINDOW = 13
+GAKCO_OPT_WINDOW_MIN = 14
 
 EXPORTS = ("gakco_create", "gakco_set_shard", "gakco_set_option", "gakco_accumulate",
            "gakco_finalize", "gakco_kernel", "gakco_kernel_k", "gakco_kernel_rect",
@@ -54,7 +56,8 @@ class gakco_stats(ctypes.Structure):
         (n, ctypes.c_int64) for n in (
             "n_encode", "n_sort", "n_segment", "n_light", "n_heavy", "n_epilogue", "keys32",
             "sort_passes32", "grouping")] + [("ms_dense", ctypes.c_double)] + [
-        (n, ctypes.c_int64) for n in ("n_dense", "n_pad", "gram_fp4", "heavy_macs_fp4")]
+        (n, ctypes.c_int64) for n in ("n_dense", "n_pad", "gram_fp4", "heavy_macs_fp4",
+                                        "win_groups", "win_macs")]
 
     def as_dict(self):
         return {n: getattr(self, n) for n, _ in self._fields_}

@@ -185,6 +185,28 @@ def test_light_relabel(gk, oracle_lib):
         ref = oracle_lib.compute(cp, g, k, M)
         assert_parity(run(gk, cp, g, k, M, light_relabel=1), ref)
         assert_parity(run(gk, cp, g, k, M, light_relabel=1, heavy_min_seqs=1 << 50), ref)
+        assert_parity(run(gk, cp, g, k, M, light_relabel=1, light_window=0), ref)
+
+
+def test_light_window_gram(gk, oracle_lib):
+    """Window Gram (relabelled accumulator; groups inside one window of 256 labels
+    -> u8 columns of that window's block on the tensor cores) == oracle: every
+    multi-sequence group a candidate (flat 1, window min 2), windows straddling the
+    end of the label range (N not a multiple of 128), counts > 1, several windows."""
+    rng = np.random.default_rng(131)
+    cases = [(sc.gen_families(11, 300, 12, 70, 40, 70, sigma=20), 6, 3, 3),
+             (sc.gen_families(12, 517, 9, 90, 90, 90, sigma=4), 7, 4, 3),
+             (sc.gen_families(13, 700, 40, 60, 60, 60, sigma=20), 6, 2, 4),
+             (sc.random_small(rng, 4, n_max=300, l_max=120), 5, 2, 3)]
+    for cp, g, k, M in cases:
+        ref = oracle_lib.compute(cp, g, k, M)
+        r = run(gk, cp, g, k, M, light_window=1, light_flat=1, window_min=2,
+                heavy_min_seqs=1 << 50)
+        assert_parity(r, ref)
+        r2 = run(gk, cp, g, k, M, light_window=1)
+        assert_parity(r2, ref)
+        if cp.n_seq > 300:
+            assert r["stats"]["win_groups"] > 0 and r["stats"]["win_macs"] > 0
 
 
 def test_light_binning(gk, oracle_lib):
