@@ -47,13 +47,17 @@ def args_():
                     help="target seconds of oracle work per CPU sample")
     ap.add_argument("--heavy-min", type=int, default=0)
     ap.add_argument("--batch-keys", type=int, default=0)
-    ap.add_argument("--sort", type=int, default=None, choices=[-1, 0, 1, 2, 3, 4, 5, 6],
+    ap.add_argument("--sort", type=int, default=None, choices=[-1, 0, 1, 2, 3, 4, 5, 6, 7],
                     help="grouping: -1 auto, 0 chunked LSD sort, 1 onesweep LSD, 2 hash partition, "
                          "3/4/5 chunked LSD v2 (bulk-copy tiles; atomicOr / match.any / ballot ranking), "
-                         "6 mask trie (shared leading-position passes)")
+                         "6 mask trie (shared leading-position passes), 7 batched mask trie")
     ap.add_argument("--sort-ctas", type=int, default=0)
     ap.add_argument("--light-flat", type=int, default=0,
                     help="light groups of <= this many sequences share a warp (1..32)")
+    ap.add_argument("--light-window", type=int, default=None, choices=[-1, 0, 1],
+                    help="window Gram of cluster-local light groups (-1 auto)")
+    ap.add_argument("--window-min", type=int, default=0,
+                    help="smallest group for the window Gram (0: default)")
     ap.add_argument("--relabel", type=int, default=None, choices=[-1, 0, 1],
                     help="light accumulator relabelling: -1 auto, 0 off, 1 on")
     ap.add_argument("--fp4", type=int, default=None, choices=[-1, 0, 1],
@@ -288,6 +292,10 @@ def run_ours(a):
         plan.set_option(gakco.GAKCO_OPT_LIGHT_FLAT, a.light_flat)
     if a.relabel is not None:
         plan.set_option(gakco.GAKCO_OPT_LIGHT_RELABEL, a.relabel)
+    if a.light_window is not None:
+        plan.set_option(gakco.GAKCO_OPT_LIGHT_WINDOW, a.light_window)
+    if a.window_min:
+        plan.set_option(gakco.GAKCO_OPT_WINDOW_MIN, a.window_min)
     if a.fp4 is not None:
         plan.set_option(gakco.GAKCO_OPT_GRAM_FP4, a.fp4)
     if a.pipeline is not None:

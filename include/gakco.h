@@ -73,7 +73,12 @@ typedef enum {
                                      6 = mask trie: per-position stable passes over packed
                                      windows + sequence ids, passes of common leading kept
                                      positions shared between masks (auto when a mask has
-                                     >= 2M g-mers and g*ceil(log2 sigma) <= 64) */
+                                     >= 2M g-mers and g*ceil(log2 sigma) <= 64),
+                                     7 = batched mask trie over one-word composites (window
+                                     << sb | seq): up to 4 symbols per pass, a batch's trie
+                                     run depth by depth, one launch per depth (auto below
+                                     2M g-mers when g*ceil(log2 sigma) + ceil(log2 N) <= 64)
+                                     */
     GAKCO_OPT_SORT_CTAS_PER_SM = 5, /* chunked pass grid size in CTAs per SM (defaults: 4 for
                                        the batched LSD passes on u64 composites, 8 on u32,
                                        2 for the mask trie; setting it sets all three) */
@@ -134,7 +139,7 @@ typedef struct {
     int64_t sort_passes32;  /* of `sort_passes`, those over 32-bit composites */
     int64_t grouping;       /* path of the last accumulate: 0 chunked LSD sort,
                                1 onesweep LSD sort, 2 hash partition (bucket.cu),
-                               3 mask trie */
+                               3 mask trie, 4 batched mask trie */
     double ms_dense;        /* building the dense u8 count columns of heavy groups */
     int64_t n_dense;
     int64_t n_pad;          /* rows of the dense count matrix (0: no tensor-core Gram) */

@@ -225,6 +225,29 @@ cudaError_t launch_onesweep(const uint64_t* in, uint64_t* out, uint64_t n, int n
                             const uint32_t* hist, int pass, int npass, uint64_t* status,
                             uint32_t* ctr, uint32_t epoch, cudaStream_t s);
 // Chunked LSD pass (radix_hist + radix_scatter); hist: >= (target_ctas + nseg) * 256 u32.
+// batched mask trie pass descriptor (one per segment of a launch)
+struct PassDesc {
+    uint64_t in_off;   // first key of the segment's input (elements)
+    uint64_t out_off;  // first key of its output
+    uint64_t omask;    // output = key & omask (a leaf: the mask's key bits | seq bits)
+    uint8_t sh[4];     // bit offsets of the digit's symbols (least significant first)
+    uint32_t nsym;     // symbols in the digit (1..4)
+    uint32_t symbits;  // bits per symbol
+};
+template <typename K>
+__device__ __forceinline__ uint32_t pd_digit(K k, const PassDesc& d) {
+    const uint32_t m = (1u << d.symbits) - 1u;
+    uint32_t v = (uint32_t)(k >> d.sh[0]) & m;
+    if (d.nsym > 1) v |= ((uint32_t)(k >> d.sh[1]) & m) << d.symbits;
+    if (d.nsym > 2) v |= ((uint32_t)(k >> d.sh[2]) & m) << (2 * d.symbits);
+    if (d.nsym > 3) v |= ((uint32_t)(k >> d.sh[3]) & m) << (3 * d.symbits);
+    return v;
+}
+cudaError_t launch_trie_batch(const void* in, void* out, bool k64, uint64_t n, int nseg,
+                              const PassDesc* desc, uint32_t* hist, int target_ctas,
+                              cudaStream_t s, int* nlaunch);
+cudaError_t launch_trie_root(const uint64_t* win, const uint32_t* seq, uint64_t n, int sb,
+                             bool k64, void* out, int sm_count, cudaStream_t s);
 cudaError_t launch_trie_pass(const uint64_t* win, uint64_t* wout, const void* sin, void* sout,
                              bool seq16, uint64_t n, int shift, uint32_t dmask, uint64_t omask,
                              uint32_t* hist, int target_ctas, cudaStream_t s, int* nlaunch);

@@ -92,6 +92,7 @@ cudaError_t launch_apply_bins(uint32_t* acc, LightBins bn, int sm_count, cudaStr
     return cudaMemsetAsync(bn.cnt, 0, bn.nb * sizeof(uint32_t), s);
 }
 
+template <bool WIN>
 __global__ void __launch_bounds__(256) light_kernel(SegmentOut so, int64_t heavy_min, int64_t N,
                                                     uint32_t* acc, uint2* heavy_list,
                                                     uint64_t ldd, uint32_t* dense_fill,
@@ -199,7 +200,7 @@ __global__ void __launch_bounds__(256) light_kernel(SegmentOut so, int64_t heavy
         // that window's block (window Gram); counts > 255 or a full window: light.
         // (Splitting groups that straddle windows -- their in-window pairs to the Gram,
         // the rest light -- was measured: no gain on Scale.)
-        if (wa.nw) {
+        if (WIN && wa.nw) {  // (a separate instantiation: no register cost otherwise)
             uint32_t cand = __ballot_sync(0xffffffffu, lane < ng && !flat &&
                                                            (int64_t)my_s < heavy_min &&
                                                            my_s >= wa.wmin) & ~got;
@@ -307,9 +308,14 @@ cudaError_t launch_light(SegmentOut so, uint64_t max_groups, int64_t heavy_min, 
     uint64_t blocks = (max_groups + 255) / 256;  // 8 warps x 32 groups per block-round
     uint64_t cap = (uint64_t)sm_count * 8;
     if (blocks > cap) blocks = cap;
-    light_kernel<<<(unsigned)blocks, 256, 0, s>>>(so, heavy_min, N, acc, heavy_list, ldd,
-                                                  dense_fill, bins, flat_max, NA, perm,
-                                                  heavy_cmax, stats, wa);
+    if (wa.nw)
+        light_kernel<true><<<(unsigned)blocks, 256, 0, s>>>(so, heavy_min, N, acc, heavy_list,
+                                                            ldd, dense_fill, bins, flat_max, NA,
+                                                            perm, heavy_cmax, stats, wa);
+    else
+        light_kernel<false><<<(unsigned)blocks, 256, 0, s>>>(so, heavy_min, N, acc, heavy_list,
+                                                             ldd, dense_fill, bins, flat_max, NA,
+                                                             perm, heavy_cmax, stats, wa);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess || bins.nb == 0) return e;
     return launch_apply_bins(acc, bins, sm_count, s);

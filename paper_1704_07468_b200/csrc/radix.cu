@@ -184,10 +184,11 @@ cudaError_t launch_onesweep(const uint64_t* in, uint64_t* out, uint64_t n, int n
 constexpr int RS_THREADS = SORT_THREADS;  // 512
 constexpr int RS_WARPS = RS_THREADS / 32;
 
-template <typename K>
+template <typename K, bool DESC = false>
 __global__ void __launch_bounds__(RS_THREADS) radix_hist_kernel(
     const K* __restrict__ in, uint64_t n, uint32_t cps, uint64_t L, int shift,
-    uint32_t* __restrict__ hist, uint32_t dmask = 0xffu) {
+    uint32_t* __restrict__ hist, uint32_t dmask = 0xffu,
+    const PassDesc* __restrict__ pdesc = nullptr) {
     constexpr int E = 16 / sizeof(K);  // keys per 16-byte load
     __shared__ uint32_t s_h[RS_WARPS][RADIX];
     const int tid = threadIdx.x, w = tid >> 5;
@@ -196,12 +197,18 @@ __global__ void __launch_bounds__(RS_THREADS) radix_hist_kernel(
     const uint32_t seg = blockIdx.x / cps, c = blockIdx.x - seg * cps;
     const uint64_t lo = (uint64_t)c * L;
     const uint64_t hi = min(n, lo + L);
-    const K* p = in + (uint64_t)seg * n;
+    PassDesc pd{};
+    if constexpr (DESC) pd = pdesc[seg];
+    const K* p = in + (DESC ? pd.in_off : (uint64_t)seg * n);
+    auto digit = [&](K k) -> uint32_t {
+        if constexpr (DESC) return pd_digit(k, pd);
+        else return (uint32_t)(k >> shift) & dmask;
+    };
     if (lo < hi) {
         // 16-byte loads on the aligned body, scalars on the edges
         uint64_t a = lo;
         while (a < hi && ((uintptr_t)(p + a) & 15)) {
-            if (tid == 0) atomicAdd(&s_h[0][(uint32_t)(p[a] >> shift) & dmask], 1u);
+            if (tid == 0) atomicAdd(&s_h[0][digit(p[a])], 1u);
             ++a;
         }
         const uint64_t nv = (hi - a) / E;
@@ -210,10 +217,10 @@ __global__ void __launch_bounds__(RS_THREADS) radix_hist_kernel(
             const uint4 q = v[i];
             const K* kq = (const K*)&q;
 #pragma unroll
-            for (int e = 0; e < E; ++e) atomicAdd(&s_h[w][(uint32_t)(kq[e] >> shift) & dmask], 1u);
+            for (int e = 0; e < E; ++e) atomicAdd(&s_h[w][digit(kq[e])], 1u);
         }
         for (uint64_t i = a + nv * E + tid; i < hi; i += RS_THREADS)
-            atomicAdd(&s_h[w][(uint32_t)(p[i] >> shift) & dmask], 1u);
+            atomicAdd(&s_h[w][digit(p[i])], 1u);
     }
     __syncthreads();
     if (tid < RADIX) {
@@ -446,9 +453,9 @@ __device__ __forceinline__ void rs2_issue(K* buf, const K* in, P* pbuf, const P*
     if constexpr (rs2_haspay<P>()) rs2_copy(pbuf, pin, g0, cnt, bar);
 }
 
-template <typename K, int RANK, bool FULL>
+template <typename K, int RANK, bool FULL, typename Dig>
 __device__ __forceinline__ void rs2_rank(const K (&keys)[RS2_ITEMS], uint32_t (&rank)[RS2_ITEMS],
-                                         int shift, uint32_t dmask, uint32_t cnt, uint32_t* whist,
+                                         const Dig& digit, uint32_t cnt, uint32_t* whist,
                                          uint32_t* mbin, int w, int lane) {
     const uint32_t lt = lanemask_lt();
     if (RANK == 1) {
@@ -456,7 +463,7 @@ __device__ __forceinline__ void rs2_rank(const K (&keys)[RS2_ITEMS], uint32_t (&
 #pragma unroll
         for (int i = 0; i < RS2_ITEMS; ++i) {
             const uint32_t idx = (uint32_t)(w * RS2_ITEMS * 32 + i * 32 + lane);
-            uint32_t d = (uint32_t)(keys[i] >> shift) & dmask;
+            uint32_t d = digit(keys[i]);
             if (!FULL && idx >= cnt) d = 0x100u;  // invalid lanes only match each other
             rank[i] = __match_any_sync(0xffffffffu, d);
         }
@@ -464,7 +471,7 @@ __device__ __forceinline__ void rs2_rank(const K (&keys)[RS2_ITEMS], uint32_t (&
         for (int i = 0; i < RS2_ITEMS; ++i) {
             const uint32_t idx = (uint32_t)(w * RS2_ITEMS * 32 + i * 32 + lane);
             const bool valid = FULL || idx < cnt;
-            const uint32_t d = (uint32_t)(keys[i] >> shift) & dmask;
+            const uint32_t d = digit(keys[i]);
             const uint32_t peers = rank[i];
             const uint32_t prior = valid ? whist[d] : 0u;
             __syncwarp();
@@ -478,7 +485,7 @@ __device__ __forceinline__ void rs2_rank(const K (&keys)[RS2_ITEMS], uint32_t (&
         for (int i = 0; i < RS2_ITEMS; ++i) {
             const uint32_t idx = (uint32_t)(w * RS2_ITEMS * 32 + i * 32 + lane);
             const bool valid = FULL || idx < cnt;
-            const uint32_t d = (uint32_t)(keys[i] >> shift) & dmask;
+            const uint32_t d = digit(keys[i]);
             const uint32_t peers = digit_peers(d, __ballot_sync(0xffffffffu, valid));
             const uint32_t prior = valid ? whist[d] : 0u;
             __syncwarp();
@@ -491,7 +498,7 @@ __device__ __forceinline__ void rs2_rank(const K (&keys)[RS2_ITEMS], uint32_t (&
         for (int i = 0; i < RS2_ITEMS; ++i) {
             const uint32_t idx = (uint32_t)(w * RS2_ITEMS * 32 + i * 32 + lane);
             const bool valid = FULL || idx < cnt;
-            const uint32_t d = (uint32_t)(keys[i] >> shift) & dmask;
+            const uint32_t d = digit(keys[i]);
             if (valid) atomicOr(&mbin[d], 1u << lane);
             __syncwarp();
             const uint32_t peers = valid ? mbin[d] : 0u;
@@ -507,15 +514,15 @@ __device__ __forceinline__ void rs2_rank(const K (&keys)[RS2_ITEMS], uint32_t (&
     }
 }
 
-template <typename K, typename P, int RANK>
+template <typename K, typename P, int RANK, bool DESC = false>
 __global__ void __launch_bounds__(RS2_THREADS, (sizeof(K) == 8 ? 2 : 3)) radix_scatter2_kernel(
     const K* __restrict__ in, K* __restrict__ out, const P* __restrict__ pin, P* __restrict__ pout,
     uint64_t n, uint32_t cps, uint64_t L, int shift, uint32_t dmask_,
-    const uint32_t* __restrict__ hist, K omask_, int prescanned) {
+    const uint32_t* __restrict__ hist, K omask_, int prescanned,
+    const PassDesc* __restrict__ pdesc = nullptr) {
     constexpr bool HASP = rs2_haspay<P>();
     // (the plain LSD passes: full 8-bit digits, no output mask -- compile-time)
     const uint32_t dmask = HASP ? dmask_ : 0xffu;
-    const K omask = HASP ? omask_ : ~(K)0;
     extern __shared__ __align__(16) unsigned char smem[];
     K* const buf0 = (K*)smem;
     K* const buf1 = (K*)(smem + rs2_buf_bytes<K>());
@@ -535,9 +542,18 @@ __global__ void __launch_bounds__(RS2_THREADS, (sizeof(K) == 8 ? 2 : 3)) radix_s
     const uint32_t seg = blockIdx.x / cps, c = blockIdx.x - seg * cps;
     const uint64_t lo = (uint64_t)c * L;
     const uint64_t hi = min(n, lo + L);
-    const uint64_t seg_base = (uint64_t)seg * n;
-    const K* src = in + seg_base;
+    // batched trie passes (DESC): each segment reads its own input array, sorts by
+    // its own digit (up to 4 symbols) and writes its own (masked) output
+    PassDesc pd{};
+    if constexpr (DESC) pd = pdesc[seg];
+    const uint64_t seg_base = DESC ? pd.out_off : (uint64_t)seg * n;
+    const K* src = in + (DESC ? pd.in_off : seg_base);
     const P* psrc = HASP ? pin + seg_base : nullptr;
+    const K omask = DESC ? (K)pd.omask : (HASP ? omask_ : ~(K)0);
+    auto digit = [&](K k) -> uint32_t {
+        if constexpr (DESC) return pd_digit(k, pd);
+        else return (uint32_t)(k >> shift) & dmask;
+    };
     const uint32_t ntile = hi > lo ? (uint32_t)((hi - lo + RS2_TILE - 1) / RS2_TILE) : 0u;
 
     for (int i = tid; i < 2 * RS2_WARPS * RADIX; i += RS2_THREADS) (&s_whist[0][0])[i] = 0u;
@@ -597,9 +613,9 @@ __global__ void __launch_bounds__(RS2_THREADS, (sizeof(K) == 8 ? 2 : 3)) radix_s
             keys[i] = (cnt == RS2_TILE || idx < cnt) ? kin[idx] : (K)0;
         }
         if (cnt == RS2_TILE)
-            rs2_rank<K, RANK, true>(keys, rank, shift, dmask, cnt, whist, mbin, w, lane);
+            rs2_rank<K, RANK, true>(keys, rank, digit, cnt, whist, mbin, w, lane);
         else
-            rs2_rank<K, RANK, false>(keys, rank, shift, dmask, cnt, whist, mbin, w, lane);
+            rs2_rank<K, RANK, false>(keys, rank, digit, cnt, whist, mbin, w, lane);
         __syncthreads();  // (A) every warp's counters final; every key of buf read
         uint32_t tcnt = 0;
 #pragma unroll
@@ -623,7 +639,7 @@ __global__ void __launch_bounds__(RS2_THREADS, (sizeof(K) == 8 ? 2 : 3)) radix_s
         for (int i = 0; i < RS2_ITEMS; ++i) {
             const uint32_t idx = (uint32_t)(w * RS2_ITEMS * 32 + i * 32 + lane);
             if (cnt == RS2_TILE || idx < cnt) {
-                const uint32_t d = (uint32_t)(keys[i] >> shift) & dmask;
+                const uint32_t d = digit(keys[i]);
                 const uint32_t pos = whist[d] + rank[i];
                 buf[pos] = keys[i];
                 if constexpr (HASP) s_pout[pos] = pk[idx];
@@ -636,7 +652,7 @@ __global__ void __launch_bounds__(RS2_THREADS, (sizeof(K) == 8 ? 2 : 3)) radix_s
         __syncthreads();  // (C) tile reordered in buf
         for (uint32_t j = tid; j < cnt; j += RS2_THREADS) {
             const K k = buf[j];
-            const uint32_t d = (uint32_t)(k >> shift) & dmask;
+            const uint32_t d = digit(k);
             const uint64_t dst = seg_base + (uint64_t)(s_goff[d] + (int64_t)j);
             out[dst] = k & omask;  // (the trie's leaf pass applies the mask's key bits)
             if constexpr (HASP) pout[dst] = s_pout[j];
@@ -734,6 +750,63 @@ cudaError_t launch_trie_pass(const uint64_t* win, uint64_t* wout, const void* si
     return radix_chunked2<uint64_t, uint32_t, 0>(win, wout, (const uint32_t*)sin, (uint32_t*)sout,
                                                  n, 1, shift, dmask, hist, target_ctas, s, omask,
                                                  nlaunch);
+}
+
+// One depth of the batched mask trie: nseg segments, segment s = a stable pass of
+// n keys at in + desc[s].in_off by its digit (desc[s]: up to 4 symbols), written
+// to out + desc[s].out_off (masked by desc[s].omask).
+template <typename K>
+static cudaError_t trie_batch(const K* in, K* out, uint64_t n, int nseg, const PassDesc* desc,
+                              uint32_t* hist, int target_ctas, cudaStream_t s, int* nlaunch) {
+    uint64_t tiles = (n + RS2_TILE - 1) / RS2_TILE;
+    uint64_t cps = std::max<uint64_t>(1, std::min<uint64_t>(tiles, (target_ctas + nseg - 1) / nseg));
+    uint64_t L = (tiles + cps - 1) / cps * RS2_TILE;
+    cps = (n + L - 1) / L;
+    const unsigned grid = (unsigned)(cps * nseg);
+    radix_hist_kernel<K, true><<<grid, RS_THREADS, 0, s>>>(in, n, (uint32_t)cps, L, 0, hist, 0u,
+                                                            desc);
+    const int prescan = cps > 128 ? 1 : 0;
+    if (prescan)
+        hist_scan_kernel<<<(unsigned)(nseg * RADIX / 8), 256, 0, s>>>(hist, (uint32_t)cps,
+                                                                      (uint32_t)nseg);
+    if (nlaunch) *nlaunch = 2 + prescan;
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    cudaFuncSetAttribute(radix_scatter2_kernel<K, NoPay, 0, true>,
+                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rs2_smem<K>());
+    radix_scatter2_kernel<K, NoPay, 0, true><<<grid, RS2_THREADS, rs2_smem<K>(), s>>>(
+        in, out, nullptr, nullptr, n, (uint32_t)cps, L, 0, 0xffu, hist, ~(K)0, prescan, desc);
+    return cudaGetLastError();
+}
+
+cudaError_t launch_trie_batch(const void* in, void* out, bool k64, uint64_t n, int nseg,
+                              const PassDesc* desc, uint32_t* hist, int target_ctas,
+                              cudaStream_t s, int* nlaunch) {
+    if (n == 0 || nseg == 0) return cudaGetLastError();
+    if (k64)
+        return trie_batch<uint64_t>((const uint64_t*)in, (uint64_t*)out, n, nseg, desc, hist,
+                                    target_ctas, s, nlaunch);
+    return trie_batch<uint32_t>((const uint32_t*)in, (uint32_t*)out, n, nseg, desc, hist,
+                                target_ctas, s, nlaunch);
+}
+
+// trie root: composites (packed window << sb | sequence id) of every g-mer
+template <typename K>
+__global__ void trie_root_kernel(const uint64_t* __restrict__ win, const uint32_t* __restrict__ seq,
+                                 uint64_t n, int sb, K* __restrict__ out) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        out[i] = (K)((win ? win[i] << sb : 0ull) | seq[i]);  // (no window: key 0)
+}
+cudaError_t launch_trie_root(const uint64_t* win, const uint32_t* seq, uint64_t n, int sb,
+                             bool k64, void* out, int sm_count, cudaStream_t s) {
+    if (n == 0) return cudaGetLastError();
+    const uint64_t blocks = std::min<uint64_t>((n + 255) / 256, (uint64_t)sm_count * 8);
+    if (k64)
+        trie_root_kernel<uint64_t><<<(unsigned)blocks, 256, 0, s>>>(win, seq, n, sb, (uint64_t*)out);
+    else
+        trie_root_kernel<uint32_t><<<(unsigned)blocks, 256, 0, s>>>(win, seq, n, sb, (uint32_t*)out);
+    return cudaGetLastError();
 }
 
 __global__ void seq16_kernel(const uint32_t* __restrict__ a, uint16_t* __restrict__ b,

@@ -235,6 +235,7 @@ def test_batch_size_invariance(gk, oracle_lib):
         assert_parity(run(gk, cp, 7, 5, 2, batch_keys=bk, sort=4), ref)
         assert_parity(run(gk, cp, 7, 5, 2, batch_keys=bk, sort=6), ref)
         assert_parity(run(gk, cp, 7, 5, 2, batch_keys=bk, sort=6, heavy_min_seqs=2), ref)
+        assert_parity(run(gk, cp, 7, 5, 2, batch_keys=bk, sort=7), ref)
         assert_parity(run(gk, cp, 7, 5, 2, batch_keys=bk, pipeline=0), ref)
         assert_parity(run(gk, cp, 7, 5, 2, batch_keys=bk, level_order=0), ref)
         assert_parity(run(gk, cp, 7, 5, 2, batch_keys=bk, heavy_min_seqs=2), ref)
@@ -249,22 +250,22 @@ def test_sort_modes_ragged(gk, oracle_lib):
     cp = sc.from_sequences(20, seqs)
     ref = oracle_lib.compute(cp, 8, 4, 4)
     for bk in (0, 50001, 4097 * 3):
-        for mode in (0, 1, 3, 4, 5, 6):
+        for mode in (0, 1, 3, 4, 5, 6, 7):
             assert_parity(run(gk, cp, 8, 4, 4, batch_keys=bk, sort=mode), ref)
     cp4 = sc.from_sequences(4, [rng.integers(0, 4, size=int(rng.integers(0, 5000)))
                                 for _ in range(23)])
     ref4 = oracle_lib.compute(cp4, 6, 3, 3)
     for bk in (0, 12289):
-        for mode in (0, 3, 4, 5):
+        for mode in (0, 3, 4, 5, 7):
             r = run(gk, cp4, 6, 3, 3, batch_keys=bk, sort=mode)
             assert r["stats"]["keys32"] > 0
             assert_parity(r, ref4)
 
 
 def test_grouping_modes(gk, oracle_lib):
-    """Hash-partition grouping (bucket.cu, GAKCO_OPT_SORT 2) == chunked LSD sort
-    (0, the default) == onesweep LSD sort (1) == oracle; the stats report which
-    path ran."""
+    """Every grouping path == oracle: chunked LSD sort (0; v2: 3-5), onesweep (1),
+    hash partition (2), mask trie (6), batched mask trie (7, the default for masks
+    below 2M g-mers); the stats report which path ran."""
     rng = np.random.default_rng(108)
     for it in range(10):
         sigma = int(rng.choice([2, 4, 20, 36]))
@@ -273,12 +274,16 @@ def test_grouping_modes(gk, oracle_lib):
         M = int(rng.integers(0, g + 1))
         cp = sc.random_small(rng, sigma, n_max=200, l_max=300)
         ref = oracle_lib.compute(cp, g, k, M)
-        for mode in (0, 1, 2, 3, 4, 5, 6):
+        for mode in (0, 1, 2, 3, 4, 5, 6, 7):
             r = run(gk, cp, g, k, M, sort=mode)
             assert_parity(r, ref)
             if r["stats"]["keys"] > 0:
-                assert r["stats"]["grouping"] == (mode if mode < 3 else (3 if mode == 6 else 0))
-        assert run(gk, cp, g, k, M)["stats"]["grouping"] == 0
+                assert r["stats"]["grouping"] == {6: 3, 7: 4}.get(mode, mode if mode < 3 else 0)
+        r = run(gk, cp, g, k, M)
+        if r["stats"]["keys"] > 0:  # auto: the batched trie where one word holds the composite
+            bits = max(1, int(np.ceil(np.log2(max(sigma, 2)))))
+            sb = int(np.ceil(np.log2(cp.n_seq))) if cp.n_seq > 1 else 0
+            assert r["stats"]["grouping"] == (4 if g * bits + sb <= 64 else 0)
 
 
 def test_hash_big_buckets(gk, oracle_lib):
