@@ -239,7 +239,28 @@ def stage_model(stats, cfg, N):
     trip, grp = stats["triples"], stats["groups_multi"]
     M = cfg.M
     epi = N * N * ((M + 1) * 4 + (M + 1) * 4 + (M + 1) * 8 + 16) + N * (M + 1) * 8
-    if stats.get("grouping", 0) == 2:
+    grouping = stats.get("grouping", 0)
+    n_gm = keys / max(1, stats["masks"])  # g-mers per mask
+    if grouping == 3:
+        # mask trie (SoA): u64 window + u16 (N <= 65536) or u32 sequence id per element,
+        # read + written per pass; no per-mask encode (the windows are packed once)
+        esz = 8.0 + (2.0 if N <= 65536 else 4.0)
+        return {
+            "encode": ("hbm", 8.0 * n_gm + 4.0 * n_gm),
+            "sort": ("hbm", 2.0 * esz * passes),
+            "segment": ("hbm", esz * keys + 8.0 * trip + 8.0 * grp),
+            "light": ("hbm", 8.0 * stats["light_pairs"]),
+            "heavy": ("tensor", 2.0 * (stats["heavy_macs"] + stats.get("win_macs", 0))),
+            "dense": ("hbm", float(stats["heavy_groups"]) * float(stats.get("n_pad", 0))
+                      + 256.0 * float(stats.get("win_groups", 0))),
+            "epilogue": ("hbm", float(epi)),
+        }
+    if grouping == 4:
+        # batched mask trie: one-word composites built once (root), read + written per
+        # pass (sort_passes32 counts the 4-byte ones)
+        enc = ("hbm", 12.0 * n_gm + (4.0 if k32 else 8.0) * n_gm)
+        srt = ("hbm", 16.0 * (passes - p32) + 8.0 * p32)
+    elif grouping == 2:
         # hash partition (bucket.cu): the count pass recomputes keys from the packed
         # windows (ALU work, windows re-read once per CTA mask group: L2);
         # the scatter pass writes every composite once; group reads it once
@@ -248,14 +269,17 @@ def stage_model(stats, cfg, N):
     else:
         enc = ("hbm", kbytes + 4.0 * keys)     # write the key + read the 4 B seq id
         srt = ("hbm", 16.0 * (passes - p32) + 8.0 * p32)  # read + write per key per pass
+    e2m1 = float(stats.get("gram_fp4", 0) or 0) > 0
     return {
         "encode": enc,
         "sort": srt,
         "segment": ("hbm", kbytes + 8.0 * trip + 8.0 * grp),  # read keys; write triples, groups
         "light": ("hbm", 8.0 * stats["light_pairs"]),  # u32 read-modify-write per update
-        "heavy": ("tensor", 2.0 * stats["heavy_macs"]),
-        # one n_pad-byte u8 column per heavy group, written once
-        "dense": ("hbm", float(stats["heavy_groups"]) * float(stats.get("n_pad", 0))),
+        "heavy": ("tensor", 2.0 * (stats["heavy_macs"] + stats.get("win_macs", 0))),
+        # one n_pad-byte u8 (n_pad/2 e2m1) column per heavy group, written once
+        "dense": ("hbm", float(stats["heavy_groups"]) * float(stats.get("n_pad", 0))
+                  * (0.5 if e2m1 and stats.get("heavy_macs_fp4", 0) == stats["heavy_macs"] else 1.0)
+                  + 256.0 * float(stats.get("win_groups", 0))),
         "epilogue": ("hbm", float(epi)),
     }
 

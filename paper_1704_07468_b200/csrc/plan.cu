@@ -1356,6 +1356,7 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
                                          s, &nl));
                     p->launches += nl - 1;
                     passkeys += (int64_t)at[d].size() * (int64_t)n;
+                    if (!tb64) passkeys32 += (int64_t)at[d].size() * (int64_t)n;
                 }
                 // (desc: pageable staging, copied out before cudaMemcpyAsync returns; the
                 // next batch's upload is stream-ordered after these launches)

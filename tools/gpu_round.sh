@@ -16,7 +16,7 @@ timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > $O/${TAG}_be
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 2000 --csv \
   --log-file $O/${TAG}_launches.csv python bench.py --steps 1 --warmup 0 --no-e2e --no-cpu-baseline > $O/${TAG}_ncu_launch.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on \
-  -k 'regex:gram4_kernel|gram2_kernel|light_kernel|radix_scatter2|radix_hist|segment_kernel|encode_win|build_dense3|epilogue_kernel' \
-  -s ${SKIP:-0} -c 18 \
+  -k 'regex:gram4_kernel|gram2_kernel|light_kernel|radix_scatter2|radix_hist|segment_kernel|build_dense3|epilogue_kernel|trie_root' \
+  -s ${SKIP:-40} -c 16 \
   -o $O/${TAG}_prof -f python bench.py --steps 1 --warmup 0 --no-e2e --no-cpu-baseline --no-timing > $O/${TAG}_ncu_full.log 2>&1
 echo done > $O/${TAG}_done

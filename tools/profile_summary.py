@@ -32,7 +32,9 @@ STAGE = {"encode_kernel": "encode", "encode_win_kernel": "encode", "window_kerne
          "bk_bscan_kernel": "sort", "bk_group_kernel": "segment",
          "radix_scatter2_kernel": "sort", "hist_scan_kernel": "sort", "seq16_kernel": "sort",
          "symbol_hist_kernel": "encode", "thresh_union_kernel": "light",
-         "light_flush_rect_kernel": "light", "fill_reset4_kernel": "heavy"}
+         "light_flush_rect_kernel": "light", "fill_reset4_kernel": "heavy",
+         "trie_root_kernel": "encode", "window_build_kernel": "dense", "window_round_kernel": "dense",
+         "window_reset_kernel": "heavy", "window_flush_kernel": "light"}
 
 
 def short(name):
