@@ -262,7 +262,8 @@ cudaError_t launch_radix_chunked(const void* in, void* out, bool k64, uint64_t n
 // diag[X * dstride] receives the within-sequence repeat term of C_m(X,X)
 cudaError_t launch_segment_soa(const uint64_t* w, const void* sq, bool seq16, uint64_t n,
                                int nseg, int64_t dstride, int64_t* diag, uint32_t* counters,
-                               SegmentOut so, unsigned long long* stats, cudaStream_t s);
+                               SegmentOut so, unsigned long long* stats, cudaStream_t s,
+                               const uint64_t* km = nullptr);
 cudaError_t launch_segment(const void* keys, bool k64, uint64_t n, int nseg, int sb,
                            int64_t dstride, int64_t* diag, uint32_t* counters, SegmentOut so,
                            unsigned long long* stats, cudaStream_t s);

@@ -106,7 +106,7 @@ struct gakco_plan {
     std::vector<std::array<uint8_t, GMAX>> mask_kept;
     std::vector<int> key_bits;  // per level
 
-    DevBuf trieR, trieX0, trieX1, pdesc, wD, wlist, wfill, wC, winv, wtiles, trieS0, trieW, trieS, keptsh, dense2, heavy2, hcount2, tseq2, tcnt2, gstart2, counts2, perm, iota, best, parent, Dgscr, Kdscr, codes, off, gofs, gmseq, keysA, keysB, hist, status, ctr, tseq, tcnt, gstart, gend,
+    DevBuf genW0, genW1, genS0, genS1, kmdev, trieR, trieX0, trieX1, pdesc, wD, wlist, wfill, wC, winv, wtiles, trieS0, trieW, trieS, keptsh, dense2, heavy2, hcount2, tseq2, tcnt2, gstart2, counts2, perm, iota, best, parent, Dgscr, Kdscr, codes, off, gofs, gmseq, keysA, keysB, hist, status, ctr, tseq, tcnt, gstart, gend,
         counts, kept, stats, flags, kdiag, Cscr, Nmscr, Kscr, Knscr, heavy, hcount, dense, tiles, tiles4, symhist,
         lightacc, binrec, bincnt, win, bkH, bktot, bkbase, bkdesc, bktab, bktcnt, bkgs, bkocc;
     int64_t tiles_npad = -1;
@@ -449,7 +449,7 @@ extern "C" void gakco_destroy(gakco_plan* p) {
                       &p->hist,  &p->status, &p->ctr,  &p->tseq,   &p->tcnt,  &p->gstart,
                       &p->gend,  &p->counts, &p->kept, &p->stats,  &p->flags, &p->kdiag,
                       &p->Cscr,  &p->Nmscr, &p->Kscr,  &p->Knscr, &p->heavy, &p->hcount,
-                      &p->dense, &p->tiles, &p->tiles4, &p->symhist, &p->trieS0, &p->trieW, &p->trieS, &p->trieR, &p->trieX0, &p->trieX1, &p->pdesc, &p->wD, &p->wlist, &p->wfill, &p->wC, &p->winv, &p->wtiles, &p->lightacc, &p->binrec, &p->bincnt,
+                      &p->dense, &p->tiles, &p->tiles4, &p->symhist, &p->trieS0, &p->trieW, &p->trieS, &p->genW0, &p->genW1, &p->genS0, &p->genS1, &p->kmdev, &p->trieR, &p->trieX0, &p->trieX1, &p->pdesc, &p->wD, &p->wlist, &p->wfill, &p->wC, &p->winv, &p->wtiles, &p->lightacc, &p->binrec, &p->bincnt,
                       &p->win,   &p->bkH,   &p->bktot, &p->bkbase, &p->bkdesc, &p->bktab,
                       &p->bktcnt, &p->bkgs, &p->bkocc};
     for (DevBuf* b : bufs)
@@ -697,9 +697,34 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
     const bool tb64 = g * bits + sb > 32;
     if (trie_b) p->last_grouping = 4;
     std::vector<std::array<uint8_t, GMAX>> trie_chain;  // per position in mine
+    // cross-level reuse (mask trie): with levels processed as k rises (m falls), a
+    // level-m mask S is one pass (by a position x) over the unmasked sorted arrays of
+    // the level-(m+1) mask S \ {x}, kept from the previous level in a generation
+    // buffer; only the first level of the chain is a trie from the windows.
+    // (Relabelling needs level 0 first: then 0, M, M-1, ..., 1.)
+    std::vector<int> xl_parent, xl_x, xl_slot, xl_run;  // per position in mine
+    bool xl = false;
+    size_t xl_maxrun = 0;
+    if (trie && n >= (uint64_t)SEG_ITEMS) {
+        std::vector<int> order;
+        for (int v : mine) order.push_back(v);
+        auto key = [&](int v) {
+            const int lm = p->mask_level[v];
+            return relabel_pre ? (lm == 0 ? -1000 : -lm) : -lm;
+        };
+        std::stable_sort(order.begin(), order.end(), [&](int a, int b) { return key(a) < key(b); });
+        mine = order;
+        xl = true;
+    }
     if (trie) {
         size_t a0 = 0;
         trie_chain.resize(mine.size());
+        xl_parent.assign(mine.size(), -1);
+        xl_x.assign(mine.size(), -1);
+        xl_slot.assign(mine.size(), 0);
+        xl_run.assign(mine.size(), 0);
+        int run = 0, prev_level = -1;
+        std::vector<uint32_t> prev_sets;  // previous run's masks (sets), by slot
         while (a0 < mine.size()) {
             size_t a1 = a0;
             while (a1 < mine.size() && p->mask_level[mine[a1]] == p->mask_level[mine[a0]]) ++a1;
@@ -709,14 +734,57 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
                 for (int r = 0; r < g - p->mask_level[mine[i]]; ++r) b |= 1u << p->mask_kept[mine[i]][r];
                 sets.push_back(b);
             }
-            std::vector<int> ord;
-            std::vector<std::array<uint8_t, GMAX>> ch;
-            build_mask_trie(sets, g - p->mask_level[mine[a0]], ord, ch);
+            const int lm = p->mask_level[mine[a0]];
             std::vector<int> lv(mine.begin() + a0, mine.begin() + a1);
-            for (size_t i = 0; i < ord.size(); ++i) {
-                mine[a0 + i] = lv[ord[i]];
-                trie_chain[a0 + i] = ch[ord[i]];
+            // parents in the previous run (level m + 1, one position fewer)?
+            std::vector<int> par(sets.size(), -1), px(sets.size(), -1);
+            bool all = xl && prev_level == lm + 1;
+            if (all) {
+                std::vector<std::pair<uint32_t, int>> ps;
+                for (size_t q = 0; q < prev_sets.size(); ++q) ps.push_back({prev_sets[q], (int)q});
+                std::sort(ps.begin(), ps.end());
+                for (size_t i = 0; i < sets.size() && all; ++i) {
+                    for (int x = 0; x < 32 && par[i] < 0; ++x) {
+                        if (!((sets[i] >> x) & 1u)) continue;
+                        const uint32_t pset = sets[i] & ~(1u << x);
+                        auto it = std::lower_bound(ps.begin(), ps.end(), std::make_pair(pset, -1));
+                        if (it != ps.end() && it->first == pset) {
+                            par[i] = it->second;
+                            px[i] = x;
+                        }
+                    }
+                    if (par[i] < 0) all = false;
+                }
             }
+            std::vector<uint32_t> cur_sets(sets.size());
+            if (all) {  // one pass per mask, in parent order (locality)
+                std::vector<int> ord(sets.size());
+                for (size_t i = 0; i < ord.size(); ++i) ord[i] = (int)i;
+                std::stable_sort(ord.begin(), ord.end(), [&](int a, int b) { return par[a] < par[b]; });
+                for (size_t i = 0; i < ord.size(); ++i) {
+                    mine[a0 + i] = lv[ord[i]];
+                    xl_parent[a0 + i] = par[ord[i]];
+                    xl_x[a0 + i] = px[ord[i]];
+                    cur_sets[i] = sets[ord[i]];
+                }
+            } else {
+                std::vector<int> ord;
+                std::vector<std::array<uint8_t, GMAX>> ch;
+                build_mask_trie(sets, g - lm, ord, ch);
+                for (size_t i = 0; i < ord.size(); ++i) {
+                    mine[a0 + i] = lv[ord[i]];
+                    trie_chain[a0 + i] = ch[ord[i]];
+                    cur_sets[i] = sets[ord[i]];
+                }
+            }
+            for (size_t i = a0; i < a1; ++i) {
+                xl_slot[i] = (int)(i - a0);
+                xl_run[i] = run;
+            }
+            xl_maxrun = std::max(xl_maxrun, a1 - a0);
+            prev_sets = cur_sets;
+            prev_level = lm;
+            ++run;
             a0 = a1;
         }
         p->last_grouping = 3;
@@ -952,6 +1020,25 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
             CK(cudaMemcpyAsync(p->trieS0.p, p->gmseq.p, n * 4, cudaMemcpyDeviceToDevice, s));
         CK(p->ensure(p->trieW, (size_t)g * n * 8 + 64, s));
         CK(p->ensure(p->trieS, (size_t)g * n * ssz + 64, s));
+        if (xl) {  // generation buffers: a level's unmasked sorted arrays, two levels
+            const size_t need = 2 * xl_maxrun * n * (8 + ssz) + 256;
+            size_t fr = 0, tot = 0;
+            cudaMemGetInfo(&fr, &tot);
+            const bool have = p->genW0.cap >= xl_maxrun * n * 8 + 64 &&
+                              p->genW1.cap >= xl_maxrun * n * 8 + 64 &&
+                              p->genS0.cap >= xl_maxrun * n * ssz + 64 &&
+                              p->genS1.cap >= xl_maxrun * n * ssz + 64;
+            if (have || fr > need + (4ull << 30)) {
+                CK(p->ensure(p->genW0, xl_maxrun * n * 8 + 64, s));
+                CK(p->ensure(p->genW1, xl_maxrun * n * 8 + 64, s));
+                CK(p->ensure(p->genS0, xl_maxrun * n * ssz + 64, s));
+                CK(p->ensure(p->genS1, xl_maxrun * n * ssz + 64, s));
+                CK(p->ensure(p->kmdev, (bmax_masks + 2) * 8, s));
+            } else {
+                xl = false;  // (not enough memory: per-level tries, leaves masked)
+                for (auto& v : xl_parent) v = -1;
+            }
+        }
     }
     if (use_win) {
         CK(p->ensure(p->win, n * 8, s));
@@ -1377,18 +1464,44 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
             // windows to the mask's segment of the batch
             const int kk = g - m;
             const uint32_t dmask = (1u << bits) - 1u;
+            // (cross-level: this run's generation buffer; else the batch buffers)
+            const int gen = xl ? (xl_run[pos] & 1) : 0;
+            uint64_t* genW = (uint64_t*)(gen ? p->genW1.p : p->genW0.p);
+            uint8_t* genS = (uint8_t*)(gen ? p->genS1.p : p->genS0.p);
+            const uint64_t* pgenW = (const uint64_t*)(gen ? p->genW0.p : p->genW1.p);
+            const uint8_t* pgenS = (const uint8_t*)(gen ? p->genS0.p : p->genS1.p);
+            std::vector<uint64_t> kms;
             p->stage_begin(s, &a);
             for (size_t j = pos; j < end; ++j) {
                 const uint8_t* kept = trie_chain[j].data();  // positions in pass order
-                uint64_t* wleaf = (uint64_t*)p->keysA.p + (j - pos) * n;
-                uint8_t* sleaf = (uint8_t*)p->keysB.p + (j - pos) * n * ssz;
-                if (kk == 0) {  // no kept position: one key, identity order
-                    CK(cudaMemsetAsync(wleaf, 0, n * 8, s));
+                uint64_t* wleaf = xl ? genW + (size_t)xl_slot[j] * n
+                                     : (uint64_t*)p->keysA.p + (j - pos) * n;
+                uint8_t* sleaf = xl ? genS + (size_t)xl_slot[j] * n * ssz
+                                    : (uint8_t*)p->keysB.p + (j - pos) * n * ssz;
+                uint64_t kmask = 0;
+                for (int r = 0; r < kk; ++r)
+                    kmask |= (uint64_t)dmask << (bits * (g - 1 - p->mask_kept[mine[j]][r]));
+                kms.push_back(kmask);
+                if (kk == 0) {  // no kept position: one key, identity order (cross-level:
+                    // the unmasked windows, the next level's parent; the segment masks)
+                    if (xl)
+                        CK(cudaMemcpyAsync(wleaf, p->win.p, n * 8, cudaMemcpyDeviceToDevice, s));
+                    else
+                        CK(cudaMemsetAsync(wleaf, 0, n * 8, s));
                     CK(cudaMemcpyAsync(sleaf, p->trieS0.p, n * ssz, cudaMemcpyDeviceToDevice, s));
                     continue;
                 }
-                uint64_t kmask = 0;
-                for (int r = 0; r < kk; ++r) kmask |= (uint64_t)dmask << (bits * (g - 1 - kept[r]));
+                if (xl && xl_parent[j] >= 0) {  // one pass over the parent mask's arrays
+                    int nl = 2;
+                    LK(launch_trie_pass(pgenW + (size_t)xl_parent[j] * n, wleaf,
+                                        pgenS + (size_t)xl_parent[j] * n * ssz, sleaf, seq16, n,
+                                        bits * (g - 1 - xl_x[j]), dmask, ~0ull,
+                                        (uint32_t*)p->hist.p, p->trie_ctas_per_sm * p->sm_count, s,
+                                        &nl));
+                    p->launches += nl - 1;
+                    passkeys += (int64_t)n;
+                    continue;
+                }
                 int d = 0;
                 while (d < stack_depth && d < kk - 1 && stack_pos[d] == kept[d]) ++d;
                 for (int t = d; t < kk; ++t) {
@@ -1401,7 +1514,7 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
                     void* so_ = leaf ? (void*)sleaf : (void*)((uint8_t*)p->trieS.p + (size_t)t * n * ssz);
                     int nl = 2;
                     LK(launch_trie_pass(wi, wo, si, so_, seq16, n, bits * (g - 1 - kept[t]), dmask,
-                                        leaf ? kmask : ~0ull, (uint32_t*)p->hist.p,
+                                        leaf && !xl ? kmask : ~0ull, (uint32_t*)p->hist.p,
                                         p->trie_ctas_per_sm * p->sm_count, s, &nl));
                     p->launches += nl - 1;  // hist (+ chunk scan) + scatter
                     if (!leaf) stack_pos[t] = kept[t];
@@ -1415,8 +1528,16 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
                 if (ws != GAKCO_OK) return ws;
             }
             p->stage_begin(s, &a);
-            LK(launch_segment_soa((const uint64_t*)p->keysA.p, p->keysB.p, seq16, n, nmask, dstride,
-                                  Dm, so.counts, so, stats, s));
+            if (xl) {  // the run's arrays are unmasked: the segment applies each mask's bits
+                kms.push_back(0);
+                CK(cudaMemcpyAsync(p->kmdev.p, kms.data(), kms.size() * 8, cudaMemcpyHostToDevice, s));
+                LK(launch_segment_soa(genW + (size_t)xl_slot[pos] * n, genS + (size_t)xl_slot[pos] * n * ssz,
+                                      seq16, n, nmask, dstride, Dm, so.counts, so, stats, s,
+                                      (const uint64_t*)p->kmdev.p));
+            } else {
+                LK(launch_segment_soa((const uint64_t*)p->keysA.p, p->keysB.p, seq16, n, nmask,
+                                      dstride, Dm, so.counts, so, stats, s));
+            }
             p->stage_end(s, S_SEGMENT, a);
         } else if (n > 0) {
             p->stage_begin(s, &a);

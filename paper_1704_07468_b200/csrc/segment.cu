@@ -32,7 +32,10 @@ struct SegComp {
     const K* keys;
     int sb;
     __device__ E ld(uint64_t i) const { return keys[i]; }
-    __device__ void ld8(uint64_t base, E (&c)[SEG_ITEMS]) const {
+    __device__ uint64_t kof(uint64_t) const { return 0; }
+    __device__ uint64_t kseg(uint64_t) const { return 0; }
+    __device__ E ldk(uint64_t i, uint64_t) const { return keys[i]; }
+    __device__ void ld8(uint64_t base, E (&c)[SEG_ITEMS], uint64_t) const {
         constexpr int NV = SEG_ITEMS * sizeof(K) / 16;
         const uint4* v = (const uint4*)(keys + base);
 #pragma unroll
@@ -57,26 +60,50 @@ struct SoaElem {
 template <typename S>
 struct SegSoa {
     using E = SoaElem;
-    const uint64_t* w;  // masked packed windows (the leaf pass applied the mask)
-    const S* sq;        // sequence ids
-    __device__ E ld(uint64_t i) const { return E{w[i], (uint32_t)sq[i]}; }
-    __device__ void ld8(uint64_t base, E (&c)[SEG_ITEMS]) const {
-        const uint4* v = (const uint4*)(w + base);
+    const uint64_t* w;   // packed windows (masked by the leaf pass, or by km below)
+    const S* sq;         // sequence ids
+    const uint64_t* km;  // per segment: the mask's key bits (nullptr: windows masked)
+    uint64_t n;          // keys per segment
+    __device__ E ld(uint64_t i) const {
+        return E{km ? w[i] & km[i / n] : w[i], (uint32_t)sq[i]};
+    }
+    // the key mask of key i's segment, and a load with a known mask (no division)
+    __device__ uint64_t kof(uint64_t i) const { return km ? km[i / n] : ~0ull; }
+    __device__ uint64_t kseg(uint64_t sgi) const { return km ? km[sgi] : ~0ull; }
+    __device__ E ldk(uint64_t i, uint64_t k) const { return E{w[i] & k, (uint32_t)sq[i]}; }
+    __device__ void ld8(uint64_t base, E (&c)[SEG_ITEMS], uint64_t sgi) const {
+        // (16-byte vector loads; scalar when a segment array starts off 16 bytes: the
+        // cross-level trie's generation slots are n keys apart)
+        if ((((uintptr_t)(w + base)) | ((uintptr_t)(sq + base))) & 15) {
 #pragma unroll
-        for (int i = 0; i < SEG_ITEMS / 2; ++i) {
-            const uint4 q = v[i];
-            c[2 * i].w = (uint64_t)q.x | (uint64_t)q.y << 32;
-            c[2 * i + 1].w = (uint64_t)q.z | (uint64_t)q.w << 32;
+            for (int i = 0; i < SEG_ITEMS; ++i) {
+                c[i].w = w[base + i];
+                c[i].s = (uint32_t)sq[base + i];
+            }
+        } else {
+            const uint4* v = (const uint4*)(w + base);
+#pragma unroll
+            for (int i = 0; i < SEG_ITEMS / 2; ++i) {
+                const uint4 q = v[i];
+                c[2 * i].w = (uint64_t)q.x | (uint64_t)q.y << 32;
+                c[2 * i + 1].w = (uint64_t)q.z | (uint64_t)q.w << 32;
+            }
+            const uint4* u = (const uint4*)(sq + base);
+            constexpr int NU = SEG_ITEMS * sizeof(S) / 16;
+#pragma unroll
+            for (int i = 0; i < NU; ++i) {
+                const uint4 q = u[i];
+                const S* sv = (const S*)&q;
+#pragma unroll
+                for (int e = 0; e < 16 / (int)sizeof(S); ++e)
+                    c[i * (16 / sizeof(S)) + e].s = (uint32_t)sv[e];
+            }
         }
-        const uint4* u = (const uint4*)(sq + base);
-        constexpr int NU = SEG_ITEMS * sizeof(S) / 16;
+        if (km) {  // (the items cross at most one segment boundary: n >= SEG_ITEMS)
+            const uint64_t end0 = (sgi + 1) * n;
+            const uint64_t k0 = km[sgi], k1 = km[sgi + 1];
 #pragma unroll
-        for (int i = 0; i < NU; ++i) {
-            const uint4 q = u[i];
-            const S* sv = (const S*)&q;
-#pragma unroll
-            for (int e = 0; e < 16 / (int)sizeof(S); ++e)
-                c[i * (16 / sizeof(S)) + e].s = (uint32_t)sv[e];
+            for (int i = 0; i < SEG_ITEMS; ++i) c[i].w &= (base + i < end0) ? k0 : k1;
         }
     }
     __device__ bool teq(E a, E b) const { return a.w == b.w && a.s == b.s; }
@@ -105,9 +132,11 @@ __global__ void __launch_bounds__(SEG_THREADS, 5) segment_kernel(
     const uint32_t lbase = (uint32_t)tid * SEG_ITEMS;  // tile-local index of item 0
     const uint64_t tile_end = min(tile0 + SEG_TILE, total);
 
+    // segment (mask) of this thread's first item: one 64-bit division per thread
+    const uint64_t segi0 = base < total ? base / n : 0;
     K cur[SEG_ITEMS];
     if (base + SEG_ITEMS <= total) {
-        pol.ld8(base, cur);
+        pol.ld8(base, cur, segi0);
     } else {
 #pragma unroll
         for (int i = 0; i < SEG_ITEMS; ++i) cur[i] = base + i < total ? pol.ld(base + i) : K{};
@@ -117,13 +146,13 @@ __global__ void __launch_bounds__(SEG_THREADS, 5) segment_kernel(
     const bool has_next = tile_end < total && tile_end % n != 0;
     K ext{}, lk{};
     if (warp == SEG_THREADS / 32 - 1 && has_next) {
-        lk = pol.ld(tile_end - 1);
-        ext = tile_end + lane < total ? pol.ld(tile_end + lane) : pol.other(lk);
+        const uint64_t kt = pol.kof(tile_end - 1);  // (the next key is in the same segment)
+        lk = pol.ldk(tile_end - 1, kt);
+        ext = tile_end + lane < total ? pol.ldk(tile_end + lane, kt) : pol.other(lk);
     }
-    // segment (mask) bounds of this thread's first item: one 64-bit division per
-    // thread; consecutive items cross at most one boundary each (n >= 1)
-    uint64_t seg_lo = base < total ? base / n * n : 0, seg_hi = seg_lo + n;
-    const K prev = (base < total && base != seg_lo) ? pol.ld(base - 1) : K{};
+    // its bounds; consecutive items cross at most one boundary each (n >= 1)
+    uint64_t seg_lo = segi0 * n, seg_hi = seg_lo + n;
+    const K prev = (base < total && base != seg_lo) ? pol.ldk(base - 1, pol.kseg(segi0)) : K{};
 
     // 1. head flags: a triple head where the composite changes, a group head where
     //    the key bits change (both at every segment start)
@@ -156,7 +185,9 @@ __global__ void __launch_bounds__(SEG_THREADS, 5) segment_kernel(
             cross = pol.geq(pol.shfl(ext, 0), lk);
             for (uint64_t e = tile_end;; e += 32) {
                 const uint64_t q = e + lane;
-                const K kk = e == tile_end ? ext : (q < seg_end ? pol.ld(q) : pol.other(lk));
+                const K kk = e == tile_end ? ext
+                                           : (q < seg_end ? pol.ldk(q, pol.kof(tile_end - 1))
+                                                          : pol.other(lk));
                 const bool stop = q >= seg_end || !pol.teq(kk, lk);
                 const uint32_t sm = __ballot_sync(0xffffffffu, stop);
                 if (sm) {
@@ -237,9 +268,11 @@ __global__ void __launch_bounds__(SEG_THREADS, 5) segment_kernel(
     const bool crossing = fgh != 0xffffffffu && s_cross != 0;
     uint64_t gend = tile_end;  // one past the crossing group's last key
     K gkey{};
+    uint64_t kcross = 0;
     uint64_t seg_end_t = 0;
     if (crossing) {  // (block-uniform)
-        gkey = pol.ld(tile_end - 1);
+        kcross = pol.kof(tile_end - 1);  // (the tail stays in this segment)
+        gkey = pol.ldk(tile_end - 1, kcross);
         seg_end_t = (tile_end / n + 1) * n;
         uint32_t heads = 0;
         for (uint64_t e = tile_end;; e += SEG_TILE) {
@@ -252,12 +285,12 @@ __global__ void __launch_bounds__(SEG_THREADS, 5) segment_kernel(
 #pragma unroll
             for (int i = 0; i < SEG_ITEMS; ++i) {
                 const uint64_t q = e + lbase + i;
-                const bool in = q < seg_end_t && pol.geq(pol.ld(q), gkey);
+                const bool in = q < seg_end_t && pol.geq(pol.ldk(q, kcross), gkey);
                 if (!in) {
                     atomicMin(&s_gend, (unsigned long long)q);
                     break;
                 }
-                h += !pol.teq(pol.ld(q), pol.ld(q - 1));
+                h += !pol.teq(pol.ldk(q, kcross), pol.ldk(q - 1, kcross));
             }
             if (h) atomicAdd(&s_tail, h);
             __syncthreads();
@@ -310,8 +343,8 @@ __global__ void __launch_bounds__(SEG_THREADS, 5) segment_kernel(
 #pragma unroll
             for (int i = 0; i < SEG_ITEMS; ++i) {
                 const uint64_t q = e + lbase + i;
-                kv[i] = q < gend ? pol.ld(q) : K{};
-                if (q < gend && !pol.teq(kv[i], pol.ld(q - 1))) hb |= 1u << i;
+                kv[i] = q < gend ? pol.ldk(q, kcross) : K{};
+                if (q < gend && !pol.teq(kv[i], pol.ldk(q - 1, kcross))) hb |= 1u << i;
             }
             uint32_t chunk_heads;
             const uint32_t off = scan256_excl(__popc(hb), s_w, &chunk_heads);
@@ -321,7 +354,7 @@ __global__ void __launch_bounds__(SEG_THREADS, 5) segment_kernel(
                 if (hb & (1u << i)) {
                     const uint64_t q = e + lbase + i;
                     uint64_t r = q + 1;
-                    while (r < gend && pol.teq(pol.ld(r), kv[i])) ++r;
+                    while (r < gend && pol.teq(pol.ldk(r, kcross), kv[i])) ++r;
                     so.tseq[pos] = pol.seq(kv[i]);
                     so.tcnt[pos] = (uint32_t)(r - q);
                     ++pos;
@@ -350,21 +383,24 @@ cudaError_t launch_segment(const void* keys, bool k64, uint64_t n, int nseg, int
     return cudaGetLastError();
 }
 
-// the mask trie's leaves: masked packed windows + sequence ids (u16 or u32)
+// the mask trie's leaves: packed windows + sequence ids (u16 or u32); km = per
+// segment key bits when the windows are not masked (else nullptr; km has nseg + 1
+// entries when given)
 cudaError_t launch_segment_soa(const uint64_t* w, const void* sq, bool seq16, uint64_t n,
                                int nseg, int64_t dstride, int64_t* diag, uint32_t* counters,
-                               SegmentOut so, unsigned long long* stats, cudaStream_t s) {
+                               SegmentOut so, unsigned long long* stats, cudaStream_t s,
+                               const uint64_t* km) {
     cudaError_t e = cudaMemsetAsync(counters, 0, 2 * sizeof(uint32_t), s);
     uint64_t total = n * (uint64_t)nseg;
     if (e != cudaSuccess || total == 0) return e;
     uint64_t tiles = (total + SEG_TILE - 1) / SEG_TILE;
     if (seq16)
         segment_kernel<SegSoa<uint16_t>><<<(unsigned)tiles, SEG_THREADS, 0, s>>>(
-            SegSoa<uint16_t>{w, (const uint16_t*)sq}, n, total, dstride, diag, counters, so,
+            SegSoa<uint16_t>{w, (const uint16_t*)sq, km, n}, n, total, dstride, diag, counters, so,
             stats);
     else
         segment_kernel<SegSoa<uint32_t>><<<(unsigned)tiles, SEG_THREADS, 0, s>>>(
-            SegSoa<uint32_t>{w, (const uint32_t*)sq}, n, total, dstride, diag, counters, so,
+            SegSoa<uint32_t>{w, (const uint32_t*)sq, km, n}, n, total, dstride, diag, counters, so,
             stats);
     return cudaGetLastError();
 }
