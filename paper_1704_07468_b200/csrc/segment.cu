@@ -35,8 +35,9 @@ struct SegComp {
     __device__ uint64_t kof(uint64_t) const { return 0; }
     __device__ uint64_t kseg(uint64_t) const { return 0; }
     __device__ E ldk(uint64_t i, uint64_t) const { return keys[i]; }
-    __device__ void ld8(uint64_t base, E (&c)[SEG_ITEMS], uint64_t) const {
-        constexpr int NV = SEG_ITEMS * sizeof(K) / 16;
+    template <int IT>
+    __device__ void ldn(uint64_t base, E (&c)[IT], uint64_t) const {
+        constexpr int NV = IT * sizeof(K) / 16;
         const uint4* v = (const uint4*)(keys + base);
 #pragma unroll
         for (int i = 0; i < NV; ++i) {
@@ -71,25 +72,26 @@ struct SegSoa {
     __device__ uint64_t kof(uint64_t i) const { return km ? km[i / n] : ~0ull; }
     __device__ uint64_t kseg(uint64_t sgi) const { return km ? km[sgi] : ~0ull; }
     __device__ E ldk(uint64_t i, uint64_t k) const { return E{w[i] & k, (uint32_t)sq[i]}; }
-    __device__ void ld8(uint64_t base, E (&c)[SEG_ITEMS], uint64_t sgi) const {
+    template <int IT>
+    __device__ void ldn(uint64_t base, E (&c)[IT], uint64_t sgi) const {
         // (16-byte vector loads; scalar when a segment array starts off 16 bytes: the
         // cross-level trie's generation slots are n keys apart)
         if ((((uintptr_t)(w + base)) | ((uintptr_t)(sq + base))) & 15) {
 #pragma unroll
-            for (int i = 0; i < SEG_ITEMS; ++i) {
+            for (int i = 0; i < IT; ++i) {
                 c[i].w = w[base + i];
                 c[i].s = (uint32_t)sq[base + i];
             }
         } else {
             const uint4* v = (const uint4*)(w + base);
 #pragma unroll
-            for (int i = 0; i < SEG_ITEMS / 2; ++i) {
+            for (int i = 0; i < IT / 2; ++i) {
                 const uint4 q = v[i];
                 c[2 * i].w = (uint64_t)q.x | (uint64_t)q.y << 32;
                 c[2 * i + 1].w = (uint64_t)q.z | (uint64_t)q.w << 32;
             }
             const uint4* u = (const uint4*)(sq + base);
-            constexpr int NU = SEG_ITEMS * sizeof(S) / 16;
+            constexpr int NU = IT * sizeof(S) / 16;
 #pragma unroll
             for (int i = 0; i < NU; ++i) {
                 const uint4 q = u[i];
@@ -99,11 +101,11 @@ struct SegSoa {
                     c[i * (16 / sizeof(S)) + e].s = (uint32_t)sv[e];
             }
         }
-        if (km) {  // (the items cross at most one segment boundary: n >= SEG_ITEMS)
+        if (km) {  // (the items cross at most one segment boundary: n >= IT)
             const uint64_t end0 = (sgi + 1) * n;
             const uint64_t k0 = km[sgi], k1 = km[sgi + 1];
 #pragma unroll
-            for (int i = 0; i < SEG_ITEMS; ++i) c[i].w &= (base + i < end0) ? k0 : k1;
+            for (int i = 0; i < IT; ++i) c[i].w &= (base + i < end0) ? k0 : k1;
         }
     }
     __device__ bool teq(E a, E b) const { return a.w == b.w && a.s == b.s; }
@@ -115,31 +117,33 @@ struct SegSoa {
     }
 };
 
-template <typename Pol>
-__global__ void __launch_bounds__(SEG_THREADS, 5) segment_kernel(
+template <typename Pol, int IT>
+__global__ void __launch_bounds__(SEG_THREADS, IT == 8 ? 5 : 3) segment_kernel(
     Pol pol, uint64_t n, uint64_t total, int64_t dstride,
     int64_t* diag, uint32_t* counters, SegmentOut so, unsigned long long* stats) {
     using K = typename Pol::E;
+    constexpr int TILE = SEG_THREADS * IT;
+    constexpr uint32_t FULLM = IT == 32 ? 0xffffffffu : ((1u << IT) - 1u);
     __shared__ uint32_t s_w[16];
-    __shared__ uint32_t s_gpos[SEG_TILE];
-    __shared__ uint32_t s_tx[SEG_TILE], s_tc[SEG_TILE];  // the tile's triples, staged
+    __shared__ uint16_t s_gpos[TILE];  // tile-local first triple of each group
+    __shared__ uint32_t s_tx[TILE], s_tc[TILE];  // the tile's triples, staged
     __shared__ uint32_t s_first_gh, s_base_t, s_base_g, s_tail, s_gend_done;
     __shared__ uint32_t s_wmin[SEG_THREADS / 32], s_beyond, s_cross;
     __shared__ unsigned long long s_gend;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const uint64_t tile0 = (uint64_t)blockIdx.x * SEG_TILE;
-    const uint64_t base = tile0 + (uint64_t)tid * SEG_ITEMS;
-    const uint32_t lbase = (uint32_t)tid * SEG_ITEMS;  // tile-local index of item 0
-    const uint64_t tile_end = min(tile0 + SEG_TILE, total);
+    const uint64_t tile0 = (uint64_t)blockIdx.x * TILE;
+    const uint64_t base = tile0 + (uint64_t)tid * IT;
+    const uint32_t lbase = (uint32_t)tid * IT;  // tile-local index of item 0
+    const uint64_t tile_end = min(tile0 + TILE, total);
 
     // segment (mask) of this thread's first item: one 64-bit division per thread
     const uint64_t segi0 = base < total ? base / n : 0;
-    K cur[SEG_ITEMS];
-    if (base + SEG_ITEMS <= total) {
-        pol.ld8(base, cur, segi0);
+    K cur[IT];
+    if (base + IT <= total) {
+        pol.template ldn<IT>(base, cur, segi0);
     } else {
 #pragma unroll
-        for (int i = 0; i < SEG_ITEMS; ++i) cur[i] = base + i < total ? pol.ld(base + i) : K{};
+        for (int i = 0; i < IT; ++i) cur[i] = base + i < total ? pol.ld(base + i) : K{};
     }
     // the last warp also fetches the 32 keys after the tile (the run / group
     // crossing its end), in flight together with the tile's own loads
@@ -158,7 +162,7 @@ __global__ void __launch_bounds__(SEG_THREADS, 5) segment_kernel(
     //    the key bits change (both at every segment start)
     uint32_t th_bits = 0, gh_bits = 0;
 #pragma unroll
-    for (int i = 0; i < SEG_ITEMS; ++i) {
+    for (int i = 0; i < IT; ++i) {
         const uint64_t idx = base + i;
         if (idx >= total) break;
         if (idx >= seg_hi) {
@@ -232,9 +236,9 @@ __global__ void __launch_bounds__(SEG_THREADS, 5) segment_kernel(
     // 3. backward over the items: run length = next head - head; a group head's
     //    group is shared (>= 2 sequences) iff the next triple is not a group head
     uint32_t multi_bits = 0;
-    uint32_t cnt[SEG_ITEMS];
+    uint32_t cnt[IT];
 #pragma unroll
-    for (int i = SEG_ITEMS - 1; i >= 0; --i) {
+    for (int i = IT - 1; i >= 0; --i) {
         cnt[i] = 0;
         if (!((th_bits >> i) & 1u)) continue;
         const uint32_t li = lbase + i;
@@ -255,7 +259,7 @@ __global__ void __launch_bounds__(SEG_THREADS, 5) segment_kernel(
     const uint32_t fgh = s_first_gh;
     uint32_t emit_t = 0, emit_g = 0;
     if (fgh != 0xffffffffu) {
-        const uint32_t own = lbase >= fgh ? 0xffu : (fgh - lbase < SEG_ITEMS ? (0xffu << (fgh - lbase)) & 0xffu : 0u);
+        const uint32_t own = lbase >= fgh ? FULLM : (fgh - lbase < IT ? (FULLM << (fgh - lbase)) & FULLM : 0u);
         emit_t = th_bits & multi_bits & own;
         emit_g = emit_t & gh_bits;
     }
@@ -275,7 +279,7 @@ __global__ void __launch_bounds__(SEG_THREADS, 5) segment_kernel(
         gkey = pol.ldk(tile_end - 1, kcross);
         seg_end_t = (tile_end / n + 1) * n;
         uint32_t heads = 0;
-        for (uint64_t e = tile_end;; e += SEG_TILE) {
+        for (uint64_t e = tile_end;; e += TILE) {
             if (tid == 0) {
                 s_gend = ~0ull;
                 s_gend_done = 0;
@@ -283,7 +287,7 @@ __global__ void __launch_bounds__(SEG_THREADS, 5) segment_kernel(
             __syncthreads();
             uint32_t h = 0;
 #pragma unroll
-            for (int i = 0; i < SEG_ITEMS; ++i) {
+            for (int i = 0; i < IT; ++i) {
                 const uint64_t q = e + lbase + i;
                 const bool in = q < seg_end_t && pol.geq(pol.ldk(q, kcross), gkey);
                 if (!in) {
@@ -314,12 +318,12 @@ __global__ void __launch_bounds__(SEG_THREADS, 5) segment_kernel(
     // 5. triples staged in shared memory, then written with coalesced stores
     uint32_t li = off_t, gl = off_g;
 #pragma unroll
-    for (int i = 0; i < SEG_ITEMS; ++i) {
+    for (int i = 0; i < IT; ++i) {
         if (emit_t & (1u << i)) {
             const uint32_t x = pol.seq(cur[i]);
             s_tx[li] = x | (((gh_bits >> i) & 1u) << 31);
             s_tc[li] = cnt[i];
-            if (emit_g & (1u << i)) s_gpos[gl++] = base_t + li;
+            if (emit_g & (1u << i)) s_gpos[gl++] = (uint16_t)li;
             ++li;
         }
     }
@@ -332,16 +336,17 @@ __global__ void __launch_bounds__(SEG_THREADS, 5) segment_kernel(
     // this tile's triples, its tail included)
     const uint32_t tend = base_t + agg_t + tail;
     for (uint32_t g = tid; g < agg_g; g += SEG_THREADS)
-        so.groups[base_g + g] = make_uint2(s_gpos[g], g + 1 < agg_g ? s_gpos[g + 1] : tend);
+        so.groups[base_g + g] =
+            make_uint2(base_t + s_gpos[g], g + 1 < agg_g ? base_t + s_gpos[g + 1] : tend);
     // 6. tail triples of the crossing group, after this tile's triples, in order:
     //    chunk by chunk, a block scan of the heads places them
     if (tail) {  // (block-uniform)
         uint32_t wpos = base_t + agg_t;
-        for (uint64_t e = tile_end; e < gend; e += SEG_TILE) {
+        for (uint64_t e = tile_end; e < gend; e += TILE) {
             uint32_t hb = 0;
-            K kv[SEG_ITEMS];
+            K kv[IT];
 #pragma unroll
-            for (int i = 0; i < SEG_ITEMS; ++i) {
+            for (int i = 0; i < IT; ++i) {
                 const uint64_t q = e + lbase + i;
                 kv[i] = q < gend ? pol.ldk(q, kcross) : K{};
                 if (q < gend && !pol.teq(kv[i], pol.ldk(q - 1, kcross))) hb |= 1u << i;
@@ -350,7 +355,7 @@ __global__ void __launch_bounds__(SEG_THREADS, 5) segment_kernel(
             const uint32_t off = scan256_excl(__popc(hb), s_w, &chunk_heads);
             uint32_t pos = wpos + off;
 #pragma unroll
-            for (int i = 0; i < SEG_ITEMS; ++i) {
+            for (int i = 0; i < IT; ++i) {
                 if (hb & (1u << i)) {
                     const uint64_t q = e + lbase + i;
                     uint64_t r = q + 1;
@@ -373,11 +378,11 @@ cudaError_t launch_segment(const void* keys, bool k64, uint64_t n, int nseg, int
     if (e != cudaSuccess || total == 0) return e;
     uint64_t tiles = (total + SEG_TILE - 1) / SEG_TILE;
     if (k64)
-        segment_kernel<SegComp<uint64_t>><<<(unsigned)tiles, SEG_THREADS, 0, s>>>(
+        segment_kernel<SegComp<uint64_t>, SEG_ITEMS><<<(unsigned)tiles, SEG_THREADS, 0, s>>>(
             SegComp<uint64_t>{(const uint64_t*)keys, sb}, n, total, dstride, diag, counters, so,
             stats);
     else
-        segment_kernel<SegComp<uint32_t>><<<(unsigned)tiles, SEG_THREADS, 0, s>>>(
+        segment_kernel<SegComp<uint32_t>, SEG_ITEMS><<<(unsigned)tiles, SEG_THREADS, 0, s>>>(
             SegComp<uint32_t>{(const uint32_t*)keys, sb}, n, total, dstride, diag, counters, so,
             stats);
     return cudaGetLastError();
@@ -393,13 +398,17 @@ cudaError_t launch_segment_soa(const uint64_t* w, const void* sq, bool seq16, ui
     cudaError_t e = cudaMemsetAsync(counters, 0, 2 * sizeof(uint32_t), s);
     uint64_t total = n * (uint64_t)nseg;
     if (e != cudaSuccess || total == 0) return e;
-    uint64_t tiles = (total + SEG_TILE - 1) / SEG_TILE;
+    // (16 keys per thread -- half the per-tile scans and barriers -- measured slower:
+    // 80 registers, 3 CTAs per SM; Text segment 28.4 -> 32.5 ms)
+    constexpr int IT = SEG_ITEMS;
+    uint64_t tiles = (total + SEG_THREADS * IT - 1) / (SEG_THREADS * IT);
+    if (n < (uint64_t)IT) return cudaErrorInvalidValue;  // (items cross <= 1 segment)
     if (seq16)
-        segment_kernel<SegSoa<uint16_t>><<<(unsigned)tiles, SEG_THREADS, 0, s>>>(
+        segment_kernel<SegSoa<uint16_t>, IT><<<(unsigned)tiles, SEG_THREADS, 0, s>>>(
             SegSoa<uint16_t>{w, (const uint16_t*)sq, km, n}, n, total, dstride, diag, counters, so,
             stats);
     else
-        segment_kernel<SegSoa<uint32_t>><<<(unsigned)tiles, SEG_THREADS, 0, s>>>(
+        segment_kernel<SegSoa<uint32_t>, IT><<<(unsigned)tiles, SEG_THREADS, 0, s>>>(
             SegSoa<uint32_t>{w, (const uint32_t*)sq, km, n}, n, total, dstride, diag, counters, so,
             stats);
     return cudaGetLastError();
