@@ -329,16 +329,18 @@ def test_edge_cases(gk, oracle_lib):
 
 
 def test_shard_emulation(gk, oracle_lib):
-    """P shards accumulated into one C equal the 1-GPU result (mask sharding)."""
+    """P shards accumulated into one C equal the 1-GPU result (mask sharding), also
+    with the single-mask / batched tries (a shard's masks miss some parents)."""
     cp = sc.make("tiny")
     g, k, M = 7, 5, 2
     ref = oracle_lib.compute(cp, g, k, M)
     N = cp.n_seq
-    for world in (2, 3, 8, 40):
+    for world, sort in ((2, -1), (3, -1), (8, -1), (40, -1), (2, 6), (3, 6), (3, 7)):
         C = torch.zeros((M + 1, N, N), dtype=torch.int64, device="cuda")
         total = 0
         for rank in range(world):
             plan = gk.Plan(cp.sigma, g, k, M)
+            plan.set_option(gk.GAKCO_OPT_SORT, sort)  # (6: cross-level trie, parents in other shards)
             plan.set_shard(rank, world)
             total += plan.num_masks(shard_only=True)
             plan.accumulate(cp.codes, cp.offsets, N, C)
