@@ -1295,13 +1295,18 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
             dense_masks += nmask;
         }
         if (n > 0) {
-            if (light_m != m || light_masks + nmask > light_lim) {
+            // (a first level of many batches -- a K-only call -- is relabelled after its
+            // first batch: the clusters come from that batch's share of C_m)
+            const bool early = relabel && !perm_active && light_m == m && batch_no == 1;
+            if (light_m != m || light_masks + nmask > light_lim || early) {
                 const int done = light_m;
                 gakco_status fs = lflush();
                 if (fs != GAKCO_OK) return fs;
-                if (relabel && !perm_active && done >= 0 && done != m) {
-                    // level `done` is complete in C: its Gram flush was issued at this level
-                    // change by the heavy block above, its light flush just now
+                if (relabel && !perm_active && done >= 0 && (done != m || early)) {
+                    // C of `done` holds its level (or, early, its first batch): its Gram
+                    // flush was issued at this level change by the heavy block above
+                    // (early: pending Gram columns are labelling-independent), its light
+                    // flush just now
                     fs = make_perm(done);
                     if (fs != GAKCO_OK) return fs;
                 }

@@ -407,11 +407,16 @@ def test_k_only_fast_path(gk, oracle_lib):
         N = cp.n_seq
         K = torch.empty((N, N), dtype=torch.int64, device="cuda")
         Kn = torch.empty((N, N), dtype=torch.float64, device="cuda")
-        plan = gk.Plan(cp.sigma, g, k, g - k)
-        plan.kernel_k(cp.codes if cp.codes.size else np.zeros(1, np.uint8), cp.offsets, N, K, Kn)
-        plan.close()
-        assert np.array_equal(K.cpu().numpy(), ref["K"])
-        assert_knorm(Kn.cpu().numpy(), ref["Knorm"])
+        codes = cp.codes if cp.codes.size else np.zeros(1, np.uint8)
+        for opts in ({}, {"light_relabel": 1, "batch_keys": 3000},
+                     {"light_relabel": 1, "batch_keys": 3000, "light_window": 1, "sort": 6}):
+            plan = gk.Plan(cp.sigma, g, k, g - k)
+            for opt, val in opts.items():  # (relabelled after the level's first batch)
+                plan.set_option(getattr(gk, "GAKCO_OPT_" + opt.upper()), val)
+            plan.kernel_k(codes, cp.offsets, N, K, Kn)
+            plan.close()
+            assert np.array_equal(K.cpu().numpy(), ref["K"])
+            assert_knorm(Kn.cpu().numpy(), ref["Knorm"])
     plan = gk.Plan(4, 7, 5, 1)
     with pytest.raises(gk.GakcoError):
         plan.kernel_k(cases[0][0].codes, cases[0][0].offsets, 50, K, Kn)
