@@ -29,6 +29,7 @@ namespace gk {
 template <typename K>
 struct SegComp {
     using E = K;
+    static constexpr int kMinBlocks = sizeof(K) == 4 ? 5 : 4;  // (u64: 64 registers, no spills)
     const K* keys;
     int sb;
     __device__ E ld(uint64_t i) const { return keys[i]; }
@@ -61,6 +62,7 @@ struct SoaElem {
 template <typename S>
 struct SegSoa {
     using E = SoaElem;
+    static constexpr int kMinBlocks = 4;  // (48 registers spilled 48-56 bytes)
     const uint64_t* w;   // packed windows (masked by the leaf pass, or by km below)
     const S* sq;         // sequence ids
     const uint64_t* km;  // per segment: the mask's key bits (nullptr: windows masked)
@@ -118,7 +120,7 @@ struct SegSoa {
 };
 
 template <typename Pol, int IT>
-__global__ void __launch_bounds__(SEG_THREADS, IT == 8 ? 5 : 3) segment_kernel(
+__global__ void __launch_bounds__(SEG_THREADS, IT == 8 ? Pol::kMinBlocks : 3) segment_kernel(
     Pol pol, uint64_t n, uint64_t total, int64_t dstride,
     int64_t* diag, uint32_t* counters, SegmentOut so, unsigned long long* stats) {
     using K = typename Pol::E;
@@ -381,7 +383,7 @@ cudaError_t launch_segment(const void* keys, bool k64, uint64_t n, int nseg, int
         segment_kernel<SegComp<uint64_t>, SEG_ITEMS><<<(unsigned)tiles, SEG_THREADS, 0, s>>>(
             SegComp<uint64_t>{(const uint64_t*)keys, sb}, n, total, dstride, diag, counters, so,
             stats);
-    else
+    else  // (16 keys per thread measured slower on DNA: 0.97 -> 1.13 ms)
         segment_kernel<SegComp<uint32_t>, SEG_ITEMS><<<(unsigned)tiles, SEG_THREADS, 0, s>>>(
             SegComp<uint32_t>{(const uint32_t*)keys, sb}, n, total, dstride, diag, counters, so,
             stats);
