@@ -56,6 +56,8 @@ def args_():
                     help="light groups of <= this many sequences share a warp (1..32)")
     ap.add_argument("--light-window", type=int, default=None, choices=[-1, 0, 1],
                     help="window Gram of cluster-local light groups (-1 auto)")
+    ap.add_argument("--gram-each", type=int, default=None, choices=[0, 1],
+                    help="heavy Gram after every batch (1) or per level / full D (0)")
     ap.add_argument("--window-min", type=int, default=0,
                     help="smallest group for the window Gram (0: default)")
     ap.add_argument("--relabel", type=int, default=None, choices=[-1, 0, 1],
@@ -318,6 +320,8 @@ def run_ours(a):
         plan.set_option(gakco.GAKCO_OPT_LIGHT_RELABEL, a.relabel)
     if a.light_window is not None:
         plan.set_option(gakco.GAKCO_OPT_LIGHT_WINDOW, a.light_window)
+    if a.gram_each is not None:
+        plan.set_option(gakco.GAKCO_OPT_GRAM_EACH, a.gram_each)
     if a.window_min:
         plan.set_option(gakco.GAKCO_OPT_WINDOW_MIN, a.window_min)
     if a.fp4 is not None:

@@ -116,8 +116,11 @@ typedef enum {
                                      multiplied on the tensor cores (kind::i8) and added back
                                      through the inverse labelling. -1 = automatic (default:
                                      with relabelling), 0 = off, 1 = on (relabels) */
-    GAKCO_OPT_WINDOW_MIN = 14     /* smallest group (sequences) for the window Gram (default 9;
+    GAKCO_OPT_WINDOW_MIN = 14,    /* smallest group (sequences) for the window Gram (default 9;
                                      groups of <= GAKCO_OPT_LIGHT_FLAT sequences stay light) */
+    GAKCO_OPT_GRAM_EACH = 15      /* 1: the heavy-group Gram runs after every batch (overlapping
+                                     the next batch) instead of when a level ends or D fills;
+                                     0 (default) */
 } gakco_option;
 
 /* Counters of the last gakco_accumulate (algorithmic units). */

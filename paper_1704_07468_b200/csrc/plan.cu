@@ -88,6 +88,7 @@ struct gakco_plan {
     int gram_pair = 1;         // 1: CTA-pair Gram (gram2.cu), 0: one-SM Gram (gram_tc.cu)
     int light_flat = 8;        // light groups of <= this many sequences share warps
     int light_relabel = -1;    // -1 auto (accumulator >> L2), 0 off, 1 on
+    int gram_each = 0;         // 1: a Gram flush after every batch (overlaps the next batch)
     int light_window = -1;     // window Gram of cluster-local groups: -1 auto (with relabelling), 0 off, 1 on (relabels)
     int64_t window_min = 9;    // smallest group (sequences) for the window Gram
     int level_order_desc = 0;  // process levels m = M..0 (1) or 0..M (0, measured faster on DNA)
@@ -513,6 +514,10 @@ extern "C" gakco_status gakco_set_option(gakco_plan* p, int option, int64_t valu
         case GAKCO_OPT_WINDOW_MIN:
             if (value < 2) return p->fail(GAKCO_E_ARG, "window min must be >= 2");
             p->window_min = value;
+            return GAKCO_OK;
+        case GAKCO_OPT_GRAM_EACH:
+            if (value < 0 || value > 1) return p->fail(GAKCO_E_ARG, "gram each must be 0 or 1");
+            p->gram_each = (int)value;
             return GAKCO_OK;
         case GAKCO_OPT_GRAM_FP4:
             if (value < -1 || value > 1) return p->fail(GAKCO_E_ARG, "gram fp4 must be -1..1");
@@ -1286,7 +1291,7 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
         if (gram_ok && n > 0) {
             const uint64_t bnd = (uint64_t)nmask * n / (uint64_t)heavy_min_of(m) + slab_cols_of(m);
             if (dense_m != m || dense_bound + bnd > rcap_of(m) ||
-                dense_masks + nmask > mask_lim_of(m)) {
+                dense_masks + nmask > mask_lim_of(m) || (p->gram_each && dense_bound > 0)) {
                 gakco_status fs = flush();
                 if (fs != GAKCO_OK) return fs;
             }
