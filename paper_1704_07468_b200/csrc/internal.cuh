@@ -266,7 +266,7 @@ cudaError_t launch_segment_soa(const uint64_t* w, const void* sq, bool seq16, ui
                                const uint64_t* km = nullptr);
 cudaError_t launch_segment(const void* keys, bool k64, uint64_t n, int nseg, int sb,
                            int64_t dstride, int64_t* diag, uint32_t* counters, SegmentOut so,
-                           unsigned long long* stats, cudaStream_t s);
+                           unsigned long long* stats, cudaStream_t s, const uint64_t* km = nullptr);
 // Light pair updates; a group with >= heavy_min sequences (and counts <= 255)
 // instead claims column c = atomicAdd(dense_fill) (< ldd) of the dense count
 // matrix D (u8, slabs of 128 columns: byte (c/128)*n_pad*128 + row*128 + c%128)

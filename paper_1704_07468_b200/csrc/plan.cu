@@ -710,7 +710,11 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
     std::vector<int> xl_parent, xl_x, xl_slot, xl_run;  // per position in mine
     bool xl = false;
     size_t xl_maxrun = 0;
-    if (trie && n >= (uint64_t)SEG_ITEMS) {
+    // (the batched trie too, where a pass sorts by one symbol -- Protein: a child mask
+    // is then one pass by one symbol, as the trie's own passes; DNA's 4-symbol passes
+    // gain nothing and its ascending level order measured faster)
+    const bool xlb = trie_b && std::min(4, 8 / bits) <= 1 && n >= (uint64_t)SEG_ITEMS;
+    if ((trie || xlb) && n >= (uint64_t)SEG_ITEMS) {
         std::vector<int> order;
         for (int v : mine) order.push_back(v);
         auto key = [&](int v) {
@@ -721,7 +725,7 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
         mine = order;
         xl = true;
     }
-    if (trie) {
+    if (trie || xlb) {
         size_t a0 = 0;
         trie_chain.resize(mine.size());
         xl_parent.assign(mine.size(), -1);
@@ -772,7 +776,7 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
                     xl_x[a0 + i] = px[ord[i]];
                     cur_sets[i] = sets[ord[i]];
                 }
-            } else {
+            } else if (trie) {
                 std::vector<int> ord;
                 std::vector<std::array<uint8_t, GMAX>> ch;
                 build_mask_trie(sets, g - lm, ord, ch);
@@ -781,6 +785,8 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
                     trie_chain[a0 + i] = ch[ord[i]];
                     cur_sets[i] = sets[ord[i]];
                 }
+            } else {  // (batched trie: built per batch)
+                cur_sets = sets;
             }
             for (size_t i = a0; i < a1; ++i) {
                 xl_slot[i] = (int)(i - a0);
@@ -792,7 +798,7 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
             ++run;
             a0 = a1;
         }
-        p->last_grouping = 3;
+        p->last_grouping = trie ? 3 : 4;
     }
     // (pageable host staging: cudaMemcpyAsync returns once the source is copied,
     // so the member buffers can be reused without a stream sync)
@@ -1043,6 +1049,21 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
                 xl = false;  // (not enough memory: per-level tries, leaves masked)
                 for (auto& v : xl_parent) v = -1;
             }
+        }
+    }
+    if (xlb && xl) {  // batched trie, cross-level: one-word composites per generation
+        const size_t esb = tb64 ? 8 : 4;
+        size_t fr = 0, tot = 0;
+        cudaMemGetInfo(&fr, &tot);
+        const bool have = p->genW0.cap >= xl_maxrun * n * esb + 64 &&
+                          p->genW1.cap >= xl_maxrun * n * esb + 64;
+        if (have || fr > 2 * xl_maxrun * n * esb + (4ull << 30)) {
+            CK(p->ensure(p->genW0, xl_maxrun * n * esb + 64, s));
+            CK(p->ensure(p->genW1, xl_maxrun * n * esb + 64, s));
+            CK(p->ensure(p->kmdev, (bmax_masks + 2) * 8, s));
+        } else {
+            xl = false;
+            for (auto& v : xl_parent) v = -1;
         }
     }
     if (use_win) {
@@ -1385,14 +1406,50 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
             }
             std::vector<TrieNode> nodes;
             std::vector<int> leaf_node;
+            // cross-level (xlb): this run's generation buffer holds unmasked leaves; a
+            // run with parents is one launch of one-symbol passes over their arrays
+            const int gen = xl ? (xl_run[pos] & 1) : 0;
+            uint8_t* genK = (uint8_t*)(gen ? p->genW1.p : p->genW0.p);
+            const uint8_t* pgenK = (const uint8_t*)(gen ? p->genW0.p : p->genW1.p);
+            uint8_t* outB = xl ? genK + (size_t)xl_slot[pos] * n * es : (uint8_t*)p->keysA.p;
+            const uint64_t seqm = (1ull << sb) - 1ull;
+            std::vector<uint64_t> kms;
+            for (size_t j = pos; j < end; ++j) {
+                uint64_t km = 0;
+                for (int r = 0; r < kk; ++r)
+                    km |= (uint64_t)((1u << bits) - 1u) << (sb + bits * (g - 1 - p->mask_kept[mine[j]][r]));
+                kms.push_back(km | seqm);
+            }
             p->stage_begin(s, &a);
             if (kk == 0) {  // no kept position: one key (0), identity order per mask
-                for (size_t j = pos; j < end; ++j)
-                    LK(launch_trie_root(nullptr, (const uint32_t*)p->gmseq.p, n, sb, tb64,
-                                        (uint8_t*)p->keysA.p + (j - pos) * n * es, p->sm_count,
-                                        s));
-            }
-            if (kk > 0) {
+                for (size_t j = pos; j < end; ++j)  // (cross-level: the unmasked root)
+                    LK(launch_trie_root(xl ? (const uint64_t*)p->win.p : nullptr,
+                                        (const uint32_t*)p->gmseq.p, n, sb, tb64,
+                                        outB + (j - pos) * n * es, p->sm_count, s));
+            } else if (xl && xl_parent[pos] >= 0) {
+                std::vector<PassDesc> desc;
+                for (size_t j = pos; j < end; ++j) {
+                    PassDesc pd{};
+                    pd.in_off = (uint64_t)xl_parent[j] * n;
+                    pd.out_off = (uint64_t)(j - pos) * n;
+                    pd.sh[0] = (uint8_t)(sb + bits * (g - 1 - xl_x[j]));
+                    pd.nsym = 1;
+                    pd.symbits = (uint32_t)bits;
+                    pd.omask = ~0ull;
+                    desc.push_back(pd);
+                }
+                CK(p->ensure(p->pdesc, desc.size() * sizeof(PassDesc) + 64, s));
+                CK(cudaMemcpyAsync(p->pdesc.p, desc.data(), desc.size() * sizeof(PassDesc),
+                                   cudaMemcpyHostToDevice, s));
+                int nl = 2;
+                LK(launch_trie_batch(pgenK, outB, tb64, n, (int)desc.size(),
+                                     (const PassDesc*)p->pdesc.p, (uint32_t*)p->hist.p,
+                                     (tb64 ? p->sort_ctas_per_sm : p->sort32_ctas_per_sm) * p->sm_count,
+                                     s, &nl));
+                p->launches += nl - 1;
+                passkeys += (int64_t)desc.size() * (int64_t)n;
+                if (!tb64) passkeys32 += (int64_t)desc.size() * (int64_t)n;
+            } else if (kk > 0) {
                 build_step_trie(sets, kk, P, nodes, leaf_node);
                 const int D = (kk + P - 1) / P;
                 // per depth: its nodes (index within the depth = slot in the scratch)
@@ -1426,7 +1483,7 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
                             if ((add >> x) & 1u) pd.sh[q++] = (uint8_t)(sb + bits * (g - 1 - x));
                         pd.nsym = (uint32_t)q;
                         pd.symbits = (uint32_t)bits;
-                        if (d == D) {
+                        if (d == D && !xl) {
                             uint64_t km = 0;
                             for (int x = 0; x < 32; ++x)
                                 if ((nodes[v].set >> x) & 1u)
@@ -1444,7 +1501,7 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
                                    cudaMemcpyHostToDevice, s));
                 for (int d = 1; d <= D; ++d) {
                     const void* in = d == 1 ? p->trieR.p : ((d - 1) & 1 ? p->trieX1.p : p->trieX0.p);
-                    void* outk = d == D ? p->keysA.p : (d & 1 ? p->trieX1.p : p->trieX0.p);
+                    void* outk = d == D ? (void*)outB : (d & 1 ? p->trieX1.p : p->trieX0.p);
                     int nl = 2;
                     LK(launch_trie_batch(in, outk, tb64, n, (int)at[d].size(),
                                          (const PassDesc*)p->pdesc.p + dofs[d], (uint32_t*)p->hist.p,
@@ -1465,7 +1522,15 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
                 if (ws != GAKCO_OK) return ws;
             }
             p->stage_begin(s, &a);
-            LK(launch_segment(p->keysA.p, tb64, n, nmask, sb, dstride, Dm, so.counts, so, stats, s));
+            if (xl) {  // unmasked leaves: the segment applies each mask's key bits
+                kms.push_back(0);
+                CK(cudaMemcpyAsync(p->kmdev.p, kms.data(), kms.size() * 8, cudaMemcpyHostToDevice, s));
+                LK(launch_segment(outB, tb64, n, nmask, sb, dstride, Dm, so.counts, so, stats, s,
+                                  (const uint64_t*)p->kmdev.p));
+            } else {
+                LK(launch_segment(p->keysA.p, tb64, n, nmask, sb, dstride, Dm, so.counts, so,
+                                  stats, s));
+            }
             p->stage_end(s, S_SEGMENT, a);
         } else if (n > 0 && trie) {
             // mask trie: pass t of a mask is a stable pass by the symbol at its t-th kept

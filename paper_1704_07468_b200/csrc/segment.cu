@@ -26,26 +26,41 @@ namespace gk {
 
 // Element access policies: composites (key bits << sb | seq, the LSD path) or the
 // mask trie's separate arrays (masked packed window, sequence id).
-template <typename K>
+template <typename K, bool KM = false>
 struct SegComp {
     using E = K;
     static constexpr int kMinBlocks = sizeof(K) == 4 ? 5 : 4;  // (u64: 64 registers, no spills)
     const K* keys;
     int sb;
-    __device__ E ld(uint64_t i) const { return keys[i]; }
-    __device__ uint64_t kof(uint64_t) const { return 0; }
-    __device__ uint64_t kseg(uint64_t) const { return 0; }
-    __device__ E ldk(uint64_t i, uint64_t) const { return keys[i]; }
+    const uint64_t* km;  // per segment: key bits << sb | seq bits (nullptr: keys masked)
+    uint64_t n;
+    // (KM: per-segment key masks over unmasked generation slots, which may start off
+    // 16 bytes; else the keys are masked and the batch buffer aligned)
+    __device__ E ld(uint64_t i) const { return KM ? (K)(keys[i] & km[i / n]) : keys[i]; }
+    __device__ uint64_t kof(uint64_t i) const { return KM ? km[i / n] : ~0ull; }
+    __device__ uint64_t kseg(uint64_t sgi) const { return KM ? km[sgi] : ~0ull; }
+    __device__ E ldk(uint64_t i, uint64_t k) const { return (K)(keys[i] & k); }
     template <int IT>
-    __device__ void ldn(uint64_t base, E (&c)[IT], uint64_t) const {
-        constexpr int NV = IT * sizeof(K) / 16;
-        const uint4* v = (const uint4*)(keys + base);
+    __device__ void ldn(uint64_t base, E (&c)[IT], uint64_t sgi) const {
+        if (KM && (((uintptr_t)(keys + base)) & 15)) {  // (generation slots n keys apart)
 #pragma unroll
-        for (int i = 0; i < NV; ++i) {
-            const uint4 q = v[i];
-            const K* kq = (const K*)&q;
+            for (int i = 0; i < IT; ++i) c[i] = keys[base + i];
+        } else {
+            constexpr int NV = IT * sizeof(K) / 16;
+            const uint4* v = (const uint4*)(keys + base);
 #pragma unroll
-            for (int e = 0; e < 16 / (int)sizeof(K); ++e) c[i * (16 / sizeof(K)) + e] = kq[e];
+            for (int i = 0; i < NV; ++i) {
+                const uint4 q = v[i];
+                const K* kq = (const K*)&q;
+#pragma unroll
+                for (int e = 0; e < 16 / (int)sizeof(K); ++e) c[i * (16 / sizeof(K)) + e] = kq[e];
+            }
+        }
+        if (KM) {  // (the items cross at most one segment boundary: n >= IT)
+            const uint64_t end0 = (sgi + 1) * n;
+            const uint64_t k0 = km[sgi], k1 = km[sgi + 1];
+#pragma unroll
+            for (int i = 0; i < IT; ++i) c[i] = (K)(c[i] & ((base + i < end0) ? k0 : k1));
         }
     }
     __device__ bool teq(E a, E b) const { return a == b; }
@@ -374,19 +389,24 @@ __global__ void __launch_bounds__(SEG_THREADS, IT == 8 ? Pol::kMinBlocks : 3) se
 
 cudaError_t launch_segment(const void* keys, bool k64, uint64_t n, int nseg, int sb,
                            int64_t dstride, int64_t* diag, uint32_t* counters, SegmentOut so,
-                           unsigned long long* stats, cudaStream_t s) {
+                           unsigned long long* stats, cudaStream_t s, const uint64_t* km) {
     cudaError_t e = cudaMemsetAsync(counters, 0, 2 * sizeof(uint32_t), s);
     uint64_t total = n * (uint64_t)nseg;
     if (e != cudaSuccess || total == 0) return e;
     uint64_t tiles = (total + SEG_TILE - 1) / SEG_TILE;
-    if (k64)
-        segment_kernel<SegComp<uint64_t>, SEG_ITEMS><<<(unsigned)tiles, SEG_THREADS, 0, s>>>(
-            SegComp<uint64_t>{(const uint64_t*)keys, sb}, n, total, dstride, diag, counters, so,
-            stats);
-    else  // (16 keys per thread measured slower on DNA: 0.97 -> 1.13 ms)
-        segment_kernel<SegComp<uint32_t>, SEG_ITEMS><<<(unsigned)tiles, SEG_THREADS, 0, s>>>(
-            SegComp<uint32_t>{(const uint32_t*)keys, sb}, n, total, dstride, diag, counters, so,
-            stats);
+#define SEG_COMP(KT, KMF)                                                                    \
+    segment_kernel<SegComp<KT, KMF>, SEG_ITEMS><<<(unsigned)tiles, SEG_THREADS, 0, s>>>(     \
+        SegComp<KT, KMF>{(const KT*)keys, sb, km, n}, n, total, dstride, diag, counters, so, \
+        stats)
+    if (km && n < (uint64_t)SEG_ITEMS) return cudaErrorInvalidValue;  // (items cross <= 1 segment)
+    if (k64) {
+        if (km) SEG_COMP(uint64_t, true);
+        else SEG_COMP(uint64_t, false);
+    } else {
+        if (km) SEG_COMP(uint32_t, true);
+        else SEG_COMP(uint32_t, false);
+    }
+#undef SEG_COMP
     return cudaGetLastError();
 }
 
