@@ -280,9 +280,12 @@ __global__ void __launch_bounds__(SEG_THREADS, IT == 8 ? Pol::kMinBlocks : 3) se
         emit_t = th_bits & multi_bits & own;
         emit_g = emit_t & gh_bits;
     }
-    uint32_t agg_t, agg_g;
-    const uint32_t off_t = scan256_excl(__popc(emit_t), s_w, &agg_t);
-    const uint32_t off_g = scan256_excl(__popc(emit_g), s_w, &agg_g);
+    // one block scan of both counts packed in 16-bit halves (a tile emits < 2^16)
+    static_assert(TILE < 65536, "packed scan");
+    uint32_t aggp;
+    const uint32_t offp = scan256_excl(__popc(emit_t) | (__popc(emit_g) << 16), s_w, &aggp);
+    const uint32_t off_t = offp & 0xffffu, off_g = offp >> 16;
+    const uint32_t agg_t = aggp & 0xffffu, agg_g = aggp >> 16;
 
     // 4. the last group starting here may run past the tile: all threads scan its
     //    tail in tile-sized chunks, counting its triple heads
