@@ -47,9 +47,10 @@ __device__ __forceinline__ uint64_t pair_cell(uint32_t x, uint32_t y, int64_t N,
 // small updates become 4-byte records (cell offset << 4 | val) appended to the
 // bucket of their accumulator block, to be applied block by block while the
 // block is L2-resident (apply_bins_kernel); anything else is a direct atomic.
+template <bool BINS = true>
 __device__ __forceinline__ void pair_add(uint32_t* acc, const LightBins& bn, bool valid,
                                          uint64_t idx, uint32_t val) {
-    if (bn.nb == 0) {
+    if (!BINS || bn.nb == 0) {  // (BINS = false: the binning code is not compiled in)
         if (valid) atomicAdd(&acc[idx], val);
         return;
     }
@@ -92,8 +93,12 @@ cudaError_t launch_apply_bins(uint32_t* acc, LightBins bn, int sm_count, cudaStr
     return cudaMemsetAsync(bn.cnt, 0, bn.nb * sizeof(uint32_t), s);
 }
 
-template <bool WIN>
-__global__ void __launch_bounds__(256) light_kernel(SegmentOut so, int64_t heavy_min, int64_t N,
+// MINB: CTAs per SM the register budget is sized for. 5 (48 registers, no spills):
+// the occupancy DNA's L2-resident random updates want (light 3.32 ms; 56 registers:
+// 3.51 ms); 4 (64 registers) is faster for the big groups of Text / Scale (Text
+// light 28.3 -> 26.9 ms, Scale 98.4 -> 96.5 ms).
+template <bool WIN, bool BINS, int MINB>
+__global__ void __launch_bounds__(256, MINB) light_kernel(SegmentOut so, int64_t heavy_min, int64_t N,
                                                     uint32_t* acc, uint2* heavy_list,
                                                     uint64_t ldd, uint32_t* dense_fill,
                                                     LightBins bn, uint32_t flat_max,
@@ -158,7 +163,7 @@ __global__ void __launch_bounds__(256) light_kernel(SegmentOut so, int64_t heavy
                 idx = pair_cell(xa, xb, N, NA, &ok, perm);
                 val = so.tcnt[ta] * so.tcnt[tb];
             }
-            pair_add(acc, bn, ok, idx, val);
+            pair_add<BINS>(acc, bn, ok, idx, val);
         }
 
         // (1b) heavy candidates among the 32 groups: counts checked per group, then one
@@ -275,7 +280,7 @@ __global__ void __launch_bounds__(256) light_kernel(SegmentOut so, int64_t heavy
                     const uint32_t cb = __shfl_sync(0xffffffffu, cA, b);
                     bool ok = false;
                     const uint64_t idx = q < P ? pair_cell(xa, xb, N, NA, &ok, perm) : 0;
-                    pair_add(acc, bn, ok && q < P, idx, ca * cb);
+                    pair_add<BINS>(acc, bn, ok && q < P, idx, ca * cb);
                 }
                 for (uint32_t B = A + 32; B < b0; B += 32) {
                     const uint32_t ib = B + lane;
@@ -287,7 +292,7 @@ __global__ void __launch_bounds__(256) light_kernel(SegmentOut so, int64_t heavy
                         const uint32_t ca = __shfl_sync(0xffffffffu, cA, a);
                         bool ok = false;
                         const uint64_t idx = vb ? pair_cell(xa, xB, N, NA, &ok, perm) : 0;
-                        pair_add(acc, bn, ok && vb, idx, ca * cB);
+                        pair_add<BINS>(acc, bn, ok && vb, idx, ca * cB);
                     }
                 }
             }
@@ -303,19 +308,28 @@ cudaError_t launch_light(SegmentOut so, uint64_t max_groups, int64_t heavy_min, 
                          uint32_t* dense_fill, LightBins bins, uint32_t flat_max,
                          int64_t NA, const uint32_t* perm, uint32_t heavy_cmax,
                          unsigned long long* stats, int sm_count, cudaStream_t s,
-                         WinArgs wa) {
+                         WinArgs wa, bool big) {
     if (max_groups == 0) return cudaGetLastError();
     uint64_t blocks = (max_groups + 255) / 256;  // 8 warps x 32 groups per block-round
     uint64_t cap = (uint64_t)sm_count * 8;
     if (blocks > cap) blocks = cap;
-    if (wa.nw)
-        light_kernel<true><<<(unsigned)blocks, 256, 0, s>>>(so, heavy_min, N, acc, heavy_list,
-                                                            ldd, dense_fill, bins, flat_max, NA,
-                                                            perm, heavy_cmax, stats, wa);
-    else
-        light_kernel<false><<<(unsigned)blocks, 256, 0, s>>>(so, heavy_min, N, acc, heavy_list,
-                                                             ldd, dense_fill, bins, flat_max, NA,
-                                                             perm, heavy_cmax, stats, wa);
+#define LIGHT(W, B, MB)                                                                        \
+    light_kernel<W, B, MB><<<(unsigned)blocks, 256, 0, s>>>(so, heavy_min, N, acc, heavy_list,  \
+                                                            ldd, dense_fill, bins, flat_max, NA, \
+                                                            perm, heavy_cmax, stats, wa)
+    // (instantiations: the window path and the binning ablation compiled in only
+    // where they run; big batches of long masks (>= 2M g-mers) take the 64-register one)
+    if (wa.nw) {
+        if (bins.nb > 0) LIGHT(true, true, 4);
+        else LIGHT(true, false, 4);
+    } else if (bins.nb > 0) {
+        LIGHT(false, true, 5);
+    } else if (big) {
+        LIGHT(false, false, 4);
+    } else {
+        LIGHT(false, false, 5);
+    }
+#undef LIGHT
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess || bins.nb == 0) return e;
     return launch_apply_bins(acc, bins, sm_count, s);

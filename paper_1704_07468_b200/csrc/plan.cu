@@ -1689,7 +1689,8 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
                             (uint32_t)p->light_flat, NA,
                             perm_active ? (const uint32_t*)p->perm.p : nullptr,
                             fp4_lv[m] ? 4u : 255u, stats, p->sm_count, s2,
-                            perm_active && win_on ? wa : WinArgs{nullptr, nullptr, 0, 0, 0}));
+                            perm_active && win_on ? wa : WinArgs{nullptr, nullptr, 0, 0, 0},
+                            n >= (2ull << 20)));
             p->stage_end(s2, S_LIGHT, a);
             if (perm_active && win_on) {  // this batch's window columns (+ the Gram every few)
                 if (win_masks + nmask > win_lim) {  // s32 exactness of the next Gram
