@@ -278,7 +278,11 @@ cudaError_t launch_epilogue(int64_t* C, int64_t N, int g, int k, int M, int64_t*
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     const unsigned tiles = (unsigned)((N + 31) / 32);
-    if (M <= 7)
+    if (M <= 3)  // (the profile array sized to the level count: registers, not local memory)
+        epilogue_kernel<3><<<dim3(tiles, tiles), dim3(32, 8), 0, s>>>(a, cf);
+    else if (M <= 5)
+        epilogue_kernel<5><<<dim3(tiles, tiles), dim3(32, 8), 0, s>>>(a, cf);
+    else if (M <= 7)
         epilogue_kernel<7><<<dim3(tiles, tiles), dim3(32, 8), 0, s>>>(a, cf);
     else
         epilogue_kernel<GMAX><<<dim3(tiles, tiles), dim3(32, 8), 0, s>>>(a, cf);
