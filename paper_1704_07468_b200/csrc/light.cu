@@ -95,8 +95,8 @@ cudaError_t launch_apply_bins(uint32_t* acc, LightBins bn, int sm_count, cudaStr
 
 // MINB: CTAs per SM the register budget is sized for. 5 (48 registers, no spills):
 // the occupancy DNA's L2-resident random updates want (light 3.32 ms; 56 registers:
-// 3.51 ms); 4 (64 registers) is faster for the big groups of Text / Scale (Text
-// light 28.3 -> 26.9 ms, Scale 98.4 -> 96.5 ms).
+// 3.51 ms); 3 (up to 85 registers) is faster for the big groups of Text / Scale
+// (Text light 28.3 -> 26.7 ms, Scale 98.4 -> 93.4 ms).
 template <bool WIN, bool BINS, int MINB>
 __global__ void __launch_bounds__(256, MINB) light_kernel(SegmentOut so, int64_t heavy_min, int64_t N,
                                                     uint32_t* acc, uint2* heavy_list,
@@ -320,12 +320,12 @@ cudaError_t launch_light(SegmentOut so, uint64_t max_groups, int64_t heavy_min, 
     // (instantiations: the window path and the binning ablation compiled in only
     // where they run; big batches of long masks (>= 2M g-mers) take the 64-register one)
     if (wa.nw) {
-        if (bins.nb > 0) LIGHT(true, true, 4);
-        else LIGHT(true, false, 4);
+        if (bins.nb > 0) LIGHT(true, true, 3);
+        else LIGHT(true, false, 3);
     } else if (bins.nb > 0) {
         LIGHT(false, true, 5);
     } else if (big) {
-        LIGHT(false, false, 4);
+        LIGHT(false, false, 3);
     } else {
         LIGHT(false, false, 5);
     }
