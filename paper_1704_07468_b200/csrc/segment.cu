@@ -29,7 +29,7 @@ namespace gk {
 template <typename K, bool KM = false>
 struct SegComp {
     using E = K;
-    static constexpr int kMinBlocks = sizeof(K) == 4 ? 6 : 4;  // (u64: 64 registers, no spills)
+    static constexpr int kMinBlocks = sizeof(K) == 4 ? 7 : 5;  // (u64: 64 registers, no spills)
     const K* keys;
     int sb;
     const uint64_t* km;  // per segment: key bits << sb | seq bits (nullptr: keys masked)
