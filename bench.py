@@ -1,18 +1,24 @@
 #!/usr/bin/env python
 """bench.py — the gapped k-mer kernel-matrix step on 1..8 B200s.
 
-One STEP = the whole hot path of SURVEY.md §8(a) for one synthetic corpus:
-zero C -> gakco_accumulate over this rank's masks (encode, onesweep sort,
-segment, light/heavy pair updates, diagonal) -> NCCL int64 reduce of C to rank
-0 (N > 1) -> gakco_finalize on rank 0 (Eq. 9, Eq. 7, normalisation), with the
-corpus already resident in HBM. Masks are round-robin sharded across ranks;
-total work is fixed as N grows ("strong" scaling).
+One STEP = the whole hot path of SURVEY.md §8(a) for one synthetic corpus, with
+the corpus already resident in HBM:
+  1 GPU:  zero C -> gakco_accumulate over all masks (encode, mask-trie sort,
+          segment, light / heavy pair updates, diagonal) -> gakco_finalize (Eq. 9,
+          Eq. 7, normalisation; full N x N outputs);
+  P GPUs: one process per GPU (re-launched under torch.distributed.run when
+          --gpus P > 1 is given without a torchrun environment); each rank
+          accumulates its round-robin share of the masks, the packed upper
+          triangles are reduce-scattered level by level over NCCL while later
+          levels accumulate, the diagonals all-reduced, and each rank finalises its
+          slice (parallel.ShardedStep). Total work is fixed as P grows ("strong").
 
-    python bench.py [--gpus N] [--steps K] [--warmup W] [--config dna] [--impl reference]
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config scale] [--impl reference]
 
-Default workload: BASELINE.json configs[1] ("dna"). Prints ONE JSON line on
-rank 0. value = masked g-mer keys processed per second by the whole job
-(c_gk * n / step time); ms_per_step is the gkm kernel-matrix time.
+Default workload: BASELINE.json configs[4] ("scale", the largest: 3.71e9 masked
+keys, a 20000 x 20000 output, the config north_star names for 1/2/4/8 GPUs).
+Prints ONE JSON line on rank 0. value = masked g-mer keys processed per second by
+the whole job (c_gk * n / step time); ms_per_step is the gkm kernel-matrix time.
 """
 from __future__ import annotations
 
@@ -37,9 +43,9 @@ UNIT = "keys/s"
 def args_():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="dna", choices=list(sc.CONFIGS))
+    ap.add_argument("--config", default="scale", choices=list(sc.CONFIGS))
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -226,7 +232,8 @@ def config_dict(name, cfg, cp, masks, n, world):
     return {"workload": name, "baseline_config": cfg.description, "N": cp.n_seq,
             "sigma": cfg.sigma, "g": cfg.g, "k": cfg.k, "M": cfg.M, "masks": masks,
             "gmers": n, "keys_per_step": masks * n,
-            "parallelism": f"mask-sharded x{world} + NCCL int64 reduce" if world > 1
+            "parallelism": f"mask-sharded x{world}: per-level packed-triangle NCCL "
+                           f"reduce-scatter + per-rank slice epilogue" if world > 1
             else "1 GPU, all masks",
             "l2": "flushed between timed steps (256 MiB write)"}
 
@@ -333,18 +340,31 @@ def run_ours(a):
     if a.gram_pair is not None:
         plan.set_option(gakco.GAKCO_OPT_GRAM_PAIR, a.gram_pair)
     C = torch.zeros((M + 1, N, N), dtype=torch.int64, device=dev)
-    Nm = torch.empty_like(C) if rank == 0 else None
-    K = torch.empty((N, N), dtype=torch.int64, device=dev) if rank == 0 else None
-    Kn = torch.empty((N, N), dtype=torch.float64, device=dev) if rank == 0 else None
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device=dev)
     stream = torch.cuda.current_stream(dev)
 
     from paper_1704_07468_b200 import parallel
+    nmax = int(max(0, int(cp.lengths().max()) - cfg.g + 1))
+    if world == 1:
+        # one GPU: accumulate all masks, then the full-matrix epilogue (mirrored C,
+        # N_m, K, Knorm as full N x N matrices)
+        Nm = torch.empty_like(C)
+        K = torch.empty((N, N), dtype=torch.int64, device=dev)
+        Kn = torch.empty((N, N), dtype=torch.float64, device=dev)
 
-    def step():
-        parallel.sharded_kernel_matrix(
-            C, N, lambda Ct: plan.accumulate(codes_d, offs_h, N, Ct, stream),
-            lambda Ct: plan.finalize(Ct, N, Nm, K, Kn, stream))
+        def step():
+            C.zero_()
+            plan.accumulate(codes_d, offs_h, N, C, stream)
+            plan.finalize(C, N, Nm, K, Kn, stream)
+    else:
+        # P GPUs: this rank's masks, per-level packed reduce-scatter over NCCL
+        # overlapping the later levels, diagonal all-reduce, epilogue of this rank's
+        # slice of the packed triangle (parallel.ShardedStep)
+        sh = parallel.ShardedStep(plan, N, cfg.g, cfg.k, M, nmax, dev)
+        K = sh.K
+
+        def step():
+            sh.step(codes_d, offs_h, C, stream)
 
     def barrier():
         if world > 1:
@@ -403,15 +423,17 @@ def run_ours(a):
         Kh = torch.empty((N, N), dtype=torch.int64).pin_memory() if rank == 0 else None
         Knh = torch.empty((N, N), dtype=torch.float64).pin_memory() if rank == 0 else None
 
+        if world > 1:  # this rank's slice of K and Knorm, to pinned host memory
+            Kh = torch.empty((sh.chunk,), dtype=torch.int64).pin_memory()
+            Knh = torch.empty((sh.chunk,), dtype=torch.float64).pin_memory()
+
         def e2e_step():
             if world == 1:
                 plan.kernel(codes_h, offs_h, N, C, None, Kh, Knh, stream)
             else:
-                C.zero_()
-                plan.accumulate(codes_h, offs_h, N, C, stream)
-                dist.reduce(C, dst=0, op=dist.ReduceOp.SUM)
-                if rank == 0:
-                    plan.finalize(C, N, None, Kh, Knh, stream)
+                sh.step(codes_h, offs_h, C, stream)
+                Kh.copy_(sh.K, non_blocking=True)
+                Knh.copy_(sh.Knorm, non_blocking=True)
         for _ in range(2):
             e2e_step()
         barrier()
@@ -429,11 +451,12 @@ def run_ours(a):
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
         e_ms = float(t.item()) / a.steps
         h2d = (cp.codes.nbytes + cp.offsets.nbytes) * world
-        d2h = N * N * 16
+        d2h = N * N * 16 if world == 1 else parallel.tri_size(N) * 16
         e2e = {"value": masks * n / (e_ms / 1e3), "unit": UNIT, "ms_per_step": e_ms,
                "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                "api": "gakco_kernel(host pinned codes/offsets -> host K, Knorm)" if world == 1
-               else "gakco_accumulate(host inputs) + NCCL reduce + gakco_finalize(host K, Knorm)"}
+               else "gakco_accumulate(host inputs) + per-level NCCL reduce-scatter + "
+                    "gakco_finalize_packed -> each rank's packed slice of K, Knorm to host"}
 
     # ---- K-only fast path (NEXT-1): K = C_{g-k} from the level-(g-k) masks only
     k_only = None
@@ -553,6 +576,10 @@ def run_ours(a):
 
 def main():
     a = args_()
+    if a.impl == "ours" and a.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: re-launch this command under torch.distributed.run
+        from paper_1704_07468_b200 import parallel
+        sys.exit(parallel.launch(a.gpus, os.path.abspath(__file__), sys.argv[1:]))
     if a.impl == "reference":
         run_reference(a)
     else:

@@ -218,6 +218,51 @@ gakco_status gakco_kernel_rect(gakco_plan* plan, const uint8_t* codes, const int
                                int64_t N, int64_t NA, int64_t* C, int64_t* Nm, int64_t* K,
                                double* Knorm, int64_t* Kdiag, void* cuda_stream);
 
+/* ---- Mask-sharded multi-GPU step ----
+ * The C(g,m) masks are independent (Supp. §S:5.3) and C_m is an
+ * integer sum over masks (Algorithm 1 line 17): rank r of P calls
+ * gakco_set_shard(r, P) + gakco_accumulate into its own zeroed C, then the ranks sum
+ * the upper triangles (the only part gakco_accumulate writes) level by level and
+ * each finalises a slice of it. The triangle is addressed packed, row by row:
+ *   e(X, Y) = X*N - X*(X-1)/2 + (Y - X),  0 <= X <= Y < N,  T = N*(N+1)/2 entries. */
+
+/* Make `stream` wait until level m's C_m of the last gakco_accumulate on this plan
+ * is final (all of its updates, on every stream the plan used; a level with no
+ * mask in this shard is final when the call returns). GAKCO_E_ARG if m is out of
+ * range or the last accumulate did not cover it. No host synchronisation. */
+gakco_status gakco_stream_wait_level(gakco_plan* plan, int m, void* cuda_stream);
+
+/* The levels of the last gakco_accumulate in the order they became final (levels
+ * without masks in this shard first). Writes min(count, cap) ints to out (may be
+ * NULL) and returns count (M+1 after a full accumulate), or -1 for a NULL plan. */
+int gakco_level_order(const gakco_plan* plan, int* out, int cap);
+
+/* Entries [begin, end) of the packed upper triangle of `levels` consecutive N x N
+ * row-major int64 matrices C (DEVICE) -> out[l][e - begin] (DEVICE), as int64
+ * (out_bytes = 8) or as the low 32 bits (out_bytes = 4: the caller guarantees the
+ * values it will sum stay below 2^31, e.g. C(g,m) n_max^2 < 2^31). Enqueued on
+ * cuda_stream, no synchronisation. GAKCO_E_ARG for a range outside [0, T],
+ * levels outside 1..33, out_bytes not 4 / 8 or host pointers. */
+gakco_status gakco_pack_upper(gakco_plan* plan, const int64_t* C, int64_t N, int levels,
+                              int64_t begin, int64_t end, void* out, int out_bytes,
+                              void* cuda_stream);
+
+/* out[l][X] = C_l(X, X) for l < levels (C and out DEVICE, int64). No sync. */
+gakco_status gakco_diag(gakco_plan* plan, const int64_t* C, int64_t N, int levels, int64_t* out,
+                        void* cuda_stream);
+
+/* Epilogue of one packed slice: Cp[m][e - begin] (DEVICE; int64, or u32 when
+ * in_bytes = 4) holds the COMPLETE C_m (all masks summed) of the entries [begin,
+ * end); Cdiag[m][X] (DEVICE, int64) the complete diagonals C_m(X,X) of all N
+ * sequences. Writes, for the same entries, Nm[m][e - begin] (Eq. 9),
+ * K[e - begin] (Eq. 7) and Knorm[e - begin] (K(X,Y)/sqrt(K(X,X) K(Y,Y)),
+ * reading A5), each optional (NULL), DEVICE pointers. Synchronises cuda_stream;
+ * GAKCO_E_INTERNAL on a negative N_m or K != C_{g-k}, GAKCO_E_SYMBOL if the last
+ * accumulate flagged a code >= sigma. */
+gakco_status gakco_finalize_packed(gakco_plan* plan, const void* Cp, int in_bytes, int64_t N,
+                                   int64_t begin, int64_t end, const int64_t* Cdiag, int64_t* Nm,
+                                   int64_t* K, double* Knorm, void* cuda_stream);
+
 /* Counters and (if GAKCO_OPT_TIMING) stage times of the last accumulate /
  * finalize. Synchronises the plan's last stream. */
 gakco_status gakco_get_stats(gakco_plan* plan, gakco_stats* out);

@@ -379,4 +379,18 @@ cudaError_t launch_epilogue_rect(const int64_t* C, const int64_t* Dg, int64_t N,
 cudaError_t launch_epilogue(int64_t* C, int64_t N, int g, int k, int M, int64_t* Nm, int64_t* K,
                             double* Knorm, int64_t* kdiag, int* flags, cudaStream_t s);
 
+// ---- mask-sharded step (shard.cu, epilogue.cu) ----
+// entries [begin, end) of the packed upper triangle of `levels` N x N matrices -> out
+// [levels][end - begin] as int64 (out_bytes 8) or u32 (4, truncating)
+cudaError_t launch_pack_upper(const int64_t* C, int64_t N, int levels, int64_t begin, int64_t end,
+                              void* out, int out_bytes, cudaStream_t s);
+cudaError_t launch_diag(const int64_t* C, int64_t N, int levels, int64_t* out, int sm_count,
+                        cudaStream_t s);
+// complete packed C slice [M+1][end - begin] (int64 or u32) + complete diagonals Dg
+// [M+1][N] -> packed Nm [M+1][end - begin], K, Knorm [end - begin]; kdiag [N] scratch
+cudaError_t launch_epilogue_packed(const void* Cp, int in_bytes, const int64_t* Dg, int64_t N,
+                                   int64_t begin, int64_t end, int g, int k, int M, int64_t* Nm,
+                                   int64_t* K, double* Knorm, int64_t* kdiag, int* flags,
+                                   cudaStream_t s);
+
 }  // namespace gk

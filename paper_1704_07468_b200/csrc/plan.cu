@@ -125,6 +125,10 @@ struct gakco_plan {
     size_t ev_used = 0;
     gakco_stats host_stats{};
     cudaStream_t last_stream = nullptr;
+    // per level, events on the three streams after its last update of C_m (the
+    // sharded step's reduce of level m waits on them: gakco_stream_wait_level)
+    cudaEvent_t ev_level[GMAX + 1][3] = {};
+    std::vector<int> level_order;  // levels of the last accumulate, in completion order
     int64_t last_masks = 0;
     int64_t launches = 0;
     bool after_accumulate = false;
@@ -456,6 +460,9 @@ extern "C" void gakco_destroy(gakco_plan* p) {
     for (DevBuf* b : bufs)
         if (b->p) cudaFree(b->p);
     for (cudaEvent_t e : p->ev_pool) cudaEventDestroy(e);
+    for (auto& lv : p->ev_level)
+        for (cudaEvent_t e : lv)
+            if (e) cudaEventDestroy(e);
     for (cudaEvent_t e : {p->ev_seg[0], p->ev_seg[1], p->ev_light[0], p->ev_light[1], p->ev_join,
                           p->ev_join2, p->ev_build, p->ev_gram[0], p->ev_gram[1]})
         if (e) cudaEventDestroy(e);
@@ -1293,6 +1300,28 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
         return GAKCO_OK;
     };
 
+    // level completion events: every stream that writes C_m records one after the
+    // level's last update (levels without masks in this shard: complete now)
+    p->level_order.clear();
+    auto mark_level = [&](int lv) -> gakco_status {
+        cudaStream_t st3[3] = {s, s2, s3};
+        for (int q = 0; q < 3; ++q) {
+            if (!p->ev_level[lv][q]) CK(cudaEventCreateWithFlags(&p->ev_level[lv][q], cudaEventDisableTiming));
+            CK(cudaEventRecord(p->ev_level[lv][q], st3[q]));
+        }
+        p->level_order.push_back(lv);
+        return GAKCO_OK;
+    };
+    if (only_level < 0) {
+        std::vector<char> has(M + 1, 0);
+        for (int v : mine) has[p->mask_level[v]] = 1;
+        for (int lv = 0; lv <= M; ++lv)
+            if (!has[lv]) {
+                gakco_status ms = mark_level(lv);
+                if (ms != GAKCO_OK) return ms;
+            }
+    }
+    int prev_level = -1;
     if (pipe) {  // everything enqueued on s so far (uploads, zeroing) precedes s2/s3 work
         CK(cudaEventRecord(p->ev_join, s));
         CK(cudaStreamWaitEvent(s2, p->ev_join, 0));
@@ -1340,6 +1369,12 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
             light_m = m;
             light_masks += nmask;
         }
+
+        if (prev_level >= 0 && prev_level != m && only_level < 0) {  // prev_level's C_m is final
+            gakco_status ms = mark_level(prev_level);
+            if (ms != GAKCO_OK) return ms;
+        }
+        prev_level = m;
 
         // triple buffer of this batch; its previous user (batch_no - 2) must be done
         const int bi = (int)(batch_no & 1);
@@ -1727,6 +1762,10 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
         if (fs != GAKCO_OK) return fs;
         fs = lflush();
         if (fs != GAKCO_OK) return fs;
+        if (prev_level >= 0 && only_level < 0) {
+            fs = mark_level(prev_level);
+            if (fs != GAKCO_OK) return fs;
+        }
     }
     if (pipe) {  // the caller's stream sees every s2 / s3 kernel as done
         CK(cudaEventRecord(p->ev_join, s2));
@@ -2001,5 +2040,92 @@ extern "C" gakco_status gakco_get_stats(gakco_plan* p, gakco_stats* out) {
             *ms[se.first] += t;
     }
     *out = r;
+    return GAKCO_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Mask-sharded multi-GPU step (include/gakco.h)
+extern "C" gakco_status gakco_stream_wait_level(gakco_plan* p, int m, void* stream) {
+    if (!p) return GAKCO_E_ARG;
+    if (m < 0 || m > p->M) return p->fail(GAKCO_E_ARG, "level out of range");
+    if (std::find(p->level_order.begin(), p->level_order.end(), m) == p->level_order.end())
+        return p->fail(GAKCO_E_ARG, "level not completed by the last gakco_accumulate");
+    DeviceGuard dg(p->device);
+    for (cudaEvent_t e : p->ev_level[m]) {
+        cudaError_t err = cudaStreamWaitEvent((cudaStream_t)stream, e, 0);
+        if (err != cudaSuccess) return p->cuda_fail(err, "cudaStreamWaitEvent");
+    }
+    return GAKCO_OK;
+}
+
+extern "C" int gakco_level_order(const gakco_plan* p, int* out, int cap) {
+    if (!p) return -1;
+    const int n = (int)p->level_order.size();
+    for (int i = 0; i < n && i < cap && out; ++i) out[i] = p->level_order[i];
+    return n;
+}
+
+extern "C" gakco_status gakco_pack_upper(gakco_plan* p, const int64_t* C, int64_t N, int levels,
+                                         int64_t begin, int64_t end, void* out, int out_bytes,
+                                         void* stream) {
+    if (!p) return GAKCO_E_ARG;
+    if (N < 1 || N >= ((int64_t)1 << 31) || levels < 1 || levels > GMAX + 1)
+        return p->fail(GAKCO_E_ARG, "N or levels out of range");
+    const int64_t T = N * (N + 1) / 2;
+    if (begin < 0 || end < begin || end > T) return p->fail(GAKCO_E_ARG, "range outside the triangle");
+    if (out_bytes != 4 && out_bytes != 8) return p->fail(GAKCO_E_ARG, "out_bytes must be 4 or 8");
+    if (!is_device_ptr(C) || (end > begin && !is_device_ptr(out)))
+        return p->fail(GAKCO_E_ARG, "C and out must be device pointers");
+    DeviceGuard dg(p->device);
+    cudaError_t e = launch_pack_upper(C, N, levels, begin, end, out, out_bytes, (cudaStream_t)stream);
+    return e == cudaSuccess ? GAKCO_OK : p->cuda_fail(e, "pack_upper");
+}
+
+extern "C" gakco_status gakco_diag(gakco_plan* p, const int64_t* C, int64_t N, int levels,
+                                   int64_t* out, void* stream) {
+    if (!p) return GAKCO_E_ARG;
+    if (N < 1 || N >= ((int64_t)1 << 31) || levels < 1 || levels > GMAX + 1)
+        return p->fail(GAKCO_E_ARG, "N or levels out of range");
+    if (!is_device_ptr(C) || !is_device_ptr(out))
+        return p->fail(GAKCO_E_ARG, "C and out must be device pointers");
+    DeviceGuard dg(p->device);
+    cudaError_t e = launch_diag(C, N, levels, out, p->sm_count, (cudaStream_t)stream);
+    return e == cudaSuccess ? GAKCO_OK : p->cuda_fail(e, "diag");
+}
+
+extern "C" gakco_status gakco_finalize_packed(gakco_plan* p, const void* Cp, int in_bytes,
+                                              int64_t N, int64_t begin, int64_t end,
+                                              const int64_t* Cdiag, int64_t* Nm, int64_t* K,
+                                              double* Knorm, void* stream) {
+    if (!p) return GAKCO_E_ARG;
+    if (N < 1 || N >= ((int64_t)1 << 31)) return p->fail(GAKCO_E_ARG, "N out of range");
+    const int64_t T = N * (N + 1) / 2;
+    if (begin < 0 || end < begin || end > T) return p->fail(GAKCO_E_ARG, "range outside the triangle");
+    if (in_bytes != 4 && in_bytes != 8) return p->fail(GAKCO_E_ARG, "in_bytes must be 4 or 8");
+    if (!Cdiag || !is_device_ptr(Cdiag) || (end > begin && (!Cp || !is_device_ptr(Cp))))
+        return p->fail(GAKCO_E_ARG, "Cp and Cdiag must be device pointers");
+    for (const void* o : {(const void*)Nm, (const void*)K, (const void*)Knorm})
+        if (o && end > begin && !is_device_ptr(o))
+            return p->fail(GAKCO_E_ARG, "outputs must be device pointers");
+    DeviceGuard dg(p->device);
+    cudaStream_t s = (cudaStream_t)stream;
+#define CK(x)                                               \
+    do {                                                    \
+        cudaError_t e_ = (x);                               \
+        if (e_ != cudaSuccess) return p->cuda_fail(e_, #x); \
+    } while (0)
+    CK(p->ensure(p->kdiag, N * 8, s));
+    CK(p->ensure(p->flags, 64, s, /*zero=*/true));
+    CK(cudaMemsetAsync(p->flags.p, 0, sizeof(int), s));
+    CK(launch_epilogue_packed(Cp, in_bytes, Cdiag, N, begin, end, p->g, p->k, p->M, Nm, K, Knorm,
+                              (int64_t*)p->kdiag.p, (int*)p->flags.p, s));
+    int fl[2] = {0, 0};
+    CK(cudaMemcpyAsync(fl, p->flags.p, 2 * sizeof(int), cudaMemcpyDeviceToHost, s));
+    CK(cudaMemsetAsync((int*)p->flags.p + 1, 0, sizeof(int), s));
+    CK(cudaStreamSynchronize(s));
+#undef CK
+    if (fl[1] & EF_BAD_SYMBOL) return p->fail(GAKCO_E_SYMBOL, "a code is >= sigma");
+    if (fl[0] & EF_NEGATIVE_N) return p->fail(GAKCO_E_INTERNAL, "negative N_m after Eq. 9");
+    if (fl[0] & EF_K_MISMATCH) return p->fail(GAKCO_E_INTERNAL, "K != C_{g-k}");
     return GAKCO_OK;
 }

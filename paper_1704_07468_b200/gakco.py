@@ -45,7 +45,8 @@ GAKCO_OPT_GRAM_EACH = 15
 
 EXPORTS = ("gakco_create", "gakco_set_shard", "gakco_set_option", "gakco_accumulate",
            "gakco_finalize", "gakco_kernel", "gakco_kernel_k", "gakco_kernel_rect",
-           "gakco_get_stats",
+           "gakco_get_stats", "gakco_stream_wait_level", "gakco_level_order", "gakco_pack_upper",
+           "gakco_diag", "gakco_finalize_packed",
            "gakco_num_masks", "gakco_last_error", "gakco_status_string", "gakco_destroy")
 
 
@@ -90,6 +91,12 @@ def lib():
         L.gakco_kernel_k.argtypes = [P, P, P, i64, P, P, P]
         L.gakco_kernel_rect.argtypes = [P, P, P, i64, i64, P, P, P, P, P, P]
         L.gakco_get_stats.argtypes = [P, ctypes.POINTER(gakco_stats)]
+        L.gakco_stream_wait_level.argtypes = [P, ci, P]
+        L.gakco_level_order.argtypes = [P, ctypes.POINTER(ci), ci]
+        L.gakco_level_order.restype = ci
+        L.gakco_pack_upper.argtypes = [P, P, i64, ci, i64, i64, P, ci, P]
+        L.gakco_diag.argtypes = [P, P, i64, ci, P, P]
+        L.gakco_finalize_packed.argtypes = [P, P, ci, i64, i64, i64, P, P, P, P, P]
         L.gakco_num_masks.argtypes = [P, ci]
         L.gakco_num_masks.restype = i64
         L.gakco_last_error.argtypes = [P]
@@ -100,7 +107,8 @@ def lib():
         L.gakco_destroy.restype = None
         for f in ("gakco_create", "gakco_set_shard", "gakco_set_option", "gakco_accumulate",
                   "gakco_finalize", "gakco_kernel", "gakco_kernel_k", "gakco_kernel_rect",
-                  "gakco_get_stats"):
+                  "gakco_get_stats", "gakco_stream_wait_level", "gakco_pack_upper",
+                  "gakco_diag", "gakco_finalize_packed"):
             getattr(L, f).restype = ci
         _lib = L
     return _lib
@@ -183,6 +191,34 @@ def gakco_get_stats(plan):
     return s.as_dict()
 
 
+def gakco_stream_wait_level(plan, m, stream=None):
+    _check(plan, lib().gakco_stream_wait_level(plan, m, _stream(stream)))
+
+
+def gakco_level_order(plan):
+    buf = (ctypes.c_int * 64)()
+    n = lib().gakco_level_order(plan, buf, 64)
+    if n < 0:
+        raise GakcoError(GAKCO_E_ARG, "null plan")
+    return [buf[i] for i in range(min(n, 64))]
+
+
+def gakco_pack_upper(plan, C, N, levels, begin, end, out, out_bytes, stream=None):
+    _check(plan, lib().gakco_pack_upper(plan, _ptr(C), N, levels, begin, end, _ptr(out),
+                                        out_bytes, _stream(stream)))
+
+
+def gakco_diag(plan, C, N, levels, out, stream=None):
+    _check(plan, lib().gakco_diag(plan, _ptr(C), N, levels, _ptr(out), _stream(stream)))
+
+
+def gakco_finalize_packed(plan, Cp, in_bytes, N, begin, end, Cdiag, Nm=None, K=None, Knorm=None,
+                          stream=None):
+    _check(plan, lib().gakco_finalize_packed(plan, _ptr(Cp), in_bytes, N, begin, end,
+                                             _ptr(Cdiag), _ptr(Nm), _ptr(K), _ptr(Knorm),
+                                             _stream(stream)))
+
+
 def gakco_num_masks(plan, shard_only=False):
     return int(lib().gakco_num_masks(plan, 1 if shard_only else 0))
 
@@ -224,6 +260,22 @@ class Plan:
 
     def stats(self):
         return gakco_get_stats(self.h)
+
+    def stream_wait_level(self, m, stream=None):
+        gakco_stream_wait_level(self.h, m, stream)
+
+    def level_order(self):
+        return gakco_level_order(self.h)
+
+    def pack_upper(self, C, N, levels, begin, end, out, out_bytes, stream=None):
+        gakco_pack_upper(self.h, C, N, levels, begin, end, out, out_bytes, stream)
+
+    def diag(self, C, N, levels, out, stream=None):
+        gakco_diag(self.h, C, N, levels, out, stream)
+
+    def finalize_packed(self, Cp, in_bytes, N, begin, end, Cdiag, Nm=None, K=None, Knorm=None,
+                        stream=None):
+        gakco_finalize_packed(self.h, Cp, in_bytes, N, begin, end, Cdiag, Nm, K, Knorm, stream)
 
     def num_masks(self, shard_only=False):
         return gakco_num_masks(self.h, shard_only)

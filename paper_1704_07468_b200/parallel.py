@@ -1,15 +1,37 @@
 """Mask-sharded multi-GPU orchestration (one process per GPU).
 
-The C(g,m) masks are independent (Supp. S:5.3 P:454), so rank r of
-P processes the masks whose global index (level by level m = 0..M,
-lexicographic within a level) is congruent to r mod P — the rule
-gakco_set_shard implements in libgakco.so. Each rank accumulates a partial
-int64 C (upper triangle); one reduce(SUM) over the process group (NCCL int64 on
-B200s) gives rank 0 the full C, and rank 0 runs the epilogue (gakco_finalize).
+The C(g,m) masks are independent (Supp. §S:5.3) and C_m is an
+integer sum over masks (Algorithm 1 line 17). Rank r of P processes
+the masks whose global index (level by level m = 0..M, lexicographic within a
+level) is congruent to r mod P — the rule gakco_set_shard implements in
+libgakco.so — into its own zeroed C. Then (ShardedStep.step):
+
+  * as each level's C_m becomes final on the device (gakco_stream_wait_level, no
+    host sync), a comm stream packs its upper triangle (gakco_pack_upper: the only
+    part gakco_accumulate writes, e(X,Y) = X N - X(X-1)/2 + (Y-X)) into 32-bit
+    words when the summed value is bounded below 2^31, else int64, and reduce-
+    scatters it over the process group (NCCL over NVLink on B200s): rank r receives
+    the complete C_m of packed entries [r*chunk, (r+1)*chunk). The reduces of early
+    levels overlap the accumulation of later ones;
+  * the diagonals C_m(X,X) (gakco_diag, (M+1) x N int64) are all-reduced, since
+    Knorm needs K(X,X) of every sequence;
+  * every rank runs the epilogue (Eq. 9, Eq. 7, normalisation) on its own slice
+    (gakco_finalize_packed): the outputs C, N_m, K, Knorm end sharded over the
+    ranks as packed upper-triangle slices (symmetric matrices, reading A4).
+
+Nothing here computes the method: every step runs in libgakco.so; this module
+only moves buffers between the library and torch.distributed. With the gloo
+backend (CPU tests) the collectives are staged through host memory.
 """
 from __future__ import annotations
 
+import contextlib
+import os
+import socket
+import subprocess
+import sys
 from itertools import combinations
+from math import comb
 
 
 def masks(g: int, M: int):
@@ -25,21 +47,125 @@ def shard_masks(g: int, M: int, rank: int, world: int):
     return [mk for i, mk in enumerate(masks(g, M)) if i % world == rank]
 
 
-def sharded_kernel_matrix(C, N, accumulate, finalize, group=None, reduce_op=None):
-    """One step of the sharded path.
+def tri_size(N: int) -> int:
+    """Entries of the packed upper triangle (diagonal included)."""
+    return N * (N + 1) // 2
 
-    accumulate(C): add this rank's masks into the zeroed C (gakco_accumulate);
-    finalize(C):   rank 0 only, after the reduction (gakco_finalize).
-    The reduction is torch.distributed.reduce(C, dst=0, SUM) when a process
-    group is initialised with more than one rank.
+
+def tri_slice(N: int, rank: int, world: int):
+    """(chunk, begin, end): rank's part of the packed triangle, chunk = ceil(T/world)."""
+    T = tri_size(N)
+    chunk = -(-T // world)
+    b = min(T, rank * chunk)
+    return chunk, b, min(T, b + chunk)
+
+
+def word_bytes(g: int, M: int, nmax: int) -> int:
+    """4 when every complete C_m(X,Y) <= C(g,m) n_max^2 stays below 2^31, else 8."""
+    return 4 if all(comb(g, m) * nmax * nmax < 2 ** 31 for m in range(M + 1)) else 8
+
+
+def tri_index(X, Y, N):
+    """Packed index of (X, Y), X <= Y (numpy arrays or ints)."""
+    return X * N - X * (X - 1) // 2 + (Y - X)
+
+
+class ShardedStep:
+    """One step of the mask-sharded path on this rank.
+
+    plan: gakco.Plan (or a test double with the same methods) with set_shard(rank,
+    world) applied. C: this rank's (M+1, N, N) int64 accumulator. After step()
+    the rank's slice [begin, end) of the packed triangle is in Cp (complete C_m,
+    word_bytes wide), Nm (M+1, chunk), K (chunk,), Knorm (chunk,).
     """
-    import torch.distributed as dist
-    C.zero_()
-    accumulate(C)
-    world = dist.get_world_size(group) if dist.is_available() and dist.is_initialized() else 1
-    rank = dist.get_rank(group) if world > 1 else 0
-    if world > 1:
-        dist.reduce(C, dst=0, op=reduce_op or dist.ReduceOp.SUM, group=group)
-    if rank == 0:
-        finalize(C)
-    return rank
+
+    def __init__(self, plan, N, g, k, M, nmax, device, group=None, backend=None,
+                 outputs=True):
+        import torch
+        import torch.distributed as dist
+        self.torch, self.dist = torch, dist
+        self.plan, self.N, self.g, self.k, self.M = plan, N, g, k, M
+        self.group = group
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        self.backend = backend or (dist.get_backend(group) if dist.is_initialized() else "none")
+        self.dev = torch.device(device)
+        self.cuda = self.dev.type == "cuda"
+        self.T = tri_size(N)
+        self.chunk, self.begin, self.end = tri_slice(N, self.rank, self.world)
+        self.wb = word_bytes(g, M, nmax)
+        wdt = torch.int32 if self.wb == 4 else torch.int64
+        L = M + 1
+        # per-level packed buffers (zero pad past T), the reduced slice, diagonals
+        self.pack = torch.zeros((L, self.chunk * self.world), dtype=wdt, device=self.dev)
+        self.Cp = torch.zeros((L, self.chunk), dtype=wdt, device=self.dev)
+        self.D = torch.zeros((L, N), dtype=torch.int64, device=self.dev)
+        self.Nm = torch.empty((L, self.chunk), dtype=torch.int64, device=self.dev) if outputs else None
+        self.K = torch.empty((self.chunk,), dtype=torch.int64, device=self.dev)
+        self.Knorm = torch.empty((self.chunk,), dtype=torch.float64, device=self.dev) if outputs else None
+        self.comm = torch.cuda.Stream(self.dev) if self.cuda else None
+
+    # -- collectives (NCCL on the device; gloo through host memory)
+    def _reduce_scatter(self, out, inp):
+        if self.world == 1:
+            out.copy_(inp[: self.chunk])
+        elif self.backend == "nccl":
+            self.dist.reduce_scatter_tensor(out, inp, group=self.group)
+        else:
+            t = inp.cpu()
+            self.dist.all_reduce(t, group=self.group)
+            out.copy_(t[self.rank * self.chunk:(self.rank + 1) * self.chunk])
+
+    def _all_reduce(self, t):
+        if self.world == 1:
+            return
+        if self.backend == "nccl":
+            self.dist.all_reduce(t, group=self.group)
+        else:
+            h = t.cpu()
+            self.dist.all_reduce(h, group=self.group)
+            t.copy_(h)
+
+    def _on_comm(self):
+        return self.torch.cuda.stream(self.comm) if self.cuda else contextlib.nullcontext()
+
+    def step(self, codes, offsets, C, stream=None):
+        """accumulate (this rank's masks) -> per-level pack + reduce-scatter (comm
+        stream, overlapping later levels) -> diagonal all-reduce -> slice epilogue."""
+        plan, N, L = self.plan, self.N, self.M + 1
+        C.zero_()
+        plan.accumulate(codes, offsets, N, C, stream)
+        cs = self.comm
+        with self._on_comm():
+            for m in plan.level_order():
+                plan.stream_wait_level(m, cs)
+                plan.pack_upper(C[m], N, 1, 0, self.T, self.pack[m], self.wb, cs)
+                self._reduce_scatter(self.Cp[m], self.pack[m])
+            plan.diag(C, N, L, self.D, cs)
+            self._all_reduce(self.D)
+            plan.finalize_packed(self.Cp, self.wb, N, self.begin, self.end, self.D, self.Nm,
+                                 self.K, self.Knorm, cs)
+        if self.cuda:
+            (stream or self.torch.cuda.current_stream(self.dev)).wait_stream(cs)
+        return self.begin, self.end
+
+
+# ------------------------------------------------------------------ launcher
+def free_port() -> int:
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
+def launch(nprocs: int, script: str, args, env=None) -> int:
+    """Run `script args` as nprocs ranks of one node under torch.distributed.run
+    (rendezvous on 127.0.0.1); returns the exit code. bench.py re-launches itself
+    through this when --gpus N > 1 is given without a torchrun environment."""
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={nprocs}", "--master-addr=127.0.0.1",
+           f"--master-port={free_port()}", script] + list(args)
+    e = dict(os.environ)
+    e.update(env or {})
+    return subprocess.call(cmd, env=e)

@@ -58,8 +58,10 @@ def _worker(rank, world, port, result_path):
     def fin(Ct):
         out["C"] = Ct.numpy().copy()
 
-    r = parallel.sharded_kernel_matrix(C, N, acc, fin)
-    if r == 0:
+    acc(C)
+    dist.reduce(C, dst=0, op=dist.ReduceOp.SUM)
+    if rank == 0:
+        fin(C)
         import oracle
         ref = oracle.compute(cp, g, k, M)["C"]
         upper = np.triu(np.ones((N, N), dtype=bool))
@@ -94,3 +96,32 @@ def test_gloo_world2_reduce(tmp_path, oracle_lib):
     mp.start_processes(_worker, args=(2, port, str(res)), nprocs=2, join=True,
                        start_method="spawn")
     assert res.read_text() == "ok"
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_launcher_sharded_step_gloo(tmp_path, oracle_lib, world):
+    """The launcher (parallel.launch -> torch.distributed.run) and the ShardedStep
+    that bench.py uses for --gpus N > 1, world 2 and 3 on CPU with gloo: per-level
+    packed reduce-scatter, diagonal all-reduce and per-rank slice epilogue (through
+    the CPU test double); the assembled slices equal the oracle's C, N_m, K, Knorm."""
+    from paper_1704_07468_b200 import parallel
+    res = tmp_path / "res.txt"
+    rc = parallel.launch(world, os.path.join(ROOT, "tests", "dist_worker.py"), [str(res)],
+                         env={"CUDA_VISIBLE_DEVICES": "", "OMP_NUM_THREADS": "1"})
+    assert rc == 0
+    assert res.read_text().startswith("ok"), res.read_text()
+
+
+def test_tri_slices_cover_triangle():
+    from paper_1704_07468_b200 import parallel
+    for N in (1, 2, 7, 50, 20000):
+        T = parallel.tri_size(N)
+        for world in (1, 2, 3, 8):
+            sl = [parallel.tri_slice(N, r, world) for r in range(world)]
+            assert sl[0][1] == 0 and sl[-1][2] == T
+            assert all(sl[i][2] == sl[i + 1][1] for i in range(world - 1))
+            assert all(e - b <= c for c, b, e in sl)
+    # packed index: row starts and the last entry
+    N = 9
+    assert parallel.tri_index(0, 0, N) == 0 and parallel.tri_index(N - 1, N - 1, N) == parallel.tri_size(N) - 1
+    assert parallel.tri_index(1, 1, N) == N
