@@ -118,9 +118,13 @@ typedef enum {
                                      with relabelling), 0 = off, 1 = on (relabels) */
     GAKCO_OPT_WINDOW_MIN = 14,    /* smallest group (sequences) for the window Gram (default 9;
                                      groups of <= GAKCO_OPT_LIGHT_FLAT sequences stay light) */
-    GAKCO_OPT_GRAM_EACH = 15      /* 1: the heavy-group Gram runs after every batch (overlapping
+    GAKCO_OPT_GRAM_EACH = 15,     /* 1: the heavy-group Gram runs after every batch (overlapping
                                      the next batch) instead of when a level ends or D fills;
                                      0 (default) */
+    GAKCO_OPT_TRIE_PASS = 16      /* mask-trie pass kernel: 1 (default) = the symbol-digit pass
+                                     (<= 64 buckets, chunk prefixes inside the scatter: two
+                                     launches) where sigma <= 64; 0 = the generic 8-bit radix
+                                     pass (hist + chunk scan + scatter) */
 } gakco_option;
 
 /* Counters of the last gakco_accumulate (algorithmic units). */

@@ -251,6 +251,13 @@ cudaError_t launch_trie_root(const uint64_t* win, const uint32_t* seq, uint64_t 
 cudaError_t launch_trie_pass(const uint64_t* win, uint64_t* wout, const void* sin, void* sout,
                              bool seq16, uint64_t n, int shift, uint32_t dmask, uint64_t omask,
                              uint32_t* hist, int target_ctas, cudaStream_t s, int* nlaunch);
+// Σ <= 64 variant (trie.cu): hist + scatter (chunk prefixes computed in the scatter);
+// cntp: device element count (nullptr: n); n: capacity (grid size)
+bool trie_pass64_ok(uint32_t dmask);
+cudaError_t launch_trie_pass64(const uint64_t* win, uint64_t* wout, const void* sin, void* sout,
+                               bool seq16, uint64_t n, const uint32_t* cntp, int shift,
+                               uint32_t dmask, uint64_t omask, uint32_t* H, int target_ctas,
+                               cudaStream_t s);
 cudaError_t launch_seq16(const uint32_t* a, uint16_t* b, uint64_t n, int sm_count,
                          cudaStream_t s);
 cudaError_t launch_radix_chunked2(const void* in, void* out, bool k64, uint64_t n, int nseg,

@@ -93,6 +93,7 @@ struct gakco_plan {
     int64_t window_min = 9;    // smallest group (sequences) for the window Gram
     int level_order_desc = 0;  // process levels m = M..0 (1) or 0..M (0, measured faster on DNA)
     int gram_fp4 = -1;         // -1 auto (e2m1 Gram when exact), 0 u8 / kind::i8, 1 e2m1
+    int trie_pass = 1;         // mask-trie pass kernel: 1 trie.cu (Σ <= 64), 0 generic radix
     int pipeline = 1;          // light / dense / Gram of batch b on an aux stream, overlapping
                                // encode / sort / segment of batch b+1 (double-buffered triples)
     cudaStream_t aux = nullptr, aux2 = nullptr;  // light + dense; Gram flushes
@@ -540,6 +541,10 @@ extern "C" gakco_status gakco_set_option(gakco_plan* p, int option, int64_t valu
             return GAKCO_OK;
         case GAKCO_OPT_TIMING:
             p->timing = value != 0;
+            return GAKCO_OK;
+        case GAKCO_OPT_TRIE_PASS:
+            if (value < 0 || value > 1) return p->fail(GAKCO_E_ARG, "trie pass must be 0 or 1");
+            p->trie_pass = (int)value;
             return GAKCO_OK;
         default:
             return p->fail(GAKCO_E_ARG, "unknown option");
@@ -1574,6 +1579,9 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
             // windows to the mask's segment of the batch
             const int kk = g - m;
             const uint32_t dmask = (1u << bits) - 1u;
+            // symbol digits of <= 6 bits: the two-launch pass of trie.cu (option 0: the
+            // generic three-launch radix pass, for comparison)
+            const bool tp64 = p->trie_pass == 1 && trie_pass64_ok(dmask);
             // (cross-level: this run's generation buffer; else the batch buffers)
             const int gen = xl ? (xl_run[pos] & 1) : 0;
             uint64_t* genW = (uint64_t*)(gen ? p->genW1.p : p->genW0.p);
@@ -1603,11 +1611,17 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
                 }
                 if (xl && xl_parent[j] >= 0) {  // one pass over the parent mask's arrays
                     int nl = 2;
-                    LK(launch_trie_pass(pgenW + (size_t)xl_parent[j] * n, wleaf,
-                                        pgenS + (size_t)xl_parent[j] * n * ssz, sleaf, seq16, n,
-                                        bits * (g - 1 - xl_x[j]), dmask, ~0ull,
-                                        (uint32_t*)p->hist.p, p->trie_ctas_per_sm * p->sm_count, s,
-                                        &nl));
+                    if (tp64)
+                        LK(launch_trie_pass64(pgenW + (size_t)xl_parent[j] * n, wleaf,
+                                              pgenS + (size_t)xl_parent[j] * n * ssz, sleaf, seq16, n,
+                                              nullptr, bits * (g - 1 - xl_x[j]), dmask, ~0ull,
+                                              (uint32_t*)p->hist.p, p->trie_ctas_per_sm * p->sm_count, s));
+                    else
+                        LK(launch_trie_pass(pgenW + (size_t)xl_parent[j] * n, wleaf,
+                                            pgenS + (size_t)xl_parent[j] * n * ssz, sleaf, seq16, n,
+                                            bits * (g - 1 - xl_x[j]), dmask, ~0ull,
+                                            (uint32_t*)p->hist.p, p->trie_ctas_per_sm * p->sm_count, s,
+                                            &nl));
                     p->launches += nl - 1;
                     passkeys += (int64_t)n;
                     continue;
@@ -1623,9 +1637,14 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
                     uint64_t* wo = leaf ? wleaf : (uint64_t*)p->trieW.p + (size_t)t * n;
                     void* so_ = leaf ? (void*)sleaf : (void*)((uint8_t*)p->trieS.p + (size_t)t * n * ssz);
                     int nl = 2;
-                    LK(launch_trie_pass(wi, wo, si, so_, seq16, n, bits * (g - 1 - kept[t]), dmask,
-                                        leaf && !xl ? kmask : ~0ull, (uint32_t*)p->hist.p,
-                                        p->trie_ctas_per_sm * p->sm_count, s, &nl));
+                    if (tp64)
+                        LK(launch_trie_pass64(wi, wo, si, so_, seq16, n, nullptr, bits * (g - 1 - kept[t]),
+                                              dmask, leaf && !xl ? kmask : ~0ull, (uint32_t*)p->hist.p,
+                                              p->trie_ctas_per_sm * p->sm_count, s));
+                    else
+                        LK(launch_trie_pass(wi, wo, si, so_, seq16, n, bits * (g - 1 - kept[t]), dmask,
+                                            leaf && !xl ? kmask : ~0ull, (uint32_t*)p->hist.p,
+                                            p->trie_ctas_per_sm * p->sm_count, s, &nl));
                     p->launches += nl - 1;  // hist (+ chunk scan) + scatter
                     if (!leaf) stack_pos[t] = kept[t];
                 }

@@ -1,0 +1,309 @@
+// trie.cu — one stable pass of the mask trie over (packed window, sequence id)
+// elements, specialised for symbol digits (Σ <= 64: at most 64 buckets).
+//
+// Algorithm 1 line 14, L^i <- sort(L^i), done as LSD passes over
+// the kept positions of a mask (DESIGN.md §8 "Mask trie"): a pass is a stable
+// counting sort by the symbol at ONE kept position, digit = (w >> shift) & dmask.
+// Two launches per pass instead of the generic radix path's three:
+//   tp_hist:    CTA c counts the digits of its chunk (per-warp shared counters);
+//   tp_scatter: CTA c computes its chunk prefix and the digit bases itself from the
+//               chunk histograms (64 digits x 8 chunk strides in parallel: no
+//               separate scan launch), then streams its chunk in 4096-element tiles
+//               (cp.async.bulk into shared memory, one tile ahead), ranks each tile
+//               stably (warp atomicOr match + per-warp digit counters), reorders it
+//               in shared memory and writes every digit run contiguously.
+// 512 threads x 8 elements per tile (16 warps) keep the registers at <= 64 so two
+// CTAs (1024 threads) fit an SM next to their ~100 KB of shared memory.
+//
+// The element count may live on the device (cntp != nullptr: a compacted parent
+// array of the cross-level chain, plan.cu); the grid is sized for the capacity n
+// and both kernels derive the same chunking from the actual count.
+#include <algorithm>
+#include <type_traits>
+
+#include "internal.cuh"
+#include "tc_ptx.cuh"
+
+namespace gk {
+
+namespace {
+
+constexpr int TP_THREADS = 512;
+constexpr int TP_WARPS = TP_THREADS / 32;
+constexpr int TP_ITEMS = 8;
+constexpr int TP_TILE = TP_THREADS * TP_ITEMS;  // 4096
+constexpr int TP_ND = 64;                       // digit buckets (symbols < 64)
+
+__device__ __forceinline__ void tp_bulk(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+        ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+// bytes of the 16-byte aligned window covering elements [g0, g0 + cnt) of `in`
+template <typename T>
+__device__ __forceinline__ uint32_t tp_span(const T* in, uint64_t g0, uint32_t cnt) {
+    const uintptr_t a0 = (uintptr_t)(in + g0), a1 = (uintptr_t)(in + g0 + cnt);
+    return (uint32_t)(((a1 + 15) & ~(uintptr_t)15) - (a0 & ~(uintptr_t)15));
+}
+template <typename T>
+__device__ __forceinline__ const void* tp_base(const T* in, uint64_t g0) {
+    return (const void*)((uintptr_t)(in + g0) & ~(uintptr_t)15);
+}
+template <typename T>
+__device__ __forceinline__ uint32_t tp_delta(const T* in, uint64_t g0) {
+    return (uint32_t)(((uintptr_t)(in + g0) & 15) / sizeof(T));
+}
+
+// chunking shared by both kernels: cps chunks of L elements (whole tiles)
+struct TpChunk {
+    uint64_t lo, hi;
+};
+__device__ __forceinline__ TpChunk tp_chunk(uint64_t cnt, uint32_t cps, uint32_t c) {
+    const uint64_t tiles = (cnt + TP_TILE - 1) / TP_TILE;
+    const uint64_t L = (tiles + cps - 1) / cps * TP_TILE;
+    const uint64_t lo = min(cnt, (uint64_t)c * L);
+    return {lo, min(cnt, lo + L)};
+}
+
+__global__ void __launch_bounds__(TP_THREADS) tp_hist_kernel(const uint64_t* __restrict__ w,
+                                                             uint64_t n, const uint32_t* cntp,
+                                                             int shift, uint32_t dmask,
+                                                             uint32_t* __restrict__ H) {
+    __shared__ uint32_t s_h[TP_WARPS][TP_ND];
+    const int tid = threadIdx.x, wp = tid >> 5;
+    for (int i = tid; i < TP_WARPS * TP_ND; i += TP_THREADS) (&s_h[0][0])[i] = 0;
+    __syncthreads();
+    const uint64_t cnt = cntp ? (uint64_t)*cntp : n;
+    const TpChunk ch = tp_chunk(cnt, gridDim.x, blockIdx.x);
+    uint64_t a = ch.lo;
+    if (a < ch.hi && ((uintptr_t)(w + a) & 15)) {  // (16-byte loads on the aligned body)
+        if (tid == 0) atomicAdd(&s_h[0][(uint32_t)(w[a] >> shift) & dmask], 1u);
+        ++a;
+    }
+    const uint64_t nv = a < ch.hi ? (ch.hi - a) / 2 : 0;
+    const uint4* v = (const uint4*)(w + a);
+    for (uint64_t i = tid; i < nv; i += TP_THREADS) {
+        const uint4 q = v[i];
+        atomicAdd(&s_h[wp][(uint32_t)(((uint64_t)q.y << 32 | q.x) >> shift) & dmask], 1u);
+        atomicAdd(&s_h[wp][(uint32_t)(((uint64_t)q.w << 32 | q.z) >> shift) & dmask], 1u);
+    }
+    if (a + nv * 2 < ch.hi && tid == 0)
+        atomicAdd(&s_h[0][(uint32_t)(w[ch.hi - 1] >> shift) & dmask], 1u);
+    __syncthreads();
+    if (tid < TP_ND) {
+        uint32_t s = 0;
+#pragma unroll
+        for (int ww = 0; ww < TP_WARPS; ++ww) s += s_h[ww][tid];
+        H[(uint64_t)blockIdx.x * TP_ND + tid] = s;
+    }
+}
+
+// exclusive scan of v over the 64 threads tid < 64 (two warps); s2: 2 words
+__device__ __forceinline__ uint32_t tp_scan64(uint32_t v, uint32_t* s2) {
+    const int tid = threadIdx.x, lane = tid & 31;
+    uint32_t inc = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += t;
+    }
+    if (tid == 31) s2[0] = inc;
+    __syncthreads();
+    return inc - v + (tid >= 32 && tid < 64 ? s2[0] : 0u);
+}
+
+template <typename S>
+constexpr size_t tp_smem() {
+    return 2 * (TP_TILE * 8 + 32) + 2 * (TP_TILE * sizeof(S) + 32) + TP_TILE * sizeof(S) +
+           2 * TP_ND * 8 + 2 * TP_WARPS * TP_ND * 4 + 2 * 8 * TP_ND * 4 + TP_ND * 4 + 16 + 2 * 8;
+}
+
+template <typename S>
+__global__ void __launch_bounds__(TP_THREADS, 2) tp_scatter_kernel(
+    const uint64_t* __restrict__ win, uint64_t* __restrict__ wout, const S* __restrict__ sin,
+    S* __restrict__ sout, uint64_t n, const uint32_t* cntp, int shift, uint32_t dmask,
+    uint64_t omask, const uint32_t* __restrict__ H) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    constexpr uint32_t WB = TP_TILE * 8 + 32, PB = TP_TILE * sizeof(S) + 32;
+    uint64_t* const buf0 = (uint64_t*)smem;
+    uint64_t* const buf1 = (uint64_t*)(smem + WB);
+    S* const pbuf0 = (S*)(smem + 2 * WB);
+    S* const pbuf1 = (S*)(smem + 2 * WB + PB);
+    S* const s_pout = (S*)(smem + 2 * WB + 2 * PB);
+    unsigned char* q = smem + 2 * WB + 2 * PB + TP_TILE * sizeof(S);
+    q = (unsigned char*)(((uintptr_t)q + 7) & ~(uintptr_t)7);
+    int64_t* s_run = (int64_t*)q;                                         // [ND]
+    int64_t* s_goff = s_run + TP_ND;                                      // [ND]
+    uint32_t(*s_whist)[TP_ND] = (uint32_t(*)[TP_ND])(s_goff + TP_ND);     // [WARPS][ND]
+    uint32_t* s_match = &s_whist[TP_WARPS][0];                            // [WARPS][ND]
+    uint32_t(*s_part)[TP_ND] = (uint32_t(*)[TP_ND])(s_match + TP_WARPS * TP_ND);  // [16][ND]
+    uint32_t* s_w = &s_part[16][0];                                       // [4]
+    uint64_t* s_bar = (uint64_t*)(((uintptr_t)(s_w + 4) + 7) & ~(uintptr_t)7);  // [2]
+
+    const int tid = threadIdx.x, lane = tid & 31, wp = tid >> 5;
+    const uint64_t cnt = cntp ? (uint64_t)*cntp : n;
+    const uint32_t cps = gridDim.x, c = blockIdx.x;
+    const TpChunk ch = tp_chunk(cnt, cps, c);
+    const uint64_t lo = ch.lo, hi = ch.hi;
+    const uint32_t ntile = hi > lo ? (uint32_t)((hi - lo + TP_TILE - 1) / TP_TILE) : 0u;
+
+    for (int i = tid; i < 2 * TP_WARPS * TP_ND; i += TP_THREADS) (&s_whist[0][0])[i] = 0u;
+    auto issue = [&](uint32_t t, uint64_t* bar) {
+        const uint64_t g0 = lo + (uint64_t)t * TP_TILE;
+        const uint32_t ct = (uint32_t)min((uint64_t)TP_TILE, hi - g0);
+        const uint32_t bw = tp_span(win, g0, ct), bs = tp_span(sin, g0, ct);
+        mbar_expect_tx(bar, bw + bs);
+        tp_bulk((t & 1) ? buf1 : buf0, tp_base(win, g0), bw, bar);
+        tp_bulk((t & 1) ? pbuf1 : pbuf0, tp_base(sin, g0), bs, bar);
+    };
+    if (tid == 0) {
+        mbar_init(&s_bar[0], 1);
+        mbar_init(&s_bar[1], 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        for (uint32_t t = 0; t < 2 && t < ntile; ++t) issue(t, &s_bar[t]);
+    }
+    // digit totals of the pass and this chunk's prefix, from the chunk histograms:
+    // thread (part p = tid / 64, digit d = tid % 64) sums chunks p, p + 8, ...
+    {
+        const int d = tid & (TP_ND - 1), p = tid >> 6;
+        uint32_t tot = 0, pre = 0;
+        for (uint32_t cc = p; cc < cps; cc += TP_THREADS / TP_ND) {
+            const uint32_t v = H[(uint64_t)cc * TP_ND + d];
+            tot += v;
+            pre += cc < c ? v : 0u;
+        }
+        s_part[p][d] = tot;
+        s_part[8 + p][d] = pre;
+    }
+    __syncthreads();
+    uint32_t tot = 0, pre = 0;
+    if (tid < TP_ND) {
+#pragma unroll
+        for (int p = 0; p < 8; ++p) {
+            tot += s_part[p][tid];
+            pre += s_part[8 + p][tid];
+        }
+    }
+    const uint32_t dbase = tp_scan64(tid < TP_ND ? tot : 0u, s_w);
+    if (tid < TP_ND) s_run[tid] = (int64_t)dbase + pre;
+    __syncthreads();
+
+    uint32_t* whist = s_whist[wp];
+    uint32_t* mbin = s_match + wp * TP_ND;
+    const uint32_t lt = lanemask_lt();
+    for (uint32_t t = 0; t < ntile; ++t) {
+        const int b = (int)(t & 1u);
+        const uint64_t t0 = lo + (uint64_t)t * TP_TILE;
+        const uint32_t ct = (uint32_t)min((uint64_t)TP_TILE, hi - t0);
+        uint64_t* buf = b ? buf1 : buf0;
+        const S* pbuf = b ? pbuf1 : pbuf0;
+        mbar_wait(&s_bar[b], (t >> 1) & 1u);
+        const uint64_t* kin = buf + tp_delta(win, t0);
+        const S* pin = pbuf + tp_delta(sin, t0);
+        uint64_t keys[TP_ITEMS];
+        uint32_t rank[TP_ITEMS / 2];  // two 12-bit ranks per register (tile < 2^16)
+#pragma unroll
+        for (int i = 0; i < TP_ITEMS; ++i) {
+            const uint32_t idx = (uint32_t)(wp * TP_ITEMS * 32 + i * 32 + lane);
+            keys[i] = idx < ct ? kin[idx] : 0ull;
+        }
+        // stable in-warp ranking: lanes of one digit meet in a shared atomicOr mask
+#pragma unroll
+        for (int i = 0; i < TP_ITEMS; ++i) {
+            const uint32_t idx = (uint32_t)(wp * TP_ITEMS * 32 + i * 32 + lane);
+            const bool valid = idx < ct;
+            const uint32_t d = (uint32_t)(keys[i] >> shift) & dmask;
+            if (valid) atomicOr(&mbin[d], 1u << lane);
+            __syncwarp();
+            const uint32_t peers = valid ? mbin[d] : 0u;
+            const uint32_t prior = valid ? whist[d] : 0u;
+            __syncwarp();
+            if (valid && (peers & lt) == 0u) {
+                whist[d] = prior + __popc(peers);
+                mbin[d] = 0u;
+            }
+            __syncwarp();
+            const uint32_t r = prior + __popc(peers & lt);
+            rank[i / 2] = (i & 1) ? (rank[i / 2] | r << 16) : r;
+        }
+        __syncthreads();  // (A) counters final, tile read into registers
+        uint32_t tcnt = 0;
+        if (tid < TP_ND) {
+#pragma unroll
+            for (int ww = 0; ww < TP_WARPS; ++ww) tcnt += s_whist[ww][tid];
+        }
+        const uint32_t doff = tp_scan64(tcnt, s_w);
+        if (tid < TP_ND) {
+            uint32_t sum = doff;
+#pragma unroll
+            for (int ww = 0; ww < TP_WARPS; ++ww) {
+                const uint32_t v = s_whist[ww][tid];
+                s_whist[ww][tid] = sum;
+                sum += v;
+            }
+            s_goff[tid] = s_run[tid] - (int64_t)doff;
+            s_run[tid] += tcnt;
+        }
+        __syncthreads();  // (B)
+#pragma unroll
+        for (int i = 0; i < TP_ITEMS; ++i) {
+            const uint32_t idx = (uint32_t)(wp * TP_ITEMS * 32 + i * 32 + lane);
+            if (idx < ct) {
+                const uint32_t d = (uint32_t)(keys[i] >> shift) & dmask;
+                const uint32_t pos = whist[d] + ((rank[i / 2] >> (16 * (i & 1))) & 0xffffu);
+                buf[pos] = keys[i];
+                s_pout[pos] = pin[idx];
+            }
+        }
+        __syncwarp();
+#pragma unroll
+        for (int j = 0; j < TP_ND / 32; ++j) whist[j * 32 + lane] = 0u;
+        __syncthreads();  // (C) tile reordered in buf / s_pout
+        for (uint32_t j = tid; j < ct; j += TP_THREADS) {
+            const uint64_t k = buf[j];
+            const uint32_t d = (uint32_t)(k >> shift) & dmask;
+            const uint64_t dst = (uint64_t)(s_goff[d] + (int64_t)j);
+            wout[dst] = k & omask;
+            sout[dst] = s_pout[j];
+        }
+        __syncthreads();  // (D) buf, s_pout free
+        if (t + 2 < ntile && tid == 0) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            issue(t + 2, &s_bar[b]);
+        }
+    }
+}
+
+}  // namespace
+
+// Σ <= 64 (dmask < 64): the two-launch pass above; returns false when it does not
+// apply (the caller uses launch_trie_pass)
+bool trie_pass64_ok(uint32_t dmask) { return dmask < (uint32_t)TP_ND; }
+
+cudaError_t launch_trie_pass64(const uint64_t* win, uint64_t* wout, const void* sin, void* sout,
+                               bool seq16, uint64_t n, const uint32_t* cntp, int shift,
+                               uint32_t dmask, uint64_t omask, uint32_t* H, int target_ctas,
+                               cudaStream_t s) {
+    if (n == 0) return cudaGetLastError();
+    const uint64_t tiles = (n + TP_TILE - 1) / TP_TILE;
+    const unsigned cps = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(tiles, target_ctas));
+    tp_hist_kernel<<<cps, TP_THREADS, 0, s>>>(win, n, cntp, shift, dmask, H);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    if (seq16) {
+        cudaFuncSetAttribute(tp_scatter_kernel<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)tp_smem<uint16_t>());
+        tp_scatter_kernel<uint16_t><<<cps, TP_THREADS, tp_smem<uint16_t>(), s>>>(
+            win, wout, (const uint16_t*)sin, (uint16_t*)sout, n, cntp, shift, dmask, omask, H);
+    } else {
+        cudaFuncSetAttribute(tp_scatter_kernel<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)tp_smem<uint32_t>());
+        tp_scatter_kernel<uint32_t><<<cps, TP_THREADS, tp_smem<uint32_t>(), s>>>(
+            win, wout, (const uint32_t*)sin, (uint32_t*)sout, n, cntp, shift, dmask, omask, H);
+    }
+    return cudaGetLastError();
+}
+
+}  // namespace gk

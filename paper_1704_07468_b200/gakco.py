@@ -42,6 +42,7 @@ GAKCO_OPT_LEVEL_ORDER = 12
 GAKCO_OPT_LIGHT_WINDOW = 13
 GAKCO_OPT_WINDOW_MIN = 14
 GAKCO_OPT_GRAM_EACH = 15
+GAKCO_OPT_TRIE_PASS = 16
 
 EXPORTS = ("gakco_create", "gakco_set_shard", "gakco_set_option", "gakco_accumulate",
            "gakco_finalize", "gakco_kernel", "gakco_kernel_k", "gakco_kernel_rect",

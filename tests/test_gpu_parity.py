@@ -254,6 +254,8 @@ def test_sort_modes_ragged(gk, oracle_lib):
     for bk in (0, 50001, 4097 * 3):
         for mode in (0, 1, 3, 4, 5, 6, 7):
             assert_parity(run(gk, cp, 8, 4, 4, batch_keys=bk, sort=mode), ref)
+        # the mask trie on the generic 8-bit radix pass instead of trie.cu's
+        assert_parity(run(gk, cp, 8, 4, 4, batch_keys=bk, sort=6, trie_pass=0), ref)
     cp4 = sc.from_sequences(4, [rng.integers(0, 4, size=int(rng.integers(0, 5000)))
                                 for _ in range(23)])
     ref4 = oracle_lib.compute(cp4, 6, 3, 3)
@@ -279,6 +281,7 @@ def test_grouping_modes(gk, oracle_lib):
         for mode in (0, 1, 2, 3, 4, 5, 6, 7):
             r = run(gk, cp, g, k, M, sort=mode)
             assert_parity(r, ref)
+        assert_parity(run(gk, cp, g, k, M, sort=6, trie_pass=0), ref)
             if r["stats"]["keys"] > 0:
                 assert r["stats"]["grouping"] == {6: 3, 7: 4}.get(mode, mode if mode < 3 else 0)
         r = run(gk, cp, g, k, M)
@@ -471,24 +474,89 @@ def _golden(name):
         return json.load(f)
 
 
-@pytest.mark.parametrize("name", ["tiny", "dna", "protein"])
+def _check_digests(name, r, which=None):
+    """Every C_m, N_m and K of r (device tensors) against the committed oracle
+    digests (digests taken on the device, tests/digest_gpu.py); Knorm against the
+    oracle's normalisation of the verified K (1e-12, diagonal exact)."""
+    from tests.digest_gpu import digest_torch
+    gold = _golden(name)
+    cfg = sc.CONFIGS[name]
+    d = gold["digests"]
+    for m in range(cfg.M + 1):
+        if which is None or "C" in which:
+            assert digest_torch(r["C"][m]) == int(d[f"C{m}"]), f"{name} C{m}"
+        if r.get("Nm") is not None and (which is None or "Nm" in which):
+            assert digest_torch(r["Nm"][m]) == int(d[f"N{m}"]), f"{name} N{m}"
+    assert digest_torch(r["K"]) == int(d["K"]), f"{name} K"
+    if r.get("Knorm") is not None:
+        _knorm_from_k(r["K"], r["Knorm"])
+
+
+def _knorm_from_k(K, Kn):
+    """Reading A5 recomputed from the verified K on the device in fp64 with the
+    oracle's formula (K / sqrt(Kxx * Kyy), 0 when a diagonal is 0, diagonal 1)
+    and compared at 1e-12 relative, row blocks at a time."""
+    kd = K.diagonal().to(torch.float64)
+    N = K.shape[0]
+    for r0 in range(0, N, 2048):
+        kb = K[r0:r0 + 2048].to(torch.float64)
+        a = kd[r0:r0 + 2048, None]
+        ref = kb / torch.sqrt(a * kd[None, :])
+        ref = torch.where((a > 0) & (kd[None, :] > 0), ref, torch.zeros_like(ref))
+        got = Kn[r0:r0 + 2048]
+        assert torch.allclose(got, ref, rtol=KNORM_RTOL, atol=0)
+    dg = Kn.diagonal()
+    assert torch.equal(dg, torch.where(kd > 0, torch.ones_like(dg), torch.zeros_like(dg)))
+
+
+def test_digest_gpu_matches_numpy(gk):
+    """tests/digest_gpu.py (device) == tests/refs.digest_np (numpy restatement)."""
+    from tests.digest_gpu import digest_torch
+    rng = np.random.default_rng(3)
+    a = rng.integers(-2 ** 62, 2 ** 62, size=(301, 257)).astype(np.int64)
+    b = rng.random((129, 77))
+    assert digest_torch(torch.from_numpy(a).cuda()) == refs.digest_np(a)
+    assert digest_torch(torch.from_numpy(b).cuda()) == refs.digest_np(b)
+
+
+@pytest.mark.parametrize("name", ["tiny", "dna", "protein", "text", "scale"])
 def test_full_config_digests(gk, name):
-    """Full-size configs (bench's launch configuration) against the oracle's
-    committed digests (written by oracle/make_digests.py)."""
+    """All five BASELINE.json configs at full size, in bench's launch configuration
+    (default options), against the oracle's committed digests of every output
+    matrix (tests/golden/oracle_<name>.json, written by oracle/make_digests.py)."""
     gold = _golden(name)
     cfg = sc.CONFIGS[name]
     cp = sc.make(name)
     assert cp.sha256() == gold["corpus_sha256"], "generator drifted"
     r = gk.kernel_matrix(cp.codes, cp.offsets, cfg.sigma, cfg.g, cfg.k, cfg.M)
-    d = gold["digests"]
-    for m in range(cfg.M + 1):
-        assert refs.digest_np(r["C"][m].cpu().numpy()) == int(d[f"C{m}"]), f"C{m}"
-        assert refs.digest_np(r["Nm"][m].cpu().numpy()) == int(d[f"N{m}"]), f"N{m}"
-    K = r["K"].cpu().numpy()
-    assert refs.digest_np(K) == int(d["K"])
-    # Knorm: reference recomputed from the verified K with the oracle's formula
-    import oracle
-    assert_knorm(r["Knorm"].cpu().numpy(), oracle.normalize(K))
+    _check_digests(name, r)
+    del r
+    torch.cuda.empty_cache()
+
+
+@pytest.mark.parametrize("name,opts", [
+    ("text", {"sort": 0}), ("text", {"heavy_min_seqs": 1 << 50}),
+    ("scale", {"light_relabel": 0, "light_window": 0}), ("scale", {"sort": 0}),
+    ("scale", {"heavy_min_seqs": 1 << 50, "light_window": 0}),
+])
+def test_large_config_paths_digests(gk, name, opts):
+    """Text / Scale at full size through the non-default paths (LSD sort instead of
+    the mask trie, no relabelling / window Gram, all-light) against the same
+    committed oracle digests of C_m and K: a bug confined to one path's windows,
+    tiles or batches shows up here."""
+    cfg = sc.CONFIGS[name]
+    cp = sc.make(name)
+    plan = gk.Plan(cfg.sigma, cfg.g, cfg.k, cfg.M)
+    for opt, val in opts.items():
+        plan.set_option(getattr(gk, "GAKCO_OPT_" + opt.upper()), val)
+    N = cp.n_seq
+    C = torch.zeros((cfg.M + 1, N, N), dtype=torch.int64, device="cuda")
+    K = torch.empty((N, N), dtype=torch.int64, device="cuda")
+    plan.kernel(cp.codes, cp.offsets, N, C, None, K, None)
+    plan.close()
+    _check_digests(name, {"C": C, "K": K}, which=("C",))
+    del C, K
+    torch.cuda.empty_cache()
 
 
 def test_dna_digests_hash_grouping(gk):
@@ -692,3 +760,26 @@ def test_sharded_step_two_ranks_one_gpu(gk, oracle_lib, tmp_path):
     rc = parallel.launch(2, os.path.join(root, "tests", "dist_worker.py"), [str(res), "gpu"])
     assert rc == 0
     assert res.read_text().startswith("ok"), res.read_text()
+
+
+def test_k_sweep_parity(gk, oracle_lib):
+    """NEXT-3, reduced k-sweep (Fig. 4 shape): g = 10, M = g - k =
+    1..9 (up to 1013 masks) on a DNA-like and a Zipf text-like corpus of 300
+    sequences of length 100. The oracle's Hamming histograms are computed once per
+    corpus with M = g; each point's expected C_m (Eq. 8), N_m, K (Eq. 7) and Knorm
+    follow from them; full path and K-only path must match."""
+    g = 10
+    for cp in (sc.uniform(300, 100, 4, 21), sc.gen_text(22, 300, 100, 100)):
+        hist = oracle_lib.profiles(cp, g, g)
+        for M in range(1, g):
+            k = g - M
+            nm = np.ascontiguousarray(hist[: M + 1])
+            ref = {"Nm": nm, "C": oracle_lib.cumulative(nm, g), "K": oracle_lib.kernel(nm, g, k)}
+            ref["Knorm"] = oracle_lib.normalize(ref["K"])
+            assert_parity(run(gk, cp, g, k, M), ref)
+            N = cp.n_seq
+            K = torch.empty((N, N), dtype=torch.int64, device="cuda")
+            plan = gk.Plan(cp.sigma, g, k, M)
+            plan.kernel_k(cp.codes, cp.offsets, N, K, None)
+            plan.close()
+            assert np.array_equal(K.cpu().numpy(), ref["K"])

@@ -10,11 +10,15 @@
 
 Every point: the full path through gakco_kernel (C_m, N_m, K, Knorm on the
 device; CUDA events, 1 warm-up + median of 3), and the K-only path (NEXT-1)
-where M >= g-k. The CPU oracle (oracle/, all host cores) is timed beside the
-GPU at N <= 750 of the N-sweep and once per k-sweep corpus (its direct Hamming
-count does not depend on M). Synthetic inputs only (synth/corpus.py); the paper's
-datasets are not in the container. Numbers are context for the paper's shapes,
-not bench lines.
+where M >= g-k. Every point is also PARITY-CHECKED: the oracle's Hamming
+histograms are computed once per corpus with M = g (their cost does not depend
+on M), and each point's expected C_m (Eq. 8), N_m, K (Eq. 7) and Knorm come from
+them through oracle.cumulative / oracle.kernel / oracle.normalize; the GPU
+outputs (full path and K-only) must be equal (Knorm within 1e-12), and each point
+records `parity: true/false`. The oracle is timed beside the GPU at N <= 750 of
+the N-sweep and once per k-sweep corpus. Synthetic inputs only
+(synth/corpus.py); the paper's datasets are not in the container. Numbers are
+context for the paper's shapes, not bench lines.
 """
 import argparse
 import json
@@ -65,12 +69,41 @@ def time_gpu(gk, torch, cp, g, k, M, reps=3):
 
     full = run(lambda: plan.kernel(codes, offs, N, C, Nm, K, Kn, stream=s))
     st = plan.stats()
+    outs = {"C": C.cpu().numpy(), "Nm": Nm.cpu().numpy(), "K": K.cpu().numpy(),
+            "Knorm": Kn.cpu().numpy()}
     konly = None
     if M >= g - k:
         konly = run(lambda: plan.kernel_k(codes, offs, N, K, Kn, stream=s))
+        outs["K_only"] = K.cpu().numpy()
+        outs["Knorm_only"] = Kn.cpu().numpy()
     plan.close()
     return {"ms": full, "k_only_ms": konly, "masks": int(st["masks"]), "keys": int(st["keys"]),
-            "light_pairs": int(st["light_pairs"]), "heavy_macs": int(st["heavy_macs"])}
+            "light_pairs": int(st["light_pairs"]), "heavy_macs": int(st["heavy_macs"])}, outs
+
+
+def oracle_hist(cp, g, Mmax=None):
+    """N_m(X,Y) for m = 0..Mmax (default g; Def. 1 / Eq. 5), once per corpus (the
+    direct Hamming count's cost does not depend on M)."""
+    import oracle
+    oracle.build()
+    return oracle.profiles(cp, g, g if Mmax is None else Mmax)
+
+
+def parity(hist, g, k, M, outs):
+    """The point's expected outputs from the oracle histograms (Eq. 8, Eq. 7, reading
+    A5) against the GPU's; True iff all equal (Knorm within 1e-12 relative)."""
+    import oracle
+    nm = np.ascontiguousarray(hist[: M + 1])
+    C = oracle.cumulative(nm, g)
+    K = oracle.kernel(nm, g, k)
+    Kn = oracle.normalize(K)
+    ok = (np.array_equal(outs["C"], C) and np.array_equal(outs["Nm"], nm)
+          and np.array_equal(outs["K"], K)
+          and np.allclose(outs["Knorm"], Kn, rtol=1e-12, atol=0))
+    if "K_only" in outs:
+        ok = ok and np.array_equal(outs["K_only"], K) and np.allclose(
+            outs["Knorm_only"], Kn, rtol=1e-12, atol=0)
+    return bool(ok)
 
 
 def time_oracle(cp, g, k, M):
@@ -95,11 +128,13 @@ def main():
         cp = gen(2000 if not a.quick else 300, 100, 11)
         Ms = range(1, gk_g) if not a.quick else (1, gk_g - 1)
         ora = time_oracle(cp, gk_g, gk_g - 1, 1) if not a.quick else None
+        hist = oracle_hist(cp, gk_g)
         for M in Ms:
             k = gk_g - M
-            r = time_gpu(gk, torch, cp, gk_g, k, M)
+            r, outs = time_gpu(gk, torch, cp, gk_g, k, M)
             r.update({"alphabet": name, "sigma": sigma, "N": cp.n_seq, "l": 100, "g": gk_g,
-                      "k": k, "M": M, "oracle_ms_any_M": ora})
+                      "k": k, "M": M, "oracle_ms_any_M": ora,
+                      "parity": parity(hist, gk_g, k, M, outs)})
             out["k_sweep"].append(r)
             print(json.dumps(r), flush=True)
     Ns = (100, 250, 500, 750, 1500, 3000, 6000) if not a.quick else (100, 500)
@@ -107,9 +142,10 @@ def main():
         for N in Ns:
             cp = gen(N, 100, 12)
             M = g - k
-            r = time_gpu(gk, torch, cp, g, k, M)
+            r, outs = time_gpu(gk, torch, cp, g, k, M)
             r.update({"alphabet": name, "sigma": sigma, "N": N, "l": 100, "g": g, "k": k, "M": M,
-                      "oracle_ms": time_oracle(cp, g, k, M) if N <= 750 else None})
+                      "oracle_ms": time_oracle(cp, g, k, M) if N <= 750 else None,
+                      "parity": parity(oracle_hist(cp, g, M), g, k, M, outs)})
             out["n_sweep"].append(r)
             print(json.dumps(r), flush=True)
     with open(a.out, "w") as f:
@@ -117,17 +153,19 @@ def main():
     # markdown summary next to the JSON
     md = [f"# NEXT-3 sweeps (GPU full path; oracle on {out['host_cores']} host cores)", "",
           "## k-sweep (Fig. 4 shape): N=2000, l=100", "",
-          "| alphabet | g | k | M | masks | GPU ms | K-only ms | oracle ms (any M) |",
-          "|---|---|---|---|---|---|---|---|"]
+          "| alphabet | g | k | M | masks | GPU ms | K-only ms | oracle ms (any M) | parity |",
+          "|---|---|---|---|---|---|---|---|---|"]
     for r in out["k_sweep"]:
         md.append(f"| {r['alphabet']} | {r['g']} | {r['k']} | {r['M']} | {r['masks']} | "
                   f"{r['ms']:.2f} | {r['k_only_ms'] if r['k_only_ms'] is None else round(r['k_only_ms'], 2)} | "
-                  f"{r['oracle_ms_any_M'] if r['oracle_ms_any_M'] is None else round(r['oracle_ms_any_M'])} |")
+                  f"{r['oracle_ms_any_M'] if r['oracle_ms_any_M'] is None else round(r['oracle_ms_any_M'])} | "
+                  f"{'bit-exact' if r['parity'] else 'MISMATCH'} |")
     md += ["", "## N-sweep (Fig. 5(c) shape): l=100", "",
-           "| alphabet | g | k | N | GPU ms | oracle ms |", "|---|---|---|---|---|---|"]
+           "| alphabet | g | k | N | GPU ms | oracle ms | parity |", "|---|---|---|---|---|---|---|"]
     for r in out["n_sweep"]:
         md.append(f"| {r['alphabet']} | {r['g']} | {r['k']} | {r['N']} | {r['ms']:.2f} | "
-                  f"{'-' if r['oracle_ms'] is None else round(r['oracle_ms'])} |")
+                  f"{'-' if r['oracle_ms'] is None else round(r['oracle_ms'])} | "
+                  f"{'bit-exact' if r['parity'] else 'MISMATCH'} |")
     with open(os.path.splitext(a.out)[0] + ".md", "w") as f:
         f.write("\n".join(md) + "\n")
 
