@@ -48,8 +48,10 @@ typedef enum {
     GAKCO_OK = 0,
     GAKCO_E_ARG = 1,       /* invalid parameter, pointer or shape */
     GAKCO_E_SYMBOL = 2,    /* a code >= sigma in the corpus */
-    GAKCO_E_RANGE = 3,     /* key+seq id do not fit 64 bits, a segment of more than
-                              2^30 g-mers, or a C_m entry bound overflows int64 */
+    GAKCO_E_RANGE = 3,     /* key+seq id do not fit 64 bits, more than 2^30 g-mers in the
+                              corpus, a sequence with more than 65535 g-mers (the light
+                              path's u32 pair sums need n_X * n_Y < 2^32), or a C_m / K
+                              entry bound (C(g,m) n_max^2) overflows int64 */
     GAKCO_E_NOMEM = 4,     /* device allocation failed */
     GAKCO_E_CUDA = 5,      /* a CUDA runtime error */
     GAKCO_E_INTERNAL = 6   /* a failed invariant (negative N_m, K != C_{g-k}) */
@@ -62,8 +64,11 @@ typedef enum {
                                      a huge value = never (all light); 2 = all heavy */
     GAKCO_OPT_BATCH_KEYS = 2,     /* max keys (masks x g-mers) per batch; 0 = auto */
     GAKCO_OPT_TIMING = 3,         /* 1 = record per-stage CUDA events (gakco_get_stats) */
-    GAKCO_OPT_SORT = 4,           /* grouping of masked keys: -1 = automatic (default; = 3,
-                                     measured fastest), 0 = LSD radix sort,
+    GAKCO_OPT_SORT = 4,           /* grouping of masked keys: -1 = automatic (default): the
+                                     mask trie (6) when a mask has >= 2M g-mers and
+                                     g*ceil(log2 sigma) <= 64, else the batched mask trie (7)
+                                     when the one-word composite fits 64 bits, else the
+                                     chunked LSD v2 (3); 0 = LSD radix sort,
                                      chunked two-kernel passes (v1), 1 = LSD onesweep with
                                      decoupled look-back, 2 = hash partition + shared-memory
                                      hash grouping (falls back to the LSD sort where it does

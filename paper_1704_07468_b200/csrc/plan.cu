@@ -20,6 +20,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "internal.cuh"
 
 using namespace gk;
@@ -32,6 +34,12 @@ struct DevBuf {
 };
 
 enum Stage { S_ENCODE = 0, S_SORT, S_SEGMENT, S_LIGHT, S_HEAVY, S_EPILOGUE, S_DENSE, S_NSTAGE };
+
+// NVTX range for profilers (nsys / ncu --nvtx): host-side enqueue of one phase
+struct Nvtx {
+    explicit Nvtx(const char* name) { nvtxRangePushA(name); }
+    ~Nvtx() { nvtxRangePop(); }
+};
 
 struct DeviceGuard {
     int prev = -1;
@@ -77,9 +85,10 @@ struct gakco_plan {
     int rank = 0, world = 1;
     int64_t heavy_min = 0, batch_keys = 0;
     bool timing = false;
-    // grouping: -1 auto (chunked LSD),
-    // 0 chunked two-kernel LSD pass, 1 onesweep LSD (decoupled look-back),
-    // 2 hash partition + shared-memory hash grouping (bucket.cu)
+    // grouping (GAKCO_OPT_SORT): -1 auto = mask trie (6) for masks of >= 2M g-mers,
+    // else the batched mask trie (7) where the one-word composite fits, else chunked
+    // LSD v2 (3); 0 chunked two-kernel LSD pass, 1 onesweep LSD (decoupled look-back),
+    // 2 hash partition + shared-memory hash grouping (bucket.cu), 3-5 LSD v2 variants
     int sort_mode = -1;
     int sort_ctas_per_sm = 4;  // chunked pass grid = this x SMs (2 resident: 2 full waves; measured best of 2..4)
     int trie_ctas_per_sm = 2;  // trie passes (one mask each): one full wave (Text sort 91 -> 76 ms vs 4)
@@ -1130,6 +1139,7 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
     int64_t fp4_used = 0;  // levels whose Gram ran on e2m1
     auto flush = [&]() -> gakco_status {
         if (dense_m < 0 || dense_bound == 0) return GAKCO_OK;
+        Nvtx nv("gram flush");
         if (pipe) {  // every build of this slot (s2) precedes its Gram (s3)
             CK(cudaEventRecord(p->ev_build, s2));
             CK(cudaStreamWaitEvent(s3, p->ev_build, 0));
@@ -1233,6 +1243,7 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
         CK(cudaStreamSynchronize(s));  // io is a local buffer
     }
     auto make_perm = [&](int m_done) -> gakco_status {
+        Nvtx nv("relabel");
         CK(cudaStreamSynchronize(s2));  // C of level m_done complete (light + Gram flushes)
         CK(cudaStreamSynchronize(s3));
         cudaEvent_t ar = nullptr;
@@ -1282,6 +1293,7 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
     };
     auto lflush = [&]() -> gakco_status {
         if (light_m < 0 || light_masks == 0) return GAKCO_OK;
+        Nvtx nv("light flush");
         cudaEvent_t al = nullptr;
         p->stage_begin(s2, &al);
         if (rect)
@@ -1338,6 +1350,9 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
         size_t end = pos;
         while (end < mine.size() && p->mask_level[mine[end]] == m && end - pos < bmax_masks) ++end;
         const int nmask = (int)(end - pos);
+        char nvname[64];
+        std::snprintf(nvname, sizeof nvname, "batch m=%d masks=%d", m, nmask);
+        Nvtx nvb(nvname);
         const int kb = p->key_bits[m];
         const int npass = (kb + RADIX_BITS - 1) / RADIX_BITS;
         int64_t* Cm = level_ptr(m);
@@ -1813,6 +1828,7 @@ extern "C" gakco_status gakco_accumulate(gakco_plan* p, const uint8_t* codes,
                                          void* stream) {
     if (!p) return GAKCO_E_ARG;
     DeviceGuard dg(p->device);
+    Nvtx nv("gakco_accumulate");
     return accumulate_impl(p, codes, offsets, N, C, (cudaStream_t)stream, p->rank, p->world);
 }
 
@@ -1891,6 +1907,7 @@ extern "C" gakco_status gakco_finalize(gakco_plan* p, int64_t* C, int64_t N, int
                                        int64_t* K, double* Knorm, void* stream) {
     if (!p) return GAKCO_E_ARG;
     DeviceGuard dg(p->device);
+    Nvtx nv("gakco_finalize");
     return finalize_impl(p, C, N, Nm, K, Knorm, (cudaStream_t)stream, false);
 }
 
@@ -2127,6 +2144,7 @@ extern "C" gakco_status gakco_finalize_packed(gakco_plan* p, const void* Cp, int
         if (o && end > begin && !is_device_ptr(o))
             return p->fail(GAKCO_E_ARG, "outputs must be device pointers");
     DeviceGuard dg(p->device);
+    Nvtx nv("gakco_finalize_packed");
     cudaStream_t s = (cudaStream_t)stream;
 #define CK(x)                                               \
     do {                                                    \

@@ -29,7 +29,11 @@ namespace gk {
 template <typename K, bool KM = false>
 struct SegComp {
     using E = K;
-    static constexpr int kMinBlocks = sizeof(K) == 4 ? 7 : 5;  // (u64: 64 registers, no spills)
+    // CTAs per SM the register budget is sized for: u32 7 (32 registers; ptxas spills
+    // 68-84 B per thread), u64 5 (48 registers; 24-52 B spilled). The spills stay in
+    // L1 and these budgets measured faster on DNA / Protein (segment 0.95 -> 0.90 ms)
+    // than the spill-free 4 CTAs/SM of abdb978.
+    static constexpr int kMinBlocks = sizeof(K) == 4 ? 7 : 5;
     const K* keys;
     int sb;
     const uint64_t* km;  // per segment: key bits << sb | seq bits (nullptr: keys masked)

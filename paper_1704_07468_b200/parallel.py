@@ -126,6 +126,9 @@ class ShardedStep:
             self.dist.all_reduce(h, group=self.group)
             t.copy_(h)
 
+    def _nvtx(self, name):
+        return self.torch.cuda.nvtx.range(name) if self.cuda else contextlib.nullcontext()
+
     def _on_comm(self):
         return self.torch.cuda.stream(self.comm) if self.cuda else contextlib.nullcontext()
 
@@ -136,7 +139,7 @@ class ShardedStep:
         C.zero_()
         plan.accumulate(codes, offsets, N, C, stream)
         cs = self.comm
-        with self._on_comm():
+        with self._on_comm(), self._nvtx("sharded exchange + slice epilogue"):
             for m in plan.level_order():
                 plan.stream_wait_level(m, cs)
                 plan.pack_upper(C[m], N, 1, 0, self.T, self.pack[m], self.wb, cs)

@@ -113,6 +113,32 @@ def test_heavy_light_equivalence(gk, oracle_lib):
         assert_parity(run(gk, cp, g, k, M), ref)
 
 
+def test_e2m1_gram_large_sums(gk, oracle_lib):
+    """ADVICE r01: the e2m1 Gram (tcgen05 kind::mxf4, f32 accumulators) is exact only
+    if the tensor core keeps every bit of sums up to 2^24 within one flush. Here the
+    per-cell sums of one flush reach ~2^20 with every count <= 4: four copies of a
+    period-16 sequence (n = 64 g-mers, each masked key 4 times per sequence),
+    g = 16, M = 6 (level 6: 8008 masks, flushes of (2^24 - 1) / 64^2 = 4095 masks,
+    each adding up to 16 keys * 4 * 4 = 256 per mask and cell). e2m1 forced ==
+    u8 / s32 == oracle."""
+    rng = np.random.default_rng(141)
+    period = list(rng.integers(0, 4, 16))
+    rep = (period * 6)[:79]
+    seqs = [rep] * 4 + [list(rng.integers(0, 4, 79)) for _ in range(4)]
+    cp = sc.from_sequences(4, seqs)
+    g, k, M = 16, 10, 6
+    ref = oracle_lib.compute(cp, g, k, M)
+    # the premise: one flush of level 6 carries a cell sum near 2^20
+    assert ref["C"][6, 0, 1] - ref["C"][5, 0, 1] > 0
+    r4 = run(gk, cp, g, k, M, heavy_min_seqs=2, gram_fp4=1)
+    assert r4["stats"]["gram_fp4"] == (1 << (M + 1)) - 1
+    assert r4["stats"]["heavy_macs_fp4"] > 0
+    assert_parity(r4, ref)
+    assert_parity(run(gk, cp, g, k, M, heavy_min_seqs=2, gram_fp4=0), ref)
+    # the largest single-level cell value (a bound on any flush's partial sum there)
+    assert ref["C"][6, 0, 1] > (1 << 20)
+
+
 def _fp4_levels(cp, g, M):
     """The documented auto policy (include/gakco.h GAKCO_OPT_GRAM_FP4): level m uses
     e2m1 when n_max * p_max^(g-m) <= 1/8."""
@@ -281,9 +307,9 @@ def test_grouping_modes(gk, oracle_lib):
         for mode in (0, 1, 2, 3, 4, 5, 6, 7):
             r = run(gk, cp, g, k, M, sort=mode)
             assert_parity(r, ref)
-        assert_parity(run(gk, cp, g, k, M, sort=6, trie_pass=0), ref)
             if r["stats"]["keys"] > 0:
                 assert r["stats"]["grouping"] == {6: 3, 7: 4}.get(mode, mode if mode < 3 else 0)
+        assert_parity(run(gk, cp, g, k, M, sort=6, trie_pass=0), ref)
         r = run(gk, cp, g, k, M)
         if r["stats"]["keys"] > 0:  # auto: the batched trie where one word holds the composite
             bits = max(1, int(np.ceil(np.log2(max(sigma, 2)))))
