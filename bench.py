@@ -76,6 +76,10 @@ def args_():
                     help="0: levels m = 0..M (default), 1: m = M..0")
     ap.add_argument("--gram-pair", type=int, default=None, choices=[0, 1],
                     help="heavy Gram kernel: 1 CTA pairs (default), 0 one SM per tile")
+    ap.add_argument("--far-near", type=int, default=None,
+                    help="far-pair records from this label distance (-1 auto, 0 off)")
+    ap.add_argument("--trie-pass", type=int, default=None, choices=[0, 1],
+                    help="mask-trie pass kernel: 1 symbol-digit (trie.cu), 0 generic radix")
     ap.add_argument("--no-timing", action="store_true",
                     help="no per-stage events (roofline then uses the last timed stages)")
     return ap.parse_args()
@@ -95,6 +99,33 @@ def peaks():
                 "bf16_tflops_sustained": d.get("bf16_tflops_sustained"), "source": "measured"}
     return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0,
             "source": "fallback"}
+
+
+def red_peaks():
+    """Measured random u32 RED ceilings (tools/measure_peaks.py -> profiles/peaks_r02.json):
+    G updates/s into an L2-resident (32 MB) and a DRAM-resident (800 MB) array."""
+    p = os.path.join(ROOT, "profiles", "peaks_r02.json")
+    if not os.path.exists(p):
+        return None
+    with open(p) as f:
+        d = json.load(f)
+    out = {"source": "measured (tools/measure_peaks.py, profiles/peaks_r02.json)"}
+    for r in d.get("red", []):
+        if r["pattern"] == "random cells":
+            out["l2" if r["array_MB"] <= 64 else "dram"] = r["G_updates_per_s"]
+    out["int8_tops"] = d.get("int8_gemm", {}).get("TOPS")
+    out["fp4_tflops"] = d.get("fp4_gemm", {}).get("TFLOPS")
+    return out
+
+
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
 
 
 def workload(cfg_name):
@@ -222,7 +253,7 @@ def run_reference(a):
            "data": "synthetic",
            "config": config_dict(a.config, cfg, cp, masks, n, 1),
            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "oracle",
-                            "sample": sample},
+                            "cpu": cpu_model(), "sample": sample},
            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0,
                    "d2h_bytes_per_step": 0}}
     print(json.dumps(out), flush=True)
@@ -339,6 +370,10 @@ def run_ours(a):
         plan.set_option(gakco.GAKCO_OPT_LEVEL_ORDER, a.level_order)
     if a.gram_pair is not None:
         plan.set_option(gakco.GAKCO_OPT_GRAM_PAIR, a.gram_pair)
+    if a.far_near is not None:
+        plan.set_option(gakco.GAKCO_OPT_FAR_NEAR, a.far_near)
+    if a.trie_pass is not None:
+        plan.set_option(gakco.GAKCO_OPT_TRIE_PASS, a.trie_pass)
     C = torch.zeros((M + 1, N, N), dtype=torch.int64, device=dev)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device=dev)
     stream = torch.cuda.current_stream(dev)
@@ -515,11 +550,26 @@ def run_ours(a):
         "sort": "shared-memory ranking latency and bank conflicts (ncu: 27% of HBM)",
     }
 
+    rp = red_peaks()
+
     def roof_of(st):
         b_, algo_ = model[st]
         t_ = per_step[st] / 1e3
         nl_ = max(1, int(last.get("n_" + st, 0) or 1))
         traffic_ = tr.get(st, {}).get("dram_bytes_per_launch_mean")
+        if st == "light" and rp and rp.get("l2"):
+            # the light updates are L2 atomics (REDs): achieved pair updates/s against
+            # the measured random-RED ceiling into an L2-resident array (the near pairs;
+            # far pairs go through records); the DRAM-resident ceiling is
+            # what unrelabelled / record-less REDs into a triangle beyond L2 get
+            ups = float(last["light_pairs"]) / t_ / 1e9 if t_ > 0 else 0.0
+            return {"bound": "l2_atomics", "kernel": st, "achieved": ups, "peak": rp["l2"],
+                    "unit": "G updates/s", "frac": ups / rp["l2"], "traffic": traffic_,
+                    "algorithmic_updates_per_launch": float(last["light_pairs"]) / nl_,
+                    "launches_per_step": nl_, "avg_launch_ms": per_step[st] / nl_,
+                    "dram_resident_red_peak": rp.get("dram"),
+                    "far_records": int(last.get("far_records", 0)),
+                    "peak_source": rp["source"] + ": random u32 RED into 32 MB"}
         if b_ == "hbm":
             ach = algo_ / t_ / 1e9 if t_ > 0 else 0.0
             r = {"bound": "hbm", "kernel": st, "achieved": ach, "peak": pk["hbm_gbs"],
@@ -535,17 +585,40 @@ def run_ours(a):
             f4 = float(last.get("heavy_macs_fp4", 0) or 0) / macs if macs > 0 else 0.0
             ratio = 1.0 / (f4 / 4.0 + (1.0 - f4) / 2.0)
             peak_ = pk["bf16_tflops"] * ratio
+            src_ = pk["source"] + " bf16_tflops x %.3g (e2m1 x4, int8 x2 nominal ratios, " \
+                                  "weighted by the MAC mix)" % ratio
+            if rp and rp.get("int8_tops") and rp.get("fp4_tflops"):
+                # measured library GEMM peaks for the two operand types (cuBLASLt int8,
+                # cuBLAS nvfp4), mixed by the MAC share
+                peak_ = 1.0 / (f4 / rp["fp4_tflops"] + (1.0 - f4) / rp["int8_tops"])
+                src_ = ("measured cuBLASLt int8 %.0f TOPS / nvfp4 %.0f TFLOPS "
+                        "(profiles/peaks_r02.json), weighted by the MAC mix"
+                        % (rp["int8_tops"], rp["fp4_tflops"]))
             r = {"bound": "tensor", "kernel": st, "achieved": ach, "peak": peak_,
                  "unit": "TFLOP/s", "frac": ach / peak_, "traffic": traffic_,
                  "algorithmic_ops_per_launch": algo_ / nl_, "launches_per_step": nl_,
                  "avg_launch_ms": per_step[st] / nl_, "e2m1_mac_share": round(f4, 4),
-                 "peak_source": pk["source"] + " bf16_tflops x %.3g (e2m1 x4, int8 x2 nominal "
-                                               "ratios, weighted by the MAC mix)" % ratio}
+                 "peak_source": src_}
         if st in limiter:
             r["limiter"] = limiter[st]
         return r
 
     roof = roof_of(dom)
+    # SURVEY §8(d) headline: encode + sort + segment against HBM at the algorithmic
+    # floor of 38-44 B per masked key (encode write 8, one sort read + write 16,
+    # segment read 8, triple write 6-12)
+    ess_ms = sum(per_step.get(k_, 0.0) for k_ in ("encode", "sort", "segment"))
+    keys_ = float(last["keys"])
+    hbm_headline = None
+    if ess_ms > 0:
+        lo_, hi_ = 38.0 * keys_ / (ess_ms / 1e3) / 1e9, 44.0 * keys_ / (ess_ms / 1e3) / 1e9
+        hbm_headline = {"floor_bytes_per_key": [38, 44], "keys": keys_,
+                        "ms_encode_sort_segment": ess_ms,
+                        "achieved_gbs": [lo_, hi_], "peak_gbs": pk["hbm_gbs"],
+                        "frac": [lo_ / pk["hbm_gbs"], hi_ / pk["hbm_gbs"]],
+                        "target_frac": 0.6,
+                        "model_bytes_gbs": sum(model[k_][1] for k_ in ("encode", "sort", "segment")
+                                               if model[k_][0] == "hbm") / (ess_ms / 1e3) / 1e9}
     roof["stage_times"] = ("single-stream profiling steps (pipeline off), CUDA events on the "
                            "launching stream; the timed steps overlap stages on two streams")
     others = {st: roof_of(st) for st in ("heavy", "sort", "light", "segment", "encode")
@@ -557,6 +630,7 @@ def run_ours(a):
            "scaling": "strong", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
            "config": config_dict(a.config, cfg, cp, masks, n, world),
            "roofline": roof, "roofline_other_stages": others, "stages": stages,
+           "hbm_headline_encode_sort_segment": hbm_headline,
            "gpu_launches": int(launches),
            "clocks": clocks, "e2e": e2e, "k_only": k_only,
            "counters": {k: v for k, v in last.items() if not k.startswith("ms_")}}
@@ -567,6 +641,7 @@ def run_ours(a):
         dt, frac, r = oracle_sample(cp, cfg, a.cpu_seconds, threads)
         out["cpu_baseline"] = {
             "value": masks * n / (dt / frac), "unit": UNIT, "cores": threads, "kind": "oracle",
+            "cpu": cpu_model(),
             "sample": f"oracle rows [0,{r}) x all Y>=X ({100 * frac:.2f}% of the upper-triangle "
                       f"pair work, {dt:.1f} s), extrapolated to the full matrix by pair work"}
     print(json.dumps(out), flush=True)

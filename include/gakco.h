@@ -126,10 +126,16 @@ typedef enum {
     GAKCO_OPT_GRAM_EACH = 15,     /* 1: the heavy-group Gram runs after every batch (overlapping
                                      the next batch) instead of when a level ends or D fills;
                                      0 (default) */
-    GAKCO_OPT_TRIE_PASS = 16      /* mask-trie pass kernel: 1 (default) = the symbol-digit pass
+    GAKCO_OPT_TRIE_PASS = 16,     /* mask-trie pass kernel: 1 (default) = the symbol-digit pass
                                      (<= 64 buckets, chunk prefixes inside the scatter: two
                                      launches) where sigma <= 64; 0 = the generic 8-bit radix
                                      pass (hist + chunk scan + scatter) */
+    GAKCO_OPT_FAR_NEAR = 17       /* far-pair records of the light path: once the accumulator is
+                                     relabelled and larger than 96 MB, a pair whose labels are
+                                     >= this far apart (random cross-cluster matches, whose cells
+                                     miss L2) is appended as a record and added per accumulator
+                                     block after its batch (L2-resident) instead of a RED into
+                                     DRAM. -1 = automatic (default: 256), 0 = off (all REDs) */
 } gakco_option;
 
 /* Counters of the last gakco_accumulate (algorithmic units). */
@@ -160,6 +166,7 @@ typedef struct {
     int64_t heavy_macs_fp4; /* the part of heavy_macs issued as e2m1 (kind::mxf4) */
     int64_t win_groups;     /* light groups sent to the window Gram (GAKCO_OPT_LIGHT_WINDOW) */
     int64_t win_macs;       /* u8 multiply-accumulates issued by the window Gram */
+    int64_t far_records;    /* light pair updates applied as far-pair records */
 } gakco_stats;
 
 /* Create a plan for alphabet size sigma (1..255), g-mer length g (1..32),

@@ -143,7 +143,7 @@ __device__ __forceinline__ uint32_t digit_peers(uint32_t d, uint32_t valid_mask)
 
 // Device counters of gakco_stats (int64 slots).
 enum { ST_KEYS = 0, ST_PASSKEYS, ST_TRIPLES, ST_GROUPS, ST_LIGHT_PAIRS, ST_HEAVY_GROUPS,
-       ST_HEAVY_MACS, ST_HEAVY_MACS4, ST_WIN_GROUPS, ST_WIN_MACS, ST_COUNT };
+       ST_HEAVY_MACS, ST_HEAVY_MACS4, ST_WIN_GROUPS, ST_WIN_MACS, ST_FAR_RECORDS, ST_COUNT };
 
 // Error flags raised by kernels (bit mask in a device int).
 enum { EF_NEGATIVE_N = 1, EF_K_MISMATCH = 2, EF_BAD_SYMBOL = 4 };
@@ -300,6 +300,23 @@ struct WinArgs {
     uint32_t nw;      // windows (0: the window path is off)
     uint32_t wmin;    // smallest group (sequences) taken
 };
+// Far-pair records (relabelled accumulator far beyond L2): a light pair
+// whose labels are >= near apart (a random cross-cluster match: its cell would miss
+// L2, 24 G REDs/s into 800 MB vs 208 G/s into 32 MB) is appended as a record
+// (cell << 24 | val) to per-warp chunks of rec instead of a RED; launch_far_apply
+// buckets the records by accumulator block and adds them block by block (L2-resident
+// REDs). fill[0] counts reserved record slots (chunks of FAR_CHUNK; every reserved
+// slot is written, unused ones with 0); a chunk past cap is never reserved (the warp
+// falls back to REDs). near = 0: off.
+constexpr uint32_t FAR_CHUNK = 1024;
+struct FarRec {
+    uint64_t* rec;     // [cap] records
+    uint32_t* fill;    // [0] slots reserved (all warps)
+    uint64_t cap;      // a multiple of FAR_CHUNK
+    uint32_t near;     // label distance from which a pair is far (0: off)
+};
+cudaError_t launch_far_apply(FarRec fr, uint64_t* scratch, uint32_t* bins, int bshift, int nbins,
+                             uint32_t* acc, int sm_count, cudaStream_t s);
 cudaError_t launch_window_build(SegmentOut so, WinArgs wa, const uint32_t* perm, uint8_t* wD,
                                 int sm_count, cudaStream_t s);
 cudaError_t launch_window_gram(uint8_t* wD, WinArgs wa, int64_t* wC, const int2* tiles,
@@ -312,7 +329,8 @@ cudaError_t launch_light(SegmentOut so, uint64_t max_groups, int64_t heavy_min, 
                          uint32_t* dense_fill, LightBins bins, uint32_t flat_max,
                          int64_t NA, const uint32_t* perm, uint32_t heavy_cmax,
                          unsigned long long* stats, int sm_count, cudaStream_t s,
-                         WinArgs wa = WinArgs{nullptr, nullptr, 0, 0, 0}, bool big = false);
+                         WinArgs wa = WinArgs{nullptr, nullptr, 0, 0, 0}, bool big = false,
+                         FarRec fr = FarRec{nullptr, nullptr, 0, 0});
 // Light accumulator relabelled by perm (sequence -> accumulator index): flush it into
 // C_m (original order) and zero it.
 cudaError_t launch_light_flush_perm(uint32_t* acc, int64_t N, int64_t* Cm, const uint32_t* perm,

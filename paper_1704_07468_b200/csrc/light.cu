@@ -26,14 +26,17 @@ __device__ __forceinline__ uint64_t tri_index(uint32_t x, uint32_t y, int64_t N)
 // Accumulator cell of the unordered pair {x, y} (x != y): the strictly-upper
 // packed triangle (full mode, NA = 0), or, in rectangular mode (NA > 0: sequences
 // [0, NA) are the rows, [NA, N) the columns), row-major NA x (N - NA) for a
-// cross pair; a pair inside one set is not a cell (*ok = false).
+// cross pair; a pair inside one set is not a cell (*ok = false). With a relabelled
+// accumulator, *dist = the label distance (far-pair records).
 __device__ __forceinline__ uint64_t pair_cell(uint32_t x, uint32_t y, int64_t N, int64_t NA,
-                                              bool* ok, const uint32_t* perm = nullptr) {
+                                              bool* ok, const uint32_t* perm = nullptr,
+                                              uint32_t* dist = nullptr) {
     if (perm) {  // relabelled accumulator (full mode only): cell of {perm[x], perm[y]}
         x = perm[x];
         y = perm[y];
     }
     const uint32_t lo = min(x, y), hi = max(x, y);
+    if (dist) *dist = hi - lo;
     if (NA == 0) {
         *ok = true;
         return tri_index(lo, hi, N);
@@ -73,6 +76,129 @@ __device__ __forceinline__ void pair_add(uint32_t* acc, const LightBins& bn, boo
     }
 }
 
+// Per-warp appender of far-pair records (FarRec): every lane calls put() (warp-
+// uniform control flow); the lanes whose update became a record get true.
+struct FarSink {
+    FarRec fr;
+    uint64_t base;  // first slot of the warp's chunk
+    uint32_t used;  // slots of the chunk used (warp-uniform)
+    bool have;      // a chunk is held
+    bool ok;        // records on (and chunks left)
+    __device__ void start(const FarRec& f) {
+        fr = f;
+        base = 0;
+        used = FAR_CHUNK;
+        have = false;
+        ok = f.near != 0;
+    }
+    __device__ void zero_rest() {  // unused slots of the held chunk -> 0 (no-op records)
+        if (!have) return;
+        for (uint32_t i = used + (threadIdx.x & 31); i < FAR_CHUNK; i += 32) fr.rec[base + i] = 0ull;
+    }
+    __device__ bool put(bool want, uint64_t cell, uint32_t val) {
+        want = want && ok && val < (1u << 24) && cell < (1ull << 40);
+        const uint32_t m = __ballot_sync(0xffffffffu, want);
+        if (!m) return false;
+        const uint32_t nf = __popc(m);
+        if (used + nf > FAR_CHUNK) {
+            zero_rest();
+            uint64_t b = 0;
+            if ((threadIdx.x & 31) == 0) b = atomicAdd(fr.fill, FAR_CHUNK);
+            b = __shfl_sync(0xffffffffu, b, 0);
+            if (b + FAR_CHUNK > fr.cap) {  // buffer full: this warp goes back to REDs
+                ok = false;
+                have = false;
+                return false;
+            }
+            base = b;
+            used = 0;
+            have = true;
+        }
+        if (want) fr.rec[base + used + __popc(m & lanemask_lt())] = cell << 24 | val;
+        used += nf;
+        return want;
+    }
+    __device__ void finish() { zero_rest(); }
+};
+
+// far-pair records -> accumulator: count per bin (block of 2^bshift cells), scan,
+// scatter into bins (unstable: the adds commute), add bin by bin (the grid sweeps
+// the bins in order, so the touched accumulator blocks stay in L2)
+__device__ __forceinline__ uint64_t far_total(const FarRec& fr) {
+    return min((uint64_t)*fr.fill, fr.cap);
+}
+__global__ void far_count_kernel(FarRec fr, int bshift, uint32_t* bins) {
+    __shared__ uint32_t s_b[64];
+    if (threadIdx.x < 64) s_b[threadIdx.x] = 0;
+    __syncthreads();
+    const uint64_t tot = far_total(fr);
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < tot;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t r = fr.rec[i];
+        if (r & 0xffffffull) atomicAdd(&s_b[(uint32_t)((r >> 24) >> bshift)], 1u);
+    }
+    __syncthreads();
+    if (threadIdx.x < 64 && s_b[threadIdx.x]) atomicAdd(&bins[threadIdx.x], s_b[threadIdx.x]);
+}
+__global__ void far_scan_kernel(uint32_t* bins) {  // bins[64 + b] <- exclusive prefix
+    if (threadIdx.x == 0) {
+        uint32_t run = 0;
+        for (int b = 0; b < 64; ++b) {
+            bins[64 + b] = run;
+            run += bins[b];
+        }
+        bins[128] = run;
+    }
+}
+__global__ void far_scatter_kernel(FarRec fr, int bshift, uint32_t* bins, uint64_t* out) {
+    __shared__ uint32_t s_b[64], s_base[64];
+    const uint64_t tot = far_total(fr);
+    const uint64_t per = (tot + gridDim.x - 1) / gridDim.x;
+    const uint64_t lo = min(tot, blockIdx.x * per), hi = min(tot, lo + per);
+    if (threadIdx.x < 64) s_b[threadIdx.x] = 0;
+    __syncthreads();
+    for (uint64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+        const uint64_t r = fr.rec[i];
+        if (r & 0xffffffull) atomicAdd(&s_b[(uint32_t)((r >> 24) >> bshift)], 1u);
+    }
+    __syncthreads();
+    if (threadIdx.x < 64) {
+        s_base[threadIdx.x] = s_b[threadIdx.x] ? atomicAdd(&bins[64 + threadIdx.x], s_b[threadIdx.x]) : 0u;
+        s_b[threadIdx.x] = 0;
+    }
+    __syncthreads();
+    for (uint64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
+        const uint64_t r = fr.rec[i];
+        if (!(r & 0xffffffull)) continue;
+        const uint32_t b = (uint32_t)((r >> 24) >> bshift);
+        out[s_base[b] + atomicAdd(&s_b[b], 1u)] = r;
+    }
+}
+__global__ void far_add_kernel(const uint64_t* __restrict__ recs, const uint32_t* bins,
+                               uint32_t* acc) {
+    const uint64_t tot = bins[128];
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < tot;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint64_t r = recs[i];
+        atomicAdd(&acc[r >> 24], (uint32_t)(r & 0xffffffull));
+    }
+}
+
+cudaError_t launch_far_apply(FarRec fr, uint64_t* scratch, uint32_t* bins, int bshift, int nbins,
+                             uint32_t* acc, int sm_count, cudaStream_t s) {
+    (void)nbins;
+    cudaError_t e = cudaMemsetAsync(bins, 0, 64 * sizeof(uint32_t), s);
+    if (e != cudaSuccess) return e;
+    const int grid = sm_count * 8;
+    far_count_kernel<<<grid, 256, 0, s>>>(fr, bshift, bins);
+    far_scan_kernel<<<1, 32, 0, s>>>(bins);
+    far_scatter_kernel<<<grid, 256, 0, s>>>(fr, bshift, bins, scratch);
+    far_add_kernel<<<grid, 256, 0, s>>>(scratch, bins, acc);
+    e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    return cudaMemsetAsync(fr.fill, 0, sizeof(uint32_t), s);
+}
+
 __global__ void apply_bins_kernel(uint32_t* __restrict__ acc, LightBins bn, int b) {
     const uint64_t c = min((uint64_t)bn.cnt[b], bn.cap);
     const uint32_t* r = bn.rec + (uint64_t)b * bn.cap;
@@ -97,14 +223,15 @@ cudaError_t launch_apply_bins(uint32_t* acc, LightBins bn, int sm_count, cudaStr
 // the occupancy DNA's L2-resident random updates want (light 3.32 ms; 56 registers:
 // 3.51 ms); 3 (up to 85 registers) is faster for the big groups of Text / Scale
 // (Text light 28.3 -> 26.7 ms, Scale 98.4 -> 93.4 ms).
-template <bool WIN, bool BINS, int MINB>
+template <bool WIN, bool BINS, int MINB, bool FAR = false>
 __global__ void __launch_bounds__(256, MINB) light_kernel(SegmentOut so, int64_t heavy_min, int64_t N,
                                                     uint32_t* acc, uint2* heavy_list,
                                                     uint64_t ldd, uint32_t* dense_fill,
                                                     LightBins bn, uint32_t flat_max,
                                                     int64_t NA, const uint32_t* perm,
                                                     uint32_t heavy_cmax,
-                                                    unsigned long long* stats, WinArgs wa) {
+                                                    unsigned long long* stats, WinArgs wa,
+                                                    FarRec frec) {
     // triangle table: pairs (a < b < 32) ordered by b, so the first n(n-1)/2
     // entries are exactly the pairs of an n-triple chunk
     __shared__ uint16_t s_tri[496];
@@ -116,7 +243,20 @@ __global__ void __launch_bounds__(256, MINB) light_kernel(SegmentOut so, int64_t
     const int lane = threadIdx.x & 31;
     const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
     const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
-    unsigned long long pairs = 0, nheavy = 0, nwin = 0;
+    unsigned long long pairs = 0, nheavy = 0, nwin = 0, nfar = 0;
+    FarSink sink;
+    if (FAR) sink.start(frec);
+    // one pair update: a far pair (labels >= frec.near apart) becomes a record, the
+    // rest are REDs (every lane calls it: warp-uniform)
+    auto upd = [&](bool ok, uint64_t idx, uint32_t val, uint32_t dist) {
+        if constexpr (FAR) {
+            const bool rec = sink.put(ok && dist >= frec.near, idx, val);
+            nfar += rec ? 1u : 0u;
+            if (ok && !rec) atomicAdd(&acc[idx], val);
+        } else {
+            pair_add<BINS>(acc, bn, ok, idx, val);
+        }
+    };
     // A warp takes 32 groups at a time: one coalesced load brings all their
     // triple ranges, and the first 32 triples of the next group are loaded while
     // the current one is processed.
@@ -154,16 +294,16 @@ __global__ void __launch_bounds__(256, MINB) light_kernel(SegmentOut so, int64_t
             const uint32_t ej = __shfl_sync(0xffffffffu, excl, j);
             const uint32_t sj = __shfl_sync(0xffffffffu, my_start, j);
             uint64_t idx = 0;
-            uint32_t val = 0;
+            uint32_t val = 0, dist = 0;
             bool ok = false;
             if (q < Ptot) {
                 const uint32_t ab = s_tri[q - ej];
                 const uint32_t ta = sj + (ab & 31), tb = sj + (ab >> 5);
                 const uint32_t xa = so.tseq[ta] & 0x7fffffffu, xb = so.tseq[tb] & 0x7fffffffu;
-                idx = pair_cell(xa, xb, N, NA, &ok, perm);
+                idx = pair_cell(xa, xb, N, NA, &ok, perm, FAR ? &dist : nullptr);
                 val = so.tcnt[ta] * so.tcnt[tb];
             }
-            pair_add<BINS>(acc, bn, ok, idx, val);
+            upd(ok, idx, val, dist);
         }
 
         // (1b) heavy candidates among the 32 groups: counts checked per group, then one
@@ -279,8 +419,10 @@ __global__ void __launch_bounds__(256, MINB) light_kernel(SegmentOut so, int64_t
                     const uint32_t xb = __shfl_sync(0xffffffffu, xA, b);
                     const uint32_t cb = __shfl_sync(0xffffffffu, cA, b);
                     bool ok = false;
-                    const uint64_t idx = q < P ? pair_cell(xa, xb, N, NA, &ok, perm) : 0;
-                    pair_add<BINS>(acc, bn, ok && q < P, idx, ca * cb);
+                    uint32_t dist = 0;
+                    const uint64_t idx =
+                        q < P ? pair_cell(xa, xb, N, NA, &ok, perm, FAR ? &dist : nullptr) : 0;
+                    upd(ok && q < P, idx, ca * cb, dist);
                 }
                 for (uint32_t B = A + 32; B < b0; B += 32) {
                     const uint32_t ib = B + lane;
@@ -291,14 +433,21 @@ __global__ void __launch_bounds__(256, MINB) light_kernel(SegmentOut so, int64_t
                         const uint32_t xa = __shfl_sync(0xffffffffu, xA, a);
                         const uint32_t ca = __shfl_sync(0xffffffffu, cA, a);
                         bool ok = false;
-                        const uint64_t idx = vb ? pair_cell(xa, xB, N, NA, &ok, perm) : 0;
-                        pair_add<BINS>(acc, bn, ok && vb, idx, ca * cB);
+                        uint32_t dist = 0;
+                        const uint64_t idx =
+                            vb ? pair_cell(xa, xB, N, NA, &ok, perm, FAR ? &dist : nullptr) : 0;
+                        upd(ok && vb, idx, ca * cB, dist);
                     }
                 }
             }
         }
     }
+    if (FAR) sink.finish();
     if (lane == 0 && pairs) atomicAdd(&stats[ST_LIGHT_PAIRS], pairs);
+    if (FAR) {
+        for (int o = 16; o > 0; o >>= 1) nfar += __shfl_xor_sync(0xffffffffu, nfar, o);
+        if (lane == 0 && nfar) atomicAdd(&stats[ST_FAR_RECORDS], nfar);
+    }
     if (lane == 0 && nheavy) atomicAdd(&stats[ST_HEAVY_GROUPS], nheavy);
     if (lane == 0 && nwin) atomicAdd(&stats[ST_WIN_GROUPS], nwin);
 }
@@ -308,7 +457,7 @@ cudaError_t launch_light(SegmentOut so, uint64_t max_groups, int64_t heavy_min, 
                          uint32_t* dense_fill, LightBins bins, uint32_t flat_max,
                          int64_t NA, const uint32_t* perm, uint32_t heavy_cmax,
                          unsigned long long* stats, int sm_count, cudaStream_t s,
-                         WinArgs wa, bool big) {
+                         WinArgs wa, bool big, FarRec fr) {
     if (max_groups == 0) return cudaGetLastError();
     uint64_t blocks = (max_groups + 255) / 256;  // 8 warps x 32 groups per block-round
     uint64_t cap = (uint64_t)sm_count * 8;
@@ -316,10 +465,17 @@ cudaError_t launch_light(SegmentOut so, uint64_t max_groups, int64_t heavy_min, 
 #define LIGHT(W, B, MB)                                                                        \
     light_kernel<W, B, MB><<<(unsigned)blocks, 256, 0, s>>>(so, heavy_min, N, acc, heavy_list,  \
                                                             ldd, dense_fill, bins, flat_max, NA, \
-                                                            perm, heavy_cmax, stats, wa)
+                                                            perm, heavy_cmax, stats, wa, fr)
+#define LIGHT_FAR(W)                                                                             \
+    light_kernel<W, false, 3, true><<<(unsigned)blocks, 256, 0, s>>>(                              \
+        so, heavy_min, N, acc, heavy_list, ldd, dense_fill, bins, flat_max, NA, perm, heavy_cmax, \
+        stats, wa, fr)
     // (instantiations: the window path and the binning ablation compiled in only
     // where they run; big batches of long masks (>= 2M g-mers) take the 64-register one)
-    if (wa.nw) {
+    if (fr.near && perm && bins.nb == 0) {
+        if (wa.nw) LIGHT_FAR(true);
+        else LIGHT_FAR(false);
+    } else if (wa.nw) {
         if (bins.nb > 0) LIGHT(true, true, 3);
         else LIGHT(true, false, 3);
     } else if (bins.nb > 0) {
@@ -330,6 +486,7 @@ cudaError_t launch_light(SegmentOut so, uint64_t max_groups, int64_t heavy_min, 
         LIGHT(false, false, 5);
     }
 #undef LIGHT
+#undef LIGHT_FAR
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess || bins.nb == 0) return e;
     return launch_apply_bins(acc, bins, sm_count, s);

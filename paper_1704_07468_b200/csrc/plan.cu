@@ -103,6 +103,8 @@ struct gakco_plan {
     int level_order_desc = 0;  // process levels m = M..0 (1) or 0..M (0, measured faster on DNA)
     int gram_fp4 = -1;         // -1 auto (e2m1 Gram when exact), 0 u8 / kind::i8, 1 e2m1
     int trie_pass = 1;         // mask-trie pass kernel: 1 trie.cu (Σ <= 64), 0 generic radix
+    int64_t far_near = -1;     // far-pair records from this label distance: -1 auto (256
+                               // with a relabelled accumulator), 0 off
     int pipeline = 1;          // light / dense / Gram of batch b on an aux stream, overlapping
                                // encode / sort / segment of batch b+1 (double-buffered triples)
     cudaStream_t aux = nullptr, aux2 = nullptr;  // light + dense; Gram flushes
@@ -119,7 +121,7 @@ struct gakco_plan {
 
     DevBuf genW0, genW1, genS0, genS1, kmdev, trieR, trieX0, trieX1, pdesc, wD, wlist, wfill, wC, winv, wtiles, trieS0, trieW, trieS, keptsh, dense2, heavy2, hcount2, tseq2, tcnt2, gstart2, counts2, perm, iota, best, parent, Dgscr, Kdscr, codes, off, gofs, gmseq, keysA, keysB, hist, status, ctr, tseq, tcnt, gstart, gend,
         counts, kept, stats, flags, kdiag, Cscr, Nmscr, Kscr, Knscr, heavy, hcount, dense, tiles, tiles4, symhist,
-        lightacc, binrec, bincnt, win, bkH, bktot, bkbase, bkdesc, bktab, bktcnt, bkgs, bkocc;
+        lightacc, binrec, bincnt, farrec, farscr, farbins, win, bkH, bktot, bkbase, bkdesc, bktab, bktcnt, bkgs, bkocc;
     int64_t tiles_npad = -1;
     int tiles_pair = -1;
     int64_t tiles_na = -1;
@@ -464,7 +466,7 @@ extern "C" void gakco_destroy(gakco_plan* p) {
                       &p->hist,  &p->status, &p->ctr,  &p->tseq,   &p->tcnt,  &p->gstart,
                       &p->gend,  &p->counts, &p->kept, &p->stats,  &p->flags, &p->kdiag,
                       &p->Cscr,  &p->Nmscr, &p->Kscr,  &p->Knscr, &p->heavy, &p->hcount,
-                      &p->dense, &p->tiles, &p->tiles4, &p->symhist, &p->trieS0, &p->trieW, &p->trieS, &p->genW0, &p->genW1, &p->genS0, &p->genS1, &p->kmdev, &p->trieR, &p->trieX0, &p->trieX1, &p->pdesc, &p->wD, &p->wlist, &p->wfill, &p->wC, &p->winv, &p->wtiles, &p->lightacc, &p->binrec, &p->bincnt,
+                      &p->dense, &p->tiles, &p->tiles4, &p->symhist, &p->trieS0, &p->trieW, &p->trieS, &p->genW0, &p->genW1, &p->genS0, &p->genS1, &p->kmdev, &p->trieR, &p->trieX0, &p->trieX1, &p->pdesc, &p->wD, &p->wlist, &p->wfill, &p->wC, &p->winv, &p->wtiles, &p->lightacc, &p->binrec, &p->bincnt, &p->farrec, &p->farscr, &p->farbins,
                       &p->win,   &p->bkH,   &p->bktot, &p->bkbase, &p->bkdesc, &p->bktab,
                       &p->bktcnt, &p->bkgs, &p->bkocc};
     for (DevBuf* b : bufs)
@@ -550,6 +552,10 @@ extern "C" gakco_status gakco_set_option(gakco_plan* p, int option, int64_t valu
             return GAKCO_OK;
         case GAKCO_OPT_TIMING:
             p->timing = value != 0;
+            return GAKCO_OK;
+        case GAKCO_OPT_FAR_NEAR:
+            if (value < -1 || value > ((int64_t)1 << 31)) return p->fail(GAKCO_E_ARG, "far near must be -1..2^31");
+            p->far_near = value;
             return GAKCO_OK;
         case GAKCO_OPT_TRIE_PASS:
             if (value < 0 || value > 1) return p->fail(GAKCO_E_ARG, "trie pass must be 0 or 1");
@@ -1232,6 +1238,22 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
                      (uint32_t)std::max<int64_t>(p->window_min, (int64_t)p->light_flat + 1)};
     }
     bool perm_active = false;
+    // far-pair records: with a relabelled accumulator far beyond L2, a
+    // light pair whose labels are >= near apart is recorded and added block by block
+    FarRec far{nullptr, nullptr, 0, 0};
+    int far_bshift = 0;
+    if (relabel && p->far_near != 0 && ntri * 4 > (96ull << 20)) {
+        const uint64_t cap = 128ull << 20;  // records per batch (1 GB); past it: REDs
+        CK(p->ensure(p->farrec, cap * 8, s));
+        CK(p->ensure(p->farscr, cap * 8, s));
+        CK(p->ensure(p->farbins, 256 * 4, s, /*zero=*/true));
+        CK(cudaMemsetAsync(p->farbins.p, 0, 256 * 4, s));
+        int lb = 0;
+        while (((uint64_t)1 << lb) < ntri) ++lb;
+        far_bshift = std::max(16, lb - 6);  // <= 64 accumulator blocks
+        far = FarRec{(uint64_t*)p->farrec.p, (uint32_t*)p->farbins.p + 192, cap,
+                     (uint32_t)(p->far_near > 0 ? p->far_near : 256)};
+    }
     if (relabel) {
         CK(p->ensure(p->perm, N * 4, s));
         CK(p->ensure(p->iota, N * 4, s));
@@ -1759,7 +1781,12 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
                             perm_active ? (const uint32_t*)p->perm.p : nullptr,
                             fp4_lv[m] ? 4u : 255u, stats, p->sm_count, s2,
                             perm_active && win_on ? wa : WinArgs{nullptr, nullptr, 0, 0, 0},
-                            n >= (2ull << 20)));
+                            n >= (2ull << 20), perm_active ? far : FarRec{nullptr, nullptr, 0, 0}));
+            if (perm_active && far.near) {  // this batch's far records into the accumulator
+                p->launches += 3;
+                LK(launch_far_apply(far, (uint64_t*)p->farscr.p, (uint32_t*)p->farbins.p, far_bshift,
+                                    64, (uint32_t*)p->lightacc.p, p->sm_count, s2));
+            }
             p->stage_end(s2, S_LIGHT, a);
             if (perm_active && win_on) {  // this batch's window columns (+ the Gram every few)
                 if (win_masks + nmask > win_lim) {  // s32 exactness of the next Gram
@@ -2066,6 +2093,7 @@ extern "C" gakco_status gakco_get_stats(gakco_plan* p, gakco_stats* out) {
         r.heavy_macs_fp4 = (int64_t)d[ST_HEAVY_MACS4];
         r.win_groups = (int64_t)d[ST_WIN_GROUPS];
         r.win_macs = (int64_t)d[ST_WIN_MACS];
+        r.far_records = (int64_t)d[ST_FAR_RECORDS];
     }
     double* ms[S_NSTAGE] = {&r.ms_encode, &r.ms_sort,     &r.ms_segment, &r.ms_light,
                             &r.ms_heavy,  &r.ms_epilogue, &r.ms_dense};

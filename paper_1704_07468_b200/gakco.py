@@ -43,6 +43,7 @@ GAKCO_OPT_LIGHT_WINDOW = 13
 GAKCO_OPT_WINDOW_MIN = 14
 GAKCO_OPT_GRAM_EACH = 15
 GAKCO_OPT_TRIE_PASS = 16
+GAKCO_OPT_FAR_NEAR = 17
 
 EXPORTS = ("gakco_create", "gakco_set_shard", "gakco_set_option", "gakco_accumulate",
            "gakco_finalize", "gakco_kernel", "gakco_kernel_k", "gakco_kernel_rect",
@@ -60,7 +61,7 @@ class gakco_stats(ctypes.Structure):
             "n_encode", "n_sort", "n_segment", "n_light", "n_heavy", "n_epilogue", "keys32",
             "sort_passes32", "grouping")] + [("ms_dense", ctypes.c_double)] + [
         (n, ctypes.c_int64) for n in ("n_dense", "n_pad", "gram_fp4", "heavy_macs_fp4",
-                                        "win_groups", "win_macs")]
+                                        "win_groups", "win_macs", "far_records")]
 
     def as_dict(self):
         return {n: getattr(self, n) for n, _ in self._fields_}

@@ -193,6 +193,28 @@ def test_light_flat_threshold(gk, oracle_lib):
             assert_parity(run(gk, cp, g, k, g - k, light_flat=flat, heavy_min_seqs=1 << 50), ref)
 
 
+def test_far_pair_records(gk, oracle_lib):
+    """Far-pair records (GAKCO_OPT_FAR_NEAR): with the relabelled accumulator past
+    96 MB (N = 7200: 104 MB), light pairs whose labels are >= near apart are
+    appended as records and added per accumulator block after each batch. Default
+    (256), every pair a record (1), none (2^30), off (0), and many batches (record
+    buffer reused) all equal the oracle; the stats count the records."""
+    cp = sc.gen_families(31, 7200, 72, 70, 50, 70, sigma=20)
+    g, k, M = 7, 4, 3
+    ref = oracle_lib.compute(cp, g, k, M)
+    r = run(gk, cp, g, k, M)
+    assert r["stats"]["far_records"] > 0
+    assert_parity(r, ref)
+    r1 = run(gk, cp, g, k, M, far_near=1)
+    assert r1["stats"]["far_records"] > r["stats"]["far_records"]
+    assert_parity(r1, ref)
+    assert run(gk, cp, g, k, M, far_near=1 << 30)["stats"]["far_records"] == 0
+    r0 = run(gk, cp, g, k, M, far_near=0)
+    assert r0["stats"]["far_records"] == 0
+    assert_parity(r0, ref)
+    assert_parity(run(gk, cp, g, k, M, far_near=64, batch_keys=400000, light_window=0), ref)
+
+
 def test_light_relabel(gk, oracle_lib):
     """Light accumulator relabelled after the first level by best-partner clusters
     (forced on; automatic only for accumulators far beyond L2) == oracle, on
