@@ -130,6 +130,12 @@ typedef enum {
                                      (<= 64 buckets, chunk prefixes inside the scatter: two
                                      launches) where sigma <= 64; 0 = the generic 8-bit radix
                                      pass (hist + chunk scan + scatter) */
+    GAKCO_OPT_XL_COMPACT = 18,    /* cross-level mask-trie chain (levels processed as k rises, a
+                                     level-m mask one pass over its level-(m+1) parent): 1
+                                     (default) = each level keeps only the elements of groups of
+                                     >= 2 g-mers for its children (a g-mer alone under a mask
+                                     stays alone under every refinement; its diagonal term is
+                                     the closed form), 0 = full arrays */
     GAKCO_OPT_FAR_NEAR = 17       /* far-pair records of the light path: once the accumulator is
                                      relabelled and larger than 96 MB, a pair whose labels are
                                      >= this far apart (random cross-cluster matches, whose cells

@@ -257,7 +257,17 @@ bool trie_pass64_ok(uint32_t dmask);
 cudaError_t launch_trie_pass64(const uint64_t* win, uint64_t* wout, const void* sin, void* sout,
                                bool seq16, uint64_t n, const uint32_t* cntp, int shift,
                                uint32_t dmask, uint64_t omask, uint32_t* H, int target_ctas,
-                               cudaStream_t s);
+                               cudaStream_t s, uint32_t* cnt_out = nullptr);
+cudaError_t launch_fill_u32(uint32_t* p, uint32_t v, uint32_t count, cudaStream_t s);
+// segrag.cu: the cross-level chain's leaves, ragged segments (cnt[s] valid elements
+// of segment s at [s n, s n + cnt[s])), km[s] the key mask of segment s; cw != nullptr:
+// also the compacted copy of segment s (elements of groups of >= 2) at cw/cs + s n,
+// its length at ccnt[s] (zeroed by the caller)
+cudaError_t launch_segment_rag(const uint64_t* w, const void* sq, bool seq16, uint64_t n, int nseg,
+                               const uint32_t* cnt, const uint64_t* km, int64_t dstride,
+                               int64_t* diag, uint32_t* counters, SegmentOut so,
+                               unsigned long long* stats, cudaStream_t s, uint64_t* cw,
+                               void* cs, uint32_t* ccnt);
 cudaError_t launch_seq16(const uint32_t* a, uint16_t* b, uint64_t n, int sm_count,
                          cudaStream_t s);
 cudaError_t launch_radix_chunked2(const void* in, void* out, bool k64, uint64_t n, int nseg,

@@ -103,6 +103,7 @@ struct gakco_plan {
     int level_order_desc = 0;  // process levels m = M..0 (1) or 0..M (0, measured faster on DNA)
     int gram_fp4 = -1;         // -1 auto (e2m1 Gram when exact), 0 u8 / kind::i8, 1 e2m1
     int trie_pass = 1;         // mask-trie pass kernel: 1 trie.cu (Σ <= 64), 0 generic radix
+    int xl_compact = 1;        // cross-level chain: compacted parents (segrag.cu), 0 off
     int64_t far_near = -1;     // far-pair records from this label distance: -1 auto (256
                                // with a relabelled accumulator), 0 off
     int pipeline = 1;          // light / dense / Gram of batch b on an aux stream, overlapping
@@ -121,7 +122,7 @@ struct gakco_plan {
 
     DevBuf genW0, genW1, genS0, genS1, kmdev, trieR, trieX0, trieX1, pdesc, wD, wlist, wfill, wC, winv, wtiles, trieS0, trieW, trieS, keptsh, dense2, heavy2, hcount2, tseq2, tcnt2, gstart2, counts2, perm, iota, best, parent, Dgscr, Kdscr, codes, off, gofs, gmseq, keysA, keysB, hist, status, ctr, tseq, tcnt, gstart, gend,
         counts, kept, stats, flags, kdiag, Cscr, Nmscr, Kscr, Knscr, heavy, hcount, dense, tiles, tiles4, symhist,
-        lightacc, binrec, bincnt, farrec, farscr, farbins, win, bkH, bktot, bkbase, bkdesc, bktab, bktcnt, bkgs, bkocc;
+        lightacc, binrec, bincnt, farrec, farscr, farbins, xccnt, xbcnt, win, bkH, bktot, bkbase, bkdesc, bktab, bktcnt, bkgs, bkocc;
     int64_t tiles_npad = -1;
     int tiles_pair = -1;
     int64_t tiles_na = -1;
@@ -466,7 +467,7 @@ extern "C" void gakco_destroy(gakco_plan* p) {
                       &p->hist,  &p->status, &p->ctr,  &p->tseq,   &p->tcnt,  &p->gstart,
                       &p->gend,  &p->counts, &p->kept, &p->stats,  &p->flags, &p->kdiag,
                       &p->Cscr,  &p->Nmscr, &p->Kscr,  &p->Knscr, &p->heavy, &p->hcount,
-                      &p->dense, &p->tiles, &p->tiles4, &p->symhist, &p->trieS0, &p->trieW, &p->trieS, &p->genW0, &p->genW1, &p->genS0, &p->genS1, &p->kmdev, &p->trieR, &p->trieX0, &p->trieX1, &p->pdesc, &p->wD, &p->wlist, &p->wfill, &p->wC, &p->winv, &p->wtiles, &p->lightacc, &p->binrec, &p->bincnt, &p->farrec, &p->farscr, &p->farbins,
+                      &p->dense, &p->tiles, &p->tiles4, &p->symhist, &p->trieS0, &p->trieW, &p->trieS, &p->genW0, &p->genW1, &p->genS0, &p->genS1, &p->kmdev, &p->trieR, &p->trieX0, &p->trieX1, &p->pdesc, &p->wD, &p->wlist, &p->wfill, &p->wC, &p->winv, &p->wtiles, &p->lightacc, &p->binrec, &p->bincnt, &p->farrec, &p->farscr, &p->farbins, &p->xccnt, &p->xbcnt,
                       &p->win,   &p->bkH,   &p->bktot, &p->bkbase, &p->bkdesc, &p->bktab,
                       &p->bktcnt, &p->bkgs, &p->bkocc};
     for (DevBuf* b : bufs)
@@ -552,6 +553,10 @@ extern "C" gakco_status gakco_set_option(gakco_plan* p, int option, int64_t valu
             return GAKCO_OK;
         case GAKCO_OPT_TIMING:
             p->timing = value != 0;
+            return GAKCO_OK;
+        case GAKCO_OPT_XL_COMPACT:
+            if (value < 0 || value > 1) return p->fail(GAKCO_E_ARG, "xl compact must be 0 or 1");
+            p->xl_compact = (int)value;
             return GAKCO_OK;
         case GAKCO_OPT_FAR_NEAR:
             if (value < -1 || value > ((int64_t)1 << 31)) return p->fail(GAKCO_E_ARG, "far near must be -1..2^31");
@@ -735,6 +740,7 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
     // buffer; only the first level of the chain is a trie from the windows.
     // (Relabelling needs level 0 first: then 0, M, M-1, ..., 1.)
     std::vector<int> xl_parent, xl_x, xl_slot, xl_run;  // per position in mine
+    std::vector<char> xl_link;  // per run: its masks are one pass over the previous run's
     bool xl = false;
     size_t xl_maxrun = 0;
     // (the batched trie too, where a pass sorts by one symbol -- Protein: a child mask
@@ -820,6 +826,7 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
                 xl_run[i] = run;
             }
             xl_maxrun = std::max(xl_maxrun, a1 - a0);
+            xl_link.push_back(all ? 1 : 0);
             prev_sets = cur_sets;
             prev_level = lm;
             ++run;
@@ -1093,6 +1100,18 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
             for (auto& v : xl_parent) v = -1;
         }
     }
+    // cross-level chain with compaction (segrag.cu): leaves in the batch buffers
+    // (keysA windows, keysB ids), each run's compacted arrays in the generation
+    // buffers with their counts in xccnt [2][maxrun]; the next run's passes read them
+    const bool xlc = trie && xl && p->xl_compact && p->trie_pass == 1 &&
+                     trie_pass64_ok((1u << bits) - 1u);
+    if (xlc) {
+        CK(p->ensure(p->xccnt, 2 * xl_maxrun * 4 + 16, s));
+        CK(p->ensure(p->xbcnt, (bmax_masks + 2) * 4, s));
+    }
+    auto run_has_kids = [&](int r) {
+        return r + 1 < (int)xl_link.size() && xl_link[r + 1] != 0;
+    };
     if (use_win) {
         CK(p->ensure(p->win, n * 8, s));
         std::vector<uint8_t> ksh(mine.size() * GMAX + GMAX, 0);
@@ -1608,6 +1627,84 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
                 LK(launch_segment(p->keysA.p, tb64, n, nmask, sb, dstride, Dm, so.counts, so,
                                   stats, s));
             }
+            p->stage_end(s, S_SEGMENT, a);
+        } else if (n > 0 && trie && xlc) {
+            // cross-level chain with compaction: a child mask is one pass (by its added
+            // position) over its parent's COMPACTED sorted elements (device count); the
+            // first run of the chain is a trie from the windows; leaves go to the batch
+            // buffers and the segment writes this run's compacted copies
+            const int kk = g - m;
+            const uint32_t dmask = (1u << bits) - 1u;
+            const int gen = xl_run[pos] & 1;
+            uint64_t* cW = (uint64_t*)(gen ? p->genW1.p : p->genW0.p);
+            uint8_t* cS = (uint8_t*)(gen ? p->genS1.p : p->genS0.p);
+            uint32_t* cC = (uint32_t*)p->xccnt.p + (size_t)gen * xl_maxrun;
+            const uint64_t* pW = (const uint64_t*)(gen ? p->genW0.p : p->genW1.p);
+            const uint8_t* pS = (const uint8_t*)(gen ? p->genS0.p : p->genS1.p);
+            const uint32_t* pC = (const uint32_t*)p->xccnt.p + (size_t)(gen ^ 1) * xl_maxrun;
+            uint32_t* bcnt = (uint32_t*)p->xbcnt.p;
+            const bool kids = run_has_kids(xl_run[pos]);
+            if (xl_slot[pos] == 0 && kids)  // a run starts: its compacted counts from 0
+                CK(cudaMemsetAsync(cC, 0, xl_maxrun * 4, s));
+            std::vector<uint64_t> kms;
+            p->stage_begin(s, &a);
+            for (size_t j = pos; j < end; ++j) {
+                const uint8_t* kept = trie_chain[j].data();
+                uint64_t* wleaf = (uint64_t*)p->keysA.p + (j - pos) * n;
+                uint8_t* sleaf = (uint8_t*)p->keysB.p + (j - pos) * n * ssz;
+                uint64_t kmask = 0;
+                for (int r = 0; r < kk; ++r)
+                    kmask |= (uint64_t)dmask << (bits * (g - 1 - p->mask_kept[mine[j]][r]));
+                kms.push_back(kmask);
+                if (kk == 0) {  // no kept position: one key, identity order (raw windows)
+                    CK(cudaMemcpyAsync(wleaf, p->win.p, n * 8, cudaMemcpyDeviceToDevice, s));
+                    CK(cudaMemcpyAsync(sleaf, p->trieS0.p, n * ssz, cudaMemcpyDeviceToDevice, s));
+                    LK(launch_fill_u32(bcnt + (j - pos), (uint32_t)n, 1, s));
+                    continue;
+                }
+                if (xl_parent[j] >= 0) {  // one pass over the parent's compacted elements
+                    LK(launch_trie_pass64(pW + (size_t)xl_parent[j] * n, wleaf,
+                                          pS + (size_t)xl_parent[j] * n * ssz, sleaf, seq16, n,
+                                          pC + xl_parent[j], bits * (g - 1 - xl_x[j]), dmask, ~0ull,
+                                          (uint32_t*)p->hist.p, p->trie_ctas_per_sm * p->sm_count,
+                                          s, bcnt + (j - pos)));
+                    p->launches += 1;  // hist + scatter
+                    passkeys += (int64_t)n;  // (capacity: the actual count is on the device)
+                    continue;
+                }
+                int d = 0;
+                while (d < stack_depth && d < kk - 1 && stack_pos[d] == kept[d]) ++d;
+                for (int t = d; t < kk; ++t) {
+                    const bool leaf = t == kk - 1;
+                    const uint64_t* wi = t == 0 ? (const uint64_t*)p->win.p
+                                                : (const uint64_t*)p->trieW.p + (size_t)(t - 1) * n;
+                    const void* si = t == 0 ? p->trieS0.p
+                                            : (const void*)((const uint8_t*)p->trieS.p + (size_t)(t - 1) * n * ssz);
+                    uint64_t* wo = leaf ? wleaf : (uint64_t*)p->trieW.p + (size_t)t * n;
+                    void* so_ = leaf ? (void*)sleaf : (void*)((uint8_t*)p->trieS.p + (size_t)t * n * ssz);
+                    LK(launch_trie_pass64(wi, wo, si, so_, seq16, n, nullptr, bits * (g - 1 - kept[t]),
+                                          dmask, ~0ull, (uint32_t*)p->hist.p,
+                                          p->trie_ctas_per_sm * p->sm_count, s,
+                                          leaf ? bcnt + (j - pos) : nullptr));
+                    p->launches += 1;
+                    if (!leaf) stack_pos[t] = kept[t];
+                }
+                stack_depth = kk - 1;
+                passkeys += (int64_t)(kk - d) * (int64_t)n;
+            }
+            p->stage_end(s, S_SORT, a);
+            {
+                gakco_status ws = wait_buf();
+                if (ws != GAKCO_OK) return ws;
+            }
+            p->stage_begin(s, &a);
+            kms.push_back(0);
+            CK(cudaMemcpyAsync(p->kmdev.p, kms.data(), kms.size() * 8, cudaMemcpyHostToDevice, s));
+            const size_t slot0 = (size_t)xl_slot[pos];
+            LK(launch_segment_rag((const uint64_t*)p->keysA.p, p->keysB.p, seq16, n, nmask, bcnt,
+                                  (const uint64_t*)p->kmdev.p, dstride, Dm, so.counts, so, stats, s,
+                                  kids ? cW + slot0 * n : nullptr, kids ? cS + slot0 * n * ssz : nullptr,
+                                  kids ? cC + slot0 : nullptr));
             p->stage_end(s, S_SEGMENT, a);
         } else if (n > 0 && trie) {
             // mask trie: pass t of a mask is a stable pass by the symbol at its t-th kept

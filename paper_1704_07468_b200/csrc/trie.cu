@@ -124,7 +124,7 @@ template <typename S>
 __global__ void __launch_bounds__(TP_THREADS, 2) tp_scatter_kernel(
     const uint64_t* __restrict__ win, uint64_t* __restrict__ wout, const S* __restrict__ sin,
     S* __restrict__ sout, uint64_t n, const uint32_t* cntp, int shift, uint32_t dmask,
-    uint64_t omask, const uint32_t* __restrict__ H) {
+    uint64_t omask, const uint32_t* __restrict__ H, uint32_t* cnt_out) {
     extern __shared__ __align__(16) unsigned char smem[];
     constexpr uint32_t WB = TP_TILE * 8 + 32, PB = TP_TILE * sizeof(S) + 32;
     uint64_t* const buf0 = (uint64_t*)smem;
@@ -148,6 +148,7 @@ __global__ void __launch_bounds__(TP_THREADS, 2) tp_scatter_kernel(
     const TpChunk ch = tp_chunk(cnt, cps, c);
     const uint64_t lo = ch.lo, hi = ch.hi;
     const uint32_t ntile = hi > lo ? (uint32_t)((hi - lo + TP_TILE - 1) / TP_TILE) : 0u;
+    if (cnt_out && c == 0 && tid == 0) *cnt_out = (uint32_t)cnt;  // (the output's count)
 
     for (int i = tid; i < 2 * TP_WARPS * TP_ND; i += TP_THREADS) (&s_whist[0][0])[i] = 0u;
     auto issue = [&](uint32_t t, uint64_t* bar) {
@@ -276,7 +277,18 @@ __global__ void __launch_bounds__(TP_THREADS, 2) tp_scatter_kernel(
     }
 }
 
+__global__ void fill_u32_kernel(uint32_t* p, uint32_t v, uint32_t count) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < count; i += gridDim.x * blockDim.x)
+        p[i] = v;
+}
+
 }  // namespace
+
+cudaError_t launch_fill_u32(uint32_t* p, uint32_t v, uint32_t count, cudaStream_t s) {
+    if (count == 0) return cudaGetLastError();
+    fill_u32_kernel<<<(count + 255) / 256 < 64 ? (count + 255) / 256 : 64, 256, 0, s>>>(p, v, count);
+    return cudaGetLastError();
+}
 
 // Σ <= 64 (dmask < 64): the two-launch pass above; returns false when it does not
 // apply (the caller uses launch_trie_pass)
@@ -285,7 +297,7 @@ bool trie_pass64_ok(uint32_t dmask) { return dmask < (uint32_t)TP_ND; }
 cudaError_t launch_trie_pass64(const uint64_t* win, uint64_t* wout, const void* sin, void* sout,
                                bool seq16, uint64_t n, const uint32_t* cntp, int shift,
                                uint32_t dmask, uint64_t omask, uint32_t* H, int target_ctas,
-                               cudaStream_t s) {
+                               cudaStream_t s, uint32_t* cnt_out) {
     if (n == 0) return cudaGetLastError();
     const uint64_t tiles = (n + TP_TILE - 1) / TP_TILE;
     const unsigned cps = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(tiles, target_ctas));
@@ -296,12 +308,12 @@ cudaError_t launch_trie_pass64(const uint64_t* win, uint64_t* wout, const void* 
         cudaFuncSetAttribute(tp_scatter_kernel<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)tp_smem<uint16_t>());
         tp_scatter_kernel<uint16_t><<<cps, TP_THREADS, tp_smem<uint16_t>(), s>>>(
-            win, wout, (const uint16_t*)sin, (uint16_t*)sout, n, cntp, shift, dmask, omask, H);
+            win, wout, (const uint16_t*)sin, (uint16_t*)sout, n, cntp, shift, dmask, omask, H, cnt_out);
     } else {
         cudaFuncSetAttribute(tp_scatter_kernel<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)tp_smem<uint32_t>());
         tp_scatter_kernel<uint32_t><<<cps, TP_THREADS, tp_smem<uint32_t>(), s>>>(
-            win, wout, (const uint32_t*)sin, (uint32_t*)sout, n, cntp, shift, dmask, omask, H);
+            win, wout, (const uint32_t*)sin, (uint32_t*)sout, n, cntp, shift, dmask, omask, H, cnt_out);
     }
     return cudaGetLastError();
 }

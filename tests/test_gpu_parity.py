@@ -193,6 +193,22 @@ def test_light_flat_threshold(gk, oracle_lib):
             assert_parity(run(gk, cp, g, k, g - k, light_flat=flat, heavy_min_seqs=1 << 50), ref)
 
 
+def test_xl_compaction_families(gk, oracle_lib):
+    """Cross-level mask-trie chain with compacted parents (GAKCO_OPT_XL_COMPACT): family
+    corpora (groups of many sizes, repeated keys within a sequence, Σ = 4 and 20),
+    segments of many tiles, several batches per level (ragged device counts reused),
+    relabelled or not; == the uncompacted chain == oracle."""
+    cases = [(sc.gen_families(41, 60, 4, 2000, 1500, 2000, sigma=20), 8, 4, 4),
+             (sc.gen_families(42, 80, 8, 900, 600, 900, sigma=4), 9, 5, 4),
+             (sc.from_sequences(4, [[0, 1] * 700, [0, 1] * 650, [1, 0] * 500] +
+                                [list(np.random.default_rng(43).integers(0, 4, 1200))
+                                 for _ in range(20)]), 6, 2, 4)]
+    for cp, g, k, M in cases:
+        ref = oracle_lib.compute(cp, g, k, M)
+        for opts in ({}, {"batch_keys": 70000}, {"light_relabel": 1}, {"xl_compact": 0}):
+            assert_parity(run(gk, cp, g, k, M, sort=6, **opts), ref)
+
+
 def test_far_pair_records(gk, oracle_lib):
     """Far-pair records (GAKCO_OPT_FAR_NEAR): with the relabelled accumulator past
     96 MB (N = 7200: 104 MB), light pairs whose labels are >= near apart are
@@ -302,8 +318,10 @@ def test_sort_modes_ragged(gk, oracle_lib):
     for bk in (0, 50001, 4097 * 3):
         for mode in (0, 1, 3, 4, 5, 6, 7):
             assert_parity(run(gk, cp, 8, 4, 4, batch_keys=bk, sort=mode), ref)
-        # the mask trie on the generic 8-bit radix pass instead of trie.cu's
+        # the mask trie on the generic 8-bit radix pass instead of trie.cu's, and the
+        # cross-level chain without compaction
         assert_parity(run(gk, cp, 8, 4, 4, batch_keys=bk, sort=6, trie_pass=0), ref)
+        assert_parity(run(gk, cp, 8, 4, 4, batch_keys=bk, sort=6, xl_compact=0), ref)
     cp4 = sc.from_sequences(4, [rng.integers(0, 4, size=int(rng.integers(0, 5000)))
                                 for _ in range(23)])
     ref4 = oracle_lib.compute(cp4, 6, 3, 3)
@@ -332,6 +350,7 @@ def test_grouping_modes(gk, oracle_lib):
             if r["stats"]["keys"] > 0:
                 assert r["stats"]["grouping"] == {6: 3, 7: 4}.get(mode, mode if mode < 3 else 0)
         assert_parity(run(gk, cp, g, k, M, sort=6, trie_pass=0), ref)
+        assert_parity(run(gk, cp, g, k, M, sort=6, xl_compact=0), ref)
         r = run(gk, cp, g, k, M)
         if r["stats"]["keys"] > 0:  # auto: the batched trie where one word holds the composite
             bits = max(1, int(np.ceil(np.log2(max(sigma, 2)))))
