@@ -258,6 +258,8 @@ cudaError_t launch_trie_pass64(const uint64_t* win, uint64_t* wout, const void* 
                                bool seq16, uint64_t n, const uint32_t* cntp, int shift,
                                uint32_t dmask, uint64_t omask, uint32_t* H, int target_ctas,
                                cudaStream_t s, uint32_t* cnt_out = nullptr);
+cudaError_t launch_tp_records(const uint64_t* in, uint64_t* out, uint64_t n, const uint32_t* cntp,
+                              int shift, uint32_t* H, int target_ctas, cudaStream_t s);
 cudaError_t launch_fill_u32(uint32_t* p, uint32_t v, uint32_t count, cudaStream_t s);
 // segrag.cu: the cross-level chain's leaves, ragged segments (cnt[s] valid elements
 // of segment s at [s n, s n + cnt[s])), km[s] the key mask of segment s; cw != nullptr:
@@ -325,7 +327,7 @@ struct FarRec {
     uint64_t cap;      // a multiple of FAR_CHUNK
     uint32_t near;     // label distance from which a pair is far (0: off)
 };
-cudaError_t launch_far_apply(FarRec fr, uint64_t* scratch, uint32_t* bins, int bshift, int nbins,
+cudaError_t launch_far_apply(FarRec fr, uint64_t* scratch, uint32_t* H, int bshift,
                              uint32_t* acc, int sm_count, cudaStream_t s);
 cudaError_t launch_window_build(SegmentOut so, WinArgs wa, const uint32_t* perm, uint8_t* wD,
                                 int sm_count, cudaStream_t s);

@@ -121,79 +121,27 @@ struct FarSink {
     __device__ void finish() { zero_rest(); }
 };
 
-// far-pair records -> accumulator: count per bin (block of 2^bshift cells), scan,
-// scatter into bins (unstable: the adds commute), add bin by bin (the grid sweeps
-// the bins in order, so the touched accumulator blocks stay in L2)
-__device__ __forceinline__ uint64_t far_total(const FarRec& fr) {
-    return min((uint64_t)*fr.fill, fr.cap);
-}
-__global__ void far_count_kernel(FarRec fr, int bshift, uint32_t* bins) {
-    __shared__ uint32_t s_b[64];
-    if (threadIdx.x < 64) s_b[threadIdx.x] = 0;
-    __syncthreads();
-    const uint64_t tot = far_total(fr);
-    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < tot;
-         i += (uint64_t)gridDim.x * blockDim.x) {
-        const uint64_t r = fr.rec[i];
-        if (r & 0xffffffull) atomicAdd(&s_b[(uint32_t)((r >> 24) >> bshift)], 1u);
-    }
-    __syncthreads();
-    if (threadIdx.x < 64 && s_b[threadIdx.x]) atomicAdd(&bins[threadIdx.x], s_b[threadIdx.x]);
-}
-__global__ void far_scan_kernel(uint32_t* bins) {  // bins[64 + b] <- exclusive prefix
-    if (threadIdx.x == 0) {
-        uint32_t run = 0;
-        for (int b = 0; b < 64; ++b) {
-            bins[64 + b] = run;
-            run += bins[b];
-        }
-        bins[128] = run;
-    }
-}
-__global__ void far_scatter_kernel(FarRec fr, int bshift, uint32_t* bins, uint64_t* out) {
-    __shared__ uint32_t s_b[64], s_base[64];
-    const uint64_t tot = far_total(fr);
-    const uint64_t per = (tot + gridDim.x - 1) / gridDim.x;
-    const uint64_t lo = min(tot, blockIdx.x * per), hi = min(tot, lo + per);
-    if (threadIdx.x < 64) s_b[threadIdx.x] = 0;
-    __syncthreads();
-    for (uint64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
-        const uint64_t r = fr.rec[i];
-        if (r & 0xffffffull) atomicAdd(&s_b[(uint32_t)((r >> 24) >> bshift)], 1u);
-    }
-    __syncthreads();
-    if (threadIdx.x < 64) {
-        s_base[threadIdx.x] = s_b[threadIdx.x] ? atomicAdd(&bins[64 + threadIdx.x], s_b[threadIdx.x]) : 0u;
-        s_b[threadIdx.x] = 0;
-    }
-    __syncthreads();
-    for (uint64_t i = lo + threadIdx.x; i < hi; i += blockDim.x) {
-        const uint64_t r = fr.rec[i];
-        if (!(r & 0xffffffull)) continue;
-        const uint32_t b = (uint32_t)((r >> 24) >> bshift);
-        out[s_base[b] + atomicAdd(&s_b[b], 1u)] = r;
-    }
-}
-__global__ void far_add_kernel(const uint64_t* __restrict__ recs, const uint32_t* bins,
-                               uint32_t* acc) {
-    const uint64_t tot = bins[128];
+// far-pair records -> accumulator: the records are bucketed by accumulator block
+// (2^bshift cells; one stable 6-bit pass of trie.cu, digit = cell >> bshift), then
+// added in bucket order: the grid sweeps the blocks in order, so the cells it
+// touches stay in L2 (zero records, the unused slots of warp chunks, add nothing)
+__global__ void far_add_kernel(const uint64_t* __restrict__ recs, const uint32_t* fill,
+                               uint64_t cap, uint32_t* acc) {
+    const uint64_t tot = min((uint64_t)*fill, cap);
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < tot;
          i += (uint64_t)gridDim.x * blockDim.x) {
         const uint64_t r = recs[i];
-        atomicAdd(&acc[r >> 24], (uint32_t)(r & 0xffffffull));
+        const uint32_t v = (uint32_t)(r & 0xffffffull);
+        if (v) atomicAdd(&acc[r >> 24], v);
     }
 }
 
-cudaError_t launch_far_apply(FarRec fr, uint64_t* scratch, uint32_t* bins, int bshift, int nbins,
-                             uint32_t* acc, int sm_count, cudaStream_t s) {
-    (void)nbins;
-    cudaError_t e = cudaMemsetAsync(bins, 0, 64 * sizeof(uint32_t), s);
+cudaError_t launch_far_apply(FarRec fr, uint64_t* scratch, uint32_t* H, int bshift, uint32_t* acc,
+                             int sm_count, cudaStream_t s) {
+    cudaError_t e = launch_tp_records(fr.rec, scratch, fr.cap, fr.fill, 24 + bshift, H,
+                                      sm_count * 2, s);
     if (e != cudaSuccess) return e;
-    const int grid = sm_count * 8;
-    far_count_kernel<<<grid, 256, 0, s>>>(fr, bshift, bins);
-    far_scan_kernel<<<1, 32, 0, s>>>(bins);
-    far_scatter_kernel<<<grid, 256, 0, s>>>(fr, bshift, bins, scratch);
-    far_add_kernel<<<grid, 256, 0, s>>>(scratch, bins, acc);
+    far_add_kernel<<<sm_count * 8, 256, 0, s>>>(scratch, fr.fill, fr.cap, acc);
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     return cudaMemsetAsync(fr.fill, 0, sizeof(uint32_t), s);

@@ -1265,7 +1265,8 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
         const uint64_t cap = 128ull << 20;  // records per batch (1 GB); past it: REDs
         CK(p->ensure(p->farrec, cap * 8, s));
         CK(p->ensure(p->farscr, cap * 8, s));
-        CK(p->ensure(p->farbins, 256 * 4, s, /*zero=*/true));
+        // farbins: [0..255] the fill counter (at 192), then 2 x SMs x 64 chunk histograms
+        CK(p->ensure(p->farbins, (256 + (size_t)p->sm_count * 2 * 64) * 4, s, /*zero=*/true));
         CK(cudaMemsetAsync(p->farbins.p, 0, 256 * 4, s));
         int lb = 0;
         while (((uint64_t)1 << lb) < ntri) ++lb;
@@ -1880,9 +1881,9 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
                             perm_active && win_on ? wa : WinArgs{nullptr, nullptr, 0, 0, 0},
                             n >= (2ull << 20), perm_active ? far : FarRec{nullptr, nullptr, 0, 0}));
             if (perm_active && far.near) {  // this batch's far records into the accumulator
-                p->launches += 3;
-                LK(launch_far_apply(far, (uint64_t*)p->farscr.p, (uint32_t*)p->farbins.p, far_bshift,
-                                    64, (uint32_t*)p->lightacc.p, p->sm_count, s2));
+                p->launches += 2;
+                LK(launch_far_apply(far, (uint64_t*)p->farscr.p, (uint32_t*)p->farbins.p + 256,
+                                    far_bshift, (uint32_t*)p->lightacc.p, p->sm_count, s2));
             }
             p->stage_end(s2, S_LIGHT, a);
             if (perm_active && win_on) {  // this batch's window columns (+ the Gram every few)

@@ -75,7 +75,7 @@ __global__ void __launch_bounds__(TP_THREADS) tp_hist_kernel(const uint64_t* __r
     const int tid = threadIdx.x, wp = tid >> 5;
     for (int i = tid; i < TP_WARPS * TP_ND; i += TP_THREADS) (&s_h[0][0])[i] = 0;
     __syncthreads();
-    const uint64_t cnt = cntp ? (uint64_t)*cntp : n;
+    const uint64_t cnt = cntp ? min((uint64_t)*cntp, n) : n;
     const TpChunk ch = tp_chunk(cnt, gridDim.x, blockIdx.x);
     uint64_t a = ch.lo;
     if (a < ch.hi && ((uintptr_t)(w + a) & 15)) {  // (16-byte loads on the aligned body)
@@ -114,9 +114,20 @@ __device__ __forceinline__ uint32_t tp_scan64(uint32_t v, uint32_t* s2) {
     return inc - v + (tid >= 32 && tid < 64 ? s2[0] : 0u);
 }
 
+// payload-less passes (far-pair records): S = TpNoPay
+struct TpNoPay {};
+template <typename S>
+__host__ __device__ constexpr bool tp_pay() {
+    return !std::is_same<S, TpNoPay>::value;
+}
+template <typename S>
+__host__ __device__ constexpr uint32_t tp_psz() {
+    return tp_pay<S>() ? (uint32_t)sizeof(S) : 0u;
+}
+
 template <typename S>
 constexpr size_t tp_smem() {
-    return 2 * (TP_TILE * 8 + 32) + 2 * (TP_TILE * sizeof(S) + 32) + TP_TILE * sizeof(S) +
+    return 2 * (TP_TILE * 8 + 32) + (tp_pay<S>() ? 2 * (TP_TILE * tp_psz<S>() + 32) + TP_TILE * tp_psz<S>() : 0) +
            2 * TP_ND * 8 + 2 * TP_WARPS * TP_ND * 4 + 2 * 8 * TP_ND * 4 + TP_ND * 4 + 16 + 2 * 8;
 }
 
@@ -126,13 +137,14 @@ __global__ void __launch_bounds__(TP_THREADS, 2) tp_scatter_kernel(
     S* __restrict__ sout, uint64_t n, const uint32_t* cntp, int shift, uint32_t dmask,
     uint64_t omask, const uint32_t* __restrict__ H, uint32_t* cnt_out) {
     extern __shared__ __align__(16) unsigned char smem[];
-    constexpr uint32_t WB = TP_TILE * 8 + 32, PB = TP_TILE * sizeof(S) + 32;
+    constexpr bool PAY = tp_pay<S>();
+    constexpr uint32_t WB = TP_TILE * 8 + 32, PB = PAY ? TP_TILE * tp_psz<S>() + 32 : 0;
     uint64_t* const buf0 = (uint64_t*)smem;
     uint64_t* const buf1 = (uint64_t*)(smem + WB);
     S* const pbuf0 = (S*)(smem + 2 * WB);
     S* const pbuf1 = (S*)(smem + 2 * WB + PB);
     S* const s_pout = (S*)(smem + 2 * WB + 2 * PB);
-    unsigned char* q = smem + 2 * WB + 2 * PB + TP_TILE * sizeof(S);
+    unsigned char* q = smem + 2 * WB + 2 * PB + (PAY ? TP_TILE * tp_psz<S>() : 0);
     q = (unsigned char*)(((uintptr_t)q + 7) & ~(uintptr_t)7);
     int64_t* s_run = (int64_t*)q;                                         // [ND]
     int64_t* s_goff = s_run + TP_ND;                                      // [ND]
@@ -143,7 +155,7 @@ __global__ void __launch_bounds__(TP_THREADS, 2) tp_scatter_kernel(
     uint64_t* s_bar = (uint64_t*)(((uintptr_t)(s_w + 4) + 7) & ~(uintptr_t)7);  // [2]
 
     const int tid = threadIdx.x, lane = tid & 31, wp = tid >> 5;
-    const uint64_t cnt = cntp ? (uint64_t)*cntp : n;
+    const uint64_t cnt = cntp ? min((uint64_t)*cntp, n) : n;
     const uint32_t cps = gridDim.x, c = blockIdx.x;
     const TpChunk ch = tp_chunk(cnt, cps, c);
     const uint64_t lo = ch.lo, hi = ch.hi;
@@ -154,10 +166,12 @@ __global__ void __launch_bounds__(TP_THREADS, 2) tp_scatter_kernel(
     auto issue = [&](uint32_t t, uint64_t* bar) {
         const uint64_t g0 = lo + (uint64_t)t * TP_TILE;
         const uint32_t ct = (uint32_t)min((uint64_t)TP_TILE, hi - g0);
-        const uint32_t bw = tp_span(win, g0, ct), bs = tp_span(sin, g0, ct);
+        const uint32_t bw = tp_span(win, g0, ct);
+        uint32_t bs = 0;
+        if constexpr (PAY) bs = tp_span(sin, g0, ct);
         mbar_expect_tx(bar, bw + bs);
         tp_bulk((t & 1) ? buf1 : buf0, tp_base(win, g0), bw, bar);
-        tp_bulk((t & 1) ? pbuf1 : pbuf0, tp_base(sin, g0), bs, bar);
+        if constexpr (PAY) tp_bulk((t & 1) ? pbuf1 : pbuf0, tp_base(sin, g0), bs, bar);
     };
     if (tid == 0) {
         mbar_init(&s_bar[0], 1);
@@ -202,7 +216,8 @@ __global__ void __launch_bounds__(TP_THREADS, 2) tp_scatter_kernel(
         const S* pbuf = b ? pbuf1 : pbuf0;
         mbar_wait(&s_bar[b], (t >> 1) & 1u);
         const uint64_t* kin = buf + tp_delta(win, t0);
-        const S* pin = pbuf + tp_delta(sin, t0);
+        const S* pin = nullptr;
+        if constexpr (PAY) pin = pbuf + tp_delta(sin, t0);
         uint64_t keys[TP_ITEMS];
         uint32_t rank[TP_ITEMS / 2];  // two 12-bit ranks per register (tile < 2^16)
 #pragma unroll
@@ -255,7 +270,7 @@ __global__ void __launch_bounds__(TP_THREADS, 2) tp_scatter_kernel(
                 const uint32_t d = (uint32_t)(keys[i] >> shift) & dmask;
                 const uint32_t pos = whist[d] + ((rank[i / 2] >> (16 * (i & 1))) & 0xffffu);
                 buf[pos] = keys[i];
-                s_pout[pos] = pin[idx];
+                if constexpr (PAY) s_pout[pos] = pin[idx];
             }
         }
         __syncwarp();
@@ -267,7 +282,7 @@ __global__ void __launch_bounds__(TP_THREADS, 2) tp_scatter_kernel(
             const uint32_t d = (uint32_t)(k >> shift) & dmask;
             const uint64_t dst = (uint64_t)(s_goff[d] + (int64_t)j);
             wout[dst] = k & omask;
-            sout[dst] = s_pout[j];
+            if constexpr (PAY) sout[dst] = s_pout[j];
         }
         __syncthreads();  // (D) buf, s_pout free
         if (t + 2 < ntile && tid == 0) {
@@ -287,6 +302,23 @@ __global__ void fill_u32_kernel(uint32_t* p, uint32_t v, uint32_t count) {
 cudaError_t launch_fill_u32(uint32_t* p, uint32_t v, uint32_t count, cudaStream_t s) {
     if (count == 0) return cudaGetLastError();
     fill_u32_kernel<<<(count + 255) / 256 < 64 ? (count + 255) / 256 : 64, 256, 0, s>>>(p, v, count);
+    return cudaGetLastError();
+}
+
+// records bucketed by a <= 6-bit digit (far-pair records: the accumulator block),
+// payload-less; cntp: device count (clamped to n)
+cudaError_t launch_tp_records(const uint64_t* in, uint64_t* out, uint64_t n, const uint32_t* cntp,
+                              int shift, uint32_t* H, int target_ctas, cudaStream_t s) {
+    if (n == 0) return cudaGetLastError();
+    const uint64_t tiles = (n + TP_TILE - 1) / TP_TILE;
+    const unsigned cps = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(tiles, target_ctas));
+    tp_hist_kernel<<<cps, TP_THREADS, 0, s>>>(in, n, cntp, shift, 63u, H);
+    cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) return e;
+    cudaFuncSetAttribute(tp_scatter_kernel<TpNoPay>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)tp_smem<TpNoPay>());
+    tp_scatter_kernel<TpNoPay><<<cps, TP_THREADS, tp_smem<TpNoPay>(), s>>>(
+        in, out, nullptr, nullptr, n, cntp, shift, 63u, ~0ull, H, nullptr);
     return cudaGetLastError();
 }
 
