@@ -30,13 +30,14 @@ __device__ __forceinline__ uint64_t tri_index(uint32_t x, uint32_t y, int64_t N)
 // accumulator, *dist = the label distance (far-pair records).
 __device__ __forceinline__ uint64_t pair_cell(uint32_t x, uint32_t y, int64_t N, int64_t NA,
                                               bool* ok, const uint32_t* perm = nullptr,
-                                              uint32_t* dist = nullptr) {
+                                              uint32_t* dist = nullptr, uint32_t* lo_out = nullptr) {
     if (perm) {  // relabelled accumulator (full mode only): cell of {perm[x], perm[y]}
         x = perm[x];
         y = perm[y];
     }
     const uint32_t lo = min(x, y), hi = max(x, y);
     if (dist) *dist = hi - lo;
+    if (lo_out) *lo_out = lo;
     if (NA == 0) {
         *ok = true;
         return tri_index(lo, hi, N);
@@ -192,6 +193,7 @@ __global__ void __launch_bounds__(256, MINB) light_kernel(SegmentOut so, int64_t
     const uint64_t warp = (blockIdx.x * (uint64_t)blockDim.x + threadIdx.x) >> 5;
     const uint64_t nwarps = ((uint64_t)gridDim.x * blockDim.x) >> 5;
     unsigned long long pairs = 0, nheavy = 0, nwin = 0, nfar = 0;
+    uint32_t lpairs = 0;  // per lane: light updates of split groups
     FarSink sink;
     if (FAR) sink.start(frec);
     // one pair update: a far pair (labels >= frec.near apart) becomes a record, the
@@ -288,11 +290,13 @@ __global__ void __launch_bounds__(256, MINB) light_kernel(SegmentOut so, int64_t
             }
         }
 
-        // (1c) window candidates (relabelled accumulator): light groups of >= wmin
-        // sequences whose labels lie in one window of 256 become u8 count columns of
-        // that window's block (window Gram); counts > 255 or a full window: light.
-        // (Splitting groups that straddle windows -- their in-window pairs to the Gram,
-        // the rest light -- was measured: no gain on Scale.)
+        // (1c) window candidates (relabelled accumulator): a light group of >= wmin
+        // sequences becomes a u8 count column of the window of 256 labels holding most
+        // of its members (window Gram); the pairs with a member outside the window (a
+        // cluster's group plus a few random members from other clusters) stay on the
+        // light path below. Counts > 255, < wmin members inside, or a full window: light.
+        uint32_t split = 0;       // claimed groups that keep their outside pairs
+        uint32_t my_win = 0xffffffffu;  // (lane jj: first label of group jj's window)
         if (WIN && wa.nw) {  // (a separate instantiation: no register cost otherwise)
             uint32_t cand = __ballot_sync(0xffffffffu, lane < ng && !flat &&
                                                            (int64_t)my_s < heavy_min &&
@@ -302,24 +306,42 @@ __global__ void __launch_bounds__(256, MINB) light_kernel(SegmentOut so, int64_t
                 cand &= cand - 1;
                 const uint32_t a0 = __shfl_sync(0xffffffffu, my_start, jj);
                 const uint32_t b0 = __shfl_sync(0xffffffffu, my_end, jj);
-                uint32_t lmin = 0xffffffffu, lmax = 0, cmax = 0;
+                // the most populated label bucket (128 labels) among the first 32 members,
+                // then the window (2 buckets) around it with the more members
+                const bool v0 = a0 + lane < b0;
+                const uint32_t bk = v0 ? perm[so.tseq[a0 + lane] & 0x7fffffffu] / WIN_STEP : 0xffffffffu;
+                const uint32_t peers = __match_any_sync(0xffffffffu, bk);
+                uint64_t key = v0 ? ((uint64_t)__popc(peers) << 32 | (uint64_t)(0xffffffffu - bk)) : 0ull;
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) key = max(key, __shfl_xor_sync(0xffffffffu, key, o));
+                const uint32_t bs = 0xffffffffu - (uint32_t)(key & 0xffffffffull);
+                const uint32_t cm = __popc(__ballot_sync(0xffffffffu, v0 && bs > 0 && bk == bs - 1));
+                const uint32_t cp = __popc(__ballot_sync(0xffffffffu, v0 && bk == bs + 1));
+                uint32_t w = (cm > cp && bs > 0) ? bs - 1 : bs;
+                if (w >= wa.nw) w = wa.nw - 1;
+                const uint32_t lo = w * WIN_STEP;
+                uint32_t nin = 0, nout = 0, cmax = 0;
                 for (uint32_t t = a0 + lane; t < b0; t += 32) {
                     const uint32_t lb = perm[so.tseq[t] & 0x7fffffffu];
-                    lmin = min(lmin, lb);
-                    lmax = max(lmax, lb);
-                    cmax = max(cmax, so.tcnt[t]);
+                    if (lb - lo < (uint32_t)WIN_ROWS) {
+                        ++nin;
+                        cmax = max(cmax, so.tcnt[t]);
+                    } else {
+                        ++nout;
+                    }
                 }
-                lmin = __reduce_min_sync(0xffffffffu, lmin);
-                lmax = __reduce_max_sync(0xffffffffu, lmax);
+                nin = __reduce_add_sync(0xffffffffu, nin);
+                nout = __reduce_add_sync(0xffffffffu, nout);
                 cmax = __reduce_max_sync(0xffffffffu, cmax);
-                const uint32_t w = lmin / WIN_STEP;
-                if (cmax <= 255u && lmax < w * WIN_STEP + WIN_ROWS) {
+                if (cmax <= 255u && nin >= wa.wmin) {
                     uint32_t col = 0;
                     if (lane == 0) col = atomicAdd(&wa.fill[w], 1u);
                     col = __shfl_sync(0xffffffffu, col, 0);
                     if (col < wa.cap) {
                         if (lane == 0) wa.list[(uint64_t)w * wa.cap + col] = make_uint2(a0, b0);
-                        got |= 1u << jj;
+                        if (nout == 0) got |= 1u << jj;
+                        else split |= 1u << jj;
+                        if (lane == jj) my_win = lo;
                         nwin += lane == 0 ? 1u : 0u;
                     }
                 }
@@ -328,6 +350,7 @@ __global__ void __launch_bounds__(256, MINB) light_kernel(SegmentOut so, int64_t
 
         // (2) the other groups one by one (big light groups)
         uint32_t todo = __ballot_sync(0xffffffffu, lane < ng && !flat) & ~got;
+        (void)split;
         uint32_t pa0 = 0, pb0 = 0, pX = 0, pC = 0;
         auto prefetch = [&](uint32_t jj) {
             pa0 = __shfl_sync(0xffffffffu, my_start, jj);
@@ -340,12 +363,16 @@ __global__ void __launch_bounds__(256, MINB) light_kernel(SegmentOut so, int64_t
         };
         if (todo) prefetch(__ffs(todo) - 1);
         while (todo) {
+            const int jcur = __ffs(todo) - 1;
             todo &= todo - 1;
             const uint32_t a0 = pa0, b0 = pb0;
             const uint32_t xA0 = pX, cA0 = pC;
             if (todo) prefetch(__ffs(todo) - 1);  // the next group's first chunk
             const uint32_t s = b0 - a0;
-            pairs += (unsigned long long)s * (s - 1) / 2;
+            // a split group (window column claimed): its pairs inside the window
+            // [wl, wl + 256) are on the tensor cores, the rest here
+            const uint32_t wl = WIN ? __shfl_sync(0xffffffffu, my_win, jcur) : 0xffffffffu;
+            pairs += wl == 0xffffffffu ? (unsigned long long)s * (s - 1) / 2 : 0ull;
             // the group's triples in 32-wide register chunks; pairs enumerated
             // lane-parallel: within a chunk through the triangle table, across
             // chunks as full 32 x 32 blocks (every lane busy on every atomic)
@@ -367,9 +394,15 @@ __global__ void __launch_bounds__(256, MINB) light_kernel(SegmentOut so, int64_t
                     const uint32_t xb = __shfl_sync(0xffffffffu, xA, b);
                     const uint32_t cb = __shfl_sync(0xffffffffu, cA, b);
                     bool ok = false;
-                    uint32_t dist = 0;
+                    uint32_t dist = 0, lol = 0;
                     const uint64_t idx =
-                        q < P ? pair_cell(xa, xb, N, NA, &ok, perm, FAR ? &dist : nullptr) : 0;
+                        q < P ? pair_cell(xa, xb, N, NA, &ok, perm, (FAR || WIN) ? &dist : nullptr,
+                                          WIN ? &lol : nullptr)
+                              : 0;
+                    if (WIN && wl != 0xffffffffu) {  // (split group: skip in-window pairs)
+                        ok = ok && !(lol - wl < (uint32_t)WIN_ROWS && lol + dist - wl < (uint32_t)WIN_ROWS);
+                        lpairs += (ok && q < P) ? 1u : 0u;
+                    }
                     upd(ok && q < P, idx, ca * cb, dist);
                 }
                 for (uint32_t B = A + 32; B < b0; B += 32) {
@@ -381,9 +414,15 @@ __global__ void __launch_bounds__(256, MINB) light_kernel(SegmentOut so, int64_t
                         const uint32_t xa = __shfl_sync(0xffffffffu, xA, a);
                         const uint32_t ca = __shfl_sync(0xffffffffu, cA, a);
                         bool ok = false;
-                        uint32_t dist = 0;
+                        uint32_t dist = 0, lol = 0;
                         const uint64_t idx =
-                            vb ? pair_cell(xa, xB, N, NA, &ok, perm, FAR ? &dist : nullptr) : 0;
+                            vb ? pair_cell(xa, xB, N, NA, &ok, perm, (FAR || WIN) ? &dist : nullptr,
+                                           WIN ? &lol : nullptr)
+                               : 0;
+                        if (WIN && wl != 0xffffffffu) {
+                            ok = ok && !(lol - wl < (uint32_t)WIN_ROWS && lol + dist - wl < (uint32_t)WIN_ROWS);
+                            lpairs += (ok && vb) ? 1u : 0u;
+                        }
                         upd(ok && vb, idx, ca * cB, dist);
                     }
                 }
@@ -391,6 +430,7 @@ __global__ void __launch_bounds__(256, MINB) light_kernel(SegmentOut so, int64_t
         }
     }
     if (FAR) sink.finish();
+    if (WIN) pairs += __reduce_add_sync(0xffffffffu, lpairs) * (lane == 0 ? 1ull : 0ull);
     if (lane == 0 && pairs) atomicAdd(&stats[ST_LIGHT_PAIRS], pairs);
     if (FAR) {
         for (int o = 16; o > 0; o >>= 1) nfar += __shfl_xor_sync(0xffffffffu, nfar, o);
