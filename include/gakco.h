@@ -141,7 +141,9 @@ typedef enum {
                                      >= this far apart (random cross-cluster matches, whose cells
                                      miss L2) is appended as a record and added per accumulator
                                      block after its batch (L2-resident) instead of a RED into
-                                     DRAM. -1 = automatic (default: 256), 0 = off (all REDs) */
+                                     DRAM. -1 = automatic (default: 256 when the relabelled
+                                     accumulator exceeds 96 MB), 0 = off (all REDs), > 0 = this
+                                     distance whenever the accumulator is relabelled */
 } gakco_option;
 
 /* Counters of the last gakco_accumulate (algorithmic units). */

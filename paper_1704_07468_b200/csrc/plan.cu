@@ -1261,7 +1261,7 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
     // light pair whose labels are >= near apart is recorded and added block by block
     FarRec far{nullptr, nullptr, 0, 0};
     int far_bshift = 0;
-    if (relabel && p->far_near != 0 && ntri * 4 > (96ull << 20)) {
+    if (relabel && (p->far_near > 0 || (p->far_near == -1 && ntri * 4 > (96ull << 20)))) {
         const uint64_t cap = 128ull << 20;  // records per batch (1 GB); past it: REDs
         CK(p->ensure(p->farrec, cap * 8, s));
         CK(p->ensure(p->farscr, cap * 8, s));

@@ -250,6 +250,8 @@ def test_light_relabel(gk, oracle_lib):
         assert_parity(run(gk, cp, g, k, M, light_relabel=1), ref)
         assert_parity(run(gk, cp, g, k, M, light_relabel=1, heavy_min_seqs=1 << 50), ref)
         assert_parity(run(gk, cp, g, k, M, light_relabel=1, light_window=0), ref)
+        # far-pair records forced at small N (every pair >= 3 labels apart a record)
+        assert_parity(run(gk, cp, g, k, M, light_relabel=1, far_near=3), ref)
         # single-mask trie with cross-level reuse: relabelling puts level 0 first
         assert_parity(run(gk, cp, g, k, M, light_relabel=1, sort=6), ref)
 

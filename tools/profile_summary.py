@@ -34,7 +34,11 @@ STAGE = {"encode_kernel": "encode", "encode_win_kernel": "encode", "window_kerne
          "symbol_hist_kernel": "encode", "thresh_union_kernel": "light",
          "light_flush_rect_kernel": "light", "fill_reset4_kernel": "heavy",
          "trie_root_kernel": "encode", "window_build_kernel": "dense", "window_round_kernel": "dense",
-         "window_reset_kernel": "heavy", "window_flush_kernel": "light"}
+         "window_reset_kernel": "heavy", "window_flush_kernel": "light",
+         "tp_hist_kernel": "sort", "tp_scatter_kernel": "sort", "segment_rag_kernel": "segment",
+         "far_add_kernel": "light", "fill_u32_kernel": "sort", "pack_upper_kernel": "exchange",
+         "diag_kernel": "exchange", "epilogue_packed_kernel": "epilogue",
+         "kdiag_rect_kernel": "epilogue"}
 
 
 def short(name):
