@@ -287,10 +287,15 @@ def stage_model(stats, cfg, N):
         # mask trie (SoA): u64 window + u16 (N <= 65536) or u32 sequence id per element,
         # read + written per pass; no per-mask encode (the windows are packed once)
         esz = 8.0 + (2.0 if N <= 65536 else 4.0)
+        # the compacted cross-level chain moves fewer elements than its capacities:
+        # pass_keys (device count) when the trie.cu pass reports it
+        pk = float(stats.get("pass_keys", 0) or 0) or float(passes)
         return {
             "encode": ("hbm", 8.0 * n_gm + 4.0 * n_gm),
-            "sort": ("hbm", 2.0 * esz * passes),
-            "segment": ("hbm", esz * keys + 8.0 * trip + 8.0 * grp),
+            "sort": ("hbm", 2.0 * esz * pk),
+            "segment": ("hbm", esz * min(float(keys), pk) + 8.0 * trip + 8.0 * grp),
+            # far-pair records: written once, bucketed (hist read, read + write), added
+            "far": ("hbm", 40.0 * float(stats.get("far_records", 0) or 0)),
             "light": ("hbm", 8.0 * stats["light_pairs"]),
             "heavy": ("tensor", 2.0 * (stats["heavy_macs"] + stats.get("win_macs", 0))),
             "dense": ("hbm", float(stats["heavy_groups"]) * float(stats.get("n_pad", 0))
@@ -316,6 +321,7 @@ def stage_model(stats, cfg, N):
         "encode": enc,
         "sort": srt,
         "segment": ("hbm", kbytes + 8.0 * trip + 8.0 * grp),  # read keys; write triples, groups
+        "far": ("hbm", 40.0 * float(stats.get("far_records", 0) or 0)),
         "light": ("hbm", 8.0 * stats["light_pairs"]),  # u32 read-modify-write per update
         "heavy": ("tensor", 2.0 * (stats["heavy_macs"] + stats.get("win_macs", 0))),
         # one n_pad-byte u8 (n_pad/2 e2m1) column per heavy group, written once

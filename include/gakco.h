@@ -175,6 +175,10 @@ typedef struct {
     int64_t win_groups;     /* light groups sent to the window Gram (GAKCO_OPT_LIGHT_WINDOW) */
     int64_t win_macs;       /* u8 multiply-accumulates issued by the window Gram */
     int64_t far_records;    /* light pair updates applied as far-pair records */
+    double ms_far;          /* bucketing + adding the far-pair records (GAKCO_OPT_FAR_NEAR) */
+    int64_t n_far;
+    int64_t pass_keys;      /* elements actually moved by the mask-trie passes (device count;
+                               sort_passes counts capacities on the compacted chain) */
 } gakco_stats;
 
 /* Create a plan for alphabet size sigma (1..255), g-mer length g (1..32),
@@ -275,16 +279,17 @@ gakco_status gakco_pack_upper(gakco_plan* plan, const int64_t* C, int64_t N, int
 gakco_status gakco_diag(gakco_plan* plan, const int64_t* C, int64_t N, int levels, int64_t* out,
                         void* cuda_stream);
 
-/* Epilogue of one packed slice: Cp[m][e - begin] (DEVICE; int64, or u32 when
- * in_bytes = 4) holds the COMPLETE C_m (all masks summed) of the entries [begin,
- * end); Cdiag[m][X] (DEVICE, int64) the complete diagonals C_m(X,X) of all N
- * sequences. Writes, for the same entries, Nm[m][e - begin] (Eq. 9),
+/* Epilogue of one packed slice: Cp[m * ld + e - begin] (DEVICE; int64, or u32 when
+ * in_bytes = 4; ld >= end - begin elements between levels) holds the COMPLETE C_m
+ * (all masks summed) of the entries [begin, end); Cdiag[m][X] (DEVICE, int64) the
+ * complete diagonals C_m(X,X) of all N sequences. Writes, for the same entries,
+ * Nm[m * ld + e - begin] (Eq. 9),
  * K[e - begin] (Eq. 7) and Knorm[e - begin] (K(X,Y)/sqrt(K(X,X) K(Y,Y)),
  * reading A5), each optional (NULL), DEVICE pointers. Synchronises cuda_stream;
  * GAKCO_E_INTERNAL on a negative N_m or K != C_{g-k}, GAKCO_E_SYMBOL if the last
  * accumulate flagged a code >= sigma. */
-gakco_status gakco_finalize_packed(gakco_plan* plan, const void* Cp, int in_bytes, int64_t N,
-                                   int64_t begin, int64_t end, const int64_t* Cdiag, int64_t* Nm,
+gakco_status gakco_finalize_packed(gakco_plan* plan, const void* Cp, int in_bytes, int64_t ld,
+                                   int64_t N, int64_t begin, int64_t end, const int64_t* Cdiag, int64_t* Nm,
                                    int64_t* K, double* Knorm, void* cuda_stream);
 
 /* Counters and (if GAKCO_OPT_TIMING) stage times of the last accumulate /

@@ -143,7 +143,8 @@ __device__ __forceinline__ uint32_t digit_peers(uint32_t d, uint32_t valid_mask)
 
 // Device counters of gakco_stats (int64 slots).
 enum { ST_KEYS = 0, ST_PASSKEYS, ST_TRIPLES, ST_GROUPS, ST_LIGHT_PAIRS, ST_HEAVY_GROUPS,
-       ST_HEAVY_MACS, ST_HEAVY_MACS4, ST_WIN_GROUPS, ST_WIN_MACS, ST_FAR_RECORDS, ST_COUNT };
+       ST_HEAVY_MACS, ST_HEAVY_MACS4, ST_WIN_GROUPS, ST_WIN_MACS, ST_FAR_RECORDS,
+       ST_PASS_KEYS, ST_COUNT };
 
 // Error flags raised by kernels (bit mask in a device int).
 enum { EF_NEGATIVE_N = 1, EF_K_MISMATCH = 2, EF_BAD_SYMBOL = 4 };
@@ -257,7 +258,8 @@ bool trie_pass64_ok(uint32_t dmask);
 cudaError_t launch_trie_pass64(const uint64_t* win, uint64_t* wout, const void* sin, void* sout,
                                bool seq16, uint64_t n, const uint32_t* cntp, int shift,
                                uint32_t dmask, uint64_t omask, uint32_t* H, int target_ctas,
-                               cudaStream_t s, uint32_t* cnt_out = nullptr);
+                               cudaStream_t s, uint32_t* cnt_out = nullptr,
+                               unsigned long long* stats = nullptr);
 cudaError_t launch_tp_records(const uint64_t* in, uint64_t* out, uint64_t n, const uint32_t* cntp,
                               int shift, uint32_t* H, int target_ctas, cudaStream_t s);
 cudaError_t launch_fill_u32(uint32_t* p, uint32_t v, uint32_t count, cudaStream_t s);
@@ -323,12 +325,13 @@ struct WinArgs {
 constexpr uint32_t FAR_CHUNK = 1024;
 struct FarRec {
     uint64_t* rec;     // [cap] records
-    uint32_t* fill;    // [0] slots reserved (all warps)
+    uint32_t* fill;    // [0] slots reserved (all warps), [1] the count an apply processes
     uint64_t cap;      // a multiple of FAR_CHUNK
     uint32_t near;     // label distance from which a pair is far (0: off)
 };
+// (applies only when fill[0] >= thresh; fill[1] is the gated count; thresh 0: forced)
 cudaError_t launch_far_apply(FarRec fr, uint64_t* scratch, uint32_t* H, int bshift,
-                             uint32_t* acc, int sm_count, cudaStream_t s);
+                             uint32_t* acc, int sm_count, cudaStream_t s, uint32_t thresh);
 cudaError_t launch_window_build(SegmentOut so, WinArgs wa, const uint32_t* perm, uint8_t* wD,
                                 int sm_count, cudaStream_t s);
 cudaError_t launch_window_gram(uint8_t* wD, WinArgs wa, int64_t* wC, const int2* tiles,
@@ -425,7 +428,7 @@ cudaError_t launch_diag(const int64_t* C, int64_t N, int levels, int64_t* out, i
                         cudaStream_t s);
 // complete packed C slice [M+1][end - begin] (int64 or u32) + complete diagonals Dg
 // [M+1][N] -> packed Nm [M+1][end - begin], K, Knorm [end - begin]; kdiag [N] scratch
-cudaError_t launch_epilogue_packed(const void* Cp, int in_bytes, const int64_t* Dg, int64_t N,
+cudaError_t launch_epilogue_packed(const void* Cp, int in_bytes, int64_t ld, const int64_t* Dg, int64_t N,
                                    int64_t begin, int64_t end, int g, int k, int M, int64_t* Nm,
                                    int64_t* K, double* Knorm, int64_t* kdiag, int* flags,
                                    cudaStream_t s);

@@ -128,7 +128,7 @@ struct FarSink {
 // touches stay in L2 (zero records, the unused slots of warp chunks, add nothing)
 __global__ void far_add_kernel(const uint64_t* __restrict__ recs, const uint32_t* fill,
                                uint64_t cap, uint32_t* acc) {
-    const uint64_t tot = min((uint64_t)*fill, cap);
+    const uint64_t tot = min((uint64_t)*fill, cap);  // (the gated count, fill[1])
     for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < tot;
          i += (uint64_t)gridDim.x * blockDim.x) {
         const uint64_t r = recs[i];
@@ -137,15 +137,26 @@ __global__ void far_add_kernel(const uint64_t* __restrict__ recs, const uint32_t
     }
 }
 
+// the apply runs only once the records fill half the buffer (or when forced before
+// the accumulator is flushed): a block's cells must be hit several times per apply
+// for the bucketing to pay (a batch alone adds ~0.3 records per cell on Scale)
+__global__ void far_gate_kernel(uint32_t* fill, uint64_t cap, uint32_t thresh) {
+    const uint32_t f = (uint32_t)min((uint64_t)fill[0], cap);
+    fill[1] = f >= thresh ? f : 0u;  // the count this apply processes
+}
+__global__ void far_reset_kernel(uint32_t* fill) {
+    if (fill[1]) fill[0] = 0u;
+}
+
 cudaError_t launch_far_apply(FarRec fr, uint64_t* scratch, uint32_t* H, int bshift, uint32_t* acc,
-                             int sm_count, cudaStream_t s) {
-    cudaError_t e = launch_tp_records(fr.rec, scratch, fr.cap, fr.fill, 24 + bshift, H,
+                             int sm_count, cudaStream_t s, uint32_t thresh) {
+    far_gate_kernel<<<1, 1, 0, s>>>(fr.fill, fr.cap, thresh);
+    cudaError_t e = launch_tp_records(fr.rec, scratch, fr.cap, fr.fill + 1, 24 + bshift, H,
                                       sm_count * 2, s);
     if (e != cudaSuccess) return e;
-    far_add_kernel<<<sm_count * 8, 256, 0, s>>>(scratch, fr.fill, fr.cap, acc);
-    e = cudaGetLastError();
-    if (e != cudaSuccess) return e;
-    return cudaMemsetAsync(fr.fill, 0, sizeof(uint32_t), s);
+    far_add_kernel<<<sm_count * 8, 256, 0, s>>>(scratch, fr.fill + 1, fr.cap, acc);
+    far_reset_kernel<<<1, 1, 0, s>>>(fr.fill);
+    return cudaGetLastError();
 }
 
 __global__ void apply_bins_kernel(uint32_t* __restrict__ acc, LightBins bn, int b) {

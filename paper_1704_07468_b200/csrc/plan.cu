@@ -33,7 +33,7 @@ struct DevBuf {
     size_t cap = 0;
 };
 
-enum Stage { S_ENCODE = 0, S_SORT, S_SEGMENT, S_LIGHT, S_HEAVY, S_EPILOGUE, S_DENSE, S_NSTAGE };
+enum Stage { S_ENCODE = 0, S_SORT, S_SEGMENT, S_LIGHT, S_HEAVY, S_EPILOGUE, S_DENSE, S_FAR, S_NSTAGE };
 
 // NVTX range for profilers (nsys / ncu --nvtx): host-side enqueue of one phase
 struct Nvtx {
@@ -182,7 +182,7 @@ struct gakco_plan {
         }
         return ev_pool[ev_used++];
     }
-    int64_t stage_launches[S_NSTAGE] = {0, 0, 0, 0, 0, 0, 0};
+    int64_t stage_launches[S_NSTAGE] = {0, 0, 0, 0, 0, 0, 0, 0};
     int64_t launches_at_begin = 0;
     int last_grouping = 0;
     void stage_begin(cudaStream_t s, cudaEvent_t* a) {
@@ -1261,8 +1261,19 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
     // light pair whose labels are >= near apart is recorded and added block by block
     FarRec far{nullptr, nullptr, 0, 0};
     int far_bshift = 0;
+    uint32_t far_thresh = 0;
     if (relabel && (p->far_near > 0 || (p->far_near == -1 && ntri * 4 > (96ull << 20)))) {
-        const uint64_t cap = 128ull << 20;  // records per batch (1 GB); past it: REDs
+        // records are applied once they fill half the buffer (every cell of a block hit
+        // several times per apply) and before each accumulator flush; up to 2^30
+        // records (8 GB + the same for the bucketed copy) while 16 GB stay free
+        size_t fr = 0, tot = 0;
+        cudaMemGetInfo(&fr, &tot);
+        const size_t have = std::max(p->farrec.cap, p->farscr.cap) / 8;
+        uint64_t cap = std::min<uint64_t>(1ull << 30, std::max<uint64_t>(
+            std::max<uint64_t>(1ull << 24, have),
+            fr > (16ull << 30) ? (fr - (16ull << 30)) / 16 : 0));
+        cap = cap / FAR_CHUNK * FAR_CHUNK;
+        far_thresh = (uint32_t)(cap / 2);
         CK(p->ensure(p->farrec, cap * 8, s));
         CK(p->ensure(p->farscr, cap * 8, s));
         // farbins: [0..255] the fill counter (at 192), then 2 x SMs x 64 chunk histograms
@@ -1337,6 +1348,13 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
         if (light_m < 0 || light_masks == 0) return GAKCO_OK;
         Nvtx nv("light flush");
         cudaEvent_t al = nullptr;
+        if (perm_active && far.near) {  // every pending far record first
+            p->stage_begin(s2, &al);
+            p->launches += 4;
+            LK(launch_far_apply(far, (uint64_t*)p->farscr.p, (uint32_t*)p->farbins.p + 256,
+                                far_bshift, (uint32_t*)p->lightacc.p, p->sm_count, s2, 0u));
+            p->stage_end(s2, S_FAR, al);
+        }
         p->stage_begin(s2, &al);
         if (rect)
             LK(launch_light_flush_rect((uint32_t*)p->lightacc.p, ntri, level_ptr(light_m),
@@ -1668,7 +1686,7 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
                                           pS + (size_t)xl_parent[j] * n * ssz, sleaf, seq16, n,
                                           pC + xl_parent[j], bits * (g - 1 - xl_x[j]), dmask, ~0ull,
                                           (uint32_t*)p->hist.p, p->trie_ctas_per_sm * p->sm_count,
-                                          s, bcnt + (j - pos)));
+                                          s, bcnt + (j - pos), stats));
                     p->launches += 1;  // hist + scatter
                     passkeys += (int64_t)n;  // (capacity: the actual count is on the device)
                     continue;
@@ -1686,7 +1704,7 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
                     LK(launch_trie_pass64(wi, wo, si, so_, seq16, n, nullptr, bits * (g - 1 - kept[t]),
                                           dmask, ~0ull, (uint32_t*)p->hist.p,
                                           p->trie_ctas_per_sm * p->sm_count, s,
-                                          leaf ? bcnt + (j - pos) : nullptr));
+                                          leaf ? bcnt + (j - pos) : nullptr, stats));
                     p->launches += 1;
                     if (!leaf) stack_pos[t] = kept[t];
                 }
@@ -1750,7 +1768,8 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
                         LK(launch_trie_pass64(pgenW + (size_t)xl_parent[j] * n, wleaf,
                                               pgenS + (size_t)xl_parent[j] * n * ssz, sleaf, seq16, n,
                                               nullptr, bits * (g - 1 - xl_x[j]), dmask, ~0ull,
-                                              (uint32_t*)p->hist.p, p->trie_ctas_per_sm * p->sm_count, s));
+                                              (uint32_t*)p->hist.p, p->trie_ctas_per_sm * p->sm_count, s,
+                                              nullptr, stats));
                     else
                         LK(launch_trie_pass(pgenW + (size_t)xl_parent[j] * n, wleaf,
                                             pgenS + (size_t)xl_parent[j] * n * ssz, sleaf, seq16, n,
@@ -1775,7 +1794,7 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
                     if (tp64)
                         LK(launch_trie_pass64(wi, wo, si, so_, seq16, n, nullptr, bits * (g - 1 - kept[t]),
                                               dmask, leaf && !xl ? kmask : ~0ull, (uint32_t*)p->hist.p,
-                                              p->trie_ctas_per_sm * p->sm_count, s));
+                                              p->trie_ctas_per_sm * p->sm_count, s, nullptr, stats));
                     else
                         LK(launch_trie_pass(wi, wo, si, so_, seq16, n, bits * (g - 1 - kept[t]), dmask,
                                             leaf && !xl ? kmask : ~0ull, (uint32_t*)p->hist.p,
@@ -1880,12 +1899,15 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
                             fp4_lv[m] ? 4u : 255u, stats, p->sm_count, s2,
                             perm_active && win_on ? wa : WinArgs{nullptr, nullptr, 0, 0, 0},
                             n >= (2ull << 20), perm_active ? far : FarRec{nullptr, nullptr, 0, 0}));
-            if (perm_active && far.near) {  // this batch's far records into the accumulator
-                p->launches += 2;
-                LK(launch_far_apply(far, (uint64_t*)p->farscr.p, (uint32_t*)p->farbins.p + 256,
-                                    far_bshift, (uint32_t*)p->lightacc.p, p->sm_count, s2));
-            }
             p->stage_end(s2, S_LIGHT, a);
+            if (perm_active && far.near) {  // far records into the accumulator (gated)
+                p->stage_begin(s2, &a);
+                p->launches += 4;
+                LK(launch_far_apply(far, (uint64_t*)p->farscr.p, (uint32_t*)p->farbins.p + 256,
+                                    far_bshift, (uint32_t*)p->lightacc.p, p->sm_count, s2,
+                                    far_thresh));
+                p->stage_end(s2, S_FAR, a);
+            }
             if (perm_active && win_on) {  // this batch's window columns (+ the Gram every few)
                 if (win_masks + nmask > win_lim) {  // s32 exactness of the next Gram
                     gakco_status ws = wgram();
@@ -2175,7 +2197,7 @@ extern "C" gakco_status gakco_get_stats(gakco_plan* p, gakco_stats* out) {
     gakco_stats r = p->host_stats;
     r.launches = p->launches;
     int64_t* nl[S_NSTAGE] = {&r.n_encode, &r.n_sort,     &r.n_segment, &r.n_light,
-                             &r.n_heavy,  &r.n_epilogue, &r.n_dense};
+                             &r.n_heavy,  &r.n_epilogue, &r.n_dense,   &r.n_far};
     for (int i = 0; i < S_NSTAGE; ++i) *nl[i] = p->stage_launches[i];
     if (p->stats.p) {
         unsigned long long d[ST_COUNT];
@@ -2192,9 +2214,10 @@ extern "C" gakco_status gakco_get_stats(gakco_plan* p, gakco_stats* out) {
         r.win_groups = (int64_t)d[ST_WIN_GROUPS];
         r.win_macs = (int64_t)d[ST_WIN_MACS];
         r.far_records = (int64_t)d[ST_FAR_RECORDS];
+        r.pass_keys = (int64_t)d[ST_PASS_KEYS];
     }
     double* ms[S_NSTAGE] = {&r.ms_encode, &r.ms_sort,     &r.ms_segment, &r.ms_light,
-                            &r.ms_heavy,  &r.ms_epilogue, &r.ms_dense};
+                            &r.ms_heavy,  &r.ms_epilogue, &r.ms_dense,   &r.ms_far};
     for (auto& se : p->evs) {
         float t = 0;
         cudaEventSynchronize(se.second.second);
@@ -2256,7 +2279,7 @@ extern "C" gakco_status gakco_diag(gakco_plan* p, const int64_t* C, int64_t N, i
 }
 
 extern "C" gakco_status gakco_finalize_packed(gakco_plan* p, const void* Cp, int in_bytes,
-                                              int64_t N, int64_t begin, int64_t end,
+                                              int64_t ld, int64_t N, int64_t begin, int64_t end,
                                               const int64_t* Cdiag, int64_t* Nm, int64_t* K,
                                               double* Knorm, void* stream) {
     if (!p) return GAKCO_E_ARG;
@@ -2264,6 +2287,7 @@ extern "C" gakco_status gakco_finalize_packed(gakco_plan* p, const void* Cp, int
     const int64_t T = N * (N + 1) / 2;
     if (begin < 0 || end < begin || end > T) return p->fail(GAKCO_E_ARG, "range outside the triangle");
     if (in_bytes != 4 && in_bytes != 8) return p->fail(GAKCO_E_ARG, "in_bytes must be 4 or 8");
+    if (ld < end - begin) return p->fail(GAKCO_E_ARG, "ld < end - begin");
     if (!Cdiag || !is_device_ptr(Cdiag) || (end > begin && (!Cp || !is_device_ptr(Cp))))
         return p->fail(GAKCO_E_ARG, "Cp and Cdiag must be device pointers");
     for (const void* o : {(const void*)Nm, (const void*)K, (const void*)Knorm})
@@ -2280,7 +2304,7 @@ extern "C" gakco_status gakco_finalize_packed(gakco_plan* p, const void* Cp, int
     CK(p->ensure(p->kdiag, N * 8, s));
     CK(p->ensure(p->flags, 64, s, /*zero=*/true));
     CK(cudaMemsetAsync(p->flags.p, 0, sizeof(int), s));
-    CK(launch_epilogue_packed(Cp, in_bytes, Cdiag, N, begin, end, p->g, p->k, p->M, Nm, K, Knorm,
+    CK(launch_epilogue_packed(Cp, in_bytes, ld, Cdiag, N, begin, end, p->g, p->k, p->M, Nm, K, Knorm,
                               (int64_t*)p->kdiag.p, (int*)p->flags.p, s));
     int fl[2] = {0, 0};
     CK(cudaMemcpyAsync(fl, p->flags.p, 2 * sizeof(int), cudaMemcpyDeviceToHost, s));

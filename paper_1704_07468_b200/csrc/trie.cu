@@ -84,7 +84,18 @@ __global__ void __launch_bounds__(TP_THREADS) tp_hist_kernel(const uint64_t* __r
     }
     const uint64_t nv = a < ch.hi ? (ch.hi - a) / 2 : 0;
     const uint4* v = (const uint4*)(w + a);
-    for (uint64_t i = tid; i < nv; i += TP_THREADS) {
+    uint64_t i = tid;
+    for (; i + 3 * TP_THREADS < nv; i += 4 * TP_THREADS) {  // (4 loads in flight)
+        uint4 q[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) q[u] = v[i + u * TP_THREADS];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            atomicAdd(&s_h[wp][(uint32_t)(((uint64_t)q[u].y << 32 | q[u].x) >> shift) & dmask], 1u);
+            atomicAdd(&s_h[wp][(uint32_t)(((uint64_t)q[u].w << 32 | q[u].z) >> shift) & dmask], 1u);
+        }
+    }
+    for (; i < nv; i += TP_THREADS) {
         const uint4 q = v[i];
         atomicAdd(&s_h[wp][(uint32_t)(((uint64_t)q.y << 32 | q.x) >> shift) & dmask], 1u);
         atomicAdd(&s_h[wp][(uint32_t)(((uint64_t)q.w << 32 | q.z) >> shift) & dmask], 1u);
@@ -135,7 +146,7 @@ template <typename S>
 __global__ void __launch_bounds__(TP_THREADS, 2) tp_scatter_kernel(
     const uint64_t* __restrict__ win, uint64_t* __restrict__ wout, const S* __restrict__ sin,
     S* __restrict__ sout, uint64_t n, const uint32_t* cntp, int shift, uint32_t dmask,
-    uint64_t omask, const uint32_t* __restrict__ H, uint32_t* cnt_out) {
+    uint64_t omask, const uint32_t* __restrict__ H, uint32_t* cnt_out, unsigned long long* stats) {
     extern __shared__ __align__(16) unsigned char smem[];
     constexpr bool PAY = tp_pay<S>();
     constexpr uint32_t WB = TP_TILE * 8 + 32, PB = PAY ? TP_TILE * tp_psz<S>() + 32 : 0;
@@ -160,7 +171,10 @@ __global__ void __launch_bounds__(TP_THREADS, 2) tp_scatter_kernel(
     const TpChunk ch = tp_chunk(cnt, cps, c);
     const uint64_t lo = ch.lo, hi = ch.hi;
     const uint32_t ntile = hi > lo ? (uint32_t)((hi - lo + TP_TILE - 1) / TP_TILE) : 0u;
-    if (cnt_out && c == 0 && tid == 0) *cnt_out = (uint32_t)cnt;  // (the output's count)
+    if (c == 0 && tid == 0) {
+        if (cnt_out) *cnt_out = (uint32_t)cnt;  // (the output's count)
+        if (stats) atomicAdd(&stats[ST_PASS_KEYS], (unsigned long long)cnt);
+    }
 
     for (int i = tid; i < 2 * TP_WARPS * TP_ND; i += TP_THREADS) (&s_whist[0][0])[i] = 0u;
     auto issue = [&](uint32_t t, uint64_t* bar) {
@@ -184,10 +198,20 @@ __global__ void __launch_bounds__(TP_THREADS, 2) tp_scatter_kernel(
     {
         const int d = tid & (TP_ND - 1), p = tid >> 6;
         uint32_t tot = 0, pre = 0;
-        for (uint32_t cc = p; cc < cps; cc += TP_THREADS / TP_ND) {
-            const uint32_t v = H[(uint64_t)cc * TP_ND + d];
-            tot += v;
-            pre += cc < c ? v : 0u;
+        constexpr uint32_t ST = TP_THREADS / TP_ND;  // 8 chunk strides
+        // (8 independent loads in flight per round trip: the chunk rows are L2 reads)
+        for (uint32_t c0 = p; c0 < cps; c0 += 8 * ST) {
+            uint32_t v[8];
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                const uint32_t cc = c0 + u * ST;
+                v[u] = cc < cps ? H[(uint64_t)cc * TP_ND + d] : 0u;
+            }
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                tot += v[u];
+                pre += c0 + u * ST < c ? v[u] : 0u;
+            }
         }
         s_part[p][d] = tot;
         s_part[8 + p][d] = pre;
@@ -318,7 +342,7 @@ cudaError_t launch_tp_records(const uint64_t* in, uint64_t* out, uint64_t n, con
     cudaFuncSetAttribute(tp_scatter_kernel<TpNoPay>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)tp_smem<TpNoPay>());
     tp_scatter_kernel<TpNoPay><<<cps, TP_THREADS, tp_smem<TpNoPay>(), s>>>(
-        in, out, nullptr, nullptr, n, cntp, shift, 63u, ~0ull, H, nullptr);
+        in, out, nullptr, nullptr, n, cntp, shift, 63u, ~0ull, H, nullptr, nullptr);
     return cudaGetLastError();
 }
 
@@ -329,7 +353,7 @@ bool trie_pass64_ok(uint32_t dmask) { return dmask < (uint32_t)TP_ND; }
 cudaError_t launch_trie_pass64(const uint64_t* win, uint64_t* wout, const void* sin, void* sout,
                                bool seq16, uint64_t n, const uint32_t* cntp, int shift,
                                uint32_t dmask, uint64_t omask, uint32_t* H, int target_ctas,
-                               cudaStream_t s, uint32_t* cnt_out) {
+                               cudaStream_t s, uint32_t* cnt_out, unsigned long long* stats) {
     if (n == 0) return cudaGetLastError();
     const uint64_t tiles = (n + TP_TILE - 1) / TP_TILE;
     const unsigned cps = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(tiles, target_ctas));
@@ -340,12 +364,12 @@ cudaError_t launch_trie_pass64(const uint64_t* win, uint64_t* wout, const void* 
         cudaFuncSetAttribute(tp_scatter_kernel<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)tp_smem<uint16_t>());
         tp_scatter_kernel<uint16_t><<<cps, TP_THREADS, tp_smem<uint16_t>(), s>>>(
-            win, wout, (const uint16_t*)sin, (uint16_t*)sout, n, cntp, shift, dmask, omask, H, cnt_out);
+            win, wout, (const uint16_t*)sin, (uint16_t*)sout, n, cntp, shift, dmask, omask, H, cnt_out, stats);
     } else {
         cudaFuncSetAttribute(tp_scatter_kernel<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)tp_smem<uint32_t>());
         tp_scatter_kernel<uint32_t><<<cps, TP_THREADS, tp_smem<uint32_t>(), s>>>(
-            win, wout, (const uint32_t*)sin, (uint32_t*)sout, n, cntp, shift, dmask, omask, H, cnt_out);
+            win, wout, (const uint32_t*)sin, (uint32_t*)sout, n, cntp, shift, dmask, omask, H, cnt_out, stats);
     }
     return cudaGetLastError();
 }

@@ -62,7 +62,8 @@ class gakco_stats(ctypes.Structure):
             "n_encode", "n_sort", "n_segment", "n_light", "n_heavy", "n_epilogue", "keys32",
             "sort_passes32", "grouping")] + [("ms_dense", ctypes.c_double)] + [
         (n, ctypes.c_int64) for n in ("n_dense", "n_pad", "gram_fp4", "heavy_macs_fp4",
-                                        "win_groups", "win_macs", "far_records")]
+                                        "win_groups", "win_macs", "far_records")] + [
+        ("ms_far", ctypes.c_double), ("n_far", ctypes.c_int64), ("pass_keys", ctypes.c_int64)]
 
     def as_dict(self):
         return {n: getattr(self, n) for n, _ in self._fields_}
@@ -99,7 +100,7 @@ def lib():
         L.gakco_level_order.restype = ci
         L.gakco_pack_upper.argtypes = [P, P, i64, ci, i64, i64, P, ci, P]
         L.gakco_diag.argtypes = [P, P, i64, ci, P, P]
-        L.gakco_finalize_packed.argtypes = [P, P, ci, i64, i64, i64, P, P, P, P, P]
+        L.gakco_finalize_packed.argtypes = [P, P, ci, i64, i64, i64, i64, P, P, P, P, P]
         L.gakco_num_masks.argtypes = [P, ci]
         L.gakco_num_masks.restype = i64
         L.gakco_last_error.argtypes = [P]
@@ -215,9 +216,9 @@ def gakco_diag(plan, C, N, levels, out, stream=None):
     _check(plan, lib().gakco_diag(plan, _ptr(C), N, levels, _ptr(out), _stream(stream)))
 
 
-def gakco_finalize_packed(plan, Cp, in_bytes, N, begin, end, Cdiag, Nm=None, K=None, Knorm=None,
-                          stream=None):
-    _check(plan, lib().gakco_finalize_packed(plan, _ptr(Cp), in_bytes, N, begin, end,
+def gakco_finalize_packed(plan, Cp, in_bytes, ld, N, begin, end, Cdiag, Nm=None, K=None,
+                          Knorm=None, stream=None):
+    _check(plan, lib().gakco_finalize_packed(plan, _ptr(Cp), in_bytes, ld, N, begin, end,
                                              _ptr(Cdiag), _ptr(Nm), _ptr(K), _ptr(Knorm),
                                              _stream(stream)))
 
@@ -276,9 +277,9 @@ class Plan:
     def diag(self, C, N, levels, out, stream=None):
         gakco_diag(self.h, C, N, levels, out, stream)
 
-    def finalize_packed(self, Cp, in_bytes, N, begin, end, Cdiag, Nm=None, K=None, Knorm=None,
+    def finalize_packed(self, Cp, in_bytes, ld, N, begin, end, Cdiag, Nm=None, K=None, Knorm=None,
                         stream=None):
-        gakco_finalize_packed(self.h, Cp, in_bytes, N, begin, end, Cdiag, Nm, K, Knorm, stream)
+        gakco_finalize_packed(self.h, Cp, in_bytes, ld, N, begin, end, Cdiag, Nm, K, Knorm, stream)
 
     def num_masks(self, shard_only=False):
         return gakco_num_masks(self.h, shard_only)

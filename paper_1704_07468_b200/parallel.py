@@ -146,8 +146,8 @@ class ShardedStep:
                 self._reduce_scatter(self.Cp[m], self.pack[m])
             plan.diag(C, N, L, self.D, cs)
             self._all_reduce(self.D)
-            plan.finalize_packed(self.Cp, self.wb, N, self.begin, self.end, self.D, self.Nm,
-                                 self.K, self.Knorm, cs)
+            plan.finalize_packed(self.Cp, self.wb, self.chunk, N, self.begin, self.end, self.D,
+                                 self.Nm, self.K, self.Knorm, cs)
         if self.cuda:
             (stream or self.torch.cuda.current_stream(self.dev)).wait_stream(cs)
         return self.begin, self.end

@@ -58,7 +58,7 @@ class MockPlan:
         for lv in range(levels):
             out[lv] = __import__("torch").from_numpy(np.diagonal(c[lv]).copy())
 
-    def finalize_packed(self, Cp, in_bytes, N, begin, end, Cdiag, Nm=None, K=None, Knorm=None,
+    def finalize_packed(self, Cp, in_bytes, ld, N, begin, end, Cdiag, Nm=None, K=None, Knorm=None,
                         stream=None):
         g, k, M = self.g, self.k, self.M
         h = [comb(g - m, k) if m <= g - k else 0 for m in range(M + 1)]

@@ -809,7 +809,7 @@ def test_sharded_packed_emulation(gk, oracle_lib):
                 K = torch.empty((chunk,), dtype=torch.int64, device="cuda")
                 Kn = torch.empty((chunk,), dtype=torch.float64, device="cuda")
                 plan = gk.Plan(cp.sigma, g, k, M)
-                plan.finalize_packed(Cp, wb, N, b, e, D, Nm, K, Kn)
+                plan.finalize_packed(Cp, wb, chunk, N, b, e, D, Nm, K, Kn)
                 plan.close()
                 slices.append((b, e, {"C": Cp[:, : e - b].long().cpu().numpy(),
                                       "Nm": Nm[:, : e - b].cpu().numpy(),

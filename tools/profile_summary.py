@@ -36,7 +36,7 @@ STAGE = {"encode_kernel": "encode", "encode_win_kernel": "encode", "window_kerne
          "trie_root_kernel": "encode", "window_build_kernel": "dense", "window_round_kernel": "dense",
          "window_reset_kernel": "heavy", "window_flush_kernel": "light",
          "tp_hist_kernel": "sort", "tp_scatter_kernel": "sort", "segment_rag_kernel": "segment",
-         "far_add_kernel": "light", "fill_u32_kernel": "sort", "pack_upper_kernel": "exchange",
+         "far_add_kernel": "far", "far_gate_kernel": "far", "far_reset_kernel": "far", "fill_u32_kernel": "sort", "pack_upper_kernel": "exchange",
          "diag_kernel": "exchange", "epilogue_packed_kernel": "epilogue",
          "kdiag_rect_kernel": "epilogue"}
 
@@ -45,6 +45,7 @@ def short(name):
     n = name.strip()
     if n.startswith("void "):
         n = n[5:]
+    n = n.replace("(anonymous namespace)::", "").replace("<unnamed>::", "").replace("unnamed>::", "")
     cut = min([i for i in (n.find("<"), n.find("(")) if i >= 0] or [len(n)])
     return n[:cut].split("::")[-1]
 

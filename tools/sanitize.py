@@ -77,7 +77,7 @@ def main():
         plan.close()
     plan = gk.Plan(cp.sigma, g, k, M)
     Kp = torch.empty((chunk,), dtype=torch.int64, device="cuda")
-    plan.finalize_packed(packs[:, :chunk].contiguous(), 4, N, 0, chunk, D, None, Kp, None)
+    plan.finalize_packed(packs[:, :chunk].contiguous(), 4, chunk, N, 0, chunk, D, None, Kp, None)
     plan.close()
     iu = np.triu_indices(N)
     assert np.array_equal(Kp.cpu().numpy(), ref["K"][iu][:chunk])
