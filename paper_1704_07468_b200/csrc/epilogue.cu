@@ -279,9 +279,9 @@ cudaError_t launch_epilogue_rect(const int64_t* C, const int64_t* Dg, int64_t N,
 // One CTA per row X0 + blockIdx.x.
 template <int MM, typename T>
 __global__ void __launch_bounds__(256) epilogue_packed_kernel(
-    const T* __restrict__ Cp, int64_t ld, int64_t N, int64_t begin, int64_t cnt, int64_t X0, int g,
-    int k, int M, int64_t* Nm, int64_t* K, double* Knorm, const int64_t* __restrict__ kdiag,
-    int* flags, const __grid_constant__ EpiCoef cf) {
+    const T* __restrict__ Cp, int nsrc, int64_t ld, int64_t N, int64_t begin, int64_t cnt,
+    int64_t X0, int g, int k, int M, int64_t* Nm, int64_t* K, double* Knorm,
+    const int64_t* __restrict__ kdiag, int* flags, const __grid_constant__ EpiCoef cf) {
     const int64_t X = X0 + blockIdx.x;
     const int64_t R = X * N - X * (X - 1) / 2;
     const int64_t lo = max(R, begin), hi = min(R + (N - X), begin + cnt);
@@ -292,7 +292,11 @@ __global__ void __launch_bounds__(256) epilogue_packed_kernel(
         int64_t prof[MM + 1];
 #pragma unroll
         for (int m = 0; m <= MM; ++m)
-            if (m <= M) prof[m] = (int64_t)Cp[(size_t)m * ld + i];
+            if (m <= M) {  // (nsrc > 1: the ranks' contributions, summed here)
+                int64_t v = 0;
+                for (int q = 0; q < nsrc; ++q) v += (int64_t)Cp[((size_t)q * (M + 1) + m) * ld + i];
+                prof[m] = v;
+            }
         const int64_t kv = entry<MM>(prof, cf, g, k, M, &bad);
         if (Nm) {
 #pragma unroll
@@ -308,24 +312,24 @@ __global__ void __launch_bounds__(256) epilogue_packed_kernel(
 int64_t tri_row_of(int64_t e, int64_t N);  // shard.cu
 
 template <typename T>
-static void epi_packed(const T* Cp, int64_t ld, int64_t N, int64_t begin, int64_t cnt, int64_t X0,
+static void epi_packed(const T* Cp, int nsrc, int64_t ld, int64_t N, int64_t begin, int64_t cnt, int64_t X0,
                        unsigned rows, int g, int k, int M, int64_t* Nm, int64_t* K, double* Knorm,
                        const int64_t* kdiag, int* flags, const EpiCoef& cf, cudaStream_t s) {
     if (M <= 3)
-        epilogue_packed_kernel<3, T><<<rows, 256, 0, s>>>(Cp, ld, N, begin, cnt, X0, g, k, M, Nm, K,
+        epilogue_packed_kernel<3, T><<<rows, 256, 0, s>>>(Cp, nsrc, ld, N, begin, cnt, X0, g, k, M, Nm, K,
                                                           Knorm, kdiag, flags, cf);
     else if (M <= 5)
-        epilogue_packed_kernel<5, T><<<rows, 256, 0, s>>>(Cp, ld, N, begin, cnt, X0, g, k, M, Nm, K,
+        epilogue_packed_kernel<5, T><<<rows, 256, 0, s>>>(Cp, nsrc, ld, N, begin, cnt, X0, g, k, M, Nm, K,
                                                           Knorm, kdiag, flags, cf);
     else if (M <= 7)
-        epilogue_packed_kernel<7, T><<<rows, 256, 0, s>>>(Cp, ld, N, begin, cnt, X0, g, k, M, Nm, K,
+        epilogue_packed_kernel<7, T><<<rows, 256, 0, s>>>(Cp, nsrc, ld, N, begin, cnt, X0, g, k, M, Nm, K,
                                                           Knorm, kdiag, flags, cf);
     else
-        epilogue_packed_kernel<GMAX, T><<<rows, 256, 0, s>>>(Cp, ld, N, begin, cnt, X0, g, k, M, Nm,
+        epilogue_packed_kernel<GMAX, T><<<rows, 256, 0, s>>>(Cp, nsrc, ld, N, begin, cnt, X0, g, k, M, Nm,
                                                              K, Knorm, kdiag, flags, cf);
 }
 
-cudaError_t launch_epilogue_packed(const void* Cp, int in_bytes, int64_t ld, const int64_t* Dg, int64_t N,
+cudaError_t launch_epilogue_packed(const void* Cp, int in_bytes, int nsrc, int64_t ld, const int64_t* Dg, int64_t N,
                                    int64_t begin, int64_t end, int g, int k, int M, int64_t* Nm,
                                    int64_t* K, double* Knorm, int64_t* kdiag, int* flags,
                                    cudaStream_t s) {
@@ -338,10 +342,10 @@ cudaError_t launch_epilogue_packed(const void* Cp, int in_bytes, int64_t ld, con
     const int64_t X0 = tri_row_of(begin, N), X1 = tri_row_of(end - 1, N);
     const unsigned rows = (unsigned)(X1 - X0 + 1);
     if (in_bytes == 8)
-        epi_packed<int64_t>((const int64_t*)Cp, ld, N, begin, end - begin, X0, rows, g, k, M, Nm, K,
+        epi_packed<int64_t>((const int64_t*)Cp, nsrc, ld, N, begin, end - begin, X0, rows, g, k, M, Nm, K,
                             Knorm, kdiag, flags, cf, s);
     else
-        epi_packed<uint32_t>((const uint32_t*)Cp, ld, N, begin, end - begin, X0, rows, g, k, M, Nm, K,
+        epi_packed<uint32_t>((const uint32_t*)Cp, nsrc, ld, N, begin, end - begin, X0, rows, g, k, M, Nm, K,
                              Knorm, kdiag, flags, cf, s);
     return cudaGetLastError();
 }

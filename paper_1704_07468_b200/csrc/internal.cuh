@@ -420,6 +420,13 @@ cudaError_t launch_epilogue(int64_t* C, int64_t N, int g, int k, int M, int64_t*
                             double* Knorm, int64_t* kdiag, int* flags, cudaStream_t s);
 
 // ---- mask-sharded step (shard.cu, epilogue.cu) ----
+constexpr int MAX_PEERS = 64;
+struct PeerPtrs {
+    void* p[MAX_PEERS];  // device (peer-mapped) receive buffers, one per rank
+};
+cudaError_t launch_pack_upper_peers(const int64_t* C, int64_t N, int level, int levels,
+                                    int64_t chunk, const PeerPtrs& dst, int src, int out_bytes,
+                                    cudaStream_t s);
 // entries [begin, end) of the packed upper triangle of `levels` N x N matrices -> out
 // [levels][end - begin] as int64 (out_bytes 8) or u32 (4, truncating)
 cudaError_t launch_pack_upper(const int64_t* C, int64_t N, int levels, int64_t begin, int64_t end,
@@ -428,7 +435,7 @@ cudaError_t launch_diag(const int64_t* C, int64_t N, int levels, int64_t* out, i
                         cudaStream_t s);
 // complete packed C slice [M+1][end - begin] (int64 or u32) + complete diagonals Dg
 // [M+1][N] -> packed Nm [M+1][end - begin], K, Knorm [end - begin]; kdiag [N] scratch
-cudaError_t launch_epilogue_packed(const void* Cp, int in_bytes, int64_t ld, const int64_t* Dg, int64_t N,
+cudaError_t launch_epilogue_packed(const void* Cp, int in_bytes, int nsrc, int64_t ld, const int64_t* Dg, int64_t N,
                                    int64_t begin, int64_t end, int g, int k, int M, int64_t* Nm,
                                    int64_t* K, double* Knorm, int64_t* kdiag, int* flags,
                                    cudaStream_t s);

@@ -306,7 +306,6 @@ __global__ void __launch_bounds__(256, MINB) light_kernel(SegmentOut so, int64_t
         // of its members (window Gram); the pairs with a member outside the window (a
         // cluster's group plus a few random members from other clusters) stay on the
         // light path below. Counts > 255, < wmin members inside, or a full window: light.
-        uint32_t split = 0;       // claimed groups that keep their outside pairs
         uint32_t my_win = 0xffffffffu;  // (lane jj: first label of group jj's window)
         if (WIN && wa.nw) {  // (a separate instantiation: no register cost otherwise)
             uint32_t cand = __ballot_sync(0xffffffffu, lane < ng && !flat &&
@@ -351,24 +350,25 @@ __global__ void __launch_bounds__(256, MINB) light_kernel(SegmentOut so, int64_t
                     if (col < wa.cap) {
                         if (lane == 0) wa.list[(uint64_t)w * wa.cap + col] = make_uint2(a0, b0);
                         if (nout == 0) got |= 1u << jj;
-                        else split |= 1u << jj;
-                        if (lane == jj) my_win = lo;
+                        else if (lane == jj) my_win = lo;  // (split: outside pairs below)
                         nwin += lane == 0 ? 1u : 0u;
                     }
                 }
             }
         }
 
-        // (2) the other groups one by one (big light groups)
+        // (2) the other groups one by one (big light groups). Relabelled accumulator:
+        // the sequence ids are turned into labels once per triple as they are loaded
+        // (not per pair)
         uint32_t todo = __ballot_sync(0xffffffffu, lane < ng && !flat) & ~got;
-        (void)split;
+        auto lab = [&](uint32_t x) -> uint32_t { return perm ? perm[x] : x; };
         uint32_t pa0 = 0, pb0 = 0, pX = 0, pC = 0;
         auto prefetch = [&](uint32_t jj) {
             pa0 = __shfl_sync(0xffffffffu, my_start, jj);
             pb0 = __shfl_sync(0xffffffffu, my_end, jj);
             pX = pC = 0;
             if (pa0 + lane < pb0) {
-                pX = so.tseq[pa0 + lane] & 0x7fffffffu;
+                pX = lab(so.tseq[pa0 + lane] & 0x7fffffffu);
                 pC = so.tcnt[pa0 + lane];
             }
         };
@@ -381,9 +381,42 @@ __global__ void __launch_bounds__(256, MINB) light_kernel(SegmentOut so, int64_t
             if (todo) prefetch(__ffs(todo) - 1);  // the next group's first chunk
             const uint32_t s = b0 - a0;
             // a split group (window column claimed): its pairs inside the window
-            // [wl, wl + 256) are on the tensor cores, the rest here
+            // [wl, wl + 256) are on the tensor cores; only the pairs with an outside
+            // member are enumerated, one outsider at a time against all members
             const uint32_t wl = WIN ? __shfl_sync(0xffffffffu, my_win, jcur) : 0xffffffffu;
-            pairs += wl == 0xffffffffu ? (unsigned long long)s * (s - 1) / 2 : 0ull;
+            if (WIN && wl != 0xffffffffu) {
+                for (uint32_t O = a0; O < b0; O += 32) {
+                    const uint32_t io = O + lane;
+                    const bool vo = io < b0;
+                    const uint32_t lO = O == a0 ? xA0 : (vo ? lab(so.tseq[io] & 0x7fffffffu) : 0u);
+                    const uint32_t cO = O == a0 ? cA0 : (vo ? so.tcnt[io] : 0u);
+                    uint32_t om = __ballot_sync(0xffffffffu, vo && lO - wl >= (uint32_t)WIN_ROWS);
+                    while (om) {
+                        const int o = __ffs(om) - 1;
+                        om &= om - 1;
+                        const uint32_t lo_l = __shfl_sync(0xffffffffu, lO, o);
+                        const uint32_t co = __shfl_sync(0xffffffffu, cO, o);
+                        const uint32_t gio = O + o;
+                        for (uint32_t B = a0; B < b0; B += 32) {
+                            const uint32_t ib = B + lane;
+                            const bool vb = ib < b0;
+                            const uint32_t lB = B == a0 ? xA0 : (vb ? lab(so.tseq[ib] & 0x7fffffffu) : 0u);
+                            const uint32_t cB = B == a0 ? cA0 : (vb ? so.tcnt[ib] : 0u);
+                            // each unordered pair once: an inside member, or a later outsider
+                            const bool take = vb && ib != gio &&
+                                              (lB - wl < (uint32_t)WIN_ROWS || ib > gio);
+                            bool ok = false;
+                            uint32_t dist = 0;
+                            const uint64_t idx =
+                                take ? pair_cell(lo_l, lB, N, NA, &ok, nullptr, FAR ? &dist : nullptr) : 0;
+                            lpairs += (ok && take) ? 1u : 0u;
+                            upd(ok && take, idx, co * cB, dist);
+                        }
+                    }
+                }
+                continue;
+            }
+            pairs += (unsigned long long)s * (s - 1) / 2;
             // the group's triples in 32-wide register chunks; pairs enumerated
             // lane-parallel: within a chunk through the triangle table, across
             // chunks as full 32 x 32 blocks (every lane busy on every atomic)
@@ -391,7 +424,7 @@ __global__ void __launch_bounds__(256, MINB) light_kernel(SegmentOut so, int64_t
                 uint32_t xA = xA0, cA = cA0;
                 if (A != a0) {
                     const uint32_t ia = A + lane;
-                    xA = ia < b0 ? (so.tseq[ia] & 0x7fffffffu) : 0u;
+                    xA = ia < b0 ? lab(so.tseq[ia] & 0x7fffffffu) : 0u;
                     cA = ia < b0 ? so.tcnt[ia] : 0u;
                 }
                 const uint32_t na = min(32u, b0 - A);
@@ -405,35 +438,23 @@ __global__ void __launch_bounds__(256, MINB) light_kernel(SegmentOut so, int64_t
                     const uint32_t xb = __shfl_sync(0xffffffffu, xA, b);
                     const uint32_t cb = __shfl_sync(0xffffffffu, cA, b);
                     bool ok = false;
-                    uint32_t dist = 0, lol = 0;
+                    uint32_t dist = 0;
                     const uint64_t idx =
-                        q < P ? pair_cell(xa, xb, N, NA, &ok, perm, (FAR || WIN) ? &dist : nullptr,
-                                          WIN ? &lol : nullptr)
-                              : 0;
-                    if (WIN && wl != 0xffffffffu) {  // (split group: skip in-window pairs)
-                        ok = ok && !(lol - wl < (uint32_t)WIN_ROWS && lol + dist - wl < (uint32_t)WIN_ROWS);
-                        lpairs += (ok && q < P) ? 1u : 0u;
-                    }
+                        q < P ? pair_cell(xa, xb, N, NA, &ok, nullptr, FAR ? &dist : nullptr) : 0;
                     upd(ok && q < P, idx, ca * cb, dist);
                 }
                 for (uint32_t B = A + 32; B < b0; B += 32) {
                     const uint32_t ib = B + lane;
                     const bool vb = ib < b0;
-                    const uint32_t xB = vb ? (so.tseq[ib] & 0x7fffffffu) : 0u;
+                    const uint32_t xB = vb ? lab(so.tseq[ib] & 0x7fffffffu) : 0u;
                     const uint32_t cB = vb ? so.tcnt[ib] : 0u;
                     for (uint32_t a = 0; a < na; ++a) {
                         const uint32_t xa = __shfl_sync(0xffffffffu, xA, a);
                         const uint32_t ca = __shfl_sync(0xffffffffu, cA, a);
                         bool ok = false;
-                        uint32_t dist = 0, lol = 0;
+                        uint32_t dist = 0;
                         const uint64_t idx =
-                            vb ? pair_cell(xa, xB, N, NA, &ok, perm, (FAR || WIN) ? &dist : nullptr,
-                                           WIN ? &lol : nullptr)
-                               : 0;
-                        if (WIN && wl != 0xffffffffu) {
-                            ok = ok && !(lol - wl < (uint32_t)WIN_ROWS && lol + dist - wl < (uint32_t)WIN_ROWS);
-                            lpairs += (ok && vb) ? 1u : 0u;
-                        }
+                            vb ? pair_cell(xa, xB, N, NA, &ok, nullptr, FAR ? &dist : nullptr) : 0;
                         upd(ok && vb, idx, ca * cB, dist);
                     }
                 }

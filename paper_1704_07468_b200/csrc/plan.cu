@@ -2278,10 +2278,31 @@ extern "C" gakco_status gakco_diag(gakco_plan* p, const int64_t* C, int64_t N, i
     return e == cudaSuccess ? GAKCO_OK : p->cuda_fail(e, "diag");
 }
 
+static gakco_status finalize_packed_impl(gakco_plan* p, const void* Cp, int in_bytes, int nsrc,
+                                         int64_t ld, int64_t N, int64_t begin, int64_t end,
+                                         const int64_t* Cdiag, int64_t* Nm, int64_t* K,
+                                         double* Knorm, void* stream);
+
 extern "C" gakco_status gakco_finalize_packed(gakco_plan* p, const void* Cp, int in_bytes,
                                               int64_t ld, int64_t N, int64_t begin, int64_t end,
                                               const int64_t* Cdiag, int64_t* Nm, int64_t* K,
                                               double* Knorm, void* stream) {
+    return finalize_packed_impl(p, Cp, in_bytes, 1, ld, N, begin, end, Cdiag, Nm, K, Knorm, stream);
+}
+
+extern "C" gakco_status gakco_finalize_packed_sum(gakco_plan* p, const void* Cp, int in_bytes,
+                                                  int nsrc, int64_t ld, int64_t N, int64_t begin,
+                                                  int64_t end, const int64_t* Cdiag, int64_t* Nm,
+                                                  int64_t* K, double* Knorm, void* stream) {
+    if (!p) return GAKCO_E_ARG;
+    if (nsrc < 1 || nsrc > MAX_PEERS) return p->fail(GAKCO_E_ARG, "nsrc must be 1..64");
+    return finalize_packed_impl(p, Cp, in_bytes, nsrc, ld, N, begin, end, Cdiag, Nm, K, Knorm, stream);
+}
+
+static gakco_status finalize_packed_impl(gakco_plan* p, const void* Cp, int in_bytes, int nsrc,
+                                         int64_t ld, int64_t N, int64_t begin, int64_t end,
+                                         const int64_t* Cdiag, int64_t* Nm, int64_t* K,
+                                         double* Knorm, void* stream) {
     if (!p) return GAKCO_E_ARG;
     if (N < 1 || N >= ((int64_t)1 << 31)) return p->fail(GAKCO_E_ARG, "N out of range");
     const int64_t T = N * (N + 1) / 2;
@@ -2304,7 +2325,7 @@ extern "C" gakco_status gakco_finalize_packed(gakco_plan* p, const void* Cp, int
     CK(p->ensure(p->kdiag, N * 8, s));
     CK(p->ensure(p->flags, 64, s, /*zero=*/true));
     CK(cudaMemsetAsync(p->flags.p, 0, sizeof(int), s));
-    CK(launch_epilogue_packed(Cp, in_bytes, ld, Cdiag, N, begin, end, p->g, p->k, p->M, Nm, K, Knorm,
+    CK(launch_epilogue_packed(Cp, in_bytes, nsrc, ld, Cdiag, N, begin, end, p->g, p->k, p->M, Nm, K, Knorm,
                               (int64_t*)p->kdiag.p, (int*)p->flags.p, s));
     int fl[2] = {0, 0};
     CK(cudaMemcpyAsync(fl, p->flags.p, 2 * sizeof(int), cudaMemcpyDeviceToHost, s));
@@ -2315,4 +2336,64 @@ extern "C" gakco_status gakco_finalize_packed(gakco_plan* p, const void* Cp, int
     if (fl[0] & EF_NEGATIVE_N) return p->fail(GAKCO_E_INTERNAL, "negative N_m after Eq. 9");
     if (fl[0] & EF_K_MISMATCH) return p->fail(GAKCO_E_INTERNAL, "K != C_{g-k}");
     return GAKCO_OK;
+}
+
+// ---- fused pack + exchange over peer memory (CUDA IPC) ----
+extern "C" gakco_status gakco_ipc_handle(const void* dev_ptr, void* handle_out) {
+    if (!dev_ptr || !handle_out) return GAKCO_E_ARG;
+    cudaIpcMemHandle_t h;
+    cudaError_t e = cudaIpcGetMemHandle(&h, (void*)dev_ptr);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return GAKCO_E_CUDA;
+    }
+    std::memcpy(handle_out, &h, sizeof h);
+    return GAKCO_OK;
+}
+
+extern "C" gakco_status gakco_ipc_open(const void* handle, int device, void** dev_ptr) {
+    if (!handle || !dev_ptr) return GAKCO_E_ARG;
+    DeviceGuard dg(device);
+    cudaIpcMemHandle_t h;
+    std::memcpy(&h, handle, sizeof h);
+    cudaError_t e = cudaIpcOpenMemHandle(dev_ptr, h, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return GAKCO_E_CUDA;
+    }
+    return GAKCO_OK;
+}
+
+extern "C" gakco_status gakco_ipc_close(void* dev_ptr) {
+    if (!dev_ptr) return GAKCO_E_ARG;
+    cudaError_t e = cudaIpcCloseMemHandle(dev_ptr);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return GAKCO_E_CUDA;
+    }
+    return GAKCO_OK;
+}
+
+extern "C" gakco_status gakco_pack_upper_peers(gakco_plan* p, const int64_t* Cm, int64_t N,
+                                               int level, int levels, int64_t chunk,
+                                               void* const* dst, int P, int rank, int out_bytes,
+                                               void* stream) {
+    if (!p) return GAKCO_E_ARG;
+    if (N < 1 || N >= ((int64_t)1 << 31) || levels < 1 || level < 0 || level >= levels)
+        return p->fail(GAKCO_E_ARG, "N / level out of range");
+    if (P < 1 || P > MAX_PEERS || rank < 0 || rank >= P || !dst)
+        return p->fail(GAKCO_E_ARG, "P must be 1..64, rank < P, dst given");
+    if (out_bytes != 4 && out_bytes != 8) return p->fail(GAKCO_E_ARG, "out_bytes must be 4 or 8");
+    if (chunk * P < N * (N + 1) / 2) return p->fail(GAKCO_E_ARG, "chunk * P < N(N+1)/2");
+    if (!is_device_ptr(Cm)) return p->fail(GAKCO_E_ARG, "C must be a device pointer");
+    PeerPtrs pp{};
+    for (int i = 0; i < P; ++i) {
+        if (!dst[i]) return p->fail(GAKCO_E_ARG, "a receive buffer is NULL");
+        pp.p[i] = dst[i];
+    }
+    DeviceGuard dg(p->device);
+    Nvtx nv("gakco_pack_upper_peers");
+    cudaError_t e = launch_pack_upper_peers(Cm, N, level, levels, chunk, pp, rank, out_bytes,
+                                            (cudaStream_t)stream);
+    return e == cudaSuccess ? GAKCO_OK : p->cuda_fail(e, "pack_upper_peers");
 }

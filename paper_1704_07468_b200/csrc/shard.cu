@@ -55,6 +55,37 @@ __global__ void diag_kernel(const int64_t* __restrict__ C, int64_t N, int levels
     }
 }
 
+// Fused pack + exchange: level `level` of this rank's C, packed, goes
+// straight into the OWNER's receive buffer over NVLink (peer-mapped pointers from
+// CUDA IPC): entry e belongs to rank d = e / chunk and lands at
+// dst[d][(src * levels + level) * chunk + e - d * chunk]; the owner sums the P
+// contributions inside its epilogue (epilogue_packed_kernel with nsrc = P).
+template <typename T>
+__global__ void __launch_bounds__(256) pack_upper_peers_kernel(const int64_t* __restrict__ C, int64_t N,
+                                                               int level, int levels, int64_t chunk,
+                                                               PeerPtrs dst, int src) {
+    const int64_t X = blockIdx.x;
+    const int64_t R = tri_row_start(X, N);
+    const int64_t* row = C + (size_t)X * (size_t)N + X - R;
+    const int64_t hi = R + (N - X);
+    for (int64_t e = R + threadIdx.x; e < hi; e += blockDim.x) {
+        const int64_t d = e / chunk;
+        T* out = (T*)dst.p[d];
+        out[((int64_t)src * levels + level) * chunk + (e - d * chunk)] = (T)row[e];
+    }
+}
+
+cudaError_t launch_pack_upper_peers(const int64_t* C, int64_t N, int level, int levels,
+                                    int64_t chunk, const PeerPtrs& dst, int src, int out_bytes,
+                                    cudaStream_t s) {
+    if (N <= 0) return cudaGetLastError();
+    if (out_bytes == 8)
+        pack_upper_peers_kernel<int64_t><<<(unsigned)N, 256, 0, s>>>(C, N, level, levels, chunk, dst, src);
+    else
+        pack_upper_peers_kernel<uint32_t><<<(unsigned)N, 256, 0, s>>>(C, N, level, levels, chunk, dst, src);
+    return cudaGetLastError();
+}
+
 cudaError_t launch_pack_upper(const int64_t* C, int64_t N, int levels, int64_t begin, int64_t end,
                               void* out, int out_bytes, cudaStream_t s) {
     if (end <= begin || levels <= 0) return cudaGetLastError();
