@@ -292,6 +292,42 @@ gakco_status gakco_finalize_packed(gakco_plan* plan, const void* Cp, int in_byte
                                    int64_t N, int64_t begin, int64_t end, const int64_t* Cdiag, int64_t* Nm,
                                    int64_t* K, double* Knorm, void* cuda_stream);
 
+/* ---- The same exchange fused into the pack, over peer memory (CUDA IPC) ----
+ * Instead of pack + NCCL reduce-scatter: every rank allocates a receive buffer
+ * R[P][M+1][chunk] (gakco_ipc_alloc: cudaMalloc, so the IPC handle maps the buffer
+ * itself), the ranks exchange the 64-byte handles (e.g. torch.distributed
+ * all_gather_object) and open each other's (gakco_ipc_open: peer-mapped device
+ * pointers over NVLink / NVSwitch). gakco_pack_upper_peers then writes level m of
+ * this rank's C straight into the owners' buffers; after every rank's packs are
+ * complete (the caller synchronises its stream and barriers), each rank runs
+ * gakco_finalize_packed_sum on its own buffer, which adds the P contributions
+ * inside the epilogue. */
+gakco_status gakco_ipc_alloc(size_t bytes, int device, void** dev_ptr, void* handle_out /*64 B*/);
+gakco_status gakco_ipc_free(void* dev_ptr);
+/* handle of the allocation containing dev_ptr (the allocation's base must be dev_ptr) */
+gakco_status gakco_ipc_handle(const void* dev_ptr, void* handle_out /*64 B*/);
+/* map another process's buffer on `device`; close with gakco_ipc_close */
+gakco_status gakco_ipc_open(const void* handle /*64 B*/, int device, void** dev_ptr);
+gakco_status gakco_ipc_close(void* dev_ptr);
+
+/* Level `level` (of `levels`) of this rank's upper-triangular C_m (DEVICE int64 N x N)
+ * into the receive buffers dst[0..P-1] (a HOST array of device pointers, peer-mapped):
+ * packed entry e goes to rank d = e / chunk at
+ *   dst[d][(rank * levels + level) * chunk + e - d * chunk]
+ * as int64 (out_bytes 8) or u32 (4; values below 2^31). chunk * P >= N(N+1)/2.
+ * Enqueued on cuda_stream. */
+gakco_status gakco_pack_upper_peers(gakco_plan* plan, const int64_t* Cm, int64_t N, int level,
+                                    int levels, int64_t chunk, void* const* dst, int P, int rank,
+                                    int out_bytes, void* cuda_stream);
+
+/* gakco_finalize_packed over nsrc contributions: level m of source q at
+ * Cp + (q * (M+1) + m) * ld (elements); C_m = their sum (the receive buffer of the
+ * fused exchange, nsrc = P). Same outputs, synchronisation and errors. */
+gakco_status gakco_finalize_packed_sum(gakco_plan* plan, const void* Cp, int in_bytes, int nsrc,
+                                       int64_t ld, int64_t N, int64_t begin, int64_t end,
+                                       const int64_t* Cdiag, int64_t* Nm, int64_t* K,
+                                       double* Knorm, void* cuda_stream);
+
 /* Counters and (if GAKCO_OPT_TIMING) stage times of the last accumulate /
  * finalize. Synchronises the plan's last stream. */
 gakco_status gakco_get_stats(gakco_plan* plan, gakco_stats* out);

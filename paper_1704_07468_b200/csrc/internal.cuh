@@ -322,7 +322,7 @@ struct WinArgs {
 // REDs). fill[0] counts reserved record slots (chunks of FAR_CHUNK; every reserved
 // slot is written, unused ones with 0); a chunk past cap is never reserved (the warp
 // falls back to REDs). near = 0: off.
-constexpr uint32_t FAR_CHUNK = 1024;
+constexpr uint32_t FAR_CHUNK = 256;
 struct FarRec {
     uint64_t* rec;     // [cap] records
     uint32_t* fill;    // [0] slots reserved (all warps), [1] the count an apply processes

@@ -2339,6 +2339,32 @@ static gakco_status finalize_packed_impl(gakco_plan* p, const void* Cp, int in_b
 }
 
 // ---- fused pack + exchange over peer memory (CUDA IPC) ----
+extern "C" gakco_status gakco_ipc_alloc(size_t bytes, int device, void** dev_ptr, void* handle_out) {
+    if (!dev_ptr || !handle_out || bytes == 0) return GAKCO_E_ARG;
+    DeviceGuard dg(device);
+    *dev_ptr = nullptr;
+    cudaError_t e = cudaMalloc(dev_ptr, bytes);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        return e == cudaErrorMemoryAllocation ? GAKCO_E_NOMEM : GAKCO_E_CUDA;
+    }
+    cudaIpcMemHandle_t h;
+    e = cudaIpcGetMemHandle(&h, *dev_ptr);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        cudaFree(*dev_ptr);
+        *dev_ptr = nullptr;
+        return GAKCO_E_CUDA;
+    }
+    std::memcpy(handle_out, &h, sizeof h);
+    return GAKCO_OK;
+}
+
+extern "C" gakco_status gakco_ipc_free(void* dev_ptr) {
+    if (!dev_ptr) return GAKCO_E_ARG;
+    return cudaFree(dev_ptr) == cudaSuccess ? GAKCO_OK : GAKCO_E_CUDA;
+}
+
 extern "C" gakco_status gakco_ipc_handle(const void* dev_ptr, void* handle_out) {
     if (!dev_ptr || !handle_out) return GAKCO_E_ARG;
     cudaIpcMemHandle_t h;

@@ -49,7 +49,9 @@ GAKCO_OPT_XL_COMPACT = 18
 EXPORTS = ("gakco_create", "gakco_set_shard", "gakco_set_option", "gakco_accumulate",
            "gakco_finalize", "gakco_kernel", "gakco_kernel_k", "gakco_kernel_rect",
            "gakco_get_stats", "gakco_stream_wait_level", "gakco_level_order", "gakco_pack_upper",
-           "gakco_diag", "gakco_finalize_packed",
+           "gakco_diag", "gakco_finalize_packed", "gakco_finalize_packed_sum", "gakco_ipc_alloc",
+           "gakco_ipc_free", "gakco_ipc_handle", "gakco_ipc_open", "gakco_ipc_close",
+           "gakco_pack_upper_peers",
            "gakco_num_masks", "gakco_last_error", "gakco_status_string", "gakco_destroy")
 
 
@@ -101,6 +103,13 @@ def lib():
         L.gakco_pack_upper.argtypes = [P, P, i64, ci, i64, i64, P, ci, P]
         L.gakco_diag.argtypes = [P, P, i64, ci, P, P]
         L.gakco_finalize_packed.argtypes = [P, P, ci, i64, i64, i64, i64, P, P, P, P, P]
+        L.gakco_finalize_packed_sum.argtypes = [P, P, ci, ci, i64, i64, i64, i64, P, P, P, P, P]
+        L.gakco_ipc_alloc.argtypes = [ctypes.c_size_t, ci, ctypes.POINTER(P), P]
+        L.gakco_ipc_free.argtypes = [P]
+        L.gakco_ipc_handle.argtypes = [P, P]
+        L.gakco_ipc_open.argtypes = [P, ci, ctypes.POINTER(P)]
+        L.gakco_ipc_close.argtypes = [P]
+        L.gakco_pack_upper_peers.argtypes = [P, P, i64, ci, ci, i64, ctypes.POINTER(P), ci, ci, ci, P]
         L.gakco_num_masks.argtypes = [P, ci]
         L.gakco_num_masks.restype = i64
         L.gakco_last_error.argtypes = [P]
@@ -112,7 +121,9 @@ def lib():
         for f in ("gakco_create", "gakco_set_shard", "gakco_set_option", "gakco_accumulate",
                   "gakco_finalize", "gakco_kernel", "gakco_kernel_k", "gakco_kernel_rect",
                   "gakco_get_stats", "gakco_stream_wait_level", "gakco_pack_upper",
-                  "gakco_diag", "gakco_finalize_packed"):
+                  "gakco_diag", "gakco_finalize_packed", "gakco_finalize_packed_sum",
+                  "gakco_ipc_alloc", "gakco_ipc_free", "gakco_ipc_handle", "gakco_ipc_open",
+                  "gakco_ipc_close", "gakco_pack_upper_peers"):
             getattr(L, f).restype = ci
         _lib = L
     return _lib
@@ -223,6 +234,47 @@ def gakco_finalize_packed(plan, Cp, in_bytes, ld, N, begin, end, Cdiag, Nm=None,
                                              _stream(stream)))
 
 
+def gakco_finalize_packed_sum(plan, Cp, in_bytes, nsrc, ld, N, begin, end, Cdiag, Nm=None,
+                              K=None, Knorm=None, stream=None):
+    _check(plan, lib().gakco_finalize_packed_sum(plan, _ptr(Cp), in_bytes, nsrc, ld, N, begin, end,
+                                                 _ptr(Cdiag), _ptr(Nm), _ptr(K), _ptr(Knorm),
+                                                 _stream(stream)))
+
+
+def gakco_pack_upper_peers(plan, Cm, N, level, levels, chunk, dst, P, rank, out_bytes, stream=None):
+    arr = (ctypes.c_void_p * P)(*[int(d) for d in dst])
+    _check(plan, lib().gakco_pack_upper_peers(plan, _ptr(Cm), N, level, levels, chunk, arr, P,
+                                              rank, out_bytes, _stream(stream)))
+
+
+def _ipc_check(st, what):
+    if st != GAKCO_OK:
+        raise GakcoError(st, what + ": " + lib().gakco_status_string(st).decode())
+
+
+def gakco_ipc_alloc(nbytes, device=0):
+    """(device pointer, 64-byte IPC handle) of a new cudaMalloc buffer."""
+    ptr = ctypes.c_void_p()
+    h = ctypes.create_string_buffer(64)
+    _ipc_check(lib().gakco_ipc_alloc(nbytes, device, ctypes.byref(ptr), h), "ipc_alloc")
+    return ptr.value, h.raw
+
+
+def gakco_ipc_free(ptr):
+    _ipc_check(lib().gakco_ipc_free(ptr), "ipc_free")
+
+
+def gakco_ipc_open(handle, device=0):
+    ptr = ctypes.c_void_p()
+    _ipc_check(lib().gakco_ipc_open(ctypes.create_string_buffer(bytes(handle), 64), device,
+                                    ctypes.byref(ptr)), "ipc_open")
+    return ptr.value
+
+
+def gakco_ipc_close(ptr):
+    _ipc_check(lib().gakco_ipc_close(ptr), "ipc_close")
+
+
 def gakco_num_masks(plan, shard_only=False):
     return int(lib().gakco_num_masks(plan, 1 if shard_only else 0))
 
@@ -276,6 +328,14 @@ class Plan:
 
     def diag(self, C, N, levels, out, stream=None):
         gakco_diag(self.h, C, N, levels, out, stream)
+
+    def pack_upper_peers(self, Cm, N, level, levels, chunk, dst, P, rank, out_bytes, stream=None):
+        gakco_pack_upper_peers(self.h, Cm, N, level, levels, chunk, dst, P, rank, out_bytes, stream)
+
+    def finalize_packed_sum(self, Cp, in_bytes, nsrc, ld, N, begin, end, Cdiag, Nm=None, K=None,
+                            Knorm=None, stream=None):
+        gakco_finalize_packed_sum(self.h, Cp, in_bytes, nsrc, ld, N, begin, end, Cdiag, Nm, K,
+                                  Knorm, stream)
 
     def finalize_packed(self, Cp, in_bytes, ld, N, begin, end, Cdiag, Nm=None, K=None, Knorm=None,
                         stream=None):

@@ -80,7 +80,7 @@ class ShardedStep:
     """
 
     def __init__(self, plan, N, g, k, M, nmax, device, group=None, backend=None,
-                 outputs=True):
+                 outputs=True, exchange="auto"):
         import torch
         import torch.distributed as dist
         self.torch, self.dist = torch, dist
@@ -104,6 +104,58 @@ class ShardedStep:
         self.K = torch.empty((self.chunk,), dtype=torch.int64, device=self.dev)
         self.Knorm = torch.empty((self.chunk,), dtype=torch.float64, device=self.dev) if outputs else None
         self.comm = torch.cuda.Stream(self.dev) if self.cuda else None
+        # exchange: "p2p" = pack fused with the transfer over peer memory (CUDA IPC:
+        # gakco_pack_upper_peers into the owners' receive buffers, the P contributions
+        # summed inside gakco_finalize_packed_sum); "collective" = pack + reduce-scatter
+        self.exchange = "collective"
+        self._ipc_own, self._ipc_open = [], []
+        if exchange in ("auto", "p2p") and self.cuda and self.world > 1 and \
+                hasattr(plan, "pack_upper_peers"):
+            try:
+                self._setup_p2p()
+                self.exchange = "p2p"
+            except Exception:  # noqa: BLE001  (no IPC / peer access: the collective path)
+                if exchange == "p2p":
+                    raise
+                self.close()
+        self.parity = 0
+
+    def _setup_p2p(self):
+        from paper_1704_07468_b200 import gakco
+        L, P = self.M + 1, self.world
+        nbytes = P * L * self.chunk * self.wb
+        dev = self.dev.index or 0
+        mine = []
+        for _ in range(2):  # two buffers: a step's packs never overwrite what a slower
+            ptr, h = gakco.gakco_ipc_alloc(nbytes, dev)  # peer is still reading
+            self._ipc_own.append(ptr)
+            mine.append(h)
+        allh = [None] * P
+        self.dist.all_gather_object(allh, mine, group=self.group)
+        self.dst = [[0] * P for _ in range(2)]
+        for q in range(2):
+            for d in range(P):
+                if d == self.rank:
+                    self.dst[q][d] = self._ipc_own[q]
+                else:
+                    ptr = gakco.gakco_ipc_open(allh[d][q], dev)
+                    self._ipc_open.append(ptr)
+                    self.dst[q][d] = ptr
+
+    def close(self):
+        """Release the peer mappings and receive buffers of the p2p exchange."""
+        from paper_1704_07468_b200 import gakco
+        for ptr in self._ipc_open:
+            try:
+                gakco.gakco_ipc_close(ptr)
+            except Exception:  # noqa: BLE001
+                pass
+        for ptr in self._ipc_own:
+            try:
+                gakco.gakco_ipc_free(ptr)
+            except Exception:  # noqa: BLE001
+                pass
+        self._ipc_open, self._ipc_own = [], []
 
     # -- collectives (NCCL on the device; gloo through host memory)
     def _reduce_scatter(self, out, inp):
@@ -139,6 +191,8 @@ class ShardedStep:
         C.zero_()
         plan.accumulate(codes, offsets, N, C, stream)
         cs = self.comm
+        if self.exchange == "p2p":
+            return self._step_p2p(C, stream)
         with self._on_comm(), self._nvtx("sharded exchange + slice epilogue"):
             for m in plan.level_order():
                 plan.stream_wait_level(m, cs)
@@ -151,6 +205,48 @@ class ShardedStep:
         if self.cuda:
             (stream or self.torch.cuda.current_stream(self.dev)).wait_stream(cs)
         return self.begin, self.end
+
+    def _step_p2p(self, C, stream):
+        plan, N, L, P, cs = self.plan, self.N, self.M + 1, self.world, self.comm
+        q = self.parity
+        with self._on_comm(), self._nvtx("p2p exchange + slice epilogue"):
+            for m in plan.level_order():  # each level straight into its owners' buffers
+                plan.stream_wait_level(m, cs)
+                plan.pack_upper_peers(C[m], N, m, L, self.chunk, self.dst[q], P, self.rank,
+                                      self.wb, cs)
+            plan.diag(C, N, L, self.D, cs)
+            self._all_reduce(self.D)
+        cs.synchronize()      # this rank's writes into every owner are complete ...
+        self.dist.barrier(group=self.group)  # ... and every other rank's into ours
+        with self._on_comm():
+            plan.finalize_packed_sum(self._ipc_own[q], self.wb, P, self.chunk, N, self.begin,
+                                     self.end, self.D, self.Nm, self.K, self.Knorm, cs)
+        (stream or self.torch.cuda.current_stream(self.dev)).wait_stream(cs)
+        self.parity ^= 1
+        return self.begin, self.end
+
+    def complete_C(self):
+        """This rank's slice of the complete C (M+1, end - begin) on the device (for the
+        p2p exchange the sum of the receive buffer's contributions)."""
+        cnt = self.end - self.begin
+        if self.exchange != "p2p":
+            return self.Cp[:, :cnt].long()
+        from paper_1704_07468_b200 import gakco  # noqa: F401
+        wdt = self.torch.int32 if self.wb == 4 else self.torch.int64
+        q = self.parity ^ 1  # the buffer of the last step
+        nel = self.world * (self.M + 1) * self.chunk
+        buf = _tensor_from_ptr(self.torch, self._ipc_own[q], nel, wdt, self.dev)
+        return buf.view(self.world, self.M + 1, self.chunk)[:, :, :cnt].long().sum(0)
+
+
+def _tensor_from_ptr(torch, ptr, nel, dtype, dev):
+    """A torch view of device memory owned by libgakco (test / inspection only)."""
+    class _Arr:
+        pass
+    a = _Arr()
+    a.__cuda_array_interface__ = {"shape": (nel,), "typestr": "<i4" if dtype == torch.int32 else "<i8",
+                                  "data": (ptr, False), "version": 3}
+    return torch.as_tensor(a, device=dev)
 
 
 # ------------------------------------------------------------------ launcher

@@ -39,12 +39,14 @@ def main():
         dev = "cpu"
     N = cp.n_seq
     nmax = int(max(0, max(int(l) - g + 1 for l in cp.lengths())))
-    st = parallel.ShardedStep(plan, N, g, k, M, nmax, dev)
+    exch = sys.argv[3] if len(sys.argv) > 3 else "auto"
+    st = parallel.ShardedStep(plan, N, g, k, M, nmax, dev, exchange=exch)
     C = torch.zeros((M + 1, N, N), dtype=torch.int64, device=dev)
-    b, e = st.step(cp.codes, cp.offsets, C)
+    for _ in range(2 if gpu else 1):  # (twice on the GPU: both receive buffers)
+        b, e = st.step(cp.codes, cp.offsets, C)
     if gpu:
         torch.cuda.synchronize()
-    mine = {"b": b, "e": e, "Cp": st.Cp[:, : e - b].cpu(), "Nm": st.Nm[:, : e - b].cpu(),
+    mine = {"b": b, "e": e, "Cp": st.complete_C().cpu(), "Nm": st.Nm[:, : e - b].cpu(),
             "K": st.K[: e - b].cpu(), "Kn": st.Knorm[: e - b].cpu()}
     got = [None] * world
     dist.all_gather_object(got, mine)
@@ -68,7 +70,8 @@ def main():
               and np.allclose(Kn, ref["Knorm"][iu], rtol=1e-12, atol=0)
               and sorted((r["b"], r["e"]) for r in got)[-1][1] == T)
         with open(out_path, "w") as f:
-            f.write(f"ok world={world} N={N}" if ok else "mismatch")
+            f.write(f"ok world={world} N={N} exchange={st.exchange}" if ok else "mismatch")
+    st.close()
     dist.destroy_process_group()
 
 

@@ -818,17 +818,22 @@ def test_sharded_packed_emulation(gk, oracle_lib):
             _assert_packed(_assemble_packed(N, M, slices), ref, N)
 
 
-def test_sharded_step_two_ranks_one_gpu(gk, oracle_lib, tmp_path):
-    """parallel.launch + ShardedStep with the real library: two ranks (gloo,
-    collectives staged through host memory) on cuda:0, Tiny config; the assembled
-    packed slices equal the oracle. (The NCCL path differs only in the collective
-    calls; multi-GPU boxes are not available to this build.)"""
+@pytest.mark.parametrize("exchange", ["p2p", "collective"])
+def test_sharded_step_two_ranks_one_gpu(gk, oracle_lib, tmp_path, exchange):
+    """parallel.launch + ShardedStep with the real library: two ranks on cuda:0, Tiny
+    config, two steps (both receive buffers); the assembled packed slices equal the
+    oracle. p2p: the fused pack writes into the other rank's receive buffer through a
+    CUDA IPC mapping (on one GPU the 'peer' memory is local), the epilogue sums the
+    contributions; collective: pack + reduce-scatter (gloo, staged through host
+    memory; NCCL on a multi-GPU box). Multi-GPU boxes are not available to this
+    build."""
     from paper_1704_07468_b200 import parallel
     res = tmp_path / "res.txt"
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    rc = parallel.launch(2, os.path.join(root, "tests", "dist_worker.py"), [str(res), "gpu"])
+    rc = parallel.launch(2, os.path.join(root, "tests", "dist_worker.py"), [str(res), "gpu", exchange])
     assert rc == 0
     assert res.read_text().startswith("ok"), res.read_text()
+    assert f"exchange={exchange}" in res.read_text()
 
 
 def test_k_sweep_parity(gk, oracle_lib):
