@@ -325,13 +325,13 @@ struct WinArgs {
 constexpr uint32_t FAR_CHUNK = 256;
 struct FarRec {
     uint64_t* rec;     // [cap] records
-    uint32_t* fill;    // [0] slots reserved (all warps), [1] the count an apply processes
+    uint32_t* fill;    // [0] slots reserved (all warps)
     uint64_t cap;      // a multiple of FAR_CHUNK
     uint32_t near;     // label distance from which a pair is far (0: off)
 };
-// (applies only when fill[0] >= thresh; fill[1] is the gated count; thresh 0: forced)
+// every pending record into acc (ntri cells); H: >= 2 * sm_count * 64 + 72 u32 scratch
 cudaError_t launch_far_apply(FarRec fr, uint64_t* scratch, uint32_t* H, int bshift,
-                             uint32_t* acc, int sm_count, cudaStream_t s, uint32_t thresh);
+                             uint32_t* acc, uint64_t ntri, int sm_count, cudaStream_t s);
 cudaError_t launch_window_build(SegmentOut so, WinArgs wa, const uint32_t* perm, uint8_t* wD,
                                 int sm_count, cudaStream_t s);
 cudaError_t launch_window_gram(uint8_t* wD, WinArgs wa, int64_t* wC, const int2* tiles,

@@ -104,6 +104,8 @@ struct gakco_plan {
     int gram_fp4 = -1;         // -1 auto (e2m1 Gram when exact), 0 u8 / kind::i8, 1 e2m1
     int trie_pass = 1;         // mask-trie pass kernel: 1 trie.cu (Σ <= 64), 0 generic radix
     int xl_compact = 1;        // cross-level chain: compacted parents (segrag.cu), 0 off
+    uint32_t* far_seen = nullptr;     // pinned copy of the record count (lagged gate)
+    cudaEvent_t ev_far = nullptr;
     int64_t far_near = -1;     // far-pair records from this label distance: -1 auto (256
                                // with a relabelled accumulator), 0 off
     int pipeline = 1;          // light / dense / Gram of batch b on an aux stream, overlapping
@@ -479,6 +481,8 @@ extern "C" void gakco_destroy(gakco_plan* p) {
     for (cudaEvent_t e : {p->ev_seg[0], p->ev_seg[1], p->ev_light[0], p->ev_light[1], p->ev_join,
                           p->ev_join2, p->ev_build, p->ev_gram[0], p->ev_gram[1]})
         if (e) cudaEventDestroy(e);
+    if (p->far_seen) cudaFreeHost(p->far_seen);
+    if (p->ev_far) cudaEventDestroy(p->ev_far);
     if (p->aux) cudaStreamDestroy(p->aux);
     if (p->aux2) cudaStreamDestroy(p->aux2);
     delete p;
@@ -1276,8 +1280,14 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
         far_thresh = (uint32_t)(cap / 2);
         CK(p->ensure(p->farrec, cap * 8, s));
         CK(p->ensure(p->farscr, cap * 8, s));
-        // farbins: [0..255] the fill counter (at 192), then 2 x SMs x 64 chunk histograms
-        CK(p->ensure(p->farbins, (256 + (size_t)p->sm_count * 2 * 64) * 4, s, /*zero=*/true));
+        // farbins: [0..255] the fill counter (at 192), then 2 x SMs x 64 chunk histograms,
+        // bucket offsets [65] and a sink word
+        CK(p->ensure(p->farbins, (256 + (size_t)p->sm_count * 2 * 64 + 72) * 4, s, /*zero=*/true));
+        if (!p->far_seen) {
+            CK(cudaMallocHost(&p->far_seen, 4));
+            CK(cudaEventCreateWithFlags(&p->ev_far, cudaEventDisableTiming));
+        }
+        *p->far_seen = 0;
         CK(cudaMemsetAsync(p->farbins.p, 0, 256 * 4, s));
         int lb = 0;
         while (((uint64_t)1 << lb) < ntri) ++lb;
@@ -1350,10 +1360,12 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
         cudaEvent_t al = nullptr;
         if (perm_active && far.near) {  // every pending far record first
             p->stage_begin(s2, &al);
-            p->launches += 4;
+            p->launches += 4 + 2 * 16;
             LK(launch_far_apply(far, (uint64_t*)p->farscr.p, (uint32_t*)p->farbins.p + 256,
-                                far_bshift, (uint32_t*)p->lightacc.p, p->sm_count, s2, 0u));
+                                far_bshift, (uint32_t*)p->lightacc.p, ntri, p->sm_count, s2));
             p->stage_end(s2, S_FAR, al);
+            CK(cudaEventSynchronize(p->ev_far));  // (the pinned copy is rewritten below)
+            *p->far_seen = 0;
         }
         p->stage_begin(s2, &al);
         if (rect)
@@ -1900,13 +1912,22 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
                             perm_active && win_on ? wa : WinArgs{nullptr, nullptr, 0, 0, 0},
                             n >= (2ull << 20), perm_active ? far : FarRec{nullptr, nullptr, 0, 0}));
             p->stage_end(s2, S_LIGHT, a);
-            if (perm_active && far.near) {  // far records into the accumulator (gated)
-                p->stage_begin(s2, &a);
-                p->launches += 4;
-                LK(launch_far_apply(far, (uint64_t*)p->farscr.p, (uint32_t*)p->farbins.p + 256,
-                                    far_bshift, (uint32_t*)p->lightacc.p, p->sm_count, s2,
-                                    far_thresh));
-                p->stage_end(s2, S_FAR, a);
+            if (perm_active && far.near) {
+                // the apply is worth it once the records fill half the buffer (each
+                // block's cells then hit several times); the count is read back one
+                // batch late (pinned copy + event, no host sync)
+                const bool seen = cudaEventQuery(p->ev_far) == cudaSuccess;
+                cudaGetLastError();  // (cudaErrorNotReady is not an error here)
+                if (seen && *p->far_seen >= far_thresh) {
+                    p->stage_begin(s2, &a);
+                    p->launches += 4 + 2 * 16;
+                    LK(launch_far_apply(far, (uint64_t*)p->farscr.p, (uint32_t*)p->farbins.p + 256,
+                                        far_bshift, (uint32_t*)p->lightacc.p, ntri, p->sm_count, s2));
+                    p->stage_end(s2, S_FAR, a);
+                    *p->far_seen = 0;
+                }
+                CK(cudaMemcpyAsync(p->far_seen, far.fill, 4, cudaMemcpyDeviceToHost, s2));
+                CK(cudaEventRecord(p->ev_far, s2));
             }
             if (perm_active && win_on) {  // this batch's window columns (+ the Gram every few)
                 if (win_masks + nmask > win_lim) {  // s32 exactness of the next Gram
