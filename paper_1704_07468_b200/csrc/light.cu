@@ -513,7 +513,7 @@ cudaError_t launch_light(SegmentOut so, uint64_t max_groups, int64_t heavy_min, 
                          uint32_t* dense_fill, LightBins bins, uint32_t flat_max,
                          int64_t NA, const uint32_t* perm, uint32_t heavy_cmax,
                          unsigned long long* stats, int sm_count, cudaStream_t s,
-                         WinArgs wa, bool big, FarRec fr) {
+                         WinArgs wa, bool big, FarRec fr, int ctas) {
     if (max_groups == 0) return cudaGetLastError();
     uint64_t blocks = (max_groups + 255) / 256;  // 8 warps x 32 groups per block-round
     uint64_t cap = (uint64_t)sm_count * 8;
@@ -522,17 +522,25 @@ cudaError_t launch_light(SegmentOut so, uint64_t max_groups, int64_t heavy_min, 
     light_kernel<W, B, MB><<<(unsigned)blocks, 256, 0, s>>>(so, heavy_min, N, acc, heavy_list,  \
                                                             ldd, dense_fill, bins, flat_max, NA, \
                                                             perm, heavy_cmax, stats, wa, fr)
-#define LIGHT_FAR(W)                                                                             \
-    light_kernel<W, false, 3, true><<<(unsigned)blocks, 256, 0, s>>>(                              \
+#define LIGHT_FAR(W, MB)                                                                         \
+    light_kernel<W, false, MB, true><<<(unsigned)blocks, 256, 0, s>>>(                             \
         so, heavy_min, N, acc, heavy_list, ldd, dense_fill, bins, flat_max, NA, perm, heavy_cmax, \
         stats, wa, fr)
     // (instantiations: the window path and the binning ablation compiled in only
-    // where they run; big batches of long masks (>= 2M g-mers) take the 64-register one)
+    // where they run; big batches of long masks (>= 2M g-mers) take the 64-register one;
+    // the relabelled variants at `ctas` CTAs per SM: 3 (72 registers), 4 or 6)
     if (fr.near && perm && bins.nb == 0) {
-        if (wa.nw) LIGHT_FAR(true);
-        else LIGHT_FAR(false);
+        if (wa.nw) {
+            if (ctas >= 6) LIGHT_FAR(true, 6);
+            else if (ctas == 4) LIGHT_FAR(true, 4);
+            else LIGHT_FAR(true, 3);
+        } else {
+            LIGHT_FAR(false, 3);
+        }
     } else if (wa.nw) {
         if (bins.nb > 0) LIGHT(true, true, 3);
+        else if (ctas >= 6) LIGHT(true, false, 6);
+        else if (ctas == 4) LIGHT(true, false, 4);
         else LIGHT(true, false, 3);
     } else if (bins.nb > 0) {
         LIGHT(false, true, 5);

@@ -104,6 +104,7 @@ struct gakco_plan {
     int gram_fp4 = -1;         // -1 auto (e2m1 Gram when exact), 0 u8 / kind::i8, 1 e2m1
     int trie_pass = 1;         // mask-trie pass kernel: 1 trie.cu (Σ <= 64), 0 generic radix
     int xl_compact = 1;        // cross-level chain: compacted parents (segrag.cu), 0 off
+    int light_ctas = 3;        // relabelled light kernel register budget: CTAs per SM (3, 4, 6)
     uint32_t* far_seen = nullptr;     // pinned copy of the record count (lagged gate)
     cudaEvent_t ev_far = nullptr;
     int64_t far_near = -1;     // far-pair records from this label distance: -1 auto (256
@@ -557,6 +558,10 @@ extern "C" gakco_status gakco_set_option(gakco_plan* p, int option, int64_t valu
             return GAKCO_OK;
         case GAKCO_OPT_TIMING:
             p->timing = value != 0;
+            return GAKCO_OK;
+        case GAKCO_OPT_LIGHT_CTAS:
+            if (value != 3 && value != 4 && value != 6) return p->fail(GAKCO_E_ARG, "light ctas: 3, 4 or 6");
+            p->light_ctas = (int)value;
             return GAKCO_OK;
         case GAKCO_OPT_XL_COMPACT:
             if (value < 0 || value > 1) return p->fail(GAKCO_E_ARG, "xl compact must be 0 or 1");
@@ -1910,7 +1915,8 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
                             perm_active ? (const uint32_t*)p->perm.p : nullptr,
                             fp4_lv[m] ? 4u : 255u, stats, p->sm_count, s2,
                             perm_active && win_on ? wa : WinArgs{nullptr, nullptr, 0, 0, 0},
-                            n >= (2ull << 20), perm_active ? far : FarRec{nullptr, nullptr, 0, 0}));
+                            n >= (2ull << 20), perm_active ? far : FarRec{nullptr, nullptr, 0, 0},
+                            p->light_ctas));
             p->stage_end(s2, S_LIGHT, a);
             if (perm_active && far.near) {
                 // the apply is worth it once the records fill half the buffer (each
