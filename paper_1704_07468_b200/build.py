@@ -14,6 +14,10 @@ ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 OBJ = os.path.join(ROOT, "build", "obj")
 LIB = os.path.join(PKG, "libgakco.so")
+# bounds-checked variant (device asserts, GK_CHECK): compute-sanitizer is closed on the
+# GPU pool, so the test suite runs against this one instead (GAKCO_LIB=...)
+OBJ_CHECKED = os.path.join(ROOT, "build", "obj_checked")
+LIB_CHECKED = os.path.join(PKG, "libgakco_checked.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
@@ -38,7 +42,7 @@ def _stale(target, deps):
 
 
 def _compile(src, extra):
-    obj = os.path.join(OBJ, os.path.basename(src) + ".o")
+    obj = os.path.join(extra.get("obj", OBJ), os.path.basename(src) + ".o")
     if _stale(obj, [src] + _deps()) or extra.get("force"):
         cmd = [NVCC] + ARCH + FLAGS + extra.get("flags", []) + ["-c", src, "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
@@ -49,19 +53,21 @@ def _compile(src, extra):
     return obj
 
 
-def build(force: bool = False, verbose: bool = False, flags=None) -> str:
-    os.makedirs(OBJ, exist_ok=True)
+def build(force: bool = False, verbose: bool = False, flags=None, checked: bool = False) -> str:
+    obj_dir, lib = (OBJ_CHECKED, LIB_CHECKED) if checked else (OBJ, LIB)
+    os.makedirs(obj_dir, exist_ok=True)
     srcs = sources()
-    extra = {"force": force, "verbose": verbose, "flags": list(flags or [])}
+    extra = {"force": force, "verbose": verbose, "obj": obj_dir,
+             "flags": list(flags or []) + (["-DGAKCO_CHECKS"] if checked else [])}
     with cf.ThreadPoolExecutor(max_workers=min(8, len(srcs))) as ex:
         objs = list(ex.map(lambda s: _compile(s, extra), srcs))
-    if force or _stale(LIB, objs):
-        cmd = [NVCC] + ARCH + ["-shared", "-o", LIB] + objs + ["-lcudart", "-ldl"]
+    if force or _stale(lib, objs):
+        cmd = [NVCC] + ARCH + ["-shared", "-o", lib] + objs + ["-lcudart", "-ldl"]
         subprocess.check_call(cmd)
-    return LIB
+    return lib
 
 
 if __name__ == "__main__":
-    build(force="--force" in sys.argv, verbose="-v" in sys.argv,
-          flags=["-Xptxas", "-v"] if "--ptxas" in sys.argv else None)
-    print(LIB)
+    print(build(force="--force" in sys.argv, verbose="-v" in sys.argv,
+                flags=["-Xptxas", "-v"] if "--ptxas" in sys.argv else None,
+                checked="--checked" in sys.argv))

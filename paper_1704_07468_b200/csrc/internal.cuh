@@ -9,6 +9,16 @@
 
 #include "gakco.h"
 
+// Bounds-checked build (compute-sanitizer is closed on this GPU pool): compiled with
+// -DGAKCO_CHECKS (python -m paper_1704_07468_b200.build --checked -> libgakco_checked.so),
+// every GK_CHECK is a device assert on an index about to be written / read.
+#ifdef GAKCO_CHECKS
+#include <cassert>
+#define GK_CHECK(c) assert(c)
+#else
+#define GK_CHECK(c) ((void)0)
+#endif
+
 namespace gk {
 
 constexpr int GMAX = 32;          // longest supported g-mer

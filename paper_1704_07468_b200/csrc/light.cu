@@ -115,6 +115,7 @@ struct FarSink {
             used = 0;
             have = true;
         }
+        GK_CHECK(!want || base + used + __popc(m & lanemask_lt()) < fr.cap);
         if (want) fr.rec[base + used + __popc(m & lanemask_lt())] = cell << 24 | val;
         used += nf;
         return want;
@@ -161,12 +162,13 @@ __global__ void far_warm_kernel(const uint32_t* __restrict__ acc, uint64_t c0, u
     if (x == 0x9e3779b9u) *sink = x;  // (keeps the loads)
 }
 __global__ void far_add_kernel(const uint64_t* __restrict__ recs, const uint32_t* offs, int b0,
-                               int b1, uint32_t* acc) {
+                               int b1, uint32_t* acc, uint64_t ntri) {
     const uint64_t lo = offs[b0], hi = offs[b1];
     for (uint64_t i = lo + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < hi;
          i += (uint64_t)gridDim.x * blockDim.x) {
         const uint64_t r = recs[i];
         const uint32_t v = (uint32_t)(r & 0xffffffull);
+        GK_CHECK(!v || (r >> 24) < ntri);
         if (v) atomicAdd(&acc[r >> 24], v);
     }
 }
@@ -188,7 +190,7 @@ cudaError_t launch_far_apply(FarRec fr, uint64_t* scratch, uint32_t* H, int bshi
         uint64_t c1 = std::min<uint64_t>((uint64_t)b1 << bshift, ntri);
         c1 = c1 / 4 * 4;
         if (c1 > c0) far_warm_kernel<<<sm_count * 4, 256, 0, s>>>(acc, c0, c1, offs, b0, b1, sink);
-        far_add_kernel<<<sm_count * 8, 256, 0, s>>>(scratch, offs, b0, b1, acc);
+        far_add_kernel<<<sm_count * 8, 256, 0, s>>>(scratch, offs, b0, b1, acc, ntri);
     }
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;
@@ -246,6 +248,7 @@ __global__ void __launch_bounds__(256, MINB) light_kernel(SegmentOut so, int64_t
     // one pair update: a far pair (labels >= frec.near apart) becomes a record, the
     // rest are REDs (every lane calls it: warp-uniform)
     auto upd = [&](bool ok, uint64_t idx, uint32_t val, uint32_t dist) {
+        GK_CHECK(!ok || NA != 0 || idx < (uint64_t)N * (uint64_t)(N - 1) / 2);
         if constexpr (FAR) {
             const bool rec = sink.put(ok && dist >= frec.near, idx, val);
             nfar += rec ? 1u : 0u;

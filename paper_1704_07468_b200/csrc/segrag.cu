@@ -228,11 +228,13 @@ __global__ void __launch_bounds__(RG_THREADS, 4) segment_rag_kernel(
 #pragma unroll
         for (int i = 0; i < RG_IT; ++i)
             if (keep & (1u << i)) {
+                GK_CHECK(s_base_c + k < n);
                 cw[cb + k] = cur[i].w;
                 cs[cb + k] = (S)cur[i].s;
                 ++k;
             }
         for (uint32_t j = tid; j < tail_len; j += RG_THREADS) {
+            GK_CHECK(s_base_c + agg_k + j < n);
             cw[cb + agg_k + j] = w[tile_end + j];
             cs[cb + agg_k + j] = sq[tile_end + j];
         }

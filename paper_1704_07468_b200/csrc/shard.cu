@@ -70,6 +70,7 @@ __global__ void __launch_bounds__(256) pack_upper_peers_kernel(const int64_t* __
     const int64_t hi = R + (N - X);
     for (int64_t e = R + threadIdx.x; e < hi; e += blockDim.x) {
         const int64_t d = e / chunk;
+        GK_CHECK(d < MAX_PEERS && dst.p[d] != nullptr);
         T* out = (T*)dst.p[d];
         out[((int64_t)src * levels + level) * chunk + (e - d * chunk)] = (T)row[e];
     }

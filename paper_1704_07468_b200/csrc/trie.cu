@@ -293,6 +293,7 @@ __global__ void __launch_bounds__(TP_THREADS, 2) tp_scatter_kernel(
             if (idx < ct) {
                 const uint32_t d = (uint32_t)(keys[i] >> shift) & dmask;
                 const uint32_t pos = whist[d] + ((rank[i / 2] >> (16 * (i & 1))) & 0xffffu);
+                GK_CHECK(pos < ct);
                 buf[pos] = keys[i];
                 if constexpr (PAY) s_pout[pos] = pin[idx];
             }
@@ -305,6 +306,7 @@ __global__ void __launch_bounds__(TP_THREADS, 2) tp_scatter_kernel(
             const uint64_t k = buf[j];
             const uint32_t d = (uint32_t)(k >> shift) & dmask;
             const uint64_t dst = (uint64_t)(s_goff[d] + (int64_t)j);
+            GK_CHECK(dst < cnt);
             wout[dst] = k & omask;
             if constexpr (PAY) sout[dst] = s_pout[j];
         }

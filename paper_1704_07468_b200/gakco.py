@@ -17,7 +17,8 @@ import os
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "libgakco.so")
+# (GAKCO_LIB selects another build of the same library, e.g. the bounds-checked one)
+LIB_PATH = os.environ.get("GAKCO_LIB") or os.path.join(_PKG, "libgakco.so")
 
 GAKCO_OK = 0
 GAKCO_E_ARG = 1
