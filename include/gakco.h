@@ -131,7 +131,7 @@ typedef enum {
                                      launches) where sigma <= 64; 0 = the generic 8-bit radix
                                      pass (hist + chunk scan + scatter) */
     GAKCO_OPT_LIGHT_CTAS = 19,    /* register budget of the relabelled light kernel: CTAs per SM
-                                     it is compiled for (3 = default, 4, 6) */
+                                     it is compiled for (3, 4 = default, 6) */
     GAKCO_OPT_XL_COMPACT = 18,    /* cross-level mask-trie chain (levels processed as k rises, a
                                      level-m mask one pass over its level-(m+1) parent): 1
                                      (default) = each level keeps only the elements of groups of

@@ -217,6 +217,8 @@ cudaError_t launch_apply_bins(uint32_t* acc, LightBins bn, int sm_count, cudaStr
     return cudaMemsetAsync(bn.cnt, 0, bn.nb * sizeof(uint32_t), s);
 }
 
+constexpr int LF_STAGE = 256;  // staged triples per warp (flat groups of 32 groups x <= 8)
+
 // MINB: CTAs per SM the register budget is sized for. 5 (48 registers, no spills):
 // the occupancy DNA's L2-resident random updates want (light 3.32 ms; 56 registers:
 // 3.51 ms); 3 (up to 85 registers) is faster for the big groups of Text / Scale
@@ -233,6 +235,8 @@ __global__ void __launch_bounds__(256, MINB) light_kernel(SegmentOut so, int64_t
     // triangle table: pairs (a < b < 32) ordered by b, so the first n(n-1)/2
     // entries are exactly the pairs of an n-triple chunk
     __shared__ uint16_t s_tri[496];
+    // per warp: the flat groups' triples (labels, counts), LF_STAGE entries
+    __shared__ uint32_t s_stx[8][LF_STAGE], s_stc[8][LF_STAGE];
     for (int b = 1, q = 0; b < 32; ++b)
         for (int a = 0; a < b; ++a, ++q)
             if (q % blockDim.x == threadIdx.x) s_tri[q] = (uint16_t)(a | (b << 5));
@@ -282,6 +286,23 @@ __global__ void __launch_bounds__(256, MINB) light_kernel(SegmentOut so, int64_t
         const uint32_t excl = incl - P;
         const uint32_t Ptot = __shfl_sync(0xffffffffu, incl, 31);
         pairs += lane == 0 ? Ptot : 0u;
+        // the flat groups' triples usually form one short span of the triple arrays:
+        // staged in shared memory with coalesced loads (ids already turned into labels),
+        // the per-pair gathers then read shared memory instead of a dependent chain of
+        // global loads
+        const uint32_t glo = __reduce_min_sync(0xffffffffu, flat ? my_start : 0xffffffffu);
+        const uint32_t ghi = __reduce_max_sync(0xffffffffu, flat ? my_end : 0u);
+        const bool staged = Ptot > 0 && ghi - glo <= (uint32_t)LF_STAGE;
+        uint32_t* sx = s_stx[threadIdx.x >> 5];
+        uint32_t* sc = s_stc[threadIdx.x >> 5];
+        if (staged) {
+            for (uint32_t t = glo + lane; t < ghi; t += 32) {
+                const uint32_t x = so.tseq[t] & 0x7fffffffu;
+                sx[t - glo] = perm ? perm[x] : x;
+                sc[t - glo] = so.tcnt[t];
+            }
+            __syncwarp();
+        }
         for (uint32_t q0 = 0; q0 < Ptot; q0 += 32) {
             const uint32_t q = q0 + lane;
             // group of pair q: the last lane j with excl_j <= q
@@ -299,12 +320,19 @@ __global__ void __launch_bounds__(256, MINB) light_kernel(SegmentOut so, int64_t
             if (q < Ptot) {
                 const uint32_t ab = s_tri[q - ej];
                 const uint32_t ta = sj + (ab & 31), tb = sj + (ab >> 5);
-                const uint32_t xa = so.tseq[ta] & 0x7fffffffu, xb = so.tseq[tb] & 0x7fffffffu;
-                idx = pair_cell(xa, xb, N, NA, &ok, perm, FAR ? &dist : nullptr);
-                val = so.tcnt[ta] * so.tcnt[tb];
+                if (staged) {
+                    idx = pair_cell(sx[ta - glo], sx[tb - glo], N, NA, &ok, nullptr,
+                                    FAR ? &dist : nullptr);
+                    val = sc[ta - glo] * sc[tb - glo];
+                } else {
+                    const uint32_t xa = so.tseq[ta] & 0x7fffffffu, xb = so.tseq[tb] & 0x7fffffffu;
+                    idx = pair_cell(xa, xb, N, NA, &ok, perm, FAR ? &dist : nullptr);
+                    val = so.tcnt[ta] * so.tcnt[tb];
+                }
             }
             upd(ok, idx, val, dist);
         }
+        __syncwarp();  // (the staging buffer is rewritten by the next 32 groups)
 
         // (1b) heavy candidates among the 32 groups: counts checked per group, then one
         // atomicAdd claims all their dense columns (a claim per group would serialise

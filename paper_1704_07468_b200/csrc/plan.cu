@@ -104,7 +104,8 @@ struct gakco_plan {
     int gram_fp4 = -1;         // -1 auto (e2m1 Gram when exact), 0 u8 / kind::i8, 1 e2m1
     int trie_pass = 1;         // mask-trie pass kernel: 1 trie.cu (Σ <= 64), 0 generic radix
     int xl_compact = 1;        // cross-level chain: compacted parents (segrag.cu), 0 off
-    int light_ctas = 3;        // relabelled light kernel register budget: CTAs per SM (3, 4, 6)
+    int light_ctas = 4;        // relabelled light kernel register budget: CTAs per SM (3, 4, 6;
+                               // Scale light 74.3 / 65.7 / 69.8 ms with far records)
     uint32_t* far_seen = nullptr;     // pinned copy of the record count (lagged gate)
     cudaEvent_t ev_far = nullptr;
     int64_t far_near = -1;     // far-pair records from this label distance: -1 auto (256

@@ -60,8 +60,29 @@ __global__ void __launch_bounds__(RG_THREADS, 4) segment_rag_kernel(
     auto teq = [&](const RagElem& a, const RagElem& b) { return geq(a, b) && a.s == b.s; };
 
     RagElem cur[RG_IT];
+    if (base + RG_IT <= tile_end &&
+        ((((uintptr_t)(w + base)) | ((uintptr_t)(sq + base))) & 15) == 0) {
+        // 16-byte vector loads (4 of windows, 1 or 2 of ids)
+        const uint4* v = (const uint4*)(w + base);
 #pragma unroll
-    for (int i = 0; i < RG_IT; ++i) cur[i] = base + i < tile_end ? ld(base + i) : RagElem{0ull, 0u};
+        for (int i = 0; i < RG_IT / 2; ++i) {
+            const uint4 q = v[i];
+            cur[2 * i].w = (uint64_t)q.x | (uint64_t)q.y << 32;
+            cur[2 * i + 1].w = (uint64_t)q.z | (uint64_t)q.w << 32;
+        }
+        const uint4* u = (const uint4*)(sq + base);
+        constexpr int NU = RG_IT * sizeof(S) / 16;
+#pragma unroll
+        for (int i = 0; i < NU; ++i) {
+            const uint4 q = u[i];
+            const S* sv = (const S*)&q;
+#pragma unroll
+            for (int e = 0; e < 16 / (int)sizeof(S); ++e) cur[i * (16 / sizeof(S)) + e].s = (uint32_t)sv[e];
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < RG_IT; ++i) cur[i] = base + i < tile_end ? ld(base + i) : RagElem{0ull, 0u};
+    }
     const bool has_next = tile_end < seg_end;
     RagElem ext{0ull, 0u}, lk{0ull, 0u};
     if (warp == RG_THREADS / 32 - 1 && has_next) {
