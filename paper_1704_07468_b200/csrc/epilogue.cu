@@ -81,14 +81,21 @@ __device__ __forceinline__ double knorm(int64_t kxy, int64_t kxx, int64_t kyy, b
     return __ddiv_rn((double)kxy, __dsqrt_rn(__dmul_rn((double)kxx, (double)kyy)));
 }
 
-// blockDim (32, 8); grid (tiles, tiles); block (bx=bj, by=bi) works iff bi <= bj.
+// blockDim (32, 8); a 1-D grid over the t(t+1)/2 tile pairs bi <= bj (t = tiles per
+// side), row-major: block L -> the largest bi with R(bi) = bi t - bi (bi - 1) / 2 <= L.
 // MM bounds M so the per-thread profiles stay in registers.
 template <int MM>
 __global__ void __launch_bounds__(256) epilogue_kernel(EpiArgs a,
                                                        const __grid_constant__ EpiCoef cf) {
     __shared__ int64_t st[32][33];
-    const int bi = blockIdx.y, bj = blockIdx.x;
-    if (bi > bj) return;
+    const int64_t t = (a.N + 31) / 32, L = blockIdx.x;
+    int64_t lo = 0, hi = t - 1;
+    while (lo < hi) {  // (block-uniform)
+        const int64_t mid = (lo + hi + 1) / 2;
+        if (mid * t - mid * (mid - 1) / 2 <= L) lo = mid;
+        else hi = mid - 1;
+    }
+    const int bi = (int)lo, bj = (int)(lo + (L - (lo * t - lo * (lo - 1) / 2)));
     const int tx = threadIdx.x, ty = threadIdx.y;
     const int64_t N = a.N, nn = N * N;
     const int M = a.M;
@@ -358,15 +365,16 @@ cudaError_t launch_epilogue(int64_t* C, int64_t N, int g, int k, int M, int64_t*
     kdiag_kernel<<<(int)(blocks < 1024 ? blocks : 1024), 256, 0, s>>>(a, cf);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    const unsigned tiles = (unsigned)((N + 31) / 32);
+    const uint64_t tiles = (uint64_t)((N + 31) / 32);
+    const unsigned pairs = (unsigned)(tiles * (tiles + 1) / 2);  // (upper tile pairs only)
     if (M <= 3)  // (the profile array sized to the level count: registers, not local memory)
-        epilogue_kernel<3><<<dim3(tiles, tiles), dim3(32, 8), 0, s>>>(a, cf);
+        epilogue_kernel<3><<<pairs, dim3(32, 8), 0, s>>>(a, cf);
     else if (M <= 5)
-        epilogue_kernel<5><<<dim3(tiles, tiles), dim3(32, 8), 0, s>>>(a, cf);
+        epilogue_kernel<5><<<pairs, dim3(32, 8), 0, s>>>(a, cf);
     else if (M <= 7)
-        epilogue_kernel<7><<<dim3(tiles, tiles), dim3(32, 8), 0, s>>>(a, cf);
+        epilogue_kernel<7><<<pairs, dim3(32, 8), 0, s>>>(a, cf);
     else
-        epilogue_kernel<GMAX><<<dim3(tiles, tiles), dim3(32, 8), 0, s>>>(a, cf);
+        epilogue_kernel<GMAX><<<pairs, dim3(32, 8), 0, s>>>(a, cf);
     return cudaGetLastError();
 }
 
