@@ -84,6 +84,8 @@ def args_():
                     help="cross-level trie chain with compacted parents (1, default) or full arrays")
     ap.add_argument("--light-ctas", type=int, default=None, choices=[3, 4, 6],
                     help="relabelled light kernel register budget (CTAs per SM)")
+    ap.add_argument("--light-grid", type=int, default=None,
+                    help="light kernel grid in CTAs per SM (0 = 8)")
     ap.add_argument("--no-timing", action="store_true",
                     help="no per-stage events (roofline then uses the last timed stages)")
     return ap.parse_args()
@@ -388,6 +390,8 @@ def run_ours(a):
         plan.set_option(gakco.GAKCO_OPT_XL_COMPACT, a.xl_compact)
     if a.light_ctas is not None:
         plan.set_option(gakco.GAKCO_OPT_LIGHT_CTAS, a.light_ctas)
+    if a.light_grid is not None:
+        plan.set_option(gakco.GAKCO_OPT_LIGHT_GRID, a.light_grid)
     C = torch.zeros((M + 1, N, N), dtype=torch.int64, device=dev)
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.int32, device=dev)
     stream = torch.cuda.current_stream(dev)

@@ -355,7 +355,8 @@ cudaError_t launch_light(SegmentOut so, uint64_t max_groups, int64_t heavy_min, 
                          int64_t NA, const uint32_t* perm, uint32_t heavy_cmax,
                          unsigned long long* stats, int sm_count, cudaStream_t s,
                          WinArgs wa = WinArgs{nullptr, nullptr, 0, 0, 0}, bool big = false,
-                         FarRec fr = FarRec{nullptr, nullptr, 0, 0}, int ctas = 3);
+                         FarRec fr = FarRec{nullptr, nullptr, 0, 0}, int ctas = 3,
+                         int grid_per_sm = 0);
 // Light accumulator relabelled by perm (sequence -> accumulator index): flush it into
 // C_m (original order) and zero it.
 cudaError_t launch_light_flush_perm(uint32_t* acc, int64_t N, int64_t* Cm, const uint32_t* perm,

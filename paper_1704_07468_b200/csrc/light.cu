@@ -544,10 +544,12 @@ cudaError_t launch_light(SegmentOut so, uint64_t max_groups, int64_t heavy_min, 
                          uint32_t* dense_fill, LightBins bins, uint32_t flat_max,
                          int64_t NA, const uint32_t* perm, uint32_t heavy_cmax,
                          unsigned long long* stats, int sm_count, cudaStream_t s,
-                         WinArgs wa, bool big, FarRec fr, int ctas) {
+                         WinArgs wa, bool big, FarRec fr, int ctas, int grid_per_sm) {
     if (max_groups == 0) return cudaGetLastError();
     uint64_t blocks = (max_groups + 255) / 256;  // 8 warps x 32 groups per block-round
-    uint64_t cap = (uint64_t)sm_count * 8;
+    // (grid_per_sm < the resident CTAs leaves room on every SM for the other stream's
+    // sort / segment kernels of the next batch)
+    uint64_t cap = (uint64_t)sm_count * (grid_per_sm > 0 ? grid_per_sm : 8);
     if (blocks > cap) blocks = cap;
 #define LIGHT(W, B, MB)                                                                        \
     light_kernel<W, B, MB><<<(unsigned)blocks, 256, 0, s>>>(so, heavy_min, N, acc, heavy_list,  \

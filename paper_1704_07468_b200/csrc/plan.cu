@@ -104,6 +104,7 @@ struct gakco_plan {
     int gram_fp4 = -1;         // -1 auto (e2m1 Gram when exact), 0 u8 / kind::i8, 1 e2m1
     int trie_pass = 1;         // mask-trie pass kernel: 1 trie.cu (Σ <= 64), 0 generic radix
     int xl_compact = 1;        // cross-level chain: compacted parents (segrag.cu), 0 off
+    int light_grid = 0;        // light kernel grid in CTAs per SM (0: 8)
     int light_ctas = 4;        // relabelled light kernel register budget: CTAs per SM (3, 4, 6;
                                // Scale light 74.3 / 65.7 / 69.8 ms with far records)
     uint32_t* far_seen = nullptr;     // pinned copy of the record count (lagged gate)
@@ -559,6 +560,10 @@ extern "C" gakco_status gakco_set_option(gakco_plan* p, int option, int64_t valu
             return GAKCO_OK;
         case GAKCO_OPT_TIMING:
             p->timing = value != 0;
+            return GAKCO_OK;
+        case GAKCO_OPT_LIGHT_GRID:
+            if (value < 0 || value > 64) return p->fail(GAKCO_E_ARG, "light grid: 0..64 CTAs per SM");
+            p->light_grid = (int)value;
             return GAKCO_OK;
         case GAKCO_OPT_LIGHT_CTAS:
             if (value != 3 && value != 4 && value != 6) return p->fail(GAKCO_E_ARG, "light ctas: 3, 4 or 6");
@@ -1917,7 +1922,7 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
                             fp4_lv[m] ? 4u : 255u, stats, p->sm_count, s2,
                             perm_active && win_on ? wa : WinArgs{nullptr, nullptr, 0, 0, 0},
                             n >= (2ull << 20), perm_active ? far : FarRec{nullptr, nullptr, 0, 0},
-                            p->light_ctas));
+                            p->light_ctas, p->light_grid));
             p->stage_end(s2, S_LIGHT, a);
             if (perm_active && far.near) {
                 // the apply is worth it once the records fill half the buffer (each
