@@ -81,12 +81,14 @@ __device__ __forceinline__ double knorm(int64_t kxy, int64_t kxx, int64_t kyy, b
     return __ddiv_rn((double)kxy, __dsqrt_rn(__dmul_rn((double)kxx, (double)kyy)));
 }
 
-// blockDim (32, 8); a 1-D grid over the t(t+1)/2 tile pairs bi <= bj (t = tiles per
-// side), row-major: block L -> the largest bi with R(bi) = bi t - bi (bi - 1) / 2 <= L.
-// MM bounds M so the per-thread profiles stay in registers.
+// blockDim (32, 32 / EP_RPT); a 1-D grid over the t(t+1)/2 tile pairs bi <= bj (t =
+// tiles per side), row-major: block L -> the largest bi with R(bi) = bi t - bi (bi-1)/2
+// <= L. Each thread holds EP_RPT rows of the 32 x 32 tile (2: the profiles stay in
+// registers, 4 CTAs of 512 threads per SM). MM bounds M.
+constexpr int EP_RPT = 2, EP_TY = 32 / EP_RPT;
 template <int MM>
-__global__ void __launch_bounds__(256) epilogue_kernel(EpiArgs a,
-                                                       const __grid_constant__ EpiCoef cf) {
+__global__ void __launch_bounds__(32 * EP_TY, 2) epilogue_kernel(EpiArgs a,
+                                                                const __grid_constant__ EpiCoef cf) {
     __shared__ int64_t st[32][33];
     const int64_t t = (a.N + 31) / 32, L = blockIdx.x;
     int64_t lo = 0, hi = t - 1;
@@ -100,13 +102,14 @@ __global__ void __launch_bounds__(256) epilogue_kernel(EpiArgs a,
     const int64_t N = a.N, nn = N * N;
     const int M = a.M;
     const bool diag_tile = bi == bj;
-    int64_t prof[4][MM + 1];
-    int64_t kv[4];
-    bool ok[4];
+    int64_t prof[EP_RPT][MM + 1];
+    int64_t kv[EP_RPT];
+    double kn[EP_RPT];
+    bool ok[EP_RPT];
     int bad = 0;
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-        const int r = ty + 8 * q;
+    for (int q = 0; q < EP_RPT; ++q) {
+        const int r = ty + EP_TY * q;
         const int64_t X = (int64_t)bi * 32 + r, Y = (int64_t)bj * 32 + tx;
         ok[q] = X < N && Y < N;
         kv[q] = 0;
@@ -129,29 +132,30 @@ __global__ void __launch_bounds__(256) epilogue_kernel(EpiArgs a,
             if (o > M) break;
             __syncthreads();
 #pragma unroll
-            for (int q = 0; q < 4; ++q) st[ty + 8 * q][tx] = prof[q][o];
+            for (int q = 0; q < EP_RPT; ++q) st[ty + EP_TY * q][tx] = prof[q][o];
             __syncthreads();
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const int r = ty + 8 * q;
+            for (int q = 0; q < EP_RPT; ++q) {
+                const int r = ty + EP_TY * q;
                 const int64_t X = (int64_t)bj * 32 + r, Y = (int64_t)bi * 32 + tx;
                 if (X < N && Y < N) a.C[o * nn + X * N + Y] = st[tx][r];
             }
         }
     }
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
+    for (int q = 0; q < EP_RPT; ++q) {
         if (!ok[q]) continue;
-        const int r = ty + 8 * q;
+        const int r = ty + EP_TY * q;
         const int64_t X = (int64_t)bi * 32 + r, Y = (int64_t)bj * 32 + tx;
         kv[q] = entry<MM>(prof[q], cf, a.g, a.k, M, &bad);  // prof now holds N_m
+        kn[q] = knorm(kv[q], a.kdiag[X], a.kdiag[Y], X == Y);  // (reused transposed)
         if (a.Nm) {
 #pragma unroll
             for (int m = 0; m <= MM; ++m)
                 if (m <= M) a.Nm[m * nn + X * N + Y] = prof[q][m];
         }
         if (a.K) a.K[X * N + Y] = kv[q];
-        if (a.Knorm) a.Knorm[X * N + Y] = knorm(kv[q], a.kdiag[X], a.kdiag[Y], X == Y);
+        if (a.Knorm) a.Knorm[X * N + Y] = kn[q];
     }
     if (bad) atomicOr(a.flags, bad);
     if (diag_tile) return;
@@ -163,11 +167,11 @@ __global__ void __launch_bounds__(256) epilogue_kernel(EpiArgs a,
             if (o > M) break;
             __syncthreads();
 #pragma unroll
-            for (int q = 0; q < 4; ++q) st[ty + 8 * q][tx] = prof[q][o];
+            for (int q = 0; q < EP_RPT; ++q) st[ty + EP_TY * q][tx] = prof[q][o];
             __syncthreads();
 #pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const int r = ty + 8 * q;
+            for (int q = 0; q < EP_RPT; ++q) {
+                const int r = ty + EP_TY * q;
                 const int64_t X = (int64_t)bj * 32 + r, Y = (int64_t)bi * 32 + tx;
                 if (X < N && Y < N) a.Nm[o * nn + X * N + Y] = st[tx][r];
             }
@@ -177,17 +181,15 @@ __global__ void __launch_bounds__(256) epilogue_kernel(EpiArgs a,
         if (o == 0 ? a.K == nullptr : a.Knorm == nullptr) continue;
         __syncthreads();
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const int r = ty + 8 * q;
+        for (int q = 0; q < EP_RPT; ++q) {
+            const int r = ty + EP_TY * q;
             if (!ok[q]) continue;
-            const int64_t X = (int64_t)bi * 32 + r, Y = (int64_t)bj * 32 + tx;
-            st[r][tx] = o == 0 ? kv[q]
-                               : __double_as_longlong(knorm(kv[q], a.kdiag[X], a.kdiag[Y], false));
+            st[r][tx] = o == 0 ? kv[q] : __double_as_longlong(kn[q]);
         }
         __syncthreads();
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            const int r = ty + 8 * q;                  // row within the transposed tile
+        for (int q = 0; q < EP_RPT; ++q) {
+            const int r = ty + EP_TY * q;                  // row within the transposed tile
             const int64_t X = (int64_t)bj * 32 + r, Y = (int64_t)bi * 32 + tx;
             if (X >= N || Y >= N) continue;
             const int64_t v = st[tx][r];
@@ -368,13 +370,13 @@ cudaError_t launch_epilogue(int64_t* C, int64_t N, int g, int k, int M, int64_t*
     const uint64_t tiles = (uint64_t)((N + 31) / 32);
     const unsigned pairs = (unsigned)(tiles * (tiles + 1) / 2);  // (upper tile pairs only)
     if (M <= 3)  // (the profile array sized to the level count: registers, not local memory)
-        epilogue_kernel<3><<<pairs, dim3(32, 8), 0, s>>>(a, cf);
+        epilogue_kernel<3><<<pairs, dim3(32, EP_TY), 0, s>>>(a, cf);
     else if (M <= 5)
-        epilogue_kernel<5><<<pairs, dim3(32, 8), 0, s>>>(a, cf);
+        epilogue_kernel<5><<<pairs, dim3(32, EP_TY), 0, s>>>(a, cf);
     else if (M <= 7)
-        epilogue_kernel<7><<<pairs, dim3(32, 8), 0, s>>>(a, cf);
+        epilogue_kernel<7><<<pairs, dim3(32, EP_TY), 0, s>>>(a, cf);
     else
-        epilogue_kernel<GMAX><<<pairs, dim3(32, 8), 0, s>>>(a, cf);
+        epilogue_kernel<GMAX><<<pairs, dim3(32, EP_TY), 0, s>>>(a, cf);
     return cudaGetLastError();
 }
 
