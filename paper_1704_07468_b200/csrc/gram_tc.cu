@@ -591,7 +591,10 @@ cudaError_t launch_gram_flush(uint8_t* D, int64_t n_pad, uint64_t ldd, uint32_t*
 // [wa.fill[nw + w], wa.fill[w]) of window w (the batch start is slab-aligned): 128
 // columns x 256 rows of u8 counts assembled in shared memory (zeros elsewhere),
 // stored as one contiguous 32 KB block of wD [slab][nw * 256][128]. A warp takes 8
-// columns, their members gathered together (latency: list -> triple -> label).
+// columns, their members gathered together (latency: list -> triple -> label). The
+// tile's 4-byte words are XOR-swizzled by row (word w of row r at r * 32 + (w ^ (r &
+// 31))): the lanes of a warp write one column at 32 different rows, which would
+// otherwise all hit one bank; the copy-out un-swizzles.
 constexpr int WB_Q = 16;
 constexpr int WB_THREADS = 512;
 constexpr int WB_CPW = GT_KB / (WB_THREADS / 32);  // columns per warp per slab (8)
@@ -621,12 +624,18 @@ __global__ void __launch_bounds__(WB_THREADS) window_build_kernel(SegmentOut so,
             for (uint32_t t = g[jj].x + lane; t < g[jj].y; t += 32) {
                 const uint32_t r = perm[so.tseq[t] & 0x7fffffffu] - lab0;
                 if (r < (uint32_t)WIN_ROWS)  // (a split group: its members in this window)
-                    tile[r * GT_KB + j] = (uint8_t)so.tcnt[t];
+                    tile[r * GT_KB + ((((uint32_t)j >> 2) ^ (r & 31u)) << 2) + (j & 3)] =
+                        (uint8_t)so.tcnt[t];
             }
         }
         __syncthreads();
         uint4* dst = (uint4*)(wD + ((uint64_t)sl * wa.nw * WIN_ROWS + (uint64_t)w * WIN_ROWS) * GT_KB);
-        for (int i = threadIdx.x; i < WIN_ROWS * GT_KB / 16; i += WB_THREADS) dst[i] = t4[i];
+        const uint32_t* t1 = (const uint32_t*)tile;
+        for (int i = threadIdx.x; i < WIN_ROWS * GT_KB / 16; i += WB_THREADS) {
+            const uint32_t r = (uint32_t)i >> 3, w0 = ((uint32_t)i & 7u) * 4, sw = r & 31u;
+            dst[i] = make_uint4(t1[r * 32 + ((w0 + 0) ^ sw)], t1[r * 32 + ((w0 + 1) ^ sw)],
+                                t1[r * 32 + ((w0 + 2) ^ sw)], t1[r * 32 + ((w0 + 3) ^ sw)]);
+        }
         __syncthreads();
     }
 }
