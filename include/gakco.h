@@ -130,9 +130,9 @@ typedef enum {
                                      (<= 64 buckets, chunk prefixes inside the scatter: two
                                      launches) where sigma <= 64; 0 = the generic 8-bit radix
                                      pass (hist + chunk scan + scatter) */
-    GAKCO_OPT_LIGHT_GRID = 20,    /* light kernel grid size in CTAs per SM (0 = default 8); fewer
-                                     leave room for the next batch's sort / segment kernels on
-                                     the other stream */
+    GAKCO_OPT_LIGHT_GRID = 20,    /* light kernel grid size in CTAs per SM (0 = automatic: 3 for
+                                     a relabelled accumulator, else 8); fewer leave room for the
+                                     next batch's sort / segment kernels on the other stream */
     GAKCO_OPT_LIGHT_CTAS = 19,    /* register budget of the relabelled light kernel: CTAs per SM
                                      it is compiled for (3, 4 = default, 6) */
     GAKCO_OPT_XL_COMPACT = 18,    /* cross-level mask-trie chain (levels processed as k rises, a

@@ -104,7 +104,7 @@ struct gakco_plan {
     int gram_fp4 = -1;         // -1 auto (e2m1 Gram when exact), 0 u8 / kind::i8, 1 e2m1
     int trie_pass = 1;         // mask-trie pass kernel: 1 trie.cu (Σ <= 64), 0 generic radix
     int xl_compact = 1;        // cross-level chain: compacted parents (segrag.cu), 0 off
-    int light_grid = 0;        // light kernel grid in CTAs per SM (0: 8)
+    int light_grid = 0;        // light kernel grid in CTAs per SM (0: auto, 3 relabelled, else 8)
     int light_ctas = 4;        // relabelled light kernel register budget: CTAs per SM (3, 4, 6;
                                // Scale light 74.3 / 65.7 / 69.8 ms with far records)
     uint32_t* far_seen = nullptr;     // pinned copy of the record count (lagged gate)
@@ -1922,7 +1922,10 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
                             fp4_lv[m] ? 4u : 255u, stats, p->sm_count, s2,
                             perm_active && win_on ? wa : WinArgs{nullptr, nullptr, 0, 0, 0},
                             n >= (2ull << 20), perm_active ? far : FarRec{nullptr, nullptr, 0, 0},
-                            p->light_ctas, p->light_grid));
+                            p->light_ctas,
+                            // (relabelled: a 3-CTA/SM grid leaves room for the next batch's
+                            // passes on s: Scale 171-177 -> 166-167 ms; else 8 per SM)
+                            p->light_grid > 0 ? p->light_grid : (perm_active ? 3 : 8)));
             p->stage_end(s2, S_LIGHT, a);
             if (perm_active && far.near) {
                 // the apply is worth it once the records fill half the buffer (each
