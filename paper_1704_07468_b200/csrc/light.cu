@@ -85,19 +85,21 @@ struct FarSink {
     uint32_t used;  // slots of the chunk used (warp-uniform)
     bool have;      // a chunk is held
     bool ok;        // records on (and chunks left)
+    uint32_t count; // records written by this warp (warp-uniform)
     __device__ void start(const FarRec& f) {
         fr = f;
         base = 0;
         used = FAR_CHUNK;
         have = false;
         ok = f.near != 0;
+        count = 0;
     }
     __device__ void zero_rest() {  // unused slots of the held chunk -> 0 (no-op records)
         if (!have) return;
         for (uint32_t i = used + (threadIdx.x & 31); i < FAR_CHUNK; i += 32) fr.rec[base + i] = 0ull;
     }
     __device__ bool put(bool want, uint64_t cell, uint32_t val) {
-        want = want && ok && val < (1u << 24) && cell < (1ull << 40);
+        want = want && ok && val < (1u << 24);  // (cells < 2^40: N < 1.48M, checked by the host)
         const uint32_t m = __ballot_sync(0xffffffffu, want);
         if (!m) return false;
         const uint32_t nf = __popc(m);
@@ -118,6 +120,7 @@ struct FarSink {
         GK_CHECK(!want || base + used + __popc(m & lanemask_lt()) < fr.cap);
         if (want) fr.rec[base + used + __popc(m & lanemask_lt())] = cell << 24 | val;
         used += nf;
+        count += nf;
         return want;
     }
     __device__ void finish() { zero_rest(); }
@@ -237,9 +240,13 @@ __global__ void __launch_bounds__(256, MINB) light_kernel(SegmentOut so, int64_t
     __shared__ uint16_t s_tri[496];
     // per warp: the flat groups' triples (labels, counts), LF_STAGE entries
     __shared__ uint32_t s_stx[8][LF_STAGE], s_stc[8][LF_STAGE];
-    for (int b = 1, q = 0; b < 32; ++b)
-        for (int a = 0; a < b; ++a, ++q)
-            if (q % blockDim.x == threadIdx.x) s_tri[q] = (uint16_t)(a | (b << 5));
+    // entry q = b (b - 1) / 2 + a: b from the closed form (checked by one step each way)
+    for (int q = threadIdx.x; q < 496; q += blockDim.x) {
+        int b = (int)((1.0f + sqrtf(1.0f + 8.0f * (float)q)) * 0.5f);
+        if (b * (b - 1) / 2 > q) --b;
+        if ((b + 1) * b / 2 <= q) ++b;
+        s_tri[q] = (uint16_t)((q - b * (b - 1) / 2) | (b << 5));
+    }
     __syncthreads();
     const uint32_t G = so.counts[1];
     const int lane = threadIdx.x & 31;
@@ -255,7 +262,6 @@ __global__ void __launch_bounds__(256, MINB) light_kernel(SegmentOut so, int64_t
         GK_CHECK(!ok || NA != 0 || idx < (uint64_t)N * (uint64_t)(N - 1) / 2);
         if constexpr (FAR) {
             const bool rec = sink.put(ok && dist >= frec.near, idx, val);
-            nfar += rec ? 1u : 0u;
             if (ok && !rec) atomicAdd(&acc[idx], val);
         } else {
             pair_add<BINS>(acc, bn, ok, idx, val);
@@ -532,7 +538,7 @@ __global__ void __launch_bounds__(256, MINB) light_kernel(SegmentOut so, int64_t
     if (WIN) pairs += __reduce_add_sync(0xffffffffu, lpairs) * (lane == 0 ? 1ull : 0ull);
     if (lane == 0 && pairs) atomicAdd(&stats[ST_LIGHT_PAIRS], pairs);
     if (FAR) {
-        for (int o = 16; o > 0; o >>= 1) nfar += __shfl_xor_sync(0xffffffffu, nfar, o);
+        nfar = sink.count;
         if (lane == 0 && nfar) atomicAdd(&stats[ST_FAR_RECORDS], nfar);
     }
     if (lane == 0 && nheavy) atomicAdd(&stats[ST_HEAVY_GROUPS], nheavy);

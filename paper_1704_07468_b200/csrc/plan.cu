@@ -1277,7 +1277,8 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
     FarRec far{nullptr, nullptr, 0, 0};
     int far_bshift = 0;
     uint32_t far_thresh = 0;
-    if (relabel && (p->far_near > 0 || (p->far_near == -1 && ntri * 4 > (96ull << 20)))) {
+    if (relabel && ntri < (1ull << 40) &&
+        (p->far_near > 0 || (p->far_near == -1 && ntri * 4 > (96ull << 20)))) {
         // records are applied once they fill half the buffer (every cell of a block hit
         // several times per apply) and before each accumulator flush; up to 2^30
         // records (8 GB + the same for the bucketed copy) while 16 GB stay free
