@@ -173,10 +173,7 @@ struct SegmentOut {
     uint32_t* tseq;          // [T] seq id | (group-head << 31)
     uint32_t* tcnt;          // [T] run length (count of the (key, seq) pair)
     uint2* groups;           // [G] triple range [x, y) of each multi-sequence group
-    uint32_t* counts;        // [0] = T, [1] = G, [2] = Q
-    uint32_t* pairs = nullptr;  // [Q] (segrag.cu) groups of exactly 2 sequences: the index
-                                // of their first triple (the second follows); such groups
-                                // are not in `groups`. nullptr: every group is in `groups`
+    uint32_t* counts;        // [0] = T, [1] = G
 };
 
 // ---- hash-partition grouping (bucket.cu) ----

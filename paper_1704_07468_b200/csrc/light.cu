@@ -534,25 +534,6 @@ __global__ void __launch_bounds__(256, MINB) light_kernel(SegmentOut so, int64_t
             }
         }
     }
-    // (3) the pair list (segrag.cu): groups of exactly 2 sequences, one pair per lane
-    if (so.pairs) {
-        const uint32_t Q = so.counts[2];
-        for (uint64_t b0 = warp * 32; b0 < Q; b0 += nwarps * 32) {
-            const uint64_t i = b0 + lane;
-            uint64_t idx = 0;
-            uint32_t val = 0, dist = 0;
-            bool ok = false;
-            if (i < Q) {
-                const uint32_t t = so.pairs[i];
-                const uint32_t xa = so.tseq[t] & 0x7fffffffu, xb = so.tseq[t + 1] & 0x7fffffffu;
-                idx = pair_cell(xa, xb, N, NA, &ok, perm, FAR ? &dist : nullptr);
-                val = so.tcnt[t] * so.tcnt[t + 1];
-            }
-            const uint32_t nv = __popc(__ballot_sync(0xffffffffu, ok));
-            pairs += lane == 0 ? nv : 0u;
-            upd(ok, idx, val, dist);
-        }
-    }
     if (FAR) sink.finish();
     if (WIN) pairs += __reduce_add_sync(0xffffffffu, lpairs) * (lane == 0 ? 1ull : 0ull);
     if (lane == 0 && pairs) atomicAdd(&stats[ST_LIGHT_PAIRS], pairs);

@@ -127,7 +127,7 @@ struct gakco_plan {
 
     DevBuf genW0, genW1, genS0, genS1, kmdev, trieR, trieX0, trieX1, pdesc, wD, wlist, wfill, wC, winv, wtiles, trieS0, trieW, trieS, keptsh, dense2, heavy2, hcount2, tseq2, tcnt2, gstart2, counts2, perm, iota, best, parent, Dgscr, Kdscr, codes, off, gofs, gmseq, keysA, keysB, hist, status, ctr, tseq, tcnt, gstart, gend,
         counts, kept, stats, flags, kdiag, Cscr, Nmscr, Kscr, Knscr, heavy, hcount, dense, tiles, tiles4, symhist,
-        lightacc, binrec, bincnt, farrec, farscr, farbins, xccnt, xbcnt, qpairs, qpairs2, win, bkH, bktot, bkbase, bkdesc, bktab, bktcnt, bkgs, bkocc;
+        lightacc, binrec, bincnt, farrec, farscr, farbins, xccnt, xbcnt, win, bkH, bktot, bkbase, bkdesc, bktab, bktcnt, bkgs, bkocc;
     int64_t tiles_npad = -1;
     int tiles_pair = -1;
     int64_t tiles_na = -1;
@@ -472,7 +472,7 @@ extern "C" void gakco_destroy(gakco_plan* p) {
                       &p->hist,  &p->status, &p->ctr,  &p->tseq,   &p->tcnt,  &p->gstart,
                       &p->gend,  &p->counts, &p->kept, &p->stats,  &p->flags, &p->kdiag,
                       &p->Cscr,  &p->Nmscr, &p->Kscr,  &p->Knscr, &p->heavy, &p->hcount,
-                      &p->dense, &p->tiles, &p->tiles4, &p->symhist, &p->trieS0, &p->trieW, &p->trieS, &p->genW0, &p->genW1, &p->genS0, &p->genS1, &p->kmdev, &p->trieR, &p->trieX0, &p->trieX1, &p->pdesc, &p->wD, &p->wlist, &p->wfill, &p->wC, &p->winv, &p->wtiles, &p->lightacc, &p->binrec, &p->bincnt, &p->farrec, &p->farscr, &p->farbins, &p->xccnt, &p->xbcnt, &p->qpairs, &p->qpairs2,
+                      &p->dense, &p->tiles, &p->tiles4, &p->symhist, &p->trieS0, &p->trieW, &p->trieS, &p->genW0, &p->genW1, &p->genS0, &p->genS1, &p->kmdev, &p->trieR, &p->trieX0, &p->trieX1, &p->pdesc, &p->wD, &p->wlist, &p->wfill, &p->wC, &p->winv, &p->wtiles, &p->lightacc, &p->binrec, &p->bincnt, &p->farrec, &p->farscr, &p->farbins, &p->xccnt, &p->xbcnt,
                       &p->win,   &p->bkH,   &p->bktot, &p->bkbase, &p->bkdesc, &p->bktab,
                       &p->bktcnt, &p->bkgs, &p->bkocc};
     for (DevBuf* b : bufs)
@@ -1123,16 +1123,6 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
     if (xlc) {
         CK(p->ensure(p->xccnt, 2 * xl_maxrun * 4 + 16, s));
         CK(p->ensure(p->xbcnt, (bmax_masks + 2) * 4, s));
-        // groups of exactly 2 sequences as a pair list (first triple index each): the
-        // light kernel takes them one pair per lane, without the per-group machinery
-        CK(p->ensure(p->qpairs, (cap_keys / 2 + 2) * 4, s));
-        so1.pairs = (uint32_t*)p->qpairs.p;
-        if (pipe) {
-            CK(p->ensure(p->qpairs2, (cap_keys / 2 + 2) * 4, s));
-            so2.pairs = (uint32_t*)p->qpairs2.p;
-        } else {
-            so2.pairs = so1.pairs;
-        }
     }
     auto run_has_kids = [&](int r) {
         return r + 1 < (int)xl_link.size() && xl_link[r + 1] != 0;

@@ -41,8 +41,7 @@ __global__ void __launch_bounds__(RG_THREADS, 4) segment_rag_kernel(
     __shared__ uint32_t s_w[16];
     __shared__ uint16_t s_gpos[RG_TILE];
     __shared__ uint32_t s_tx[RG_TILE], s_tc[RG_TILE];
-    __shared__ uint32_t s_first_gh, s_base_t, s_base_g, s_base_c, s_base_p, s_tail;
-    __shared__ uint8_t s_isp[RG_TILE];  // group g of the tile has exactly 2 triples
+    __shared__ uint32_t s_first_gh, s_base_t, s_base_g, s_base_c, s_tail;
     __shared__ uint32_t s_wmin[RG_THREADS / 32], s_beyond, s_cross;
     __shared__ unsigned long long s_gend;
     constexpr uint32_t FULLM = (1u << RG_IT) - 1u;
@@ -236,12 +235,13 @@ __global__ void __launch_bounds__(RG_THREADS, 4) segment_rag_kernel(
     const uint32_t tail_len = (uint32_t)(gend - tile_end);
     if (tid == 0) {
         s_base_t = atomicAdd(&counters[0], agg_t + tail);
+        s_base_g = atomicAdd(&counters[1], agg_g);
         if (cw) s_base_c = atomicAdd(&ccnt[sgi], agg_k + tail_len);
         if (agg_t + tail) atomicAdd(&stats[ST_TRIPLES], (unsigned long long)(agg_t + tail));
         if (agg_g) atomicAdd(&stats[ST_GROUPS], (unsigned long long)agg_g);
     }
     __syncthreads();
-    const uint32_t base_t = s_base_t;
+    const uint32_t base_t = s_base_t, base_g = s_base_g;
     // 5. compacted elements of this tile, then the crossing group's tail
     if (cw) {
         const uint64_t cb = (uint64_t)sgi * n + s_base_c;
@@ -260,8 +260,7 @@ __global__ void __launch_bounds__(RG_THREADS, 4) segment_rag_kernel(
             cs[cb + agg_k + j] = sq[tile_end + j];
         }
     }
-    // 6. triples staged in shared memory, written coalesced; then the groups: those of
-    //    exactly 2 triples go to the pair list (so.pairs), the others get ranges
+    // 6. triples staged in shared memory, written coalesced; group ranges
     uint32_t li = off_t, gl = off_g;
 #pragma unroll
     for (int i = 0; i < RG_IT; ++i) {
@@ -277,42 +276,10 @@ __global__ void __launch_bounds__(RG_THREADS, 4) segment_rag_kernel(
         so.tseq[base_t + j] = s_tx[j];
         so.tcnt[base_t + j] = s_tc[j];
     }
-    // group g spans staged triples [s_gpos[g], s_gpos[g+1]) (the last: to agg_t, plus
-    // the crossing group's tail); thread tid classifies groups [tid G8, tid G8 + G8)
-    constexpr int G8 = RG_TILE / RG_THREADS;
-    uint32_t nq = 0, ng = 0;
-#pragma unroll
-    for (int u = 0; u < G8; ++u) {
-        const uint32_t g = (uint32_t)tid * G8 + u;
-        if (g >= agg_g) break;
-        const uint32_t e = g + 1 < agg_g ? s_gpos[g + 1] : agg_t + tail;
-        const bool pr = so.pairs && e - s_gpos[g] == 2u;
-        s_isp[g] = pr ? 1 : 0;
-        nq += pr ? 1u : 0u;
-        ng += pr ? 0u : 1u;
-    }
-    uint32_t aggqg;
-    const uint32_t offqg = scan256_excl(nq | (ng << 16), s_w, &aggqg);
-    if (tid == 0) {
-        s_base_g = atomicAdd(&counters[1], aggqg >> 16);
-        if (aggqg & 0xffffu) s_base_p = atomicAdd(&counters[2], aggqg & 0xffffu);
-    }
-    __syncthreads();
     const uint32_t tend = base_t + agg_t + tail;
-    {
-        uint32_t oq = offqg & 0xffffu, og = offqg >> 16;
-#pragma unroll
-        for (int u = 0; u < G8; ++u) {
-            const uint32_t g = (uint32_t)tid * G8 + u;
-            if (g >= agg_g) break;
-            if (s_isp[g]) {
-                so.pairs[s_base_p + oq++] = base_t + s_gpos[g];
-            } else {
-                so.groups[s_base_g + og++] =
-                    make_uint2(base_t + s_gpos[g], g + 1 < agg_g ? base_t + s_gpos[g + 1] : tend);
-            }
-        }
-    }
+    for (uint32_t g = tid; g < agg_g; g += RG_THREADS)
+        so.groups[base_g + g] =
+            make_uint2(base_t + s_gpos[g], g + 1 < agg_g ? base_t + s_gpos[g + 1] : tend);
     // 7. tail triples of the crossing group, in order
     if (tail) {  // (block-uniform)
         uint32_t wpos = base_t + agg_t;
@@ -351,7 +318,7 @@ cudaError_t launch_segment_rag(const uint64_t* w, const void* sq, bool seq16, ui
                                int64_t* diag, uint32_t* counters, SegmentOut so,
                                unsigned long long* stats, cudaStream_t s, uint64_t* cw,
                                void* cs, uint32_t* ccnt) {
-    cudaError_t e = cudaMemsetAsync(counters, 0, 3 * sizeof(uint32_t), s);
+    cudaError_t e = cudaMemsetAsync(counters, 0, 2 * sizeof(uint32_t), s);
     if (e != cudaSuccess || n == 0 || nseg == 0) return e;
     const uint64_t tps = (n + RG_TILE - 1) / RG_TILE;
     const unsigned grid = (unsigned)(tps * (uint64_t)nseg);
