@@ -89,22 +89,42 @@ METRICS = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.
            "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
            "sm__throughput.avg.pct_of_peak_sustained_elapsed",
            "lts__t_sectors.sum.pct_of_peak_sustained_elapsed",
+           "lts__t_sector_hit_rate.pct",
+           "smsp__issue_active.avg.pct_of_peak_sustained_active",
            "sm__pipe_tensor_cycles_active_realtime.avg.pct_of_peak_sustained_elapsed",
            "sm__warps_active.avg.pct_of_peak_sustained_active", "launch__grid_size",
            "launch__registers_per_thread"]
 
 
-def report(path, tag, config, out_dir):
+def report(paths, tag, config, out_dir):
+    if isinstance(paths, str):
+        paths = [paths]
+    lines, traffic = None, {}
+    for path in paths:
+        lines, traffic = _report_one(path, tag, lines, traffic)
+    with open(os.path.join(out_dir, f"{tag}_ncu.md"), "w") as f:
+        f.write("\n".join(lines) + "\n")
+    tp = os.path.join(out_dir, "ncu_traffic.json")
+    allt = json.load(open(tp)) if os.path.exists(tp) else {}
+    allt.setdefault(config, {})
+    for st, v in traffic.items():
+        allt[config][st] = {"dram_bytes_per_launch_mean": sum(v) / len(v), "launches": len(v),
+                            "source": tag}
+    json.dump(allt, open(tp, "w"), indent=1)
+
+
+def _report_one(path, tag, lines, traffic):
     raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv", "--metrics",
                           ",".join(METRICS)], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
     hdr, units = rows[0], rows[1]
     idx = {h: i for i, h in enumerate(hdr)}
-    lines = [f"# {tag}: ncu --set full capture (per launch)", "",
-             "| kernel | " + " | ".join(f"{m.split('.')[0]} [{units[idx[m]]}]"
-                                        for m in METRICS if m in idx) + " |",
-             "|---|" + "---|" * sum(1 for m in METRICS if m in idx)]
-    traffic = {}
+    if lines is None:
+        lines = [f"# {tag}: ncu --set full --clock-control none captures (per launch; "
+                 "cold caches: compare shares and counters, not absolute times)", "",
+                 "| kernel | " + " | ".join(f"{m.split('.')[0]} [{units[idx[m]]}]"
+                                            for m in METRICS if m in idx) + " |",
+                 "|---|" + "---|" * sum(1 for m in METRICS if m in idx)]
     for r in rows[2:]:
         k = short(r[idx["Kernel Name"]])
         lines.append(f"| {k} | " + " | ".join(r[idx[m]] for m in METRICS if m in idx) + " |")
@@ -115,21 +135,13 @@ def report(path, tag, config, out_dir):
             traffic.setdefault(STAGE.get(k, k), []).append(rb + wb)
         except (KeyError, ValueError):
             pass
-    with open(os.path.join(out_dir, f"{tag}_ncu.md"), "w") as f:
-        f.write("\n".join(lines) + "\n")
-    tp = os.path.join(out_dir, "ncu_traffic.json")
-    allt = json.load(open(tp)) if os.path.exists(tp) else {}
-    allt.setdefault(config, {})
-    for st, v in traffic.items():
-        allt[config][st] = {"dram_bytes_per_launch_mean": sum(v) / len(v), "launches": len(v),
-                            "source": os.path.basename(path)}
-    json.dump(allt, open(tp, "w"), indent=1)
+    return lines, traffic
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--launches")
-    ap.add_argument("--report")
+    ap.add_argument("--report", action="append")
     ap.add_argument("--tag", required=True)
     ap.add_argument("--config", default="dna")
     a = ap.parse_args()
