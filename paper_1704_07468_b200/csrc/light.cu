@@ -118,7 +118,8 @@ struct FarSink {
             have = true;
         }
         GK_CHECK(!want || base + used + __popc(m & lanemask_lt()) < fr.cap);
-        if (want) fr.rec[base + used + __popc(m & lanemask_lt())] = cell << 24 | val;
+        // (streaming store: the records must not evict the accumulator's L2-resident band)
+        if (want) __stcs(fr.rec + base + used + __popc(m & lanemask_lt()), cell << 24 | val);
         used += nf;
         count += nf;
         return want;
@@ -169,7 +170,7 @@ __global__ void far_add_kernel(const uint64_t* __restrict__ recs, const uint32_t
     const uint64_t lo = offs[b0], hi = offs[b1];
     for (uint64_t i = lo + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < hi;
          i += (uint64_t)gridDim.x * blockDim.x) {
-        const uint64_t r = recs[i];
+        const uint64_t r = __ldcs(recs + i);  // (streamed: keep the accumulator block in L2)
         const uint32_t v = (uint32_t)(r & 0xffffffull);
         GK_CHECK(!v || (r >> 24) < ntri);
         if (v) atomicAdd(&acc[r >> 24], v);
