@@ -381,6 +381,8 @@ __global__ void __launch_bounds__(256, MINB) light_kernel(SegmentOut so, int64_t
         // cluster's group plus a few random members from other clusters) stay on the
         // light path below. Counts > 255, < wmin members inside, or a full window: light.
         uint32_t my_win = 0xffffffffu;  // (lane jj: first label of group jj's window)
+        uint32_t want_w = 0xffffffffu;  // (lane jj: the window chosen for group jj)
+        bool want_split = false;
         if (WIN && wa.nw) {  // (a separate instantiation: no register cost otherwise)
             uint32_t cand = __ballot_sync(0xffffffffu, lane < ng && !flat &&
                                                            (int64_t)my_s < heavy_min &&
@@ -393,7 +395,9 @@ __global__ void __launch_bounds__(256, MINB) light_kernel(SegmentOut so, int64_t
                 // the most populated label bucket (128 labels) among the first 32 members,
                 // then the window (2 buckets) around it with the more members
                 const bool v0 = a0 + lane < b0;
-                const uint32_t bk = v0 ? perm[so.tseq[a0 + lane] & 0x7fffffffu] / WIN_STEP : 0xffffffffu;
+                const uint32_t lb0 = v0 ? perm[so.tseq[a0 + lane] & 0x7fffffffu] : 0u;
+                const uint32_t cb0 = v0 ? so.tcnt[a0 + lane] : 0u;
+                const uint32_t bk = v0 ? lb0 / WIN_STEP : 0xffffffffu;
                 const uint32_t peers = __match_any_sync(0xffffffffu, bk);
                 uint64_t key = v0 ? ((uint64_t)__popc(peers) << 32 | (uint64_t)(0xffffffffu - bk)) : 0ull;
 #pragma unroll
@@ -404,8 +408,17 @@ __global__ void __launch_bounds__(256, MINB) light_kernel(SegmentOut so, int64_t
                 uint32_t w = (cm > cp && bs > 0) ? bs - 1 : bs;
                 if (w >= wa.nw) w = wa.nw - 1;
                 const uint32_t lo = w * WIN_STEP;
+                // (the first 32 members' labels and counts are already in registers)
                 uint32_t nin = 0, nout = 0, cmax = 0;
-                for (uint32_t t = a0 + lane; t < b0; t += 32) {
+                if (v0) {
+                    if (lb0 - lo < (uint32_t)WIN_ROWS) {
+                        ++nin;
+                        cmax = cb0;
+                    } else {
+                        ++nout;
+                    }
+                }
+                for (uint32_t t = a0 + 32 + lane; t < b0; t += 32) {
                     const uint32_t lb = perm[so.tseq[t] & 0x7fffffffu];
                     if (lb - lo < (uint32_t)WIN_ROWS) {
                         ++nin;
@@ -417,18 +430,22 @@ __global__ void __launch_bounds__(256, MINB) light_kernel(SegmentOut so, int64_t
                 nin = __reduce_add_sync(0xffffffffu, nin);
                 nout = __reduce_add_sync(0xffffffffu, nout);
                 cmax = __reduce_max_sync(0xffffffffu, cmax);
-                if (cmax <= 255u && nin >= wa.wmin) {
-                    uint32_t col = 0;
-                    if (lane == 0) col = atomicAdd(&wa.fill[w], 1u);
-                    col = __shfl_sync(0xffffffffu, col, 0);
-                    if (col < wa.cap) {
-                        if (lane == 0) wa.list[(uint64_t)w * wa.cap + col] = make_uint2(a0, b0);
-                        if (nout == 0) got |= 1u << jj;
-                        else if (lane == jj) my_win = lo;  // (split: outside pairs below)
-                        nwin += lane == 0 ? 1u : 0u;
-                    }
+                if (cmax <= 255u && nin >= wa.wmin && lane == jj) {
+                    want_w = w;  // (claimed below, all of the batch's claims at once)
+                    want_split = nout > 0;
                 }
             }
+            // the claims: one column per chosen group, the atomics of all lanes in flight
+            // together (a claim per candidate would wait one round trip each)
+            uint32_t col = 0xffffffffu;
+            if (want_w != 0xffffffffu) col = atomicAdd(&wa.fill[want_w], 1u);
+            const bool claimed = want_w != 0xffffffffu && col < wa.cap;
+            if (claimed) {
+                wa.list[(uint64_t)want_w * wa.cap + col] = make_uint2(my_start, my_end);
+                if (want_split) my_win = want_w * WIN_STEP;  // (split: outside pairs below)
+            }
+            got |= __ballot_sync(0xffffffffu, claimed && !want_split);
+            nwin += lane == 0 ? __popc(__ballot_sync(0xffffffffu, claimed)) : 0u;
         }
 
         // (2) the other groups one by one (big light groups). Relabelled accumulator:
