@@ -445,7 +445,8 @@ __global__ void __launch_bounds__(256, MINB) light_kernel(SegmentOut so, int64_t
                 if (want_split) my_win = want_w * WIN_STEP;  // (split: outside pairs below)
             }
             got |= __ballot_sync(0xffffffffu, claimed && !want_split);
-            nwin += lane == 0 ? __popc(__ballot_sync(0xffffffffu, claimed)) : 0u;
+            const uint32_t ncl = __popc(__ballot_sync(0xffffffffu, claimed));  // (all lanes)
+            nwin += lane == 0 ? ncl : 0u;
         }
 
         // (2) the other groups one by one (big light groups). Relabelled accumulator:
