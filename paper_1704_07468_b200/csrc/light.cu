@@ -303,6 +303,7 @@ __global__ void __launch_bounds__(256, MINB) light_kernel(SegmentOut so, int64_t
         uint32_t* sx = s_stx[threadIdx.x >> 5];
         uint32_t* sc = s_stc[threadIdx.x >> 5];
         if (staged) {
+#pragma unroll 4
             for (uint32_t t = glo + lane; t < ghi; t += 32) {
                 const uint32_t x = so.tseq[t] & 0x7fffffffu;
                 sx[t - glo] = perm ? perm[x] : x;
@@ -387,16 +388,24 @@ __global__ void __launch_bounds__(256, MINB) light_kernel(SegmentOut so, int64_t
             uint32_t cand = __ballot_sync(0xffffffffu, lane < ng && !flat &&
                                                            (int64_t)my_s < heavy_min &&
                                                            my_s >= wa.wmin) & ~got;
+            // (the next candidate's first 32 members are loaded while one is evaluated)
+            uint32_t na0 = 0, nb0 = 0, nx0 = 0, nc0 = 0;
+            auto fetch = [&](int j) {
+                na0 = __shfl_sync(0xffffffffu, my_start, j);
+                nb0 = __shfl_sync(0xffffffffu, my_end, j);
+                nx0 = na0 + lane < nb0 ? so.tseq[na0 + lane] & 0x7fffffffu : 0u;
+                nc0 = na0 + lane < nb0 ? so.tcnt[na0 + lane] : 0u;
+            };
+            if (cand) fetch(__ffs(cand) - 1);
             while (cand) {
                 const int jj = __ffs(cand) - 1;
                 cand &= cand - 1;
-                const uint32_t a0 = __shfl_sync(0xffffffffu, my_start, jj);
-                const uint32_t b0 = __shfl_sync(0xffffffffu, my_end, jj);
+                const uint32_t a0 = na0, b0 = nb0, x0 = nx0, cb0 = nc0;
+                if (cand) fetch(__ffs(cand) - 1);
                 // the most populated label bucket (128 labels) among the first 32 members,
                 // then the window (2 buckets) around it with the more members
                 const bool v0 = a0 + lane < b0;
-                const uint32_t lb0 = v0 ? perm[so.tseq[a0 + lane] & 0x7fffffffu] : 0u;
-                const uint32_t cb0 = v0 ? so.tcnt[a0 + lane] : 0u;
+                const uint32_t lb0 = v0 ? perm[x0] : 0u;
                 const uint32_t bk = v0 ? lb0 / WIN_STEP : 0xffffffffu;
                 const uint32_t peers = __match_any_sync(0xffffffffu, bk);
                 uint64_t key = v0 ? ((uint64_t)__popc(peers) << 32 | (uint64_t)(0xffffffffu - bk)) : 0ull;
