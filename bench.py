@@ -654,6 +654,8 @@ def run_ours(a):
 
     out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
            "warmup": a.warmup, "ms_per_step": ms_per_step,
+           "step_ms_spread": {"min": min(step_ms), "median": statistics.median(step_ms),
+                              "max": max(step_ms)} if step_ms else None,
            "kernel_matrix_seconds": ms_per_step / 1e3, "higher_is_better": True,
            "scaling": "strong", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
            "config": config_dict(a.config, cfg, cp, masks, n, world),
