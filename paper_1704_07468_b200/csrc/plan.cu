@@ -107,8 +107,8 @@ struct gakco_plan {
     int light_grid = 0;        // light kernel grid in CTAs per SM (0: auto, 3 relabelled, else 8)
     int light_ctas = 4;        // relabelled light kernel register budget: CTAs per SM (3, 4, 6;
                                // Scale light 74.3 / 65.7 / 69.8 ms with far records)
-    uint32_t* far_seen = nullptr;     // pinned copy of the record count (lagged gate)
-    cudaEvent_t ev_far = nullptr;
+    uint32_t* far_seen = nullptr;     // pinned copies of the record count, a ring of 4
+    cudaEvent_t ev_far[4] = {};       // (the gate reads the copy of two batches ago)
     int64_t far_near = -1;     // far-pair records from this label distance: -1 auto (256
                                // with a relabelled accumulator), 0 off
     int pipeline = 1;          // light / dense / Gram of batch b on an aux stream, overlapping
@@ -485,7 +485,8 @@ extern "C" void gakco_destroy(gakco_plan* p) {
                           p->ev_join2, p->ev_build, p->ev_gram[0], p->ev_gram[1]})
         if (e) cudaEventDestroy(e);
     if (p->far_seen) cudaFreeHost(p->far_seen);
-    if (p->ev_far) cudaEventDestroy(p->ev_far);
+    for (cudaEvent_t e : p->ev_far)
+        if (e) cudaEventDestroy(e);
     if (p->aux) cudaStreamDestroy(p->aux);
     if (p->aux2) cudaStreamDestroy(p->aux2);
     delete p;
@@ -1277,6 +1278,7 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
     FarRec far{nullptr, nullptr, 0, 0};
     int far_bshift = 0;
     uint32_t far_thresh = 0;
+    int64_t far_batch = 0, far_last_apply = -4;  // (the gate's batch clock)
     if (relabel && ntri < (1ull << 40) &&
         (p->far_near > 0 || (p->far_near == -1 && ntri * 4 > (96ull << 20)))) {
         // records are applied once they fill half the buffer (every cell of a block hit
@@ -1296,10 +1298,10 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
         // bucket offsets [65] and a sink word
         CK(p->ensure(p->farbins, (256 + (size_t)p->sm_count * 2 * 64 + 72) * 4, s, /*zero=*/true));
         if (!p->far_seen) {
-            CK(cudaMallocHost(&p->far_seen, 4));
-            CK(cudaEventCreateWithFlags(&p->ev_far, cudaEventDisableTiming));
+            CK(cudaMallocHost(&p->far_seen, 4 * sizeof(uint32_t)));
+            for (auto& e : p->ev_far) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         }
-        *p->far_seen = 0;
+        for (int q = 0; q < 4; ++q) p->far_seen[q] = 0;
         CK(cudaMemsetAsync(p->farbins.p, 0, 256 * 4, s));
         int lb = 0;
         while (((uint64_t)1 << lb) < ntri) ++lb;
@@ -1376,8 +1378,7 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
             LK(launch_far_apply(far, (uint64_t*)p->farscr.p, (uint32_t*)p->farbins.p + 256,
                                 far_bshift, (uint32_t*)p->lightacc.p, ntri, p->sm_count, s2));
             p->stage_end(s2, S_FAR, al);
-            CK(cudaEventSynchronize(p->ev_far));  // (the pinned copy is rewritten below)
-            *p->far_seen = 0;
+            far_last_apply = far_batch;  // (copies older than this are stale)
         }
         p->stage_begin(s2, &al);
         if (rect)
@@ -1930,20 +1931,26 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
             p->stage_end(s2, S_LIGHT, a);
             if (perm_active && far.near) {
                 // the apply is worth it once the records fill half the buffer (each
-                // block's cells then hit several times); the count is read back one
-                // batch late (pinned copy + event, no host sync)
-                const bool seen = cudaEventQuery(p->ev_far) == cudaSuccess;
-                cudaGetLastError();  // (cudaErrorNotReady is not an error here)
-                if (seen && *p->far_seen >= far_thresh) {
-                    p->stage_begin(s2, &a);
-                    p->launches += 4 + 2 * 16;
-                    LK(launch_far_apply(far, (uint64_t*)p->farscr.p, (uint32_t*)p->farbins.p + 256,
-                                        far_bshift, (uint32_t*)p->lightacc.p, ntri, p->sm_count, s2));
-                    p->stage_end(s2, S_FAR, a);
-                    *p->far_seen = 0;
+                // block's cells then hit several times). The count is copied to a pinned
+                // ring after every batch; the gate reads the copy of two batches ago,
+                // waiting for it if the host is further ahead (bounded lag: at most two
+                // batches' records -- far below half the buffer -- arrive unseen, so it
+                // never overflows into REDs)
+                const int64_t fb = far_batch++;
+                if (fb >= 2) {
+                    const int q = (int)((fb - 2) & 3);
+                    CK(cudaEventSynchronize(p->ev_far[q]));
+                    if (far_last_apply < fb - 1 && p->far_seen[q] >= far_thresh) {
+                        p->stage_begin(s2, &a);
+                        p->launches += 4 + 2 * 16;
+                        LK(launch_far_apply(far, (uint64_t*)p->farscr.p, (uint32_t*)p->farbins.p + 256,
+                                            far_bshift, (uint32_t*)p->lightacc.p, ntri, p->sm_count, s2));
+                        p->stage_end(s2, S_FAR, a);
+                        far_last_apply = fb;
+                    }
                 }
-                CK(cudaMemcpyAsync(p->far_seen, far.fill, 4, cudaMemcpyDeviceToHost, s2));
-                CK(cudaEventRecord(p->ev_far, s2));
+                CK(cudaMemcpyAsync(p->far_seen + (fb & 3), far.fill, 4, cudaMemcpyDeviceToHost, s2));
+                CK(cudaEventRecord(p->ev_far[fb & 3], s2));
             }
             if (perm_active && win_on) {  // this batch's window columns (+ the Gram every few)
                 if (win_masks + nmask > win_lim) {  // s32 exactness of the next Gram
