@@ -107,8 +107,9 @@ struct gakco_plan {
     int light_grid = 0;        // light kernel grid in CTAs per SM (0: auto, 3 relabelled, else 8)
     int light_ctas = 4;        // relabelled light kernel register budget: CTAs per SM (3, 4, 6;
                                // Scale light 74.3 / 65.7 / 69.8 ms with far records)
-    uint32_t* far_seen = nullptr;     // pinned copies of the record count, a ring of 4
-    cudaEvent_t ev_far[4] = {};       // (the gate reads the copy of two batches ago)
+    static constexpr int FAR_RING = 8, FAR_LAG = 6;
+    uint32_t* far_seen = nullptr;     // pinned copies of the record count, a ring
+    cudaEvent_t ev_far[FAR_RING] = {};  // (the gate reads the copy of FAR_LAG batches ago)
     int64_t far_near = -1;     // far-pair records from this label distance: -1 auto (256
                                // with a relabelled accumulator), 0 off
     int pipeline = 1;          // light / dense / Gram of batch b on an aux stream, overlapping
@@ -1298,10 +1299,10 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
         // bucket offsets [65] and a sink word
         CK(p->ensure(p->farbins, (256 + (size_t)p->sm_count * 2 * 64 + 72) * 4, s, /*zero=*/true));
         if (!p->far_seen) {
-            CK(cudaMallocHost(&p->far_seen, 4 * sizeof(uint32_t)));
+            CK(cudaMallocHost(&p->far_seen, gakco_plan::FAR_RING * sizeof(uint32_t)));
             for (auto& e : p->ev_far) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         }
-        for (int q = 0; q < 4; ++q) p->far_seen[q] = 0;
+        for (int q = 0; q < gakco_plan::FAR_RING; ++q) p->far_seen[q] = 0;
         CK(cudaMemsetAsync(p->farbins.p, 0, 256 * 4, s));
         int lb = 0;
         while (((uint64_t)1 << lb) < ntri) ++lb;
@@ -1932,15 +1933,17 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
             if (perm_active && far.near) {
                 // the apply is worth it once the records fill half the buffer (each
                 // block's cells then hit several times). The count is copied to a pinned
-                // ring after every batch; the gate reads the copy of two batches ago,
-                // waiting for it if the host is further ahead (bounded lag: at most two
-                // batches' records -- far below half the buffer -- arrive unseen, so it
-                // never overflows into REDs)
+                // ring after every batch; the gate reads the copy of FAR_LAG batches ago,
+                // waiting for it if the host is further ahead (bounded lag: at most
+                // FAR_LAG batches' records -- below half the buffer at Scale's ~10M per
+                // batch -- arrive unseen, so it does not overflow into REDs; the host may
+                // still run FAR_LAG batches ahead of the light stream)
+                constexpr int LAG = gakco_plan::FAR_LAG, RING = gakco_plan::FAR_RING;
                 const int64_t fb = far_batch++;
-                if (fb >= 2) {
-                    const int q = (int)((fb - 2) & 3);
+                if (fb >= LAG) {
+                    const int q = (int)((fb - LAG) % RING);
                     CK(cudaEventSynchronize(p->ev_far[q]));
-                    if (far_last_apply < fb - 1 && p->far_seen[q] >= far_thresh) {
+                    if (far_last_apply < fb - LAG + 1 && p->far_seen[q] >= far_thresh) {
                         p->stage_begin(s2, &a);
                         p->launches += 4 + 2 * 16;
                         LK(launch_far_apply(far, (uint64_t*)p->farscr.p, (uint32_t*)p->farbins.p + 256,
@@ -1949,8 +1952,8 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
                         far_last_apply = fb;
                     }
                 }
-                CK(cudaMemcpyAsync(p->far_seen + (fb & 3), far.fill, 4, cudaMemcpyDeviceToHost, s2));
-                CK(cudaEventRecord(p->ev_far[fb & 3], s2));
+                CK(cudaMemcpyAsync(p->far_seen + (fb % RING), far.fill, 4, cudaMemcpyDeviceToHost, s2));
+                CK(cudaEventRecord(p->ev_far[fb % RING], s2));
             }
             if (perm_active && win_on) {  // this batch's window columns (+ the Gram every few)
                 if (win_masks + nmask > win_lim) {  // s32 exactness of the next Gram
