@@ -130,6 +130,9 @@ typedef enum {
                                      (<= 64 buckets, chunk prefixes inside the scatter: two
                                      launches) where sigma <= 64; 0 = the generic 8-bit radix
                                      pass (hist + chunk scan + scatter) */
+    GAKCO_OPT_FAR_BYTES = 21,     /* far-pair record width: 0 = automatic (4 bytes -- cell << 4 |
+                                     value, values 1..15, larger ones as REDs -- when every cell
+                                     index fits 28 bits, else 8), 4, 8 */
     GAKCO_OPT_LIGHT_GRID = 20,    /* light kernel grid size in CTAs per SM (0 = automatic: 3 for
                                      a relabelled accumulator, else 8); fewer leave room for the
                                      next batch's sort / segment kernels on the other stream */

@@ -270,7 +270,7 @@ cudaError_t launch_trie_pass64(const uint64_t* win, uint64_t* wout, const void* 
                                uint32_t dmask, uint64_t omask, uint32_t* H, int target_ctas,
                                cudaStream_t s, uint32_t* cnt_out = nullptr,
                                unsigned long long* stats = nullptr);
-cudaError_t launch_tp_records(const uint64_t* in, uint64_t* out, uint64_t n, const uint32_t* cntp,
+cudaError_t launch_tp_records(const void* in, void* out, bool k32, uint64_t n, const uint32_t* cntp,
                               int shift, uint32_t* H, int target_ctas, cudaStream_t s);
 cudaError_t launch_fill_u32(uint32_t* p, uint32_t v, uint32_t count, cudaStream_t s);
 // segrag.cu: the cross-level chain's leaves, ragged segments (cnt[s] valid elements
@@ -334,13 +334,14 @@ struct WinArgs {
 // falls back to REDs). near = 0: off.
 constexpr uint32_t FAR_CHUNK = 256;
 struct FarRec {
-    uint64_t* rec;     // [cap] records
+    uint64_t* rec;     // [cap] records: u64 cell << 24 | val, or (k32) u32 cell << 4 | val
     uint32_t* fill;    // [0] slots reserved (all warps)
     uint64_t cap;      // a multiple of FAR_CHUNK
     uint32_t near;     // label distance from which a pair is far (0: off)
+    bool k32 = false;  // 4-byte records (cells < 2^28, values 1..15; larger values: REDs)
 };
 // every pending record into acc (ntri cells); H: >= 2 * sm_count * 64 + 72 u32 scratch
-cudaError_t launch_far_apply(FarRec fr, uint64_t* scratch, uint32_t* H, int bshift,
+cudaError_t launch_far_apply(FarRec fr, void* scratch, uint32_t* H, int bshift,
                              uint32_t* acc, uint64_t ntri, int sm_count, cudaStream_t s);
 cudaError_t launch_window_build(SegmentOut so, WinArgs wa, const uint32_t* perm, uint8_t* wD,
                                 int sm_count, cudaStream_t s);

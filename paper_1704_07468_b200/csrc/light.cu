@@ -96,10 +96,14 @@ struct FarSink {
     }
     __device__ void zero_rest() {  // unused slots of the held chunk -> 0 (no-op records)
         if (!have) return;
-        for (uint32_t i = used + (threadIdx.x & 31); i < FAR_CHUNK; i += 32) fr.rec[base + i] = 0ull;
+        for (uint32_t i = used + (threadIdx.x & 31); i < FAR_CHUNK; i += 32) {
+            if (fr.k32) ((uint32_t*)fr.rec)[base + i] = 0u;
+            else fr.rec[base + i] = 0ull;
+        }
     }
     __device__ bool put(bool want, uint64_t cell, uint32_t val) {
-        want = want && ok && val < (1u << 24);  // (cells < 2^40: N < 1.48M, checked by the host)
+        // (cells < 2^40, or < 2^28 for 4-byte records: checked by the host)
+        want = want && ok && val < (fr.k32 ? 16u : (1u << 24));
         const uint32_t m = __ballot_sync(0xffffffffu, want);
         if (!m) return false;
         const uint32_t nf = __popc(m);
@@ -119,7 +123,11 @@ struct FarSink {
         }
         GK_CHECK(!want || base + used + __popc(m & lanemask_lt()) < fr.cap);
         // (streaming store: the records must not evict the accumulator's L2-resident band)
-        if (want) __stcs(fr.rec + base + used + __popc(m & lanemask_lt()), cell << 24 | val);
+        if (want) {
+            const uint64_t at = base + used + __popc(m & lanemask_lt());
+            if (fr.k32) __stcs((uint32_t*)fr.rec + at, (uint32_t)(cell << 4 | val));
+            else __stcs(fr.rec + at, cell << 24 | val);
+        }
         used += nf;
         count += nf;
         return want;
@@ -165,22 +173,25 @@ __global__ void far_warm_kernel(const uint32_t* __restrict__ acc, uint64_t c0, u
     }
     if (x == 0x9e3779b9u) *sink = x;  // (keeps the loads)
 }
-__global__ void far_add_kernel(const uint64_t* __restrict__ recs, const uint32_t* offs, int b0,
-                               int b1, uint32_t* acc, uint64_t ntri) {
+template <typename K>
+__global__ void far_add_kernel(const K* __restrict__ recs, const uint32_t* offs, int b0, int b1,
+                               uint32_t* acc, uint64_t ntri) {
+    constexpr int VB = sizeof(K) == 4 ? 4 : 24;  // value bits
     const uint64_t lo = offs[b0], hi = offs[b1];
     for (uint64_t i = lo + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < hi;
          i += (uint64_t)gridDim.x * blockDim.x) {
-        const uint64_t r = __ldcs(recs + i);  // (streamed: keep the accumulator block in L2)
-        const uint32_t v = (uint32_t)(r & 0xffffffull);
-        GK_CHECK(!v || (r >> 24) < ntri);
-        if (v) atomicAdd(&acc[r >> 24], v);
+        const K r = __ldcs(recs + i);  // (streamed: keep the accumulator block in L2)
+        const uint32_t v = (uint32_t)(r & (((K)1 << VB) - 1));
+        GK_CHECK(!v || (uint64_t)(r >> VB) < ntri);
+        if (v) atomicAdd(&acc[(uint64_t)(r >> VB)], v);
     }
 }
 
-cudaError_t launch_far_apply(FarRec fr, uint64_t* scratch, uint32_t* H, int bshift, uint32_t* acc,
+cudaError_t launch_far_apply(FarRec fr, void* scratch, uint32_t* H, int bshift, uint32_t* acc,
                              uint64_t ntri, int sm_count, cudaStream_t s) {
     const int cps = sm_count * 2;
-    cudaError_t e = launch_tp_records(fr.rec, scratch, fr.cap, fr.fill, 24 + bshift, H, cps, s);
+    cudaError_t e = launch_tp_records(fr.rec, scratch, fr.k32, fr.cap, fr.fill,
+                                      (fr.k32 ? 4 : 24) + bshift, H, cps, s);
     if (e != cudaSuccess) return e;
     uint32_t* offs = H + (size_t)cps * 64;  // [65]
     uint32_t* sink = offs + 66;
@@ -194,7 +205,12 @@ cudaError_t launch_far_apply(FarRec fr, uint64_t* scratch, uint32_t* H, int bshi
         uint64_t c1 = std::min<uint64_t>((uint64_t)b1 << bshift, ntri);
         c1 = c1 / 4 * 4;
         if (c1 > c0) far_warm_kernel<<<sm_count * 4, 256, 0, s>>>(acc, c0, c1, offs, b0, b1, sink);
-        far_add_kernel<<<sm_count * 8, 256, 0, s>>>(scratch, offs, b0, b1, acc, ntri);
+        if (fr.k32)
+            far_add_kernel<uint32_t><<<sm_count * 8, 256, 0, s>>>((const uint32_t*)scratch, offs, b0,
+                                                                  b1, acc, ntri);
+        else
+            far_add_kernel<uint64_t><<<sm_count * 8, 256, 0, s>>>((const uint64_t*)scratch, offs, b0,
+                                                                  b1, acc, ntri);
     }
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;

@@ -104,6 +104,7 @@ struct gakco_plan {
     int gram_fp4 = -1;         // -1 auto (e2m1 Gram when exact), 0 u8 / kind::i8, 1 e2m1
     int trie_pass = 1;         // mask-trie pass kernel: 1 trie.cu (Σ <= 64), 0 generic radix
     int xl_compact = 1;        // cross-level chain: compacted parents (segrag.cu), 0 off
+    int far_bytes = 0;         // far-pair record width: 0 auto (4 when cells < 2^28), 4, 8
     int light_grid = 0;        // light kernel grid in CTAs per SM (0: auto, 3 relabelled, else 8)
     int light_ctas = 4;        // relabelled light kernel register budget: CTAs per SM (3, 4, 6;
                                // Scale light 74.3 / 65.7 / 69.8 ms with far records)
@@ -562,6 +563,10 @@ extern "C" gakco_status gakco_set_option(gakco_plan* p, int option, int64_t valu
             return GAKCO_OK;
         case GAKCO_OPT_TIMING:
             p->timing = value != 0;
+            return GAKCO_OK;
+        case GAKCO_OPT_FAR_BYTES:
+            if (value != 0 && value != 4 && value != 8) return p->fail(GAKCO_E_ARG, "far bytes: 0, 4 or 8");
+            p->far_bytes = (int)value;
             return GAKCO_OK;
         case GAKCO_OPT_LIGHT_GRID:
             if (value < 0 || value > 64) return p->fail(GAKCO_E_ARG, "light grid: 0..64 CTAs per SM");
@@ -1285,16 +1290,19 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
         // records are applied once they fill half the buffer (every cell of a block hit
         // several times per apply) and before each accumulator flush; up to 2^30
         // records (8 GB + the same for the bucketed copy) while 16 GB stay free
+        // 4-byte records when every cell index fits 28 bits (Scale: 2e8 cells)
+        const bool k32 = p->far_bytes == 4 || (p->far_bytes == 0 && ntri < (1ull << 28));
+        if (k32 && ntri >= (1ull << 28)) return p->fail(GAKCO_E_ARG, "4-byte far records need < 2^28 cells");
         size_t fr = 0, tot = 0;
         cudaMemGetInfo(&fr, &tot);
-        const size_t have = std::max(p->farrec.cap, p->farscr.cap) / 8;
+        const size_t have = std::min(p->farrec.cap, p->farscr.cap) / (k32 ? 4 : 8);
         uint64_t cap = std::min<uint64_t>(1ull << 30, std::max<uint64_t>(
             std::max<uint64_t>(1ull << 24, have),
             fr > (16ull << 30) ? (fr - (16ull << 30)) / 16 : 0));
         cap = cap / FAR_CHUNK * FAR_CHUNK;
         far_thresh = (uint32_t)(cap / 2);
-        CK(p->ensure(p->farrec, cap * 8, s));
-        CK(p->ensure(p->farscr, cap * 8, s));
+        CK(p->ensure(p->farrec, cap * (k32 ? 4 : 8), s));
+        CK(p->ensure(p->farscr, cap * (k32 ? 4 : 8), s));
         // farbins: [0..255] the fill counter (at 192), then 2 x SMs x 64 chunk histograms,
         // bucket offsets [65] and a sink word
         CK(p->ensure(p->farbins, (256 + (size_t)p->sm_count * 2 * 64 + 72) * 4, s, /*zero=*/true));
@@ -1308,7 +1316,7 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
         while (((uint64_t)1 << lb) < ntri) ++lb;
         far_bshift = std::max(16, lb - 6);  // <= 64 accumulator blocks
         far = FarRec{(uint64_t*)p->farrec.p, (uint32_t*)p->farbins.p + 192, cap,
-                     (uint32_t)(p->far_near > 0 ? p->far_near : 256)};
+                     (uint32_t)(p->far_near > 0 ? p->far_near : 256), k32};
     }
     if (relabel) {
         CK(p->ensure(p->perm, N * 4, s));
@@ -1376,7 +1384,7 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
         if (perm_active && far.near) {  // every pending far record first
             p->stage_begin(s2, &al);
             p->launches += 4 + 2 * 16;
-            LK(launch_far_apply(far, (uint64_t*)p->farscr.p, (uint32_t*)p->farbins.p + 256,
+            LK(launch_far_apply(far, p->farscr.p, (uint32_t*)p->farbins.p + 256,
                                 far_bshift, (uint32_t*)p->lightacc.p, ntri, p->sm_count, s2));
             p->stage_end(s2, S_FAR, al);
             far_last_apply = far_batch;  // (copies older than this are stale)
@@ -1946,7 +1954,7 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
                     if (far_last_apply < fb - LAG + 1 && p->far_seen[q] >= far_thresh) {
                         p->stage_begin(s2, &a);
                         p->launches += 4 + 2 * 16;
-                        LK(launch_far_apply(far, (uint64_t*)p->farscr.p, (uint32_t*)p->farbins.p + 256,
+                        LK(launch_far_apply(far, p->farscr.p, (uint32_t*)p->farbins.p + 256,
                                             far_bshift, (uint32_t*)p->lightacc.p, ntri, p->sm_count, s2));
                         p->stage_end(s2, S_FAR, a);
                         far_last_apply = fb;

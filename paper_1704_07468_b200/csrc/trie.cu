@@ -67,10 +67,12 @@ __device__ __forceinline__ TpChunk tp_chunk(uint64_t cnt, uint32_t cps, uint32_t
     return {lo, min(cnt, lo + L)};
 }
 
-__global__ void __launch_bounds__(TP_THREADS) tp_hist_kernel(const uint64_t* __restrict__ w,
+template <typename K>
+__global__ void __launch_bounds__(TP_THREADS) tp_hist_kernel(const K* __restrict__ w,
                                                              uint64_t n, const uint32_t* cntp,
                                                              int shift, uint32_t dmask,
                                                              uint32_t* __restrict__ H) {
+    constexpr int E = 16 / sizeof(K);  // keys per 16-byte load
     __shared__ uint32_t s_h[TP_WARPS][TP_ND];
     const int tid = threadIdx.x, wp = tid >> 5;
     for (int i = tid; i < TP_WARPS * TP_ND; i += TP_THREADS) (&s_h[0][0])[i] = 0;
@@ -78,11 +80,11 @@ __global__ void __launch_bounds__(TP_THREADS) tp_hist_kernel(const uint64_t* __r
     const uint64_t cnt = cntp ? min((uint64_t)*cntp, n) : n;
     const TpChunk ch = tp_chunk(cnt, gridDim.x, blockIdx.x);
     uint64_t a = ch.lo;
-    if (a < ch.hi && ((uintptr_t)(w + a) & 15)) {  // (16-byte loads on the aligned body)
+    while (a < ch.hi && ((uintptr_t)(w + a) & 15)) {  // (16-byte loads on the aligned body)
         if (tid == 0) atomicAdd(&s_h[0][(uint32_t)(w[a] >> shift) & dmask], 1u);
         ++a;
     }
-    const uint64_t nv = a < ch.hi ? (ch.hi - a) / 2 : 0;
+    const uint64_t nv = a < ch.hi ? (ch.hi - a) / E : 0;
     const uint4* v = (const uint4*)(w + a);
     uint64_t i = tid;
     for (; i + 3 * TP_THREADS < nv; i += 4 * TP_THREADS) {  // (4 loads in flight)
@@ -91,17 +93,19 @@ __global__ void __launch_bounds__(TP_THREADS) tp_hist_kernel(const uint64_t* __r
         for (int u = 0; u < 4; ++u) q[u] = v[i + u * TP_THREADS];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-            atomicAdd(&s_h[wp][(uint32_t)(((uint64_t)q[u].y << 32 | q[u].x) >> shift) & dmask], 1u);
-            atomicAdd(&s_h[wp][(uint32_t)(((uint64_t)q[u].w << 32 | q[u].z) >> shift) & dmask], 1u);
+            const K* kq = (const K*)&q[u];
+#pragma unroll
+            for (int e = 0; e < E; ++e) atomicAdd(&s_h[wp][(uint32_t)(kq[e] >> shift) & dmask], 1u);
         }
     }
     for (; i < nv; i += TP_THREADS) {
         const uint4 q = v[i];
-        atomicAdd(&s_h[wp][(uint32_t)(((uint64_t)q.y << 32 | q.x) >> shift) & dmask], 1u);
-        atomicAdd(&s_h[wp][(uint32_t)(((uint64_t)q.w << 32 | q.z) >> shift) & dmask], 1u);
+        const K* kq = (const K*)&q;
+#pragma unroll
+        for (int e = 0; e < E; ++e) atomicAdd(&s_h[wp][(uint32_t)(kq[e] >> shift) & dmask], 1u);
     }
-    if (a + nv * 2 < ch.hi && tid == 0)
-        atomicAdd(&s_h[0][(uint32_t)(w[ch.hi - 1] >> shift) & dmask], 1u);
+    for (uint64_t r = a + nv * E + tid; r < ch.hi; r += TP_THREADS)
+        atomicAdd(&s_h[wp][(uint32_t)(w[r] >> shift) & dmask], 1u);
     __syncthreads();
     if (tid < TP_ND) {
         uint32_t s = 0;
@@ -136,22 +140,22 @@ __host__ __device__ constexpr uint32_t tp_psz() {
     return tp_pay<S>() ? (uint32_t)sizeof(S) : 0u;
 }
 
-template <typename S>
+template <typename K, typename S>
 constexpr size_t tp_smem() {
-    return 2 * (TP_TILE * 8 + 32) + (tp_pay<S>() ? 2 * (TP_TILE * tp_psz<S>() + 32) + TP_TILE * tp_psz<S>() : 0) +
+    return 2 * (TP_TILE * sizeof(K) + 32) + (tp_pay<S>() ? 2 * (TP_TILE * tp_psz<S>() + 32) + TP_TILE * tp_psz<S>() : 0) +
            2 * TP_ND * 8 + 2 * TP_WARPS * TP_ND * 4 + 2 * 8 * TP_ND * 4 + TP_ND * 4 + 16 + 2 * 8;
 }
 
-template <typename S>
+template <typename K, typename S>
 __global__ void __launch_bounds__(TP_THREADS, 2) tp_scatter_kernel(
-    const uint64_t* __restrict__ win, uint64_t* __restrict__ wout, const S* __restrict__ sin,
+    const K* __restrict__ win, K* __restrict__ wout, const S* __restrict__ sin,
     S* __restrict__ sout, uint64_t n, const uint32_t* cntp, int shift, uint32_t dmask,
-    uint64_t omask, const uint32_t* __restrict__ H, uint32_t* cnt_out, unsigned long long* stats) {
+    K omask, const uint32_t* __restrict__ H, uint32_t* cnt_out, unsigned long long* stats) {
     extern __shared__ __align__(16) unsigned char smem[];
     constexpr bool PAY = tp_pay<S>();
-    constexpr uint32_t WB = TP_TILE * 8 + 32, PB = PAY ? TP_TILE * tp_psz<S>() + 32 : 0;
-    uint64_t* const buf0 = (uint64_t*)smem;
-    uint64_t* const buf1 = (uint64_t*)(smem + WB);
+    constexpr uint32_t WB = TP_TILE * sizeof(K) + 32, PB = PAY ? TP_TILE * tp_psz<S>() + 32 : 0;
+    K* const buf0 = (K*)smem;
+    K* const buf1 = (K*)(smem + WB);
     S* const pbuf0 = (S*)(smem + 2 * WB);
     S* const pbuf1 = (S*)(smem + 2 * WB + PB);
     S* const s_pout = (S*)(smem + 2 * WB + 2 * PB);
@@ -236,18 +240,18 @@ __global__ void __launch_bounds__(TP_THREADS, 2) tp_scatter_kernel(
         const int b = (int)(t & 1u);
         const uint64_t t0 = lo + (uint64_t)t * TP_TILE;
         const uint32_t ct = (uint32_t)min((uint64_t)TP_TILE, hi - t0);
-        uint64_t* buf = b ? buf1 : buf0;
+        K* buf = b ? buf1 : buf0;
         const S* pbuf = b ? pbuf1 : pbuf0;
         mbar_wait(&s_bar[b], (t >> 1) & 1u);
-        const uint64_t* kin = buf + tp_delta(win, t0);
+        const K* kin = buf + tp_delta(win, t0);
         const S* pin = nullptr;
         if constexpr (PAY) pin = pbuf + tp_delta(sin, t0);
-        uint64_t keys[TP_ITEMS];
+        K keys[TP_ITEMS];
         uint32_t rank[TP_ITEMS / 2];  // two 12-bit ranks per register (tile < 2^16)
 #pragma unroll
         for (int i = 0; i < TP_ITEMS; ++i) {
             const uint32_t idx = (uint32_t)(wp * TP_ITEMS * 32 + i * 32 + lane);
-            keys[i] = idx < ct ? kin[idx] : 0ull;
+            keys[i] = idx < ct ? kin[idx] : (K)0;
         }
         // stable in-warp ranking: lanes of one digit meet in a shared atomicOr mask
 #pragma unroll
@@ -303,7 +307,7 @@ __global__ void __launch_bounds__(TP_THREADS, 2) tp_scatter_kernel(
         for (int j = 0; j < TP_ND / 32; ++j) whist[j * 32 + lane] = 0u;
         __syncthreads();  // (C) tile reordered in buf / s_pout
         for (uint32_t j = tid; j < ct; j += TP_THREADS) {
-            const uint64_t k = buf[j];
+            const K k = buf[j];
             const uint32_t d = (uint32_t)(k >> shift) & dmask;
             const uint64_t dst = (uint64_t)(s_goff[d] + (int64_t)j);
             GK_CHECK(dst < cnt);
@@ -333,19 +337,29 @@ cudaError_t launch_fill_u32(uint32_t* p, uint32_t v, uint32_t count, cudaStream_
 
 // records bucketed by a <= 6-bit digit (far-pair records: the accumulator block),
 // payload-less; cntp: device count (clamped to n)
-cudaError_t launch_tp_records(const uint64_t* in, uint64_t* out, uint64_t n, const uint32_t* cntp,
-                              int shift, uint32_t* H, int target_ctas, cudaStream_t s) {
+template <typename K>
+static cudaError_t tp_records(const K* in, K* out, uint64_t n, const uint32_t* cntp, int shift,
+                              uint32_t* H, int target_ctas, cudaStream_t s) {
     if (n == 0) return cudaGetLastError();
     const uint64_t tiles = (n + TP_TILE - 1) / TP_TILE;
     const unsigned cps = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(tiles, target_ctas));
-    tp_hist_kernel<<<cps, TP_THREADS, 0, s>>>(in, n, cntp, shift, 63u, H);
+    tp_hist_kernel<K><<<cps, TP_THREADS, 0, s>>>(in, n, cntp, shift, 63u, H);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
-    cudaFuncSetAttribute(tp_scatter_kernel<TpNoPay>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)tp_smem<TpNoPay>());
-    tp_scatter_kernel<TpNoPay><<<cps, TP_THREADS, tp_smem<TpNoPay>(), s>>>(
-        in, out, nullptr, nullptr, n, cntp, shift, 63u, ~0ull, H, nullptr, nullptr);
+    cudaFuncSetAttribute(tp_scatter_kernel<K, TpNoPay>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)tp_smem<K, TpNoPay>());
+    tp_scatter_kernel<K, TpNoPay><<<cps, TP_THREADS, tp_smem<K, TpNoPay>(), s>>>(
+        in, out, nullptr, nullptr, n, cntp, shift, 63u, ~(K)0, H, nullptr, nullptr);
     return cudaGetLastError();
+}
+
+cudaError_t launch_tp_records(const void* in, void* out, bool k32, uint64_t n, const uint32_t* cntp,
+                              int shift, uint32_t* H, int target_ctas, cudaStream_t s) {
+    if (k32)
+        return tp_records<uint32_t>((const uint32_t*)in, (uint32_t*)out, n, cntp, shift, H,
+                                    target_ctas, s);
+    return tp_records<uint64_t>((const uint64_t*)in, (uint64_t*)out, n, cntp, shift, H,
+                                target_ctas, s);
 }
 
 // Σ <= 64 (dmask < 64): the two-launch pass above; returns false when it does not
@@ -359,18 +373,18 @@ cudaError_t launch_trie_pass64(const uint64_t* win, uint64_t* wout, const void* 
     if (n == 0) return cudaGetLastError();
     const uint64_t tiles = (n + TP_TILE - 1) / TP_TILE;
     const unsigned cps = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(tiles, target_ctas));
-    tp_hist_kernel<<<cps, TP_THREADS, 0, s>>>(win, n, cntp, shift, dmask, H);
+    tp_hist_kernel<uint64_t><<<cps, TP_THREADS, 0, s>>>(win, n, cntp, shift, dmask, H);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     if (seq16) {
-        cudaFuncSetAttribute(tp_scatter_kernel<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)tp_smem<uint16_t>());
-        tp_scatter_kernel<uint16_t><<<cps, TP_THREADS, tp_smem<uint16_t>(), s>>>(
+        cudaFuncSetAttribute(tp_scatter_kernel<uint64_t, uint16_t>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tp_smem<uint64_t, uint16_t>());
+        tp_scatter_kernel<uint64_t, uint16_t><<<cps, TP_THREADS, tp_smem<uint64_t, uint16_t>(), s>>>(
             win, wout, (const uint16_t*)sin, (uint16_t*)sout, n, cntp, shift, dmask, omask, H, cnt_out, stats);
     } else {
-        cudaFuncSetAttribute(tp_scatter_kernel<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)tp_smem<uint32_t>());
-        tp_scatter_kernel<uint32_t><<<cps, TP_THREADS, tp_smem<uint32_t>(), s>>>(
+        cudaFuncSetAttribute(tp_scatter_kernel<uint64_t, uint32_t>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tp_smem<uint64_t, uint32_t>());
+        tp_scatter_kernel<uint64_t, uint32_t><<<cps, TP_THREADS, tp_smem<uint64_t, uint32_t>(), s>>>(
             win, wout, (const uint32_t*)sin, (uint32_t*)sout, n, cntp, shift, dmask, omask, H, cnt_out, stats);
     }
     return cudaGetLastError();

@@ -229,6 +229,7 @@ def test_far_pair_records(gk, oracle_lib):
     assert r0["stats"]["far_records"] == 0
     assert_parity(r0, ref)
     assert_parity(run(gk, cp, g, k, M, far_near=64, batch_keys=400000, light_window=0), ref)
+    assert_parity(run(gk, cp, g, k, M, far_bytes=8), ref)
 
 
 def test_light_relabel(gk, oracle_lib):
@@ -250,8 +251,10 @@ def test_light_relabel(gk, oracle_lib):
         assert_parity(run(gk, cp, g, k, M, light_relabel=1), ref)
         assert_parity(run(gk, cp, g, k, M, light_relabel=1, heavy_min_seqs=1 << 50), ref)
         assert_parity(run(gk, cp, g, k, M, light_relabel=1, light_window=0), ref)
-        # far-pair records forced at small N (every pair >= 3 labels apart a record)
+        # far-pair records forced at small N (every pair >= 3 labels apart a record),
+        # 4- and 8-byte records
         assert_parity(run(gk, cp, g, k, M, light_relabel=1, far_near=3), ref)
+        assert_parity(run(gk, cp, g, k, M, light_relabel=1, far_near=3, far_bytes=8), ref)
         # single-mask trie with cross-level reuse: relabelling puts level 0 first
         assert_parity(run(gk, cp, g, k, M, light_relabel=1, sort=6), ref)
 
