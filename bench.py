@@ -443,6 +443,11 @@ def run_ours(a):
     stage_ms = {}
     launches = 0
     last = None
+    # (the host enqueues every step's ~3000 launches: no garbage-collector pauses while
+    # the timed steps run)
+    import gc
+    gc.collect()
+    gc.disable()
     barrier()
     for i in range(a.steps):
         flush.fill_(i)                      # L2 flush, outside the step's events
@@ -453,6 +458,7 @@ def run_ours(a):
         launches += st["launches"]
         last = st
     barrier()
+    gc.enable()
     clocks = clk.stop() if clk else None
     # stage split: single-stream profiling steps with per-stage CUDA events (the
     # timed steps overlap light / dense / Gram of batch b with batch b+1 on two
@@ -655,7 +661,8 @@ def run_ours(a):
     out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": a.steps,
            "warmup": a.warmup, "ms_per_step": ms_per_step,
            "step_ms_spread": {"min": min(step_ms), "median": statistics.median(step_ms),
-                              "max": max(step_ms)} if step_ms else None,
+                              "max": max(step_ms), "all": [round(x, 2) for x in step_ms]}
+           if step_ms else None,
            "kernel_matrix_seconds": ms_per_step / 1e3, "higher_is_better": True,
            "scaling": "strong", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
            "config": config_dict(a.config, cfg, cp, masks, n, world),
