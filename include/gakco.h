@@ -130,6 +130,8 @@ typedef enum {
                                      (<= 64 buckets, chunk prefixes inside the scatter: two
                                      launches) where sigma <= 64; 0 = the generic 8-bit radix
                                      pass (hist + chunk scan + scatter) */
+    GAKCO_OPT_RELABEL_HOST = 22,  /* 1: the relabelling's sort by cluster runs on the host (one
+                                     host round trip per call); 0 (default): on the device */
     GAKCO_OPT_FAR_BYTES = 21,     /* far-pair record width: 0 = automatic (4 bytes -- cell << 4 |
                                      value, values 1..15, larger ones as REDs -- when every cell
                                      index fits 28 bits, else 8), 4, 8 */

@@ -367,6 +367,10 @@ cudaError_t launch_light_flush_perm(uint32_t* acc, int64_t N, int64_t* Cm, const
 cudaError_t launch_cluster_roots(const int64_t* C, int64_t N, unsigned long long* best,
                                  uint32_t* parent, const uint32_t* iota, int sm_count,
                                  cudaStream_t s);
+// device relabelling: keys root << 32 | x; labels from the root-sorted keys
+cudaError_t launch_relabel_keys(const uint32_t* root, int64_t N, uint64_t* keys, cudaStream_t s);
+cudaError_t launch_relabel_perm(const uint64_t* keys, int64_t N, uint32_t* perm, uint32_t* inv,
+                                cudaStream_t s);
 // rectangular accumulator (NA x NB, row-major) -> C_m (NA x NB), zeroed
 cudaError_t launch_light_flush_rect(uint32_t* acc, uint64_t cells, int64_t* Cm, int sm_count,
                                     cudaStream_t s);

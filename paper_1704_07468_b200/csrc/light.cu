@@ -786,6 +786,33 @@ cudaError_t launch_cluster_roots(const int64_t* C, int64_t N, unsigned long long
     return cudaGetLastError();
 }
 
+// device relabelling: keys root << 32 | x, then (after a stable sort by root) the labels
+__global__ void relabel_keys_kernel(const uint32_t* __restrict__ root, int64_t N, uint64_t* keys) {
+    for (int64_t x = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; x < N;
+         x += (int64_t)gridDim.x * blockDim.x)
+        keys[x] = (uint64_t)root[x] << 32 | (uint64_t)x;
+}
+__global__ void relabel_perm_kernel(const uint64_t* __restrict__ keys, int64_t N, uint32_t* perm,
+                                    uint32_t* inv) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < N;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t x = (uint32_t)(keys[i] & 0xffffffffull);
+        perm[x] = (uint32_t)i;
+        if (inv) inv[i] = x;
+    }
+}
+cudaError_t launch_relabel_keys(const uint32_t* root, int64_t N, uint64_t* keys, cudaStream_t s) {
+    const int blocks = (int)((N + 255) / 256 < 1024 ? (N + 255) / 256 : 1024);
+    relabel_keys_kernel<<<blocks, 256, 0, s>>>(root, N, keys);
+    return cudaGetLastError();
+}
+cudaError_t launch_relabel_perm(const uint64_t* keys, int64_t N, uint32_t* perm, uint32_t* inv,
+                                cudaStream_t s) {
+    const int blocks = (int)((N + 255) / 256 < 1024 ? (N + 255) / 256 : 1024);
+    relabel_perm_kernel<<<blocks, 256, 0, s>>>(keys, N, perm, inv);
+    return cudaGetLastError();
+}
+
 // Rectangular mode: C_m[X][Y - NA] += acc[X][Y - NA] (row-major NA x NB), zeroed.
 __global__ void light_flush_rect_kernel(uint32_t* __restrict__ acc, uint64_t cells,
                                         int64_t* __restrict__ Cm) {

@@ -105,6 +105,7 @@ struct gakco_plan {
     int trie_pass = 1;         // mask-trie pass kernel: 1 trie.cu (Σ <= 64), 0 generic radix
     int xl_compact = 1;        // cross-level chain: compacted parents (segrag.cu), 0 off
     int far_bytes = 0;         // far-pair record width: 0 auto (4 when cells < 2^28), 4, 8
+    int relabel_gpu = 1;       // relabelling computed on the device (1) or on the host (0)
     int light_grid = 0;        // light kernel grid in CTAs per SM (0: auto, 3 relabelled, else 8)
     int light_ctas = 4;        // relabelled light kernel register budget: CTAs per SM (3, 4, 6;
                                // Scale light 74.3 / 65.7 / 69.8 ms with far records)
@@ -129,7 +130,7 @@ struct gakco_plan {
 
     DevBuf genW0, genW1, genS0, genS1, kmdev, trieR, trieX0, trieX1, pdesc, wD, wlist, wfill, wC, winv, wtiles, trieS0, trieW, trieS, keptsh, dense2, heavy2, hcount2, tseq2, tcnt2, gstart2, counts2, perm, iota, best, parent, Dgscr, Kdscr, codes, off, gofs, gmseq, keysA, keysB, hist, status, ctr, tseq, tcnt, gstart, gend,
         counts, kept, stats, flags, kdiag, Cscr, Nmscr, Kscr, Knscr, heavy, hcount, dense, tiles, tiles4, symhist,
-        lightacc, binrec, bincnt, farrec, farscr, farbins, xccnt, xbcnt, win, bkH, bktot, bkbase, bkdesc, bktab, bktcnt, bkgs, bkocc;
+        lightacc, binrec, bincnt, farrec, farscr, farbins, xccnt, xbcnt, relkeys, relH, win, bkH, bktot, bkbase, bkdesc, bktab, bktcnt, bkgs, bkocc;
     int64_t tiles_npad = -1;
     int tiles_pair = -1;
     int64_t tiles_na = -1;
@@ -474,7 +475,7 @@ extern "C" void gakco_destroy(gakco_plan* p) {
                       &p->hist,  &p->status, &p->ctr,  &p->tseq,   &p->tcnt,  &p->gstart,
                       &p->gend,  &p->counts, &p->kept, &p->stats,  &p->flags, &p->kdiag,
                       &p->Cscr,  &p->Nmscr, &p->Kscr,  &p->Knscr, &p->heavy, &p->hcount,
-                      &p->dense, &p->tiles, &p->tiles4, &p->symhist, &p->trieS0, &p->trieW, &p->trieS, &p->genW0, &p->genW1, &p->genS0, &p->genS1, &p->kmdev, &p->trieR, &p->trieX0, &p->trieX1, &p->pdesc, &p->wD, &p->wlist, &p->wfill, &p->wC, &p->winv, &p->wtiles, &p->lightacc, &p->binrec, &p->bincnt, &p->farrec, &p->farscr, &p->farbins, &p->xccnt, &p->xbcnt,
+                      &p->dense, &p->tiles, &p->tiles4, &p->symhist, &p->trieS0, &p->trieW, &p->trieS, &p->genW0, &p->genW1, &p->genS0, &p->genS1, &p->kmdev, &p->trieR, &p->trieX0, &p->trieX1, &p->pdesc, &p->wD, &p->wlist, &p->wfill, &p->wC, &p->winv, &p->wtiles, &p->lightacc, &p->binrec, &p->bincnt, &p->farrec, &p->farscr, &p->farbins, &p->xccnt, &p->xbcnt, &p->relkeys, &p->relH,
                       &p->win,   &p->bkH,   &p->bktot, &p->bkbase, &p->bkdesc, &p->bktab,
                       &p->bktcnt, &p->bkgs, &p->bkocc};
     for (DevBuf* b : bufs)
@@ -563,6 +564,10 @@ extern "C" gakco_status gakco_set_option(gakco_plan* p, int option, int64_t valu
             return GAKCO_OK;
         case GAKCO_OPT_TIMING:
             p->timing = value != 0;
+            return GAKCO_OK;
+        case GAKCO_OPT_RELABEL_HOST:
+            if (value < 0 || value > 1) return p->fail(GAKCO_E_ARG, "relabel host must be 0 or 1");
+            p->relabel_gpu = value ? 0 : 1;
             return GAKCO_OK;
         case GAKCO_OPT_FAR_BYTES:
             if (value != 0 && value != 4 && value != 8) return p->fail(GAKCO_E_ARG, "far bytes: 0, 4 or 8");
@@ -1330,6 +1335,40 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
     }
     auto make_perm = [&](int m_done) -> gakco_status {
         Nvtx nv("relabel");
+        if (N < ((int64_t)1 << 31) && p->relabel_gpu) {
+            // on the device, no host round trip: the clusters, then the labels = the
+            // sequences stably sorted by cluster root (3 passes of 6 bits of the root,
+            // keys root << 32 | sequence; the sequence order is kept within a cluster)
+            if (pipe) {  // C of level m_done complete: its light and Gram flushes
+                CK(cudaEventRecord(p->ev_join, s2));
+                CK(cudaStreamWaitEvent(s, p->ev_join, 0));
+                CK(cudaEventRecord(p->ev_join2, s3));
+                CK(cudaStreamWaitEvent(s, p->ev_join2, 0));
+            }
+            cudaEvent_t ar = nullptr;
+            p->stage_begin(s, &ar);
+            p->launches += 4 + 2 * 3 + 2;
+            CK(launch_cluster_roots(level_ptr(m_done), N, (unsigned long long*)p->best.p,
+                                    (uint32_t*)p->parent.p, (const uint32_t*)p->iota.p,
+                                    p->sm_count, s));
+            CK(p->ensure(p->relkeys, (size_t)N * 16 + 64, s));
+            CK(p->ensure(p->relH, (size_t)p->sm_count * 2 * 64 * 4 + 64, s));
+            uint64_t* ka = (uint64_t*)p->relkeys.p;
+            uint64_t* kb = ka + N;
+            CK(launch_relabel_keys((const uint32_t*)p->parent.p, N, ka, s));
+            int rb = 0;
+            while (((int64_t)1 << rb) < N) ++rb;
+            for (int sh = 0; sh < rb; sh += 6) {
+                CK(launch_tp_records(ka, kb, false, (uint64_t)N, nullptr, 32 + sh,
+                                     (uint32_t*)p->relH.p, p->sm_count * 2, s));
+                std::swap(ka, kb);
+            }
+            CK(launch_relabel_perm(ka, N, (uint32_t*)p->perm.p, win_on ? (uint32_t*)p->winv.p : nullptr,
+                                   s));
+            p->stage_end(s, S_LIGHT, ar);
+            perm_active = true;
+            return GAKCO_OK;
+        }
         CK(cudaStreamSynchronize(s2));  // C of level m_done complete (light + Gram flushes)
         CK(cudaStreamSynchronize(s3));
         cudaEvent_t ar = nullptr;

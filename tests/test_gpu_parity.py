@@ -255,6 +255,7 @@ def test_light_relabel(gk, oracle_lib):
         # 4- and 8-byte records
         assert_parity(run(gk, cp, g, k, M, light_relabel=1, far_near=3), ref)
         assert_parity(run(gk, cp, g, k, M, light_relabel=1, far_near=3, far_bytes=8), ref)
+        assert_parity(run(gk, cp, g, k, M, light_relabel=1, relabel_host=1), ref)
         # single-mask trie with cross-level reuse: relabelling puts level 0 first
         assert_parity(run(gk, cp, g, k, M, light_relabel=1, sort=6), ref)
 
