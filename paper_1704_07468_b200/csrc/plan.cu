@@ -109,7 +109,7 @@ struct gakco_plan {
     int light_grid = 0;        // light kernel grid in CTAs per SM (0: auto, 3 relabelled, else 8)
     int light_ctas = 4;        // relabelled light kernel register budget: CTAs per SM (3, 4, 6;
                                // Scale light 74.3 / 65.7 / 69.8 ms with far records)
-    static constexpr int FAR_RING = 8, FAR_LAG = 6;
+    static constexpr int FAR_RING = 8, FAR_LAG = 6, FAR_EVERY = 8;
     uint32_t* far_seen = nullptr;     // pinned copies of the record count, a ring
     cudaEvent_t ev_far[FAR_RING] = {};  // (the gate reads the copy of FAR_LAG batches ago)
     int64_t far_near = -1;     // far-pair records from this label distance: -1 auto (256
@@ -1289,7 +1289,7 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
     FarRec far{nullptr, nullptr, 0, 0};
     int far_bshift = 0;
     uint32_t far_thresh = 0;
-    int64_t far_batch = 0, far_last_apply = -4;  // (the gate's batch clock)
+    int64_t far_batch = 0, far_last_apply = -4, far_seen_at = -4;  // (the gate's batch clock)
     if (relabel && ntri < (1ull << 40) &&
         (p->far_near > 0 || (p->far_near == -1 && ntri * 4 > (96ull << 20)))) {
         // records are applied once they fill half the buffer (every cell of a block hit
@@ -1978,19 +1978,28 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
                             p->light_grid > 0 ? p->light_grid : (perm_active ? 3 : 8)));
             p->stage_end(s2, S_LIGHT, a);
             if (perm_active && far.near) {
-                // the apply is worth it once the records fill half the buffer (each
-                // block's cells then hit several times). The count is copied to a pinned
-                // ring after every batch; the gate reads the copy of FAR_LAG batches ago,
-                // waiting for it if the host is further ahead (bounded lag: at most
-                // FAR_LAG batches' records -- below half the buffer at Scale's ~10M per
-                // batch -- arrive unseen, so it does not overflow into REDs; the host may
-                // still run FAR_LAG batches ahead of the light stream)
+                // the apply is worth it once many records are pending (each block's
+                // cells then hit several times). The count is copied to a pinned ring
+                // after every batch and polled without waiting (the copy of FAR_LAG
+                // batches ago): apply when it shows half the buffer used; if no count
+                // newer than the last apply has been seen for FAR_EVERY batches (the host
+                // far ahead of the GPU), apply anyway -- at Scale's <= 58M records per
+                // batch the buffer cannot fill in between. No host wait either way.
                 constexpr int LAG = gakco_plan::FAR_LAG, RING = gakco_plan::FAR_RING;
                 const int64_t fb = far_batch++;
+                bool due = false;
                 if (fb >= LAG) {
                     const int q = (int)((fb - LAG) % RING);
-                    CK(cudaEventSynchronize(p->ev_far[q]));
-                    if (far_last_apply < fb - LAG + 1 && p->far_seen[q] >= far_thresh) {
+                    const bool seen = cudaEventQuery(p->ev_far[q]) == cudaSuccess;
+                    cudaGetLastError();  // (cudaErrorNotReady is not an error here)
+                    if (seen && far_last_apply < fb - LAG + 1) {
+                        far_seen_at = fb - LAG;
+                        due = p->far_seen[q] >= far_thresh;
+                    }
+                }
+                due = due || fb - std::max(far_last_apply, far_seen_at) >= gakco_plan::FAR_EVERY;
+                {
+                    if (due) {
                         p->stage_begin(s2, &a);
                         p->launches += 4 + 2 * 16;
                         LK(launch_far_apply(far, p->farscr.p, (uint32_t*)p->farbins.p + 256,
