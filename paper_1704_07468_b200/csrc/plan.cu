@@ -109,7 +109,7 @@ struct gakco_plan {
     int light_grid = 0;        // light kernel grid in CTAs per SM (0: auto, 3 relabelled, else 8)
     int light_ctas = 4;        // relabelled light kernel register budget: CTAs per SM (3, 4, 6;
                                // Scale light 74.3 / 65.7 / 69.8 ms with far records)
-    static constexpr int FAR_RING = 8, FAR_LAG = 6, FAR_EVERY = 8;
+    static constexpr int FAR_RING = 8, FAR_LAG = 6, FAR_EVERY = 12;
     uint32_t* far_seen = nullptr;     // pinned copies of the record count, a ring
     cudaEvent_t ev_far[FAR_RING] = {};  // (the gate reads the copy of FAR_LAG batches ago)
     int64_t far_near = -1;     // far-pair records from this label distance: -1 auto (256
@@ -1982,7 +1982,7 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
                 // cells then hit several times). The count is copied to a pinned ring
                 // after every batch and polled without waiting (the copy of FAR_LAG
                 // batches ago): apply when it shows half the buffer used; if no count
-                // newer than the last apply has been seen for FAR_EVERY batches (the host
+                // newer than the last apply has been seen for FAR_EVERY (12) batches (the host
                 // far ahead of the GPU), apply anyway -- at Scale's <= 58M records per
                 // batch the buffer cannot fill in between. No host wait either way.
                 constexpr int LAG = gakco_plan::FAR_LAG, RING = gakco_plan::FAR_RING;
