@@ -189,6 +189,10 @@ typedef struct {
     int64_t n_far;
     int64_t pass_keys;      /* elements actually moved by the mask-trie passes (device count;
                                sort_passes counts capacities on the compacted chain) */
+    int64_t far_overflow;   /* warps whose far-record chunk claim found the buffer full (their
+                               remaining far pairs of that batch went to REDs; results unchanged) */
+    double ms_host;         /* host wall time of the last gakco_accumulate call (enqueueing;
+                               the host waits only where the GPU is behind) */
 } gakco_stats;
 
 /* Create a plan for alphabet size sigma (1..255), g-mer length g (1..32),

@@ -113,6 +113,7 @@ struct FarSink {
             if ((threadIdx.x & 31) == 0) b = atomicAdd(fr.fill, FAR_CHUNK);
             b = __shfl_sync(0xffffffffu, b, 0);
             if (b + FAR_CHUNK > fr.cap) {  // buffer full: this warp goes back to REDs
+                if ((threadIdx.x & 31) == 0) atomicAdd(fr.fill + 1, 1u);  // (counted: stats)
                 ok = false;
                 have = false;
                 return false;

@@ -13,9 +13,11 @@
 // P:141): partial C of several shards sum to the full C.
 #include <algorithm>
 #include <array>
+#include <chrono>
 #include <climits>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -40,6 +42,14 @@ struct Nvtx {
     explicit Nvtx(const char* name) { nvtxRangePushA(name); }
     ~Nvtx() { nvtxRangePop(); }
 };
+
+// free device memory (cudaMemGetInfo: called only when a buffer must grow -- it was
+// measured taking up to 50 ms on the box, the GPU idle meanwhile)
+static size_t free_bytes() {
+    size_t fr = 0, tot = 0;
+    if (cudaMemGetInfo(&fr, &tot) != cudaSuccess) return 0;
+    return fr;
+}
 
 struct DeviceGuard {
     int prev = -1;
@@ -155,6 +165,14 @@ struct gakco_plan {
     bool after_accumulate = false;
 
     std::vector<int64_t> h_off, h_gofs;
+    // host trace of the last accumulate (GAKCO_HOST_TRACE=1: printed to stderr)
+    int htrace_on = -1;
+    std::vector<uint8_t> h_ksh;  // host copy of keptsh (source of its async upload)
+    int64_t iota_n = -1;        // iota holds 0..iota_n-1 (uploaded once per N)
+    void* iota_at = nullptr;
+    uint32_t wtiles_nw = 0;     // wtiles holds the window-Gram tile list of wtiles_nw windows
+    void* wtiles_at = nullptr;
+    std::vector<std::pair<std::string, double>> htrace;
     std::vector<uint8_t> kept_h;
 
     gakco_status fail(gakco_status s, const std::string& msg) {
@@ -612,6 +630,17 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
                                     int64_t N, int64_t* C, cudaStream_t s, int rank, int world,
                                     int only_level = -1, int64_t NA = 0,
                                     int64_t* Dg = nullptr) {
+    const auto t_entry = std::chrono::steady_clock::now();
+    if (p->htrace_on < 0) {
+        const char* e = std::getenv("GAKCO_HOST_TRACE");
+        p->htrace_on = e && e[0] == '1';
+    }
+    p->htrace.clear();
+    auto HT = [&](const char* what) {
+        if (p->htrace_on)
+            p->htrace.emplace_back(what, std::chrono::duration<double, std::milli>(
+                                             std::chrono::steady_clock::now() - t_entry).count());
+    };
 #define CK(x)                                          \
     do {                                               \
         cudaError_t e_ = (x);                          \
@@ -646,6 +675,7 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
     for (int64_t i = 0; i < N; ++i)
         if (p->h_off[i + 1] < p->h_off[i]) return p->fail(GAKCO_E_ARG, "offsets decrease");
     const int64_t L = p->h_off[N];
+    HT("offsets");
 
     // g-mer counts n_X = max(0, l_X - g + 1) (reading A7/A8) and prefix sums
     p->h_gofs.assign(N + 1, 0);
@@ -728,6 +758,7 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
                        cudaMemcpyHostToDevice, s));
     CK(p->ensure(p->gmseq, n * sizeof(uint32_t), s));
     LK(launch_gmer_index((const int64_t*)p->gofs.p, N, (uint32_t*)p->gmseq.p, s));
+    HT("corpus");
 
     // this shard's masks, in processing order: levels ascending (default) or, with
     // GAKCO_OPT_LEVEL_ORDER, descending so the top level's long tensor-bound Gram
@@ -986,6 +1017,7 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
     unsigned long long* stats = (unsigned long long*)p->stats.p;
 
     // hash-partition buffers: packed windows, mask descriptors, big-bucket scratch
+    HT("maskplan");
     std::vector<MaskDesc> desc_h;
     if (hash_mode) {
         CK(p->ensure(p->win, n * 8, s));
@@ -1094,13 +1126,13 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
         CK(p->ensure(p->trieS, (size_t)g * n * ssz + 64, s));
         if (xl) {  // generation buffers: a level's unmasked sorted arrays, two levels
             const size_t need = 2 * xl_maxrun * n * (8 + ssz) + 256;
-            size_t fr = 0, tot = 0;
-            cudaMemGetInfo(&fr, &tot);
             const bool have = p->genW0.cap >= xl_maxrun * n * 8 + 64 &&
                               p->genW1.cap >= xl_maxrun * n * 8 + 64 &&
                               p->genS0.cap >= xl_maxrun * n * ssz + 64 &&
                               p->genS1.cap >= xl_maxrun * n * ssz + 64;
-            if (have || fr > need + (4ull << 30)) {
+            // (free memory is queried only when the buffers must grow: cudaMemGetInfo
+            // measured at up to 50 ms on the box, with the GPU idle meanwhile)
+            if (have || free_bytes() > need + (4ull << 30)) {
                 CK(p->ensure(p->genW0, xl_maxrun * n * 8 + 64, s));
                 CK(p->ensure(p->genW1, xl_maxrun * n * 8 + 64, s));
                 CK(p->ensure(p->genS0, xl_maxrun * n * ssz + 64, s));
@@ -1114,11 +1146,9 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
     }
     if (xlb && xl) {  // batched trie, cross-level: one-word composites per generation
         const size_t esb = tb64 ? 8 : 4;
-        size_t fr = 0, tot = 0;
-        cudaMemGetInfo(&fr, &tot);
         const bool have = p->genW0.cap >= xl_maxrun * n * esb + 64 &&
                           p->genW1.cap >= xl_maxrun * n * esb + 64;
-        if (have || fr > 2 * xl_maxrun * n * esb + (4ull << 30)) {
+        if (have || free_bytes() > 2 * xl_maxrun * n * esb + (4ull << 30)) {
             CK(p->ensure(p->genW0, xl_maxrun * n * esb + 64, s));
             CK(p->ensure(p->genW1, xl_maxrun * n * esb + 64, s));
             CK(p->ensure(p->kmdev, (bmax_masks + 2) * 8, s));
@@ -1141,7 +1171,10 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
     };
     if (use_win) {
         CK(p->ensure(p->win, n * 8, s));
-        std::vector<uint8_t> ksh(mine.size() * GMAX + GMAX, 0);
+        // (no stream sync: a cudaMemcpyAsync from pageable memory has staged the bytes
+        // when it returns; the source is kept in the plan all the same)
+        std::vector<uint8_t>& ksh = p->h_ksh;
+        ksh.assign(mine.size() * GMAX + GMAX, 0);
         for (size_t i = 0; i < mine.size(); ++i) {
             const int mm = p->mask_level[mine[i]];
             for (int r = 0; r < g - mm; ++r)
@@ -1149,7 +1182,6 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
         }
         CK(p->ensure(p->keptsh, ksh.size(), s));
         CK(cudaMemcpyAsync(p->keptsh.p, ksh.data(), ksh.size(), cudaMemcpyHostToDevice, s));
-        CK(cudaStreamSynchronize(s));  // ksh is a local buffer
     }
     if (hash_mode || use_win) {
         cudaEvent_t a0 = nullptr;
@@ -1271,15 +1303,20 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
         CK(p->ensure(p->wC, (size_t)nw * WIN_ROWS * WIN_ROWS * 8, s, /*zero=*/true));
         CK(cudaMemsetAsync(p->wC.p, 0, (size_t)nw * WIN_ROWS * WIN_ROWS * 8, s));
         CK(p->ensure(p->winv, N * 4, s));
-        std::vector<int2> wt;
-        for (uint32_t w = 0; w < nw; ++w) {
-            wt.push_back(make_int2((int)(2 * w), (int)w));
-            wt.push_back(make_int2((int)(2 * w + 1), (int)w));
+        CK(p->ensure(p->wtiles, (size_t)2 * nw * sizeof(int2), s));
+        if (p->wtiles_nw != nw || p->wtiles_at != p->wtiles.p) {  // (once per shape)
+            std::vector<int2> wt;
+            for (uint32_t w = 0; w < nw; ++w) {
+                wt.push_back(make_int2((int)(2 * w), (int)w));
+                wt.push_back(make_int2((int)(2 * w + 1), (int)w));
+            }
+            CK(cudaMemcpyAsync(p->wtiles.p, wt.data(), wt.size() * sizeof(int2),
+                               cudaMemcpyHostToDevice, s));
+            CK(cudaStreamSynchronize(s));  // wt is a local buffer
+            p->wtiles_nw = nw;
+            p->wtiles_at = p->wtiles.p;
         }
-        CK(p->ensure(p->wtiles, wt.size() * sizeof(int2), s));
-        CK(cudaMemcpyAsync(p->wtiles.p, wt.data(), wt.size() * sizeof(int2), cudaMemcpyHostToDevice, s));
-        CK(cudaStreamSynchronize(s));  // wt is a local buffer
-        nwtiles = (int)wt.size();
+        nwtiles = (int)(2 * nw);
         wa = WinArgs{(uint32_t*)p->wfill.p, (uint2*)p->wlist.p, (uint32_t)cap, nw,
                      (uint32_t)std::max<int64_t>(p->window_min, (int64_t)p->light_flat + 1)};
     }
@@ -1298,12 +1335,15 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
         // 4-byte records when every cell index fits 28 bits (Scale: 2e8 cells)
         const bool k32 = p->far_bytes == 4 || (p->far_bytes == 0 && ntri < (1ull << 28));
         if (k32 && ntri >= (1ull << 28)) return p->fail(GAKCO_E_ARG, "4-byte far records need < 2^28 cells");
-        size_t fr = 0, tot = 0;
-        cudaMemGetInfo(&fr, &tot);
         const size_t have = std::min(p->farrec.cap, p->farscr.cap) / (k32 ? 4 : 8);
-        uint64_t cap = std::min<uint64_t>(1ull << 30, std::max<uint64_t>(
-            std::max<uint64_t>(1ull << 24, have),
-            fr > (16ull << 30) ? (fr - (16ull << 30)) / 16 : 0));
+        // (buffers already at the 2^30-record maximum: no free-memory query)
+        uint64_t cap = 1ull << 30;
+        if (have < cap) {
+            const size_t fr = free_bytes();
+            cap = std::min<uint64_t>(1ull << 30, std::max<uint64_t>(
+                std::max<uint64_t>(1ull << 24, have),
+                fr > (16ull << 30) ? (fr - (16ull << 30)) / 16 : 0));
+        }
         cap = cap / FAR_CHUNK * FAR_CHUNK;
         far_thresh = (uint32_t)(cap / 2);
         CK(p->ensure(p->farrec, cap * (k32 ? 4 : 8), s));
@@ -1328,13 +1368,18 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
         CK(p->ensure(p->iota, N * 4, s));
         CK(p->ensure(p->best, N * 8, s));
         CK(p->ensure(p->parent, N * 4, s));
-        std::vector<uint32_t> io(N);
-        for (int64_t i = 0; i < N; ++i) io[i] = (uint32_t)i;
-        CK(cudaMemcpyAsync(p->iota.p, io.data(), N * 4, cudaMemcpyHostToDevice, s));
-        CK(cudaStreamSynchronize(s));  // io is a local buffer
+        if (p->iota_n != N || p->iota_at != p->iota.p) {  // (once per N: no per-call sync)
+            std::vector<uint32_t> io(N);
+            for (int64_t i = 0; i < N; ++i) io[i] = (uint32_t)i;
+            CK(cudaMemcpyAsync(p->iota.p, io.data(), N * 4, cudaMemcpyHostToDevice, s));
+            CK(cudaStreamSynchronize(s));  // io is a local buffer
+            p->iota_n = N;
+            p->iota_at = p->iota.p;
+        }
     }
     auto make_perm = [&](int m_done) -> gakco_status {
         Nvtx nv("relabel");
+        HT("relabel");
         if (N < ((int64_t)1 << 31) && p->relabel_gpu) {
             // on the device, no host round trip: the clusters, then the labels = the
             // sequences stably sorted by cluster root (3 passes of 6 bits of the root,
@@ -1419,6 +1464,7 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
     auto lflush = [&]() -> gakco_status {
         if (light_m < 0 || light_masks == 0) return GAKCO_OK;
         Nvtx nv("light flush");
+        HT("lflush");
         cudaEvent_t al = nullptr;
         if (perm_active && far.near) {  // every pending far record first
             p->stage_begin(s2, &al);
@@ -1477,8 +1523,10 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
         CK(cudaStreamWaitEvent(s2, p->ev_join, 0));
         CK(cudaStreamWaitEvent(s3, p->ev_join, 0));
     }
+    HT("setup");
     size_t pos = 0;
     while (pos < mine.size()) {
+        HT("batch");
         const int m = p->mask_level[mine[pos]];
         size_t end = pos;
         while (end < mine.size() && p->mask_level[mine[end]] == m && end - pos < bmax_masks) ++end;
@@ -2067,6 +2115,19 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
     p->host_stats.grouping = p->last_grouping;
     p->host_stats.n_pad = gram_ok ? n_pad : 0;
     p->host_stats.gram_fp4 = gram_ok ? fp4_used : 0;
+    p->host_stats.ms_host =
+        std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_entry).count();
+    HT("end");
+    if (p->htrace_on) {
+        std::string o = "{\"host_trace\": [";
+        for (size_t i = 0; i < p->htrace.size(); ++i) {
+            char b[96];
+            std::snprintf(b, sizeof b, "%s[\"%s\", %.2f]", i ? ", " : "", p->htrace[i].first.c_str(),
+                          p->htrace[i].second);
+            o += b;
+        }
+        std::fprintf(stderr, "%s]}\n", o.c_str());
+    }
     p->after_accumulate = true;
     return GAKCO_OK;
 #undef CK
@@ -2318,6 +2379,14 @@ extern "C" gakco_status gakco_get_stats(gakco_plan* p, gakco_stats* out) {
         r.win_macs = (int64_t)d[ST_WIN_MACS];
         r.far_records = (int64_t)d[ST_FAR_RECORDS];
         r.pass_keys = (int64_t)d[ST_PASS_KEYS];
+    }
+    if (p->farbins.p) {  // far-record chunk claims refused (buffer full: those warps used REDs)
+        uint32_t ov = 0;
+        cudaError_t e = cudaMemcpyAsync(&ov, (uint32_t*)p->farbins.p + 193, 4, cudaMemcpyDeviceToHost,
+                                        p->last_stream);
+        if (e == cudaSuccess) e = cudaStreamSynchronize(p->last_stream);
+        if (e != cudaSuccess) return p->cuda_fail(e, "stats");
+        r.far_overflow = ov;
     }
     double* ms[S_NSTAGE] = {&r.ms_encode, &r.ms_sort,     &r.ms_segment, &r.ms_light,
                             &r.ms_heavy,  &r.ms_epilogue, &r.ms_dense,   &r.ms_far};

@@ -70,7 +70,8 @@ class gakco_stats(ctypes.Structure):
             "sort_passes32", "grouping")] + [("ms_dense", ctypes.c_double)] + [
         (n, ctypes.c_int64) for n in ("n_dense", "n_pad", "gram_fp4", "heavy_macs_fp4",
                                         "win_groups", "win_macs", "far_records")] + [
-        ("ms_far", ctypes.c_double), ("n_far", ctypes.c_int64), ("pass_keys", ctypes.c_int64)]
+        ("ms_far", ctypes.c_double), ("n_far", ctypes.c_int64), ("pass_keys", ctypes.c_int64),
+        ("far_overflow", ctypes.c_int64), ("ms_host", ctypes.c_double)]
 
     def as_dict(self):
         return {n: getattr(self, n) for n, _ in self._fields_}
