@@ -1,4 +1,5 @@
 #!/bin/bash
+# bench lines of every config (Scale x3, Text, DNA, Protein, the default line)
 O=gpurun_out; T=${1:-r02ab}
 mkdir -p $O
 B="python bench.py --steps 10 --no-cpu-baseline --no-e2e"

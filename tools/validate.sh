@@ -1,5 +1,7 @@
 #!/bin/bash
-O=gpurun_out; T=${1:-r02x}
+# validation pass: smoke, the Scale-path GPU tests, three Scale bench lines
+#   gpurun --timeout 2400 -- "bash tools/validate.sh TAG"
+O=gpurun_out; T=${1:-val}
 mkdir -p $O
 python -c "import __graft_entry__ as g; g.build(); g.smoke()" > $O/${T}_smoke.log 2>&1; echo "smoke rc=$?" >> $O/${T}_smoke.log
 timeout 900 python -m pytest tests -m gpu -q -p no:cacheprovider -x -k "window or relabel or far or full_config or paths or sharded or k_only" > $O/${T}_pytest.log 2>&1; echo "pytest rc=$?" >> $O/${T}_pytest.log
