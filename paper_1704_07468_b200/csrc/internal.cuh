@@ -264,12 +264,15 @@ cudaError_t launch_trie_pass(const uint64_t* win, uint64_t* wout, const void* si
                              uint32_t* hist, int target_ctas, cudaStream_t s, int* nlaunch);
 // Σ <= 64 variant (trie.cu): hist + scatter (chunk prefixes computed in the scatter);
 // cntp: device element count (nullptr: n); n: capacity (grid size)
+constexpr int TP_HG_MAX_BLOCKS = 128;  // block sums of 8 chunk histograms (trie.cu), per parity
 bool trie_pass64_ok(uint32_t dmask);
 cudaError_t launch_trie_pass64(const uint64_t* win, uint64_t* wout, const void* sin, void* sout,
                                bool seq16, uint64_t n, const uint32_t* cntp, int shift,
                                uint32_t dmask, uint64_t omask, uint32_t* H, int target_ctas,
                                cudaStream_t s, uint32_t* cnt_out = nullptr,
-                               unsigned long long* stats = nullptr);
+                               unsigned long long* stats = nullptr, uint32_t* Hg = nullptr,
+                               uint32_t* par_ctr = nullptr);  // Hg: block sums (2 parities,
+                               // zero at first use); *par_ctr: the host's pass parity counter
 cudaError_t launch_tp_records(const void* in, void* out, bool k32, uint64_t n, const uint32_t* cntp,
                               int shift, uint32_t* H, int target_ctas, cudaStream_t s);
 cudaError_t launch_fill_u32(uint32_t* p, uint32_t v, uint32_t count, cudaStream_t s);

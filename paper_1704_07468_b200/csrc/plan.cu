@@ -140,7 +140,7 @@ struct gakco_plan {
 
     DevBuf genW0, genW1, genS0, genS1, kmdev, trieR, trieX0, trieX1, pdesc, wD, wlist, wfill, wC, winv, wtiles, trieS0, trieW, trieS, keptsh, dense2, heavy2, hcount2, tseq2, tcnt2, gstart2, counts2, perm, iota, best, parent, Dgscr, Kdscr, codes, off, gofs, gmseq, keysA, keysB, hist, status, ctr, tseq, tcnt, gstart, gend,
         counts, kept, stats, flags, kdiag, Cscr, Nmscr, Kscr, Knscr, heavy, hcount, dense, tiles, tiles4, symhist,
-        lightacc, binrec, bincnt, farrec, farscr, farbins, xccnt, xbcnt, relkeys, relH, win, bkH, bktot, bkbase, bkdesc, bktab, bktcnt, bkgs, bkocc;
+        lightacc, binrec, bincnt, farrec, farscr, farbins, xccnt, xbcnt, relkeys, relH, thg, win, bkH, bktot, bkbase, bkdesc, bktab, bktcnt, bkgs, bkocc;
     int64_t tiles_npad = -1;
     int tiles_pair = -1;
     int64_t tiles_na = -1;
@@ -168,6 +168,7 @@ struct gakco_plan {
     // host trace of the last accumulate (GAKCO_HOST_TRACE=1: printed to stderr)
     int htrace_on = -1;
     std::vector<uint8_t> h_ksh;  // host copy of keptsh (source of its async upload)
+    uint32_t tp_par = 0;        // pass parity of the trie passes' block sums (thg)
     int64_t iota_n = -1;        // iota holds 0..iota_n-1 (uploaded once per N)
     void* iota_at = nullptr;
     uint32_t wtiles_nw = 0;     // wtiles holds the window-Gram tile list of wtiles_nw windows
@@ -493,7 +494,7 @@ extern "C" void gakco_destroy(gakco_plan* p) {
                       &p->hist,  &p->status, &p->ctr,  &p->tseq,   &p->tcnt,  &p->gstart,
                       &p->gend,  &p->counts, &p->kept, &p->stats,  &p->flags, &p->kdiag,
                       &p->Cscr,  &p->Nmscr, &p->Kscr,  &p->Knscr, &p->heavy, &p->hcount,
-                      &p->dense, &p->tiles, &p->tiles4, &p->symhist, &p->trieS0, &p->trieW, &p->trieS, &p->genW0, &p->genW1, &p->genS0, &p->genS1, &p->kmdev, &p->trieR, &p->trieX0, &p->trieX1, &p->pdesc, &p->wD, &p->wlist, &p->wfill, &p->wC, &p->winv, &p->wtiles, &p->lightacc, &p->binrec, &p->bincnt, &p->farrec, &p->farscr, &p->farbins, &p->xccnt, &p->xbcnt, &p->relkeys, &p->relH,
+                      &p->dense, &p->tiles, &p->tiles4, &p->symhist, &p->trieS0, &p->trieW, &p->trieS, &p->genW0, &p->genW1, &p->genS0, &p->genS1, &p->kmdev, &p->trieR, &p->trieX0, &p->trieX1, &p->pdesc, &p->wD, &p->wlist, &p->wfill, &p->wC, &p->winv, &p->wtiles, &p->lightacc, &p->binrec, &p->bincnt, &p->farrec, &p->farscr, &p->farbins, &p->xccnt, &p->xbcnt, &p->relkeys, &p->relH, &p->thg,
                       &p->win,   &p->bkH,   &p->bktot, &p->bkbase, &p->bkdesc, &p->bktab,
                       &p->bktcnt, &p->bkgs, &p->bkocc};
     for (DevBuf* b : bufs)
@@ -1117,6 +1118,9 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
     std::array<int, GMAX> stack_pos{};
     int stack_depth = 0;
     if (trie) {
+        // block sums of the trie passes' chunk histograms (trie.cu), two parities,
+        // zero when allocated (each pass zeroes the other parity's for the next)
+        CK(p->ensure(p->thg, (size_t)2 * TP_HG_MAX_BLOCKS * 64 * 4, s, /*zero=*/true));
         CK(p->ensure(p->trieS0, n * ssz + 64, s));
         if (seq16)
             LK(launch_seq16((const uint32_t*)p->gmseq.p, (uint16_t*)p->trieS0.p, n, p->sm_count, s));
@@ -1807,7 +1811,7 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
                                           pS + (size_t)xl_parent[j] * n * ssz, sleaf, seq16, n,
                                           pC + xl_parent[j], bits * (g - 1 - xl_x[j]), dmask, ~0ull,
                                           (uint32_t*)p->hist.p, p->trie_ctas_per_sm * p->sm_count,
-                                          s, bcnt + (j - pos), stats));
+                                          s, bcnt + (j - pos), stats, (uint32_t*)p->thg.p, &p->tp_par));
                     p->launches += 1;  // hist + scatter
                     passkeys += (int64_t)n;  // (capacity: the actual count is on the device)
                     continue;
@@ -1825,7 +1829,7 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
                     LK(launch_trie_pass64(wi, wo, si, so_, seq16, n, nullptr, bits * (g - 1 - kept[t]),
                                           dmask, ~0ull, (uint32_t*)p->hist.p,
                                           p->trie_ctas_per_sm * p->sm_count, s,
-                                          leaf ? bcnt + (j - pos) : nullptr, stats));
+                                          leaf ? bcnt + (j - pos) : nullptr, stats, (uint32_t*)p->thg.p, &p->tp_par));
                     p->launches += 1;
                     if (!leaf) stack_pos[t] = kept[t];
                 }
@@ -1890,7 +1894,7 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
                                               pgenS + (size_t)xl_parent[j] * n * ssz, sleaf, seq16, n,
                                               nullptr, bits * (g - 1 - xl_x[j]), dmask, ~0ull,
                                               (uint32_t*)p->hist.p, p->trie_ctas_per_sm * p->sm_count, s,
-                                              nullptr, stats));
+                                              nullptr, stats, (uint32_t*)p->thg.p, &p->tp_par));
                     else
                         LK(launch_trie_pass(pgenW + (size_t)xl_parent[j] * n, wleaf,
                                             pgenS + (size_t)xl_parent[j] * n * ssz, sleaf, seq16, n,
@@ -1915,7 +1919,7 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
                     if (tp64)
                         LK(launch_trie_pass64(wi, wo, si, so_, seq16, n, nullptr, bits * (g - 1 - kept[t]),
                                               dmask, leaf && !xl ? kmask : ~0ull, (uint32_t*)p->hist.p,
-                                              p->trie_ctas_per_sm * p->sm_count, s, nullptr, stats));
+                                              p->trie_ctas_per_sm * p->sm_count, s, nullptr, stats, (uint32_t*)p->thg.p, &p->tp_par));
                     else
                         LK(launch_trie_pass(wi, wo, si, so_, seq16, n, bits * (g - 1 - kept[t]), dmask,
                                             leaf && !xl ? kmask : ~0ull, (uint32_t*)p->hist.p,

@@ -5,15 +5,20 @@
 // the kept positions of a mask (DESIGN.md §8 "Mask trie"): a pass is a stable
 // counting sort by the symbol at ONE kept position, digit = (w >> shift) & dmask.
 // Two launches per pass instead of the generic radix path's three:
-//   tp_hist:    CTA c counts the digits of its chunk (per-warp shared counters);
+//   tp_hist:    CTA c counts the digits of its chunk (per-warp shared counters,
+//               1024 threads); with Hg it also adds its counts into the sum of its
+//               block of 8 chunks (Hg, double-buffered by pass parity: the pass
+//               zeroes the other parity's sums for the next pass);
 //   tp_scatter: CTA c computes its chunk prefix and the digit bases itself from the
-//               chunk histograms (64 digits x 8 chunk strides in parallel: no
-//               separate scan launch), then streams its chunk in 4096-element tiles
-//               (cp.async.bulk into shared memory, one tile ahead), ranks each tile
-//               stably (warp atomicOr match + per-warp digit counters), reorders it
-//               in shared memory and writes every digit run contiguously.
-// 512 threads x 8 elements per tile (16 warps) keep the registers at <= 64 so two
-// CTAs (1024 threads) fit an SM next to their ~100 KB of shared memory.
+//               block sums and its block's chunk rows (<= 6 loads per thread, one
+//               round trip; without Hg: from every chunk row), then streams its
+//               chunk in 4096-element tiles (cp.async.bulk into shared memory, one
+//               tile ahead), ranks each tile stably (warp atomicOr match + per-warp
+//               digit counters; only digits and ranks stay in registers), records the
+//               tile's stable order as a 16-bit source-index permutation and writes
+//               every digit run contiguously, reading the elements through it.
+// 512 threads x 8 elements per tile (16 warps) keep the registers at <= 64 without
+// spills so two CTAs (1024 threads) fit an SM next to their ~90 KB of shared memory.
 //
 // The element count may live on the device (cntp != nullptr: a compacted parent
 // array of the cross-level chain, plan.cu); the grid is sized for the capacity n
@@ -67,15 +72,25 @@ __device__ __forceinline__ TpChunk tp_chunk(uint64_t cnt, uint32_t cps, uint32_t
     return {lo, min(cnt, lo + L)};
 }
 
+constexpr int TPH_THREADS = 1024;
+constexpr int TPH_WARPS = TPH_THREADS / 32;
+constexpr int TP_HG_BLOCK = 8;  // chunks per block sum
+
 template <typename K>
-__global__ void __launch_bounds__(TP_THREADS) tp_hist_kernel(const K* __restrict__ w,
-                                                             uint64_t n, const uint32_t* cntp,
-                                                             int shift, uint32_t dmask,
-                                                             uint32_t* __restrict__ H) {
+__global__ void __launch_bounds__(TPH_THREADS) tp_hist_kernel(const K* __restrict__ w,
+                                                              uint64_t n, const uint32_t* cntp,
+                                                              int shift, uint32_t dmask,
+                                                              uint32_t* __restrict__ H,
+                                                              uint32_t* __restrict__ Hg, int par) {
     constexpr int E = 16 / sizeof(K);  // keys per 16-byte load
-    __shared__ uint32_t s_h[TP_WARPS][TP_ND];
+    __shared__ uint32_t s_h[TPH_WARPS][TP_ND];
     const int tid = threadIdx.x, wp = tid >> 5;
-    for (int i = tid; i < TP_WARPS * TP_ND; i += TP_THREADS) (&s_h[0][0])[i] = 0;
+    for (int i = tid; i < TPH_WARPS * TP_ND; i += TPH_THREADS) (&s_h[0][0])[i] = 0;
+    if (Hg) {  // the other parity's block sums, zeroed for the next pass
+        uint32_t* z = Hg + (size_t)(par ^ 1) * TP_HG_MAX_BLOCKS * TP_ND;
+        const uint32_t nz = (gridDim.x + TP_HG_BLOCK - 1) / TP_HG_BLOCK * TP_ND;
+        for (uint32_t i = blockIdx.x * TPH_THREADS + tid; i < nz; i += gridDim.x * TPH_THREADS) z[i] = 0u;
+    }
     __syncthreads();
     const uint64_t cnt = cntp ? min((uint64_t)*cntp, n) : n;
     const TpChunk ch = tp_chunk(cnt, gridDim.x, blockIdx.x);
@@ -87,10 +102,10 @@ __global__ void __launch_bounds__(TP_THREADS) tp_hist_kernel(const K* __restrict
     const uint64_t nv = a < ch.hi ? (ch.hi - a) / E : 0;
     const uint4* v = (const uint4*)(w + a);
     uint64_t i = tid;
-    for (; i + 3 * TP_THREADS < nv; i += 4 * TP_THREADS) {  // (4 loads in flight)
+    for (; i + 3 * TPH_THREADS < nv; i += 4 * TPH_THREADS) {  // (4 loads in flight)
         uint4 q[4];
 #pragma unroll
-        for (int u = 0; u < 4; ++u) q[u] = v[i + u * TP_THREADS];
+        for (int u = 0; u < 4; ++u) q[u] = v[i + u * TPH_THREADS];
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
             const K* kq = (const K*)&q[u];
@@ -98,20 +113,22 @@ __global__ void __launch_bounds__(TP_THREADS) tp_hist_kernel(const K* __restrict
             for (int e = 0; e < E; ++e) atomicAdd(&s_h[wp][(uint32_t)(kq[e] >> shift) & dmask], 1u);
         }
     }
-    for (; i < nv; i += TP_THREADS) {
+    for (; i < nv; i += TPH_THREADS) {
         const uint4 q = v[i];
         const K* kq = (const K*)&q;
 #pragma unroll
         for (int e = 0; e < E; ++e) atomicAdd(&s_h[wp][(uint32_t)(kq[e] >> shift) & dmask], 1u);
     }
-    for (uint64_t r = a + nv * E + tid; r < ch.hi; r += TP_THREADS)
+    for (uint64_t r = a + nv * E + tid; r < ch.hi; r += TPH_THREADS)
         atomicAdd(&s_h[wp][(uint32_t)(w[r] >> shift) & dmask], 1u);
     __syncthreads();
     if (tid < TP_ND) {
         uint32_t s = 0;
 #pragma unroll
-        for (int ww = 0; ww < TP_WARPS; ++ww) s += s_h[ww][tid];
+        for (int ww = 0; ww < TPH_WARPS; ++ww) s += s_h[ww][tid];
         H[(uint64_t)blockIdx.x * TP_ND + tid] = s;
+        if (Hg && s)
+            atomicAdd(&Hg[((size_t)par * TP_HG_MAX_BLOCKS + blockIdx.x / TP_HG_BLOCK) * TP_ND + tid], s);
     }
 }
 
@@ -142,15 +159,16 @@ __host__ __device__ constexpr uint32_t tp_psz() {
 
 template <typename K, typename S>
 constexpr size_t tp_smem() {
-    return 2 * (TP_TILE * sizeof(K) + 32) + (tp_pay<S>() ? 2 * (TP_TILE * tp_psz<S>() + 32) + TP_TILE * tp_psz<S>() : 0) +
-           2 * TP_ND * 8 + 2 * TP_WARPS * TP_ND * 4 + 2 * 8 * TP_ND * 4 + TP_ND * 4 + 16 + 2 * 8;
+    return 2 * (TP_TILE * sizeof(K) + 32) + (tp_pay<S>() ? 2 * (TP_TILE * tp_psz<S>() + 32) : 0) +
+           TP_TILE * 2 + 2 * TP_ND * 8 + 2 * TP_WARPS * TP_ND * 4 + 2 * 8 * TP_ND * 4 + TP_ND * 4 + 16 + 2 * 8 + 8;
 }
 
 template <typename K, typename S>
 __global__ void __launch_bounds__(TP_THREADS, 2) tp_scatter_kernel(
     const K* __restrict__ win, K* __restrict__ wout, const S* __restrict__ sin,
     S* __restrict__ sout, uint64_t n, const uint32_t* cntp, int shift, uint32_t dmask,
-    K omask, const uint32_t* __restrict__ H, uint32_t* cnt_out, unsigned long long* stats) {
+    K omask, const uint32_t* __restrict__ H, const uint32_t* __restrict__ Hg, int par,
+    uint32_t* cnt_out, unsigned long long* stats) {
     extern __shared__ __align__(16) unsigned char smem[];
     constexpr bool PAY = tp_pay<S>();
     constexpr uint32_t WB = TP_TILE * sizeof(K) + 32, PB = PAY ? TP_TILE * tp_psz<S>() + 32 : 0;
@@ -158,8 +176,8 @@ __global__ void __launch_bounds__(TP_THREADS, 2) tp_scatter_kernel(
     K* const buf1 = (K*)(smem + WB);
     S* const pbuf0 = (S*)(smem + 2 * WB);
     S* const pbuf1 = (S*)(smem + 2 * WB + PB);
-    S* const s_pout = (S*)(smem + 2 * WB + 2 * PB);
-    unsigned char* q = smem + 2 * WB + 2 * PB + (PAY ? TP_TILE * tp_psz<S>() : 0);
+    uint16_t* const s_perm = (uint16_t*)(smem + 2 * WB + 2 * PB);  // [TILE] source index by output slot
+    unsigned char* q = smem + 2 * WB + 2 * PB + TP_TILE * 2;
     q = (unsigned char*)(((uintptr_t)q + 7) & ~(uintptr_t)7);
     int64_t* s_run = (int64_t*)q;                                         // [ND]
     int64_t* s_goff = s_run + TP_ND;                                      // [ND]
@@ -197,24 +215,46 @@ __global__ void __launch_bounds__(TP_THREADS, 2) tp_scatter_kernel(
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         for (uint32_t t = 0; t < 2 && t < ntile; ++t) issue(t, &s_bar[t]);
     }
-    // digit totals of the pass and this chunk's prefix, from the chunk histograms:
-    // thread (part p = tid / 64, digit d = tid % 64) sums chunks p, p + 8, ...
+    // digit totals of the pass and this chunk's prefix: thread (part p = tid / 64,
+    // digit d = tid % 64)
     {
         const int d = tid & (TP_ND - 1), p = tid >> 6;
+        constexpr uint32_t ST = TP_THREADS / TP_ND;  // 8 parts
         uint32_t tot = 0, pre = 0;
-        constexpr uint32_t ST = TP_THREADS / TP_ND;  // 8 chunk strides
-        // (8 independent loads in flight per round trip: the chunk rows are L2 reads)
-        for (uint32_t c0 = p; c0 < cps; c0 += 8 * ST) {
-            uint32_t v[8];
+        if (Hg) {
+            // block sums (8 chunks each): all blocks for the totals, those before this
+            // chunk's block for the prefix, plus the rows of the chunks of this block
+            // before it (every load independent: one round trip)
+            const uint32_t nb = (cps + TP_HG_BLOCK - 1) / TP_HG_BLOCK, cb = c / TP_HG_BLOCK;
+            const uint32_t* hg = Hg + (size_t)par * TP_HG_MAX_BLOCKS * TP_ND;
+            uint32_t v[TP_HG_MAX_BLOCKS / ST];
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
-                const uint32_t cc = c0 + u * ST;
-                v[u] = cc < cps ? H[(uint64_t)cc * TP_ND + d] : 0u;
+            for (int u = 0; u < TP_HG_MAX_BLOCKS / (int)ST; ++u) {
+                const uint32_t bb = p + u * ST;
+                v[u] = bb < nb ? hg[(size_t)bb * TP_ND + d] : 0u;
             }
+            const uint32_t own = (uint32_t)p < c - cb * TP_HG_BLOCK
+                                     ? H[(uint64_t)(cb * TP_HG_BLOCK + p) * TP_ND + d] : 0u;
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
+            for (int u = 0; u < TP_HG_MAX_BLOCKS / (int)ST; ++u) {
                 tot += v[u];
-                pre += c0 + u * ST < c ? v[u] : 0u;
+                pre += p + u * ST < cb ? v[u] : 0u;
+            }
+            pre += own;
+        } else {
+            // (8 independent loads in flight per round trip: the chunk rows are L2 reads)
+            for (uint32_t c0 = p; c0 < cps; c0 += 8 * ST) {
+                uint32_t v[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    const uint32_t cc = c0 + u * ST;
+                    v[u] = cc < cps ? H[(uint64_t)cc * TP_ND + d] : 0u;
+                }
+#pragma unroll
+                for (int u = 0; u < 8; ++u) {
+                    tot += v[u];
+                    pre += c0 + u * ST < c ? v[u] : 0u;
+                }
             }
         }
         s_part[p][d] = tot;
@@ -240,25 +280,22 @@ __global__ void __launch_bounds__(TP_THREADS, 2) tp_scatter_kernel(
         const int b = (int)(t & 1u);
         const uint64_t t0 = lo + (uint64_t)t * TP_TILE;
         const uint32_t ct = (uint32_t)min((uint64_t)TP_TILE, hi - t0);
-        K* buf = b ? buf1 : buf0;
+        const K* const buf = b ? buf1 : buf0;
         const S* pbuf = b ? pbuf1 : pbuf0;
         mbar_wait(&s_bar[b], (t >> 1) & 1u);
         const K* kin = buf + tp_delta(win, t0);
         const S* pin = nullptr;
         if constexpr (PAY) pin = pbuf + tp_delta(sin, t0);
-        K keys[TP_ITEMS];
-        uint32_t rank[TP_ITEMS / 2];  // two 12-bit ranks per register (tile < 2^16)
-#pragma unroll
-        for (int i = 0; i < TP_ITEMS; ++i) {
-            const uint32_t idx = (uint32_t)(wp * TP_ITEMS * 32 + i * 32 + lane);
-            keys[i] = idx < ct ? kin[idx] : (K)0;
-        }
-        // stable in-warp ranking: lanes of one digit meet in a shared atomicOr mask
+        // stable in-warp ranking: lanes of one digit meet in a shared atomicOr mask;
+        // only the digits (8 bits each, 4 per register) and ranks (16 bits, 2 per
+        // register) stay in registers -- the elements are read again by source index
+        uint32_t dg[TP_ITEMS / 4], rank[TP_ITEMS / 2];
 #pragma unroll
         for (int i = 0; i < TP_ITEMS; ++i) {
             const uint32_t idx = (uint32_t)(wp * TP_ITEMS * 32 + i * 32 + lane);
             const bool valid = idx < ct;
-            const uint32_t d = (uint32_t)(keys[i] >> shift) & dmask;
+            const uint32_t d = valid ? (uint32_t)(kin[idx] >> shift) & dmask : 0u;
+            dg[i / 4] = (i & 3) ? (dg[i / 4] | d << (8 * (i & 3))) : d;
             if (valid) atomicOr(&mbin[d], 1u << lane);
             __syncwarp();
             const uint32_t peers = valid ? mbin[d] : 0u;
@@ -272,7 +309,7 @@ __global__ void __launch_bounds__(TP_THREADS, 2) tp_scatter_kernel(
             const uint32_t r = prior + __popc(peers & lt);
             rank[i / 2] = (i & 1) ? (rank[i / 2] | r << 16) : r;
         }
-        __syncthreads();  // (A) counters final, tile read into registers
+        __syncthreads();  // (A) counters final
         uint32_t tcnt = 0;
         if (tid < TP_ND) {
 #pragma unroll
@@ -295,26 +332,26 @@ __global__ void __launch_bounds__(TP_THREADS, 2) tp_scatter_kernel(
         for (int i = 0; i < TP_ITEMS; ++i) {
             const uint32_t idx = (uint32_t)(wp * TP_ITEMS * 32 + i * 32 + lane);
             if (idx < ct) {
-                const uint32_t d = (uint32_t)(keys[i] >> shift) & dmask;
+                const uint32_t d = (dg[i / 4] >> (8 * (i & 3))) & 0xffu;
                 const uint32_t pos = whist[d] + ((rank[i / 2] >> (16 * (i & 1))) & 0xffffu);
                 GK_CHECK(pos < ct);
-                buf[pos] = keys[i];
-                if constexpr (PAY) s_pout[pos] = pin[idx];
+                s_perm[pos] = (uint16_t)idx;
             }
         }
         __syncwarp();
 #pragma unroll
         for (int j = 0; j < TP_ND / 32; ++j) whist[j * 32 + lane] = 0u;
-        __syncthreads();  // (C) tile reordered in buf / s_pout
+        __syncthreads();  // (C) the tile's stable order in s_perm
         for (uint32_t j = tid; j < ct; j += TP_THREADS) {
-            const K k = buf[j];
+            const uint32_t src = s_perm[j];
+            const K k = kin[src];
             const uint32_t d = (uint32_t)(k >> shift) & dmask;
             const uint64_t dst = (uint64_t)(s_goff[d] + (int64_t)j);
             GK_CHECK(dst < cnt);
             wout[dst] = k & omask;
-            if constexpr (PAY) sout[dst] = s_pout[j];
+            if constexpr (PAY) sout[dst] = pin[src];
         }
-        __syncthreads();  // (D) buf, s_pout free
+        __syncthreads();  // (D) the tile buffers free
         if (t + 2 < ntile && tid == 0) {
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             issue(t + 2, &s_bar[b]);
@@ -343,13 +380,13 @@ static cudaError_t tp_records(const K* in, K* out, uint64_t n, const uint32_t* c
     if (n == 0) return cudaGetLastError();
     const uint64_t tiles = (n + TP_TILE - 1) / TP_TILE;
     const unsigned cps = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(tiles, target_ctas));
-    tp_hist_kernel<K><<<cps, TP_THREADS, 0, s>>>(in, n, cntp, shift, 63u, H);
+    tp_hist_kernel<K><<<cps, TPH_THREADS, 0, s>>>(in, n, cntp, shift, 63u, H, nullptr, 0);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     cudaFuncSetAttribute(tp_scatter_kernel<K, TpNoPay>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)tp_smem<K, TpNoPay>());
     tp_scatter_kernel<K, TpNoPay><<<cps, TP_THREADS, tp_smem<K, TpNoPay>(), s>>>(
-        in, out, nullptr, nullptr, n, cntp, shift, 63u, ~(K)0, H, nullptr, nullptr);
+        in, out, nullptr, nullptr, n, cntp, shift, 63u, ~(K)0, H, nullptr, 0, nullptr, nullptr);
     return cudaGetLastError();
 }
 
@@ -369,23 +406,30 @@ bool trie_pass64_ok(uint32_t dmask) { return dmask < (uint32_t)TP_ND; }
 cudaError_t launch_trie_pass64(const uint64_t* win, uint64_t* wout, const void* sin, void* sout,
                                bool seq16, uint64_t n, const uint32_t* cntp, int shift,
                                uint32_t dmask, uint64_t omask, uint32_t* H, int target_ctas,
-                               cudaStream_t s, uint32_t* cnt_out, unsigned long long* stats) {
+                               cudaStream_t s, uint32_t* cnt_out, unsigned long long* stats,
+                               uint32_t* Hg, uint32_t* par_ctr) {
     if (n == 0) return cudaGetLastError();
     const uint64_t tiles = (n + TP_TILE - 1) / TP_TILE;
     const unsigned cps = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(tiles, target_ctas));
-    tp_hist_kernel<uint64_t><<<cps, TP_THREADS, 0, s>>>(win, n, cntp, shift, dmask, H);
+    if (cps > (unsigned)TP_HG_BLOCK * TP_HG_MAX_BLOCKS || !par_ctr) Hg = nullptr;
+    // (the parity advances only with a pass that uses the block sums: each such pass
+    // zeroes the sums the next one accumulates into)
+    const int par = Hg ? (int)((*par_ctr)++ & 1u) : 0;
+    tp_hist_kernel<uint64_t><<<cps, TPH_THREADS, 0, s>>>(win, n, cntp, shift, dmask, H, Hg, par);
     cudaError_t e = cudaGetLastError();
     if (e != cudaSuccess) return e;
     if (seq16) {
         cudaFuncSetAttribute(tp_scatter_kernel<uint64_t, uint16_t>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tp_smem<uint64_t, uint16_t>());
         tp_scatter_kernel<uint64_t, uint16_t><<<cps, TP_THREADS, tp_smem<uint64_t, uint16_t>(), s>>>(
-            win, wout, (const uint16_t*)sin, (uint16_t*)sout, n, cntp, shift, dmask, omask, H, cnt_out, stats);
+            win, wout, (const uint16_t*)sin, (uint16_t*)sout, n, cntp, shift, dmask, omask, H, Hg, par,
+            cnt_out, stats);
     } else {
         cudaFuncSetAttribute(tp_scatter_kernel<uint64_t, uint32_t>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tp_smem<uint64_t, uint32_t>());
         tp_scatter_kernel<uint64_t, uint32_t><<<cps, TP_THREADS, tp_smem<uint64_t, uint32_t>(), s>>>(
-            win, wout, (const uint32_t*)sin, (uint32_t*)sout, n, cntp, shift, dmask, omask, H, cnt_out, stats);
+            win, wout, (const uint32_t*)sin, (uint32_t*)sout, n, cntp, shift, dmask, omask, H, Hg, par,
+            cnt_out, stats);
     }
     return cudaGetLastError();
 }
