@@ -132,6 +132,12 @@ typedef enum {
                                      pass (hist + chunk scan + scatter) */
     GAKCO_OPT_RELABEL_HOST = 22,  /* 1: the relabelling's sort by cluster runs on the host (one
                                      host round trip per call); 0 (default): on the device */
+    GAKCO_OPT_LEAF_FUSE = 23,     /* mask trie with the cross-level chain: 1 (default) = a mask's
+                                     last pass is fused with its run-length (leaf.cu: each CTA
+                                     ranks whole groups of the pass before in shared memory;
+                                     no leaf array), where the groups of the pass before are
+                                     small (expected <= 512 g-mers); 0 = a global pass + the
+                                     segment kernel */
     GAKCO_OPT_FAR_BYTES = 21,     /* far-pair record width: 0 = automatic (4 bytes -- cell << 4 |
                                      value, values 1..15, larger ones as REDs -- when every cell
                                      index fits 28 bits, else 8), 4, 8 */

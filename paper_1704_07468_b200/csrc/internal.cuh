@@ -284,7 +284,18 @@ cudaError_t launch_segment_rag(const uint64_t* w, const void* sq, bool seq16, ui
                                const uint32_t* cnt, const uint64_t* km, int64_t dstride,
                                int64_t* diag, uint32_t* counters, SegmentOut so,
                                unsigned long long* stats, cudaStream_t s, uint64_t* cw,
-                               void* cs, uint32_t* ccnt);
+                               void* cs, uint32_t* ccnt, bool reset = true,
+                               unsigned max_ctas = 0);
+// leaf.cu: a mask's last pass (by the symbol at shift / dmask) over an array grouped
+// by pmask, fused with the run-length of segrag.cu (kmask: the mask's key). Appends to
+// so (counters = so.counts, not reset); cw/cs/ccnt: the compacted copy (optional);
+// groups larger than the tile are split into ow/os at atomicAdd(ocnt) (for segrag)
+int leaf_tile();  // group heads per CTA of launch_leaf
+cudaError_t launch_leaf(const uint64_t* w, const void* sq, bool seq16, uint64_t n,
+                        const uint32_t* cntp, uint64_t pmask, uint64_t kmask, int shift,
+                        uint32_t dmask, int64_t dstride, int64_t* diag, SegmentOut so,
+                        unsigned long long* stats, uint64_t* cw, void* cs, uint32_t* ccnt,
+                        uint64_t* ow, void* os, uint32_t* ocnt, cudaStream_t s);
 cudaError_t launch_seq16(const uint32_t* a, uint16_t* b, uint64_t n, int sm_count,
                          cudaStream_t s);
 cudaError_t launch_radix_chunked2(const void* in, void* out, bool k64, uint64_t n, int nseg,

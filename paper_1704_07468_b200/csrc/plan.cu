@@ -116,6 +116,7 @@ struct gakco_plan {
     int xl_compact = 1;        // cross-level chain: compacted parents (segrag.cu), 0 off
     int far_bytes = 0;         // far-pair record width: 0 auto (4 when cells < 2^28), 4, 8
     int relabel_gpu = 1;       // relabelling computed on the device (1) or on the host (0)
+    int leaf_fuse = 1;         // fused last pass + run-length (leaf.cu) in the chain
     int light_grid = 0;        // light kernel grid in CTAs per SM (0: auto, 3 relabelled, else 8)
     int light_ctas = 4;        // relabelled light kernel register budget: CTAs per SM (3, 4, 6;
                                // Scale light 74.3 / 65.7 / 69.8 ms with far records)
@@ -588,6 +589,10 @@ extern "C" gakco_status gakco_set_option(gakco_plan* p, int option, int64_t valu
             if (value < 0 || value > 1) return p->fail(GAKCO_E_ARG, "relabel host must be 0 or 1");
             p->relabel_gpu = value ? 0 : 1;
             return GAKCO_OK;
+        case GAKCO_OPT_LEAF_FUSE:
+            if (value < 0 || value > 1) return p->fail(GAKCO_E_ARG, "leaf fuse must be 0 or 1");
+            p->leaf_fuse = (int)value;
+            return GAKCO_OK;
         case GAKCO_OPT_FAR_BYTES:
             if (value != 0 && value != 4 && value != 8) return p->fail(GAKCO_E_ARG, "far bytes: 0, 4 or 8");
             p->far_bytes = (int)value;
@@ -722,7 +727,11 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
 
     // corpus to device (+ symbol check). The symbol histogram feeds the per-level
     // Gram operand format (auto e2m1 below); counted only when that choice is open.
-    const bool need_hist = p->gram_fp4 == -1 && (p->gram_pair || NA > 0) && nmax > 0 &&
+    // (also for the fused leaves of the mask trie: their gate is the expected largest
+    // group of the pass before, from the most frequent symbol)
+    const bool trie_pre = (p->sort_mode == 6 || (p->sort_mode == -1 && n >= (2ull << 20))) &&
+                          p->leaf_fuse && n > 0;
+    const bool need_hist = trie_pre || p->gram_fp4 == -1 && (p->gram_pair || NA > 0) && nmax > 0 &&
                            (uint64_t)nmax * (uint64_t)nmax < (1ull << 24);
     std::vector<unsigned long long> hist(256, 0);
     CK(p->ensure(p->codes, (size_t)L + 16, s));
@@ -751,6 +760,13 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
             CK(cudaMemcpyAsync(p->codes.p, codes, L, cudaMemcpyHostToDevice, s));
         }
     }
+    double fmax = 1.0;  // the most frequent symbol's share (1 when not counted)
+    if (need_hist && L > 0) {
+        unsigned long long hm = 0;
+        for (int c = 0; c < 256; ++c) hm = std::max(hm, hist[c]);
+        fmax = (double)hm / (double)L;
+    }
+    auto lf_big_expect = [&](int npos) { return (double)n * std::pow(fmax, (double)npos); };
     CK(p->ensure(p->off, (N + 1) * sizeof(int64_t), s));
     CK(p->ensure(p->gofs, (N + 1) * sizeof(int64_t), s));
     CK(cudaMemcpyAsync(p->off.p, p->h_off.data(), (N + 1) * sizeof(int64_t),
@@ -1790,35 +1806,74 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
             const bool kids = run_has_kids(xl_run[pos]);
             if (xl_slot[pos] == 0 && kids)  // a run starts: its compacted counts from 0
                 CK(cudaMemsetAsync(cC, 0, xl_maxrun * 4, s));
+            // fused leaves (leaf.cu): a mask's last pass and its run-length in one kernel
+            // over whole groups of the pass before -- where those groups are small: the
+            // expected LARGEST one, n f_max^positions (f_max: the most frequent symbol's
+            // share; independent symbols), at most half a tile (Text's level-5 leaves:
+            // 6e6 x 0.24^4 = 2e4 -> unfused; Scale: 41 -> fused). A larger group is
+            // split by its owner CTA into the mask's overflow slot, which the segment
+            // kernel takes afterwards.
+            auto fuse_ok = [&](int npos) {
+                return p->leaf_fuse && npos >= 1 && lf_big_expect(npos) <= (double)leaf_tile() / 2;
+            };
+            auto pos_mask = [&](int x) { return (uint64_t)dmask << (bits * (g - 1 - x)); };
+            const size_t slot0 = (size_t)xl_slot[pos];
+            // (a batch is one level: every mask has kk kept positions; kk >= 2 for a trie
+            // leaf, kk >= 1 for a chain pass -- kk - 1 >= 1 either way)
+            const bool fused_any = kk >= 2 && fuse_ok(kk - 1);
+            if (fused_any) {  // the fused leaves write this batch's segment outputs
+                gakco_status ws = wait_buf();
+                if (ws != GAKCO_OK) return ws;
+                CK(cudaMemsetAsync(so.counts, 0, 2 * sizeof(uint32_t), s));
+                CK(cudaMemsetAsync(bcnt, 0, (size_t)nmask * 4, s));
+            }
             std::vector<uint64_t> kms;
-            p->stage_begin(s, &a);
             for (size_t j = pos; j < end; ++j) {
                 const uint8_t* kept = trie_chain[j].data();
                 uint64_t* wleaf = (uint64_t*)p->keysA.p + (j - pos) * n;
                 uint8_t* sleaf = (uint8_t*)p->keysB.p + (j - pos) * n * ssz;
+                uint32_t* ocnt = bcnt + (j - pos);
                 uint64_t kmask = 0;
-                for (int r = 0; r < kk; ++r)
-                    kmask |= (uint64_t)dmask << (bits * (g - 1 - p->mask_kept[mine[j]][r]));
+                for (int r = 0; r < kk; ++r) kmask |= pos_mask(p->mask_kept[mine[j]][r]);
                 kms.push_back(kmask);
+                uint64_t* lcw = kids ? cW + (size_t)xl_slot[j] * n : nullptr;
+                void* lcs = kids ? (void*)(cS + (size_t)xl_slot[j] * n * ssz) : nullptr;
+                uint32_t* lcc = kids ? cC + xl_slot[j] : nullptr;
+                p->stage_begin(s, &a);
                 if (kk == 0) {  // no kept position: one key, identity order (raw windows)
                     CK(cudaMemcpyAsync(wleaf, p->win.p, n * 8, cudaMemcpyDeviceToDevice, s));
                     CK(cudaMemcpyAsync(sleaf, p->trieS0.p, n * ssz, cudaMemcpyDeviceToDevice, s));
-                    LK(launch_fill_u32(bcnt + (j - pos), (uint32_t)n, 1, s));
+                    LK(launch_fill_u32(ocnt, (uint32_t)n, 1, s));
+                    p->stage_end(s, S_SORT, a);
                     continue;
                 }
                 if (xl_parent[j] >= 0) {  // one pass over the parent's compacted elements
-                    LK(launch_trie_pass64(pW + (size_t)xl_parent[j] * n, wleaf,
-                                          pS + (size_t)xl_parent[j] * n * ssz, sleaf, seq16, n,
-                                          pC + xl_parent[j], bits * (g - 1 - xl_x[j]), dmask, ~0ull,
-                                          (uint32_t*)p->hist.p, p->trie_ctas_per_sm * p->sm_count,
-                                          s, bcnt + (j - pos), stats, (uint32_t*)p->thg.p, &p->tp_par));
-                    p->launches += 1;  // hist + scatter
+                    const uint64_t* iw = pW + (size_t)xl_parent[j] * n;
+                    const void* is = pS + (size_t)xl_parent[j] * n * ssz;
+                    const int sh = bits * (g - 1 - xl_x[j]);
+                    if (fuse_ok(kk - 1)) {
+                        p->stage_end(s, S_SORT, a);
+                        p->stage_begin(s, &a);
+                        p->launches += 1;
+                        LK(launch_leaf(iw, is, seq16, n, pC + xl_parent[j], kmask & ~pos_mask(xl_x[j]),
+                                       kmask, sh, dmask, dstride, Dm, so, stats, lcw, lcs, lcc, wleaf,
+                                       sleaf, ocnt, s));
+                        p->stage_end(s, S_SEGMENT, a);
+                    } else {
+                        LK(launch_trie_pass64(iw, wleaf, is, sleaf, seq16, n, pC + xl_parent[j], sh,
+                                              dmask, ~0ull, (uint32_t*)p->hist.p,
+                                              p->trie_ctas_per_sm * p->sm_count, s, ocnt, stats,
+                                              (uint32_t*)p->thg.p, &p->tp_par));
+                        p->launches += 1;  // hist + scatter
+                        p->stage_end(s, S_SORT, a);
+                    }
                     passkeys += (int64_t)n;  // (capacity: the actual count is on the device)
                     continue;
                 }
+                const bool fl = kk >= 2 && fuse_ok(kk - 1);  // (the last pass fused)
                 int d = 0;
                 while (d < stack_depth && d < kk - 1 && stack_pos[d] == kept[d]) ++d;
-                for (int t = d; t < kk; ++t) {
+                for (int t = d; t < kk - (fl ? 1 : 0); ++t) {
                     const bool leaf = t == kk - 1;
                     const uint64_t* wi = t == 0 ? (const uint64_t*)p->win.p
                                                 : (const uint64_t*)p->trieW.p + (size_t)(t - 1) * n;
@@ -1829,26 +1884,39 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
                     LK(launch_trie_pass64(wi, wo, si, so_, seq16, n, nullptr, bits * (g - 1 - kept[t]),
                                           dmask, ~0ull, (uint32_t*)p->hist.p,
                                           p->trie_ctas_per_sm * p->sm_count, s,
-                                          leaf ? bcnt + (j - pos) : nullptr, stats, (uint32_t*)p->thg.p, &p->tp_par));
+                                          leaf ? ocnt : nullptr, stats, (uint32_t*)p->thg.p, &p->tp_par));
                     p->launches += 1;
                     if (!leaf) stack_pos[t] = kept[t];
                 }
                 stack_depth = kk - 1;
                 passkeys += (int64_t)(kk - d) * (int64_t)n;
+                p->stage_end(s, S_SORT, a);
+                if (fl) {  // the last pass over the stack's top (sorted by kept[0 .. kk-2])
+                    uint64_t pm = 0;
+                    for (int r = 0; r < kk - 1; ++r) pm |= pos_mask(kept[r]);
+                    p->stage_begin(s, &a);
+                    p->launches += 1;
+                    LK(launch_leaf((const uint64_t*)p->trieW.p + (size_t)(kk - 2) * n,
+                                   (const uint8_t*)p->trieS.p + (size_t)(kk - 2) * n * ssz, seq16, n,
+                                   nullptr, pm, kmask, bits * (g - 1 - kept[kk - 1]), dmask, dstride, Dm,
+                                   so, stats, lcw, lcs, lcc, wleaf, sleaf, ocnt, s));
+                    p->stage_end(s, S_SEGMENT, a);
+                }
             }
-            p->stage_end(s, S_SORT, a);
-            {
+            if (!fused_any) {
                 gakco_status ws = wait_buf();
                 if (ws != GAKCO_OK) return ws;
             }
             p->stage_begin(s, &a);
             kms.push_back(0);
             CK(cudaMemcpyAsync(p->kmdev.p, kms.data(), kms.size() * 8, cudaMemcpyHostToDevice, s));
-            const size_t slot0 = (size_t)xl_slot[pos];
+            // the leaves of unfused masks, the overflow of fused ones (most slots empty:
+            // a looping grid)
             LK(launch_segment_rag((const uint64_t*)p->keysA.p, p->keysB.p, seq16, n, nmask, bcnt,
                                   (const uint64_t*)p->kmdev.p, dstride, Dm, so.counts, so, stats, s,
                                   kids ? cW + slot0 * n : nullptr, kids ? cS + slot0 * n * ssz : nullptr,
-                                  kids ? cC + slot0 : nullptr));
+                                  kids ? cC + slot0 : nullptr, /*reset=*/!fused_any,
+                                  fused_any ? (unsigned)(4 * p->sm_count) : 0u));
             p->stage_end(s, S_SEGMENT, a);
         } else if (n > 0 && trie) {
             // mask trie: pass t of a mask is a stable pass by the symbol at its t-th kept

@@ -17,6 +17,8 @@
 //    meet another g-mer: it only adds to the diagonal, which the closed form
 //    C(g,m) n_X (launch_diag_closed_form) already counts. Dropping such elements
 //    keeps every child's groups, triples and counts unchanged.
+#include <algorithm>
+
 #include "internal.cuh"
 
 namespace gk {
@@ -32,10 +34,11 @@ constexpr int RG_THREADS = SEG_THREADS;  // 256
 constexpr int RG_IT = SEG_ITEMS;         // 8
 constexpr int RG_TILE = RG_THREADS * RG_IT;
 
-template <typename S>
+template <typename S, bool LOOP>
 __global__ void __launch_bounds__(RG_THREADS, 4) segment_rag_kernel(
     const uint64_t* __restrict__ w, const S* __restrict__ sq, const uint64_t* __restrict__ km,
-    uint64_t n, const uint32_t* __restrict__ cnt, uint32_t tps, int64_t dstride, int64_t* diag,
+    uint64_t n, const uint32_t* __restrict__ cnt, uint32_t tps, uint32_t nblk, int64_t dstride,
+    int64_t* diag,
     uint32_t* counters, SegmentOut so, unsigned long long* stats, uint64_t* cw, S* cs,
     uint32_t* ccnt) {
     __shared__ uint32_t s_w[16];
@@ -46,7 +49,10 @@ __global__ void __launch_bounds__(RG_THREADS, 4) segment_rag_kernel(
     __shared__ unsigned long long s_gend;
     constexpr uint32_t FULLM = (1u << RG_IT) - 1u;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const uint32_t sgi = blockIdx.x / tps, t = blockIdx.x - sgi * tps;
+    // (a grid smaller than segments x tiles loops: the overflow slots of leaf.cu are
+    // mostly empty)
+    auto body = [&](const uint32_t blk) {
+    const uint32_t sgi = blk / tps, t = blk - sgi * tps;
     const uint64_t seg_lo = (uint64_t)sgi * n;
     const uint64_t seg_end = seg_lo + (cnt ? (uint64_t)cnt[sgi] : n);
     const uint64_t tile0 = seg_lo + (uint64_t)t * RG_TILE;
@@ -309,6 +315,15 @@ __global__ void __launch_bounds__(RG_THREADS, 4) segment_rag_kernel(
             wpos += chunk_heads;
         }
     }
+    };
+    if constexpr (LOOP) {
+        for (uint32_t blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
+            body(blk);
+            __syncthreads();  // (this tile's shared-memory reads done)
+        }
+    } else {
+        body(blockIdx.x);
+    }
 }
 
 }  // namespace
@@ -317,19 +332,23 @@ cudaError_t launch_segment_rag(const uint64_t* w, const void* sq, bool seq16, ui
                                const uint32_t* cnt, const uint64_t* km, int64_t dstride,
                                int64_t* diag, uint32_t* counters, SegmentOut so,
                                unsigned long long* stats, cudaStream_t s, uint64_t* cw,
-                               void* cs, uint32_t* ccnt) {
-    cudaError_t e = cudaMemsetAsync(counters, 0, 2 * sizeof(uint32_t), s);
+                               void* cs, uint32_t* ccnt, bool reset, unsigned max_ctas) {
+    cudaError_t e = reset ? cudaMemsetAsync(counters, 0, 2 * sizeof(uint32_t), s) : cudaSuccess;
     if (e != cudaSuccess || n == 0 || nseg == 0) return e;
     const uint64_t tps = (n + RG_TILE - 1) / RG_TILE;
-    const unsigned grid = (unsigned)(tps * (uint64_t)nseg);
-    if (seq16)
-        segment_rag_kernel<uint16_t><<<grid, RG_THREADS, 0, s>>>(
-            w, (const uint16_t*)sq, km, n, cnt, (uint32_t)tps, dstride, diag, counters, so, stats,
-            cw, (uint16_t*)cs, ccnt);
-    else
-        segment_rag_kernel<uint32_t><<<grid, RG_THREADS, 0, s>>>(
-            w, (const uint32_t*)sq, km, n, cnt, (uint32_t)tps, dstride, diag, counters, so, stats,
-            cw, (uint32_t*)cs, ccnt);
+    const uint32_t nblk = (uint32_t)(tps * (uint64_t)nseg);
+    const unsigned grid = max_ctas ? std::min<unsigned>(nblk, max_ctas) : nblk;
+    auto go = [&](auto kern, auto* sqp, auto* csp) {
+        kern<<<grid, RG_THREADS, 0, s>>>(w, sqp, km, n, cnt, (uint32_t)tps, nblk, dstride, diag,
+                                         counters, so, stats, cw, csp, ccnt);
+    };
+    if (seq16) {
+        if (grid < nblk) go(segment_rag_kernel<uint16_t, true>, (const uint16_t*)sq, (uint16_t*)cs);
+        else go(segment_rag_kernel<uint16_t, false>, (const uint16_t*)sq, (uint16_t*)cs);
+    } else {
+        if (grid < nblk) go(segment_rag_kernel<uint32_t, true>, (const uint32_t*)sq, (uint32_t*)cs);
+        else go(segment_rag_kernel<uint32_t, false>, (const uint32_t*)sq, (uint32_t*)cs);
+    }
     return cudaGetLastError();
 }
 

@@ -50,6 +50,7 @@ GAKCO_OPT_LIGHT_CTAS = 19
 GAKCO_OPT_LIGHT_GRID = 20
 GAKCO_OPT_FAR_BYTES = 21
 GAKCO_OPT_RELABEL_HOST = 22
+GAKCO_OPT_LEAF_FUSE = 23
 
 EXPORTS = ("gakco_create", "gakco_set_shard", "gakco_set_option", "gakco_accumulate",
            "gakco_finalize", "gakco_kernel", "gakco_kernel_k", "gakco_kernel_rect",

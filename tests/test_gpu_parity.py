@@ -205,8 +205,31 @@ def test_xl_compaction_families(gk, oracle_lib):
                                  for _ in range(20)]), 6, 2, 4)]
     for cp, g, k, M in cases:
         ref = oracle_lib.compute(cp, g, k, M)
-        for opts in ({}, {"batch_keys": 70000}, {"light_relabel": 1}, {"xl_compact": 0}):
+        for opts in ({}, {"batch_keys": 70000}, {"light_relabel": 1}, {"xl_compact": 0},
+                     {"leaf_fuse": 0}):
             assert_parity(run(gk, cp, g, k, M, sort=6, **opts), ref)
+
+
+def test_leaf_fused_big_groups(gk, oracle_lib):
+    """Fused last pass + run-length (leaf.cu, GAKCO_OPT_LEAF_FUSE): groups of the pass
+    before larger than a CTA's tile (2048) are split into the overflow slot and taken
+    by the segment kernel -- periodic sequences make groups of ~10^4 g-mers next to
+    small random ones, in the trie and the compacted chain, several batches per
+    level; == the unfused path == oracle."""
+    rng = np.random.default_rng(44)
+    seqs = [[0, 1, 2] * 900 for _ in range(4)] + [[1, 2, 0, 3] * 600 for _ in range(3)]
+    seqs += [list(rng.integers(0, 4, int(rng.integers(200, 1500)))) for _ in range(40)]
+    cp = sc.from_sequences(4, seqs)
+    for g, k, M in [(7, 3, 4), (8, 4, 3)]:
+        ref = oracle_lib.compute(cp, g, k, M)
+        r = run(gk, cp, g, k, M, sort=6)
+        assert_parity(r, ref)
+        assert_parity(run(gk, cp, g, k, M, sort=6, batch_keys=90000), ref)
+        assert_parity(run(gk, cp, g, k, M, sort=6, light_relabel=1), ref)
+        r0 = run(gk, cp, g, k, M, sort=6, leaf_fuse=0)
+        assert_parity(r0, ref)
+        assert r["stats"]["triples"] == r0["stats"]["triples"]
+        assert r["stats"]["groups_multi"] == r0["stats"]["groups_multi"]
 
 
 def test_far_pair_records(gk, oracle_lib):
