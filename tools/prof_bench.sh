@@ -1,7 +1,7 @@
 #!/bin/bash
-# r02 pass p: the profiles of the bench configuration (Scale): launch list of one step
+# profiles of the bench configuration (Scale): launch list of one step
 # (gpu__time_duration, --clock-control none) and full captures of its top kernels
-O=gpurun_out; T=${1:-r02p}
+O=gpurun_out; T=${1:-r02z}
 mkdir -p $O
 python -c "import __graft_entry__ as g; g.build()" > $O/${T}_build.log 2>&1
 B="python bench.py --steps 1 --warmup 0 --no-e2e --no-cpu-baseline --no-timing"
@@ -11,7 +11,7 @@ N="ncu --set full --clock-control none --import-source on"
 timeout 600 $N -k 'regex:light_kernel' -s 100 -c 1 -o $O/${T}_light -f $B > $O/${T}_l.log 2>&1
 timeout 600 $N -k 'regex:tp_scatter' -s 400 -c 1 -o $O/${T}_tps -f $B > $O/${T}_t.log 2>&1
 timeout 600 $N -k 'regex:tp_hist' -s 400 -c 1 -o $O/${T}_tph -f $B > $O/${T}_th.log 2>&1
-timeout 600 $N -k 'regex:segment_rag' -s 40 -c 1 -o $O/${T}_seg -f $B > $O/${T}_s.log 2>&1
+timeout 600 $N -k 'regex:leaf_kernel' -s 300 -c 1 -o $O/${T}_leaf -f $B > $O/${T}_s.log 2>&1
 timeout 600 $N -k 'regex:far_add' -s 10 -c 1 -o $O/${T}_far -f $B > $O/${T}_f.log 2>&1
 timeout 600 $N -k 'regex:epilogue_kernel' -s 0 -c 1 -o $O/${T}_epi -f $B > $O/${T}_e.log 2>&1
 timeout 600 $N -k 'regex:window_build' -s 60 -c 1 -o $O/${T}_wb -f $B > $O/${T}_w.log 2>&1

@@ -38,7 +38,9 @@ STAGE = {"encode_kernel": "encode", "encode_win_kernel": "encode", "window_kerne
          "tp_hist_kernel": "sort", "tp_scatter_kernel": "sort", "segment_rag_kernel": "segment",
          "far_add_kernel": "far", "far_gate_kernel": "far", "far_reset_kernel": "far", "fill_u32_kernel": "sort", "pack_upper_kernel": "exchange",
          "diag_kernel": "exchange", "epilogue_packed_kernel": "epilogue",
-         "kdiag_rect_kernel": "epilogue"}
+         "kdiag_rect_kernel": "epilogue", "leaf_kernel": "segment", "far_warm_kernel": "far",
+         "far_offsets_kernel": "far", "far_scan_kernel": "far", "cluster_roots_kernel": "light",
+         "relabel_keys_kernel": "light", "relabel_perm_kernel": "light"}
 
 
 def short(name):
