@@ -115,25 +115,43 @@ def report(paths, tag, config, out_dir):
     json.dump(allt, open(tp, "w"), indent=1)
 
 
+_SCALE = {"nsecond": ("us", 1e-3), "usecond": ("us", 1.0), "msecond": ("us", 1e3),
+          "second": ("us", 1e6), "byte": ("MB", 1e-6), "Kbyte": ("MB", 1e-3),
+          "Mbyte": ("MB", 1.0), "Gbyte": ("MB", 1e3), "ns": ("us", 1e-3), "us": ("us", 1.0),
+          "ms": ("us", 1e3), "s": ("us", 1e6)}
+
+
 def _report_one(path, tag, lines, traffic):
+    # values normalised per report (ncu picks a unit per report): times in us, bytes in MB
     raw = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv", "--metrics",
                           ",".join(METRICS)], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(raw)))
     hdr, units = rows[0], rows[1]
     idx = {h: i for i, h in enumerate(hdr)}
+    cols = [m for m in METRICS if m in idx]
+
+    def unit(m):
+        u = units[idx[m]]
+        return _SCALE[u][0] if u in _SCALE else u
+
+    def val(r, m):
+        u = units[idx[m]]
+        try:
+            return f"{float(r[idx[m]]) * _SCALE[u][1]:.6g}" if u in _SCALE else r[idx[m]]
+        except ValueError:
+            return r[idx[m]]
+
     if lines is None:
         lines = [f"# {tag}: ncu --set full --clock-control none captures (per launch; "
                  "cold caches: compare shares and counters, not absolute times)", "",
-                 "| kernel | " + " | ".join(f"{m.split('.')[0]} [{units[idx[m]]}]"
-                                            for m in METRICS if m in idx) + " |",
-                 "|---|" + "---|" * sum(1 for m in METRICS if m in idx)]
+                 "| kernel | " + " | ".join(f"{m.split('.')[0]} [{unit(m)}]" for m in cols) + " |",
+                 "|---|" + "---|" * len(cols)]
     for r in rows[2:]:
         k = short(r[idx["Kernel Name"]])
-        lines.append(f"| {k} | " + " | ".join(r[idx[m]] for m in METRICS if m in idx) + " |")
+        lines.append(f"| {k} | " + " | ".join(val(r, m) for m in cols) + " |")
         try:
-            mult = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
-            rb = float(r[idx["dram__bytes_read.sum"]]) * mult[units[idx["dram__bytes_read.sum"]]]
-            wb = float(r[idx["dram__bytes_write.sum"]]) * mult[units[idx["dram__bytes_write.sum"]]]
+            rb = float(val(r, "dram__bytes_read.sum")) * 1e6
+            wb = float(val(r, "dram__bytes_write.sum")) * 1e6
             traffic.setdefault(STAGE.get(k, k), []).append(rb + wb)
         except (KeyError, ValueError):
             pass
