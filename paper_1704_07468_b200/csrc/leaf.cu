@@ -33,7 +33,8 @@ template <int TH>
 struct Lf {
     static constexpr int WARPS = TH / 32;
     static constexpr int C = TH * LF_IT;  // range capacity (shared memory)
-    static constexpr int T = C / 2;       // tile of group heads per CTA
+    static constexpr int T = C / 4 * 3;   // tile of group heads per CTA (the rest: the
+                                          // last group's tail)
 };
 
 struct LfElem {
