@@ -21,6 +21,7 @@
 // group, then stable chunk ranks placed at the digit offsets); segrag.cu processes
 // the overflow slots afterwards.
 #include "internal.cuh"
+#include "tc_ptx.cuh"
 
 namespace gk {
 
@@ -37,6 +38,13 @@ struct Lf {
                                           // last group's tail)
 };
 
+__device__ __forceinline__ void lf_bulk(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+        ::"r"(smem_u32(dst)), "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
 struct LfElem {
     uint64_t w;
     uint32_t s;
@@ -44,10 +52,11 @@ struct LfElem {
 
 template <typename S, int TH>
 constexpr size_t lf_smem() {
-    // window keys [C + 8] (then the triple staging), ids [C + 8], perm [C] u16 (then
+    // window keys [C + 8] (then the triple staging), ids [C + 24] (the 16-byte aligned
+    // bulk-copy spans need the slack), perm [C] u16 (then
     // the group starts), warp digit counters + match masks, digit starts / counts /
     // offsets, scratch
-    return (size_t)(Lf<TH>::C + 8) * 8 + (size_t)(Lf<TH>::C + 8) * sizeof(S) + (size_t)Lf<TH>::C * 2 +
+    return (size_t)(Lf<TH>::C + 8) * 8 + (size_t)(Lf<TH>::C + 24) * sizeof(S) + (size_t)Lf<TH>::C * 2 +
            2 * Lf<TH>::WARPS * LF_ND * 4 + 3 * LF_ND * 4 + 64 * 4 + 64;
 }
 
@@ -97,8 +106,8 @@ struct LfShared {
 // perm[p] = the source index (from off) of sorted position p; cstart / tcnt: each
 // digit's start and count. Every thread must call it (it synchronises the block).
 template <int TH>
-__device__ __forceinline__ void lf_rank(const LfShared& sh, uint32_t off, uint32_t len, int shift,
-                                        uint32_t dmask) {
+__device__ __forceinline__ void lf_rank(const LfShared& sh, const uint64_t* keys, uint32_t off,
+                                        uint32_t len, int shift, uint32_t dmask) {
     constexpr int W = Lf<TH>::WARPS;
     const int tid = threadIdx.x, lane = tid & 31, wp = tid >> 5;
     uint32_t* whist = sh.whist + wp * LF_ND;
@@ -109,7 +118,7 @@ __device__ __forceinline__ void lf_rank(const LfShared& sh, uint32_t off, uint32
     for (int i = 0; i < LF_IT; ++i) {
         const uint32_t idx = (uint32_t)(wp * LF_IT * 32 + i * 32 + lane);
         const bool valid = idx < len;
-        const uint32_t d = valid ? (uint32_t)(sh.sw[off + idx] >> shift) & dmask : 0u;
+        const uint32_t d = valid ? (uint32_t)(keys[off + idx] >> shift) & dmask : 0u;
         dg[i / 4] = (i & 3) ? (dg[i / 4] | d << (8 * (i & 3))) : d;
         if (valid) atomicOr(&mbin[d], 1u << lane);
         __syncwarp();
@@ -182,7 +191,7 @@ __global__ void __launch_bounds__(TH, 1024 / TH) leaf_kernel(
     LfShared sh;
     sh.sw = (uint64_t*)smem;
     S* const ss = (S*)(smem + (size_t)(C + 8) * 8);
-    sh.perm = (uint16_t*)(smem + (size_t)(C + 8) * 8 + (size_t)(C + 8) * sizeof(S));
+    sh.perm = (uint16_t*)(smem + (size_t)(C + 8) * 8 + (size_t)(C + 24) * sizeof(S));
     sh.whist = (uint32_t*)(sh.perm + C);
     sh.match = sh.whist + W * LF_ND;
     sh.cstart = sh.match + W * LF_ND;
@@ -190,6 +199,7 @@ __global__ void __launch_bounds__(TH, 1024 / TH) leaf_kernel(
     sh.aux = sh.tcnt + LF_ND;
     sh.s_w = sh.aux + LF_ND;
     __shared__ uint32_t s_first, s_last, s_next;
+    __shared__ __align__(8) uint64_t s_bar;
     __shared__ unsigned long long s_end;
     __shared__ uint32_t s_wmin[W], s_base_t, s_base_g, s_base_c, s_obase;
 
@@ -207,58 +217,57 @@ __global__ void __launch_bounds__(TH, 1024 / TH) leaf_kernel(
         s_next = 0xffffffffu;
         s_end = ~0ull;
     }
-    // 1. the tile and the element before it into shared memory (local index l =
-    //    global - t0 + 1), its group heads: the first (start of the owned range) and
-    //    the last
-    for (uint32_t l = tid; l <= tl; l += TH) {
-        if (l == 0 && t0 == 0) continue;
-        const uint64_t gi = t0 + l - 1;
-        sh.sw[l] = w[gi];
-        ss[l] = sq[gi];
+    // 1. the window [t0 - 1, t0 + C) of the input (local index l = global - t0 + 1) into
+    //    shared memory by two bulk copies (16-byte aligned spans; SW / SS address it by
+    //    local index)
+    const uint64_t wend = min(t0 + C, cnt);
+    const uint32_t wl = (uint32_t)(wend - t0);  // window elements after t0 - 1
+    const uint64_t gb = t0 ? t0 - 1 : 0;        // first element copied
+    const uint32_t lgb = t0 ? 0u : 1u;          // its local index
+    const uintptr_t aw0 = (uintptr_t)(w + gb) & ~(uintptr_t)15, aw1 = ((uintptr_t)(w + wend) + 15) & ~(uintptr_t)15;
+    const uintptr_t as0 = (uintptr_t)(sq + gb) & ~(uintptr_t)15, as1 = ((uintptr_t)(sq + wend) + 15) & ~(uintptr_t)15;
+    const uint64_t* SW = sh.sw + (int)(((uintptr_t)(w + gb) - aw0) / 8) - (int)lgb;
+    const S* SS = ss + (int)(((uintptr_t)(sq + gb) - as0) / sizeof(S)) - (int)lgb;
+    if (tid == 0) {
+        mbar_init(&s_bar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        mbar_expect_tx(&s_bar, (uint32_t)(aw1 - aw0) + (uint32_t)(as1 - as0));
+        lf_bulk(sh.sw, (const void*)aw0, (uint32_t)(aw1 - aw0), &s_bar);
+        lf_bulk(ss, (const void*)as0, (uint32_t)(as1 - as0), &s_bar);
     }
-    __syncthreads();
+    __syncthreads();  // (the barrier initialised)
+    mbar_wait(&s_bar, 0);
+    // 2. group heads: the first and the last in the tile (the owned range starts at the
+    //    first), the first after the tile (the owned range ends there)
     {
-        uint32_t fmin = 0xffffffffu, lmax = 0u;
-        for (uint32_t l = 1 + tid; l <= tl; l += TH) {
-            const bool h = (l == 1 && t0 == 0) || ((sh.sw[l] ^ sh.sw[l - 1]) & pmask) != 0;
+        const uint32_t lt1 = (uint32_t)(t1 - t0) + 1;
+        uint32_t fmin = 0xffffffffu, lmax = 0u, nmin = 0xffffffffu;
+        for (uint32_t l = 1 + tid; l <= wl; l += TH) {
+            const bool h = (l == 1 && t0 == 0) || ((SW[l] ^ SW[l - 1]) & pmask) != 0;
             if (h) {
-                fmin = min(fmin, l);
-                lmax = max(lmax, l);
+                if (l < lt1) {
+                    fmin = min(fmin, l);
+                    lmax = max(lmax, l);
+                } else {
+                    nmin = min(nmin, l);
+                }
             }
         }
         fmin = __reduce_min_sync(0xffffffffu, fmin);
         lmax = __reduce_max_sync(0xffffffffu, lmax);
-        if (lane == 0 && fmin != 0xffffffffu) {
-            atomicMin(&s_first, fmin);
-            atomicMax(&s_last, lmax);
+        nmin = __reduce_min_sync(0xffffffffu, nmin);
+        if (lane == 0) {
+            if (fmin != 0xffffffffu) {
+                atomicMin(&s_first, fmin);
+                atomicMax(&s_last, lmax);
+            }
+            if (nmin != 0xffffffffu) atomicMin(&s_next, nmin);
         }
     }
     __syncthreads();
     const uint32_t a0l = s_first;
     if (a0l == 0xffffffffu) return;  // no group starts here (block-uniform)
     const uint32_t hll = s_last;
-    // 2. the rest of the last owned group: elements after the tile, loaded into the
-    //    window while looking for the next head (a round: one 32-element chunk per
-    //    warp); past the window capacity the group is big (split below)
-    uint32_t wl = tl;  // window elements after t0 - 1
-    for (uint64_t e0 = t1; e0 < cnt && e0 - t0 < (uint64_t)C; e0 += TH) {  // (block-uniform)
-        const uint64_t i = e0 + tid;
-        const uint32_t l = (uint32_t)(i - t0) + 1;
-        bool h = false;
-        if (i < cnt && l <= (uint32_t)C) {
-            const uint64_t k = w[i];
-            sh.sw[l] = k;
-            ss[l] = sq[i];
-            h = ((k ^ w[i - 1]) & pmask) != 0;
-        }
-        const uint32_t hm = __reduce_min_sync(0xffffffffu, h ? l : 0xffffffffu);
-        if (lane == 0 && hm != 0xffffffffu) atomicMin(&s_next, hm);
-        __syncthreads();
-        wl = (uint32_t)min(min(e0 + TH, cnt) - t0, (uint64_t)C);
-        const bool found = s_next != 0xffffffffu;
-        __syncthreads();  // (every thread has read s_next before the next round's atomics)
-        if (found) break;
-    }
     // the owned range ends at the next head, or at the array end; with neither within
     // the window capacity, the last group runs past it (big)
     const bool big = s_next == 0xffffffffu && t0 + wl < cnt;
@@ -266,16 +275,15 @@ __global__ void __launch_bounds__(TH, 1024 / TH) leaf_kernel(
     const uint32_t m = big ? hll : el;
     const uint32_t len = m - a0l;
     GK_CHECK(len <= (uint32_t)C);
-    const uint64_t wend = t0 + wl;
 
     // 3. the range of whole groups: ranked by digit x, then the segment logic
     if (len > 0) {  // (block-uniform)
-        lf_rank<TH>(sh, a0l, len, shift, dmask);
+        lf_rank<TH>(sh, SW, a0l, len, shift, dmask);
         // thread tid owns sorted positions [tid * IT, tid * IT + IT)
         const uint32_t lbase = (uint32_t)tid * LF_IT;
         auto elem = [&](uint32_t p) -> LfElem {
             const uint32_t l = a0l + sh.perm[p];
-            return LfElem{sh.sw[l], (uint32_t)ss[l]};
+            return LfElem{SW[l], (uint32_t)SS[l]};
         };
         auto geq = [&](const LfElem& x, const LfElem& y) { return ((x.w ^ y.w) & kmask) == 0; };
         LfElem cur[LF_IT];
@@ -444,7 +452,7 @@ __global__ void __launch_bounds__(TH, 1024 / TH) leaf_kernel(
                 ss[l] = sq[c0 + l];
             }
             __syncthreads();
-            lf_rank<TH>(sh, 0, cl, shift, dmask);
+            lf_rank<TH>(sh, sh.sw, 0, cl, shift, dmask);
             for (uint32_t p = tid; p < cl; p += TH) {
                 const uint32_t l = sh.perm[p];
                 const uint64_t k = sh.sw[l];
