@@ -123,6 +123,8 @@ struct gakco_plan {
     static constexpr int FAR_RING = 8, FAR_LAG = 6, FAR_EVERY = 12;
     uint32_t* far_seen = nullptr;     // pinned copies of the record count, a ring
     cudaEvent_t ev_far[FAR_RING] = {};  // (the gate reads the copy of FAR_LAG batches ago)
+    // (pipelined: records double-buffered, applies on the third stream)
+    cudaEvent_t ev_fsrc = nullptr, ev_fapply[2] = {nullptr, nullptr};
     int64_t far_near = -1;     // far-pair records from this label distance: -1 auto (256
                                // with a relabelled accumulator), 0 off
     int pipeline = 1;          // light / dense / Gram of batch b on an aux stream, overlapping
@@ -508,6 +510,8 @@ extern "C" void gakco_destroy(gakco_plan* p) {
                           p->ev_join2, p->ev_build, p->ev_gram[0], p->ev_gram[1]})
         if (e) cudaEventDestroy(e);
     if (p->far_seen) cudaFreeHost(p->far_seen);
+    for (cudaEvent_t e : {p->ev_fsrc, p->ev_fapply[0], p->ev_fapply[1]})
+        if (e) cudaEventDestroy(e);
     for (cudaEvent_t e : p->ev_far)
         if (e) cudaEventDestroy(e);
     if (p->aux) cudaStreamDestroy(p->aux);
@@ -1344,6 +1348,12 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
     // far-pair records: with a relabelled accumulator far beyond L2, a
     // light pair whose labels are >= near apart is recorded and added block by block
     FarRec far{nullptr, nullptr, 0, 0};
+    // pipelined: two record buffers; a due apply runs on s3 over the full one while the
+    // light kernels on s2 append to the other (atomic adds into the accumulator commute)
+    FarRec farb[2] = {far, far};
+    int fcur = 0;
+    bool fapplied[2] = {false, false};
+    const bool far2 = pipe;
     int far_bshift = 0;
     uint32_t far_thresh = 0;
     int64_t far_batch = 0, far_last_apply = -4, far_seen_at = -4;  // (the gate's batch clock)
@@ -1355,7 +1365,7 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
         // 4-byte records when every cell index fits 28 bits (Scale: 2e8 cells)
         const bool k32 = p->far_bytes == 4 || (p->far_bytes == 0 && ntri < (1ull << 28));
         if (k32 && ntri >= (1ull << 28)) return p->fail(GAKCO_E_ARG, "4-byte far records need < 2^28 cells");
-        const size_t have = std::min(p->farrec.cap, p->farscr.cap) / (k32 ? 4 : 8);
+        const size_t have = std::min(p->farrec.cap / (far2 ? 2 : 1), p->farscr.cap) / (k32 ? 4 : 8);
         // (buffers already at the 2^30-record maximum: no free-memory query)
         uint64_t cap = 1ull << 30;
         if (have < cap) {
@@ -1366,7 +1376,7 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
         }
         cap = cap / FAR_CHUNK * FAR_CHUNK;
         far_thresh = (uint32_t)(cap / 2);
-        CK(p->ensure(p->farrec, cap * (k32 ? 4 : 8), s));
+        CK(p->ensure(p->farrec, cap * (k32 ? 4 : 8) * (far2 ? 2 : 1), s));
         CK(p->ensure(p->farscr, cap * (k32 ? 4 : 8), s));
         // farbins: [0..255] the fill counter (at 192), then 2 x SMs x 64 chunk histograms,
         // bucket offsets [65] and a sink word
@@ -1374,6 +1384,8 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
         if (!p->far_seen) {
             CK(cudaMallocHost(&p->far_seen, gakco_plan::FAR_RING * sizeof(uint32_t)));
             for (auto& e : p->ev_far) CK(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            for (cudaEvent_t* e : {&p->ev_fsrc, &p->ev_fapply[0], &p->ev_fapply[1]})
+                CK(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
         }
         for (int q = 0; q < gakco_plan::FAR_RING; ++q) p->far_seen[q] = 0;
         CK(cudaMemsetAsync(p->farbins.p, 0, 256 * 4, s));
@@ -1382,6 +1394,11 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
         far_bshift = std::max(16, lb - 6);  // <= 64 accumulator blocks
         far = FarRec{(uint64_t*)p->farrec.p, (uint32_t*)p->farbins.p + 192, cap,
                      (uint32_t)(p->far_near > 0 ? p->far_near : 256), k32};
+        farb[0] = far;
+        farb[1] = far;
+        // (the second buffer's fill counter at 196, its overflow count at 197)
+        farb[1].rec = (uint64_t*)((uint8_t*)p->farrec.p + cap * (k32 ? 4 : 8));
+        farb[1].fill = (uint32_t*)p->farbins.p + 196;
     }
     if (relabel) {
         CK(p->ensure(p->perm, N * 4, s));
@@ -1487,9 +1504,13 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
         HT("lflush");
         cudaEvent_t al = nullptr;
         if (perm_active && far.near) {  // every pending far record first
+            if (far2) {  // (the applies in flight on s3 done)
+                CK(cudaEventRecord(p->ev_join2, s3));
+                CK(cudaStreamWaitEvent(s2, p->ev_join2, 0));
+            }
             p->stage_begin(s2, &al);
             p->launches += 4 + 2 * 16;
-            LK(launch_far_apply(far, p->farscr.p, (uint32_t*)p->farbins.p + 256,
+            LK(launch_far_apply(farb[fcur], p->farscr.p, (uint32_t*)p->farbins.p + 256,
                                 far_bshift, (uint32_t*)p->lightacc.p, ntri, p->sm_count, s2));
             p->stage_end(s2, S_FAR, al);
             far_last_apply = far_batch;  // (copies older than this are stale)
@@ -2091,7 +2112,7 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
                             perm_active ? (const uint32_t*)p->perm.p : nullptr,
                             fp4_lv[m] ? 4u : 255u, stats, p->sm_count, s2,
                             perm_active && win_on ? wa : WinArgs{nullptr, nullptr, 0, 0, 0},
-                            n >= (2ull << 20), perm_active ? far : FarRec{nullptr, nullptr, 0, 0},
+                            n >= (2ull << 20), perm_active ? farb[fcur] : FarRec{nullptr, nullptr, 0, 0},
                             p->light_ctas,
                             // (relabelled: a 3-CTA/SM grid leaves room for the next batch's
                             // passes on s: Scale 171-177 -> 166-167 ms; else 8 per SM)
@@ -2120,15 +2141,26 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
                 due = due || fb - std::max(far_last_apply, far_seen_at) >= gakco_plan::FAR_EVERY;
                 {
                     if (due) {
-                        p->stage_begin(s2, &a);
+                        cudaStream_t sf = far2 ? s3 : s2;
+                        if (far2) {  // (this batch's records written)
+                            CK(cudaEventRecord(p->ev_fsrc, s2));
+                            CK(cudaStreamWaitEvent(s3, p->ev_fsrc, 0));
+                        }
+                        p->stage_begin(sf, &a);
                         p->launches += 4 + 2 * 16;
-                        LK(launch_far_apply(far, p->farscr.p, (uint32_t*)p->farbins.p + 256,
-                                            far_bshift, (uint32_t*)p->lightacc.p, ntri, p->sm_count, s2));
-                        p->stage_end(s2, S_FAR, a);
+                        LK(launch_far_apply(farb[fcur], p->farscr.p, (uint32_t*)p->farbins.p + 256,
+                                            far_bshift, (uint32_t*)p->lightacc.p, ntri, p->sm_count, sf));
+                        p->stage_end(sf, S_FAR, a);
+                        if (far2) {  // the other buffer next, once its own last apply is done
+                            CK(cudaEventRecord(p->ev_fapply[fcur], s3));
+                            fapplied[fcur] = true;
+                            fcur ^= 1;
+                            if (fapplied[fcur]) CK(cudaStreamWaitEvent(s2, p->ev_fapply[fcur], 0));
+                        }
                         far_last_apply = fb;
                     }
                 }
-                CK(cudaMemcpyAsync(p->far_seen + (fb % RING), far.fill, 4, cudaMemcpyDeviceToHost, s2));
+                CK(cudaMemcpyAsync(p->far_seen + (fb % RING), farb[fcur].fill, 4, cudaMemcpyDeviceToHost, s2));
                 CK(cudaEventRecord(p->ev_far[fb % RING], s2));
             }
             if (perm_active && win_on) {  // this batch's window columns (+ the Gram every few)
@@ -2453,12 +2485,12 @@ extern "C" gakco_status gakco_get_stats(gakco_plan* p, gakco_stats* out) {
         r.pass_keys = (int64_t)d[ST_PASS_KEYS];
     }
     if (p->farbins.p) {  // far-record chunk claims refused (buffer full: those warps used REDs)
-        uint32_t ov = 0;
-        cudaError_t e = cudaMemcpyAsync(&ov, (uint32_t*)p->farbins.p + 193, 4, cudaMemcpyDeviceToHost,
+        uint32_t ov[5] = {0, 0, 0, 0, 0};  // (words 193 and 197: the two buffers' counts)
+        cudaError_t e = cudaMemcpyAsync(ov, (uint32_t*)p->farbins.p + 193, 20, cudaMemcpyDeviceToHost,
                                         p->last_stream);
         if (e == cudaSuccess) e = cudaStreamSynchronize(p->last_stream);
         if (e != cudaSuccess) return p->cuda_fail(e, "stats");
-        r.far_overflow = ov;
+        r.far_overflow = (int64_t)ov[0] + ov[4];
     }
     double* ms[S_NSTAGE] = {&r.ms_encode, &r.ms_sort,     &r.ms_segment, &r.ms_light,
                             &r.ms_heavy,  &r.ms_epilogue, &r.ms_dense,   &r.ms_far};
