@@ -113,10 +113,14 @@ __device__ __forceinline__ void lf_rank(const LfShared& sh, const uint64_t* keys
     uint32_t* whist = sh.whist + wp * LF_ND;
     uint32_t* mbin = sh.match + wp * LF_ND;
     const uint32_t lt = lanemask_lt();
-    uint32_t dg[LF_IT / 4], rank[LF_IT / 2];
+    // each warp ranks a block of ipw * 32 consecutive elements (ipw = len / the block
+    // width, rounded up: no warp idles through predicated-off items)
+    const uint32_t ipw = (len + W * 32 - 1) / (W * 32);
+    uint32_t dg[LF_IT / 4] = {0, 0}, rank[LF_IT / 2] = {0, 0, 0, 0};
 #pragma unroll
     for (int i = 0; i < LF_IT; ++i) {
-        const uint32_t idx = (uint32_t)(wp * LF_IT * 32 + i * 32 + lane);
+        if ((uint32_t)i >= ipw) break;  // (warp-uniform)
+        const uint32_t idx = (uint32_t)(wp * ipw * 32 + i * 32 + lane);
         const bool valid = idx < len;
         const uint32_t d = valid ? (uint32_t)(keys[off + idx] >> shift) & dmask : 0u;
         dg[i / 4] = (i & 3) ? (dg[i / 4] | d << (8 * (i & 3))) : d;
@@ -165,7 +169,8 @@ __device__ __forceinline__ void lf_rank(const LfShared& sh, const uint64_t* keys
     __syncthreads();
 #pragma unroll
     for (int i = 0; i < LF_IT; ++i) {
-        const uint32_t idx = (uint32_t)(wp * LF_IT * 32 + i * 32 + lane);
+        if ((uint32_t)i >= ipw) break;
+        const uint32_t idx = (uint32_t)(wp * ipw * 32 + i * 32 + lane);
         if (idx < len) {
             const uint32_t d = (dg[i / 4] >> (8 * (i & 3))) & 0xffu;
             const uint32_t pos = whist[d] + ((rank[i / 2] >> (16 * (i & 1))) & 0xffffu);
@@ -279,8 +284,10 @@ __global__ void __launch_bounds__(TH, 1024 / TH) leaf_kernel(
     // 3. the range of whole groups: ranked by digit x, then the segment logic
     if (len > 0) {  // (block-uniform)
         lf_rank<TH>(sh, SW, a0l, len, shift, dmask);
-        // thread tid owns sorted positions [tid * IT, tid * IT + IT)
-        const uint32_t lbase = (uint32_t)tid * LF_IT;
+        // thread tid owns sorted positions [tid * ipt, tid * ipt + ipt), ipt = len / TH
+        // rounded up (<= IT): every thread has items
+        const uint32_t ipt = (len + TH - 1) / TH;
+        const uint32_t lbase = (uint32_t)tid * ipt;
         auto elem = [&](uint32_t p) -> LfElem {
             const uint32_t l = a0l + sh.perm[p];
             return LfElem{SW[l], (uint32_t)SS[l]};
@@ -292,6 +299,8 @@ __global__ void __launch_bounds__(TH, 1024 / TH) leaf_kernel(
             LfElem prev = (lbase > 0 && lbase < len) ? elem(lbase - 1) : LfElem{0ull, 0u};
 #pragma unroll
             for (int i = 0; i < LF_IT; ++i) {
+                cur[i] = LfElem{0ull, 0u};
+                if ((uint32_t)i >= ipt) continue;  // (block-uniform)
                 const uint32_t p = lbase + i;
                 cur[i] = p < len ? elem(p) : LfElem{0ull, 0u};
                 if (p < len) {
