@@ -352,6 +352,15 @@ gakco_status gakco_finalize_packed_sum(gakco_plan* plan, const void* Cp, int in_
  * finalize. Synchronises the plan's last stream. */
 gakco_status gakco_get_stats(gakco_plan* plan, gakco_stats* out);
 
+/* With GAKCO_OPT_TIMING: the stage events of the last accumulate / finalize as a
+ * timeline (also with the pipeline on, where the stages of different streams
+ * overlap): entry i is stage[i] (0 encode, 1 sort, 2 segment, 3 light, 4 heavy,
+ * 5 epilogue, 6 dense, 7 far; the order of gakco_stats' ms_* fields) from t0[i] to
+ * t1[i] ms after the first event. Host arrays of cap entries; *count = the number of
+ * events (entries beyond cap are not written). Synchronises the plan's last stream. */
+gakco_status gakco_stage_timeline(gakco_plan* plan, int32_t* stage, float* t0, float* t1,
+                                  int64_t cap, int64_t* count);
+
 /* Number of masks c_gk = sum_{m<=M} C(g,m) (Table 1) and of this shard. */
 int64_t gakco_num_masks(const gakco_plan* plan, int shard_only);
 

@@ -2504,6 +2504,26 @@ extern "C" gakco_status gakco_get_stats(gakco_plan* p, gakco_stats* out) {
     return GAKCO_OK;
 }
 
+extern "C" gakco_status gakco_stage_timeline(gakco_plan* p, int32_t* stage, float* t0, float* t1,
+                                             int64_t cap, int64_t* count) {
+    if (!p || !count || (cap > 0 && (!stage || !t0 || !t1))) return GAKCO_E_ARG;
+    DeviceGuard dg(p->device);
+    *count = (int64_t)p->evs.size();
+    if (p->evs.empty()) return GAKCO_OK;
+    const cudaEvent_t ref = p->evs.front().second.first;
+    for (size_t i = 0; i < p->evs.size() && (int64_t)i < cap; ++i) {
+        const auto& se = p->evs[i];
+        cudaEventSynchronize(se.second.second);
+        float a = 0, b = 0;
+        cudaEventElapsedTime(&a, ref, se.second.first);
+        cudaEventElapsedTime(&b, ref, se.second.second);
+        stage[i] = se.first;
+        t0[i] = a;
+        t1[i] = b;
+    }
+    return GAKCO_OK;
+}
+
 // ---------------------------------------------------------------------------
 // Mask-sharded multi-GPU step (include/gakco.h)
 extern "C" gakco_status gakco_stream_wait_level(gakco_plan* p, int m, void* stream) {

@@ -57,7 +57,7 @@ EXPORTS = ("gakco_create", "gakco_set_shard", "gakco_set_option", "gakco_accumul
            "gakco_get_stats", "gakco_stream_wait_level", "gakco_level_order", "gakco_pack_upper",
            "gakco_diag", "gakco_finalize_packed", "gakco_finalize_packed_sum", "gakco_ipc_alloc",
            "gakco_ipc_free", "gakco_ipc_handle", "gakco_ipc_open", "gakco_ipc_close",
-           "gakco_pack_upper_peers",
+           "gakco_pack_upper_peers", "gakco_stage_timeline",
            "gakco_num_masks", "gakco_last_error", "gakco_status_string", "gakco_destroy")
 
 
@@ -104,6 +104,7 @@ def lib():
         L.gakco_kernel_k.argtypes = [P, P, P, i64, P, P, P]
         L.gakco_kernel_rect.argtypes = [P, P, P, i64, i64, P, P, P, P, P, P]
         L.gakco_get_stats.argtypes = [P, ctypes.POINTER(gakco_stats)]
+        L.gakco_stage_timeline.argtypes = [P, P, P, P, i64, ctypes.POINTER(i64)]
         L.gakco_stream_wait_level.argtypes = [P, ci, P]
         L.gakco_level_order.argtypes = [P, ctypes.POINTER(ci), ci]
         L.gakco_level_order.restype = ci
@@ -130,7 +131,7 @@ def lib():
                   "gakco_get_stats", "gakco_stream_wait_level", "gakco_pack_upper",
                   "gakco_diag", "gakco_finalize_packed", "gakco_finalize_packed_sum",
                   "gakco_ipc_alloc", "gakco_ipc_free", "gakco_ipc_handle", "gakco_ipc_open",
-                  "gakco_ipc_close", "gakco_pack_upper_peers"):
+                  "gakco_ipc_close", "gakco_pack_upper_peers", "gakco_stage_timeline"):
             getattr(L, f).restype = ci
         _lib = L
     return _lib
@@ -211,6 +212,16 @@ def gakco_get_stats(plan):
     s = gakco_stats()
     _check(plan, lib().gakco_get_stats(plan, ctypes.byref(s)))
     return s.as_dict()
+
+
+def gakco_stage_timeline(plan, cap=100000):
+    """(stage, t0 ms, t1 ms) per stage event of the last call (GAKCO_OPT_TIMING)."""
+    st = (ctypes.c_int32 * cap)()
+    a = (ctypes.c_float * cap)()
+    b = (ctypes.c_float * cap)()
+    n = ctypes.c_int64(0)
+    _check(plan, lib().gakco_stage_timeline(plan, st, a, b, cap, ctypes.byref(n)))
+    return [(st[i], a[i], b[i]) for i in range(min(n.value, cap))]
 
 
 def gakco_stream_wait_level(plan, m, stream=None):
@@ -323,6 +334,9 @@ class Plan:
 
     def stats(self):
         return gakco_get_stats(self.h)
+
+    def stage_timeline(self):
+        return gakco_stage_timeline(self.h)
 
     def stream_wait_level(self, m, stream=None):
         gakco_stream_wait_level(self.h, m, stream)
