@@ -91,6 +91,37 @@ __device__ __forceinline__ uint32_t lf_scan(uint32_t v, uint32_t* s_w, uint32_t*
     return r;
 }
 
+// the same over 64-bit values; s_w: 2 (WARPS + 1) words
+template <int TH>
+__device__ __forceinline__ uint64_t lf_scan64(uint64_t v, unsigned long long* s_w, uint64_t* total) {
+    constexpr int W = Lf<TH>::WARPS;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    uint64_t inc = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const uint64_t t = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += t;
+    }
+    if (lane == 31) s_w[w] = inc;
+    __syncthreads();
+    if (w == 0) {
+        const uint64_t x = lane < W ? s_w[lane] : 0ull;
+        uint64_t y = x;
+#pragma unroll
+        for (int o = 1; o < W; o <<= 1) {
+            const uint64_t t = __shfl_up_sync(0xffffffffu, y, o);
+            if (lane >= o) y += t;
+        }
+        if (lane < W) s_w[lane] = y - x;
+        if (lane == W - 1) s_w[W] = y;
+    }
+    __syncthreads();
+    const uint64_t r = s_w[w] + inc - v;
+    *total = s_w[W];
+    __syncthreads();
+    return r;
+}
+
 struct LfShared {
     uint64_t* sw;         // [C + 8] window keys
     uint16_t* perm;       // [C] source index (from the range start) by sorted position
@@ -364,11 +395,14 @@ __global__ void __launch_bounds__(TH, 1024 / TH) leaf_kernel(
         const uint32_t emit_g = emit_t & gh_bits;
         uint32_t keep = 0;
         if (cw) keep = valid_bits & (~gh_bits | ~ghn) & 0xffu;
-        uint32_t aggp, agg_k = 0, off_k = 0;
-        const uint32_t offp = lf_scan<TH>(__popc(emit_t) | (__popc(emit_g) << 16), sh.s_w, &aggp);
-        const uint32_t off_t = offp & 0xffffu, off_g = offp >> 16;
-        const uint32_t agg_t = aggp & 0xffffu, agg_g = aggp >> 16;
-        if (cw) off_k = lf_scan<TH>(__popc(keep), sh.s_w, &agg_k);
+        // one block scan of the three counts (16-bit fields: each total <= C = 4 * 256)
+        uint64_t aggp;
+        const uint64_t offp = lf_scan64<TH>((uint64_t)__popc(emit_t) | (uint64_t)__popc(emit_g) << 16 |
+                                                (uint64_t)__popc(keep) << 32,
+                                            (unsigned long long*)sh.s_w, &aggp);
+        const uint32_t off_t = (uint32_t)offp & 0xffffu, off_g = (uint32_t)(offp >> 16) & 0xffffu;
+        const uint32_t agg_t = (uint32_t)aggp & 0xffffu, agg_g = (uint32_t)(aggp >> 16) & 0xffffu;
+        const uint32_t off_k = (uint32_t)(offp >> 32), agg_k = (uint32_t)(aggp >> 32);
         if (tid == 0) {
             s_base_t = agg_t ? atomicAdd(&counters[0], agg_t) : 0u;
             s_base_g = agg_g ? atomicAdd(&counters[1], agg_g) : 0u;
