@@ -136,8 +136,9 @@ typedef enum {
                                      last pass is fused with its run-length (leaf.cu: each CTA
                                      ranks whole groups of the pass before in shared memory;
                                      no leaf array), where the groups of the pass before are
-                                     small (expected <= 512 g-mers); 0 = a global pass + the
-                                     segment kernel */
+                                     small (the expected largest, n f_max^positions, <= 8
+                                     tiles of 768 g-mers); 0 = a global pass + the segment
+                                     kernel */
     GAKCO_OPT_FAR_BYTES = 21,     /* far-pair record width: 0 = automatic (4 bytes -- cell << 4 |
                                      value, values 1..15, larger ones as REDs -- when every cell
                                      index fits 28 bits, else 8), 4, 8 */

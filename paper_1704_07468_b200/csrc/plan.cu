@@ -1830,12 +1830,16 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
             // fused leaves (leaf.cu): a mask's last pass and its run-length in one kernel
             // over whole groups of the pass before -- where those groups are small: the
             // expected LARGEST one, n f_max^positions (f_max: the most frequent symbol's
-            // share; independent symbols), at most half a tile (Text's level-5 leaves:
-            // 6e6 x 0.24^4 = 2e4 -> unfused; Scale: 41 -> fused). A larger group is
-            // split by its owner CTA into the mask's overflow slot, which the segment
-            // kernel takes afterwards.
+            // share; independent symbols), at most 8 tiles (Text's level-5 leaves:
+            // 6e6 x 0.24^4 = 2e4 -> unfused, its chain levels from 5 positions (4.8e3)
+            // fused; Scale: 41 -> fused). A group past the window is split by its owner
+            // CTA into the mask's overflow slot, which the segment kernel takes afterwards.
             auto fuse_ok = [&](int npos) {
-                return p->leaf_fuse && npos >= 1 && lf_big_expect(npos) <= (double)leaf_tile() / 2;
+                // (the bound, in tiles: Text 0.5 -> 84.5 ms, 1.5 -> 83.6, 8 -> 79.5, 16 ->
+                // 79.5, >= 30 -> 92.3: its level-5 leaves, largest groups ~2e4, serialise
+                // on their owner CTAs; Scale's expected 41 fuses under any bound)
+                constexpr double kBigTiles = 8.0;
+                return p->leaf_fuse && npos >= 1 && lf_big_expect(npos) <= (double)leaf_tile() * kBigTiles;
             };
             auto pos_mask = [&](int x) { return (uint64_t)dmask << (bits * (g - 1 - x)); };
             const size_t slot0 = (size_t)xl_slot[pos];
