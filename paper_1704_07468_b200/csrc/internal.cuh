@@ -290,12 +290,33 @@ cudaError_t launch_segment_rag(const uint64_t* w, const void* sq, bool seq16, ui
 // by pmask, fused with the run-length of segrag.cu (kmask: the mask's key). Appends to
 // so (counters = so.counts, not reset); cw/cs/ccnt: the compacted copy (optional);
 // groups larger than the tile are split into ow/os at atomicAdd(ocnt) (for segrag)
+// a group of the pass before too large for a leaf CTA, queued for leaf_big_kernel
+struct LfBig {
+    const uint64_t* w;  // the input array (grouped by pmask) and its ids
+    const void* sq;
+    uint64_t* ow;       // the mask's overflow slot, its fill
+    void* os;
+    uint32_t* ocnt;
+    uint64_t start;     // the group's first element; the array's element count
+    uint64_t cnt;
+    uint64_t pmask;
+    int shift;
+    uint32_t dmask;
+};
+struct LfBigList {
+    LfBig* e;
+    uint32_t* count;  // [0] entries queued, [1] entries claimed (both zeroed per batch)
+    uint32_t cap;
+};
 int leaf_tile();  // group heads per CTA of launch_leaf
+// the queued large groups of a batch, split into their overflow slots (after the
+// batch's launch_leaf calls, before the segment kernel over the overflow slots)
+cudaError_t launch_leaf_big(LfBigList bl, bool seq16, int sm_count, cudaStream_t s);
 cudaError_t launch_leaf(const uint64_t* w, const void* sq, bool seq16, uint64_t n,
                         const uint32_t* cntp, uint64_t pmask, uint64_t kmask, int shift,
                         uint32_t dmask, int64_t dstride, int64_t* diag, SegmentOut so,
                         unsigned long long* stats, uint64_t* cw, void* cs, uint32_t* ccnt,
-                        uint64_t* ow, void* os, uint32_t* ocnt, cudaStream_t s);
+                        uint64_t* ow, void* os, uint32_t* ocnt, LfBigList bl, cudaStream_t s);
 cudaError_t launch_seq16(const uint32_t* a, uint16_t* b, uint64_t n, int sm_count,
                          cudaStream_t s);
 cudaError_t launch_radix_chunked2(const void* in, void* out, bool k64, uint64_t n, int nseg,

@@ -220,7 +220,7 @@ __global__ void __launch_bounds__(TH, 1024 / TH) leaf_kernel(
     const uint64_t* __restrict__ w, const S* __restrict__ sq, const uint32_t* cntp, uint64_t n,
     uint64_t pmask, uint64_t kmask, int shift, uint32_t dmask, int64_t dstride, int64_t* diag,
     uint32_t* counters, SegmentOut so, unsigned long long* stats, uint64_t* cw, S* cs,
-    uint32_t* ccnt, uint64_t* ow, S* os, uint32_t* ocnt) {
+    uint32_t* ccnt, uint64_t* ow, S* os, uint32_t* ocnt, LfBigList bl) {
     using L = Lf<TH>;
     constexpr int C = L::C, T = L::T, W = L::WARPS;
     extern __shared__ __align__(16) unsigned char smem[];
@@ -450,7 +450,17 @@ __global__ void __launch_bounds__(TH, 1024 / TH) leaf_kernel(
     }
 
     // 4. a group running past the window [hl, e): split by digit x into the overflow slot
-    if (big) {  // (block-uniform)
+    if (big && bl.e) {  // (queued for leaf_big_kernel: one large CTA per group)
+        if (tid == 0) {
+            const uint32_t q = atomicAdd(&bl.count[0], 1u);
+            GK_CHECK(q < bl.cap);
+            if (q < bl.cap)
+                bl.e[q] = LfBig{w, (const void*)sq, ow, (void*)os, ocnt, t0 + hll - 1, cnt, pmask,
+                                shift, dmask};
+        }
+        return;
+    }
+    if (big) {  // (block-uniform; no queue: split here)
         const uint64_t hl = t0 + hll - 1;
         for (uint64_t e0 = wend; e0 < cnt; e0 += TH) {
             const uint64_t i = e0 + tid;
@@ -512,24 +522,126 @@ __global__ void __launch_bounds__(TH, 1024 / TH) leaf_kernel(
     }
 }
 
+// A group of the pass before that runs past a leaf CTA's window: split by the symbol
+// at x into the mask's overflow slot by one 1024-thread CTA per group (queued by
+// leaf_kernel; CTAs claim entries from the list): the group's end, its digit
+// histogram, then 8192-element chunks ranked stably and placed at the digit offsets.
+constexpr int LB_TH = 1024;
+
+template <typename S>
+__global__ void __launch_bounds__(LB_TH, 1) leaf_big_kernel(LfBigList bl) {
+    using L = Lf<LB_TH>;
+    constexpr int C = L::C, W = L::WARPS;
+    extern __shared__ __align__(16) unsigned char smem[];
+    LfShared sh;
+    sh.sw = (uint64_t*)smem;
+    S* const ss = (S*)(smem + (size_t)C * 8);
+    sh.perm = (uint16_t*)(ss + C);
+    sh.whist = (uint32_t*)(sh.perm + C);
+    sh.match = sh.whist + W * LF_ND;
+    sh.cstart = sh.match + W * LF_ND;
+    sh.tcnt = sh.cstart + LF_ND;
+    sh.aux = sh.tcnt + LF_ND;
+    sh.s_w = sh.aux + LF_ND;
+    __shared__ unsigned long long s_end;
+    __shared__ uint32_t s_q, s_obase;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (int i = tid; i < 2 * W * LF_ND; i += LB_TH) sh.whist[i] = 0u;
+    for (;;) {
+        if (tid == 0) {
+            s_q = atomicAdd(&bl.count[1], 1u);
+            s_end = ~0ull;
+        }
+        __syncthreads();
+        const uint32_t q = s_q;
+        if (q >= min(bl.count[0], bl.cap)) return;  // (block-uniform)
+        const LfBig g = bl.e[q];
+        const uint64_t* w = g.w;
+        const S* sq = (const S*)g.sq;
+        // the group's end: the first head after its start
+        for (uint64_t e0 = g.start + 1; e0 < g.cnt; e0 += LB_TH) {
+            const uint64_t i = e0 + tid;
+            if (i < g.cnt && ((w[i] ^ w[i - 1]) & g.pmask) != 0) atomicMin(&s_end, (unsigned long long)i);
+            __syncthreads();
+            const bool found = s_end != ~0ull;
+            __syncthreads();
+            if (found) break;
+        }
+        const uint64_t e = min((uint64_t)s_end, g.cnt), hl = g.start;
+        const uint64_t gs = e - hl;
+        // digit histogram (per-warp counters), exclusive digit offsets
+        for (uint64_t i = hl + tid; i < e; i += LB_TH)
+            atomicAdd(&sh.whist[warp * LF_ND + ((uint32_t)(w[i] >> g.shift) & g.dmask)], 1u);
+        __syncthreads();
+        if (tid < LF_ND) {
+            uint32_t t = 0;
+            for (int ww = 0; ww < W; ++ww) {
+                t += sh.whist[ww * LF_ND + tid];
+                sh.whist[ww * LF_ND + tid] = 0u;
+            }
+            uint32_t inc = t;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t v = __shfl_up_sync(0xffffffffu, inc, o);
+                if (lane >= o) inc += v;
+            }
+            if (tid == 31) sh.s_w[32] = inc;
+            sh.aux[tid] = inc - t;  // (the upper half adds the lower total below)
+        }
+        if (tid == 0) s_obase = atomicAdd(g.ocnt, (uint32_t)gs);
+        __syncthreads();
+        if (tid >= 32 && tid < LF_ND) sh.aux[tid] += sh.s_w[32];
+        __syncthreads();
+        const uint32_t ob = s_obase;
+        uint64_t* ow = g.ow;
+        S* os = (S*)g.os;
+        for (uint64_t c0 = hl; c0 < e; c0 += C) {
+            const uint32_t cl = (uint32_t)min((uint64_t)C, e - c0);
+            for (uint32_t l = tid; l < cl; l += LB_TH) {
+                sh.sw[l] = w[c0 + l];
+                ss[l] = sq[c0 + l];
+            }
+            __syncthreads();
+            lf_rank<LB_TH>(sh, sh.sw, 0, cl, g.shift, g.dmask);
+            for (uint32_t p = tid; p < cl; p += LB_TH) {
+                const uint32_t l = sh.perm[p];
+                const uint64_t k = sh.sw[l];
+                const uint32_t d = (uint32_t)(k >> g.shift) & g.dmask;
+                ow[(uint64_t)ob + sh.aux[d] + (p - sh.cstart[d])] = k;
+                os[(uint64_t)ob + sh.aux[d] + (p - sh.cstart[d])] = ss[l];
+            }
+            __syncthreads();
+            if (tid < LF_ND) sh.aux[tid] += sh.tcnt[tid];
+            __syncthreads();
+        }
+    }
+}
+
+template <typename S>
+constexpr size_t lb_smem() {
+    return (size_t)Lf<LB_TH>::C * (8 + sizeof(S) + 2) + 2 * Lf<LB_TH>::WARPS * LF_ND * 4 + 3 * LF_ND * 4 +
+           64 * 4 + 64;
+}
+
 template <int TH>
 cudaError_t leaf_go(const uint64_t* w, const void* sq, bool seq16, uint64_t n, const uint32_t* cntp,
                     uint64_t pmask, uint64_t kmask, int shift, uint32_t dmask, int64_t dstride,
                     int64_t* diag, SegmentOut so, unsigned long long* stats, uint64_t* cw, void* cs,
-                    uint32_t* ccnt, uint64_t* ow, void* os, uint32_t* ocnt, cudaStream_t s) {
+                    uint32_t* ccnt, uint64_t* ow, void* os, uint32_t* ocnt, LfBigList bl,
+                    cudaStream_t s) {
     const unsigned grid = (unsigned)((n + Lf<TH>::T - 1) / Lf<TH>::T);
     if (seq16) {
         cudaFuncSetAttribute(leaf_kernel<uint16_t, TH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)lf_smem<uint16_t, TH>());
         leaf_kernel<uint16_t, TH><<<grid, TH, lf_smem<uint16_t, TH>(), s>>>(
             w, (const uint16_t*)sq, cntp, n, pmask, kmask, shift, dmask, dstride, diag, so.counts, so,
-            stats, cw, (uint16_t*)cs, ccnt, ow, (uint16_t*)os, ocnt);
+            stats, cw, (uint16_t*)cs, ccnt, ow, (uint16_t*)os, ocnt, bl);
     } else {
         cudaFuncSetAttribute(leaf_kernel<uint32_t, TH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)lf_smem<uint32_t, TH>());
         leaf_kernel<uint32_t, TH><<<grid, TH, lf_smem<uint32_t, TH>(), s>>>(
             w, (const uint32_t*)sq, cntp, n, pmask, kmask, shift, dmask, dstride, diag, so.counts, so,
-            stats, cw, (uint32_t*)cs, ccnt, ow, (uint32_t*)os, ocnt);
+            stats, cw, (uint32_t*)cs, ccnt, ow, (uint32_t*)os, ocnt, bl);
     }
     return cudaGetLastError();
 }
@@ -543,10 +655,23 @@ cudaError_t launch_leaf(const uint64_t* w, const void* sq, bool seq16, uint64_t 
                         const uint32_t* cntp, uint64_t pmask, uint64_t kmask, int shift,
                         uint32_t dmask, int64_t dstride, int64_t* diag, SegmentOut so,
                         unsigned long long* stats, uint64_t* cw, void* cs, uint32_t* ccnt,
-                        uint64_t* ow, void* os, uint32_t* ocnt, cudaStream_t s) {
+                        uint64_t* ow, void* os, uint32_t* ocnt, LfBigList bl, cudaStream_t s) {
     if (n == 0) return cudaGetLastError();
     return leaf_go<LEAF_TH>(w, sq, seq16, n, cntp, pmask, kmask, shift, dmask, dstride, diag, so,
-                                 stats, cw, cs, ccnt, ow, os, ocnt, s);
+                                 stats, cw, cs, ccnt, ow, os, ocnt, bl, s);
+}
+
+cudaError_t launch_leaf_big(LfBigList bl, bool seq16, int sm_count, cudaStream_t s) {
+    if (seq16) {
+        cudaFuncSetAttribute(leaf_big_kernel<uint16_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)lb_smem<uint16_t>());
+        leaf_big_kernel<uint16_t><<<sm_count, LB_TH, lb_smem<uint16_t>(), s>>>(bl);
+    } else {
+        cudaFuncSetAttribute(leaf_big_kernel<uint32_t>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)lb_smem<uint32_t>());
+        leaf_big_kernel<uint32_t><<<sm_count, LB_TH, lb_smem<uint32_t>(), s>>>(bl);
+    }
+    return cudaGetLastError();
 }
 
 }  // namespace gk

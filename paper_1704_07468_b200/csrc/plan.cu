@@ -143,7 +143,7 @@ struct gakco_plan {
 
     DevBuf genW0, genW1, genS0, genS1, kmdev, trieR, trieX0, trieX1, pdesc, wD, wlist, wfill, wC, winv, wtiles, trieS0, trieW, trieS, keptsh, dense2, heavy2, hcount2, tseq2, tcnt2, gstart2, counts2, perm, iota, best, parent, Dgscr, Kdscr, codes, off, gofs, gmseq, keysA, keysB, hist, status, ctr, tseq, tcnt, gstart, gend,
         counts, kept, stats, flags, kdiag, Cscr, Nmscr, Kscr, Knscr, heavy, hcount, dense, tiles, tiles4, symhist,
-        lightacc, binrec, bincnt, farrec, farscr, farbins, xccnt, xbcnt, relkeys, relH, thg, win, bkH, bktot, bkbase, bkdesc, bktab, bktcnt, bkgs, bkocc;
+        lightacc, binrec, bincnt, farrec, farscr, farbins, xccnt, xbcnt, relkeys, relH, thg, lbig, win, bkH, bktot, bkbase, bkdesc, bktab, bktcnt, bkgs, bkocc;
     int64_t tiles_npad = -1;
     int tiles_pair = -1;
     int64_t tiles_na = -1;
@@ -497,7 +497,7 @@ extern "C" void gakco_destroy(gakco_plan* p) {
                       &p->hist,  &p->status, &p->ctr,  &p->tseq,   &p->tcnt,  &p->gstart,
                       &p->gend,  &p->counts, &p->kept, &p->stats,  &p->flags, &p->kdiag,
                       &p->Cscr,  &p->Nmscr, &p->Kscr,  &p->Knscr, &p->heavy, &p->hcount,
-                      &p->dense, &p->tiles, &p->tiles4, &p->symhist, &p->trieS0, &p->trieW, &p->trieS, &p->genW0, &p->genW1, &p->genS0, &p->genS1, &p->kmdev, &p->trieR, &p->trieX0, &p->trieX1, &p->pdesc, &p->wD, &p->wlist, &p->wfill, &p->wC, &p->winv, &p->wtiles, &p->lightacc, &p->binrec, &p->bincnt, &p->farrec, &p->farscr, &p->farbins, &p->xccnt, &p->xbcnt, &p->relkeys, &p->relH, &p->thg,
+                      &p->dense, &p->tiles, &p->tiles4, &p->symhist, &p->trieS0, &p->trieW, &p->trieS, &p->genW0, &p->genW1, &p->genS0, &p->genS1, &p->kmdev, &p->trieR, &p->trieX0, &p->trieX1, &p->pdesc, &p->wD, &p->wlist, &p->wfill, &p->wC, &p->winv, &p->wtiles, &p->lightacc, &p->binrec, &p->bincnt, &p->farrec, &p->farscr, &p->farbins, &p->xccnt, &p->xbcnt, &p->relkeys, &p->relH, &p->thg, &p->lbig,
                       &p->win,   &p->bkH,   &p->bktot, &p->bkbase, &p->bkdesc, &p->bktab,
                       &p->bktcnt, &p->bkgs, &p->bkocc};
     for (DevBuf* b : bufs)
@@ -1836,8 +1836,9 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
             // CTA into the mask's overflow slot, which the segment kernel takes afterwards.
             auto fuse_ok = [&](int npos) {
                 // (the bound, in tiles: Text 0.5 -> 84.5 ms, 1.5 -> 83.6, 8 -> 79.5, 16 ->
-                // 79.5, >= 30 -> 92.3: its level-5 leaves, largest groups ~2e4, serialise
-                // on their owner CTAs; Scale's expected 41 fuses under any bound)
+                // 79.5, >= 30 -> 92.3 with the owner-CTA split, 86.8 with the queue of
+                // leaf.cu: its level-5 leaves, largest groups ~2e4; Scale's expected 41
+                // fuses under any bound)
                 constexpr double kBigTiles = 8.0;
                 return p->leaf_fuse && npos >= 1 && lf_big_expect(npos) <= (double)leaf_tile() * kBigTiles;
             };
@@ -1846,11 +1847,20 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
             // (a batch is one level: every mask has kk kept positions; kk >= 2 for a trie
             // leaf, kk >= 1 for a chain pass -- kk - 1 >= 1 either way)
             const bool fused_any = kk >= 2 && fuse_ok(kk - 1);
+            // the queue of groups too large for a leaf CTA (leaf_big_kernel): entries,
+            // then the two counters
+            const uint32_t lbcap = (uint32_t)std::min<uint64_t>(
+                1u << 30, (uint64_t)nmask * (n / 256 + 1));
+            LfBigList lbl{nullptr, nullptr, 0};
             if (fused_any) {  // the fused leaves write this batch's segment outputs
                 gakco_status ws = wait_buf();
                 if (ws != GAKCO_OK) return ws;
                 CK(cudaMemsetAsync(so.counts, 0, 2 * sizeof(uint32_t), s));
                 CK(cudaMemsetAsync(bcnt, 0, (size_t)nmask * 4, s));
+                CK(p->ensure(p->lbig, (size_t)lbcap * sizeof(LfBig) + 64, s));
+                lbl = LfBigList{(LfBig*)p->lbig.p, (uint32_t*)((uint8_t*)p->lbig.p + (size_t)lbcap * sizeof(LfBig)),
+                                lbcap};
+                CK(cudaMemsetAsync(lbl.count, 0, 2 * sizeof(uint32_t), s));
             }
             std::vector<uint64_t> kms;
             for (size_t j = pos; j < end; ++j) {
@@ -1882,7 +1892,7 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
                         p->launches += 1;
                         LK(launch_leaf(iw, is, seq16, n, pC + xl_parent[j], kmask & ~pos_mask(xl_x[j]),
                                        kmask, sh, dmask, dstride, Dm, so, stats, lcw, lcs, lcc, wleaf,
-                                       sleaf, ocnt, s));
+                                       sleaf, ocnt, lbl, s));
                         p->stage_end(s, S_SEGMENT, a);
                     } else {
                         LK(launch_trie_pass64(iw, wleaf, is, sleaf, seq16, n, pC + xl_parent[j], sh,
@@ -1921,16 +1931,33 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
                     for (int r = 0; r < kk - 1; ++r) pm |= pos_mask(kept[r]);
                     p->stage_begin(s, &a);
                     p->launches += 1;
+                    // (groups past a CTA's window expected: queued and split right after
+                    // this leaf, while the stack top still holds its input; else the rare
+                    // one is split by its own CTA)
+                    const bool tq = lf_big_expect(kk - 1) > (double)leaf_tile();
                     LK(launch_leaf((const uint64_t*)p->trieW.p + (size_t)(kk - 2) * n,
                                    (const uint8_t*)p->trieS.p + (size_t)(kk - 2) * n * ssz, seq16, n,
                                    nullptr, pm, kmask, bits * (g - 1 - kept[kk - 1]), dmask, dstride, Dm,
-                                   so, stats, lcw, lcs, lcc, wleaf, sleaf, ocnt, s));
+                                   so, stats, lcw, lcs, lcc, wleaf, sleaf, ocnt,
+                                   tq ? lbl : LfBigList{nullptr, nullptr, 0}, s));
+                    if (tq) {
+                        p->launches += 1;
+                        LK(launch_leaf_big(lbl, seq16, p->sm_count, s));
+                        CK(cudaMemsetAsync(lbl.count, 0, 2 * sizeof(uint32_t), s));
+                    }
                     p->stage_end(s, S_SEGMENT, a);
                 }
             }
             if (!fused_any) {
                 gakco_status ws = wait_buf();
                 if (ws != GAKCO_OK) return ws;
+            } else if (xl_parent[pos] >= 0) {  // the chain's queued large groups (the
+                // parents' compacted arrays are stable through the batch)
+                p->stage_begin(s, &a);
+                p->launches += 1;
+                LK(launch_leaf_big(lbl, seq16, p->sm_count, s));
+                CK(cudaMemsetAsync(lbl.count, 0, 2 * sizeof(uint32_t), s));
+                p->stage_end(s, S_SEGMENT, a);
             }
             p->stage_begin(s, &a);
             kms.push_back(0);
