@@ -618,13 +618,29 @@ __global__ void __launch_bounds__(WB_THREADS) window_build_kernel(SegmentOut so,
             const uint32_t col = sl * GT_KB + warp * WB_CPW + jj;
             g[jj] = col < c1 ? wa.list[(uint64_t)w * wa.cap + col] : make_uint2(0u, 0u);
         }
+        // the first 32 members of all 8 columns: ids, then labels, loaded together (the
+        // dependent id -> label loads were the latency, column after column); members
+        // past 32 below
+        uint32_t xm[WB_CPW], cm[WB_CPW];
+#pragma unroll
+        for (int jj = 0; jj < WB_CPW; ++jj) {
+            const uint32_t t = g[jj].x + lane;
+            const bool v = t < g[jj].y;
+            xm[jj] = v ? so.tseq[t] & 0x7fffffffu : 0xffffffffu;
+            cm[jj] = v ? so.tcnt[t] : 0u;
+        }
+#pragma unroll
+        for (int jj = 0; jj < WB_CPW; ++jj) xm[jj] = xm[jj] != 0xffffffffu ? perm[xm[jj]] - lab0 : 0xffffffffu;
 #pragma unroll
         for (int jj = 0; jj < WB_CPW; ++jj) {
             const int j = warp * WB_CPW + jj;
-            for (uint32_t t = g[jj].x + lane; t < g[jj].y; t += 32) {
-                const uint32_t r = perm[so.tseq[t] & 0x7fffffffu] - lab0;
-                if (r < (uint32_t)WIN_ROWS)  // (a split group: its members in this window)
-                    tile[r * GT_KB + ((((uint32_t)j >> 2) ^ (r & 31u)) << 2) + (j & 3)] =
+            const uint32_t r = xm[jj];
+            if (r < (uint32_t)WIN_ROWS)  // (a split group: its members in this window)
+                tile[r * GT_KB + ((((uint32_t)j >> 2) ^ (r & 31u)) << 2) + (j & 3)] = (uint8_t)cm[jj];
+            for (uint32_t t = g[jj].x + 32 + lane; t < g[jj].y; t += 32) {
+                const uint32_t r2 = perm[so.tseq[t] & 0x7fffffffu] - lab0;
+                if (r2 < (uint32_t)WIN_ROWS)
+                    tile[r2 * GT_KB + ((((uint32_t)j >> 2) ^ (r2 & 31u)) << 2) + (j & 3)] =
                         (uint8_t)so.tcnt[t];
             }
         }
