@@ -537,6 +537,31 @@ def test_k_only_dna_digest(gk):
     assert refs.digest_np(K.cpu().numpy()) == int(gold["digests"]["K"])
 
 
+def test_stage_timeline(gk, oracle_lib):
+    """gakco_stage_timeline (GAKCO_OPT_TIMING, pipeline on and off): every stage event
+    of the last call as (stage, t0, t1), 0 <= t0 <= t1, stages 0..7, and per stage the
+    same totals as the stats' ms_* fields; the results stay exact."""
+    cp = sc.gen_families(61, 120, 8, 200, 120, 200, sigma=20)
+    g, k, M = 8, 4, 3
+    ref = oracle_lib.compute(cp, g, k, M)
+    names = ["encode", "sort", "segment", "light", "heavy", "epilogue", "dense", "far"]
+    for pipe in (0, 1):
+        plan = gk.Plan(cp.sigma, g, k, M)
+        plan.set_option(gk.GAKCO_OPT_TIMING, 1)
+        plan.set_option(gk.GAKCO_OPT_PIPELINE, pipe)
+        r = gk.kernel_matrix(cp.codes, cp.offsets, cp.sigma, g, k, M, plan=plan)
+        assert_parity({key: v.cpu().numpy() for key, v in r.items()}, ref)
+        tl = plan.stage_timeline()
+        st = plan.stats()
+        plan.close()
+        assert tl and all(0 <= s < 8 and 0.0 <= a <= b for s, a, b in tl)
+        tot = {}
+        for s, a, b in tl:
+            tot[names[s]] = tot.get(names[s], 0.0) + (b - a)
+        for nm, v in tot.items():
+            assert abs(v - st["ms_" + nm]) <= 1e-3 * max(1.0, v)
+
+
 def test_errors(gk):
     with pytest.raises(gk.GakcoError) as e:
         gk.Plan(4, 3, 4, 0)
