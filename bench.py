@@ -417,7 +417,7 @@ def run_ours(a):
         Kn = torch.empty((N, N), dtype=torch.float64, device=dev)
 
         def step():
-            C.zero_()
+            plan.zero_upper(C, N, M + 1, stream)  # (accumulate adds into the upper triangles)
             plan.accumulate(codes_d, offs_h, N, C, stream)
             plan.finalize(C, N, Nm, K, Kn, stream)
     else:

@@ -215,6 +215,12 @@ gakco_status gakco_set_shard(gakco_plan* plan, int rank, int world);
 
 gakco_status gakco_set_option(gakco_plan* plan, int option, int64_t value);
 
+/* Zero the upper triangles (Y >= X, diagonal included) of `levels` consecutive N x N
+ * int64 matrices at device pointer C (the part gakco_accumulate adds into and
+ * gakco_finalize reads: half the bytes of zeroing C whole). Asynchronous on
+ * cuda_stream. */
+gakco_status gakco_zero_upper(gakco_plan* plan, int64_t* C, int64_t N, int levels, void* cuda_stream);
+
 /* Add this shard's contribution to C: for each of its masks, every pair of
  * sequences sharing a masked key adds count_X*count_Y.
  * A code >= sigma gives GAKCO_E_SYMBOL: here if codes is a host pointer; for a

@@ -308,6 +308,7 @@ struct LfBigList {
     uint32_t* count;  // [0] entries queued, [1] entries claimed (both zeroed per batch)
     uint32_t cap;
 };
+cudaError_t launch_zero_upper(int64_t* C, int64_t N, int levels, int sm_count, cudaStream_t s);
 int leaf_tile();  // group heads per CTA of launch_leaf
 // the queued large groups of a batch, split into their overflow slots (after the
 // batch's launch_leaf calls, before the segment kernel over the overflow slots)

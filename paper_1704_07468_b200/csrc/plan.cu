@@ -2372,8 +2372,10 @@ extern "C" gakco_status gakco_kernel(gakco_plan* p, const uint8_t* codes, const 
         if (e != cudaSuccess) return p->cuda_fail(e, "C scratch");
         dC = (int64_t*)p->Cscr.p;
     }
-    cudaError_t e = cudaMemsetAsync(dC, 0, bytes, s);
-    if (e != cudaSuccess) return p->cuda_fail(e, "memset C");
+    // (the upper triangles only: accumulate adds there, finalize reads there and
+    // writes the mirror)
+    cudaError_t e = launch_zero_upper(dC, N, p->M + 1, p->sm_count, s);
+    if (e != cudaSuccess) return p->cuda_fail(e, "zero C");
     gakco_status st = accumulate_impl(p, codes, offsets, N, dC, s, 0, 1);
     if (st != GAKCO_OK) return st;
     st = finalize_impl(p, dC, N, Nm, K, Knorm, s, true);
@@ -2400,8 +2402,8 @@ extern "C" gakco_status gakco_kernel_k(gakco_plan* p, const uint8_t* codes,
     cudaError_t e = p->ensure(p->Cscr, bytes, s);
     if (e != cudaSuccess) return p->cuda_fail(e, "C scratch");
     int64_t* dC = (int64_t*)p->Cscr.p;
-    e = cudaMemsetAsync(dC, 0, bytes, s);
-    if (e != cudaSuccess) return p->cuda_fail(e, "memset C");
+    e = launch_zero_upper(dC, N, 1, p->sm_count, s);
+    if (e != cudaSuccess) return p->cuda_fail(e, "zero C");
     gakco_status st = accumulate_impl(p, codes, offsets, N, dC, s, 0, 1, p->g - p->k);
     if (st != GAKCO_OK) return st;
     return finalize_impl(p, dC, N, nullptr, K, Knorm, s, true, /*k_only=*/true);
@@ -2532,6 +2534,16 @@ extern "C" gakco_status gakco_get_stats(gakco_plan* p, gakco_stats* out) {
             *ms[se.first] += t;
     }
     *out = r;
+    return GAKCO_OK;
+}
+
+extern "C" gakco_status gakco_zero_upper(gakco_plan* p, int64_t* C, int64_t N, int levels,
+                                         void* stream) {
+    if (!p || !C || N < 0 || levels < 0) return GAKCO_E_ARG;
+    if (!is_device_ptr(C)) return p->fail(GAKCO_E_ARG, "C must be a device pointer");
+    DeviceGuard dg(p->device);
+    cudaError_t e = launch_zero_upper(C, N, levels, p->sm_count, (cudaStream_t)stream);
+    if (e != cudaSuccess) return p->cuda_fail(e, "zero_upper");
     return GAKCO_OK;
 }
 

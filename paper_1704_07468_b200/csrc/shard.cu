@@ -45,6 +45,34 @@ __global__ void __launch_bounds__(256) pack_upper_kernel(const int64_t* __restri
     for (int64_t e = lo + threadIdx.x; e < hi; e += blockDim.x) dst[e] = (T)src[e];
 }
 
+// rows of the upper triangles: row (l, X) zeroes [X, N), 16-byte stores on the aligned
+// body
+__global__ void __launch_bounds__(256) zero_upper_kernel(int64_t* __restrict__ C, int64_t N,
+                                                         int levels) {
+    const int64_t rows = (int64_t)levels * N;
+    for (int64_t r = blockIdx.x; r < rows; r += gridDim.x) {
+        const int64_t X = r % N;
+        int64_t* row = C + (size_t)r * (size_t)N;
+        int64_t a = X;
+        if (a < N && (((uintptr_t)(row + a)) & 15)) {  // (8-byte aligned: one scalar head)
+            if (threadIdx.x == 0) row[a] = 0;
+            ++a;
+        }
+        const int64_t nv = (N - a) / 2;
+        int4* v = (int4*)(row + a);
+        for (int64_t i = threadIdx.x; i < nv; i += blockDim.x) v[i] = make_int4(0, 0, 0, 0);
+        if (threadIdx.x == 0 && a + 2 * nv < N) row[N - 1] = 0;
+    }
+}
+
+cudaError_t launch_zero_upper(int64_t* C, int64_t N, int levels, int sm_count, cudaStream_t s) {
+    const int64_t rows = (int64_t)levels * N;
+    if (rows <= 0) return cudaGetLastError();
+    const int64_t blocks = std::min<int64_t>(rows, (int64_t)sm_count * 8);
+    zero_upper_kernel<<<(unsigned)blocks, 256, 0, s>>>(C, N, levels);
+    return cudaGetLastError();
+}
+
 __global__ void diag_kernel(const int64_t* __restrict__ C, int64_t N, int levels,
                             int64_t* __restrict__ out) {
     const int64_t nn = N * N;

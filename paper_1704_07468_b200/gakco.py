@@ -57,7 +57,7 @@ EXPORTS = ("gakco_create", "gakco_set_shard", "gakco_set_option", "gakco_accumul
            "gakco_get_stats", "gakco_stream_wait_level", "gakco_level_order", "gakco_pack_upper",
            "gakco_diag", "gakco_finalize_packed", "gakco_finalize_packed_sum", "gakco_ipc_alloc",
            "gakco_ipc_free", "gakco_ipc_handle", "gakco_ipc_open", "gakco_ipc_close",
-           "gakco_pack_upper_peers", "gakco_stage_timeline",
+           "gakco_pack_upper_peers", "gakco_stage_timeline", "gakco_zero_upper",
            "gakco_num_masks", "gakco_last_error", "gakco_status_string", "gakco_destroy")
 
 
@@ -105,6 +105,7 @@ def lib():
         L.gakco_kernel_rect.argtypes = [P, P, P, i64, i64, P, P, P, P, P, P]
         L.gakco_get_stats.argtypes = [P, ctypes.POINTER(gakco_stats)]
         L.gakco_stage_timeline.argtypes = [P, P, P, P, i64, ctypes.POINTER(i64)]
+        L.gakco_zero_upper.argtypes = [P, P, i64, ci, P]
         L.gakco_stream_wait_level.argtypes = [P, ci, P]
         L.gakco_level_order.argtypes = [P, ctypes.POINTER(ci), ci]
         L.gakco_level_order.restype = ci
@@ -131,7 +132,8 @@ def lib():
                   "gakco_get_stats", "gakco_stream_wait_level", "gakco_pack_upper",
                   "gakco_diag", "gakco_finalize_packed", "gakco_finalize_packed_sum",
                   "gakco_ipc_alloc", "gakco_ipc_free", "gakco_ipc_handle", "gakco_ipc_open",
-                  "gakco_ipc_close", "gakco_pack_upper_peers", "gakco_stage_timeline"):
+                  "gakco_ipc_close", "gakco_pack_upper_peers", "gakco_stage_timeline",
+                  "gakco_zero_upper"):
             getattr(L, f).restype = ci
         _lib = L
     return _lib
@@ -337,6 +339,10 @@ class Plan:
 
     def stage_timeline(self):
         return gakco_stage_timeline(self.h)
+
+    def zero_upper(self, C, N, levels, stream=None):
+        """Zero the upper triangles of `levels` N x N int64 matrices (device C)."""
+        _check(self.h, lib().gakco_zero_upper(self.h, _ptr(C), N, levels, _stream(stream)))
 
     def stream_wait_level(self, m, stream=None):
         gakco_stream_wait_level(self.h, m, stream)

@@ -188,7 +188,7 @@ class ShardedStep:
         """accumulate (this rank's masks) -> per-level pack + reduce-scatter (comm
         stream, overlapping later levels) -> diagonal all-reduce -> slice epilogue."""
         plan, N, L = self.plan, self.N, self.M + 1
-        C.zero_()
+        plan.zero_upper(C, N, L, stream)  # (accumulate adds into the upper triangles)
         plan.accumulate(codes, offsets, N, C, stream)
         cs = self.comm
         if self.exchange == "p2p":

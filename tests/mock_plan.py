@@ -23,6 +23,12 @@ class MockPlan:
         self.cp, self.g, self.k, self.M = corpus, g, k, M
         self.mine = parallel.shard_masks(g, M, rank, world)
 
+    def zero_upper(self, C, N, levels, stream=None):
+        """gakco_zero_upper: the upper triangles (Y >= X) of `levels` N x N matrices."""
+        iu = np.triu_indices(N)
+        for lv in range(levels):
+            C[lv][iu] = 0
+
     def accumulate(self, codes, offsets, N, C, stream=None):
         """Upper triangle (Y >= X) of this shard's C_m, Algorithm 1."""
         per_seq = [gmers(self.cp.seq(i), self.g) for i in range(N)]

@@ -537,6 +537,25 @@ def test_k_only_dna_digest(gk):
     assert refs.digest_np(K.cpu().numpy()) == int(gold["digests"]["K"])
 
 
+def test_zero_upper(gk):
+    """gakco_zero_upper zeroes exactly the upper triangles (Y >= X) of each level,
+    odd and even N (16-byte vector body, scalar head and tail); the lower triangles
+    keep their values."""
+    import torch
+    plan = gk.Plan(4, 5, 3, 2)
+    for N, L in ((1, 1), (7, 3), (64, 2), (333, 3)):
+        C = torch.randint(1, 1 << 40, (L, N, N), dtype=torch.int64, device="cuda")
+        ref = C.clone().cpu().numpy()
+        plan.zero_upper(C, N, L)
+        torch.cuda.synchronize()
+        got = C.cpu().numpy()
+        iu = np.triu_indices(N)
+        for lv in range(L):
+            ref[lv][iu] = 0
+        assert np.array_equal(got, ref)
+    plan.close()
+
+
 def test_stage_timeline(gk, oracle_lib):
     """gakco_stage_timeline (GAKCO_OPT_TIMING, pipeline on and off): every stage event
     of the last call as (stage, t0, t1), 0 <= t0 <= t1, stages 0..7, and per stage the
