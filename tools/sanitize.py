@@ -32,7 +32,8 @@ def main():
              {"heavy_min_seqs": 2}, {"heavy_min_seqs": 2, "gram_fp4": 0},
              {"heavy_min_seqs": 2, "gram_pair": 0}, {"heavy_min_seqs": 1 << 50},
              {"pipeline": 0}, {"light_relabel": 1, "light_window": 1, "far_near": 2},
-             {"light_relabel": 1, "sort": 6, "far_near": 4}]
+             {"light_relabel": 1, "sort": 6, "far_near": 4}, {"sort": 6, "leaf_fuse": 0},
+             {"sort": 6, "light_relabel": 1, "batch_keys": 30000}]
     only = os.environ.get("SAN_CASES")
     for i, opts in enumerate(cases):
         if only and str(i) not in only.split(","):
@@ -45,6 +46,21 @@ def main():
         assert np.array_equal(r["C"].cpu().numpy(), ref["C"]), opts
         assert np.array_equal(r["K"].cpu().numpy(), ref["K"]), opts
         print("ok", opts, flush=True)
+    # fused leaves with groups past a CTA's window (periodic sequences: groups of ~10^4
+    # g-mers), both the queued 1024-thread split and the owner-CTA split
+    rng = np.random.default_rng(44)
+    seqs = [[0, 1, 2] * 900 for _ in range(4)] + [[1, 2, 0, 3] * 600 for _ in range(3)]
+    seqs += [list(rng.integers(0, 4, int(rng.integers(200, 1500)))) for _ in range(40)]
+    cpb = sc.from_sequences(4, seqs)
+    refb = oracle.compute(cpb, 7, 3, 4)
+    for opts in ({"sort": 6}, {"sort": 6, "batch_keys": 90000}):
+        plan = gk.Plan(cpb.sigma, 7, 3, 4)
+        for o, v in opts.items():
+            plan.set_option(getattr(gk, "GAKCO_OPT_" + o.upper()), v)
+        r = gk.kernel_matrix(cpb.codes, cpb.offsets, cpb.sigma, 7, 3, 4, plan=plan)
+        plan.close()
+        assert np.array_equal(r["C"].cpu().numpy(), refb["C"]), opts
+        print("ok big groups", opts, flush=True)
     N = cp.n_seq
     # K-only and train x test
     plan = gk.Plan(cp.sigma, g, k, M)
