@@ -288,9 +288,15 @@ __global__ void __launch_bounds__(256, MINB) light_kernel(SegmentOut so, int64_t
     // A warp takes 32 groups at a time: one coalesced load brings all their
     // triple ranges, and the first 32 triples of the next group are loaded while
     // the current one is processed.
+    // (the next 32 groups' ranges are loaded while these are processed)
+    uint2 rg_next = warp * 32 + lane < G ? so.groups[warp * 32 + lane] : make_uint2(0u, 0u);
     for (uint64_t base = warp * 32; base < G; base += nwarps * 32) {
         const uint32_t ng = (uint32_t)min((uint64_t)32, (uint64_t)G - base);
-        const uint2 rg = lane < ng ? so.groups[base + lane] : make_uint2(0u, 0u);
+        const uint2 rg = rg_next;
+        {
+            const uint64_t nb = base + nwarps * 32 + lane;
+            rg_next = nb < G ? so.groups[nb] : make_uint2(0u, 0u);
+        }
         const uint32_t my_start = rg.x, my_end = rg.y;
         const uint32_t my_s = my_end - my_start;
 
