@@ -56,7 +56,7 @@ constexpr size_t lf_smem() {
     // bulk-copy spans need the slack), perm [C] u16 (then
     // the group starts), warp digit counters + match masks, digit starts / counts /
     // offsets, scratch
-    return (size_t)(Lf<TH>::C + 8) * 8 + (size_t)(Lf<TH>::C + 24) * sizeof(S) + (size_t)Lf<TH>::C * 2 +
+    return (size_t)(Lf<TH>::C + 8) * 8 + (size_t)(Lf<TH>::C + 24) * sizeof(S) + (size_t)Lf<TH>::C * 4 +
            2 * Lf<TH>::WARPS * LF_ND * 4 + 3 * LF_ND * 4 + 64 * 4 + 64;
 }
 
@@ -228,7 +228,8 @@ __global__ void __launch_bounds__(TH, 1024 / TH) leaf_kernel(
     sh.sw = (uint64_t*)smem;
     S* const ss = (S*)(smem + (size_t)(C + 8) * 8);
     sh.perm = (uint16_t*)(smem + (size_t)(C + 8) * 8 + (size_t)(C + 24) * sizeof(S));
-    sh.whist = (uint32_t*)(sh.perm + C);
+    uint16_t* const s_kl = sh.perm + C;  // [C] sorted positions of the compacted elements
+    sh.whist = (uint32_t*)(s_kl + C);
     sh.match = sh.whist + W * LF_ND;
     sh.cstart = sh.match + W * LF_ND;
     sh.tcnt = sh.cstart + LF_ND;
@@ -410,19 +411,26 @@ __global__ void __launch_bounds__(TH, 1024 / TH) leaf_kernel(
             if (agg_t) atomicAdd(&stats[ST_TRIPLES], (unsigned long long)agg_t);
             if (agg_g) atomicAdd(&stats[ST_GROUPS], (unsigned long long)agg_g);
         }
-        __syncthreads();  // (also: every read of the window / perm done)
+        // the compacted elements' sorted positions, in order (their copy below is
+        // coalesced: consecutive threads, consecutive outputs)
+        if (cw) {
+            uint32_t k = off_k;
+#pragma unroll
+            for (int i = 0; i < LF_IT; ++i)
+                if (keep & (1u << i)) s_kl[k++] = (uint16_t)(lbase + i);
+        }
+        __syncthreads();
         const uint32_t base_t = s_base_t, base_g = s_base_g;
         // compacted elements (groups of >= 2 elements), in sorted order
         if (cw) {
-            uint32_t k = s_base_c + off_k;
-#pragma unroll
-            for (int i = 0; i < LF_IT; ++i)
-                if (keep & (1u << i)) {
-                    GK_CHECK(k < n);
-                    cw[k] = cur[i].w;
-                    cs[k] = (S)cur[i].s;
-                    ++k;
-                }
+            const uint32_t bc = s_base_c;
+            for (uint32_t j = tid; j < agg_k; j += TH) {
+                GK_CHECK(bc + j < n);
+                const uint32_t l = a0l + sh.perm[s_kl[j]];
+                cw[bc + j] = SW[l];
+                cs[bc + j] = SS[l];
+            }
+            __syncthreads();  // (every read of the window / perm done: staging below)
         }
         // triples staged in shared memory (the window), written coalesced; group ranges
         uint32_t* s_tx = (uint32_t*)sh.sw;
