@@ -44,6 +44,8 @@ __global__ void __launch_bounds__(RG_THREADS, 4) segment_rag_kernel(
     __shared__ uint32_t s_w[16];
     __shared__ uint16_t s_gpos[RG_TILE];
     __shared__ uint32_t s_tx[RG_TILE], s_tc[RG_TILE];
+    __shared__ uint64_t s_kw[RG_TILE];  // the tile's compacted elements, in order (staged:
+    __shared__ S s_ks[RG_TILE];         // their copy out is coalesced)
     __shared__ uint32_t s_first_gh, s_base_t, s_base_g, s_base_c, s_tail;
     __shared__ uint32_t s_wmin[RG_THREADS / 32], s_beyond, s_cross;
     __shared__ unsigned long long s_gend;
@@ -239,6 +241,16 @@ __global__ void __launch_bounds__(RG_THREADS, 4) segment_rag_kernel(
     __syncthreads();
     const uint32_t tail = s_tail;
     const uint32_t tail_len = (uint32_t)(gend - tile_end);
+    if (cw) {
+        uint32_t k = off_k;
+#pragma unroll
+        for (int i = 0; i < RG_IT; ++i)
+            if (keep & (1u << i)) {
+                s_kw[k] = cur[i].w;
+                s_ks[k] = (S)cur[i].s;
+                ++k;
+            }
+    }
     if (tid == 0) {
         s_base_t = atomicAdd(&counters[0], agg_t + tail);
         s_base_g = atomicAdd(&counters[1], agg_g);
@@ -251,15 +263,11 @@ __global__ void __launch_bounds__(RG_THREADS, 4) segment_rag_kernel(
     // 5. compacted elements of this tile, then the crossing group's tail
     if (cw) {
         const uint64_t cb = (uint64_t)sgi * n + s_base_c;
-        uint32_t k = off_k;
-#pragma unroll
-        for (int i = 0; i < RG_IT; ++i)
-            if (keep & (1u << i)) {
-                GK_CHECK(s_base_c + k < n);
-                cw[cb + k] = cur[i].w;
-                cs[cb + k] = (S)cur[i].s;
-                ++k;
-            }
+        for (uint32_t j = tid; j < agg_k; j += RG_THREADS) {
+            GK_CHECK(s_base_c + j < n);
+            cw[cb + j] = s_kw[j];
+            cs[cb + j] = s_ks[j];
+        }
         for (uint32_t j = tid; j < tail_len; j += RG_THREADS) {
             GK_CHECK(s_base_c + agg_k + j < n);
             cw[cb + agg_k + j] = w[tile_end + j];
