@@ -309,7 +309,7 @@ struct LfBigList {
     uint32_t cap;
 };
 cudaError_t launch_zero_upper(int64_t* C, int64_t N, int levels, int sm_count, cudaStream_t s);
-int leaf_tile();  // group heads per CTA of launch_leaf
+int leaf_tile(bool wide = false);  // group heads per CTA of launch_leaf
 // the queued large groups of a batch, split into their overflow slots (after the
 // batch's launch_leaf calls, before the segment kernel over the overflow slots)
 cudaError_t launch_leaf_big(LfBigList bl, bool seq16, int sm_count, cudaStream_t s);
@@ -317,7 +317,8 @@ cudaError_t launch_leaf(const uint64_t* w, const void* sq, bool seq16, uint64_t 
                         const uint32_t* cntp, uint64_t pmask, uint64_t kmask, int shift,
                         uint32_t dmask, int64_t dstride, int64_t* diag, SegmentOut so,
                         unsigned long long* stats, uint64_t* cw, void* cs, uint32_t* ccnt,
-                        uint64_t* ow, void* os, uint32_t* ocnt, LfBigList bl, cudaStream_t s);
+                        uint64_t* ow, void* os, uint32_t* ocnt, LfBigList bl, cudaStream_t s,
+                        bool wide = false);  // wide: 12 items per thread (1536-element ranges)
 cudaError_t launch_seq16(const uint32_t* a, uint16_t* b, uint64_t n, int sm_count,
                          cudaStream_t s);
 cudaError_t launch_radix_chunked2(const void* in, void* out, bool k64, uint64_t n, int nseg,

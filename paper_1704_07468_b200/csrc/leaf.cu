@@ -27,13 +27,13 @@ namespace gk {
 
 namespace {
 
-constexpr int LF_IT = 8;
+constexpr int LF_IT = 8;  // items per thread (12: the "wide" variant, see launch_leaf)
 constexpr int LF_ND = 64;  // digit buckets (symbols < 64)
 
-template <int TH>
+template <int TH, int IT = LF_IT>
 struct Lf {
     static constexpr int WARPS = TH / 32;
-    static constexpr int C = TH * LF_IT;  // range capacity (shared memory)
+    static constexpr int C = TH * IT;  // range capacity (shared memory)
     static constexpr int T = C / 4 * 3;   // tile of group heads per CTA (the rest: the
                                           // last group's tail)
 };
@@ -50,14 +50,15 @@ struct LfElem {
     uint32_t s;
 };
 
-template <typename S, int TH>
+template <typename S, int TH, int IT>
 constexpr size_t lf_smem() {
     // window keys [C + 8] (then the triple staging), ids [C + 24] (the 16-byte aligned
     // bulk-copy spans need the slack), perm [C] u16 (then
     // the group starts), warp digit counters + match masks, digit starts / counts /
     // offsets, scratch
-    return (size_t)(Lf<TH>::C + 8) * 8 + (size_t)(Lf<TH>::C + 24) * sizeof(S) + (size_t)Lf<TH>::C * 4 +
-           2 * Lf<TH>::WARPS * LF_ND * 4 + 3 * LF_ND * 4 + 64 * 4 + 64;
+    using L = Lf<TH, IT>;
+    return (size_t)(L::C + 8) * 8 + (size_t)(L::C + 24) * sizeof(S) + (size_t)L::C * 4 +
+           2 * L::WARPS * LF_ND * 4 + 3 * LF_ND * 4 + 64 * 4 + 64;
 }
 
 // exclusive scan over the TH threads of v (every thread must call); s_w: WARPS + 1 words
@@ -136,7 +137,7 @@ struct LfShared {
 // stable rank of sw[off, off + len) (len <= C) by digit (sw >> shift) & dmask:
 // perm[p] = the source index (from off) of sorted position p; cstart / tcnt: each
 // digit's start and count. Every thread must call it (it synchronises the block).
-template <int TH>
+template <int TH, int IT>
 __device__ __forceinline__ void lf_rank(const LfShared& sh, const uint64_t* keys, uint32_t off,
                                         uint32_t len, int shift, uint32_t dmask) {
     constexpr int W = Lf<TH>::WARPS;
@@ -147,9 +148,9 @@ __device__ __forceinline__ void lf_rank(const LfShared& sh, const uint64_t* keys
     // each warp ranks a block of ipw * 32 consecutive elements (ipw = len / the block
     // width, rounded up: no warp idles through predicated-off items)
     const uint32_t ipw = (len + W * 32 - 1) / (W * 32);
-    uint32_t dg[LF_IT / 4] = {0, 0}, rank[LF_IT / 2] = {0, 0, 0, 0};
+    uint32_t dg[(IT + 3) / 4] = {}, rank[(IT + 1) / 2] = {};
 #pragma unroll
-    for (int i = 0; i < LF_IT; ++i) {
+    for (int i = 0; i < IT; ++i) {
         if ((uint32_t)i >= ipw) break;  // (warp-uniform)
         const uint32_t idx = (uint32_t)(wp * ipw * 32 + i * 32 + lane);
         const bool valid = idx < len;
@@ -199,7 +200,7 @@ __device__ __forceinline__ void lf_rank(const LfShared& sh, const uint64_t* keys
     }
     __syncthreads();
 #pragma unroll
-    for (int i = 0; i < LF_IT; ++i) {
+    for (int i = 0; i < IT; ++i) {
         if ((uint32_t)i >= ipw) break;
         const uint32_t idx = (uint32_t)(wp * ipw * 32 + i * 32 + lane);
         if (idx < len) {
@@ -215,13 +216,13 @@ __device__ __forceinline__ void lf_rank(const LfShared& sh, const uint64_t* keys
     __syncthreads();
 }
 
-template <typename S, int TH>
+template <typename S, int TH, int IT>
 __global__ void __launch_bounds__(TH, 1024 / TH) leaf_kernel(
     const uint64_t* __restrict__ w, const S* __restrict__ sq, const uint32_t* cntp, uint64_t n,
     uint64_t pmask, uint64_t kmask, int shift, uint32_t dmask, int64_t dstride, int64_t* diag,
     uint32_t* counters, SegmentOut so, unsigned long long* stats, uint64_t* cw, S* cs,
     uint32_t* ccnt, uint64_t* ow, S* os, uint32_t* ocnt, LfBigList bl) {
-    using L = Lf<TH>;
+    using L = Lf<TH, IT>;
     constexpr int C = L::C, T = L::T, W = L::WARPS;
     extern __shared__ __align__(16) unsigned char smem[];
     LfShared sh;
@@ -315,7 +316,7 @@ __global__ void __launch_bounds__(TH, 1024 / TH) leaf_kernel(
 
     // 3. the range of whole groups: ranked by digit x, then the segment logic
     if (len > 0) {  // (block-uniform)
-        lf_rank<TH>(sh, SW, a0l, len, shift, dmask);
+        lf_rank<TH, IT>(sh, SW, a0l, len, shift, dmask);
         // thread tid owns sorted positions [tid * ipt, tid * ipt + ipt), ipt = len / TH
         // rounded up (<= IT): every thread has items
         const uint32_t ipt = (len + TH - 1) / TH;
@@ -325,12 +326,12 @@ __global__ void __launch_bounds__(TH, 1024 / TH) leaf_kernel(
             return LfElem{SW[l], (uint32_t)SS[l]};
         };
         auto geq = [&](const LfElem& x, const LfElem& y) { return ((x.w ^ y.w) & kmask) == 0; };
-        LfElem cur[LF_IT];
+        LfElem cur[IT];
         uint32_t th_bits = 0, gh_bits = 0, valid_bits = 0;
         {
             LfElem prev = (lbase > 0 && lbase < len) ? elem(lbase - 1) : LfElem{0ull, 0u};
 #pragma unroll
-            for (int i = 0; i < LF_IT; ++i) {
+            for (int i = 0; i < IT; ++i) {
                 cur[i] = LfElem{0ull, 0u};
                 if ((uint32_t)i >= ipt) continue;  // (block-uniform)
                 const uint32_t p = lbase + i;
@@ -377,9 +378,9 @@ __global__ void __launch_bounds__(TH, 1024 / TH) leaf_kernel(
         }
         // backward: run lengths, groups of >= 2 triples, the diagonal repeat term
         uint32_t multi_bits = 0;
-        uint32_t cntv[LF_IT];
+        uint32_t cntv[IT];
 #pragma unroll
-        for (int i = LF_IT - 1; i >= 0; --i) {
+        for (int i = IT - 1; i >= 0; --i) {
             cntv[i] = 0;
             if (!((th_bits >> i) & 1u)) continue;
             const uint32_t li = lbase + i;
@@ -395,7 +396,7 @@ __global__ void __launch_bounds__(TH, 1024 / TH) leaf_kernel(
         const uint32_t emit_t = th_bits & multi_bits;
         const uint32_t emit_g = emit_t & gh_bits;
         uint32_t keep = 0;
-        if (cw) keep = valid_bits & (~gh_bits | ~ghn) & 0xffu;
+        if (cw) keep = valid_bits & (~gh_bits | ~ghn) & ((1u << IT) - 1u);
         // one block scan of the three counts (16-bit fields: each total <= C = 4 * 256)
         uint64_t aggp;
         const uint64_t offp = lf_scan64<TH>((uint64_t)__popc(emit_t) | (uint64_t)__popc(emit_g) << 16 |
@@ -416,7 +417,7 @@ __global__ void __launch_bounds__(TH, 1024 / TH) leaf_kernel(
         if (cw) {
             uint32_t k = off_k;
 #pragma unroll
-            for (int i = 0; i < LF_IT; ++i)
+            for (int i = 0; i < IT; ++i)
                 if (keep & (1u << i)) s_kl[k++] = (uint16_t)(lbase + i);
         }
         __syncthreads();
@@ -438,7 +439,7 @@ __global__ void __launch_bounds__(TH, 1024 / TH) leaf_kernel(
         uint16_t* s_gpos = sh.perm;
         uint32_t li = off_t, gl = off_g;
 #pragma unroll
-        for (int i = 0; i < LF_IT; ++i) {
+        for (int i = 0; i < IT; ++i) {
             if (emit_t & (1u << i)) {
                 s_tx[li] = cur[i].s | (((gh_bits >> i) & 1u) << 31);
                 s_tc[li] = cntv[i];
@@ -513,7 +514,7 @@ __global__ void __launch_bounds__(TH, 1024 / TH) leaf_kernel(
                 ss[l] = sq[c0 + l];
             }
             __syncthreads();
-            lf_rank<TH>(sh, sh.sw, 0, cl, shift, dmask);
+            lf_rank<TH, IT>(sh, sh.sw, 0, cl, shift, dmask);
             for (uint32_t p = tid; p < cl; p += TH) {
                 const uint32_t l = sh.perm[p];
                 const uint64_t k = sh.sw[l];
@@ -610,7 +611,7 @@ __global__ void __launch_bounds__(LB_TH, 1) leaf_big_kernel(LfBigList bl) {
                 ss[l] = sq[c0 + l];
             }
             __syncthreads();
-            lf_rank<LB_TH>(sh, sh.sw, 0, cl, g.shift, g.dmask);
+            lf_rank<LB_TH, LF_IT>(sh, sh.sw, 0, cl, g.shift, g.dmask);
             for (uint32_t p = tid; p < cl; p += LB_TH) {
                 const uint32_t l = sh.perm[p];
                 const uint64_t k = sh.sw[l];
@@ -631,23 +632,23 @@ constexpr size_t lb_smem() {
            64 * 4 + 64;
 }
 
-template <int TH>
+template <int TH, int IT>
 cudaError_t leaf_go(const uint64_t* w, const void* sq, bool seq16, uint64_t n, const uint32_t* cntp,
                     uint64_t pmask, uint64_t kmask, int shift, uint32_t dmask, int64_t dstride,
                     int64_t* diag, SegmentOut so, unsigned long long* stats, uint64_t* cw, void* cs,
                     uint32_t* ccnt, uint64_t* ow, void* os, uint32_t* ocnt, LfBigList bl,
                     cudaStream_t s) {
-    const unsigned grid = (unsigned)((n + Lf<TH>::T - 1) / Lf<TH>::T);
+    const unsigned grid = (unsigned)((n + Lf<TH, IT>::T - 1) / Lf<TH, IT>::T);
     if (seq16) {
-        cudaFuncSetAttribute(leaf_kernel<uint16_t, TH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)lf_smem<uint16_t, TH>());
-        leaf_kernel<uint16_t, TH><<<grid, TH, lf_smem<uint16_t, TH>(), s>>>(
+        cudaFuncSetAttribute(leaf_kernel<uint16_t, TH, IT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)lf_smem<uint16_t, TH, IT>());
+        leaf_kernel<uint16_t, TH, IT><<<grid, TH, lf_smem<uint16_t, TH, IT>(), s>>>(
             w, (const uint16_t*)sq, cntp, n, pmask, kmask, shift, dmask, dstride, diag, so.counts, so,
             stats, cw, (uint16_t*)cs, ccnt, ow, (uint16_t*)os, ocnt, bl);
     } else {
-        cudaFuncSetAttribute(leaf_kernel<uint32_t, TH>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)lf_smem<uint32_t, TH>());
-        leaf_kernel<uint32_t, TH><<<grid, TH, lf_smem<uint32_t, TH>(), s>>>(
+        cudaFuncSetAttribute(leaf_kernel<uint32_t, TH, IT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)lf_smem<uint32_t, TH, IT>());
+        leaf_kernel<uint32_t, TH, IT><<<grid, TH, lf_smem<uint32_t, TH, IT>(), s>>>(
             w, (const uint32_t*)sq, cntp, n, pmask, kmask, shift, dmask, dstride, diag, so.counts, so,
             stats, cw, (uint32_t*)cs, ccnt, ow, (uint32_t*)os, ocnt, bl);
     }
@@ -657,15 +658,19 @@ cudaError_t leaf_go(const uint64_t* w, const void* sq, bool seq16, uint64_t n, c
 }  // namespace
 
 constexpr int LEAF_TH = 128;  // threads per CTA (Scale: 128 -> 54.8 ms, 256 -> 57.6, 512 -> 63.2)
-int leaf_tile() { return Lf<LEAF_TH>::T; }
+int leaf_tile(bool wide) { return wide ? Lf<LEAF_TH, 12>::T : Lf<LEAF_TH>::T; }
 
 cudaError_t launch_leaf(const uint64_t* w, const void* sq, bool seq16, uint64_t n,
                         const uint32_t* cntp, uint64_t pmask, uint64_t kmask, int shift,
                         uint32_t dmask, int64_t dstride, int64_t* diag, SegmentOut so,
                         unsigned long long* stats, uint64_t* cw, void* cs, uint32_t* ccnt,
-                        uint64_t* ow, void* os, uint32_t* ocnt, LfBigList bl, cudaStream_t s) {
+                        uint64_t* ow, void* os, uint32_t* ocnt, LfBigList bl, cudaStream_t s,
+                        bool wide) {
     if (n == 0) return cudaGetLastError();
-    return leaf_go<LEAF_TH>(w, sq, seq16, n, cntp, pmask, kmask, shift, dmask, dstride, diag, so,
+    if (wide)
+        return leaf_go<LEAF_TH, 12>(w, sq, seq16, n, cntp, pmask, kmask, shift, dmask, dstride, diag,
+                                    so, stats, cw, cs, ccnt, ow, os, ocnt, bl, s);
+    return leaf_go<LEAF_TH, LF_IT>(w, sq, seq16, n, cntp, pmask, kmask, shift, dmask, dstride, diag, so,
                                  stats, cw, cs, ccnt, ow, os, ocnt, bl, s);
 }
 

@@ -1837,13 +1837,19 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
             // 6e6 x 0.24^4 = 2e4 -> unfused, its chain levels from 5 positions (4.8e3)
             // fused; Scale: 41 -> fused). A group past the window is split by its owner
             // CTA into the mask's overflow slot, which the segment kernel takes afterwards.
+            // wide leaf CTAs (12 items per thread) where the light path does not share the
+            // machine heavily (no relabelled accumulator: Text 76.1 -> 74.7 ms); with the
+            // relabelled light path 8 (Scale: 12 gives the leaves 39.3 -> 37.3 ms alone but
+            // the step 124.1 -> 129.4, the longer CTAs crowding the light kernel out)
+            const bool lf_wide = !relabel;
             auto fuse_ok = [&](int npos) {
                 // (the bound, in tiles: Text 0.5 -> 84.5 ms, 1.5 -> 83.6, 8 -> 79.5, 16 ->
                 // 79.5, >= 30 -> 92.3 with the owner-CTA split, 86.8 with the queue of
                 // leaf.cu: its level-5 leaves, largest groups ~2e4; Scale's expected 41
                 // fuses under any bound)
                 constexpr double kBigTiles = 8.0;
-                return p->leaf_fuse && npos >= 1 && lf_big_expect(npos) <= (double)leaf_tile() * kBigTiles;
+                return p->leaf_fuse && npos >= 1 &&
+                       lf_big_expect(npos) <= (double)leaf_tile(lf_wide) * kBigTiles;
             };
             auto pos_mask = [&](int x) { return (uint64_t)dmask << (bits * (g - 1 - x)); };
             const size_t slot0 = (size_t)xl_slot[pos];
@@ -1895,7 +1901,7 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
                         p->launches += 1;
                         LK(launch_leaf(iw, is, seq16, n, pC + xl_parent[j], kmask & ~pos_mask(xl_x[j]),
                                        kmask, sh, dmask, dstride, Dm, so, stats, lcw, lcs, lcc, wleaf,
-                                       sleaf, ocnt, lbl, s));
+                                       sleaf, ocnt, lbl, s, lf_wide));
                         p->stage_end(s, S_SEGMENT, a);
                     } else {
                         LK(launch_trie_pass64(iw, wleaf, is, sleaf, seq16, n, pC + xl_parent[j], sh,
@@ -1937,12 +1943,12 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
                     // (groups past a CTA's window expected: queued and split right after
                     // this leaf, while the stack top still holds its input; else the rare
                     // one is split by its own CTA)
-                    const bool tq = lf_big_expect(kk - 1) > (double)leaf_tile();
+                    const bool tq = lf_big_expect(kk - 1) > (double)leaf_tile(lf_wide);
                     LK(launch_leaf((const uint64_t*)p->trieW.p + (size_t)(kk - 2) * n,
                                    (const uint8_t*)p->trieS.p + (size_t)(kk - 2) * n * ssz, seq16, n,
                                    nullptr, pm, kmask, bits * (g - 1 - kept[kk - 1]), dmask, dstride, Dm,
                                    so, stats, lcw, lcs, lcc, wleaf, sleaf, ocnt,
-                                   tq ? lbl : LfBigList{nullptr, nullptr, 0}, s));
+                                   tq ? lbl : LfBigList{nullptr, nullptr, 0}, s, lf_wide));
                     if (tq) {
                         p->launches += 1;
                         LK(launch_leaf_big(lbl, seq16, p->sm_count, s));
