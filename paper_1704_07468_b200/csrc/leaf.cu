@@ -246,7 +246,6 @@ __global__ void __launch_bounds__(TH, 1024 / TH) leaf_kernel(
     const uint64_t t0 = (uint64_t)blockIdx.x * T;
     if (t0 >= cnt) return;  // (block-uniform)
     const uint64_t t1 = min(t0 + T, cnt);
-    const uint32_t tl = (uint32_t)(t1 - t0);  // tile elements
 
     for (int i = tid; i < 2 * W * LF_ND; i += TH) sh.whist[i] = 0u;
     if (tid == 0) {
