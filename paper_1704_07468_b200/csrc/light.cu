@@ -755,6 +755,7 @@ __global__ void thresh_union_kernel(const int64_t* __restrict__ C, int64_t N,
             if (v < 2) continue;
             const uint64_t by = best[y] >> 32;
             if ((uint64_t)v * 4 < bx && (uint64_t)v * 4 < by) continue;
+            if (parent[x] == parent[y]) continue;  // (already one cluster: flattened paths)
             uint32_t a = (uint32_t)x, c = (uint32_t)y;
             while (true) {
                 a = uf_find(parent, a);
@@ -788,6 +789,9 @@ cudaError_t launch_cluster_roots(const int64_t* C, int64_t N, unsigned long long
     if (rows > 0) best_partner_kernel<<<(unsigned)rows, 256, 0, s>>>(C, N, best);
     const int blocks = (int)((N + 255) / 256 < 1024 ? (N + 255) / 256 : 1024);
     best_union_kernel<<<blocks, 256, 0, s>>>(best, N, parent);
+    // (paths flattened first: the threshold unions mostly meet pairs the best-partner
+    // links already joined, and then each find is one load)
+    uf_roots_kernel<<<blocks, 256, 0, s>>>(parent, N);
     if (rows > 0) thresh_union_kernel<<<(unsigned)rows, 256, 0, s>>>(C, N, best, parent);
     uf_roots_kernel<<<blocks, 256, 0, s>>>(parent, N);
     return cudaGetLastError();
