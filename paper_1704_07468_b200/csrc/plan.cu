@@ -1424,33 +1424,34 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
             // on the device, no host round trip: the clusters, then the labels = the
             // sequences stably sorted by cluster root (3 passes of 6 bits of the root,
             // keys root << 32 | sequence; the sequence order is kept within a cluster)
-            if (pipe) {  // C of level m_done complete: its light and Gram flushes
-                CK(cudaEventRecord(p->ev_join, s2));
-                CK(cudaStreamWaitEvent(s, p->ev_join, 0));
+            // (on the light stream, after level m_done's light and window flushes; it
+            // waits for the Gram stream's flushes. The next level's sort / segment on s
+            // does not use the labels, so it runs meanwhile)
+            if (pipe) {
                 CK(cudaEventRecord(p->ev_join2, s3));
-                CK(cudaStreamWaitEvent(s, p->ev_join2, 0));
+                CK(cudaStreamWaitEvent(s2, p->ev_join2, 0));
             }
             cudaEvent_t ar = nullptr;
-            p->stage_begin(s, &ar);
+            p->stage_begin(s2, &ar);
             p->launches += 4 + 2 * 3 + 2;
             CK(launch_cluster_roots(level_ptr(m_done), N, (unsigned long long*)p->best.p,
                                     (uint32_t*)p->parent.p, (const uint32_t*)p->iota.p,
-                                    p->sm_count, s));
-            CK(p->ensure(p->relkeys, (size_t)N * 16 + 64, s));
-            CK(p->ensure(p->relH, (size_t)p->sm_count * 2 * 64 * 4 + 64, s));
+                                    p->sm_count, s2));
+            CK(p->ensure(p->relkeys, (size_t)N * 16 + 64, s2));
+            CK(p->ensure(p->relH, (size_t)p->sm_count * 2 * 64 * 4 + 64, s2));
             uint64_t* ka = (uint64_t*)p->relkeys.p;
             uint64_t* kb = ka + N;
-            CK(launch_relabel_keys((const uint32_t*)p->parent.p, N, ka, s));
+            CK(launch_relabel_keys((const uint32_t*)p->parent.p, N, ka, s2));
             int rb = 0;
             while (((int64_t)1 << rb) < N) ++rb;
             for (int sh = 0; sh < rb; sh += 6) {
                 CK(launch_tp_records(ka, kb, false, (uint64_t)N, nullptr, 32 + sh,
-                                     (uint32_t*)p->relH.p, p->sm_count * 2, s));
+                                     (uint32_t*)p->relH.p, p->sm_count * 2, s2));
                 std::swap(ka, kb);
             }
             CK(launch_relabel_perm(ka, N, (uint32_t*)p->perm.p, win_on ? (uint32_t*)p->winv.p : nullptr,
-                                   s));
-            p->stage_end(s, S_LIGHT, ar);
+                                   s2));
+            p->stage_end(s2, S_LIGHT, ar);
             perm_active = true;
             return GAKCO_OK;
         }
