@@ -42,6 +42,39 @@ __host__ __device__ inline uint64_t lb_pack(uint32_t epoch, uint32_t flag, uint3
     return ((uint64_t)epoch << 32) | ((uint64_t)flag << 30) | (uint64_t)(value & 0x3fffffffu);
 }
 
+// Programmatic dependent launch on the grouping chain (trie pass hist -> scatter ->
+// ... -> fused leaf, one stream): a kernel launched by launch_pdl may be scheduled
+// while its predecessor's last wave still runs; pdl_enter() -- its first statement --
+// waits until the predecessor has completed and its writes are visible, then lets
+// the next kernel of the chain be scheduled the same way (single-wave kernels whose
+// CTAs stay resident trigger only after their main loop -- pdl_wait() first,
+// pdl_trigger() late -- so waiting CTAs do not hold SM slots the other stream could
+// use). In a kernel launched without the attribute both are no-ops.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() {
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+__device__ __forceinline__ void pdl_enter() {
+    pdl_wait();
+    pdl_trigger();
+}
+bool pdl_enabled();  // GAKCO_PDL=0 in the environment turns the attribute off (A/B)
+template <typename... KA, typename... A>
+cudaError_t launch_pdl(void (*kern)(KA...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                       A... args) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl_enabled() ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kern, ((KA)args)...);
+}
+
 __device__ __forceinline__ uint32_t lanemask_lt() {
     uint32_t r;
     asm("mov.u32 %0, %%lanemask_lt;" : "=r"(r));

@@ -225,6 +225,7 @@ __global__ void __launch_bounds__(TH, 1024 / TH) leaf_kernel(
     using L = Lf<TH, IT>;
     constexpr int C = L::C, T = L::T, W = L::WARPS;
     extern __shared__ __align__(16) unsigned char smem[];
+    pdl_enter();
     LfShared sh;
     sh.sw = (uint64_t*)smem;
     S* const ss = (S*)(smem + (size_t)(C + 8) * 8);
@@ -641,15 +642,15 @@ cudaError_t leaf_go(const uint64_t* w, const void* sq, bool seq16, uint64_t n, c
     if (seq16) {
         cudaFuncSetAttribute(leaf_kernel<uint16_t, TH, IT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)lf_smem<uint16_t, TH, IT>());
-        leaf_kernel<uint16_t, TH, IT><<<grid, TH, lf_smem<uint16_t, TH, IT>(), s>>>(
-            w, (const uint16_t*)sq, cntp, n, pmask, kmask, shift, dmask, dstride, diag, so.counts, so,
-            stats, cw, (uint16_t*)cs, ccnt, ow, (uint16_t*)os, ocnt, bl);
+        return launch_pdl(leaf_kernel<uint16_t, TH, IT>, grid, TH, lf_smem<uint16_t, TH, IT>(), s, w,
+                          (const uint16_t*)sq, cntp, n, pmask, kmask, shift, dmask, dstride, diag, so.counts,
+                          so, stats, cw, (uint16_t*)cs, ccnt, ow, (uint16_t*)os, ocnt, bl);
     } else {
         cudaFuncSetAttribute(leaf_kernel<uint32_t, TH, IT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)lf_smem<uint32_t, TH, IT>());
-        leaf_kernel<uint32_t, TH, IT><<<grid, TH, lf_smem<uint32_t, TH, IT>(), s>>>(
-            w, (const uint32_t*)sq, cntp, n, pmask, kmask, shift, dmask, dstride, diag, so.counts, so,
-            stats, cw, (uint32_t*)cs, ccnt, ow, (uint32_t*)os, ocnt, bl);
+        return launch_pdl(leaf_kernel<uint32_t, TH, IT>, grid, TH, lf_smem<uint32_t, TH, IT>(), s, w,
+                          (const uint32_t*)sq, cntp, n, pmask, kmask, shift, dmask, dstride, diag, so.counts,
+                          so, stats, cw, (uint32_t*)cs, ccnt, ow, (uint32_t*)os, ocnt, bl);
     }
     return cudaGetLastError();
 }

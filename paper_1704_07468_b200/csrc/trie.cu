@@ -24,6 +24,7 @@
 // array of the cross-level chain, plan.cu); the grid is sized for the capacity n
 // and both kernels derive the same chunking from the actual count.
 #include <algorithm>
+#include <cstdlib>
 #include <type_traits>
 
 #include "internal.cuh"
@@ -84,6 +85,7 @@ __global__ void __launch_bounds__(TPH_THREADS) tp_hist_kernel(const K* __restric
                                                               uint32_t* __restrict__ Hg, int par) {
     constexpr int E = 16 / sizeof(K);  // keys per 16-byte load
     __shared__ uint32_t s_h[TPH_WARPS][TP_ND];
+    pdl_wait();
     const int tid = threadIdx.x, wp = tid >> 5;
     for (int i = tid; i < TPH_WARPS * TP_ND; i += TPH_THREADS) (&s_h[0][0])[i] = 0;
     if (Hg) {  // the other parity's block sums, zeroed for the next pass
@@ -121,6 +123,7 @@ __global__ void __launch_bounds__(TPH_THREADS) tp_hist_kernel(const K* __restric
     }
     for (uint64_t r = a + nv * E + tid; r < ch.hi; r += TPH_THREADS)
         atomicAdd(&s_h[wp][(uint32_t)(w[r] >> shift) & dmask], 1u);
+    pdl_trigger();
     __syncthreads();
     if (tid < TP_ND) {
         uint32_t s = 0;
@@ -187,6 +190,7 @@ __global__ void __launch_bounds__(TP_THREADS, 2) tp_scatter_kernel(
     uint32_t* s_w = &s_part[16][0];                                       // [4]
     uint64_t* s_bar = (uint64_t*)(((uintptr_t)(s_w + 4) + 7) & ~(uintptr_t)7);  // [2]
 
+    pdl_wait();
     const int tid = threadIdx.x, lane = tid & 31, wp = tid >> 5;
     const uint64_t cnt = cntp ? min((uint64_t)*cntp, n) : n;
     const uint32_t cps = gridDim.x, c = blockIdx.x;
@@ -357,6 +361,7 @@ __global__ void __launch_bounds__(TP_THREADS, 2) tp_scatter_kernel(
             issue(t + 2, &s_bar[b]);
         }
     }
+    pdl_trigger();
 }
 
 __global__ void fill_u32_kernel(uint32_t* p, uint32_t v, uint32_t count) {
@@ -415,23 +420,31 @@ cudaError_t launch_trie_pass64(const uint64_t* win, uint64_t* wout, const void* 
     // (the parity advances only with a pass that uses the block sums: each such pass
     // zeroes the sums the next one accumulates into)
     const int par = Hg ? (int)((*par_ctr)++ & 1u) : 0;
-    tp_hist_kernel<uint64_t><<<cps, TPH_THREADS, 0, s>>>(win, n, cntp, shift, dmask, H, Hg, par);
-    cudaError_t e = cudaGetLastError();
+    cudaError_t e = launch_pdl(tp_hist_kernel<uint64_t>, cps, TPH_THREADS, 0, s, win, n, cntp, shift,
+                               dmask, H, Hg, par);
     if (e != cudaSuccess) return e;
     if (seq16) {
         cudaFuncSetAttribute(tp_scatter_kernel<uint64_t, uint16_t>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tp_smem<uint64_t, uint16_t>());
-        tp_scatter_kernel<uint64_t, uint16_t><<<cps, TP_THREADS, tp_smem<uint64_t, uint16_t>(), s>>>(
-            win, wout, (const uint16_t*)sin, (uint16_t*)sout, n, cntp, shift, dmask, omask, H, Hg, par,
-            cnt_out, stats);
+        e = launch_pdl(tp_scatter_kernel<uint64_t, uint16_t>, cps, TP_THREADS, tp_smem<uint64_t, uint16_t>(),
+                       s, win, wout, (const uint16_t*)sin, (uint16_t*)sout, n, cntp, shift, dmask, omask,
+                       H, Hg, par, cnt_out, stats);
     } else {
         cudaFuncSetAttribute(tp_scatter_kernel<uint64_t, uint32_t>,
                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)tp_smem<uint64_t, uint32_t>());
-        tp_scatter_kernel<uint64_t, uint32_t><<<cps, TP_THREADS, tp_smem<uint64_t, uint32_t>(), s>>>(
-            win, wout, (const uint32_t*)sin, (uint32_t*)sout, n, cntp, shift, dmask, omask, H, Hg, par,
-            cnt_out, stats);
+        e = launch_pdl(tp_scatter_kernel<uint64_t, uint32_t>, cps, TP_THREADS, tp_smem<uint64_t, uint32_t>(),
+                       s, win, wout, (const uint32_t*)sin, (uint32_t*)sout, n, cntp, shift, dmask, omask,
+                       H, Hg, par, cnt_out, stats);
     }
-    return cudaGetLastError();
+    return e != cudaSuccess ? e : cudaGetLastError();
+}
+
+bool pdl_enabled() {
+    static const bool on = [] {
+        const char* v = std::getenv("GAKCO_PDL");
+        return !(v && v[0] == '0');
+    }();
+    return on;
 }
 
 }  // namespace gk
