@@ -225,7 +225,7 @@ __global__ void __launch_bounds__(TH, 1024 / TH) leaf_kernel(
     using L = Lf<TH, IT>;
     constexpr int C = L::C, T = L::T, W = L::WARPS;
     extern __shared__ __align__(16) unsigned char smem[];
-    pdl_enter();
+    pdl_wait();  // (no explicit trigger: the next grid launches as the CTAs exit)
     LfShared sh;
     sh.sw = (uint64_t*)smem;
     S* const ss = (S*)(smem + (size_t)(C + 8) * 8);
