@@ -1363,17 +1363,22 @@ static gakco_status accumulate_impl(gakco_plan* p, const uint8_t* codes, const i
     if (relabel && ntri < (1ull << 40) &&
         (p->far_near > 0 || (p->far_near == -1 && ntri * 4 > (96ull << 20)))) {
         // records are applied once they fill half the buffer (every cell of a block hit
-        // several times per apply) and before each accumulator flush; up to 2^30
-        // records (8 GB + the same for the bucketed copy) while 16 GB stay free
-        // 4-byte records when every cell index fits 28 bits (Scale: 2e8 cells)
+        // several times per apply) and before each accumulator flush; up to 2^31
+        // 4-byte records (8 GB per buffer + the same for the bucketed copy; 2^30 8-byte
+        // ones) while 16 GB stay free. 4-byte records when every cell index fits 28 bits
+        // (Scale: 2e8 cells). (2^30 4-byte records overflowed at Scale: with the host
+        // ahead of the GPU the gate applies blindly every FAR_EVERY batches, and 12 of
+        // level 5's 128M-key batches can record more: one light launch per step fell
+        // back to DRAM REDs.)
         const bool k32 = p->far_bytes == 4 || (p->far_bytes == 0 && ntri < (1ull << 28));
         if (k32 && ntri >= (1ull << 28)) return p->fail(GAKCO_E_ARG, "4-byte far records need < 2^28 cells");
         const size_t have = std::min(p->farrec.cap / (far2 ? 2 : 1), p->farscr.cap) / (k32 ? 4 : 8);
-        // (buffers already at the 2^30-record maximum: no free-memory query)
-        uint64_t cap = 1ull << 30;
+        // (buffers already at the record maximum: no free-memory query)
+        const uint64_t cmax = k32 ? (1ull << 31) : (1ull << 30);
+        uint64_t cap = cmax;
         if (have < cap) {
             const size_t fr = free_bytes();
-            cap = std::min<uint64_t>(1ull << 30, std::max<uint64_t>(
+            cap = std::min<uint64_t>(cmax, std::max<uint64_t>(
                 std::max<uint64_t>(1ull << 24, have),
                 fr > (16ull << 30) ? (fr - (16ull << 30)) / 16 : 0));
         }
