@@ -145,6 +145,7 @@ struct FarSink {
 __global__ void far_offsets_kernel(const uint32_t* __restrict__ H, uint32_t cps, uint32_t* offs) {
     // offs[b] = records in buckets < b (H: cps chunk rows of 64 bucket counts)
     __shared__ uint32_t tot[64];
+    pdl_wait();
     const int d = threadIdx.x;
     if (d < 64) {
         uint32_t t = 0;
@@ -163,6 +164,7 @@ __global__ void far_offsets_kernel(const uint32_t* __restrict__ H, uint32_t cps,
 }
 __global__ void far_warm_kernel(const uint32_t* __restrict__ acc, uint64_t c0, uint64_t c1,
                                 const uint32_t* offs, int b0, int b1, uint32_t* sink) {
+    pdl_wait();
     if (offs[b1] == offs[b0]) return;  // (no records in these blocks)
     const uint4* a = (const uint4*)(acc + c0);
     const uint64_t nv = (c1 - c0) / 4;
@@ -178,6 +180,7 @@ template <typename K>
 __global__ void far_add_kernel(const K* __restrict__ recs, const uint32_t* offs, int b0, int b1,
                                uint32_t* acc, uint64_t ntri) {
     constexpr int VB = sizeof(K) == 4 ? 4 : 24;  // value bits
+    pdl_wait();
     const uint64_t lo = offs[b0], hi = offs[b1];
     for (uint64_t i = lo + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < hi;
          i += (uint64_t)gridDim.x * blockDim.x) {
@@ -196,8 +199,12 @@ cudaError_t launch_far_apply(FarRec fr, void* scratch, uint32_t* H, int bshift, 
     if (e != cudaSuccess) return e;
     uint32_t* offs = H + (size_t)cps * 64;  // [65]
     uint32_t* sink = offs + 66;
-    far_offsets_kernel<<<1, 64, 0, s>>>(H, (uint32_t)std::min<uint64_t>(cps, std::max<uint64_t>(
-                                            1, (fr.cap + 4095) / 4096)), offs);
+    // (the chain's launches overlap their predecessor's tail: programmatic dependent
+    // launch, each kernel waiting at entry)
+    e = launch_pdl(far_offsets_kernel, 1, 64, 0, s, (const uint32_t*)H,
+                   (uint32_t)std::min<uint64_t>(cps, std::max<uint64_t>(1, (fr.cap + 4095) / 4096)),
+                   offs);
+    if (e != cudaSuccess) return e;
     const int nb = (int)std::min<uint64_t>(64, (ntri + (1ull << bshift) - 1) >> bshift);
     constexpr int GRP = 4;  // blocks per group: 64 MB of u32 cells, resident in L2
     for (int b0 = 0; b0 < nb; b0 += GRP) {
@@ -205,13 +212,17 @@ cudaError_t launch_far_apply(FarRec fr, void* scratch, uint32_t* H, int bshift, 
         const uint64_t c0 = (uint64_t)b0 << bshift;
         uint64_t c1 = std::min<uint64_t>((uint64_t)b1 << bshift, ntri);
         c1 = c1 / 4 * 4;
-        if (c1 > c0) far_warm_kernel<<<sm_count * 4, 256, 0, s>>>(acc, c0, c1, offs, b0, b1, sink);
+        if (c1 > c0)
+            e = launch_pdl(far_warm_kernel, sm_count * 4, 256, 0, s, (const uint32_t*)acc, c0, c1,
+                           (const uint32_t*)offs, b0, b1, sink);
+        if (e != cudaSuccess) return e;
         if (fr.k32)
-            far_add_kernel<uint32_t><<<sm_count * 8, 256, 0, s>>>((const uint32_t*)scratch, offs, b0,
-                                                                  b1, acc, ntri);
+            e = launch_pdl(far_add_kernel<uint32_t>, sm_count * 8, 256, 0, s, (const uint32_t*)scratch,
+                           (const uint32_t*)offs, b0, b1, acc, ntri);
         else
-            far_add_kernel<uint64_t><<<sm_count * 8, 256, 0, s>>>((const uint64_t*)scratch, offs, b0,
-                                                                  b1, acc, ntri);
+            e = launch_pdl(far_add_kernel<uint64_t>, sm_count * 8, 256, 0, s, (const uint64_t*)scratch,
+                           (const uint32_t*)offs, b0, b1, acc, ntri);
+        if (e != cudaSuccess) return e;
     }
     e = cudaGetLastError();
     if (e != cudaSuccess) return e;

@@ -385,14 +385,15 @@ static cudaError_t tp_records(const K* in, K* out, uint64_t n, const uint32_t* c
     if (n == 0) return cudaGetLastError();
     const uint64_t tiles = (n + TP_TILE - 1) / TP_TILE;
     const unsigned cps = (unsigned)std::max<uint64_t>(1, std::min<uint64_t>(tiles, target_ctas));
-    tp_hist_kernel<K><<<cps, TPH_THREADS, 0, s>>>(in, n, cntp, shift, 63u, H, nullptr, 0);
-    cudaError_t e = cudaGetLastError();
+    cudaError_t e = launch_pdl(tp_hist_kernel<K>, cps, TPH_THREADS, 0, s, in, n, cntp, shift, 63u, H,
+                               (uint32_t*)nullptr, 0);
     if (e != cudaSuccess) return e;
     cudaFuncSetAttribute(tp_scatter_kernel<K, TpNoPay>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)tp_smem<K, TpNoPay>());
-    tp_scatter_kernel<K, TpNoPay><<<cps, TP_THREADS, tp_smem<K, TpNoPay>(), s>>>(
-        in, out, nullptr, nullptr, n, cntp, shift, 63u, ~(K)0, H, nullptr, 0, nullptr, nullptr);
-    return cudaGetLastError();
+    e = launch_pdl(tp_scatter_kernel<K, TpNoPay>, cps, TP_THREADS, tp_smem<K, TpNoPay>(), s, in, out,
+                   (const TpNoPay*)nullptr, (TpNoPay*)nullptr, n, cntp, shift, 63u, ~(K)0, H,
+                   (const uint32_t*)nullptr, 0, (uint32_t*)nullptr, (unsigned long long*)nullptr);
+    return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 cudaError_t launch_tp_records(const void* in, void* out, bool k32, uint64_t n, const uint32_t* cntp,
