@@ -50,6 +50,7 @@ __global__ void __launch_bounds__(RG_THREADS, 4) segment_rag_kernel(
     __shared__ uint32_t s_wmin[RG_THREADS / 32], s_beyond, s_cross;
     __shared__ unsigned long long s_gend;
     constexpr uint32_t FULLM = (1u << RG_IT) - 1u;
+    pdl_wait();  // (launched as a programmatic dependent of the chain's last pass)
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     // (a grid smaller than segments x tiles loops: the overflow slots of leaf.cu are
     // mostly empty)
@@ -347,8 +348,8 @@ cudaError_t launch_segment_rag(const uint64_t* w, const void* sq, bool seq16, ui
     const uint32_t nblk = (uint32_t)(tps * (uint64_t)nseg);
     const unsigned grid = max_ctas ? std::min<unsigned>(nblk, max_ctas) : nblk;
     auto go = [&](auto kern, auto* sqp, auto* csp) {
-        kern<<<grid, RG_THREADS, 0, s>>>(w, sqp, km, n, cnt, (uint32_t)tps, nblk, dstride, diag,
-                                         counters, so, stats, cw, csp, ccnt);
+        e = launch_pdl(kern, grid, RG_THREADS, 0, s, w, sqp, km, n, cnt, (uint32_t)tps, nblk, dstride,
+                       diag, counters, so, stats, cw, csp, ccnt);
     };
     if (seq16) {
         if (grid < nblk) go(segment_rag_kernel<uint16_t, true>, (const uint16_t*)sq, (uint16_t*)cs);
@@ -357,7 +358,7 @@ cudaError_t launch_segment_rag(const uint64_t* w, const void* sq, bool seq16, ui
         if (grid < nblk) go(segment_rag_kernel<uint32_t, true>, (const uint32_t*)sq, (uint32_t*)cs);
         else go(segment_rag_kernel<uint32_t, false>, (const uint32_t*)sq, (uint32_t*)cs);
     }
-    return cudaGetLastError();
+    return e != cudaSuccess ? e : cudaGetLastError();
 }
 
 }  // namespace gk
