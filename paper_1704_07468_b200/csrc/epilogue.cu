@@ -14,6 +14,8 @@
 #include <math.h>
 #include <string.h>
 
+#include <type_traits>
+
 #include "internal.cuh"
 
 namespace gk {
@@ -44,8 +46,10 @@ __device__ __forceinline__ int64_t entry(int64_t (&prof)[MM + 1], const EpiCoef&
                                          int M, int* bad) {
     int64_t cgk = 0;
 #pragma unroll
-    for (int m = 0; m <= MM; ++m)
-        if (m <= M && m == g - k) cgk = prof[m];
+    // (selected by a mask: `if (m == g - k) cgk = prof[m]` compiled to prof[g - k], a
+    // dynamic index that put the whole profile array in local memory -- ncu: 16 GB of
+    // local stores per Scale epilogue)
+    for (int m = 0; m <= MM; ++m) cgk |= prof[m] & -(int64_t)(m <= M && m == g - k);
 #pragma unroll
     for (int m = 0; m <= MM; ++m) {
         if (m > M) break;
@@ -83,12 +87,12 @@ __device__ __forceinline__ double knorm(int64_t kxy, int64_t kxx, int64_t kyy, b
 
 // blockDim (32, 32 / EP_RPT); a 1-D grid over the t(t+1)/2 tile pairs bi <= bj (t =
 // tiles per side), row-major: block L -> the largest bi with R(bi) = bi t - bi (bi-1)/2
-// <= L. Each thread holds EP_RPT rows of the 32 x 32 tile (2: the profiles stay in
-// registers, 4 CTAs of 512 threads per SM). MM bounds M.
-constexpr int EP_RPT = 2, EP_TY = 32 / EP_RPT;
-template <int MM>
-__global__ void __launch_bounds__(32 * EP_TY, 2) epilogue_kernel(EpiArgs a,
-                                                                const __grid_constant__ EpiCoef cf) {
+// <= L. Each thread holds EP_RPT rows of the 32 x 32 tile; MINB CTAs per SM the
+// register budget is sized for. MM bounds M.
+template <int MM, int EP_RPT, int MINB>
+__global__ void __launch_bounds__(32 * (32 / EP_RPT), MINB) epilogue_kernel(
+    EpiArgs a, const __grid_constant__ EpiCoef cf) {
+    constexpr int EP_TY = 32 / EP_RPT;
     __shared__ int64_t st[32][33];
     const int64_t t = (a.N + 31) / 32, L = blockIdx.x;
     int64_t lo = 0, hi = t - 1;
@@ -369,14 +373,17 @@ cudaError_t launch_epilogue(int64_t* C, int64_t N, int g, int k, int M, int64_t*
     if (e != cudaSuccess) return e;
     const uint64_t tiles = (uint64_t)((N + 31) / 32);
     const unsigned pairs = (unsigned)(tiles * (tiles + 1) / 2);  // (upper tile pairs only)
-    if (M <= 3)  // (the profile array sized to the level count: registers, not local memory)
-        epilogue_kernel<3><<<pairs, dim3(32, EP_TY), 0, s>>>(a, cf);
-    else if (M <= 5)
-        epilogue_kernel<5><<<pairs, dim3(32, EP_TY), 0, s>>>(a, cf);
-    else if (M <= 7)
-        epilogue_kernel<7><<<pairs, dim3(32, EP_TY), 0, s>>>(a, cf);
-    else
-        epilogue_kernel<GMAX><<<pairs, dim3(32, EP_TY), 0, s>>>(a, cf);
+    // (2 rows per thread, 2 x 512 threads per SM, 64 registers: 9.4 ms at Scale; the
+    // spill-free 1 x 512 (96 registers) and 1 row x 1024 threads took 11.5 / 12.3 ms)
+    auto go = [&](auto mm) {
+        constexpr int MM = decltype(mm)::value;
+        epilogue_kernel<MM, 2, 2><<<pairs, dim3(32, 16), 0, s>>>(a, cf);
+    };
+    // (the profile array sized to the level count: registers, not local memory)
+    if (M <= 3) go(std::integral_constant<int, 3>());
+    else if (M <= 5) go(std::integral_constant<int, 5>());
+    else if (M <= 7) go(std::integral_constant<int, 7>());
+    else go(std::integral_constant<int, GMAX>());
     return cudaGetLastError();
 }
 
