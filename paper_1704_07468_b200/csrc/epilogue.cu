@@ -163,24 +163,8 @@ __global__ void __launch_bounds__(32 * (32 / EP_RPT), MINB) epilogue_kernel(
     }
     if (bad) atomicOr(a.flags, bad);
     if (diag_tile) return;
-    // transposed writes of tile (bj, bi): Nm (static level index, prof stays in
-    // registers), then K and Knorm (the C mirror went out above)
-    if (a.Nm) {
-#pragma unroll
-        for (int o = 0; o <= MM; ++o) {
-            if (o > M) break;
-            __syncthreads();
-#pragma unroll
-            for (int q = 0; q < EP_RPT; ++q) st[ty + EP_TY * q][tx] = prof[q][o];
-            __syncthreads();
-#pragma unroll
-            for (int q = 0; q < EP_RPT; ++q) {
-                const int r = ty + EP_TY * q;
-                const int64_t X = (int64_t)bj * 32 + r, Y = (int64_t)bi * 32 + tx;
-                if (X < N && Y < N) a.Nm[o * nn + X * N + Y] = st[tx][r];
-            }
-        }
-    }
+    // transposed writes of tile (bj, bi): K and Knorm (their registers die first), then
+    // Nm (static level index, prof stays in registers; the C mirror went out above)
     for (int o = 0; o < 2; ++o) {
         if (o == 0 ? a.K == nullptr : a.Knorm == nullptr) continue;
         __syncthreads();
@@ -199,6 +183,22 @@ __global__ void __launch_bounds__(32 * (32 / EP_RPT), MINB) epilogue_kernel(
             const int64_t v = st[tx][r];
             if (o == 0) a.K[X * N + Y] = v;
             else a.Knorm[X * N + Y] = __longlong_as_double(v);
+        }
+    }
+    if (a.Nm) {
+#pragma unroll
+        for (int o = 0; o <= MM; ++o) {
+            if (o > M) break;
+            __syncthreads();
+#pragma unroll
+            for (int q = 0; q < EP_RPT; ++q) st[ty + EP_TY * q][tx] = prof[q][o];
+            __syncthreads();
+#pragma unroll
+            for (int q = 0; q < EP_RPT; ++q) {
+                const int r = ty + EP_TY * q;
+                const int64_t X = (int64_t)bj * 32 + r, Y = (int64_t)bi * 32 + tx;
+                if (X < N && Y < N) a.Nm[o * nn + X * N + Y] = st[tx][r];
+            }
         }
     }
 }
